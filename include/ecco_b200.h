@@ -1,0 +1,282 @@
+/*
+ * ecco_b200.h -- C-ABI of the B200-native group-retraining path of ECCO
+ * (arXiv 2512.11727).
+ *
+ * The reference (a C++20 simulator, /root/reference/proj) drives this path
+ * through three callback seams and a handful of free functions:
+ *
+ *   TrainingBackend::evaluate / ::train   proj/core/include/ecco/gpu_allocator.hpp:37-42
+ *   ModelEvalFn                           proj/core/include/ecco/grouping.hpp:23
+ *   ProbeFn (+ build_profile_table)       proj/core/include/ecco/transmission.hpp:46,52-56
+ *   eval / train_step / seed_model        proj/core/include/ecco/accuracy_model.hpp:72-94
+ *
+ * Every entry point below replaces a batch of those per-item calls; the
+ * comment on each names the reference interface it stands in for.  All
+ * arguments are plain pointers and sizes; host buffers are copied
+ * synchronously unless the name ends in _dev (device pointers, stream-ordered
+ * on the context's stream).  Errors are reported as an ecco_status whose
+ * values map 1:1 onto the reference's exception types (see ecco_status), with
+ * the message available from ecco_last_error().  A context is not
+ * thread-safe, matching the reference's single-owner contract
+ * (proj/README.md:42-43).
+ *
+ * Two backends share the boundary:
+ *   ECCO_BACKEND_PARAMETRIC  device restatement of accuracy_model.cpp, fp64,
+ *                            bit-identical to the reference library;
+ *   ECCO_BACKEND_LEARNED     real per-group MLPs (fwd + bwd + SGD) over
+ *                            synthetic camera streams resident in HBM.
+ */
+#ifndef ECCO_B200_H_
+#define ECCO_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ecco_ctx ecco_ctx;
+
+/* Status codes; the C++ wrapper rethrows them as the reference's exceptions. */
+typedef enum {
+  ECCO_OK = 0,
+  ECCO_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument                  */
+  ECCO_ERR_LOGIC = 2,            /* std::logic_error                       */
+  ECCO_ERR_INFEASIBLE = 3,       /* ecco::InfeasibleScheduleError          */
+  ECCO_ERR_SCHEMA = 4,           /* ecco::SchemaError                      */
+  ECCO_ERR_CUDA = 5,             /* device failure (no reference analogue) */
+  ECCO_ERR_RUNTIME = 6           /* std::runtime_error                     */
+} ecco_status;
+
+typedef enum { ECCO_BACKEND_PARAMETRIC = 0, ECCO_BACKEND_LEARNED = 1 } ecco_backend;
+
+/* Arithmetic of the learned backend's dense contractions. */
+typedef enum {
+  ECCO_MATH_FFMA_EXACT = 0, /* fp32 FFMA in the oracle's order: bit-exact   */
+  ECCO_MATH_TC_BF16 = 1     /* tcgen05 bf16 x bf16 -> fp32 TMEM: tolerance */
+} ecco_math;
+
+/* ModelParams (proj/core/include/ecco/accuracy_model.hpp:18-24). */
+typedef struct {
+  double learning_rate_k;
+  double similarity_lambda;
+  double acc_floor;
+  double acc_ceil;
+  double cluster_similarity_threshold;
+} ecco_model_params;
+
+typedef struct {
+  int backend;          /* ecco_backend                                   */
+  int device;           /* CUDA ordinal                                   */
+  int scene_dims;       /* D, shared by every scene                       */
+  int max_clusters;     /* P: cluster capacity per model (K_max)          */
+  int max_jobs;         /* model slots                                    */
+  int max_cameras;      /* camera table capacity                          */
+  ecco_model_params params;
+  /* learned backend */
+  int math;             /* ecco_math                                      */
+  int feat_dim;         /* F  (frame feature width)                       */
+  int hidden_dim;       /* H                                              */
+  int num_classes;      /* C                                              */
+  int minibatch;        /* B samples per SGD step                         */
+  int ring_frames;      /* R training frames per camera per window        */
+  int eval_samples;     /* S labelled eval frames per camera              */
+  int max_depth;        /* speculative trajectory depth kept as snapshots */
+  float sgd_lr;
+  float feature_noise;  /* sigma of the synthetic frame noise             */
+  double steps_per_gpu_s; /* SGD steps one effective GPU-second buys      */
+  uint64_t seed;
+} ecco_config;
+
+/* Defaults equal to the reference's ModelParams{} plus the learned-backend
+ * classifier shape of SURVEY.md 8(a'): F=512, H=256, C=16, B=128. */
+void ecco_default_config(ecco_config* cfg);
+
+ecco_status ecco_create(const ecco_config* cfg, ecco_ctx** out);
+void ecco_destroy(ecco_ctx* ctx);
+const char* ecco_last_error(const ecco_ctx* ctx);
+/* Number of kernels this context has launched (the bench's gpu_launches). */
+uint64_t ecco_kernel_launches(const ecco_ctx* ctx);
+/* cudaStream_t the context launches on (as void*). */
+void* ecco_stream(ecco_ctx* ctx);
+ecco_status ecco_synchronize(ecco_ctx* ctx);
+
+/* ---- camera table --------------------------------------------------------
+ * CameraState (accuracy_model.hpp:27-34): scene + gpu_pixel_throughput.
+ * Camera indices are positions in this table; the host keeps the
+ * CameraId <-> index map and passes member lists in std::string order. */
+ecco_status ecco_set_cameras(ecco_ctx* ctx, int n, const double* scenes /* n*D */,
+                             const double* gpu_pixel_throughput /* n */);
+/* apply_drift's scene change (accuracy_model.cpp:113-122) for a subset. */
+ecco_status ecco_update_scenes(ecco_ctx* ctx, int n, const int* cam_idx,
+                               const double* scenes /* n*D */);
+/* Learned backend: (re)generate window `window`'s synthetic frame rings and
+ * eval sets for every camera from (seed, camera, window, scene). */
+ecco_status ecco_generate_frames(ecco_ctx* ctx, int window);
+/* Learned backend, end-to-end path: upload frames produced on the host
+ * (pinned or pageable) instead of generating them on the device.
+ * frames: n*R*F bf16 bits, labels: n*R, eval: n*S*F bf16 bits, eval labels. */
+ecco_status ecco_upload_frames(ecco_ctx* ctx, int n_cams, const uint16_t* frames,
+                               const int32_t* labels, const uint16_t* eval_frames,
+                               const int32_t* eval_labels);
+/* Same upload from device buffers already resident in HBM (stream-ordered). */
+ecco_status ecco_upload_frames_dev(ecco_ctx* ctx, int n_cams, const void* frames,
+                                   const void* labels, const void* eval_frames,
+                                   const void* eval_labels);
+
+/* ---- job models (RetrainJob::model, job.hpp:25-36) -----------------------
+ * Parametric: ModelState = K clusters (K*D), K proficiencies, centroid (D;
+ * centroid_len 0 = empty model).  Arrays are packed per job with stride
+ * max_clusters. */
+ecco_status ecco_put_models(ecco_ctx* ctx, int n, const int* job_ids,
+                            const int* n_clusters, const double* clusters,
+                            const double* proficiency, const double* centroid,
+                            const int* centroid_len);
+ecco_status ecco_get_models(ecco_ctx* ctx, int n, const int* job_ids, int* n_clusters,
+                            double* clusters, double* proficiency, double* centroid,
+                            int* centroid_len);
+/* seed_model (accuracy_model.cpp:124-134) for new jobs: parametric seeds
+ * cluster = centroid = scene, prof = clamp((acc - floor)/span); learned
+ * initialises the MLP from (seed, job_id). */
+ecco_status ecco_seed_models(ecco_ctx* ctx, int n, const int* job_ids,
+                             const double* scenes /* n*D */, const double* device_acc);
+/* Job termination (orchestrator.cpp:375): frees the slots. */
+ecco_status ecco_drop_models(ecco_ctx* ctx, int n, const int* job_ids);
+/* Learned backend: read / write the fp32 master weights of one job
+ * (W1[F*H] row-major by feature, b1[H], W2[H*C], b2[C]). */
+ecco_status ecco_get_weights(ecco_ctx* ctx, int job_id, float* w1, float* b1, float* w2,
+                             float* b2);
+ecco_status ecco_set_weights(ecco_ctx* ctx, int job_id, const float* w1, const float* b1,
+                             const float* w2, const float* b2);
+
+/* ---- TrainingBackend::evaluate (orchestrator.cpp:43-50) -------------------
+ * Mean accuracy of each job's model over its members (camera indices in
+ * member order, CSR); summed sequentially in that order, then divided. */
+ecco_status ecco_eval_jobs(ecco_ctx* ctx, int n_jobs, const int* job_ids,
+                           const int* member_offsets /* n_jobs+1 */,
+                           const int* member_cams, double* out_mean /* n_jobs */);
+
+/* ---- ModelEvalFn batch: the camera x group evaluation matrix ---------------
+ * out[i*n_jobs + j] = eval(model(job_ids[j]), probe i).  A probe is a scene
+ * (parametric: `scenes`, n_probes*D) or a camera's labelled eval set
+ * (learned: `cam_idx`).  `mask` (nullable, n_probes*n_jobs bytes) skips
+ * pairs rejected by correlation_filter (grouping.cpp:9-16); skipped entries
+ * are written as NaN.  Replaces eval_job_on_scene (orchestrator.cpp:186-191)
+ * called from group_request (grouping.cpp:33). */
+ecco_status ecco_eval_matrix(ecco_ctx* ctx, int n_probes, const double* scenes,
+                             const int* cam_idx, int n_jobs, const int* job_ids,
+                             const uint8_t* mask, double* out);
+/* Device-resident variant: out_dev is an n_probes*n_jobs fp64 device buffer. */
+ecco_status ecco_eval_matrix_dev(ecco_ctx* ctx, int n_probes, const double* scenes,
+                                 const int* cam_idx, int n_jobs, const int* job_ids,
+                                 const uint8_t* mask, void* out_dev);
+/* Sparse form of the same matrix: out[p] = eval(model(job_ids[p]), probe p)
+ * where probe p is scenes[p] (parametric; nullable = the camera's current
+ * scene cams[p]) or camera cams[p]'s eval set (learned).  Used for the
+ * window-end per-member accuracies (orchestrator.cpp:330-341) and for
+ * routing passes whose candidate pairs were pruned by the filter. */
+ecco_status ecco_eval_pairs(ecco_ctx* ctx, int n_pairs, const double* scenes, const int* cams,
+                            const int* job_ids, double* out);
+/* Re-keys model slots (a model seeded under a provisional id becomes the
+ * job the host commits it as). */
+ecco_status ecco_rename_models(ecco_ctx* ctx, int n, const int* old_ids, const int* new_ids);
+/* Fused epilogue of group_request (grouping.cpp:30-39): for each probe the
+ * lowest-index job j (in job_ids order) maximising out[i,j] among unmasked
+ * pairs with out[i,j] >= req_acc[i] (strict '>' between candidates);
+ * best_col = -1 when none qualifies.  The host commits in request order. */
+ecco_status ecco_route_propose(ecco_ctx* ctx, int n_probes, const double* scenes,
+                               const int* cam_idx, const double* req_acc, int n_jobs,
+                               const int* job_ids, const uint8_t* mask, int* best_col,
+                               double* best_acc);
+
+/* ---- TrainingBackend::train batches: marginal-gain probes ------------------
+ * Batch description = TrainingBatchStats (accuracy_model.hpp:50-56) with the
+ * source_mix flattened to CSR (cameras in std::map order). */
+typedef struct {
+  double delivered_frame_rate;
+  double resolution;
+  double quality_factor;
+} ecco_batch;
+
+/* Speculative trajectories: for every job, from its committed model,
+ *   acc[j][0] = evaluate(j); for t = 1..depth: train(j, gpu_s); acc[j][t] =
+ *   evaluate(j)
+ * exactly as WindowAllocation::run_micro (gpu_allocator.cpp:125-135) would
+ * observe them.  `micro_base[j]` is the job's count of already committed
+ * micro-windows this window (keys the learned sampler; nullable = 0).  The
+ * model after every step is kept as a snapshot (depth <= max_depth) for
+ * ecco_commit.  Chains always start from the committed model: a caller that
+ * needs a longer chain for a job commits the granted prefix and asks again
+ * (the host replay only runs out of a chain when all of it was granted). */
+ecco_status ecco_train_trajectories(
+    ecco_ctx* ctx, int n_jobs, const int* job_ids, const ecco_batch* batches,
+    const int* src_offsets /* n_jobs+1 */, const int* src_cams, const double* src_fracs,
+    const int* member_offsets /* n_jobs+1 */, const int* member_cams,
+    const int* micro_base, int window, double gpu_seconds, int depth,
+    double* out_acc /* n_jobs*(depth+1) */);
+/* Makes the snapshot after granted[j] steps of the last chain (0 = keep the
+ * committed model) the committed model. */
+ecco_status ecco_commit(ecco_ctx* ctx, int n_jobs, const int* job_ids, const int* granted);
+/* Learned backend: mean minibatch loss of the last speculative chain per step
+ * (diagnostics; n_jobs*depth floats, NaN where no step ran). */
+ecco_status ecco_last_losses(ecco_ctx* ctx, int n_jobs, const int* job_ids, int depth,
+                             float* out);
+/* Sample indices the learned sampler draws for one (job, micro, step):
+ * out_cam/out_frame[B].  Exposed for the bit-exactness tests. */
+ecco_status ecco_sample_indices(ecco_ctx* ctx, int job_id, int n_src, const int* src_cams,
+                                const double* src_fracs, int window, int micro, int step,
+                                int* out_cam, int* out_frame);
+
+/* ---- ProbeFn batch: offline profile tables ---------------------------------
+ * build_profile_table (transmission.cpp:52-100) with make_accuracy_probe
+ * (transmission.cpp:102-118) for every camera in one launch, including the
+ * tie_epsilon / bias tie-break.  bias[i]: 0 resolution, 1 frame_rate.
+ * Outputs n_cams*n_levels rows in ascending budget order. */
+ecco_status ecco_profile_tables(ecco_ctx* ctx, int n_cams, const int* cam_idx,
+                                const int* bias, int n_levels, const double* levels,
+                                int n_grid, const double* grid_fps, const double* grid_res,
+                                double window_s, double tie_eps, double ref_rate_bps,
+                                double bpp_ref, double* out_budget, double* out_fps,
+                                double* out_res, uint8_t* out_feasible);
+
+/* ---- whole-window driver (Simulation::step_window, orchestrator.cpp:211-413)
+ * A host C++ restatement of the reference control loop that calls the
+ * batched entry points above.  Scenario JSON follows proj/README.md:107-169. */
+typedef struct ecco_sim ecco_sim;
+typedef struct {
+  int backend;         /* ecco_backend */
+  int math;            /* ecco_math (learned) */
+  int device;
+  int spec_depth;      /* initial speculative depth for run_remaining */
+  int feat_dim, hidden_dim, num_classes, minibatch, ring_frames, eval_samples;
+  float sgd_lr;
+  double steps_per_gpu_s;
+  uint64_t seed;
+  int host_frames;     /* learned: generate frames on the host and upload (e2e) */
+  int full_matrix;     /* evaluate the dense camera x group matrix every routing pass */
+} ecco_sim_options;
+void ecco_sim_default_options(ecco_sim_options* opt);
+ecco_status ecco_sim_create(const char* scenario_json, const ecco_sim_options* opt,
+                            ecco_sim** out, char* err, size_t err_len);
+void ecco_sim_destroy(ecco_sim* sim);
+const char* ecco_sim_last_error(const ecco_sim* sim);
+/* Returns 1 when a window ran, 0 when all windows have run. */
+ecco_status ecco_sim_step_window(ecco_sim* sim, int* ran);
+/* Timings of the last window in milliseconds: [0] whole window, [1] regroup
+ * (window-end eval + update_grouping + reroute + next routing), [2] train
+ * phase, [3] eval matrix, [4] host decision replay. */
+ecco_status ecco_sim_last_timings(const ecco_sim* sim, double* out5);
+/* Samples trained in the last window (sum over granted micro-windows). */
+int64_t ecco_sim_last_samples(const ecco_sim* sim);
+/* trace.csv / summary.json bytes (metrics.cpp:49-59, orchestrator.cpp:420-459).
+ * Returns the required size; copies at most cap bytes. */
+size_t ecco_sim_trace_csv(const ecco_sim* sim, char* buf, size_t cap);
+size_t ecco_sim_summary_json(const ecco_sim* sim, char* buf, size_t cap);
+ecco_ctx* ecco_sim_context(ecco_sim* sim);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ECCO_B200_H_ */

@@ -1,0 +1,480 @@
+"""B200-native group-retraining path of ECCO (arXiv 2512.11727).
+
+Python host mirror of the C-ABI in include/ecco_b200.h.  The compute lives in
+``libecco_b200.so`` (hand-written sm_100a CUDA kernels + the C++ window
+driver); this module only binds it.  There is no CPU fallback: importing the
+package without the built library, or calling into it without a GPU, raises.
+
+Names follow the reference interfaces the entry points replace
+(proj/core/include/ecco/*.hpp): ``Context.eval_jobs`` is a batch of
+``TrainingBackend::evaluate``, ``Context.eval_matrix`` a batch of
+``ModelEvalFn``, ``Context.train_trajectories`` the allocator's
+evaluate/train/evaluate probes, ``Context.profile_tables`` the ``ProbeFn`` grid
+of ``build_profile_table``, and ``Simulation`` the window loop of
+``ecco::Simulation``.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libecco_b200.so")
+
+OK, INVALID_ARGUMENT, LOGIC, INFEASIBLE, SCHEMA, CUDA, RUNTIME = range(7)
+PARAMETRIC, LEARNED = 0, 1
+FFMA_EXACT, TC_BF16 = 0, 1
+
+
+class EccoError(RuntimeError):
+    """Base of the errors raised for a non-OK ecco_status."""
+
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(EccoError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class LogicError(EccoError):
+    """std::logic_error in the reference."""
+
+
+class InfeasibleScheduleError(EccoError):
+    """ecco::InfeasibleScheduleError in the reference."""
+
+
+class SchemaError(EccoError, ValueError):
+    """ecco::SchemaError in the reference."""
+
+
+class CudaError(EccoError):
+    pass
+
+
+_ERRORS = {INVALID_ARGUMENT: InvalidArgument, LOGIC: LogicError, INFEASIBLE: InfeasibleScheduleError,
+           SCHEMA: SchemaError, CUDA: CudaError, RUNTIME: EccoError}
+
+
+class ModelParams(C.Structure):
+    _fields_ = [("learning_rate_k", C.c_double), ("similarity_lambda", C.c_double),
+                ("acc_floor", C.c_double), ("acc_ceil", C.c_double),
+                ("cluster_similarity_threshold", C.c_double)]
+
+
+class Config(C.Structure):
+    _fields_ = [("backend", C.c_int), ("device", C.c_int), ("scene_dims", C.c_int),
+                ("max_clusters", C.c_int), ("max_jobs", C.c_int), ("max_cameras", C.c_int),
+                ("params", ModelParams), ("math", C.c_int), ("feat_dim", C.c_int),
+                ("hidden_dim", C.c_int), ("num_classes", C.c_int), ("minibatch", C.c_int),
+                ("ring_frames", C.c_int), ("eval_samples", C.c_int), ("max_depth", C.c_int),
+                ("sgd_lr", C.c_float), ("feature_noise", C.c_float),
+                ("steps_per_gpu_s", C.c_double), ("seed", C.c_uint64)]
+
+
+class Batch(C.Structure):
+    _fields_ = [("delivered_frame_rate", C.c_double), ("resolution", C.c_double),
+                ("quality_factor", C.c_double)]
+
+
+class SimOptions(C.Structure):
+    _fields_ = [("backend", C.c_int), ("math", C.c_int), ("device", C.c_int),
+                ("spec_depth", C.c_int), ("feat_dim", C.c_int), ("hidden_dim", C.c_int),
+                ("num_classes", C.c_int), ("minibatch", C.c_int), ("ring_frames", C.c_int),
+                ("eval_samples", C.c_int), ("sgd_lr", C.c_float),
+                ("steps_per_gpu_s", C.c_double), ("seed", C.c_uint64),
+                ("host_frames", C.c_int), ("full_matrix", C.c_int)]
+
+
+_lib = None
+
+# Every symbol include/ecco_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "ecco_default_config", "ecco_create", "ecco_destroy", "ecco_last_error",
+    "ecco_kernel_launches", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
+    "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
+    "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
+    "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
+    "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
+    "ecco_train_trajectories", "ecco_commit", "ecco_last_losses", "ecco_sample_indices",
+    "ecco_profile_tables", "ecco_sim_default_options", "ecco_sim_create", "ecco_sim_destroy",
+    "ecco_sim_last_error", "ecco_sim_step_window", "ecco_sim_last_timings",
+    "ecco_sim_last_samples", "ecco_sim_trace_csv", "ecco_sim_summary_json", "ecco_sim_context",
+]
+
+
+def lib():
+    """Loads libecco_b200.so (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                              "(there is no CPU fallback for the CUDA path)")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.ecco_default_config.argtypes = [C.POINTER(Config)]
+        L.ecco_create.argtypes = [C.POINTER(Config), C.POINTER(vp)]
+        L.ecco_destroy.argtypes = [vp]
+        L.ecco_last_error.restype = C.c_char_p
+        L.ecco_last_error.argtypes = [vp]
+        L.ecco_kernel_launches.restype = C.c_uint64
+        L.ecco_kernel_launches.argtypes = [vp]
+        L.ecco_stream.restype = vp
+        L.ecco_stream.argtypes = [vp]
+        L.ecco_sim_default_options.argtypes = [C.POINTER(SimOptions)]
+        L.ecco_sim_create.argtypes = [C.c_char_p, C.POINTER(SimOptions), C.POINTER(vp),
+                                      C.c_char_p, C.c_size_t]
+        L.ecco_sim_destroy.argtypes = [vp]
+        L.ecco_sim_last_error.restype = C.c_char_p
+        L.ecco_sim_last_error.argtypes = [vp]
+        L.ecco_sim_step_window.argtypes = [vp, C.POINTER(C.c_int)]
+        L.ecco_sim_last_timings.argtypes = [vp, C.POINTER(C.c_double)]
+        L.ecco_sim_last_samples.restype = C.c_int64
+        L.ecco_sim_last_samples.argtypes = [vp]
+        L.ecco_sim_trace_csv.restype = C.c_size_t
+        L.ecco_sim_trace_csv.argtypes = [vp, C.c_char_p, C.c_size_t]
+        L.ecco_sim_summary_json.restype = C.c_size_t
+        L.ecco_sim_summary_json.argtypes = [vp, C.c_char_p, C.c_size_t]
+        L.ecco_sim_context.restype = vp
+        L.ecco_sim_context.argtypes = [vp]
+        for name in EXPORTS:
+            f = getattr(L, name)
+            if f.restype is C.c_int or name in ("ecco_synchronize",):
+                pass
+        _lib = L
+    return _lib
+
+
+def _p(a, dtype):
+    """Pointer to a contiguous numpy array of `dtype` (None passes NULL)."""
+    if a is None:
+        return None, None
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr, arr.ctypes.data_as(C.c_void_p)
+
+
+def default_config(**kw):
+    cfg = Config()
+    lib().ecco_default_config(C.byref(cfg))
+    for k, v in kw.items():
+        if k == "params":
+            for pk, pv in v.items():
+                setattr(cfg.params, pk, pv)
+        else:
+            setattr(cfg, k, v)
+    return cfg
+
+
+class Context:
+    """One ecco_ctx: device state of one GPU (cameras, job models, streams)."""
+
+    def __init__(self, **kw):
+        self.cfg = default_config(**kw)
+        self._h = C.c_void_p()
+        self._check(lib().ecco_create(C.byref(self.cfg), C.byref(self._h)), ctx=False)
+
+    def _check(self, st, ctx=True):
+        if st != OK:
+            msg = lib().ecco_last_error(self._h).decode() if ctx and self._h else "ecco_create failed"
+            raise _ERRORS.get(st, EccoError)(st, msg)
+
+    def close(self):
+        if self._h:
+            lib().ecco_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def launches(self):
+        return lib().ecco_kernel_launches(self._h)
+
+    @property
+    def stream(self):
+        return lib().ecco_stream(self._h)
+
+    def synchronize(self):
+        self._check(lib().ecco_synchronize(self._h))
+
+    # camera table
+    def set_cameras(self, scenes, throughput):
+        s, sp = _p(scenes, np.float64)
+        t, tpp = _p(throughput, np.float64)
+        self._check(lib().ecco_set_cameras(self._h, len(t), sp, tpp))
+
+    def update_scenes(self, cam_idx, scenes):
+        c, cp = _p(cam_idx, np.int32)
+        s, sp = _p(scenes, np.float64)
+        self._check(lib().ecco_update_scenes(self._h, len(c), cp, sp))
+
+    def generate_frames(self, window):
+        self._check(lib().ecco_generate_frames(self._h, int(window)))
+
+    def upload_frames(self, frames, labels, eval_frames, eval_labels):
+        f, fp = _p(frames, np.uint16)
+        l, lp = _p(labels, np.int32)
+        e, ep = _p(eval_frames, np.uint16)
+        el, elp = _p(eval_labels, np.int32)
+        n = len(l) // self.cfg.ring_frames
+        self._check(lib().ecco_upload_frames(self._h, n, fp, lp, ep, elp))
+
+    def upload_frames_dev(self, n_cams, frames_ptr, labels_ptr, eval_ptr, eval_labels_ptr):
+        self._check(lib().ecco_upload_frames_dev(self._h, int(n_cams), C.c_void_p(frames_ptr),
+                                                 C.c_void_p(labels_ptr), C.c_void_p(eval_ptr),
+                                                 C.c_void_p(eval_labels_ptr)))
+
+    # models
+    def put_models(self, job_ids, n_clusters, clusters, prof, centroid, centroid_len):
+        j, jp = _p(job_ids, np.int32)
+        k, kp = _p(n_clusters, np.int32)
+        c, cp = _p(clusters, np.float64)
+        pr, pp = _p(prof, np.float64)
+        ce, cep = _p(centroid, np.float64)
+        cl, clp = _p(centroid_len, np.int32)
+        self._check(lib().ecco_put_models(self._h, len(j), jp, kp, cp, pp, cep, clp))
+
+    def get_models(self, job_ids):
+        j, jp = _p(job_ids, np.int32)
+        n, K, D = len(j), self.cfg.max_clusters, self.cfg.scene_dims
+        k = np.zeros(n, np.int32)
+        c = np.zeros((n, K, D))
+        pr = np.zeros((n, K))
+        ce = np.zeros((n, D))
+        cl = np.zeros(n, np.int32)
+        self._check(lib().ecco_get_models(self._h, n, jp, k.ctypes.data_as(C.c_void_p),
+                                          c.ctypes.data_as(C.c_void_p), pr.ctypes.data_as(C.c_void_p),
+                                          ce.ctypes.data_as(C.c_void_p), cl.ctypes.data_as(C.c_void_p)))
+        return k, c, pr, ce, cl
+
+    def seed_models(self, job_ids, scenes=None, device_acc=None):
+        j, jp = _p(job_ids, np.int32)
+        s, sp = _p(scenes, np.float64)
+        a, ap = _p(device_acc, np.float64)
+        self._check(lib().ecco_seed_models(self._h, len(j), jp, sp, ap))
+
+    def drop_models(self, job_ids):
+        j, jp = _p(job_ids, np.int32)
+        self._check(lib().ecco_drop_models(self._h, len(j), jp))
+
+    def rename_models(self, old_ids, new_ids):
+        o, op = _p(old_ids, np.int32)
+        n, np_ = _p(new_ids, np.int32)
+        self._check(lib().ecco_rename_models(self._h, len(o), op, np_))
+
+    def _wshapes(self):
+        F, H, Cc = self.cfg.feat_dim, self.cfg.hidden_dim, self.cfg.num_classes
+        return (F, H), (H,), (H, Cc), (Cc,)
+
+    def get_weights(self, job_id):
+        arrs = [np.zeros(s, np.float32) for s in self._wshapes()]
+        self._check(lib().ecco_get_weights(self._h, int(job_id),
+                                           *[a.ctypes.data_as(C.c_void_p) for a in arrs]))
+        return arrs
+
+    def set_weights(self, job_id, w1, b1, w2, b2):
+        arrs = [np.ascontiguousarray(a, np.float32) for a in (w1, b1, w2, b2)]
+        self._check(lib().ecco_set_weights(self._h, int(job_id),
+                                           *[a.ctypes.data_as(C.c_void_p) for a in arrs]))
+
+    # evaluation
+    def eval_jobs(self, job_ids, members):
+        """TrainingBackend::evaluate for many jobs; members: list of camera-index lists."""
+        j, jp = _p(job_ids, np.int32)
+        off = np.zeros(len(members) + 1, np.int32)
+        off[1:] = np.cumsum([len(m) for m in members])
+        mc = np.array([c for m in members for c in m] or [0], np.int32)
+        out = np.zeros(len(j))
+        self._check(lib().ecco_eval_jobs(self._h, len(j), jp, off.ctypes.data_as(C.c_void_p),
+                                         mc.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def eval_matrix(self, job_ids, scenes=None, cams=None, mask=None):
+        j, jp = _p(job_ids, np.int32)
+        s, sp = _p(scenes, np.float64)
+        c, cp = _p(cams, np.int32)
+        m, mp = _p(mask, np.uint8)
+        n = len(c) if c is not None else len(s) // self.cfg.scene_dims if s.ndim == 1 else len(s)
+        out = np.zeros((n, len(j)))
+        self._check(lib().ecco_eval_matrix(self._h, n, sp, cp, len(j), jp, mp,
+                                           out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def eval_matrix_dev(self, job_ids, out_ptr, scenes=None, cams=None, mask=None):
+        j, jp = _p(job_ids, np.int32)
+        s, sp = _p(scenes, np.float64)
+        c, cp = _p(cams, np.int32)
+        m, mp = _p(mask, np.uint8)
+        n = len(c) if c is not None else len(s)
+        self._check(lib().ecco_eval_matrix_dev(self._h, n, sp, cp, len(j), jp, mp,
+                                               C.c_void_p(out_ptr)))
+
+    def eval_pairs(self, job_ids, scenes=None, cams=None):
+        j, jp = _p(job_ids, np.int32)
+        s, sp = _p(scenes, np.float64)
+        c, cp = _p(cams, np.int32)
+        out = np.zeros(len(j))
+        self._check(lib().ecco_eval_pairs(self._h, len(j), sp, cp, jp, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def route_propose(self, job_ids, req_acc, scenes=None, cams=None, mask=None):
+        j, jp = _p(job_ids, np.int32)
+        r, rp = _p(req_acc, np.float64)
+        s, sp = _p(scenes, np.float64)
+        c, cp = _p(cams, np.int32)
+        m, mp = _p(mask, np.uint8)
+        n = len(r)
+        best = np.zeros(n, np.int32)
+        acc = np.zeros(n)
+        self._check(lib().ecco_route_propose(self._h, n, sp, cp, rp, len(j), jp, mp,
+                                             best.ctypes.data_as(C.c_void_p),
+                                             acc.ctypes.data_as(C.c_void_p)))
+        return best, acc
+
+    # training
+    def train_trajectories(self, job_ids, batches, sources, fracs, members, gpu_seconds, depth,
+                           micro_base=None, window=0):
+        """Speculative evaluate/train chains.  batches: list of (fps, res, quality);
+        sources/fracs: per-job source_mix (camera indices in map order, fractions);
+        members: per-job member camera indices.  Returns acc[n_jobs, depth+1]."""
+        j, jp = _p(job_ids, np.int32)
+        n = len(j)
+        bt = (Batch * max(n, 1))(*[Batch(*b) for b in batches])
+        so = np.zeros(n + 1, np.int32)
+        so[1:] = np.cumsum([len(s) for s in sources])
+        sc = np.array([c for s in sources for c in s] or [0], np.int32)
+        sf = np.array([f for s in fracs for f in s] or [0.0], np.float64)
+        mo = np.zeros(n + 1, np.int32)
+        mo[1:] = np.cumsum([len(m) for m in members])
+        mc = np.array([c for m in members for c in m] or [0], np.int32)
+        mb, mbp = _p(micro_base if micro_base is not None else np.zeros(n), np.int32)
+        out = np.zeros((n, depth + 1))
+        self._check(lib().ecco_train_trajectories(
+            self._h, n, jp, bt, so.ctypes.data_as(C.c_void_p), sc.ctypes.data_as(C.c_void_p),
+            sf.ctypes.data_as(C.c_void_p), mo.ctypes.data_as(C.c_void_p),
+            mc.ctypes.data_as(C.c_void_p), mbp, C.c_int(window), C.c_double(gpu_seconds),
+            C.c_int(depth), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def commit(self, job_ids, granted):
+        j, jp = _p(job_ids, np.int32)
+        g, gp = _p(granted, np.int32)
+        self._check(lib().ecco_commit(self._h, len(j), jp, gp))
+
+    def last_losses(self, job_ids, depth):
+        j, jp = _p(job_ids, np.int32)
+        out = np.zeros((len(j), depth), np.float32)
+        self._check(lib().ecco_last_losses(self._h, len(j), jp, int(depth),
+                                           out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def sample_indices(self, job_id, src_cams, src_fracs, window, micro, step):
+        c, cp = _p(src_cams, np.int32)
+        f, fp = _p(src_fracs, np.float64)
+        B = self.cfg.minibatch
+        oc = np.zeros(B, np.int32)
+        of = np.zeros(B, np.int32)
+        self._check(lib().ecco_sample_indices(self._h, int(job_id), len(c), cp, fp, int(window),
+                                              int(micro), int(step), oc.ctypes.data_as(C.c_void_p),
+                                              of.ctypes.data_as(C.c_void_p)))
+        return oc, of
+
+    def profile_tables(self, cam_idx, levels, grid_fps, grid_res, window_s, bias=None,
+                       tie_eps=1e-9, ref_rate_bps=1e6, bpp_ref=0.1):
+        c, cp = _p(cam_idx, np.int32)
+        b, bp = _p(bias, np.int32)
+        l, lp = _p(levels, np.float64)
+        gf, gfp = _p(grid_fps, np.float64)
+        gq, gqp = _p(grid_res, np.float64)
+        rows = (len(c), len(l))
+        ob, of, oq = np.zeros(rows), np.zeros(rows), np.zeros(rows)
+        fe = np.zeros(rows, np.uint8)
+        self._check(lib().ecco_profile_tables(
+            self._h, len(c), cp, bp, len(l), lp, len(gf), gfp, gqp, C.c_double(window_s),
+            C.c_double(tie_eps), C.c_double(ref_rate_bps), C.c_double(bpp_ref),
+            ob.ctypes.data_as(C.c_void_p), of.ctypes.data_as(C.c_void_p),
+            oq.ctypes.data_as(C.c_void_p), fe.ctypes.data_as(C.c_void_p)))
+        return ob, of, oq, fe
+
+
+def default_sim_options(**kw):
+    o = SimOptions()
+    lib().ecco_sim_default_options(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+class Simulation:
+    """ecco::Simulation (orchestrator.hpp:34-73) over the B200 path."""
+
+    def __init__(self, scenario_json, **options):
+        if isinstance(scenario_json, dict):
+            import json
+            scenario_json = json.dumps(scenario_json)
+        self.options = default_sim_options(**options)
+        self._h = C.c_void_p()
+        err = C.create_string_buffer(4096)
+        st = lib().ecco_sim_create(scenario_json.encode(), C.byref(self.options), C.byref(self._h),
+                                   err, 4096)
+        if st != OK:
+            raise _ERRORS.get(st, EccoError)(st, err.value.decode())
+
+    def close(self):
+        if self._h:
+            lib().ecco_sim_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step_window(self):
+        ran = C.c_int()
+        st = lib().ecco_sim_step_window(self._h, C.byref(ran))
+        if st != OK:
+            raise _ERRORS.get(st, EccoError)(st, lib().ecco_sim_last_error(self._h).decode())
+        return bool(ran.value)
+
+    def run(self):
+        while self.step_window():
+            pass
+
+    def last_timings(self):
+        t = (C.c_double * 5)()
+        lib().ecco_sim_last_timings(self._h, t)
+        return dict(zip(("window_ms", "regroup_ms", "train_ms", "window_end_ms", "replay_ms"), list(t)))
+
+    def last_samples(self):
+        return lib().ecco_sim_last_samples(self._h)
+
+    def trace_csv(self):
+        n = lib().ecco_sim_trace_csv(self._h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        lib().ecco_sim_trace_csv(self._h, buf, n)
+        return buf.raw[:n].decode()
+
+    def summary_json(self):
+        n = lib().ecco_sim_summary_json(self._h, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        lib().ecco_sim_summary_json(self._h, buf, n)
+        return buf.raw[:n].decode()
+
+    @property
+    def context_handle(self):
+        return lib().ecco_sim_context(self._h)
+
+    @property
+    def launches(self):
+        return lib().ecco_kernel_launches(self.context_handle)

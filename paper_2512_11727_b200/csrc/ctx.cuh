@@ -1,0 +1,204 @@
+// Internal state of an ecco_ctx and the helpers shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/ecco_b200.h"
+
+// Status carried through the C++ layer as an exception, converted back to an
+// ecco_status at the C-ABI boundary (abi.cu).
+struct EccoError {
+  ecco_status code;
+  std::string msg;
+};
+
+[[noreturn]] inline void ecco_throw(ecco_status code, const std::string& msg) {
+  throw EccoError{code, msg};
+}
+
+#define ECCO_CUDA(call)                                                                \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      ecco_throw(ECCO_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+#define ECCO_REQUIRE(cond, msg)                                        \
+  do {                                                                 \
+    if (!(cond)) ecco_throw(ECCO_ERR_INVALID_ARGUMENT, (msg));         \
+  } while (0)
+
+// Growable device scratch buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
+      if (cudaMalloc(&p, want) != cudaSuccess) ecco_throw(ECCO_ERR_CUDA, "cudaMalloc scratch");
+      cap = want;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// Growable pinned host staging buffer.
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
+      if (cudaMallocHost(&p, want) != cudaSuccess) ecco_throw(ECCO_ERR_CUDA, "cudaMallocHost");
+      cap = want;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct ecco_ctx {
+  ecco_config cfg{};
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+
+  // camera table (replicated on every rank)
+  int n_cams = 0;
+  std::vector<double> h_scenes, h_tp;
+  double* d_scenes = nullptr;  // max_cameras * D
+  double* d_tp = nullptr;      // max_cameras
+  uint64_t* d_exp_tab = nullptr;
+
+  // model slots keyed by JobId
+  std::unordered_map<int, int> slot_of;
+  std::vector<int> free_slots;
+
+  // parametric models: committed state + speculative chain (max_depth+1 states)
+  int* d_k = nullptr;          // slots
+  int* d_clen = nullptr;       // slots
+  double* d_cl = nullptr;      // slots * K * D
+  double* d_prof = nullptr;    // slots * K
+  double* d_cen = nullptr;     // slots * D
+  int* d_sk = nullptr;         // slots * (max_depth+1)
+  int* d_sclen = nullptr;
+  double* d_scl = nullptr;     // slots * (max_depth+1) * K * D
+  double* d_sprof = nullptr;
+  double* d_scen = nullptr;
+  int* d_status = nullptr;     // device-side error flag
+
+  // learned backend
+  size_t n_params = 0;         // F*H + H + H*C + C
+  float* d_w = nullptr;        // slots * n_params (committed fp32 masters)
+  float* d_wspec = nullptr;    // slots * max_depth * n_params (snapshots)
+  float* d_proto_p = nullptr;  // C * F
+  float* d_proto_q = nullptr;  // C * D * F
+  uint16_t* d_frames = nullptr;  // max_cameras * R * F (bf16 bits)
+  int32_t* d_labels = nullptr;   // max_cameras * R
+  uint16_t* d_eval = nullptr;    // max_cameras * S * F
+  int32_t* d_eval_labels = nullptr;
+  float* d_losses = nullptr;     // slots * max_depth
+  int frames_window = -1;
+
+  DevBuf scratch[8];
+  HostBuf hscratch[4];
+
+  int slot(int job_id) const {
+    auto it = slot_of.find(job_id);
+    if (it == slot_of.end())
+      ecco_throw(ECCO_ERR_INVALID_ARGUMENT, "unknown job id " + std::to_string(job_id));
+    return it->second;
+  }
+  int alloc_slot(int job_id) {
+    auto it = slot_of.find(job_id);
+    if (it != slot_of.end()) return it->second;
+    if (free_slots.empty()) ecco_throw(ECCO_ERR_RUNTIME, "model slots exhausted (max_jobs)");
+    int s = free_slots.back();
+    free_slots.pop_back();
+    slot_of[job_id] = s;
+    return s;
+  }
+  // Copies a host array to a fresh scratch device buffer (stream-ordered).
+  template <class T>
+  T* upload(int which, const T* h, size_t n) {
+    if (n == 0) return nullptr;
+    T* d = (T*)scratch[which].get(n * sizeof(T));
+    ECCO_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, stream));
+    return d;
+  }
+  void check_device_status();
+};
+
+// Kernel launch bookkeeping (counts every launch for the bench's gpu_launches).
+#define ECCO_LAUNCHED(ctx)                                  \
+  do {                                                      \
+    (ctx)->launches++;                                      \
+    cudaError_t e_ = cudaGetLastError();                    \
+    if (e_ != cudaSuccess)                                  \
+      ecco_throw(ECCO_ERR_CUDA, cudaGetErrorString(e_));    \
+  } while (0)
+
+// ---- entry points implemented per backend ----
+namespace pbackend {
+void eval_matrix(ecco_ctx* ctx, int n_probes, const double* d_scenes_in, int n_jobs,
+                 const int* d_slots, const uint8_t* d_mask, double* d_out);
+void route_propose(ecco_ctx* ctx, int n_probes, const double* d_scenes_in, const double* d_req,
+                   int n_jobs, const int* d_slots, const uint8_t* d_mask, int* d_best,
+                   double* d_best_acc);
+void trajectories(ecco_ctx* ctx, int n_jobs, const int* d_slots, const double* d_batch,
+                  const int* d_src_off, const int* d_src_cam, const double* d_src_frac,
+                  const int* d_mem_off, const int* d_mem_cam, double gpu_s, int depth,
+                  double* d_out);
+void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted);
+void eval_jobs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_mem_off,
+               const int* d_mem_cam, double* d_out);
+void profile(ecco_ctx* ctx, int n_cams, const int* d_cam, const int* d_bias, int n_levels,
+             const double* d_levels, int n_grid, const double* d_gf, const double* d_gq,
+             double window_s, double tie_eps, double ref_rate, double bpp_ref, double* d_fps,
+             double* d_res, uint8_t* d_feas);
+void seed(ecco_ctx* ctx, int n, const int* d_slots, const double* d_scenes_in,
+          const double* d_acc);
+void eval_pairs(ecco_ctx* ctx, int n, const double* d_scenes_in, const int* d_cams,
+                const int* d_slots, double* d_out);
+}  // namespace pbackend
+
+namespace lbackend {
+void init(ecco_ctx* ctx);
+void generate_frames(ecco_ctx* ctx, int window);
+void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const int* d_job_ids);
+void eval_matrix(ecco_ctx* ctx, int n_probes, const int* d_cams, int n_jobs, const int* d_slots,
+                 const uint8_t* d_mask, double* d_out);
+void route_propose(ecco_ctx* ctx, int n_probes, const int* d_cams, const double* d_req,
+                   int n_jobs, const int* d_slots, const uint8_t* d_mask, int* d_best,
+                   double* d_best_acc);
+void eval_jobs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_mem_off,
+               const int* d_mem_cam, double* d_out);
+void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_slots,
+                  const int* d_job_ids, const int* h_steps, const int* d_src_off,
+                  const int* d_src_cam, const double* d_src_frac, const int* d_mem_off,
+                  const int* d_mem_cam, const int* d_micro_base, int window, int depth,
+                  double* d_out);
+void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted);
+void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, double* d_out);
+void sample_indices(ecco_ctx* ctx, int job_id, int n_src, const int* d_src_cam,
+                    const double* d_src_frac, int window, int micro, int step, int* d_cam,
+                    int* d_frame);
+}  // namespace lbackend

@@ -1,0 +1,816 @@
+// Learned backend (backend L): synthetic camera streams resident in HBM,
+// counter-based frame sampler, grouped MLP forward/backward/SGD for every
+// job in one launch per phase, and the camera x group evaluation matrix.
+//
+// Specification: oracle/ecco_oracle.c (orc_gen_frames, orc_sample,
+// orc_sgd_step, orc_count_correct).  The kernels in this file are the
+// ECCO_MATH_FFMA_EXACT path: every output element is produced by one thread
+// that accumulates in the oracle's sequential order with explicit fmaf, so
+// results are bit-identical to the oracle.  The tensor-core path
+// (tc_kernels.cu) replaces the two dense contractions.
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "ctx.cuh"
+#include "learned_common.cuh"
+
+namespace {
+
+struct LDims {
+  int F, H, C, D, B, R, S;
+  float lr, noise;
+};
+
+LDims dims(const ecco_ctx* c) {
+  return {c->cfg.feat_dim,  c->cfg.hidden_dim,  c->cfg.num_classes, c->cfg.scene_dims,
+          c->cfg.minibatch, c->cfg.ring_frames, c->cfg.eval_samples, c->cfg.sgd_lr,
+          c->cfg.feature_noise};
+}
+
+__device__ __forceinline__ void seed_key(uint64_t seed, uint32_t salt, uint32_t& k0,
+                                         uint32_t& k1) {
+  k0 = (uint32_t)seed ^ salt;
+  k1 = (uint32_t)(seed >> 32);
+}
+
+// ---------------------------------------------------------------- streams --
+
+__global__ void k_l_prototypes(LDims g, uint64_t seed, float* P, float* Q) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= g.C * g.F) return;
+  const int k = idx / g.F, f = idx % g.F;
+  uint32_t k0, k1, out[4];
+  seed_key(seed, 0u, k0, k1);
+  philox4x32((uint32_t)f, (uint32_t)k, 0u, 0xFE000000u, k0, k1, out);
+  P[idx] = usym(out[0]);
+  for (int d = 0; d < g.D; ++d) {
+    philox4x32((uint32_t)f, (uint32_t)k, 1u + d, 0xFE000000u, k0, k1, out);
+    Q[((size_t)k * g.D + d) * g.F + f] = __fmul_rn(usym(out[0]), 4.0f);
+  }
+}
+
+// One thread per (camera, frame, 4 features); labels by the f4 == 0 thread.
+// tag 0: training ring (R frames), tag 1: labelled eval set (S frames).
+__global__ void __launch_bounds__(256) k_l_gen_frames(LDims g, uint64_t seed, int n_cams,
+                                                      int window, int tag, int n_frames,
+                                                      const double* scenes, const float* P,
+                                                      const float* Q, uint16_t* x, int32_t* y) {
+  const int f4n = g.F / 4;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t total = (size_t)n_cams * n_frames * f4n;
+  if (idx >= total) return;
+  const int f4 = (int)(idx % f4n);
+  const size_t rf = idx / f4n;
+  const int r = (int)(rf % n_frames);
+  const int cam = (int)(rf / n_frames);
+  uint32_t k0, k1, out[4];
+  seed_key(seed, 0u, k0, k1);
+  const uint32_t wt = ((uint32_t)window & 0xFFFFFFu) | ((uint32_t)tag << 24);
+  philox4x32(0xFFFFFFFFu, (uint32_t)r, (uint32_t)cam, wt, k0, k1, out);
+  const int lab = (int)(out[0] % (uint32_t)g.C);
+  if (f4 == 0) y[rf] = lab;
+  philox4x32((uint32_t)f4, (uint32_t)r, (uint32_t)cam, wt, k0, k1, out);
+  float sd[8];
+  for (int d = 0; d < g.D; ++d) sd[d] = (float)scenes[(size_t)cam * g.D + d];
+  uint16_t v4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int f = f4 * 4 + i;
+    const float nz = __fsub_rn(__fmul_rn((float)((out[i] & 0xFFFFu) + (out[i] >> 16)), 0x1p-16f), 1.0f);
+    float v = P[(size_t)lab * g.F + f];
+    for (int d = 0; d < g.D; ++d) v = __fmaf_rn(sd[d], Q[((size_t)lab * g.D + d) * g.F + f], v);
+    v = __fmaf_rn(g.noise, nz, v);
+    v4[i] = f32_to_bf16(v);
+  }
+  uint2 packed;
+  packed.x = (uint32_t)v4[0] | ((uint32_t)v4[1] << 16);
+  packed.y = (uint32_t)v4[2] | ((uint32_t)v4[3] << 16);
+  *reinterpret_cast<uint2*>(x + rf * g.F + (size_t)f4 * 4) = packed;
+}
+
+// --------------------------------------------------------------- weights --
+
+// Base model (orc_init_weights): every new job starts from it.
+__global__ void k_l_init_weights(LDims g, uint64_t seed, int n, const int* slots, float* w,
+                                 size_t n_params) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)n * n_params) return;
+  const int j = (int)(idx / n_params);
+  const size_t q = idx % n_params;
+  uint32_t k0, k1, out[4];
+  seed_key(seed, 0x27D4EB2Fu, k0, k1);
+  float v = 0.0f;
+  const size_t fh = (size_t)g.F * g.H;
+  const size_t w2o = fh + g.H;
+  if (q < fh) {
+    const int f = (int)(q / g.H), h = (int)(q % g.H);
+    philox4x32((uint32_t)h, (uint32_t)f, 1u, 3u << 24, k0, k1, out);
+    v = __fmul_rn(usym(out[0]), __fsqrt_rn(__fdiv_rn(6.0f, (float)g.F)));
+  } else if (q >= w2o && q < w2o + (size_t)g.H * g.C) {
+    const size_t r = q - w2o;
+    const int k = (int)(r / g.C), c = (int)(r % g.C);
+    philox4x32((uint32_t)c, (uint32_t)k, 2u, 3u << 24, k0, k1, out);
+    v = __fmul_rn(usym(out[0]), __fsqrt_rn(__fdiv_rn(6.0f, (float)g.H)));
+  }
+  w[(size_t)slots[j] * n_params + q] = v;
+}
+
+// ------------------------------------------------------------- sampler --
+
+// Rows of one (job, step) minibatch: source by the cumulative source_mix in
+// map order, frame uniform in the ring.  Writes the element offset of the
+// row in the frame table and its label.
+__device__ __forceinline__ void sample_one(const LDims& g, uint64_t seed, int job_id, int n_src,
+                                           const int* src_cam, const double* src_frac,
+                                           int window, int micro, int step, int s, int* cam_out,
+                                           int* frame_out) {
+  uint32_t k0, k1, out[4];
+  seed_key(seed, (uint32_t)job_id * 0x9E3779B9u + 0x632BE5ABu, k0, k1);
+  const uint32_t wt = ((uint32_t)window & 0xFFFFFFu) | (2u << 24);
+  philox4x32((uint32_t)s, (uint32_t)step, (uint32_t)micro, wt, k0, k1, out);
+  const double u = __dmul_rn((double)(((uint64_t)out[0] << 21) | (out[1] >> 11)), 0x1p-53);
+  double cum = 0.0;
+  int pick = n_src - 1;
+  for (int i = 0; i < n_src; ++i) {
+    cum = __dadd_rn(cum, src_frac[i]);
+    if (u < cum) {
+      pick = i;
+      break;
+    }
+  }
+  *cam_out = src_cam[pick];
+  *frame_out = (int)(out[2] % (uint32_t)g.R);
+}
+
+__global__ void k_l_sample(LDims g, uint64_t seed, int n_jobs, const int* job_ids,
+                           const int* steps, const int* src_off, const int* src_cam,
+                           const double* src_frac, const int* micro_base, int window, int t,
+                           int step, const int32_t* labels, int64_t* row_off, int32_t* row_lab) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_jobs * g.B) return;
+  const int j = idx / g.B, s = idx % g.B;
+  if (step >= steps[j]) return;
+  int cam, frame;
+  const int s0 = src_off[j];
+  sample_one(g, seed, job_ids[j], src_off[j + 1] - s0, src_cam + s0, src_frac + s0, window,
+             micro_base[j] + t, step, s, &cam, &frame);
+  const int64_t row = (int64_t)cam * g.R + frame;
+  row_off[idx] = row * g.F;
+  row_lab[idx] = labels[row];
+}
+
+__global__ void k_l_sample_debug(LDims g, uint64_t seed, int job_id, int n_src,
+                                 const int* src_cam, const double* src_frac, int window,
+                                 int micro, int step, int* out_cam, int* out_frame) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= g.B) return;
+  sample_one(g, seed, job_id, n_src, src_cam, src_frac, window, micro, step, s, out_cam + s,
+             out_frame + s);
+}
+
+// ------------------------------------------------------ FFMA contractions --
+//
+// Row blocks of 64 rows share one model slot.  Z[row, h] = sum_f x[row,f] *
+// W1[f,h] (sequential f) + b1[h].  256 threads, 64 x 128 output tile, each
+// thread owns 4 rows x 8 columns.
+
+constexpr int kRB = 64;   // rows per block
+constexpr int kHB = 128;  // hidden columns per block
+constexpr int kKT = 32;   // k tile
+
+__global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* xbase,
+                                                       const int64_t* row_off,
+                                                       const int* blk_slot, const int* blk_on,
+                                                       const float* wbase, size_t n_params,
+                                                       float* Z) {
+  const int blk = blockIdx.x;
+  if (blk_on && !blk_on[blk]) return;
+  const int h0 = blockIdx.y * kHB;
+  const float* W1 = wbase + (size_t)blk_slot[blk] * n_params;
+  const float* b1 = W1 + (size_t)g.F * g.H;
+  __shared__ float As[kKT][kRB + 4];
+  __shared__ __align__(16) float Bs[kKT][kHB];
+  __shared__ int64_t rows[kRB];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  if (tid < kRB) rows[tid] = row_off[(size_t)blk * kRB + tid];
+  __syncthreads();
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+  for (int k0 = 0; k0 < g.F; k0 += kKT) {
+    // X tile: 64 rows x 32 k (bf16 pairs), transposed into As[k][row]
+    for (int e = tid; e < kRB * kKT / 2; e += 256) {
+      const int r = e / (kKT / 2), kk = (e % (kKT / 2)) * 2;
+      const uint32_t two = *reinterpret_cast<const uint32_t*>(xbase + rows[r] + k0 + kk);
+      As[kk][r] = __uint_as_float(two << 16);
+      As[kk + 1][r] = __uint_as_float(two & 0xFFFF0000u);
+    }
+    for (int e = tid; e < kKT * kHB / 4; e += 256) {
+      const int kk = e / (kHB / 4), c4 = (e % (kHB / 4)) * 4;
+      *reinterpret_cast<float4*>(&Bs[kk][c4]) =
+          *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + kk) * g.H + h0 + c4);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kKT; ++kk) {
+      float a[4], b[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8 + 4]);
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b4.x; b[5] = b4.y; b[6] = b4.z; b[7] = b4.w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const size_t r = (size_t)blk * kRB + ty * 4 + i;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int h = h0 + tx * 8 + j;
+      Z[r * g.H + h] = __fadd_rn(acc[i][j], b1[h]);
+    }
+  }
+}
+
+// logits[row, c] = sum_k relu(Z[row,k]) * W2[k,c] (sequential k) + b2[c].
+__global__ void __launch_bounds__(256) k_l_logits(LDims g, int n_rows, const int* blk_slot,
+                                                  const int* blk_on, const float* wbase,
+                                                  size_t n_params, const float* Z, float* L) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)n_rows * g.C) return;
+  const int r = (int)(idx / g.C), c = (int)(idx % g.C);
+  const int blk = r / kRB;
+  if (blk_on && !blk_on[blk]) return;
+  const float* W = wbase + (size_t)blk_slot[blk] * n_params;
+  const float* W2 = W + (size_t)g.F * g.H + g.H;
+  const float* b2 = W2 + (size_t)g.H * g.C;
+  const float* z = Z + (size_t)r * g.H;
+  float a = 0.0f;
+  for (int k = 0; k < g.H; ++k) {
+    const float zk = z[k];
+    a = __fmaf_rn(zk > 0.0f ? zk : 0.0f, W2[(size_t)k * g.C + c], a);
+  }
+  L[idx] = __fadd_rn(a, b2[c]);
+}
+
+// Softmax cross-entropy gradient of one training row.
+__global__ void k_l_softmax_grad(LDims g, int n_rows, const int* blk_on, const float* L,
+                                 const int32_t* lab, float* DL, float* loss_rows) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  if (blk_on && !blk_on[r / kRB]) return;
+  const float* l = L + (size_t)r * g.C;
+  float m = l[0];
+  for (int c = 1; c < g.C; ++c) m = l[c] > m ? l[c] : m;
+  float sum = 0.0f;
+  for (int c = 0; c < g.C; ++c) sum = __fadd_rn(sum, ecco_expf(__fsub_rn(l[c], m)));
+  const float invB = __fdiv_rn(1.0f, (float)g.B);
+  const int y = lab[r];
+  for (int c = 0; c < g.C; ++c) {
+    const float p = __fdiv_rn(ecco_expf(__fsub_rn(l[c], m)), sum);
+    DL[(size_t)r * g.C + c] = __fmul_rn(__fsub_rn(p, c == y ? 1.0f : 0.0f), invB);
+  }
+  loss_rows[r] = logf(sum) - (l[y] - m);
+}
+
+// dh[row, k] = Z > 0 ? sum_c DL[row,c] * W2[k,c] : 0 (pre-update W2).
+__global__ void __launch_bounds__(256) k_l_dh(LDims g, int n_rows, const int* blk_slot,
+                                              const int* blk_on, const float* wbase,
+                                              size_t n_params, const float* Z, const float* DL,
+                                              float* DH) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)n_rows * g.H) return;
+  const int r = (int)(idx / g.H), k = (int)(idx % g.H);
+  const int blk = r / kRB;
+  if (blk_on && !blk_on[blk]) return;
+  const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
+  float a = 0.0f;
+  if (Z[idx] > 0.0f)
+    for (int c = 0; c < g.C; ++c) a = __fmaf_rn(DL[(size_t)r * g.C + c], W2[(size_t)k * g.C + c], a);
+  DH[idx] = a;
+}
+
+// W2[k,c] -= lr * sum_s relu(Z[s,k]) * DL[s,c]; b2[c] -= lr * sum_s DL[s,c].
+// One job = B rows starting at job * B.
+__global__ void __launch_bounds__(256) k_l_update2(LDims g, int n_jobs, const int* slots,
+                                                   const int* steps, int step, float* wbase,
+                                                   size_t n_params, const float* Z,
+                                                   const float* DL) {
+  const int per = g.H * g.C + g.C;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)n_jobs * per) return;
+  const int j = (int)(idx / per), q = (int)(idx % per);
+  if (step >= steps[j]) return;
+  float* W2 = wbase + (size_t)slots[j] * n_params + (size_t)g.F * g.H + g.H;
+  float* b2 = W2 + (size_t)g.H * g.C;
+  const size_t r0 = (size_t)j * g.B;
+  float a = 0.0f;
+  if (q < g.H * g.C) {
+    const int k = q / g.C, c = q % g.C;
+    for (int s = 0; s < g.B; ++s) {
+      const float zk = Z[(r0 + s) * g.H + k];
+      a = __fmaf_rn(zk > 0.0f ? zk : 0.0f, DL[(r0 + s) * g.C + c], a);
+    }
+    W2[q] = __fmaf_rn(-g.lr, a, W2[q]);
+  } else {
+    const int c = q - g.H * g.C;
+    for (int s = 0; s < g.B; ++s) a = __fadd_rn(a, DL[(r0 + s) * g.C + c]);
+    b2[c] = __fmaf_rn(-g.lr, a, b2[c]);
+  }
+}
+
+// W1[f,h] -= lr * sum_s x[s,f] * dh[s,h] (sequential s).  Tile 64 f x 128 h.
+__global__ void __launch_bounds__(256) k_l_update1_ffma(LDims g, const int* slots,
+                                                        const int* steps, int step,
+                                                        const uint16_t* xbase,
+                                                        const int64_t* row_off, float* wbase,
+                                                        size_t n_params, const float* DH) {
+  const int j = blockIdx.z;
+  if (step >= steps[j]) return;
+  const int f0 = blockIdx.x * 64, h0 = blockIdx.y * kHB;
+  float* W1 = wbase + (size_t)slots[j] * n_params;
+  __shared__ float As[kKT][64 + 4];
+  __shared__ __align__(16) float Bs[kKT][kHB];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[i][q] = 0.0f;
+  const size_t r0 = (size_t)j * g.B;
+  for (int s0 = 0; s0 < g.B; s0 += kKT) {
+    for (int e = tid; e < kKT * 32; e += 256) {  // 32 samples x 64 f (bf16 pairs)
+      const int s = e / 32, ff = (e % 32) * 2;
+      const uint32_t two = *reinterpret_cast<const uint32_t*>(xbase + row_off[r0 + s0 + s] + f0 + ff);
+      As[s][ff] = __uint_as_float(two << 16);
+      As[s][ff + 1] = __uint_as_float(two & 0xFFFF0000u);
+    }
+    for (int e = tid; e < kKT * kHB / 4; e += 256) {
+      const int s = e / (kHB / 4), c4 = (e % (kHB / 4)) * 4;
+      *reinterpret_cast<float4*>(&Bs[s][c4]) =
+          *reinterpret_cast<const float4*>(DH + (r0 + s0 + s) * g.H + h0 + c4);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int s = 0; s < kKT; ++s) {
+      float a[4], b[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[s][ty * 4 + i];
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[s][tx * 8]);
+      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[s][tx * 8 + 4]);
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b4.x; b[5] = b4.y; b[6] = b4.z; b[7] = b4.w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[i][q] = __fmaf_rn(a[i], b[q], acc[i][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int f = f0 + ty * 4 + i;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const size_t o = (size_t)f * g.H + h0 + tx * 8 + q;
+      W1[o] = __fmaf_rn(-g.lr, acc[i][q], W1[o]);
+    }
+  }
+}
+
+__global__ void k_l_update_b1(LDims g, int n_jobs, const int* slots, const int* steps, int step,
+                              float* wbase, size_t n_params, const float* DH) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n_jobs * g.H) return;
+  const int j = idx / g.H, h = idx % g.H;
+  if (step >= steps[j]) return;
+  float* b1 = wbase + (size_t)slots[j] * n_params + (size_t)g.F * g.H;
+  const size_t r0 = (size_t)j * g.B;
+  float a = 0.0f;
+  for (int s = 0; s < g.B; ++s) a = __fadd_rn(a, DH[(r0 + s) * g.H + h]);
+  b1[h] = __fmaf_rn(-g.lr, a, b1[h]);
+}
+
+// Mean minibatch loss per job for this step (diagnostics).
+__global__ void k_l_loss_mean(LDims g, int n_jobs, const int* slots, const int* steps, int step,
+                              const float* loss_rows, float* out, int T, int t) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_jobs) return;
+  if (step == 0 && steps[j] == 0) out[(size_t)slots[j] * T + t] = __int_as_float(0x7fc00000);
+  if (step >= steps[j]) return;
+  double a = 0.0;
+  for (int s = 0; s < g.B; ++s) a += loss_rows[(size_t)j * g.B + s];
+  out[(size_t)slots[j] * T + t] = (float)(a / g.B);
+}
+
+// ------------------------------------------------------------- eval ------
+
+// Correct-prediction count of each (slot, camera) pair over the camera's S
+// eval frames; one warp per (pair, row), first-max argmax like the oracle.
+__global__ void k_l_count(LDims g, int n_pairs, const int* blk_on, const float* L,
+                          const int32_t* eval_labels, const int* pair_cam, int* counts) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_pairs * g.S) return;
+  const int p = r / g.S, s = r % g.S;
+  if (blk_on && !blk_on[r / kRB]) return;
+  const float* l = L + (size_t)r * g.C;
+  int best = 0;
+  for (int c = 1; c < g.C; ++c)
+    if (l[c] > l[best]) best = c;
+  if (best == eval_labels[(size_t)pair_cam[p] * g.S + s]) atomicAdd(&counts[p], 1);
+}
+
+__global__ void k_l_pair_rows(LDims g, int n_pairs, const int* pair_slot, const int* pair_cam,
+                              int64_t* row_off, int* blk_slot) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_pairs * g.S) return;
+  const int p = r / g.S, s = r % g.S;
+  row_off[r] = ((int64_t)pair_cam[p] * g.S + s) * g.F;
+  if (r % kRB == 0) blk_slot[r / kRB] = pair_slot[p];
+}
+
+// acc = count / S; masked pairs become NaN.
+__global__ void k_l_matrix_out(LDims g, int n, const int* counts, const int* pair_out,
+                               double* out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  out[pair_out[p]] = __ddiv_rn((double)counts[p], (double)g.S);
+}
+
+__global__ void k_l_fill_nan(size_t n, double* out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __longlong_as_double(0x7ff8000000000000LL);
+}
+
+// Per-job mean over members (sequential in member order).
+__global__ void k_l_job_mean(LDims g, int n_jobs, const int* mem_off, const int* counts,
+                             double floor_acc, double* out, int stride, int col) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_jobs) return;
+  const int m0 = mem_off[j], nm = mem_off[j + 1] - m0;
+  double sum = 0.0;
+  for (int m = 0; m < nm; ++m) sum = __dadd_rn(sum, __ddiv_rn((double)counts[m0 + m], (double)g.S));
+  out[(size_t)j * stride + col] = nm == 0 ? floor_acc : __ddiv_rn(sum, (double)nm);
+}
+
+__global__ void k_l_route(int n, int g, const double* M, const double* req, int* best_col,
+                          double* best_acc) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (i >= n) return;
+  int bc = -1;
+  double ba = 0.0;
+  const double r = req[i];
+  for (int j = lane; j < g; j += 32) {
+    const double a = M[(size_t)i * g + j];
+    if (a != a || a < r) continue;  // masked (NaN) or below the device accuracy
+    if (bc < 0 || a > ba) {
+      bc = j;
+      ba = a;
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    const int oc = __shfl_down_sync(0xffffffffu, bc, off);
+    const double oa = __shfl_down_sync(0xffffffffu, ba, off);
+    if (oc >= 0 && (bc < 0 || oa > ba || (oa == ba && oc < bc))) {
+      bc = oc;
+      ba = oa;
+    }
+  }
+  if (lane == 0) {
+    best_col[i] = bc;
+    best_acc[i] = bc >= 0 ? ba : 0.0;
+  }
+}
+
+__global__ void k_l_copy_weights(int n_jobs, const int* slots, const float* src_base,
+                                 size_t src_slot_stride, size_t src_off, float* dst_base,
+                                 size_t dst_slot_stride, size_t dst_off, size_t n_params,
+                                 const int* sel) {
+  const int j = blockIdx.y;
+  if (sel && sel[j] <= 0) return;
+  const int slot = slots[j];
+  const float4* s = reinterpret_cast<const float4*>(src_base + (size_t)slot * src_slot_stride +
+                                                    src_off + (sel ? (size_t)(sel[j] - 1) * n_params : 0));
+  float4* d = reinterpret_cast<float4*>(dst_base + (size_t)slot * dst_slot_stride + dst_off);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_params / 4;
+       i += (size_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+}  // namespace
+
+// ====================================================================
+namespace lbackend {
+
+static inline unsigned nblk(size_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+void init(ecco_ctx* ctx) {
+  const LDims g = dims(ctx);
+  k_l_prototypes<<<nblk((size_t)g.C * g.F, 256), 256, 0, ctx->stream>>>(g, ctx->cfg.seed,
+                                                                         ctx->d_proto_p, ctx->d_proto_q);
+  ECCO_LAUNCHED(ctx);
+}
+
+void generate_frames(ecco_ctx* ctx, int window) {
+  const LDims g = dims(ctx);
+  if (ctx->n_cams == 0) return;
+  size_t total = (size_t)ctx->n_cams * g.R * (g.F / 4);
+  k_l_gen_frames<<<nblk(total, 256), 256, 0, ctx->stream>>>(
+      g, ctx->cfg.seed, ctx->n_cams, window, 0, g.R, ctx->d_scenes, ctx->d_proto_p,
+      ctx->d_proto_q, ctx->d_frames, ctx->d_labels);
+  ECCO_LAUNCHED(ctx);
+  total = (size_t)ctx->n_cams * g.S * (g.F / 4);
+  k_l_gen_frames<<<nblk(total, 256), 256, 0, ctx->stream>>>(
+      g, ctx->cfg.seed, ctx->n_cams, window, 1, g.S, ctx->d_scenes, ctx->d_proto_p,
+      ctx->d_proto_q, ctx->d_eval, ctx->d_eval_labels);
+  ECCO_LAUNCHED(ctx);
+  ctx->frames_window = window;
+}
+
+void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const int* d_job_ids) {
+  (void)h_job_ids;
+  (void)d_job_ids;
+  if (n == 0) return;
+  const LDims g = dims(ctx);
+  k_l_init_weights<<<nblk((size_t)n * ctx->n_params, 256), 256, 0, ctx->stream>>>(
+      g, ctx->cfg.seed, n, d_slots, ctx->d_w, ctx->n_params);
+  ECCO_LAUNCHED(ctx);
+}
+
+// Counts for a list of (slot, camera) pairs, chunked to bound scratch.
+static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, const int* d_pair_cam,
+                        int* d_counts) {
+  const LDims g = dims(ctx);
+  ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(n_pairs, 1), ctx->stream));
+  const int chunk = std::max(1, (int)std::min<size_t>(n_pairs, (size_t)(256u << 20) / ((size_t)g.S * g.H * 4)));
+  for (int p0 = 0; p0 < n_pairs; p0 += chunk) {
+    const int np = std::min(chunk, n_pairs - p0);
+    const int rows = np * g.S;
+    const int nb = rows / kRB;
+    int64_t* row_off = (int64_t*)ctx->scratch[4].get(sizeof(int64_t) * rows);
+    int* blk_slot = (int*)ctx->scratch[5].get(sizeof(int) * nb);
+    float* Z = (float*)ctx->scratch[6].get(sizeof(float) * (size_t)rows * g.H);
+    float* L = (float*)ctx->scratch[7].get(sizeof(float) * (size_t)rows * g.C);
+    k_l_pair_rows<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, d_pair_slot + p0,
+                                                             d_pair_cam + p0, row_off, blk_slot);
+    ECCO_LAUNCHED(ctx);
+    k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
+        g, ctx->d_eval, row_off, blk_slot, nullptr, ctx->d_w, ctx->n_params, Z);
+    ECCO_LAUNCHED(ctx);
+    k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
+        g, rows, blk_slot, nullptr, ctx->d_w, ctx->n_params, Z, L);
+    ECCO_LAUNCHED(ctx);
+    k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, nullptr, L, ctx->d_eval_labels,
+                                                         d_pair_cam + p0, d_counts + p0);
+    ECCO_LAUNCHED(ctx);
+  }
+}
+
+void eval_matrix(ecco_ctx* ctx, int n, const int* d_cams, int gj, const int* d_slots,
+                 const uint8_t* d_mask, double* d_out) {
+  if (n == 0 || gj == 0) return;
+  // host-side pair list (mask applied on the host copy when given)
+  const size_t total = (size_t)n * gj;
+  std::vector<int> slots(gj), cams(n);
+  ECCO_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * gj, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(cudaMemcpyAsync(cams.data(), d_cams, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  std::vector<uint8_t> mask;
+  if (d_mask) {
+    mask.resize(total);
+    ECCO_CUDA(cudaMemcpyAsync(mask.data(), d_mask, total, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<int> ps, pc, po;
+  ps.reserve(total);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < gj; ++j) {
+      const size_t o = (size_t)i * gj + j;
+      if (d_mask && !mask[o]) continue;
+      ps.push_back(slots[j]);
+      pc.push_back(cams[i]);
+      po.push_back((int)o);
+    }
+  if (d_mask) {
+    k_l_fill_nan<<<nblk(total, 256), 256, 0, ctx->stream>>>(total, d_out);
+    ECCO_LAUNCHED(ctx);
+  }
+  const int np = (int)ps.size();
+  if (np == 0) return;
+  int* d_ps = ctx->upload(0, ps.data(), np);
+  int* d_pc = ctx->upload(1, pc.data(), np);
+  int* d_po = ctx->upload(2, po.data(), np);
+  int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * np);
+  pair_counts(ctx, np, d_ps, d_pc, d_cnt);
+  k_l_matrix_out<<<nblk(np, 256), 256, 0, ctx->stream>>>(dims(ctx), np, d_cnt, d_po, d_out);
+  ECCO_LAUNCHED(ctx);
+}
+
+void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, double* d_out) {
+  if (n == 0) return;
+  DevBuf cnt, idx;
+  int* d_cnt = (int*)cnt.get(sizeof(int) * n);
+  std::vector<int> po(n);
+  for (int i = 0; i < n; ++i) po[i] = i;
+  int* d_po = (int*)idx.get(sizeof(int) * n);
+  ECCO_CUDA(cudaMemcpyAsync(d_po, po.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+  pair_counts(ctx, n, d_slots, d_cams, d_cnt);
+  k_l_matrix_out<<<nblk(n, 256), 256, 0, ctx->stream>>>(dims(ctx), n, d_cnt, d_po, d_out);
+  ECCO_LAUNCHED(ctx);
+  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  cnt.release();
+  idx.release();
+}
+
+void route_propose(ecco_ctx* ctx, int n, const int* d_cams, const double* d_req, int gj,
+                   const int* d_slots, const uint8_t* d_mask, int* d_best, double* d_best_acc) {
+  if (n == 0) return;
+  double* M = nullptr;
+  DevBuf tmp;
+  if (gj > 0) {
+    M = (double*)tmp.get(sizeof(double) * (size_t)n * gj);
+    eval_matrix(ctx, n, d_cams, gj, d_slots, d_mask, M);
+  }
+  k_l_route<<<nblk((size_t)n * 32, 256), 256, 0, ctx->stream>>>(n, gj, M, d_req, d_best, d_best_acc);
+  ECCO_LAUNCHED(ctx);
+  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  tmp.release();
+}
+
+static void member_pairs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_mem_off,
+                         const int* d_mem_cam, std::vector<int>& h_off, int** d_ps) {
+  h_off.resize(n_jobs + 1);
+  std::vector<int> slots(n_jobs);
+  ECCO_CUDA(cudaMemcpyAsync(h_off.data(), d_mem_off, sizeof(int) * (n_jobs + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<int> ps(h_off[n_jobs]);
+  for (int j = 0; j < n_jobs; ++j)
+    for (int m = h_off[j]; m < h_off[j + 1]; ++m) ps[m] = slots[j];
+  *d_ps = ctx->upload(0, ps.data(), ps.size());
+  (void)d_mem_cam;
+}
+
+void eval_jobs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_mem_off,
+               const int* d_mem_cam, double* d_out) {
+  if (n_jobs == 0) return;
+  std::vector<int> off;
+  int* d_ps = nullptr;
+  member_pairs(ctx, n_jobs, d_slots, d_mem_off, d_mem_cam, off, &d_ps);
+  const int np = off[n_jobs];
+  int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * std::max(np, 1));
+  if (np) pair_counts(ctx, np, d_ps, d_mem_cam, d_cnt);
+  k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(dims(ctx), n_jobs, d_mem_off, d_cnt,
+                                                            ctx->cfg.params.acc_floor, d_out, 1, 0);
+  ECCO_LAUNCHED(ctx);
+}
+
+void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_slots,
+                  const int* d_job_ids, const int* h_steps, const int* d_src_off,
+                  const int* d_src_cam, const double* d_src_frac, const int* d_mem_off,
+                  const int* d_mem_cam, const int* d_micro_base, int window, int depth,
+                  double* d_out) {
+  (void)h_job_ids;
+  if (n_jobs == 0) return;
+  const LDims g = dims(ctx);
+  const size_t np = ctx->n_params;
+  const int T = ctx->cfg.max_depth;
+  ECCO_REQUIRE(depth <= T, "depth exceeds max_depth");
+  int max_steps = 0;
+  for (int j = 0; j < n_jobs; ++j) max_steps = std::max(max_steps, h_steps[j]);
+  int* d_steps = ctx->upload(1, h_steps, n_jobs);
+  // member pairs for evaluate
+  std::vector<int> off;
+  int* d_ps = nullptr;
+  member_pairs(ctx, n_jobs, d_slots, d_mem_off, d_mem_cam, off, &d_ps);
+  const int n_mem = off[n_jobs];
+  int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * std::max(n_mem, 1));
+  // training scratch: rows = n_jobs * B
+  const int rows = n_jobs * g.B;
+  const int nb = rows / kRB;
+  DevBuf b_row, b_lab, b_slot, b_on, b_z, b_l, b_dl, b_dh, b_loss;
+  int64_t* row_off = (int64_t*)b_row.get(sizeof(int64_t) * rows);
+  int32_t* row_lab = (int32_t*)b_lab.get(sizeof(int32_t) * rows);
+  int* blk_slot = (int*)b_slot.get(sizeof(int) * nb);
+  int* blk_on = (int*)b_on.get(sizeof(int) * nb);
+  float* Z = (float*)b_z.get(sizeof(float) * (size_t)rows * g.H);
+  float* L = (float*)b_l.get(sizeof(float) * (size_t)rows * g.C);
+  float* DL = (float*)b_dl.get(sizeof(float) * (size_t)rows * g.C);
+  float* DH = (float*)b_dh.get(sizeof(float) * (size_t)rows * g.H);
+  float* loss_rows = (float*)b_loss.get(sizeof(float) * rows);
+  // spec chain buffer per slot: T snapshots; train in place in snapshot t-1
+  std::vector<int> slots(n_jobs);
+  ECCO_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<int> hb_slot(nb), hb_on(nb);
+  const int rb_per_job = g.B / kRB;
+  for (int j = 0; j < n_jobs; ++j)
+    for (int q = 0; q < rb_per_job; ++q) hb_slot[j * rb_per_job + q] = slots[j];
+  ECCO_CUDA(cudaMemcpyAsync(blk_slot, hb_slot.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, ctx->stream));
+  // the spec snapshots use a virtual "slot" base: wspec + slot * T * np + (t-1) * np
+  const size_t spec_stride = (size_t)T * np;
+  // acc[:, 0] from the committed models
+  if (n_mem) pair_counts(ctx, n_mem, d_ps, d_mem_cam, d_cnt);
+  k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
+                                                            ctx->cfg.params.acc_floor, d_out, depth + 1, 0);
+  ECCO_LAUNCHED(ctx);
+  for (int t = 1; t <= depth; ++t) {
+    // state t starts as a copy of state t-1
+    if (t == 1)
+      k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(n_jobs, d_slots, ctx->d_w, np, 0,
+                                                                  ctx->d_wspec, spec_stride, 0, np, nullptr);
+    else
+      k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(
+          n_jobs, d_slots, ctx->d_wspec, spec_stride, (size_t)(t - 2) * np, ctx->d_wspec,
+          spec_stride, (size_t)(t - 1) * np, np, nullptr);
+    ECCO_LAUNCHED(ctx);
+    // weights of state t are addressed as wbase + slot * spec_stride
+    float* wt = ctx->d_wspec + (size_t)(t - 1) * np;
+    // the per-slot stride for kernels is spec_stride: pass n_params = spec_stride
+    for (int step = 0; step < max_steps; ++step) {
+      for (int j = 0; j < n_jobs; ++j)
+        for (int q = 0; q < rb_per_job; ++q) hb_on[j * rb_per_job + q] = step < h_steps[j];
+      ECCO_CUDA(cudaMemcpyAsync(blk_on, hb_on.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, ctx->stream));
+      k_l_sample<<<nblk(rows, 256), 256, 0, ctx->stream>>>(
+          g, ctx->cfg.seed, n_jobs, d_job_ids, d_steps, d_src_off, d_src_cam, d_src_frac,
+          d_micro_base, window, t - 1, step, ctx->d_labels, row_off, row_lab);
+      ECCO_LAUNCHED(ctx);
+      k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
+          g, ctx->d_frames, row_off, blk_slot, blk_on, wt, spec_stride, Z);
+      ECCO_LAUNCHED(ctx);
+      k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
+          g, rows, blk_slot, blk_on, wt, spec_stride, Z, L);
+      ECCO_LAUNCHED(ctx);
+      k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(g, rows, blk_on, L, row_lab, DL,
+                                                                  loss_rows);
+      ECCO_LAUNCHED(ctx);
+      k_l_dh<<<nblk((size_t)rows * g.H, 256), 256, 0, ctx->stream>>>(
+          g, rows, blk_slot, blk_on, wt, spec_stride, Z, DL, DH);
+      ECCO_LAUNCHED(ctx);
+      k_l_update2<<<nblk((size_t)n_jobs * (g.H * g.C + g.C), 256), 256, 0, ctx->stream>>>(
+          g, n_jobs, d_slots, d_steps, step, wt, spec_stride, Z, DL);
+      ECCO_LAUNCHED(ctx);
+      k_l_update1_ffma<<<dim3(g.F / 64, g.H / kHB, n_jobs), 256, 0, ctx->stream>>>(
+          g, d_slots, d_steps, step, ctx->d_frames, row_off, wt, spec_stride, DH);
+      ECCO_LAUNCHED(ctx);
+      k_l_update_b1<<<nblk((size_t)n_jobs * g.H, 256), 256, 0, ctx->stream>>>(
+          g, n_jobs, d_slots, d_steps, step, wt, spec_stride, DH);
+      ECCO_LAUNCHED(ctx);
+      k_l_loss_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(
+          g, n_jobs, d_slots, d_steps, step, loss_rows, ctx->d_losses, T, t - 1);
+      ECCO_LAUNCHED(ctx);
+    }
+    // evaluate state t: temporarily point the pair evaluation at the snapshot
+    float* saved = ctx->d_w;
+    const size_t saved_np = ctx->n_params;
+    ctx->d_w = wt;
+    ctx->n_params = spec_stride;
+    try {
+      if (n_mem) pair_counts(ctx, n_mem, d_ps, d_mem_cam, d_cnt);
+    } catch (...) {
+      ctx->d_w = saved;
+      ctx->n_params = saved_np;
+      throw;
+    }
+    ctx->d_w = saved;
+    ctx->n_params = saved_np;
+    k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
+                                                              ctx->cfg.params.acc_floor, d_out, depth + 1, t);
+    ECCO_LAUNCHED(ctx);
+  }
+  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  b_row.release(); b_lab.release(); b_slot.release(); b_on.release(); b_z.release();
+  b_l.release(); b_dl.release(); b_dh.release(); b_loss.release();
+}
+
+void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted) {
+  if (n_jobs == 0) return;
+  const size_t np = ctx->n_params;
+  const size_t spec_stride = (size_t)ctx->cfg.max_depth * np;
+  k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(n_jobs, d_slots, ctx->d_wspec,
+                                                              spec_stride, 0, ctx->d_w, np, 0, np,
+                                                              d_granted);
+  ECCO_LAUNCHED(ctx);
+}
+
+void sample_indices(ecco_ctx* ctx, int job_id, int n_src, const int* d_src_cam,
+                    const double* d_src_frac, int window, int micro, int step, int* d_cam,
+                    int* d_frame) {
+  const LDims g = dims(ctx);
+  k_l_sample_debug<<<nblk(g.B, 128), 128, 0, ctx->stream>>>(g, ctx->cfg.seed, job_id, n_src,
+                                                             d_src_cam, d_src_frac, window, micro,
+                                                             step, d_cam, d_frame);
+  ECCO_LAUNCHED(ctx);
+}
+
+}  // namespace lbackend

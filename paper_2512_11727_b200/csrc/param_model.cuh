@@ -1,0 +1,125 @@
+// Device restatement of the reference's parametric accuracy model
+// (proj/core/src/accuracy_model.cpp).  Compiled with -fmad=false: every
+// expression keeps the reference's left-to-right evaluation order and
+// rounding, and exp comes from the bit-exact glibc port in ecco_exp.cuh, so
+// each function returns the same double the reference returns.
+#pragma once
+#include <stdint.h>
+
+#include "ecco_exp.cuh"
+
+#define ECCO_PMAX_D 8      // scene dimensions supported on the device
+#define ECCO_PMAX_K 32     // cluster capacity supported on the device
+
+struct PParams {
+  double k, lambda, floor, ceil, thr;
+};
+
+// euclidean + similarity: accuracy_model.cpp:10-17, 28-34.
+__device__ __forceinline__ double p_similarity(const double* a, const double* b, int d,
+                                               double lambda, const uint64_t* tab) {
+  double sq = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double t = __dsub_rn(a[i], b[i]);
+    sq = __dadd_rn(sq, __dmul_rn(t, t));
+  }
+  return ecco_exp_tab(__ddiv_rn(-__dsqrt_rn(sq), lambda), tab);
+}
+
+// find_cluster: accuracy_model.cpp:36-49 (strict '>' from 0.0, then >= thr).
+__device__ __forceinline__ int p_find_cluster(int k, const double* cl, int d, const double* scene,
+                                              const PParams& p, const uint64_t* tab) {
+  int best = -1;
+  double best_sim = 0.0;
+  for (int c = 0; c < k; ++c) {
+    const double s = p_similarity(cl + c * d, scene, d, p.lambda, tab);
+    if (s > best_sim) {
+      best_sim = s;
+      best = c;
+    }
+  }
+  if (best >= 0 && best_sim >= p.thr) return best;
+  return -1;
+}
+
+// eval: accuracy_model.cpp:60-67; floor + ((ceil - floor) * prof) * sim.
+__device__ __forceinline__ double p_eval(int k, const double* cl, const double* prof, int clen,
+                                         const double* cen, int d, const double* scene,
+                                         const PParams& p, const uint64_t* tab) {
+  if (k == 0 || clen == 0) return p.floor;
+  const int c = p_find_cluster(k, cl, d, scene, p, tab);
+  const double pr = c < 0 ? 0.0 : prof[c];
+  const double sim = p_similarity(scene, cen, d, p.lambda, tab);
+  return __dadd_rn(p.floor, __dmul_rn(__dmul_rn(__dsub_rn(p.ceil, p.floor), pr), sim));
+}
+
+// pixels_per_frame: types.cpp:11-13.
+__device__ __forceinline__ double p_ppf(double q) {
+  return __dmul_rn(q, __ddiv_rn(__dmul_rn(16.0, q), 9.0));
+}
+
+// effort of train_step: accuracy_model.cpp:82-86 (sources' throughputs in
+// source order; mean = sequential sum / count).
+__device__ __forceinline__ double p_effort(double fps, double res, double quality, double gpu_s,
+                                           int n_src, const int* src_cam, const double* cam_tp) {
+  const double supplied = __dmul_rn(fps, p_ppf(res));
+  double required = 0.0;
+  if (n_src > 0) {
+    double sum = 0.0;
+    for (int i = 0; i < n_src; ++i) sum = __dadd_rn(sum, cam_tp[src_cam[i]]);
+    required = __ddiv_rn(sum, (double)n_src);
+  }
+  double suff = 1.0;
+  if (required > 0.0) {
+    const double r = __ddiv_rn(supplied, required);
+    suff = r < 1.0 ? r : 1.0;  // std::min(1.0, r)
+  }
+  return __dmul_rn(__dmul_rn(gpu_s, suff), quality);
+}
+
+// train_step body after validation: accuracy_model.cpp:86-110.  The model
+// (cl: kmax*d, prof: kmax) is updated in place.  Returns 0, or 2 when a new
+// cluster would exceed kmax.
+__device__ __forceinline__ int p_train_step(int* k, double* cl, double* prof, int* clen,
+                                            double* cen, int kmax, int d, double effort,
+                                            int n_src, const int* src_cam, const double* src_frac,
+                                            const double* cam_scenes, const PParams& p,
+                                            const uint64_t* tab) {
+  if (!(effort > 0.0)) return 0;
+  double weight[ECCO_PMAX_K];
+  bool touched[ECCO_PMAX_K];
+  for (int c = 0; c < kmax; ++c) {
+    weight[c] = 0.0;
+    touched[c] = false;
+  }
+  double acc_cen[ECCO_PMAX_D];
+  bool have_cen = false;
+  for (int i = 0; i < n_src; ++i) {
+    const double* sc = cam_scenes + (size_t)src_cam[i] * d;
+    int c = p_find_cluster(*k, cl, d, sc, p, tab);
+    if (c < 0) {
+      if (*k >= kmax) return 2;
+      for (int j = 0; j < d; ++j) cl[*k * d + j] = sc[j];
+      prof[*k] = 0.0;
+      c = (*k)++;
+    }
+    weight[c] = __dadd_rn(weight[c], src_frac[i]);
+    touched[c] = true;
+    if (!have_cen) {
+      for (int j = 0; j < d; ++j) acc_cen[j] = 0.0;
+      have_cen = true;
+    }
+    for (int j = 0; j < d; ++j) acc_cen[j] = __dadd_rn(acc_cen[j], __dmul_rn(src_frac[i], sc[j]));
+  }
+  for (int c = 0; c < *k; ++c) {
+    if (!touched[c] || weight[c] <= 0.0) continue;
+    const double pr = prof[c];
+    const double e = ecco_exp_tab(__dmul_rn(__dmul_rn(-p.k, effort), weight[c]), tab);
+    prof[c] = __dsub_rn(1.0, __dmul_rn(__dsub_rn(1.0, pr), e));
+  }
+  if (have_cen) {
+    for (int j = 0; j < d; ++j) cen[j] = acc_cen[j];
+    *clen = d;
+  }
+  return 0;
+}
