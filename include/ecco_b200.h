@@ -120,6 +120,10 @@ ecco_status ecco_generate_frames(ecco_ctx* ctx, int window);
 ecco_status ecco_upload_frames(ecco_ctx* ctx, int n_cams, const uint16_t* frames,
                                const int32_t* labels, const uint16_t* eval_frames,
                                const int32_t* eval_labels);
+/* Copies the first n_cams cameras' resident frames back to the host (same
+ * layouts as ecco_upload_frames; any pointer may be NULL). */
+ecco_status ecco_read_frames(ecco_ctx* ctx, int n_cams, uint16_t* frames, int32_t* labels,
+                             uint16_t* eval_frames, int32_t* eval_labels);
 /* Same upload from device buffers already resident in HBM (stream-ordered). */
 ecco_status ecco_upload_frames_dev(ecco_ctx* ctx, int n_cams, const void* frames,
                                    const void* labels, const void* eval_frames,

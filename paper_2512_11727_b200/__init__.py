@@ -95,6 +95,7 @@ EXPORTS = [
     "ecco_default_config", "ecco_create", "ecco_destroy", "ecco_last_error",
     "ecco_kernel_launches", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
     "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
+    "ecco_read_frames",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
@@ -227,6 +228,16 @@ class Context:
         el, elp = _p(eval_labels, np.int32)
         n = len(l) // self.cfg.ring_frames
         self._check(lib().ecco_upload_frames(self._h, n, fp, lp, ep, elp))
+
+    def read_frames(self, n_cams):
+        g = self.cfg
+        fr = np.zeros((n_cams, g.ring_frames, g.feat_dim), np.uint16)
+        lb = np.zeros((n_cams, g.ring_frames), np.int32)
+        ev = np.zeros((n_cams, g.eval_samples, g.feat_dim), np.uint16)
+        el = np.zeros((n_cams, g.eval_samples), np.int32)
+        self._check(lib().ecco_read_frames(self._h, int(n_cams), *[a.ctypes.data_as(C.c_void_p)
+                                                                   for a in (fr, lb, ev, el)]))
+        return fr, lb, ev, el
 
     def upload_frames_dev(self, n_cams, frames_ptr, labels_ptr, eval_ptr, eval_labels_ptr):
         self._check(lib().ecco_upload_frames_dev(self._h, int(n_cams), C.c_void_p(frames_ptr),

@@ -277,6 +277,22 @@ ecco_status ecco_upload_frames(ecco_ctx* ctx, int n, const uint16_t* frames, con
   });
 }
 
+ecco_status ecco_read_frames(ecco_ctx* ctx, int n, uint16_t* frames, int32_t* labels,
+                             uint16_t* eval, int32_t* eval_labels) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(learned(ctx), "read_frames: learned backend only");
+    ECCO_REQUIRE(n >= 0 && n <= ctx->n_cams, "read_frames: camera count");
+    const ecco_config& g = ctx->cfg;
+    const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n * g.eval_samples;
+    const cudaMemcpyKind k = cudaMemcpyDeviceToHost;
+    if (frames) ECCO_CUDA(cudaMemcpyAsync(frames, ctx->d_frames, fr * g.feat_dim * 2, k, ctx->stream));
+    if (labels) ECCO_CUDA(cudaMemcpyAsync(labels, ctx->d_labels, fr * 4, k, ctx->stream));
+    if (eval) ECCO_CUDA(cudaMemcpyAsync(eval, ctx->d_eval, ev * g.feat_dim * 2, k, ctx->stream));
+    if (eval_labels) ECCO_CUDA(cudaMemcpyAsync(eval_labels, ctx->d_eval_labels, ev * 4, k, ctx->stream));
+    ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 ecco_status ecco_upload_frames_dev(ecco_ctx* ctx, int n, const void* frames, const void* labels,
                                    const void* eval, const void* eval_labels) {
   return guarded(ctx, [&] {

@@ -177,16 +177,28 @@ __global__ void k_l_sample_debug(LDims g, uint64_t seed, int job_id, int n_src,
 // thread owns 4 rows x 8 columns.
 
 constexpr int kRB = 64;   // rows per block
+
+// Which training rows are live in this SGD step: rows of job j are
+// [j*rows_per_job, (j+1)*rows_per_job); a job whose step budget is spent
+// (step >= steps[j]) is skipped.  steps == nullptr means always live.
+struct Gate {
+  const int* steps;
+  int step;
+  int rows_per_job;
+  __device__ __forceinline__ bool live_row(size_t r) const {
+    return steps == nullptr || step < steps[r / rows_per_job];
+  }
+};
 constexpr int kHB = 128;  // hidden columns per block
 constexpr int kKT = 32;   // k tile
 
 __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* xbase,
                                                        const int64_t* row_off,
-                                                       const int* blk_slot, const int* blk_on,
+                                                       const int* blk_slot, Gate gate,
                                                        const float* wbase, size_t n_params,
                                                        float* Z) {
   const int blk = blockIdx.x;
-  if (blk_on && !blk_on[blk]) return;
+  if (!gate.live_row((size_t)blk * kRB)) return;
   const int h0 = blockIdx.y * kHB;
   const float* W1 = wbase + (size_t)blk_slot[blk] * n_params;
   const float* b1 = W1 + (size_t)g.F * g.H;
@@ -244,13 +256,13 @@ __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* 
 
 // logits[row, c] = sum_k relu(Z[row,k]) * W2[k,c] (sequential k) + b2[c].
 __global__ void __launch_bounds__(256) k_l_logits(LDims g, int n_rows, const int* blk_slot,
-                                                  const int* blk_on, const float* wbase,
+                                                  Gate gate, const float* wbase,
                                                   size_t n_params, const float* Z, float* L) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)n_rows * g.C) return;
   const int r = (int)(idx / g.C), c = (int)(idx % g.C);
   const int blk = r / kRB;
-  if (blk_on && !blk_on[blk]) return;
+  if (!gate.live_row((size_t)blk * kRB)) return;
   const float* W = wbase + (size_t)blk_slot[blk] * n_params;
   const float* W2 = W + (size_t)g.F * g.H + g.H;
   const float* b2 = W2 + (size_t)g.H * g.C;
@@ -264,11 +276,11 @@ __global__ void __launch_bounds__(256) k_l_logits(LDims g, int n_rows, const int
 }
 
 // Softmax cross-entropy gradient of one training row.
-__global__ void k_l_softmax_grad(LDims g, int n_rows, const int* blk_on, const float* L,
+__global__ void k_l_softmax_grad(LDims g, int n_rows, Gate gate, const float* L,
                                  const int32_t* lab, float* DL, float* loss_rows) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
-  if (blk_on && !blk_on[r / kRB]) return;
+  if (!gate.live_row(r)) return;
   const float* l = L + (size_t)r * g.C;
   float m = l[0];
   for (int c = 1; c < g.C; ++c) m = l[c] > m ? l[c] : m;
@@ -285,14 +297,14 @@ __global__ void k_l_softmax_grad(LDims g, int n_rows, const int* blk_on, const f
 
 // dh[row, k] = Z > 0 ? sum_c DL[row,c] * W2[k,c] : 0 (pre-update W2).
 __global__ void __launch_bounds__(256) k_l_dh(LDims g, int n_rows, const int* blk_slot,
-                                              const int* blk_on, const float* wbase,
+                                              Gate gate, const float* wbase,
                                               size_t n_params, const float* Z, const float* DL,
                                               float* DH) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)n_rows * g.H) return;
   const int r = (int)(idx / g.H), k = (int)(idx % g.H);
   const int blk = r / kRB;
-  if (blk_on && !blk_on[blk]) return;
+  if (!gate.live_row((size_t)blk * kRB)) return;
   const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
   float a = 0.0f;
   if (Z[idx] > 0.0f)
@@ -417,12 +429,11 @@ __global__ void k_l_loss_mean(LDims g, int n_jobs, const int* slots, const int* 
 
 // Correct-prediction count of each (slot, camera) pair over the camera's S
 // eval frames; one warp per (pair, row), first-max argmax like the oracle.
-__global__ void k_l_count(LDims g, int n_pairs, const int* blk_on, const float* L,
+__global__ void k_l_count(LDims g, int n_pairs, const float* L,
                           const int32_t* eval_labels, const int* pair_cam, int* counts) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_pairs * g.S) return;
   const int p = r / g.S, s = r % g.S;
-  if (blk_on && !blk_on[r / kRB]) return;
   const float* l = L + (size_t)r * g.C;
   int best = 0;
   for (int c = 1; c < g.C; ++c)
@@ -566,12 +577,12 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
                                                              d_pair_cam + p0, row_off, blk_slot);
     ECCO_LAUNCHED(ctx);
     k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
-        g, ctx->d_eval, row_off, blk_slot, nullptr, ctx->d_w, ctx->n_params, Z);
+        g, ctx->d_eval, row_off, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z);
     ECCO_LAUNCHED(ctx);
     k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
-        g, rows, blk_slot, nullptr, ctx->d_w, ctx->n_params, Z, L);
+        g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L);
     ECCO_LAUNCHED(ctx);
-    k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, nullptr, L, ctx->d_eval_labels,
+    k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, L, ctx->d_eval_labels,
                                                          d_pair_cam + p0, d_counts + p0);
     ECCO_LAUNCHED(ctx);
   }
@@ -698,11 +709,10 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   // training scratch: rows = n_jobs * B
   const int rows = n_jobs * g.B;
   const int nb = rows / kRB;
-  DevBuf b_row, b_lab, b_slot, b_on, b_z, b_l, b_dl, b_dh, b_loss;
+  DevBuf b_row, b_lab, b_slot, b_z, b_l, b_dl, b_dh, b_loss;
   int64_t* row_off = (int64_t*)b_row.get(sizeof(int64_t) * rows);
   int32_t* row_lab = (int32_t*)b_lab.get(sizeof(int32_t) * rows);
   int* blk_slot = (int*)b_slot.get(sizeof(int) * nb);
-  int* blk_on = (int*)b_on.get(sizeof(int) * nb);
   float* Z = (float*)b_z.get(sizeof(float) * (size_t)rows * g.H);
   float* L = (float*)b_l.get(sizeof(float) * (size_t)rows * g.C);
   float* DL = (float*)b_dl.get(sizeof(float) * (size_t)rows * g.C);
@@ -712,7 +722,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   std::vector<int> slots(n_jobs);
   ECCO_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
-  std::vector<int> hb_slot(nb), hb_on(nb);
+  std::vector<int> hb_slot(nb);
   const int rb_per_job = g.B / kRB;
   for (int j = 0; j < n_jobs; ++j)
     for (int q = 0; q < rb_per_job; ++q) hb_slot[j * rb_per_job + q] = slots[j];
@@ -738,24 +748,22 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     float* wt = ctx->d_wspec + (size_t)(t - 1) * np;
     // the per-slot stride for kernels is spec_stride: pass n_params = spec_stride
     for (int step = 0; step < max_steps; ++step) {
-      for (int j = 0; j < n_jobs; ++j)
-        for (int q = 0; q < rb_per_job; ++q) hb_on[j * rb_per_job + q] = step < h_steps[j];
-      ECCO_CUDA(cudaMemcpyAsync(blk_on, hb_on.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, ctx->stream));
+      const Gate gate{d_steps, step, g.B};
       k_l_sample<<<nblk(rows, 256), 256, 0, ctx->stream>>>(
           g, ctx->cfg.seed, n_jobs, d_job_ids, d_steps, d_src_off, d_src_cam, d_src_frac,
           d_micro_base, window, t - 1, step, ctx->d_labels, row_off, row_lab);
       ECCO_LAUNCHED(ctx);
       k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
-          g, ctx->d_frames, row_off, blk_slot, blk_on, wt, spec_stride, Z);
+          g, ctx->d_frames, row_off, blk_slot, gate, wt, spec_stride, Z);
       ECCO_LAUNCHED(ctx);
       k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
-          g, rows, blk_slot, blk_on, wt, spec_stride, Z, L);
+          g, rows, blk_slot, gate, wt, spec_stride, Z, L);
       ECCO_LAUNCHED(ctx);
-      k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(g, rows, blk_on, L, row_lab, DL,
+      k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(g, rows, gate, L, row_lab, DL,
                                                                   loss_rows);
       ECCO_LAUNCHED(ctx);
       k_l_dh<<<nblk((size_t)rows * g.H, 256), 256, 0, ctx->stream>>>(
-          g, rows, blk_slot, blk_on, wt, spec_stride, Z, DL, DH);
+          g, rows, blk_slot, gate, wt, spec_stride, Z, DL, DH);
       ECCO_LAUNCHED(ctx);
       k_l_update2<<<nblk((size_t)n_jobs * (g.H * g.C + g.C), 256), 256, 0, ctx->stream>>>(
           g, n_jobs, d_slots, d_steps, step, wt, spec_stride, Z, DL);
@@ -789,7 +797,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     ECCO_LAUNCHED(ctx);
   }
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
-  b_row.release(); b_lab.release(); b_slot.release(); b_on.release(); b_z.release();
+  b_row.release(); b_lab.release(); b_slot.release(); b_z.release();
   b_l.release(); b_dl.release(); b_dh.release(); b_loss.release();
 }
 

@@ -1,0 +1,154 @@
+"""Parity of the learned backend with its CPU oracle (oracle/learned.py).
+
+FFMA_EXACT path: synthetic frames, labels, sampler indices, SGD weights,
+per-member accuracies, trajectories and eval matrices are bit-identical.
+TC_BF16 path: weights and losses within the stated bf16 tolerance, and the
+fraction of equal decisions is reported.
+"""
+import numpy as np
+import pytest
+
+import paper_2512_11727_b200 as ecco
+from oracle.learned import LearnedOracle
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(feat_dim=128, hidden_dim=128, num_classes=16, minibatch=64, ring_frames=96,
+             eval_samples=64, steps_per_gpu_s=0.5)
+
+
+def setup(n_cams=6, seed=0, math=ecco.FFMA_EXACT, **kw):
+    rng = np.random.default_rng(seed)
+    cfg = dict(SMALL)
+    cfg.update(kw)
+    ctx = ecco.Context(backend=ecco.LEARNED, max_cameras=64, max_jobs=32, max_depth=4, math=math,
+                       **cfg)
+    scenes = np.round(rng.random((n_cams, 2)), 1)
+    tp = np.full(n_cams, 8.192e6)
+    ctx.set_cameras(scenes, tp)
+    ctx.generate_frames(3)
+    orc = LearnedOracle(ctx.cfg, scenes, tp)
+    orc.generate(3)
+    return ctx, orc, rng
+
+
+def test_frames_and_labels_bit_exact():
+    ctx, orc, _ = setup()
+    fr, lb, ev, el = ctx.read_frames(6)
+    assert fr.tobytes() == orc.frames.tobytes()
+    assert lb.tobytes() == orc.labels.tobytes()
+    assert ev.tobytes() == orc.eval.tobytes()
+    assert el.tobytes() == orc.eval_labels.tobytes()
+
+
+def test_sampler_indices_bit_exact():
+    ctx, orc, rng = setup()
+    import ctypes as C
+    for trial in range(20):
+        k = int(rng.integers(1, 5))
+        src = np.sort(rng.choice(6, k, replace=False)).astype(np.int32)
+        f = rng.random(k) + 0.01
+        f = f / f.sum()
+        job, micro, step = int(rng.integers(0, 1000)), int(rng.integers(0, 50)), int(rng.integers(0, 9))
+        gc, gf = ctx.sample_indices(job, src, f, 3, micro, step)
+        wc, wf = np.zeros(64, np.int32), np.zeros(64, np.int32)
+        orc.L.orc_sample(orc.cp, job, k, src, f, 3, micro, step, wc, wf)
+        assert (gc == wc).all() and (gf == wf).all()
+
+
+def test_base_model_and_eval_pairs_bit_exact():
+    ctx, orc, _ = setup()
+    ctx.seed_models([5])
+    w = ctx.get_weights(5)
+    base = orc.base_weights()
+    for a, b in zip(w, base):
+        assert a.reshape(-1).tobytes() == b.tobytes()
+    got = ctx.eval_pairs([5] * 6, cams=np.arange(6))
+    want = np.array([orc.count(base, c) / orc.c.S for c in range(6)])
+    assert got.tobytes() == want.tobytes()
+
+
+def _jobs(rng, n_jobs, n_cams):
+    members, sources, fracs, batches = [], [], [], []
+    for j in range(n_jobs):
+        m = sorted(rng.choice(n_cams, rng.integers(1, 4), replace=False).tolist())
+        members.append(m)
+        s = sorted(set(m) | set(rng.choice(n_cams, rng.integers(0, 2), replace=False).tolist()))
+        f = rng.random(len(s)) + 0.1
+        fracs.append((f / f.sum()).tolist())
+        sources.append(s)
+        batches.append((float(rng.choice([5, 10, 15])), float(rng.choice([720, 960])), 1.0))
+    return members, sources, fracs, batches
+
+
+def test_trajectories_commit_and_weights_bit_exact():
+    ctx, orc, rng = setup(seed=1)
+    n_jobs, depth = 4, 3
+    ids = [11, 12, 13, 14]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members, sources, fracs, batches = _jobs(rng, n_jobs, 6)
+    mb = [0, 1, 2, 0]
+    got = ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, depth, micro_base=mb,
+                                 window=3)
+    want = orc.trajectories(ids, batches, sources, fracs, members, 6.0, depth, micro_base=mb)
+    assert got.tobytes() == want.tobytes()
+    granted = [0, 1, 3, 2]
+    ctx.commit(ids, granted)
+    orc.commit(ids, granted)
+    for j in ids:
+        for a, b in zip(ctx.get_weights(j), orc.models[j]):
+            assert a.reshape(-1).tobytes() == b.tobytes(), j
+    # the next chain starts from the committed models
+    got2 = ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, 1, window=3)
+    want2 = orc.trajectories(ids, batches, sources, fracs, members, 6.0, 1)
+    assert got2.tobytes() == want2.tobytes()
+    assert got.max() > got[:, 0].min()  # training moved the accuracies
+
+
+def test_eval_matrix_and_jobs_bit_exact():
+    ctx, orc, rng = setup(seed=2)
+    ids = [1, 2, 3]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members, sources, fracs, batches = _jobs(rng, 3, 6)
+    ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, 1, window=3)
+    orc.trajectories(ids, batches, sources, fracs, members, 6.0, 1)
+    ctx.commit(ids, [1, 1, 1])
+    orc.commit(ids, [1, 1, 1])
+    cams = np.arange(6)
+    M = ctx.eval_matrix(ids, cams=cams)
+    want = np.array([[orc.count(orc.models[j], c) / orc.c.S for j in ids] for c in cams])
+    assert M.tobytes() == want.tobytes()
+    mask = np.ones((6, 3), np.uint8)
+    mask[::2, 1] = 0
+    Mm = ctx.eval_matrix(ids, cams=cams, mask=mask)
+    assert np.isnan(Mm[mask == 0]).all() and Mm[mask == 1].tobytes() == want[mask == 1].tobytes()
+    ev = ctx.eval_jobs(ids, members)
+    assert ev.tobytes() == np.array([orc.evaluate(orc.models[j], m) for j, m in zip(ids, members)]).tobytes()
+    req = np.full(6, 0.0)
+    best, acc = ctx.route_propose(ids, req, cams=cams)
+    assert (best == np.argmax(want, axis=1)).all()
+
+
+def test_uploaded_frames_equal_generated():
+    ctx, orc, rng = setup(seed=4)
+    ctx.upload_frames(orc.frames, orc.labels, orc.eval, orc.eval_labels)
+    fr, lb, ev, el = ctx.read_frames(6)
+    assert fr.tobytes() == orc.frames.tobytes() and el.tobytes() == orc.eval_labels.tobytes()
+
+
+def test_learned_simulation_runs_and_groups():
+    from paper_2512_11727_b200 import scenarios
+    sc = scenarios.synthetic(24, 3, windows=2, micro_windows=8, drift_frac=0.1, local_acc=0.0, seed=3)
+    opts = dict(SMALL, steps_per_gpu_s=16.0)
+    sim = ecco.Simulation(sc, backend=ecco.LEARNED, **opts)
+    sim.run()
+    trace = sim.trace_csv()
+    assert trace.count("\nnew_job,0,") == 3  # one job per spatial cluster
+    assert sim.last_samples() > 0
+    import json
+    summ = json.loads(sim.summary_json())
+    assert summ["windows_run"] == 2

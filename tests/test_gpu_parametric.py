@@ -17,7 +17,7 @@ P = oracle.default_params()
 
 
 def make_ctx(**kw):
-    return ecco.Context(backend=ecco.PARAMETRIC, max_clusters=8, max_jobs=256, max_cameras=4096,
+    return ecco.Context(backend=ecco.PARAMETRIC, max_clusters=8, max_jobs=1024, max_cameras=4096,
                         max_depth=16, **kw)
 
 
@@ -167,6 +167,7 @@ def test_eval_jobs_is_trajectory_column_zero():
     n_cams = 32
     ctx.set_cameras(rng.random((n_cams, 2)), rng.uniform(2e6, 2e7, n_cams))
     ks, cl, pr, ce, clen = random_models(rng, 10)
+    ks[:] = np.minimum(ks, 2)
     ids = np.arange(10, dtype=np.int32)
     ctx.put_models(ids, ks, cl, pr, ce, clen)
     members, sources, fracs, batches = _traj_inputs(rng, 10, n_cams)
