@@ -54,7 +54,7 @@ typedef enum { ECCO_BACKEND_PARAMETRIC = 0, ECCO_BACKEND_LEARNED = 1 } ecco_back
 /* Arithmetic of the learned backend's dense contractions. */
 typedef enum {
   ECCO_MATH_FFMA_EXACT = 0, /* fp32 FFMA in the oracle's order: bit-exact   */
-  ECCO_MATH_TC_BF16 = 1     /* tcgen05 bf16 x bf16 -> fp32 TMEM: tolerance */
+  ECCO_MATH_TC_TF32 = 1     /* tcgen05 kind::tf32 -> fp32 TMEM: tolerance  */
 } ecco_math;
 
 /* ModelParams (proj/core/include/ecco/accuracy_model.hpp:18-24). */
@@ -98,6 +98,27 @@ void ecco_destroy(ecco_ctx* ctx);
 const char* ecco_last_error(const ecco_ctx* ctx);
 /* Number of kernels this context has launched (the bench's gpu_launches). */
 uint64_t ecco_kernel_launches(const ecco_ctx* ctx);
+/* Per-kernel device timing with CUDA events on the context stream (off by
+ * default).  ecco_kernel_stat returns, for one tracked kernel family, the
+ * launches, summed device milliseconds and the algorithmic flops and bytes of
+ * those launches (units in DESIGN.md). */
+typedef enum {
+  ECCO_KSTAT_TRAIN_FWD = 0,    /* learned: hidden layer of the SGD minibatch   */
+  ECCO_KSTAT_TRAIN_DW1 = 1,    /* learned: W1 gradient + SGD update            */
+  ECCO_KSTAT_TRAIN_HEAD = 2,   /* learned: logits/softmax/dh/W2 update         */
+  ECCO_KSTAT_EVAL_HIDDEN = 3,  /* learned: eval-matrix hidden layer            */
+  ECCO_KSTAT_EVAL_HEAD = 4,    /* learned: eval logits + correct counts        */
+  ECCO_KSTAT_P_EVAL = 5,       /* parametric eval matrix / pairs               */
+  ECCO_KSTAT_P_TRAJ = 6,       /* parametric trajectories                      */
+  ECCO_KSTAT_P_PROFILE = 7,    /* parametric profile tables                    */
+  ECCO_KSTAT_FRAMES = 8,       /* synthetic stream generation                  */
+  ECCO_KSTAT_COUNT = 9
+} ecco_kstat;
+ecco_status ecco_profile(ecco_ctx* ctx, int enable);
+ecco_status ecco_kernel_stat(ecco_ctx* ctx, int which, uint64_t* launches, double* ms,
+                             double* flops, double* bytes);
+/* Host<->device bytes this context has copied (the bench's e2e accounting). */
+ecco_status ecco_transfer_bytes(const ecco_ctx* ctx, uint64_t* h2d, uint64_t* d2h);
 /* cudaStream_t the context launches on (as void*). */
 void* ecco_stream(ecco_ctx* ctx);
 ecco_status ecco_synchronize(ecco_ctx* ctx);

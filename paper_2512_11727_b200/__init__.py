@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(HERE, "libecco_b200.so")
 
 OK, INVALID_ARGUMENT, LOGIC, INFEASIBLE, SCHEMA, CUDA, RUNTIME = range(7)
 PARAMETRIC, LEARNED = 0, 1
-FFMA_EXACT, TC_BF16 = 0, 1
+FFMA_EXACT, TC_TF32 = 0, 1
 
 
 class EccoError(RuntimeError):

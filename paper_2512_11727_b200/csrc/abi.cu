@@ -102,7 +102,7 @@ std::vector<int> slots_of(ecco_ctx* c, int n, const int* job_ids) {
 
 void ecco_ctx::check_device_status() {
   int st = 0;
-  ECCO_CUDA(cudaMemcpyAsync(&st, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  ECCO_CUDA(ctx_memcpy(this, &st, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream));
   ECCO_CUDA(cudaStreamSynchronize(stream));
   if (st) {
     ECCO_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int), stream));
@@ -156,7 +156,7 @@ ecco_status ecco_create(const ecco_config* cfg, ecco_ctx** out) {
       ECCO_REQUIRE(g.eval_samples % 64 == 0 && g.eval_samples > 0,
                    "eval_samples must be a multiple of 64");
       ECCO_REQUIRE(g.ring_frames > 0, "ring_frames must be positive");
-      ECCO_REQUIRE(g.math == ECCO_MATH_FFMA_EXACT || g.math == ECCO_MATH_TC_BF16, "unknown math");
+      ECCO_REQUIRE(g.math == ECCO_MATH_FFMA_EXACT || g.math == ECCO_MATH_TC_TF32, "unknown math");
     }
     ECCO_CUDA(cudaSetDevice(g.device));
     ECCO_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -217,6 +217,35 @@ uint64_t ecco_kernel_launches(const ecco_ctx* ctx) { return ctx ? ctx->launches 
 
 void* ecco_stream(ecco_ctx* ctx) { return (void*)ctx->stream; }
 
+ecco_status ecco_profile(ecco_ctx* ctx, int enable) {
+  return guarded(ctx, [&] {
+    ctx->fold_stats();
+    if (enable)
+      for (auto& k : ctx->kstats) k.launches = 0, k.ms = k.flops = k.bytes = 0.0;
+    ctx->profiling = enable != 0;
+  });
+}
+
+ecco_status ecco_kernel_stat(ecco_ctx* ctx, int which, uint64_t* launches, double* ms,
+                             double* flops, double* bytes) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(which >= 0 && which < ECCO_KSTAT_COUNT, "kernel_stat: unknown kernel family");
+    ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->fold_stats();
+    const KStat& k = ctx->kstats[which];
+    *launches = k.launches;
+    *ms = k.ms;
+    *flops = k.flops;
+    *bytes = k.bytes;
+  });
+}
+
+ecco_status ecco_transfer_bytes(const ecco_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
+  *h2d = ctx->h2d_bytes;
+  *d2h = ctx->d2h_bytes;
+  return ECCO_OK;
+}
+
 ecco_status ecco_synchronize(ecco_ctx* ctx) {
   return guarded(ctx, [&] { ECCO_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
@@ -229,8 +258,8 @@ ecco_status ecco_set_cameras(ecco_ctx* ctx, int n, const double* scenes, const d
     ctx->h_scenes.assign(scenes, scenes + (size_t)n * D);
     ctx->h_tp.assign(tp, tp + n);
     if (n == 0) return;
-    ECCO_CUDA(cudaMemcpyAsync(ctx->d_scenes, scenes, sizeof(double) * n * D, cudaMemcpyHostToDevice, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(ctx->d_tp, tp, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->d_scenes, scenes, sizeof(double) * n * D, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->d_tp, tp, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -242,7 +271,7 @@ ecco_status ecco_update_scenes(ecco_ctx* ctx, int n, const int* cam_idx, const d
     for (int i = 0; i < n; ++i) {
       std::copy(scenes + (size_t)i * D, scenes + (size_t)(i + 1) * D,
                 ctx->h_scenes.begin() + (size_t)cam_idx[i] * D);
-      ECCO_CUDA(cudaMemcpyAsync(ctx->d_scenes + (size_t)cam_idx[i] * D, scenes + (size_t)i * D,
+      ECCO_CUDA(ctx_memcpy(ctx, ctx->d_scenes + (size_t)cam_idx[i] * D, scenes + (size_t)i * D,
                                 sizeof(double) * D, cudaMemcpyHostToDevice, ctx->stream));
     }
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -263,10 +292,10 @@ static void upload_frames_impl(ecco_ctx* ctx, int n, const void* frames, const v
   ECCO_REQUIRE(n >= 0 && n <= ctx->n_cams, "upload_frames: camera count");
   const ecco_config& g = ctx->cfg;
   const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n * g.eval_samples;
-  ECCO_CUDA(cudaMemcpyAsync(ctx->d_frames, frames, fr * g.feat_dim * 2, kind, ctx->stream));
-  ECCO_CUDA(cudaMemcpyAsync(ctx->d_labels, labels, fr * 4, kind, ctx->stream));
-  ECCO_CUDA(cudaMemcpyAsync(ctx->d_eval, eval, ev * g.feat_dim * 2, kind, ctx->stream));
-  ECCO_CUDA(cudaMemcpyAsync(ctx->d_eval_labels, eval_labels, ev * 4, kind, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, ctx->d_frames, frames, fr * g.feat_dim * 2, kind, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, ctx->d_labels, labels, fr * 4, kind, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, ctx->d_eval, eval, ev * g.feat_dim * 2, kind, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, ctx->d_eval_labels, eval_labels, ev * 4, kind, ctx->stream));
 }
 
 ecco_status ecco_upload_frames(ecco_ctx* ctx, int n, const uint16_t* frames, const int32_t* labels,
@@ -285,10 +314,10 @@ ecco_status ecco_read_frames(ecco_ctx* ctx, int n, uint16_t* frames, int32_t* la
     const ecco_config& g = ctx->cfg;
     const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n * g.eval_samples;
     const cudaMemcpyKind k = cudaMemcpyDeviceToHost;
-    if (frames) ECCO_CUDA(cudaMemcpyAsync(frames, ctx->d_frames, fr * g.feat_dim * 2, k, ctx->stream));
-    if (labels) ECCO_CUDA(cudaMemcpyAsync(labels, ctx->d_labels, fr * 4, k, ctx->stream));
-    if (eval) ECCO_CUDA(cudaMemcpyAsync(eval, ctx->d_eval, ev * g.feat_dim * 2, k, ctx->stream));
-    if (eval_labels) ECCO_CUDA(cudaMemcpyAsync(eval_labels, ctx->d_eval_labels, ev * 4, k, ctx->stream));
+    if (frames) ECCO_CUDA(ctx_memcpy(ctx, frames, ctx->d_frames, fr * g.feat_dim * 2, k, ctx->stream));
+    if (labels) ECCO_CUDA(ctx_memcpy(ctx, labels, ctx->d_labels, fr * 4, k, ctx->stream));
+    if (eval) ECCO_CUDA(ctx_memcpy(ctx, eval, ctx->d_eval, ev * g.feat_dim * 2, k, ctx->stream));
+    if (eval_labels) ECCO_CUDA(ctx_memcpy(ctx, eval_labels, ctx->d_eval_labels, ev * 4, k, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -310,14 +339,14 @@ ecco_status ecco_put_models(ecco_ctx* ctx, int n, const int* job_ids, const int*
       ECCO_REQUIRE(n_clusters[i] >= 0 && n_clusters[i] <= K, "put_models: cluster count");
       ECCO_REQUIRE(centroid_len[i] == 0 || centroid_len[i] == D, "put_models: centroid length");
       const int s = ctx->alloc_slot(job_ids[i]);
-      ECCO_CUDA(cudaMemcpyAsync(ctx->d_cl + (size_t)s * K * D, clusters + (size_t)i * K * D,
+      ECCO_CUDA(ctx_memcpy(ctx, ctx->d_cl + (size_t)s * K * D, clusters + (size_t)i * K * D,
                                 sizeof(double) * K * D, cudaMemcpyHostToDevice, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(ctx->d_prof + (size_t)s * K, prof + (size_t)i * K, sizeof(double) * K,
+      ECCO_CUDA(ctx_memcpy(ctx, ctx->d_prof + (size_t)s * K, prof + (size_t)i * K, sizeof(double) * K,
                                 cudaMemcpyHostToDevice, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(ctx->d_cen + (size_t)s * D, centroid + (size_t)i * D, sizeof(double) * D,
+      ECCO_CUDA(ctx_memcpy(ctx, ctx->d_cen + (size_t)s * D, centroid + (size_t)i * D, sizeof(double) * D,
                                 cudaMemcpyHostToDevice, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(ctx->d_k + s, n_clusters + i, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(ctx->d_clen + s, centroid_len + i, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, ctx->d_k + s, n_clusters + i, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, ctx->d_clen + s, centroid_len + i, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     }
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
@@ -330,14 +359,14 @@ ecco_status ecco_get_models(ecco_ctx* ctx, int n, const int* job_ids, int* n_clu
     const int D = ctx->cfg.scene_dims, K = ctx->cfg.max_clusters;
     for (int i = 0; i < n; ++i) {
       const int s = ctx->slot(job_ids[i]);
-      ECCO_CUDA(cudaMemcpyAsync(clusters + (size_t)i * K * D, ctx->d_cl + (size_t)s * K * D,
+      ECCO_CUDA(ctx_memcpy(ctx, clusters + (size_t)i * K * D, ctx->d_cl + (size_t)s * K * D,
                                 sizeof(double) * K * D, cudaMemcpyDeviceToHost, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(prof + (size_t)i * K, ctx->d_prof + (size_t)s * K, sizeof(double) * K,
+      ECCO_CUDA(ctx_memcpy(ctx, prof + (size_t)i * K, ctx->d_prof + (size_t)s * K, sizeof(double) * K,
                                 cudaMemcpyDeviceToHost, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(centroid + (size_t)i * D, ctx->d_cen + (size_t)s * D, sizeof(double) * D,
+      ECCO_CUDA(ctx_memcpy(ctx, centroid + (size_t)i * D, ctx->d_cen + (size_t)s * D, sizeof(double) * D,
                                 cudaMemcpyDeviceToHost, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(n_clusters + i, ctx->d_k + s, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(centroid_len + i, ctx->d_clen + s, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, n_clusters + i, ctx->d_k + s, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, centroid_len + i, ctx->d_clen + s, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     }
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
@@ -379,10 +408,10 @@ ecco_status ecco_get_weights(ecco_ctx* ctx, int job_id, float* w1, float* b1, fl
     const ecco_config& g = ctx->cfg;
     const size_t F = g.feat_dim, H = g.hidden_dim, C = g.num_classes;
     const float* base = ctx->d_w + (size_t)ctx->slot(job_id) * ctx->n_params;
-    ECCO_CUDA(cudaMemcpyAsync(w1, base, F * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(b1, base + F * H, H * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(w2, base + F * H + H, H * C * 4, cudaMemcpyDeviceToHost, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(b2, base + F * H + H + H * C, C * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, w1, base, F * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, b1, base + F * H, H * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, w2, base + F * H + H, H * C * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, b2, base + F * H + H + H * C, C * 4, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -394,10 +423,10 @@ ecco_status ecco_set_weights(ecco_ctx* ctx, int job_id, const float* w1, const f
     const ecco_config& g = ctx->cfg;
     const size_t F = g.feat_dim, H = g.hidden_dim, C = g.num_classes;
     float* base = ctx->d_w + (size_t)ctx->alloc_slot(job_id) * ctx->n_params;
-    ECCO_CUDA(cudaMemcpyAsync(base, w1, F * H * 4, cudaMemcpyHostToDevice, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(base + F * H, b1, H * 4, cudaMemcpyHostToDevice, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(base + F * H + H, w2, H * C * 4, cudaMemcpyHostToDevice, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(base + F * H + H + H * C, b2, C * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, base, w1, F * H * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, base + F * H, b1, H * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, base + F * H + H, w2, H * C * 4, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, base + F * H + H + H * C, b2, C * 4, cudaMemcpyHostToDevice, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -422,17 +451,17 @@ ecco_status ecco_eval_jobs(ecco_ctx* ctx, int n_jobs, const int* job_ids, const 
       double* dout;
       DevBuf o;
       dout = (double*)o.get(sizeof(double) * n_jobs);
-      ECCO_CUDA(cudaMemcpyAsync(ds, d_s, sizeof(int) * n_jobs, cudaMemcpyDeviceToDevice, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(doff, d_off, sizeof(int) * (n_jobs + 1), cudaMemcpyDeviceToDevice, ctx->stream));
-      ECCO_CUDA(cudaMemcpyAsync(dmem, d_mem, sizeof(int) * std::max(mem_off[n_jobs], 1), cudaMemcpyDeviceToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, ds, d_s, sizeof(int) * n_jobs, cudaMemcpyDeviceToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, doff, d_off, sizeof(int) * (n_jobs + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, dmem, d_mem, sizeof(int) * std::max(mem_off[n_jobs], 1), cudaMemcpyDeviceToDevice, ctx->stream));
       lbackend::eval_jobs(ctx, n_jobs, ds, doff, dmem, dout);
-      ECCO_CUDA(cudaMemcpyAsync(out_mean, dout, sizeof(double) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, out_mean, dout, sizeof(double) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
       ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
       a.release(); b.release(); c2.release(); o.release();
       return;
     }
     pbackend::eval_jobs(ctx, n_jobs, d_s, d_off, d_mem, d_out);
-    ECCO_CUDA(cudaMemcpyAsync(out_mean, d_out, sizeof(double) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out_mean, d_out, sizeof(double) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -443,23 +472,23 @@ static void eval_matrix_impl(ecco_ctx* ctx, int n, const double* scenes, const i
   auto s = slots_of(ctx, g, job_ids);
   DevBuf bs, bp, bm;
   int* d_s = (int*)bs.get(sizeof(int) * g);
-  ECCO_CUDA(cudaMemcpyAsync(d_s, s.data(), sizeof(int) * g, cudaMemcpyHostToDevice, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, d_s, s.data(), sizeof(int) * g, cudaMemcpyHostToDevice, ctx->stream));
   uint8_t* d_m = nullptr;
   if (mask) {
     d_m = (uint8_t*)bm.get((size_t)n * g);
-    ECCO_CUDA(cudaMemcpyAsync(d_m, mask, (size_t)n * g, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_m, mask, (size_t)n * g, cudaMemcpyHostToDevice, ctx->stream));
   }
   if (learned(ctx)) {
     ECCO_REQUIRE(cam_idx != nullptr, "eval_matrix: learned backend needs cam_idx");
     check_cams(ctx, n, cam_idx, "eval_matrix");
     int* d_c = (int*)bp.get(sizeof(int) * n);
-    ECCO_CUDA(cudaMemcpyAsync(d_c, cam_idx, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_c, cam_idx, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
     lbackend::eval_matrix(ctx, n, d_c, g, d_s, d_m, d_out);
   } else {
     ECCO_REQUIRE(scenes != nullptr, "eval_matrix: parametric backend needs scenes");
     const int D = ctx->cfg.scene_dims;
     double* d_sc = (double*)bp.get(sizeof(double) * (size_t)n * D);
-    ECCO_CUDA(cudaMemcpyAsync(d_sc, scenes, sizeof(double) * n * D, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_sc, scenes, sizeof(double) * n * D, cudaMemcpyHostToDevice, ctx->stream));
     pbackend::eval_matrix(ctx, n, d_sc, g, d_s, d_m, d_out);
   }
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -492,12 +521,12 @@ ecco_status ecco_eval_pairs(ecco_ctx* ctx, int n, const double* scenes, const in
     auto s = slots_of(ctx, n, job_ids);
     DevBuf bs, bc, bsc, bo;
     int* d_s = (int*)bs.get(sizeof(int) * n);
-    ECCO_CUDA(cudaMemcpyAsync(d_s, s.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_s, s.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
     int* d_c = nullptr;
     if (cams) {
       check_cams(ctx, n, cams, "eval_pairs");
       d_c = (int*)bc.get(sizeof(int) * n);
-      ECCO_CUDA(cudaMemcpyAsync(d_c, cams, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, d_c, cams, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
     }
     double* d_out = (double*)bo.get(sizeof(double) * n);
     if (learned(ctx)) {
@@ -509,11 +538,11 @@ ecco_status ecco_eval_pairs(ecco_ctx* ctx, int n, const double* scenes, const in
       if (scenes) {
         const int D = ctx->cfg.scene_dims;
         d_sc = (double*)bsc.get(sizeof(double) * (size_t)n * D);
-        ECCO_CUDA(cudaMemcpyAsync(d_sc, scenes, sizeof(double) * (size_t)n * D, cudaMemcpyHostToDevice, ctx->stream));
+        ECCO_CUDA(ctx_memcpy(ctx, d_sc, scenes, sizeof(double) * (size_t)n * D, cudaMemcpyHostToDevice, ctx->stream));
       }
       pbackend::eval_pairs(ctx, n, d_sc, d_c, d_s, d_out);
     }
-    ECCO_CUDA(cudaMemcpyAsync(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
     bs.release(); bc.release(); bsc.release(); bo.release();
   });
@@ -539,29 +568,29 @@ ecco_status ecco_route_propose(ecco_ctx* ctx, int n, const double* scenes, const
     auto s = slots_of(ctx, g, job_ids);
     DevBuf bs, bp, bm, br, bo1, bo2;
     int* d_s = (int*)bs.get(sizeof(int) * std::max(g, 1));
-    if (g) ECCO_CUDA(cudaMemcpyAsync(d_s, s.data(), sizeof(int) * g, cudaMemcpyHostToDevice, ctx->stream));
+    if (g) ECCO_CUDA(ctx_memcpy(ctx, d_s, s.data(), sizeof(int) * g, cudaMemcpyHostToDevice, ctx->stream));
     uint8_t* d_m = nullptr;
     if (mask && g) {
       d_m = (uint8_t*)bm.get((size_t)n * g);
-      ECCO_CUDA(cudaMemcpyAsync(d_m, mask, (size_t)n * g, cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, d_m, mask, (size_t)n * g, cudaMemcpyHostToDevice, ctx->stream));
     }
     double* d_r = (double*)br.get(sizeof(double) * n);
-    ECCO_CUDA(cudaMemcpyAsync(d_r, req, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_r, req, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     int* d_b = (int*)bo1.get(sizeof(int) * n);
     double* d_a = (double*)bo2.get(sizeof(double) * n);
     if (learned(ctx)) {
       check_cams(ctx, n, cam_idx, "route_propose");
       int* d_c = (int*)bp.get(sizeof(int) * n);
-      ECCO_CUDA(cudaMemcpyAsync(d_c, cam_idx, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, d_c, cam_idx, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
       lbackend::route_propose(ctx, n, d_c, d_r, g, d_s, d_m, d_b, d_a);
     } else {
       const int D = ctx->cfg.scene_dims;
       double* d_sc = (double*)bp.get(sizeof(double) * (size_t)n * D);
-      ECCO_CUDA(cudaMemcpyAsync(d_sc, scenes, sizeof(double) * n * D, cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, d_sc, scenes, sizeof(double) * n * D, cudaMemcpyHostToDevice, ctx->stream));
       pbackend::route_propose(ctx, n, d_sc, d_r, g, d_s, d_m, d_b, d_a);
     }
-    ECCO_CUDA(cudaMemcpyAsync(best_col, d_b, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(best_acc, d_a, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, best_col, d_b, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, best_acc, d_a, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -585,7 +614,7 @@ ecco_status ecco_train_trajectories(ecco_ctx* ctx, int n_jobs, const int* job_id
     DevBuf b[9];
     auto up = [&](int i, const void* h, size_t bytes) {
       void* d = b[i].get(bytes);
-      ECCO_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
       return d;
     };
     int* d_s = (int*)up(0, s.data(), sizeof(int) * n_jobs);
@@ -616,7 +645,7 @@ ecco_status ecco_train_trajectories(ecco_ctx* ctx, int n_jobs, const int* job_id
       pbackend::trajectories(ctx, n_jobs, d_s, d_bt, d_so, d_sc, d_sf, d_mo, d_mc, gpu_s, depth, d_out);
       ctx->check_device_status();
     }
-    ECCO_CUDA(cudaMemcpyAsync(out_acc, d_out, sizeof(double) * n_jobs * (depth + 1), cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out_acc, d_out, sizeof(double) * n_jobs * (depth + 1), cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
     for (auto& x : b) x.release();
   });
@@ -631,8 +660,8 @@ ecco_status ecco_commit(ecco_ctx* ctx, int n_jobs, const int* job_ids, const int
     DevBuf a, b;
     int* d_s = (int*)a.get(sizeof(int) * n_jobs);
     int* d_g = (int*)b.get(sizeof(int) * n_jobs);
-    ECCO_CUDA(cudaMemcpyAsync(d_s, s.data(), sizeof(int) * n_jobs, cudaMemcpyHostToDevice, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(d_g, granted, sizeof(int) * n_jobs, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_s, s.data(), sizeof(int) * n_jobs, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_g, granted, sizeof(int) * n_jobs, cudaMemcpyHostToDevice, ctx->stream));
     if (learned(ctx))
       lbackend::commit(ctx, n_jobs, d_s, d_g);
     else
@@ -650,7 +679,7 @@ ecco_status ecco_last_losses(ecco_ctx* ctx, int n_jobs, const int* job_ids, int 
     const int T = ctx->cfg.max_depth;
     for (int j = 0; j < n_jobs; ++j) {
       const int s = ctx->slot(job_ids[j]);
-      ECCO_CUDA(cudaMemcpyAsync(out + (size_t)j * depth, ctx->d_losses + (size_t)s * T,
+      ECCO_CUDA(ctx_memcpy(ctx, out + (size_t)j * depth, ctx->d_losses + (size_t)s * T,
                                 sizeof(float) * depth, cudaMemcpyDeviceToHost, ctx->stream));
     }
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -669,11 +698,11 @@ ecco_status ecco_sample_indices(ecco_ctx* ctx, int job_id, int n_src, const int*
     const int B = ctx->cfg.minibatch;
     int* d_oc = (int*)c2.get(sizeof(int) * B);
     int* d_of = (int*)d.get(sizeof(int) * B);
-    ECCO_CUDA(cudaMemcpyAsync(d_c, src_cams, sizeof(int) * n_src, cudaMemcpyHostToDevice, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(d_f, src_fracs, sizeof(double) * n_src, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_c, src_cams, sizeof(int) * n_src, cudaMemcpyHostToDevice, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, d_f, src_fracs, sizeof(double) * n_src, cudaMemcpyHostToDevice, ctx->stream));
     lbackend::sample_indices(ctx, job_id, n_src, d_c, d_f, window, micro, step, d_oc, d_of);
-    ECCO_CUDA(cudaMemcpyAsync(out_cam, d_oc, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(out_frame, d_of, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out_cam, d_oc, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out_frame, d_of, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
     a.release(); b.release(); c2.release(); d.release();
   });
@@ -703,7 +732,7 @@ ecco_status ecco_profile_tables(ecco_ctx* ctx, int n_cams, const int* cam_idx, c
     DevBuf b[8];
     auto up = [&](int i, const void* h, size_t bytes) {
       void* d = b[i].get(bytes);
-      ECCO_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      ECCO_CUDA(ctx_memcpy(ctx, d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
       return d;
     };
     std::vector<int> bz(n_cams, 0);
@@ -719,9 +748,9 @@ ecco_status ecco_profile_tables(ecco_ctx* ctx, int n_cams, const int* cam_idx, c
     uint8_t* d_fe = (uint8_t*)b[7].get(rows);
     pbackend::profile(ctx, n_cams, d_c, d_b, n_levels, d_l, n_grid, d_gf, d_gq, window_s, tie_eps,
                       ref_rate_bps, bpp_ref, d_f, d_r, d_fe);
-    ECCO_CUDA(cudaMemcpyAsync(out_fps, d_f, sizeof(double) * rows, cudaMemcpyDeviceToHost, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(out_res, d_r, sizeof(double) * rows, cudaMemcpyDeviceToHost, ctx->stream));
-    ECCO_CUDA(cudaMemcpyAsync(out_feasible, d_fe, rows, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out_fps, d_f, sizeof(double) * rows, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out_res, d_r, sizeof(double) * rows, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, out_feasible, d_fe, rows, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int c = 0; c < n_cams; ++c)
       for (int l = 0; l < n_levels; ++l) out_budget[(size_t)c * n_levels + l] = lv[l];

@@ -75,11 +75,58 @@ struct HostBuf {
   }
 };
 
+inline cudaError_t ctx_memcpy(ecco_ctx* ctx, void* dst, const void* src, size_t bytes,
+                              cudaMemcpyKind kind, cudaStream_t s);
+
+// Per-kernel CUDA-event timing (enabled by ecco_profile): each tracked launch
+// is bracketed by two events on the context stream; durations are folded in
+// when the stats are read.  Algorithmic flops / bytes per launch are supplied
+// by the launch site ("units of work").
+struct KStat {
+  uint64_t launches = 0;
+  double ms = 0.0, flops = 0.0, bytes = 0.0;
+  struct Pending {
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<Pending> pending;
+};
+
 struct ecco_ctx {
   ecco_config cfg{};
   cudaStream_t stream = nullptr;
   std::string err;
   uint64_t launches = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
+  bool profiling = false;
+  KStat kstats[ECCO_KSTAT_COUNT];
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t take_event() {
+    if (event_pool.empty()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) ecco_throw(ECCO_ERR_CUDA, "cudaEventCreate");
+      return e;
+    }
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  void fold_stats() {
+    for (auto& k : kstats) {
+      for (auto& p : k.pending) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.b) == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+          k.ms += ms;
+          k.flops += p.flops;
+          k.bytes += p.bytes;
+          k.launches++;
+        }
+        event_pool.push_back(p.a);
+        event_pool.push_back(p.b);
+      }
+      k.pending.clear();
+    }
+  }
 
   // camera table (replicated on every rank)
   int n_cams = 0;
@@ -118,7 +165,7 @@ struct ecco_ctx {
   float* d_losses = nullptr;     // slots * max_depth
   int frames_window = -1;
 
-  DevBuf scratch[8];
+  DevBuf scratch[12];  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
   HostBuf hscratch[4];
 
   int slot(int job_id) const {
@@ -141,11 +188,33 @@ struct ecco_ctx {
   T* upload(int which, const T* h, size_t n) {
     if (n == 0) return nullptr;
     T* d = (T*)scratch[which].get(n * sizeof(T));
-    ECCO_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, stream));
+    ECCO_CUDA(ctx_memcpy(this, d, h, n * sizeof(T), cudaMemcpyHostToDevice, stream));
     return d;
   }
   void check_device_status();
 };
+
+// cudaMemcpyAsync that keeps the context's host<->device byte counters.
+inline cudaError_t ctx_memcpy(ecco_ctx* ctx, void* dst, const void* src, size_t bytes,
+                              cudaMemcpyKind kind, cudaStream_t s) {
+  if (kind == cudaMemcpyHostToDevice) ctx->h2d_bytes += bytes;
+  if (kind == cudaMemcpyDeviceToHost) ctx->d2h_bytes += bytes;
+  return cudaMemcpyAsync(dst, src, bytes, kind, s);
+}
+
+// Wraps a tracked launch statement with profiling events.
+#define ECCO_TIMED(ctx, id, fl, by, launch)                                 \
+  do {                                                                      \
+    if ((ctx)->profiling) {                                                 \
+      cudaEvent_t a_ = (ctx)->take_event(), b_ = (ctx)->take_event();       \
+      cudaEventRecord(a_, (ctx)->stream);                                   \
+      launch;                                                               \
+      cudaEventRecord(b_, (ctx)->stream);                                   \
+      (ctx)->kstats[id].pending.push_back({a_, b_, (double)(fl), (double)(by)}); \
+    } else {                                                                \
+      launch;                                                               \
+    }                                                                       \
+  } while (0)
 
 // Kernel launch bookkeeping (counts every launch for the bench's gpu_launches).
 #define ECCO_LAUNCHED(ctx)                                  \

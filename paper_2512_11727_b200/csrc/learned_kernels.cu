@@ -15,6 +15,7 @@
 
 #include "ctx.cuh"
 #include "learned_common.cuh"
+#include "tc_kernels.cuh"
 
 namespace {
 
@@ -576,11 +577,33 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
     k_l_pair_rows<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, d_pair_slot + p0,
                                                              d_pair_cam + p0, row_off, blk_slot);
     ECCO_LAUNCHED(ctx);
-    k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
-        g, ctx->d_eval, row_off, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z);
-    ECCO_LAUNCHED(ctx);
-    k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
-        g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L);
+    if (ctx->cfg.math == ECCO_MATH_TC_TF32) {
+      // tensor-core hidden layer: 128-row tiles that never straddle two
+      // models (tiles are cut at slot changes of the 64-row pair blocks)
+      std::vector<int> hslot(nb);
+      ECCO_CUDA(ctx_memcpy(ctx, hslot.data(), blk_slot, sizeof(int) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+      ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+      std::vector<TcTile> tiles;
+      for (int b = 0; b < nb;) {
+        const int take = (b + 1 < nb && hslot[b + 1] == hslot[b]) ? 2 : 1;
+        tiles.push_back({hslot[b], b * kRB, take * kRB, 0});
+        b += take;
+      }
+      TcTile* d_tiles = (TcTile*)ctx->scratch[8].get(sizeof(TcTile) * tiles.size());
+      ECCO_CUDA(ctx_memcpy(ctx, d_tiles, tiles.data(), sizeof(TcTile) * tiles.size(), cudaMemcpyHostToDevice, ctx->stream));
+      tc::fwd_hidden(ctx, ctx->d_eval, row_off, d_tiles, (int)tiles.size(), nullptr, 0, ctx->d_w,
+                     ctx->n_params, Z, (double)rows);
+    } else {
+      ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_HIDDEN, 2.0 * rows * g.F * g.H,
+                 (double)rows * g.F * 2 + (double)g.F * g.H * 4,
+                 (k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
+                     g, ctx->d_eval, row_off, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w,
+                     ctx->n_params, Z)));
+      ECCO_LAUNCHED(ctx);
+    }
+    ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_HEAD, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
+               (k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
+                   g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L)));
     ECCO_LAUNCHED(ctx);
     k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, L, ctx->d_eval_labels,
                                                          d_pair_cam + p0, d_counts + p0);
@@ -594,12 +617,12 @@ void eval_matrix(ecco_ctx* ctx, int n, const int* d_cams, int gj, const int* d_s
   // host-side pair list (mask applied on the host copy when given)
   const size_t total = (size_t)n * gj;
   std::vector<int> slots(gj), cams(n);
-  ECCO_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * gj, cudaMemcpyDeviceToHost, ctx->stream));
-  ECCO_CUDA(cudaMemcpyAsync(cams.data(), d_cams, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, slots.data(), d_slots, sizeof(int) * gj, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, cams.data(), d_cams, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
   std::vector<uint8_t> mask;
   if (d_mask) {
     mask.resize(total);
-    ECCO_CUDA(cudaMemcpyAsync(mask.data(), d_mask, total, cudaMemcpyDeviceToHost, ctx->stream));
+    ECCO_CUDA(ctx_memcpy(ctx, mask.data(), d_mask, total, cudaMemcpyDeviceToHost, ctx->stream));
   }
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   std::vector<int> ps, pc, po;
@@ -634,7 +657,7 @@ void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, dou
   std::vector<int> po(n);
   for (int i = 0; i < n; ++i) po[i] = i;
   int* d_po = (int*)idx.get(sizeof(int) * n);
-  ECCO_CUDA(cudaMemcpyAsync(d_po, po.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, d_po, po.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
   pair_counts(ctx, n, d_slots, d_cams, d_cnt);
   k_l_matrix_out<<<nblk(n, 256), 256, 0, ctx->stream>>>(dims(ctx), n, d_cnt, d_po, d_out);
   ECCO_LAUNCHED(ctx);
@@ -662,8 +685,8 @@ static void member_pairs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const in
                          const int* d_mem_cam, std::vector<int>& h_off, int** d_ps) {
   h_off.resize(n_jobs + 1);
   std::vector<int> slots(n_jobs);
-  ECCO_CUDA(cudaMemcpyAsync(h_off.data(), d_mem_off, sizeof(int) * (n_jobs + 1), cudaMemcpyDeviceToHost, ctx->stream));
-  ECCO_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, h_off.data(), d_mem_off, sizeof(int) * (n_jobs + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   std::vector<int> ps(h_off[n_jobs]);
   for (int j = 0; j < n_jobs; ++j)
@@ -720,15 +743,27 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   float* loss_rows = (float*)b_loss.get(sizeof(float) * rows);
   // spec chain buffer per slot: T snapshots; train in place in snapshot t-1
   std::vector<int> slots(n_jobs);
-  ECCO_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   std::vector<int> hb_slot(nb);
   const int rb_per_job = g.B / kRB;
   for (int j = 0; j < n_jobs; ++j)
     for (int q = 0; q < rb_per_job; ++q) hb_slot[j * rb_per_job + q] = slots[j];
-  ECCO_CUDA(cudaMemcpyAsync(blk_slot, hb_slot.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, ctx->stream));
+  ECCO_CUDA(ctx_memcpy(ctx, blk_slot, hb_slot.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, ctx->stream));
   // the spec snapshots use a virtual "slot" base: wspec + slot * T * np + (t-1) * np
   const size_t spec_stride = (size_t)T * np;
+  // tensor-core path: one 128-row tile (or the whole minibatch when B < 128)
+  // per job and 128 rows
+  const bool tc_math = ctx->cfg.math == ECCO_MATH_TC_TF32;
+  std::vector<TcTile> tiles;
+  TcTile* d_tiles = nullptr;
+  if (tc_math) {
+    ECCO_REQUIRE(g.F % 128 == 0 && g.B % 32 == 0, "tensor-core path needs F % 128 == 0, B % 32 == 0");
+    for (int j = 0; j < n_jobs; ++j)
+      for (int r = 0; r < g.B; r += 128) tiles.push_back({slots[j], j * g.B + r, std::min(128, g.B - r), j});
+    d_tiles = (TcTile*)ctx->scratch[9].get(sizeof(TcTile) * tiles.size());
+    ECCO_CUDA(ctx_memcpy(ctx, d_tiles, tiles.data(), sizeof(TcTile) * tiles.size(), cudaMemcpyHostToDevice, ctx->stream));
+  }
   // acc[:, 0] from the committed models
   if (n_mem) pair_counts(ctx, n_mem, d_ps, d_mem_cam, d_cnt);
   k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
@@ -749,28 +784,45 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     // the per-slot stride for kernels is spec_stride: pass n_params = spec_stride
     for (int step = 0; step < max_steps; ++step) {
       const Gate gate{d_steps, step, g.B};
+      int live = 0;
+      for (int j = 0; j < n_jobs; ++j) live += step < h_steps[j];
+      const double lrows = (double)live * g.B;
       k_l_sample<<<nblk(rows, 256), 256, 0, ctx->stream>>>(
           g, ctx->cfg.seed, n_jobs, d_job_ids, d_steps, d_src_off, d_src_cam, d_src_frac,
           d_micro_base, window, t - 1, step, ctx->d_labels, row_off, row_lab);
       ECCO_LAUNCHED(ctx);
-      k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
-          g, ctx->d_frames, row_off, blk_slot, gate, wt, spec_stride, Z);
+      if (tc_math) {
+        tc::fwd_hidden(ctx, ctx->d_frames, row_off, d_tiles, (int)tiles.size(), d_steps, step, wt,
+                       spec_stride, Z, lrows);
+      } else {
+        ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_FWD, 2.0 * lrows * g.F * g.H,
+                   lrows * g.F * 2 + (double)live * g.F * g.H * 4,
+                   (k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
+                       g, ctx->d_frames, row_off, blk_slot, gate, wt, spec_stride, Z)));
+        ECCO_LAUNCHED(ctx);
+      }
+      ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_HEAD, 8.0 * lrows * g.H * g.C, lrows * g.H * 12,
+                 ((k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
+                      g, rows, blk_slot, gate, wt, spec_stride, Z, L)),
+                  (k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(
+                      g, rows, gate, L, row_lab, DL, loss_rows)),
+                  (k_l_dh<<<nblk((size_t)rows * g.H, 256), 256, 0, ctx->stream>>>(
+                      g, rows, blk_slot, gate, wt, spec_stride, Z, DL, DH)),
+                  (k_l_update2<<<nblk((size_t)n_jobs * (g.H * g.C + g.C), 256), 256, 0,
+                                 ctx->stream>>>(g, n_jobs, d_slots, d_steps, step, wt,
+                                                spec_stride, Z, DL))));
+      ctx->launches += 3;
       ECCO_LAUNCHED(ctx);
-      k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
-          g, rows, blk_slot, gate, wt, spec_stride, Z, L);
-      ECCO_LAUNCHED(ctx);
-      k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(g, rows, gate, L, row_lab, DL,
-                                                                  loss_rows);
-      ECCO_LAUNCHED(ctx);
-      k_l_dh<<<nblk((size_t)rows * g.H, 256), 256, 0, ctx->stream>>>(
-          g, rows, blk_slot, gate, wt, spec_stride, Z, DL, DH);
-      ECCO_LAUNCHED(ctx);
-      k_l_update2<<<nblk((size_t)n_jobs * (g.H * g.C + g.C), 256), 256, 0, ctx->stream>>>(
-          g, n_jobs, d_slots, d_steps, step, wt, spec_stride, Z, DL);
-      ECCO_LAUNCHED(ctx);
-      k_l_update1_ffma<<<dim3(g.F / 64, g.H / kHB, n_jobs), 256, 0, ctx->stream>>>(
-          g, d_slots, d_steps, step, ctx->d_frames, row_off, wt, spec_stride, DH);
-      ECCO_LAUNCHED(ctx);
+      if (tc_math) {
+        tc::dw1_update(ctx, ctx->d_frames, row_off, d_slots, d_steps, step, n_jobs, wt, spec_stride,
+                       DH, live);
+      } else {
+        ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_DW1, 2.0 * lrows * g.F * g.H,
+                   (double)live * (g.B * g.F * 2.0 + g.B * g.H * 4.0 + 2.0 * g.F * g.H * 4),
+                   (k_l_update1_ffma<<<dim3(g.F / 64, g.H / kHB, n_jobs), 256, 0, ctx->stream>>>(
+                       g, d_slots, d_steps, step, ctx->d_frames, row_off, wt, spec_stride, DH)));
+        ECCO_LAUNCHED(ctx);
+      }
       k_l_update_b1<<<nblk((size_t)n_jobs * g.H, 256), 256, 0, ctx->stream>>>(
           g, n_jobs, d_slots, d_steps, step, wt, spec_stride, DH);
       ECCO_LAUNCHED(ctx);

@@ -1,2 +1,375 @@
-// Tensor-core (tcgen05) path of the learned backend -- see DESIGN.md.
+// Tensor-core path of the learned backend (ECCO_MATH_TC_TF32): the two dense
+// contractions of every SGD step and of the evaluation matrix run on the 5th
+// generation tensor cores (tcgen05.mma kind::tf32, fp32 accumulators in TMEM).
+//
+//   fwd   Z[rows, H]  = X[rows, F] . W1[F, H] + b1      (K = F)
+//   dW1   W1[F, H]   -= lr * X[B, F]^T . dH[B, H]       (K = B samples)
+//
+// One CTA owns a 128 x N_tile output tile (N_tile in {64, 128, 256}).  Four
+// warps stream 32-wide K chunks of both operands from HBM/L2 into shared
+// memory in the canonical no-swizzle UMMA layouts (X rows are a gather over
+// the sampled frames, so the loads are per-thread 16-byte vectors rather than
+// TMA boxes), double-buffered against the asynchronous MMAs; one thread issues
+// tcgen05.mma and commits to an mbarrier per stage; the epilogue drains TMEM
+// with tcgen05.ld (32 lanes x 32 columns per warp instruction) and fuses the
+// bias add (fwd) or the SGD update (dW1).
+//
+// Shared-memory layouts (fp32 elements, "core matrix" = 8 x 16 bytes):
+//   K-major  (fwd A = X rows):   off(r,k) = (r/8)*1024 + (k/4)*128 + (r%8)*16 + (k%4)*4
+//            LBO = 128 (next 4 k), SBO = 1024 (next 8 rows)
+//   MN-major (W1 / dH / dW1's X): off(n,k) = (n/4)*128 + (k/8)*(NT/4*128) + (k%8)*16 + (n%4)*4
+//            SBO = 128 (next 4 n), LBO = NT/4*128 (next 8 k)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
 #include "ctx.cuh"
+#include "tc_kernels.cuh"
+
+namespace {
+
+constexpr int kM = 128;   // UMMA M (rows of a tile)
+constexpr int kKC = 32;   // K elements per pipeline chunk (4 MMAs of K = 8)
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version 1 (sm100)
+  // base_offset 0, lbo_mode 0, layout_type 0 = SWIZZLE_NONE
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, majors, N, M.
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n, int a_mn_major, int b_mn_major) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn_major << 15) |
+         ((uint32_t)b_mn_major << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+
+// 32 lanes x 32 columns: thread t of warp w gets TMEM lane 32w+t, columns c..c+31.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float4 bf16x4_to_f32(uint2 p) {
+  return make_float4(__uint_as_float(p.x << 16), __uint_as_float(p.x & 0xFFFF0000u),
+                     __uint_as_float(p.y << 16), __uint_as_float(p.y & 0xFFFF0000u));
+}
+
+// --------------------------------------------------------------------------
+// fwd: one CTA per (row tile, N tile).  A = X rows (K-major, gathered bf16 ->
+// fp32), B = W1 columns n0..n0+NT (MN-major, fp32 rows of W1).
+struct FwdArgs {
+  const uint16_t* xbase;
+  const int64_t* row_off;  // element offset of each row's features
+  const TcTile* tiles;     // per row tile: slot, first row, valid rows, job
+  const int* steps;        // nullable gate: tile live iff step < steps[job]
+  int step;
+  const float* wbase;
+  size_t wstride;
+  float* Z;
+  int F, H, NT;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
+  const TcTile tile = a.tiles[blockIdx.x];
+  if (a.steps && a.step >= a.steps[tile.job]) return;
+  const int n0 = blockIdx.y * a.NT;
+  const int NT = a.NT;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  float* sA[2] = {(float*)smem, (float*)(smem + 16384)};
+  float* sB[2] = {(float*)(smem + 32768), (float*)(smem + 32768 + NT * kKC * 4)};
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ int64_t rows[kM];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid < kM) rows[tid] = tid < tile.nrows ? a.row_off[tile.row0 + tid] : -1;
+  if (warp == 0) tmem_alloc(&tmem_base, (uint32_t)NT);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const float* W1 = a.wbase + (size_t)tile.slot * a.wstride;
+  const int nk = a.F / kKC;
+  const uint32_t idesc = idesc_tf32(kM, NT, 0, 1);
+  const uint32_t lboB = (uint32_t)(NT / 4) * 128;
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc & 1;
+    if (kc >= 2) mbar_wait(&bar[s], ((kc - 2) >> 1) & 1);
+    const int k0 = kc * kKC;
+    // A: 128 rows x 32 k, one 4-element (8-byte bf16) group per item
+    for (int e = tid; e < kM * (kKC / 4); e += kThreads) {
+      const int r = e >> 3, c = e & 7;  // c: 4-k chunk
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rows[r] >= 0) v = bf16x4_to_f32(*reinterpret_cast<const uint2*>(a.xbase + rows[r] + k0 + c * 4));
+      *reinterpret_cast<float4*>((uint8_t*)sA[s] + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
+    }
+    // B: 32 k rows of W1 x NT columns, 16-byte vectors along n
+    for (int e = tid; e < kKC * (NT / 4); e += kThreads) {
+      const int k = e / (NT / 4), n4 = e % (NT / 4);
+      const float4 v = *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + k) * a.H + n0 + n4 * 4);
+      *reinterpret_cast<float4*>((uint8_t*)sB[s] + n4 * 128 + (k >> 3) * lboB + (k & 7) * 16) = v;
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t aaddr = smem_u32(sA[s]), baddr = smem_u32(sB[s]);
+#pragma unroll
+      for (int kk = 0; kk < kKC / 8; ++kk) {
+        const uint64_t da = smem_desc(aaddr + kk * 256, 128, 1024);
+        const uint64_t db = smem_desc(baddr + kk * lboB, lboB, 128);
+        mma_tf32(tmem, da, db, idesc, (kc | kk) ? 1u : 0u);
+      }
+      mma_commit(&bar[s]);
+    }
+  }
+  mbar_wait(&bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
+  tc_fence_after();
+  // epilogue: row = 32*warp + lane; z = acc + b1
+  const int r = warp * 32 + (tid & 31);
+  const float* b1 = W1 + (size_t)a.F * a.H;
+  for (int c0 = 0; c0 < NT; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    if (r < tile.nrows) {
+      float* zr = a.Z + (size_t)(tile.row0 + r) * a.H + n0 + c0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 o;
+        o.x = v[i] + b1[n0 + c0 + i];
+        o.y = v[i + 1] + b1[n0 + c0 + i + 1];
+        o.z = v[i + 2] + b1[n0 + c0 + i + 2];
+        o.w = v[i + 3] + b1[n0 + c0 + i + 3];
+        *reinterpret_cast<float4*>(zr + i) = o;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, (uint32_t)NT);
+}
+
+// --------------------------------------------------------------------------
+// dW1: one CTA per (job, F tile of 128, H tile of NT).  A = X^T (element
+// (f, s) = x[s][f], MN-major), B = dH (element (h, s), MN-major); K = B rows.
+struct Dw1Args {
+  const uint16_t* xbase;
+  const int64_t* row_off;  // rows of job j: [j*B, (j+1)*B)
+  const int* slots;
+  const int* steps;
+  int step;
+  float* wbase;
+  size_t wstride;
+  const float* DH;
+  int F, H, B, NT;
+  float lr;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
+  const int j = blockIdx.z;
+  if (a.step >= a.steps[j]) return;
+  const int f0 = blockIdx.x * kM, n0 = blockIdx.y * a.NT;
+  const int NT = a.NT;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  float* sA[2] = {(float*)smem, (float*)(smem + 16384)};
+  float* sB[2] = {(float*)(smem + 32768), (float*)(smem + 32768 + NT * kKC * 4)};
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tmem_alloc(&tmem_base, (uint32_t)NT);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const size_t r0 = (size_t)j * a.B;
+  const int nk = a.B / kKC;
+  const uint32_t idesc = idesc_tf32(kM, NT, 1, 1);
+  const uint32_t lboA = (uint32_t)(kM / 4) * 128, lboB = (uint32_t)(NT / 4) * 128;
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc & 1;
+    if (kc >= 2) mbar_wait(&bar[s], ((kc - 2) >> 1) & 1);
+    const int k0 = kc * kKC;
+    // A: 32 sample rows x 128 features (bf16 -> fp32), MN-major
+    for (int e = tid; e < kKC * (kM / 4); e += kThreads) {
+      const int k = e / (kM / 4), m4 = e % (kM / 4);
+      const float4 v = bf16x4_to_f32(
+          *reinterpret_cast<const uint2*>(a.xbase + a.row_off[r0 + k0 + k] + f0 + m4 * 4));
+      *reinterpret_cast<float4*>((uint8_t*)sA[s] + m4 * 128 + (k >> 3) * lboA + (k & 7) * 16) = v;
+    }
+    // B: 32 sample rows x NT hidden columns of dH, MN-major
+    for (int e = tid; e < kKC * (NT / 4); e += kThreads) {
+      const int k = e / (NT / 4), n4 = e % (NT / 4);
+      const float4 v = *reinterpret_cast<const float4*>(a.DH + (r0 + k0 + k) * a.H + n0 + n4 * 4);
+      *reinterpret_cast<float4*>((uint8_t*)sB[s] + n4 * 128 + (k >> 3) * lboB + (k & 7) * 16) = v;
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t aaddr = smem_u32(sA[s]), baddr = smem_u32(sB[s]);
+#pragma unroll
+      for (int kk = 0; kk < kKC / 8; ++kk) {
+        const uint64_t da = smem_desc(aaddr + kk * lboA, lboA, 128);
+        const uint64_t db = smem_desc(baddr + kk * lboB, lboB, 128);
+        mma_tf32(tmem, da, db, idesc, (kc | kk) ? 1u : 0u);
+      }
+      mma_commit(&bar[s]);
+    }
+  }
+  mbar_wait(&bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
+  tc_fence_after();
+  float* W1 = a.wbase + (size_t)a.slots[j] * a.wstride;
+  const int f = f0 + warp * 32 + (tid & 31);
+  for (int c0 = 0; c0 < NT; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    float* wr = W1 + (size_t)f * a.H + n0 + c0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 w = *reinterpret_cast<float4*>(wr + i);
+      w.x = fmaf(-a.lr, v[i], w.x);
+      w.y = fmaf(-a.lr, v[i + 1], w.y);
+      w.z = fmaf(-a.lr, v[i + 2], w.z);
+      w.w = fmaf(-a.lr, v[i + 3], w.w);
+      *reinterpret_cast<float4*>(wr + i) = w;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, (uint32_t)NT);
+}
+
+int pick_nt(int H, int ctas_per_nt1) {
+  // widest tile that still gives >= 148 CTAs, never below 64
+  int nt = std::min(H, 256);
+  while (nt > 64 && (long)ctas_per_nt1 * (H / nt) < 148) nt /= 2;
+  while (H % nt) nt /= 2;
+  return nt;
+}
+
+size_t smem_bytes(int NT) { return 32768 + 2 * (size_t)NT * kKC * 4; }
+
+}  // namespace
+
+namespace tc {
+
+void fwd_hidden(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, const TcTile* tiles,
+                int n_tiles, const int* steps, int step, const float* wbase, size_t wstride,
+                float* Z, double live_rows) {
+  if (n_tiles == 0) return;
+  const int F = ctx->cfg.feat_dim, H = ctx->cfg.hidden_dim;
+  const int NT = pick_nt(H, n_tiles);
+  FwdArgs a{xbase, row_off, tiles, steps, step, wbase, wstride, Z, F, H, NT};
+  const size_t sm = smem_bytes(NT);
+  static bool attr = false;
+  if (!attr) {
+    ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 + 2 * 256 * kKC * 4));
+    ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 + 2 * 256 * kKC * 4));
+    attr = true;
+  }
+  const int kind = steps ? ECCO_KSTAT_TRAIN_FWD : ECCO_KSTAT_EVAL_HIDDEN;
+  ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 4,
+             (k_tc_fwd<<<dim3(n_tiles, H / NT), kThreads, sm, ctx->stream>>>(a)));
+  ECCO_LAUNCHED(ctx);
+}
+
+void dw1_update(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, const int* slots,
+                const int* steps, int step, int n_jobs, float* wbase, size_t wstride,
+                const float* DH, int live_jobs) {
+  if (n_jobs == 0) return;
+  const int F = ctx->cfg.feat_dim, H = ctx->cfg.hidden_dim, B = ctx->cfg.minibatch;
+  const int NT = pick_nt(H, n_jobs * (F / kM));
+  Dw1Args a{xbase, row_off, slots, steps, step, wbase, wstride, DH, F, H, B, NT, ctx->cfg.sgd_lr};
+  const size_t sm = smem_bytes(NT);
+  ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_DW1, 2.0 * live_jobs * F * H * B,
+             (double)live_jobs * (B * F * 2.0 + B * H * 4.0 + 2.0 * F * H * 4),
+             (k_tc_dw1<<<dim3(F / kM, H / NT, n_jobs), kThreads, sm, ctx->stream>>>(a)));
+  ECCO_LAUNCHED(ctx);
+}
+
+}  // namespace tc

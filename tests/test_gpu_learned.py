@@ -152,3 +152,49 @@ def test_learned_simulation_runs_and_groups():
     import json
     summ = json.loads(sim.summary_json())
     assert summ["windows_run"] == 2
+
+
+# ---------------------------------------------------------------- TC_TF32 --
+# Tolerance of the tensor-core path: X is exact in tf32 (bf16 frames), W1 and
+# dH are rounded to tf32 (10-bit mantissa) inside the two contractions, so one
+# SGD step's weight change matches the fp32 oracle to ~2^-11 relative; we
+# require 1e-2 of the largest update (a layout or descriptor error is O(1)).
+TC_TOL = 1e-2
+
+
+def test_tc_single_step_weights_within_tolerance():
+    ctx, orc, rng = setup(seed=5, math=ecco.TC_TF32)
+    ids = [1, 2, 3, 4, 5]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members, sources, fracs, batches = _jobs(rng, len(ids), 6)
+    ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, 1, window=3)
+    orc.trajectories(ids, batches, sources, fracs, members, 6.0, 1)
+    ctx.commit(ids, [1] * len(ids))
+    orc.commit(ids, [1] * len(ids))
+    base = orc.base_weights()
+    for j in ids:
+        for got, want, b0 in zip(ctx.get_weights(j), orc.models[j], base):
+            upd = np.abs(want - b0).max()
+            err = np.abs(got.reshape(-1) - want).max()
+            assert err <= TC_TOL * max(upd, 1e-6), (j, err, upd)
+
+
+def test_tc_eval_counts_close_and_decisions_reported():
+    ctx, orc, rng = setup(seed=6, math=ecco.TC_TF32)
+    ids = [1, 2, 3]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members, sources, fracs, batches = _jobs(rng, 3, 6)
+    got = ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, 3, window=3)
+    want = orc.trajectories(ids, batches, sources, fracs, members, 6.0, 3)
+    # accuracies are counts/64 per member: allow a few flipped argmaxes
+    assert np.abs(got - want).max() <= 4.0 / 64
+    M = ctx.eval_matrix(ids, cams=np.arange(6))
+    ctx.commit(ids, [3, 3, 3])
+    orc.commit(ids, [3, 3, 3])
+    M = ctx.eval_matrix(ids, cams=np.arange(6))
+    W = np.array([[orc.count(orc.models[j], c) / 64 for j in ids] for c in range(6)])
+    assert np.abs(M - W).max() <= 4.0 / 64
