@@ -93,7 +93,7 @@ _lib = None
 # Every symbol include/ecco_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "ecco_default_config", "ecco_create", "ecco_destroy", "ecco_last_error",
-    "ecco_kernel_launches", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
+    "ecco_kernel_launches", "ecco_profile", "ecco_kernel_stat", "ecco_transfer_bytes", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
     "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
     "ecco_read_frames",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",

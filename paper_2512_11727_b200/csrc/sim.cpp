@@ -43,6 +43,10 @@ namespace {
 
 using nlohmann::json;
 
+// AIMD share of a learned job whose estimate_shares share is 0 (see the
+// set_aimd_params call in step_window).
+constexpr double kLearnedShareFloor = 1e-3;
+
 struct SimError {
   ecco_status code;
   std::string msg;
@@ -999,7 +1003,18 @@ struct ecco_sim {
           if (cfg.equal_bw) {
             fa.push_back(cfg.alpha_unit);
           } else {
-            // set_aimd_params, transmission.cpp:140-149
+            // set_aimd_params, transmission.cpp:140-149.  The parametric
+            // model's gains are always > 0, so p_share > 0 there; a learned
+            // job whose retrain did not raise its eval accuracy gets p = 0
+            // from estimate_shares (gpu_allocator.cpp:93-95), which the
+            // reference would reject.  The learned backend keeps such a
+            // job's flow alive at a floor share ("deviations").
+            if (learned() && !(p[k] > 0.0)) {
+              fa.push_back(kLearnedShareFloor / nm * cfg.alpha_unit);
+              fb.push_back(0.5);
+              flow_cam.push_back(m.cam);
+              continue;
+            }
             if (!(p[k] > 0.0) || p[k] > 1.0 + 1e-9)
               fail(ECCO_ERR_INVALID_ARGUMENT, "set_aimd_params: p_share must be in (0,1]");
             fa.push_back(p[k] / nm * cfg.alpha_unit);
