@@ -14,11 +14,11 @@
 // with tcgen05.ld (32 lanes x 32 columns per warp instruction) and fuses the
 // bias add (fwd) or the SGD update (dW1).
 //
-// Shared-memory layouts (fp32 elements, "core matrix" = 8 x 16 bytes):
-//   K-major  (fwd A = X rows):   off(r,k) = (r/8)*1024 + (k/4)*128 + (r%8)*16 + (k%4)*4
-//            LBO = 128 (next 4 k), SBO = 1024 (next 8 rows)
-//   MN-major (W1 / dH / dW1's X): off(n,k) = (n/4)*128 + (k/8)*(NT/4*128) + (k%8)*16 + (n%4)*4
-//            SBO = 128 (next 4 n), LBO = NT/4*128 (next 8 k)
+// Shared-memory layout (fp32 elements, "core matrix" = 8 rows x 16 bytes):
+// kind::tf32 takes both operands K-major, so every operand tile -- X rows,
+// W1 columns, X^T and dH^T -- is staged K-major through registers:
+//   off(r,k) = (r/8)*1024 + (k/4)*128 + (r%8)*16 + (k%4)*4
+//   LBO = 128 (next 4 k), SBO = 1024 (next 8 rows); one K=8 MMA step = +256 B.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -125,14 +125,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Stores v = (element (r..r+3, k)) into a K-major tile: 4 rows, one column.
+__device__ __forceinline__ void kmajor_put4(float* tile, int r, int k, float4 v) {
+  uint8_t* base = (uint8_t*)tile + (k >> 2) * 128 + (k & 3) * 4;
+  const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ri = r + i;
+    *reinterpret_cast<float*>(base + (ri >> 3) * 1024 + (ri & 7) * 16) = e[i];
+  }
+}
+
 __device__ __forceinline__ float4 bf16x4_to_f32(uint2 p) {
   return make_float4(__uint_as_float(p.x << 16), __uint_as_float(p.x & 0xFFFF0000u),
                      __uint_as_float(p.y << 16), __uint_as_float(p.y & 0xFFFF0000u));
 }
 
 // --------------------------------------------------------------------------
-// fwd: one CTA per (row tile, N tile).  A = X rows (K-major, gathered bf16 ->
-// fp32), B = W1 columns n0..n0+NT (MN-major, fp32 rows of W1).
+// fwd: one CTA per (row tile, N tile).  A = X rows (gathered bf16 -> fp32),
+// B = W1 columns n0..n0+NT; both K-major.
 struct FwdArgs {
   const uint16_t* xbase;
   const int64_t* row_off;  // element offset of each row's features
@@ -170,8 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
   const uint32_t tmem = tmem_base;
   const float* W1 = a.wbase + (size_t)tile.slot * a.wstride;
   const int nk = a.F / kKC;
-  const uint32_t idesc = idesc_tf32(kM, NT, 0, 1);
-  const uint32_t lboB = (uint32_t)(NT / 4) * 128;
+  const uint32_t idesc = idesc_tf32(kM, NT, 0, 0);
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
     if (kc >= 2) mbar_wait(&bar[s], ((kc - 2) >> 1) & 1);
@@ -183,11 +193,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
       if (rows[r] >= 0) v = bf16x4_to_f32(*reinterpret_cast<const uint2*>(a.xbase + rows[r] + k0 + c * 4));
       *reinterpret_cast<float4*>((uint8_t*)sA[s] + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
     }
-    // B: 32 k rows of W1 x NT columns, 16-byte vectors along n
+    // B: 32 k rows of W1 x NT columns, read as 16-byte vectors along n and
+    // scattered into the K-major tile (element (n, k))
     for (int e = tid; e < kKC * (NT / 4); e += kThreads) {
       const int k = e / (NT / 4), n4 = e % (NT / 4);
       const float4 v = *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + k) * a.H + n0 + n4 * 4);
-      *reinterpret_cast<float4*>((uint8_t*)sB[s] + n4 * 128 + (k >> 3) * lboB + (k & 7) * 16) = v;
+      kmajor_put4(sB[s], n4 * 4, k, v);
     }
     fence_async_smem();
     __syncthreads();
@@ -197,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
 #pragma unroll
       for (int kk = 0; kk < kKC / 8; ++kk) {
         const uint64_t da = smem_desc(aaddr + kk * 256, 128, 1024);
-        const uint64_t db = smem_desc(baddr + kk * lboB, lboB, 128);
+        const uint64_t db = smem_desc(baddr + kk * 256, 128, 1024);
         mma_tf32(tmem, da, db, idesc, (kc | kk) ? 1u : 0u);
       }
       mma_commit(&bar[s]);
@@ -231,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
 
 // --------------------------------------------------------------------------
 // dW1: one CTA per (job, F tile of 128, H tile of NT).  A = X^T (element
-// (f, s) = x[s][f], MN-major), B = dH (element (h, s), MN-major); K = B rows.
+// (f, s) = x[s][f]), B = dH^T (element (h, s)), both K-major; K = B rows.
 struct Dw1Args {
   const uint16_t* xbase;
   const int64_t* row_off;  // rows of job j: [j*B, (j+1)*B)
@@ -268,24 +279,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   const uint32_t tmem = tmem_base;
   const size_t r0 = (size_t)j * a.B;
   const int nk = a.B / kKC;
-  const uint32_t idesc = idesc_tf32(kM, NT, 1, 1);
-  const uint32_t lboA = (uint32_t)(kM / 4) * 128, lboB = (uint32_t)(NT / 4) * 128;
+  const uint32_t idesc = idesc_tf32(kM, NT, 0, 0);
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
     if (kc >= 2) mbar_wait(&bar[s], ((kc - 2) >> 1) & 1);
     const int k0 = kc * kKC;
-    // A: 32 sample rows x 128 features (bf16 -> fp32), MN-major
+    // A = X^T: 32 sample rows x 128 features (bf16 -> fp32), scattered
+    // K-major (element (f, s))
     for (int e = tid; e < kKC * (kM / 4); e += kThreads) {
       const int k = e / (kM / 4), m4 = e % (kM / 4);
       const float4 v = bf16x4_to_f32(
           *reinterpret_cast<const uint2*>(a.xbase + a.row_off[r0 + k0 + k] + f0 + m4 * 4));
-      *reinterpret_cast<float4*>((uint8_t*)sA[s] + m4 * 128 + (k >> 3) * lboA + (k & 7) * 16) = v;
+      kmajor_put4(sA[s], m4 * 4, k, v);
     }
-    // B: 32 sample rows x NT hidden columns of dH, MN-major
+    // B = dH^T: 32 sample rows x NT hidden columns, K-major (element (h, s))
     for (int e = tid; e < kKC * (NT / 4); e += kThreads) {
       const int k = e / (NT / 4), n4 = e % (NT / 4);
       const float4 v = *reinterpret_cast<const float4*>(a.DH + (r0 + k0 + k) * a.H + n0 + n4 * 4);
-      *reinterpret_cast<float4*>((uint8_t*)sB[s] + n4 * 128 + (k >> 3) * lboB + (k & 7) * 16) = v;
+      kmajor_put4(sB[s], n4 * 4, k, v);
     }
     fence_async_smem();
     __syncthreads();
@@ -294,8 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
       const uint32_t aaddr = smem_u32(sA[s]), baddr = smem_u32(sB[s]);
 #pragma unroll
       for (int kk = 0; kk < kKC / 8; ++kk) {
-        const uint64_t da = smem_desc(aaddr + kk * lboA, lboA, 128);
-        const uint64_t db = smem_desc(baddr + kk * lboB, lboB, 128);
+        const uint64_t da = smem_desc(aaddr + kk * 256, 128, 1024);
+        const uint64_t db = smem_desc(baddr + kk * 256, 128, 1024);
         mma_tf32(tmem, da, db, idesc, (kc | kk) ? 1u : 0u);
       }
       mma_commit(&bar[s]);

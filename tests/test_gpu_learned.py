@@ -155,30 +155,94 @@ def test_learned_simulation_runs_and_groups():
 
 
 # ---------------------------------------------------------------- TC_TF32 --
-# Tolerance of the tensor-core path: X is exact in tf32 (bf16 frames), W1 and
-# dH are rounded to tf32 (10-bit mantissa) inside the two contractions, so one
-# SGD step's weight change matches the fp32 oracle to ~2^-11 relative; we
-# require 1e-2 of the largest update (a layout or descriptor error is O(1)).
-TC_TOL = 1e-2
+# Tolerance of the tensor-core path.  tcgen05 kind::tf32 reads the top 19
+# bits of each fp32 operand (truncation to a 10-bit mantissa).  X is exact
+# (bf16 frames); W1 in the forward contraction and X^T, dH in the W1-gradient
+# contraction are truncated.  Two checks:
+#  * against a float64 restatement of the SGD step that applies exactly that
+#    truncation (_step_tf32 below): agreement to 1e-3 of the update proves
+#    the layouts, descriptors and epilogues (measured: 2e-5);
+#  * against the fp32 oracle: the truncated W1 perturbs Z and therefore the
+#    ReLU mask and dH, which moves one step's W1 update by up to ~7% of its
+#    size (measured 6.7% for W1, 5.0% for b1, 4e-4 for the head), so the
+#    documented tolerance is 1e-1 of the update for one step and 1.5e-1 for
+#    a 3-step chain.
+TC_TOL_EMULATED = 1e-3
+TC_TOL_ONE_STEP = 1e-1
+TC_TOL_CHAIN = 1.5e-1
 
 
-def test_tc_single_step_weights_within_tolerance():
+def _tf32(a):
+    a = np.asarray(a, np.float32).copy()
+    a.view(np.uint32)[...] &= np.uint32(0xFFFFE000)
+    return a.astype(np.float64)
+
+
+def _step_tf32(x, y, w, lr):
+    """One SGD step (orc_sgd_step's math) in float64 with the MMA operands
+    truncated to tf32 as the tensor cores read them."""
+    w1, b1, w2, b2 = [np.asarray(t, np.float64) for t in w]
+    B, F = x.shape
+    H, Cc = b1.size, b2.size
+    W1, W2 = w1.reshape(F, H), w2.reshape(H, Cc)
+    X = x.astype(np.float64)
+    Z = X @ _tf32(W1) + b1
+    R = np.maximum(Z, 0)
+    L = R @ W2 + b2
+    P = np.exp(L - L.max(1, keepdims=True))
+    P /= P.sum(1, keepdims=True)
+    P[np.arange(B), y] -= 1
+    DL = P / B
+    DH = (DL @ W2.T) * (Z > 0)
+    return [W1 - lr * (_tf32(X).T @ _tf32(DH)), b1 - lr * DH.sum(0), W2 - lr * (R.T @ DL),
+            b2 - lr * DL.sum(0)]
+
+
+def _tc_weights_error(steps_one):
     ctx, orc, rng = setup(seed=5, math=ecco.TC_TF32)
     ids = [1, 2, 3, 4, 5]
     ctx.seed_models(ids)
     for j in ids:
         orc.seed(j)
     members, sources, fracs, batches = _jobs(rng, len(ids), 6)
-    ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, 1, window=3)
-    orc.trajectories(ids, batches, sources, fracs, members, 6.0, 1)
+    gpu_s = 6.0
+    if steps_one:
+        # fps 5 at 720p -> sufficiency 0.5625, effort 2.25 -> floor(2.25 * 0.5) = 1 step
+        batches = [(5.0, 720.0, 1.0)] * len(ids)
+        gpu_s = 4.0
+    ctx.train_trajectories(ids, batches, sources, fracs, members, gpu_s, 1, window=3)
+    orc.trajectories(ids, batches, sources, fracs, members, gpu_s, 1)
     ctx.commit(ids, [1] * len(ids))
     orc.commit(ids, [1] * len(ids))
     base = orc.base_weights()
-    for j in ids:
-        for got, want, b0 in zip(ctx.get_weights(j), orc.models[j], base):
+    worst, worst_emul = 0.0, 0.0
+    B, F = orc.c.B, orc.c.F
+    for j, jid in enumerate(ids):
+        got = [g.reshape(-1) for g in ctx.get_weights(jid)]
+        emul = None
+        if steps_one:
+            cams, frames = np.zeros(B, np.int32), np.zeros(B, np.int32)
+            orc.L.orc_sample(orc.cp, jid, len(sources[j]), np.array(sources[j], np.int32),
+                             np.array(fracs[j]), 3, 0, 0, cams, frames)
+            x = (orc.frames[cams, frames].astype(np.uint32) << 16).view(np.float32)
+            emul = _step_tf32(x, orc.labels[cams, frames], base, orc.c.lr)
+        for k, (g, want, b0) in enumerate(zip(got, orc.models[jid], base)):
             upd = np.abs(want - b0).max()
-            err = np.abs(got.reshape(-1) - want).max()
-            assert err <= TC_TOL * max(upd, 1e-6), (j, err, upd)
+            assert upd > 0
+            worst = max(worst, float(np.abs(g - want).max() / upd))
+            if emul is not None:
+                worst_emul = max(worst_emul, float(np.abs(g - emul[k].reshape(-1)).max() / upd))
+    return worst, worst_emul
+
+
+def test_tc_single_step_weights_within_tolerance():
+    vs_oracle, vs_emulated = _tc_weights_error(True)
+    assert vs_emulated <= TC_TOL_EMULATED
+    assert vs_oracle <= TC_TOL_ONE_STEP
+
+
+def test_tc_chain_weights_within_tolerance():
+    assert _tc_weights_error(False)[0] <= TC_TOL_CHAIN
 
 
 def test_tc_eval_counts_close_and_decisions_reported():
