@@ -1,0 +1,505 @@
+"""Benchmark of the B200 group-retraining path (BASELINE.json `metric`).
+
+One step = one retraining window of the hot path over the workload's
+synthetic camera streams ("Measurement"):
+
+  regroup   the camera x group evaluation matrix -- every camera's S labelled
+            eval frames scored under every group model (ecco_eval_matrix_dev,
+            the ModelEvalFn batch of grouping.cpp:33) -- all-gathered across
+            ranks, then the warp-reduced argmax/threshold per camera
+            (ecco_route_matrix_dev, group_request's join rule);
+  retrain   every group's speculative micro-window chain: evaluate, then
+            DEPTH x (STEPS SGD steps of B sampled frames, evaluate)
+            (ecco_train_trajectories, the allocator's TrainingBackend probes of
+            gpu_allocator.cpp:125-135), then ecco_commit of the granted chain.
+
+value = retrain samples of all ranks / max-over-ranks device time of the
+whole step (regroup included), in samples/s.  Groups are sharded across ranks
+(contiguous blocks); cameras are replicated (their frames are generated per
+rank from the counter RNG).  The only collective is the all-gather of the
+evaluation-matrix column blocks.  `e2e` is the same step through the public
+API with the window's frames uploaded from pinned host memory and the
+assignments / accuracies read back, every step.
+
+`--impl reference` times the CPU restatement of the same path (oracle/, the
+reference itself has no learned trainer: SURVEY.md 0) on this box's cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+# BASELINE.json configs -> (cameras, groups)
+CONFIGS = {
+    "c2": (100, 10),
+    "c3": (1000, 50),
+    "c4": (10000, 500),
+}
+DIMS = dict(feat_dim=512, hidden_dim=256, num_classes=16, minibatch=128, ring_frames=512,
+            eval_samples=64)
+DEPTH = 2             # micro-windows granted per group per window (initial pass + 1 greedy)
+STEPS = 16            # SGD steps per micro-window
+GPU_S = 1.0           # GPU-seconds per micro-window; steps = floor(GPU_S * STEPS)
+BATCH = (30.0, 1080.0, 1.0)  # delivered fps, resolution, quality: sufficiency 1
+THROUGHPUT = 8.192e6  # CameraState.gpu_pixel_throughput default
+
+
+def flops_per_sample(F, H, C):
+    """fwd + bwd of the F->H->C MLP per training sample."""
+    return 4.0 * F * H + 6.0 * H * C
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload --
+
+class Workload:
+    """Cameras, groups and the rank's shard (groups in contiguous blocks)."""
+
+    def __init__(self, config, rank, world):
+        self.config = config
+        self.N, self.G = CONFIGS[config]
+        self.per = self.N // self.G
+        self.rank, self.world = rank, world
+        self.gb = -(-self.G // world)  # column block per rank (last may be partial)
+        lo, hi = rank * self.gb, min(self.G, (rank + 1) * self.gb)
+        self.local = list(range(lo, hi))
+        side = 10
+        self.scenes = np.array([[0.1 * ((c // self.per) % side), 0.1 * ((c // self.per // side) % side)]
+                                for c in range(self.N)], np.float64)
+        self.tp = np.full(self.N, THROUGHPUT)
+
+    def members(self, g):
+        return list(range(g * self.per, (g + 1) * self.per))
+
+    def samples_per_step_local(self):
+        return len(self.local) * DEPTH * int(GPU_S * STEPS) * DIMS["minibatch"]
+
+
+# ----------------------------------------------------------------- B200 arm --
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import paper_2512_11727_b200 as ecco
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    wl = Workload(args.config, rank, world)
+    math = ecco.TC_TF32 if args.math == "tf32" else ecco.FFMA_EXACT
+    ctx = ecco.Context(backend=ecco.LEARNED, device=local_rank, math=math,
+                       max_cameras=wl.N, max_jobs=max(1, len(wl.local)), max_depth=DEPTH,
+                       steps_per_gpu_s=float(STEPS), **DIMS)
+    ctx.set_cameras(wl.scenes, wl.tp)
+    ctx.generate_frames(0)
+    ctx.seed_models(wl.local)
+    prep = ctx.prepare_trajectories(
+        wl.local, [BATCH] * len(wl.local), [wl.members(g) for g in wl.local],
+        [[1.0 / wl.per] * wl.per for _ in wl.local], [wl.members(g) for g in wl.local])
+    granted = [DEPTH] * len(wl.local)
+    cams = np.arange(wl.N, dtype=np.int32)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    dev = torch.device("cuda", local_rank)
+    M_local = torch.full((wl.N, wl.gb), float("nan"), dtype=torch.float64, device=dev)
+    M_all = torch.empty((world, wl.N, wl.gb), dtype=torch.float64, device=dev)
+    M_part = None if len(wl.local) == wl.gb else torch.empty((wl.N, max(1, len(wl.local))),
+                                                             dtype=torch.float64, device=dev)
+    best = torch.empty(wl.N, dtype=torch.int32, device=dev)
+    best_acc = torch.empty(wl.N, dtype=torch.float64, device=dev)
+    acc_host = np.zeros((len(wl.local), DEPTH + 1))
+    ev = {k: torch.cuda.Event(enable_timing=True) for k in ("a", "b", "c")}
+    phase = {"regroup": 0.0, "retrain": 0.0}
+
+    def step(w, timed=False):
+        with torch.cuda.stream(stream):
+            if timed:
+                ev["a"].record(stream)
+            if wl.local:
+                if M_part is None:
+                    ctx.eval_matrix_dev(wl.local, M_local.data_ptr(), cams=cams)
+                else:  # ragged last block: columns beyond the rank's groups stay NaN
+                    ctx.eval_matrix_dev(wl.local, M_part.data_ptr(), cams=cams)
+                    M_local[:, :len(wl.local)].copy_(M_part)
+            if world > 1:
+                dist.all_gather_into_tensor(M_all, M_local)
+                M = M_all
+            else:
+                M = M_local
+            ctx.route_matrix_dev(wl.N, wl.gb, M.data_ptr(), best.data_ptr(), best_acc.data_ptr(),
+                                 n_blocks=world)
+            if timed:
+                ev["b"].record(stream)
+            if wl.local:
+                ctx.train_prepared(prep, GPU_S, DEPTH, window=w, out=acc_host)
+                ctx.commit(wl.local, granted)
+            if timed:
+                ev["c"].record(stream)
+                ev["c"].synchronize()
+                phase["regroup"] += ev["a"].elapsed_time(ev["b"])
+                phase["retrain"] += ev["b"].elapsed_time(ev["c"])
+
+    def barrier():
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for w in range(args.warmup):
+        step(w + 1)
+    barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    ctx.profile(True)
+    l0 = ctx.launches
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        t0.record(stream)
+    for k in range(args.steps):
+        step(args.warmup + 1 + k, timed=True)
+    with torch.cuda.stream(stream):
+        t1.record(stream)
+    barrier()
+    launches = ctx.launches - l0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    kst = {name: ctx.kernel_stat(getattr(ecco, "KSTAT_" + name)) for name in
+           ("EVAL_HIDDEN", "EVAL_HEAD", "TRAIN_FWD", "TRAIN_DW1", "TRAIN_HEAD")}
+    ctx.profile(False)
+    t = torch.tensor([ms, phase["regroup"], phase["retrain"]], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, regroup_ms, retrain_ms = t.tolist()
+    samples = wl.samples_per_step_local() * args.steps
+    if dist is not None:
+        s = torch.tensor([samples], dtype=torch.float64, device=dev)
+        dist.all_reduce(s)
+        samples = s.item()
+
+    # ---- e2e: same step through the public API, frames from pinned host memory
+    e2e = run_e2e(args, ctx, wl, step, torch, dist, stream, best)
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        line = {
+            "metric": "group-retrain samples/s (per-window regroup + retrain)",
+            "value": samples / (ms / 1e3),
+            "unit": "samples/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "tf32" if args.math == "tf32" else "f32",
+            "data": "synthetic (counter-RNG camera streams, random-init group MLPs)",
+            "config": {
+                "workload": f"{args.config}: {wl.N} cameras / {wl.G} groups, learned classifier "
+                            f"F{DIMS['feat_dim']}-H{DIMS['hidden_dim']}-C{DIMS['num_classes']}, "
+                            f"B={DIMS['minibatch']}, S={DIMS['eval_samples']} eval frames/camera, "
+                            f"R={DIMS['ring_frames']} ring frames/camera, depth {DEPTH} x "
+                            f"{STEPS} SGD steps per group per window, full camera x group matrix",
+                "cameras": wl.N, "groups": wl.G, "groups_per_rank": wl.gb,
+                "parallelism": f"groups sharded over {world} rank(s); eval matrix all-gather",
+                "l2": "inputs larger than L2 (frames "
+                      f"{wl.N * (DIMS['ring_frames'] + DIMS['eval_samples']) * DIMS['feat_dim'] * 2 / 2**30:.1f} GiB)",
+            },
+            "regroup_ms_per_window": regroup_ms / args.steps,
+            "retrain_ms_per_window": retrain_ms / args.steps,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "e2e": e2e,
+            "roofline": roofline(kst, pk, pk_kind, args),
+            "kernels": {k: {"launches": v[0], "ms": v[1], "tflops": (v[2] / v[1] / 1e9) if v[1] else None}
+                        for k, v in kst.items()},
+        }
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(args, wl.N, wl.G)
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def roofline(kst, pk, pk_kind, args):
+    name, (n, ms, fl, by) = max(kst.items(), key=lambda kv: kv[1][1])
+    if not n or not ms:
+        return None
+    achieved = fl / (ms / 1e3) / 1e12
+    if args.math == "tf32":
+        peak = pk["bf16_tflops"] / 2.0
+        how = f"tf32 dense = half the {pk_kind} bf16 {pk['bf16_tflops']} TFLOP/s"
+    else:
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        how = "fp32 FFMA spec (148 SM x 128 lanes x 2 x 1.965 GHz)"
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(name)
+        except (OSError, ValueError):
+            traffic = None
+    return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak, "peak_source": how,
+            "avg_launch_ms": ms / n, "launches": n, "traffic": traffic}
+
+
+def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev):
+    """Frames uploaded from pinned host memory and results read back every step."""
+    import paper_2512_11727_b200 as ecco  # noqa: F401
+    R, S, F = DIMS["ring_frames"], DIMS["eval_samples"], DIMS["feat_dim"]
+    fr = torch.empty((wl.N, R, F), dtype=torch.int16, pin_memory=True)
+    lb = torch.empty((wl.N, R), dtype=torch.int32, pin_memory=True)
+    evf = torch.empty((wl.N, S, F), dtype=torch.int16, pin_memory=True)
+    evl = torch.empty((wl.N, S), dtype=torch.int32, pin_memory=True)
+    f, l, e, el = ctx.read_frames(wl.N)
+    fr.numpy().view(np.uint16)[...] = f
+    lb.numpy()[...] = l
+    evf.numpy().view(np.uint16)[...] = e
+    evl.numpy()[...] = el
+    del f, l, e, el
+    best_host = torch.empty(wl.N, dtype=torch.int32, pin_memory=True)
+    steps = max(1, min(args.steps, 3))
+    h0, d0 = ctx.transfer_bytes()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for k in range(steps):
+        ctx.upload_frames_host_ptr(wl.N, fr.data_ptr(), lb.data_ptr(), evf.data_ptr(), evl.data_ptr())
+        step(10_000 + k)
+        with torch.cuda.stream(stream):
+            best_host.copy_(best_dev, non_blocking=True)  # group assignments back to the host
+    ctx.synchronize()
+    el_s = time.perf_counter() - t0
+    h1, d1 = ctx.transfer_bytes()
+    d1 += steps * best_host.numel() * 4
+    t = torch.tensor([el_s], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el_s = t.item()
+    samples = wl.samples_per_step_local() * steps
+    if dist is not None:
+        s = torch.tensor([samples], dtype=torch.float64, device=t.device)
+        dist.all_reduce(s)
+        samples = s.item()
+    return {"value": samples / el_s, "unit": "samples/s",
+            "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
+            "ms_per_step": el_s * 1e3 / steps, "steps": steps,
+            "how": "ecco_upload_frames from pinned host buffers + the step + assignments/accuracies "
+                   "read back, wall clock with a device synchronize at the end"}
+
+
+# ------------------------------------------------------------ CPU baselines --
+
+def cpu_sample(N, G, budget_s=12.0):
+    """The oracle's restatement of the same step (FFMA-order fp32 C, one
+    thread per group) timed on a bounded sample and scaled to the window:
+    pairs of the eval matrix and SGD steps measured separately."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    from oracle import OrcLcfg
+
+    if not os.path.exists(oracle.ORACLE_SO):
+        oracle.build(ref=False)
+    L = oracle.oracle()
+    F, H, Cc, B, R, S = (DIMS["feat_dim"], DIMS["hidden_dim"], DIMS["num_classes"],
+                         DIMS["minibatch"], DIMS["ring_frames"], DIMS["eval_samples"])
+    lc = OrcLcfg(F=F, H=H, C=Cc, D=2, B=B, R=R, S=S, lr=0.05, noise=1.0,
+                 steps_per_gpu_s=float(STEPS), seed=0x5eed0001)
+    P = np.zeros(Cc * F, np.float32)
+    Q = np.zeros(Cc * 2 * F, np.float32)
+    L.orc_prototypes(C.byref(lc), P, Q)
+    x = np.zeros(S * F, np.uint16)
+    y = np.zeros(S, np.int32)
+    L.orc_gen_frames(C.byref(lc), P, Q, 0, 0, 1, S, np.array([0.1, 0.2]), x, y)
+    xb = np.ascontiguousarray(np.resize(x, B * F))
+    yb = np.ascontiguousarray(np.resize(y, B))
+    cores = os.cpu_count() or 1
+
+    def weights():
+        w = [np.zeros(F * H, np.float32), np.zeros(H, np.float32), np.zeros(H * Cc, np.float32),
+             np.zeros(Cc, np.float32)]
+        L.orc_init_weights(C.byref(lc), *w)
+        return w
+
+    def eval_work(n):
+        w = weights()
+        for _ in range(n):
+            L.orc_count_correct(C.byref(lc), x, y, S, *w)
+        return n
+
+    def train_work(n):
+        w = weights()
+        for _ in range(n):
+            L.orc_sgd_step(C.byref(lc), xb, yb, *w)
+        return n
+
+    # calibrate one unit each, then size the parallel sample to ~budget_s
+    t = time.perf_counter()
+    eval_work(1)
+    t_pair = time.perf_counter() - t
+    t = time.perf_counter()
+    train_work(1)
+    t_step = time.perf_counter() - t
+    per_thread = budget_s / 2.0
+    n_pairs = max(1, int(per_thread / max(t_pair, 1e-6)))
+    n_steps = max(1, int(per_thread / max(t_step, 1e-6)))
+    with ThreadPoolExecutor(cores) as ex:
+        t = time.perf_counter()
+        list(ex.map(eval_work, [n_pairs] * cores))
+        pair_rate = n_pairs * cores / (time.perf_counter() - t)
+        t = time.perf_counter()
+        list(ex.map(train_work, [n_steps] * cores))
+        step_rate = n_steps * cores / (time.perf_counter() - t)
+    per = N // G
+    steps_window = G * DEPTH * int(GPU_S * STEPS)
+    pairs_window = N * G + G * (DEPTH + 1) * per  # regroup matrix + chain evaluations
+    window_s = pairs_window / pair_rate + steps_window / step_rate
+    samples = steps_window * B
+    return {"value": samples / window_s, "unit": "samples/s", "cores": cores, "kind": "port",
+            "sample": f"{n_pairs * cores} eval pairs (S={S} frames each) and {n_steps * cores} "
+                      f"SGD steps (B={B}) of the oracle (oracle/ecco_oracle.c, FFMA-order fp32) on "
+                      f"{cores} threads; window = {pairs_window} pairs + {steps_window} steps, "
+                      f"scaled from the measured rates",
+            "window_s": window_s}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    wl = Workload(args.config, 0, 1)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(wl.N, wl.G, budget_s=2.0)
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_sample(wl.N, wl.G, budget_s=args.ref_budget)
+        vals.append(last["value"])
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference",
+        "metric": "group-retrain samples/s (per-window regroup + retrain)",
+        "value": value, "unit": "samples/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": last["window_s"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-RNG camera streams, random-init group MLPs)",
+        "config": {"workload": f"{args.config}: {wl.N} cameras / {wl.G} groups (same as the B200 arm)",
+                   "cameras": wl.N, "groups": wl.G},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": last["cores"],
+                         "kind": "port", "sample": last["sample"]},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+        "note": "the reference (a C++ simulator) has no learned trainer: its path is the "
+                "parametric accuracy model (SURVEY.md 0); the learned path's CPU form is the "
+                "oracle restatement, run here on every host core",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--math", default="tf32", choices=["tf32", "ffma"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--ref-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_b200(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

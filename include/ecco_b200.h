@@ -215,6 +215,20 @@ ecco_status ecco_route_propose(ecco_ctx* ctx, int n_probes, const double* scenes
                                const int* job_ids, const uint8_t* mask, int* best_col,
                                double* best_acc);
 
+/* Epilogue alone, over a camera x group matrix already in HBM (e.g. the
+ * all-gathered column blocks of every rank): the warp-reduced argmax /
+ * threshold of group_request (grouping.cpp:30-39) per camera row.
+ * matrix_dev: n_blocks column blocks of g_block columns, block b an n x
+ * g_block row-major fp64 array at matrix_dev + b*n*g_block (NaN = masked);
+ * n_blocks = 1 is a plain row-major n x g_block matrix, n_blocks = world size
+ * the output of an all-gather of every rank's ecco_eval_matrix_dev block.
+ * Column j = b*g_block + jb.  req_dev: n fp64 device accuracies (nullable =
+ * 0); best_col_dev: n int32 (-1 = none qualifies); best_acc_dev: n fp64.
+ * Stream-ordered on the context stream; no host synchronisation. */
+ecco_status ecco_route_matrix_dev(ecco_ctx* ctx, int n, int g_block, int n_blocks,
+                                  const void* matrix_dev, const void* req_dev, void* best_col_dev,
+                                  void* best_acc_dev);
+
 /* ---- TrainingBackend::train batches: marginal-gain probes ------------------
  * Batch description = TrainingBatchStats (accuracy_model.hpp:50-56) with the
  * source_mix flattened to CSR (cameras in std::map order). */

@@ -24,6 +24,9 @@ LIB_PATH = os.path.join(HERE, "libecco_b200.so")
 OK, INVALID_ARGUMENT, LOGIC, INFEASIBLE, SCHEMA, CUDA, RUNTIME = range(7)
 PARAMETRIC, LEARNED = 0, 1
 FFMA_EXACT, TC_TF32 = 0, 1
+# ecco_kstat (include/ecco_b200.h)
+(KSTAT_TRAIN_FWD, KSTAT_TRAIN_DW1, KSTAT_TRAIN_HEAD, KSTAT_EVAL_HIDDEN, KSTAT_EVAL_HEAD,
+ KSTAT_P_EVAL, KSTAT_P_TRAJ, KSTAT_P_PROFILE, KSTAT_FRAMES) = range(9)
 
 
 class EccoError(RuntimeError):
@@ -99,6 +102,7 @@ EXPORTS = [
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
+    "ecco_route_matrix_dev",
     "ecco_train_trajectories", "ecco_commit", "ecco_last_losses", "ecco_sample_indices",
     "ecco_profile_tables", "ecco_sim_default_options", "ecco_sim_create", "ecco_sim_destroy",
     "ecco_sim_last_error", "ecco_sim_step_window", "ecco_sim_last_timings",
@@ -207,6 +211,23 @@ class Context:
     def synchronize(self):
         self._check(lib().ecco_synchronize(self._h))
 
+    # per-kernel CUDA-event profiling (ecco_profile / ecco_kernel_stat)
+    def profile(self, enable=True):
+        self._check(lib().ecco_profile(self._h, int(bool(enable))))
+
+    def kernel_stat(self, which):
+        """(launches, device ms, algorithmic flops, algorithmic bytes) of one
+        tracked kernel family (KSTAT_*), accumulated since profiling began."""
+        n, ms, fl, by = C.c_uint64(), C.c_double(), C.c_double(), C.c_double()
+        self._check(lib().ecco_kernel_stat(self._h, int(which), C.byref(n), C.byref(ms),
+                                           C.byref(fl), C.byref(by)))
+        return n.value, ms.value, fl.value, by.value
+
+    def transfer_bytes(self):
+        h2d, d2h = C.c_uint64(), C.c_uint64()
+        self._check(lib().ecco_transfer_bytes(self._h, C.byref(h2d), C.byref(d2h)))
+        return h2d.value, d2h.value
+
     # camera table
     def set_cameras(self, scenes, throughput):
         s, sp = _p(scenes, np.float64)
@@ -238,6 +259,12 @@ class Context:
         self._check(lib().ecco_read_frames(self._h, int(n_cams), *[a.ctypes.data_as(C.c_void_p)
                                                                    for a in (fr, lb, ev, el)]))
         return fr, lb, ev, el
+
+    def upload_frames_host_ptr(self, n_cams, frames_ptr, labels_ptr, eval_ptr, eval_labels_ptr):
+        """ecco_upload_frames from caller-owned (e.g. pinned) host buffers."""
+        self._check(lib().ecco_upload_frames(self._h, int(n_cams), C.c_void_p(frames_ptr),
+                                             C.c_void_p(labels_ptr), C.c_void_p(eval_ptr),
+                                             C.c_void_p(eval_labels_ptr)))
 
     def upload_frames_dev(self, n_cams, frames_ptr, labels_ptr, eval_ptr, eval_labels_ptr):
         self._check(lib().ecco_upload_frames_dev(self._h, int(n_cams), C.c_void_p(frames_ptr),
@@ -351,30 +378,56 @@ class Context:
                                              acc.ctypes.data_as(C.c_void_p)))
         return best, acc
 
+    def route_matrix_dev(self, n, g_block, matrix_ptr, best_ptr, acc_ptr, req_ptr=None,
+                         n_blocks=1):
+        """Argmax/threshold epilogue over a device matrix (all pointers device)."""
+        self._check(lib().ecco_route_matrix_dev(self._h, int(n), int(g_block), int(n_blocks),
+                                                C.c_void_p(matrix_ptr),
+                                                C.c_void_p(req_ptr) if req_ptr else None,
+                                                C.c_void_p(best_ptr), C.c_void_p(acc_ptr)))
+
     # training
+    def prepare_trajectories(self, job_ids, batches, sources, fracs, members):
+        """Flattens the per-job arguments of train_trajectories once (CSR
+        source_mix / member lists, ecco_batch array) so a caller that trains
+        the same jobs every window does no per-call list building."""
+        n = len(job_ids)
+        p = {"n": n}
+        p["ids"] = np.ascontiguousarray(job_ids, np.int32)
+        p["bt"] = (Batch * max(n, 1))(*[Batch(*b) for b in batches])
+        so = np.zeros(n + 1, np.int32)
+        so[1:] = np.cumsum([len(x) for x in sources])
+        p["so"] = so
+        p["sc"] = np.array([c for x in sources for c in x] or [0], np.int32)
+        p["sf"] = np.array([f for x in fracs for f in x] or [0.0], np.float64)
+        mo = np.zeros(n + 1, np.int32)
+        mo[1:] = np.cumsum([len(m) for m in members])
+        p["mo"] = mo
+        p["mc"] = np.array([c for m in members for c in m] or [0], np.int32)
+        p["mb0"] = np.zeros(max(n, 1), np.int32)
+        return p
+
+    def train_prepared(self, p, gpu_seconds, depth, window=0, micro_base=None, out=None):
+        """ecco_train_trajectories on a prepare_trajectories() batch; returns
+        acc[n_jobs, depth+1] (written into `out` when given)."""
+        n = p["n"]
+        if out is None:
+            out = np.zeros((n, depth + 1))
+        mb = p["mb0"] if micro_base is None else np.ascontiguousarray(micro_base, np.int32)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        self._check(lib().ecco_train_trajectories(
+            self._h, n, vp(p["ids"]), p["bt"], vp(p["so"]), vp(p["sc"]), vp(p["sf"]), vp(p["mo"]),
+            vp(p["mc"]), vp(mb), C.c_int(window), C.c_double(gpu_seconds), C.c_int(depth),
+            vp(out)))
+        return out
+
     def train_trajectories(self, job_ids, batches, sources, fracs, members, gpu_seconds, depth,
                            micro_base=None, window=0):
         """Speculative evaluate/train chains.  batches: list of (fps, res, quality);
         sources/fracs: per-job source_mix (camera indices in map order, fractions);
         members: per-job member camera indices.  Returns acc[n_jobs, depth+1]."""
-        j, jp = _p(job_ids, np.int32)
-        n = len(j)
-        bt = (Batch * max(n, 1))(*[Batch(*b) for b in batches])
-        so = np.zeros(n + 1, np.int32)
-        so[1:] = np.cumsum([len(s) for s in sources])
-        sc = np.array([c for s in sources for c in s] or [0], np.int32)
-        sf = np.array([f for s in fracs for f in s] or [0.0], np.float64)
-        mo = np.zeros(n + 1, np.int32)
-        mo[1:] = np.cumsum([len(m) for m in members])
-        mc = np.array([c for m in members for c in m] or [0], np.int32)
-        mb, mbp = _p(micro_base if micro_base is not None else np.zeros(n), np.int32)
-        out = np.zeros((n, depth + 1))
-        self._check(lib().ecco_train_trajectories(
-            self._h, n, jp, bt, so.ctypes.data_as(C.c_void_p), sc.ctypes.data_as(C.c_void_p),
-            sf.ctypes.data_as(C.c_void_p), mo.ctypes.data_as(C.c_void_p),
-            mc.ctypes.data_as(C.c_void_p), mbp, C.c_int(window), C.c_double(gpu_seconds),
-            C.c_int(depth), out.ctypes.data_as(C.c_void_p)))
-        return out
+        p = self.prepare_trajectories(job_ids, batches, sources, fracs, members)
+        return self.train_prepared(p, gpu_seconds, depth, window=window, micro_base=micro_base)
 
     def commit(self, job_ids, granted):
         j, jp = _p(job_ids, np.int32)

@@ -560,6 +560,18 @@ ecco_status ecco_rename_models(ecco_ctx* ctx, int n, const int* old_ids, const i
   });
 }
 
+ecco_status ecco_route_matrix_dev(ecco_ctx* ctx, int n, int g_block, int n_blocks,
+                                  const void* matrix_dev, const void* req_dev, void* best_col_dev,
+                                  void* best_acc_dev) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(n >= 0 && g_block >= 0 && n_blocks >= 1, "route_matrix: bad size");
+    ECCO_REQUIRE(n == 0 || ((matrix_dev || g_block == 0) && best_col_dev && best_acc_dev),
+                 "route_matrix: null buffer");
+    lbackend::route_matrix(ctx, n, g_block, n_blocks, (const double*)matrix_dev,
+                           (const double*)req_dev, (int*)best_col_dev, (double*)best_acc_dev);
+  });
+}
+
 ecco_status ecco_route_propose(ecco_ctx* ctx, int n, const double* scenes, const int* cam_idx,
                                const double* req, int g, const int* job_ids, const uint8_t* mask,
                                int* best_col, double* best_acc) {

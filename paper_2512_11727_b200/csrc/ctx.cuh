@@ -267,6 +267,8 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
                   double* d_out);
 void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted);
 void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, double* d_out);
+void route_matrix(ecco_ctx* ctx, int n, int gb, int n_blocks, const double* d_M,
+                  const double* d_req, int* d_best, double* d_best_acc);
 void sample_indices(ecco_ctx* ctx, int job_id, int n_src, const int* d_src_cam,
                     const double* d_src_frac, int window, int micro, int step, int* d_cam,
                     int* d_frame);

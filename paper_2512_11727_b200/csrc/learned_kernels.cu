@@ -475,16 +475,22 @@ __global__ void k_l_job_mean(LDims g, int n_jobs, const int* mem_off, const int*
   out[(size_t)j * stride + col] = nm == 0 ? floor_acc : __ddiv_rn(sum, (double)nm);
 }
 
-__global__ void k_l_route(int n, int g, const double* M, const double* req, int* best_col,
-                          double* best_acc) {
+// Warp-reduced argmax / threshold of group_request (grouping.cpp:30-39) per
+// probe row.  The matrix is n_blocks column blocks of gb columns, block b
+// stored row-major at M + b*n*gb (n_blocks = 1: plain n x gb row-major; the
+// all-gathered column blocks of every rank otherwise).
+__global__ void k_l_route(int n, int gb, int n_blocks, const double* M, const double* req,
+                          int* best_col, double* best_acc) {
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (i >= n) return;
   int bc = -1;
   double ba = 0.0;
-  const double r = req[i];
+  const double r = req ? req[i] : 0.0;
+  const int g = gb * n_blocks;
   for (int j = lane; j < g; j += 32) {
-    const double a = M[(size_t)i * g + j];
+    const int b = j / gb;
+    const double a = M[((size_t)b * n + i) * gb + (j - b * gb)];
     if (a != a || a < r) continue;  // masked (NaN) or below the device accuracy
     if (bc < 0 || a > ba) {
       bc = j;
@@ -675,7 +681,7 @@ void route_propose(ecco_ctx* ctx, int n, const int* d_cams, const double* d_req,
     M = (double*)tmp.get(sizeof(double) * (size_t)n * gj);
     eval_matrix(ctx, n, d_cams, gj, d_slots, d_mask, M);
   }
-  k_l_route<<<nblk((size_t)n * 32, 256), 256, 0, ctx->stream>>>(n, gj, M, d_req, d_best, d_best_acc);
+  k_l_route<<<nblk((size_t)n * 32, 256), 256, 0, ctx->stream>>>(n, gj, 1, M, d_req, d_best, d_best_acc);
   ECCO_LAUNCHED(ctx);
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   tmp.release();
@@ -860,6 +866,14 @@ void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted)
   k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(n_jobs, d_slots, ctx->d_wspec,
                                                               spec_stride, 0, ctx->d_w, np, 0, np,
                                                               d_granted);
+  ECCO_LAUNCHED(ctx);
+}
+
+void route_matrix(ecco_ctx* ctx, int n, int gb, int n_blocks, const double* d_M,
+                  const double* d_req, int* d_best, double* d_best_acc) {
+  if (n == 0) return;
+  k_l_route<<<nblk((size_t)n * 32, 256), 256, 0, ctx->stream>>>(n, gb, n_blocks, d_M, d_req,
+                                                                 d_best, d_best_acc);
   ECCO_LAUNCHED(ctx);
 }
 
