@@ -215,6 +215,13 @@ ecco_status ecco_route_propose(ecco_ctx* ctx, int n_probes, const double* scenes
                                const int* job_ids, const uint8_t* mask, int* best_col,
                                double* best_acc);
 
+/* Diagnostic of the fused evaluation kernel (learned backend, tensor-core
+ * math): the logits (+ b2) of every eval frame of cameras cam_idx[0..n)
+ * under every model job_ids[0..g), as out[((i*S + s)*g + j)*C + c].  Exposed
+ * for the numerics tests only. */
+ecco_status ecco_debug_eval_logits(ecco_ctx* ctx, int n, const int* cam_idx, int g,
+                                   const int* job_ids, float* out);
+
 /* Epilogue alone, over a camera x group matrix already in HBM (e.g. the
  * all-gathered column blocks of every rank): the warp-reduced argmax /
  * threshold of group_request (grouping.cpp:30-39) per camera row.

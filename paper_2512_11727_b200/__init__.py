@@ -102,7 +102,7 @@ EXPORTS = [
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
-    "ecco_route_matrix_dev",
+    "ecco_route_matrix_dev", "ecco_debug_eval_logits",
     "ecco_train_trajectories", "ecco_commit", "ecco_last_losses", "ecco_sample_indices",
     "ecco_profile_tables", "ecco_sim_default_options", "ecco_sim_create", "ecco_sim_destroy",
     "ecco_sim_last_error", "ecco_sim_step_window", "ecco_sim_last_timings",
@@ -377,6 +377,16 @@ class Context:
                                              best.ctypes.data_as(C.c_void_p),
                                              acc.ctypes.data_as(C.c_void_p)))
         return best, acc
+
+    def debug_eval_logits(self, job_ids, cams):
+        """Logits (+ b2) of the fused evaluation kernel: [n_cams, S, n_jobs, C]."""
+        j, jp = _p(job_ids, np.int32)
+        c, cp = _p(cams, np.int32)
+        g = self.cfg
+        out = np.zeros((len(c), g.eval_samples, len(j), g.num_classes), np.float32)
+        self._check(lib().ecco_debug_eval_logits(self._h, len(c), cp, len(j), jp,
+                                                 out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def route_matrix_dev(self, n, g_block, matrix_ptr, best_ptr, acc_ptr, req_ptr=None,
                          n_blocks=1):

@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "ctx.cuh"
 
 namespace {
@@ -36,6 +38,9 @@ void free_all(ecco_ctx* c) {
                   c->d_eval,   c->d_eval_labels, c->d_losses};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  fused::free_shadow(c->sh_commit);
+  fused::free_shadow(c->sh_spec);
+  delete (CUtensorMap*)c->map_x;
   for (auto& b : c->scratch) b.release();
   for (auto& b : c->hscratch) b.release();
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -378,6 +383,7 @@ ecco_status ecco_seed_models(ecco_ctx* ctx, int n, const int* job_ids, const dou
     if (n == 0) return;
     std::vector<int> s(n);
     for (int i = 0; i < n; ++i) s[i] = ctx->alloc_slot(job_ids[i]);
+    for (int i = 0; i < n; ++i) ctx->mark_dirty(s[i]);
     int* d_s = ctx->upload(0, s.data(), n);
     if (learned(ctx)) {
       int* d_j = ctx->upload(1, job_ids, n);
@@ -422,7 +428,9 @@ ecco_status ecco_set_weights(ecco_ctx* ctx, int job_id, const float* w1, const f
     ECCO_REQUIRE(learned(ctx), "set_weights: learned backend only");
     const ecco_config& g = ctx->cfg;
     const size_t F = g.feat_dim, H = g.hidden_dim, C = g.num_classes;
-    float* base = ctx->d_w + (size_t)ctx->alloc_slot(job_id) * ctx->n_params;
+    const int slot = ctx->alloc_slot(job_id);
+    ctx->mark_dirty(slot);
+    float* base = ctx->d_w + (size_t)slot * ctx->n_params;
     ECCO_CUDA(ctx_memcpy(ctx, base, w1, F * H * 4, cudaMemcpyHostToDevice, ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, base + F * H, b1, H * 4, cudaMemcpyHostToDevice, ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, base + F * H + H, w2, H * C * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -483,7 +491,7 @@ static void eval_matrix_impl(ecco_ctx* ctx, int n, const double* scenes, const i
     check_cams(ctx, n, cam_idx, "eval_matrix");
     int* d_c = (int*)bp.get(sizeof(int) * n);
     ECCO_CUDA(ctx_memcpy(ctx, d_c, cam_idx, sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
-    lbackend::eval_matrix(ctx, n, d_c, g, d_s, d_m, d_out);
+    lbackend::eval_matrix(ctx, n, d_c, g, d_s, d_m, d_out, s.data());
   } else {
     ECCO_REQUIRE(scenes != nullptr, "eval_matrix: parametric backend needs scenes");
     const int D = ctx->cfg.scene_dims;
@@ -531,7 +539,7 @@ ecco_status ecco_eval_pairs(ecco_ctx* ctx, int n, const double* scenes, const in
     double* d_out = (double*)bo.get(sizeof(double) * n);
     if (learned(ctx)) {
       ECCO_REQUIRE(cams != nullptr, "eval_pairs: learned backend needs cams");
-      lbackend::eval_pairs(ctx, n, d_c, d_s, d_out);
+      lbackend::eval_pairs(ctx, n, d_c, d_s, d_out, s.data());
     } else {
       ECCO_REQUIRE(scenes != nullptr || cams != nullptr, "eval_pairs: need scenes or cams");
       double* d_sc = nullptr;
@@ -557,6 +565,18 @@ ecco_status ecco_rename_models(ecco_ctx* ctx, int n, const int* old_ids, const i
       ctx->slot_of.erase(old_ids[i]);
       ctx->slot_of[new_ids[i]] = s;
     }
+  });
+}
+
+ecco_status ecco_debug_eval_logits(ecco_ctx* ctx, int n, const int* cam_idx, int g,
+                                   const int* job_ids, float* out) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(learned(ctx) && ctx->fused_eval,
+                 "debug_eval_logits: needs the learned backend with tensor-core math");
+    if (n == 0 || g == 0) return;
+    check_cams(ctx, n, cam_idx, "debug_eval_logits");
+    auto s = slots_of(ctx, g, job_ids);
+    lbackend::debug_logits(ctx, n, cam_idx, g, s.data(), out);
   });
 }
 
@@ -669,6 +689,8 @@ ecco_status ecco_commit(ecco_ctx* ctx, int n_jobs, const int* job_ids, const int
     for (int j = 0; j < n_jobs; ++j)
       ECCO_REQUIRE(granted[j] >= 0 && granted[j] <= ctx->cfg.max_depth, "commit: granted out of range");
     auto s = slots_of(ctx, n_jobs, job_ids);
+    for (int j = 0; j < n_jobs; ++j)
+      if (granted[j] > 0) ctx->mark_dirty(s[j]);
     DevBuf a, b;
     int* d_s = (int*)a.get(sizeof(int) * n_jobs);
     int* d_g = (int*)b.get(sizeof(int) * n_jobs);

@@ -92,6 +92,15 @@ struct KStat {
   std::vector<Pending> pending;
 };
 
+// bf16 shadow of a set of fp32 model slots for the fused tensor-core
+// evaluation (eval_kernels.cu): W1^T [slot][H][F] (TMA map `map_w`) and the
+// 128B-swizzled W2^T image per slot.
+struct Shadow {
+  uint16_t* w1t = nullptr;
+  uint8_t* w2t = nullptr;
+  void* map_w = nullptr;  // CUtensorMap*
+};
+
 struct ecco_ctx {
   ecco_config cfg{};
   cudaStream_t stream = nullptr;
@@ -165,7 +174,17 @@ struct ecco_ctx {
   float* d_losses = nullptr;     // slots * max_depth
   int frames_window = -1;
 
-  DevBuf scratch[12];  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
+  // fused evaluation: shadows of the committed models (refreshed lazily for
+  // slots marked dirty) and of the speculative snapshot being evaluated
+  bool fused_eval = false;
+  Shadow sh_commit, sh_spec;
+  std::vector<char> sh_dirty;
+  void* map_x = nullptr;  // CUtensorMap* over d_eval
+  void mark_dirty(int slot) {
+    if (slot >= 0 && slot < (int)sh_dirty.size()) sh_dirty[slot] = 1;
+  }
+
+  DevBuf scratch[16];  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
   HostBuf hscratch[4];
 
   int slot(int job_id) const {
@@ -249,12 +268,31 @@ void eval_pairs(ecco_ctx* ctx, int n, const double* d_scenes_in, const int* d_ca
                 const int* d_slots, double* d_out);
 }  // namespace pbackend
 
+namespace fused {
+bool supported(const ecco_ctx* ctx);
+void init_shadow(ecco_ctx* ctx, Shadow& sh);
+void free_shadow(Shadow& sh);
+void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
+                    const std::vector<int>& slots);
+// Correct-prediction counts of (probe camera, model slot) pairs.  Dense mode
+// (d_tile_ebeg == nullptr): every probe under every entry, counts[p*ld+col].
+// Pairs mode: tile m walks entries [tile_ebeg[m], tile_ebeg[m+1]) and a probe
+// row counts only under its own slot (d_probe_slot), counts[p].
+void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wstride,
+                 int n_probes, const int* d_cams, int n_ent, const int* d_ent_slot,
+                 const int* d_ent_col, int n_tiles_override, const int* d_tile_ebeg,
+                 const int* d_probe_slot, int ld, int* d_counts, float* dbg_logits,
+                 double live_pairs);
+void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* d_mask,
+                   double* d_out);
+}  // namespace fused
+
 namespace lbackend {
 void init(ecco_ctx* ctx);
 void generate_frames(ecco_ctx* ctx, int window);
 void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const int* d_job_ids);
 void eval_matrix(ecco_ctx* ctx, int n_probes, const int* d_cams, int n_jobs, const int* d_slots,
-                 const uint8_t* d_mask, double* d_out);
+                 const uint8_t* d_mask, double* d_out, const int* h_slots = nullptr);
 void route_propose(ecco_ctx* ctx, int n_probes, const int* d_cams, const double* d_req,
                    int n_jobs, const int* d_slots, const uint8_t* d_mask, int* d_best,
                    double* d_best_acc);
@@ -266,7 +304,9 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
                   const int* d_mem_cam, const int* d_micro_base, int window, int depth,
                   double* d_out);
 void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted);
-void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, double* d_out);
+void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, double* d_out,
+                const int* h_slots = nullptr);
+void debug_logits(ecco_ctx* ctx, int n, const int* h_cams, int gj, const int* h_slots, float* out);
 void route_matrix(ecco_ctx* ctx, int n, int gb, int n_blocks, const double* d_M,
                   const double* d_req, int* d_best, double* d_best_acc);
 void sample_indices(ecco_ctx* ctx, int job_id, int n_src, const int* d_src_cam,

@@ -1,0 +1,509 @@
+// Fused camera x group evaluation (K6 of SURVEY.md 2): for every (probe
+// camera, group model) pair, the number of the camera's S labelled eval frames
+// that the group's MLP classifies correctly -- hidden layer, ReLU, logits,
+// argmax and the correct-count in ONE persistent kernel, nothing but the
+// counts written to HBM.
+//
+//   Z      = X[128 rows, F] . W1[F, H]        tcgen05 kind::f16 (bf16 in, fp32
+//                                             accumulate in TMEM), H in halves
+//                                             of N = 128
+//   R      = bf16(relu(Z + b1))               epilogue warps: TMEM -> regs ->
+//                                             TMEM (A operand of the next MMA)
+//   logits = R[128, H] . W2[H, C]             tcgen05 kind::f16, A from TMEM
+//   count += (argmax(logits + b2) == label)   warp ballot + popc, one atomic
+//                                             per (warp, pair)
+//
+// Rows of a 128-row tile are 2 x 64 eval frames (S % 64 == 0): each 64-row
+// block is one TMA box at the probe camera's eval-set row, so any camera list
+// can be probed.  The tile's X stays resident in shared memory (F <= 512:
+// <= 128 KB, loaded once per tile by TMA with 128-byte swizzle) while the
+// group models stream through a 5-6 stage TMA pipeline of 128-row W1^T boxes
+// (bf16 shadow of the fp32 masters, refreshed when a model changes), so the
+// tensor cores read only W1 from L2 per group: 256 FLOP per L2 byte.
+//
+// Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer, warps
+// 2-5 epilogue (TMEM lane quadrant = warp % 4).  TMEM (512 columns):
+//   [0,256)   Z, two 128-column buffers      (MMA <-> epilogue double buffer)
+//   [256,384) R, two 64-column bf16 buffers  (epilogue <-> MMA double buffer)
+//   [384,..)  logits, 1-2 buffers of C columns
+// Numerics: X is exact in bf16, W1 and R are rounded to bf16; accumulation is
+// fp32.  DESIGN.md states the tolerance against the fp32 oracle.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ctx.cuh"
+#include "sm100.cuh"
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kTileRows = 128;
+constexpr int kKC = 64;               // K per TMA box / pipeline stage (one 128-B swizzle atom)
+constexpr int kHalf = 128;            // N of the hidden-layer MMA
+constexpr int kThreads = 192;
+constexpr uint32_t kBoxBytes = kHalf * 128;   // one W1^T stage: 128 rows x 64 bf16
+constexpr uint32_t kAChunk = kTileRows * 128; // one X K-chunk: 128 rows x 64 bf16
+constexpr int kMaxStages = 8;
+constexpr uint32_t kTmemZ = 0, kTmemR = 256, kTmemL = 384;
+
+struct EvalArgs {
+  int n_rows;            // n_probes * S
+  int S;
+  int F, H, C;
+  int n_tiles;
+  const int* cams;       // probe -> camera table index
+  const int32_t* labels; // camera table eval labels [cam * S + s]
+  // entries: (slot, output column); dense mode: every tile walks all n_ent;
+  // pairs mode (tile_ebeg != null): tile m walks [tile_ebeg[m], tile_ebeg[m+1])
+  const int* ent_slot;
+  const int* ent_col;
+  int n_ent;
+  const int* tile_ebeg;
+  const int* probe_slot; // pairs mode: a row counts only under its probe's own slot
+  int ld;                // dense: counts[p * ld + col]; pairs: counts[p]
+  int* counts;
+  const float* wbase;    // fp32 masters: b1 at +F*H, b2 at +F*H+H+H*C
+  size_t wstride;
+  const uint8_t* w2t;    // per slot: W2^T bf16 K-major 128B-swizzled image
+  uint32_t w2t_bytes;
+  int stages;
+  int nl;                // logits buffers (1 or 2)
+  float* dbg_logits;     // optional: [n_rows][n_ent][C] logits + b2 (dense mode tests)
+};
+
+__device__ __forceinline__ int tile_ent_begin(const EvalArgs& a, int m) {
+  return a.tile_ebeg ? a.tile_ebeg[m] : 0;
+}
+__device__ __forceinline__ int tile_ent_end(const EvalArgs& a, int m) {
+  return a.tile_ebeg ? a.tile_ebeg[m + 1] : a.n_ent;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_eval_fused(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                 EvalArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int nkc = a.F / kKC;
+  const int nh = a.H / kHalf;
+  uint8_t* sA = smem;                                   // nkc x 16 KB
+  uint8_t* sB = sA + nkc * kAChunk;                     // stages x 16 KB
+  uint8_t* sW2 = sB + a.stages * kBoxBytes;             // 2 x w2t_bytes
+  __shared__ __align__(8) uint64_t a_full, a_empty;
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ __align__(8) uint64_t w2_full[2], w2_empty[2];
+  __shared__ __align__(8) uint64_t z_full[2], z_empty[2], r_full[2], r_empty[2];
+  __shared__ __align__(8) uint64_t l_full[2], l_empty[2];
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_x);
+    tma_prefetch(&map_w);
+    mbar_init(&a_full, 1);
+    mbar_init(&a_empty, 1);
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&w2_full[b], 1);
+      mbar_init(&w2_empty[b], 1);
+      mbar_init(&z_full[b], 1);
+      mbar_init(&z_empty[b], 4);
+      mbar_init(&r_full[b], 4);
+      mbar_init(&r_empty[b], 1);
+      mbar_init(&l_full[b], 1);
+      mbar_init(&l_empty[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t sph = 0;
+      uint32_t u = 0, t = 0;
+      for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x, ++t) {
+        if (t > 0) mbar_wait(&a_empty, (t - 1) & 1);
+        mbar_expect_tx(&a_full, (uint32_t)nkc * kAChunk);
+        for (int h2 = 0; h2 < 2; ++h2) {
+          int b = m * 2 + h2;
+          if (b * 64 >= a.n_rows) b = 0;  // padding rows: any valid box, masked later
+          const int p = (b * 64) / a.S, soff = (b * 64) % a.S;
+          const int row = a.cams[p] * a.S + soff;
+          for (int kc = 0; kc < nkc; ++kc)
+            tma_load_2d(sA + kc * kAChunk + h2 * (kAChunk / 2), &map_x, kc * kKC, row, &a_full);
+        }
+        const int e1 = tile_ent_end(a, m);
+        for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
+          const int slot = a.ent_slot[e];
+          const int wb = u & 1;
+          mbar_wait(&w2_empty[wb], ((u >> 1) & 1) ^ 1);
+          mbar_expect_tx(&w2_full[wb], a.w2t_bytes);
+          bulk_load(sW2 + wb * a.w2t_bytes, a.w2t + (size_t)slot * a.w2t_bytes, a.w2t_bytes,
+                    &w2_full[wb]);
+          for (int hf = 0; hf < nh; ++hf) {
+            for (int kc = 0; kc < nkc; ++kc) {
+              mbar_wait(&empty[stage], sph ^ 1);
+              mbar_expect_tx(&full[stage], kBoxBytes);
+              tma_load_2d(sB + stage * kBoxBytes, &map_w, kc * kKC, slot * a.H + hf * kHalf,
+                          &full[stage]);
+              if (++stage == a.stages) {
+                stage = 0;
+                sph ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      const uint32_t id1 = idesc(kTileRows, kHalf, kFmtBF16);
+      const uint32_t id2 = idesc(kTileRows, a.C, kFmtBF16);
+      int stage = 0;
+      uint32_t sph = 0;
+      uint32_t u = 0, t = 0;
+      long prev = -1;  // pending layer-2 for sequence index prev (v = u * nh + hf)
+      auto layer2 = [&](uint32_t w) {
+        const uint32_t uw = w / nh, hw = w % nh;
+        const uint32_t rb = w & 1, lb = uw % a.nl, wb = uw & 1;
+        if (hw == 0) {
+          mbar_wait(&w2_full[wb], (uw >> 1) & 1);
+          mbar_wait(&l_empty[lb], ((uw / a.nl) & 1) ^ 1);
+        }
+        mbar_wait(&r_full[rb], (w >> 1) & 1);
+        tc_fence_after();
+        const uint32_t w2addr = smem_u32(sW2 + wb * a.w2t_bytes);
+#pragma unroll 1
+        for (int k16 = 0; k16 < kHalf / 16; ++k16) {
+          const int kg = hw * kHalf + k16 * 16;  // K index into H
+          const uint32_t baddr = w2addr + (kg / 64) * (a.C * 128) + (kg % 64) * 2;
+          mma_bf16_ts(tmem + kTmemL + lb * a.C, tmem + kTmemR + rb * 64 + k16 * 8,
+                      desc_kmajor_sw128(baddr), id2, (hw | k16) != 0);
+        }
+        mma_commit(&r_empty[rb]);
+        if (hw == (uint32_t)nh - 1) {
+          mma_commit(&l_full[lb]);
+          mma_commit(&w2_empty[wb]);
+        }
+      };
+      for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x, ++t) {
+        mbar_wait(&a_full, t & 1);
+        tc_fence_after();
+        const int e1 = tile_ent_end(a, m);
+        for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
+          for (int hf = 0; hf < nh; ++hf) {
+            const uint32_t v = u * nh + hf, zb = v & 1;
+            mbar_wait(&z_empty[zb], ((v >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (int kc = 0; kc < nkc; ++kc) {
+              mbar_wait(&full[stage], sph);
+              tc_fence_after();
+              const uint32_t aaddr = smem_u32(sA + kc * kAChunk);
+              const uint32_t baddr = smem_u32(sB + stage * kBoxBytes);
+#pragma unroll
+              for (int kk = 0; kk < kKC / 16; ++kk)
+                mma_bf16_ss(tmem + kTmemZ + zb * kHalf, desc_kmajor_sw128(aaddr + kk * 32),
+                            desc_kmajor_sw128(baddr + kk * 32), id1, (kc | kk) != 0);
+              mma_commit(&empty[stage]);
+              if (++stage == a.stages) {
+                stage = 0;
+                sph ^= 1;
+              }
+            }
+            mma_commit(&z_full[zb]);
+            if (prev >= 0) layer2((uint32_t)prev);
+            prev = v;
+          }
+        }
+        mma_commit(&a_empty);
+      }
+      if (prev >= 0) layer2((uint32_t)prev);
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue --
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const size_t fh = (size_t)a.F * a.H;
+    uint32_t u = 0;
+    for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x) {
+      const int R = m * kTileRows + row;
+      const bool valid = R < a.n_rows;
+      const int p = valid ? R / a.S : 0;
+      const int label = valid ? a.labels[(size_t)a.cams[p] * a.S + (R % a.S)] : -1;
+      const int pslot = (valid && a.probe_slot) ? a.probe_slot[p] : -1;
+      const int e1 = tile_ent_end(a, m);
+      for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
+        const int slot = a.ent_slot[e];
+        const float* W = a.wbase + (size_t)slot * a.wstride;
+        const float* b1 = W + fh;
+        for (int hf = 0; hf < nh; ++hf) {
+          const uint32_t v = u * nh + hf, zb = v & 1;
+          mbar_wait(&z_full[zb], (v >> 1) & 1);
+          mbar_wait(&r_empty[zb], ((v >> 1) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < kHalf; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0, r);
+            tmem_ld_wait();
+            const float4* bb = reinterpret_cast<const float4*>(b1 + hf * kHalf + c0);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const float4 b = __ldg(bb + i);
+              const float z0 = fmaxf(__uint_as_float(r[4 * i + 0]) + b.x, 0.0f);
+              const float z1 = fmaxf(__uint_as_float(r[4 * i + 1]) + b.y, 0.0f);
+              const float z2 = fmaxf(__uint_as_float(r[4 * i + 2]) + b.z, 0.0f);
+              const float z3 = fmaxf(__uint_as_float(r[4 * i + 3]) + b.w, 0.0f);
+              pk[2 * i] = pack_bf16x2(z0, z1);
+              pk[2 * i + 1] = pack_bf16x2(z2, z3);
+            }
+            tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2, pk);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&z_empty[zb]);
+            mbar_arrive(&r_full[zb]);
+          }
+        }
+        // logits of pair (tile row, entry e)
+        const uint32_t lb = u % a.nl;
+        mbar_wait(&l_full[lb], (u / a.nl) & 1);
+        tc_fence_after();
+        const float* b2 = b1 + a.H + (size_t)a.H * a.C;
+        int best = 0;
+        float bestv = 0.0f;
+        for (int c0 = 0; c0 < a.C; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tmem + lane_base + kTmemL + lb * a.C + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float l = __uint_as_float(r[i]) + __ldg(b2 + c0 + i);
+            if ((c0 | i) == 0 || l > bestv) {
+              bestv = l;
+              best = c0 + i;
+            }
+            if (a.dbg_logits && valid)
+              a.dbg_logits[((size_t)R * a.n_ent + e) * a.C + c0 + i] = l;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&l_empty[lb]);
+        const bool ok = valid && best == label && (pslot < 0 || pslot == slot);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0 && bal) {
+          const size_t idx = a.probe_slot ? (size_t)p : (size_t)p * a.ld + a.ent_col[e];
+          atomicAdd(a.counts + idx, __popc(bal));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// ------------------------------------------------------------ shadows ------
+// W1^T (bf16, [slot][H][F]) from the fp32 masters W1 [F][H]: 32x32 transpose.
+__global__ void k_shadow_w1t(int F, int H, const int* slots, const float* wbase, size_t wstride,
+                             uint16_t* w1t) {
+  __shared__ float t[32][33];
+  const int slot = slots[blockIdx.z];
+  const float* W1 = wbase + (size_t)slot * wstride;
+  const int f0 = blockIdx.x * 32, h0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y)
+    t[i][threadIdx.x] = W1[(size_t)(f0 + i) * H + h0 + threadIdx.x];
+  __syncthreads();
+  uint16_t* dst = w1t + (size_t)slot * H * F;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const float x = t[threadIdx.x][i];  // W1[f0 + tx][h0 + i]
+    const uint32_t pk = pack_bf16x2(x, 0.0f);
+    dst[(size_t)(h0 + i) * F + f0 + threadIdx.x] = (uint16_t)(pk & 0xFFFF);
+  }
+}
+
+// W2^T image: C rows x H (K) bf16, K-major, 128-byte swizzle atoms of 64 K
+// elements; atom kb of row n at kb*(C*128) + n*128, 16-byte chunk j of the
+// row stored at chunk j ^ (n % 8).
+__global__ void k_shadow_w2t(int F, int H, int C, const int* slots, const float* wbase,
+                             size_t wstride, uint8_t* w2t, uint32_t w2t_bytes) {
+  const int slot = slots[blockIdx.x];
+  const float* W2 = wbase + (size_t)slot * wstride + (size_t)F * H + H;
+  uint8_t* img = w2t + (size_t)slot * w2t_bytes;
+  for (int idx = threadIdx.x; idx < H * C; idx += blockDim.x) {
+    const int n = idx % C, k = idx / C;  // W2[k][n]
+    const int kb = k / 64, kw = k % 64;
+    const int chunk = (kw * 2) / 16, within = (kw * 2) % 16;
+    const size_t off = (size_t)kb * (C * 128) + n * 128 + ((chunk ^ (n & 7)) * 16) + within;
+    const uint32_t pk = pack_bf16x2(W2[(size_t)k * C + n], 0.0f);
+    *reinterpret_cast<uint16_t*>(img + off) = (uint16_t)(pk & 0xFFFF);
+  }
+}
+
+__global__ void k_counts_to_acc(size_t n, const int* counts, int S, const uint8_t* mask,
+                                double* out) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = (mask && !mask[i]) ? __longlong_as_double(0x7ff8000000000000LL)
+                              : __ddiv_rn((double)counts[i], (double)S);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    ECCO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess)
+      ecco_throw(ECCO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major [rows][cols] map with a {64, box_rows} box, 128-B swizzle.
+CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) ecco_throw(ECCO_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+int sm_count(int device) {
+  static int n = 0;
+  if (!n) ECCO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+  return n;
+}
+
+}  // namespace
+
+namespace fused {
+
+bool supported(const ecco_ctx* ctx) {
+  const ecco_config& g = ctx->cfg;
+  return g.feat_dim % 64 == 0 && g.feat_dim <= 512 && g.hidden_dim % kHalf == 0 &&
+         g.num_classes % 16 == 0 && g.num_classes <= 64 &&
+         (size_t)g.num_classes * g.hidden_dim * 2 <= 16384 && g.eval_samples % 64 == 0;
+}
+
+uint32_t w2t_bytes(const ecco_config& g) { return (uint32_t)g.num_classes * g.hidden_dim * 2; }
+
+void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
+                    const std::vector<int>& slots) {
+  if (slots.empty()) return;
+  const ecco_config& g = ctx->cfg;
+  int* d_sl = ctx->upload(10, slots.data(), slots.size());
+  const int n = (int)slots.size();
+  k_shadow_w1t<<<dim3(g.feat_dim / 32, g.hidden_dim / 32, n), dim3(32, 8), 0, ctx->stream>>>(
+      g.feat_dim, g.hidden_dim, d_sl, wbase, wstride, sh.w1t);
+  ECCO_LAUNCHED(ctx);
+  k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_sl, wbase,
+                                           wstride, sh.w2t, w2t_bytes(g));
+  ECCO_LAUNCHED(ctx);
+}
+
+void init_shadow(ecco_ctx* ctx, Shadow& sh) {
+  const ecco_config& g = ctx->cfg;
+  const size_t slots = g.max_jobs;
+  ECCO_CUDA(cudaMalloc((void**)&sh.w1t, slots * g.hidden_dim * g.feat_dim * 2));
+  ECCO_CUDA(cudaMalloc((void**)&sh.w2t, slots * w2t_bytes(g)));
+  sh.map_w = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, kHalf));
+}
+
+void free_shadow(Shadow& sh) {
+  if (sh.w1t) cudaFree(sh.w1t);
+  if (sh.w2t) cudaFree(sh.w2t);
+  delete (CUtensorMap*)sh.map_w;
+  sh = Shadow{};
+}
+
+void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wstride,
+                 int n_probes, const int* d_cams, int n_ent, const int* d_ent_slot,
+                 const int* d_ent_col, int n_tiles_override, const int* d_tile_ebeg,
+                 const int* d_probe_slot, int ld, int* d_counts, float* dbg_logits,
+                 double live_pairs) {
+  const ecco_config& g = ctx->cfg;
+  if (!ctx->map_x) ctx->map_x = new CUtensorMap(make_map(ctx->d_eval, (uint64_t)g.max_cameras * g.eval_samples,
+                                                         g.feat_dim, 64));
+  EvalArgs a{};
+  a.n_rows = n_probes * g.eval_samples;
+  a.S = g.eval_samples;
+  a.F = g.feat_dim;
+  a.H = g.hidden_dim;
+  a.C = g.num_classes;
+  a.n_tiles = n_tiles_override > 0 ? n_tiles_override : (a.n_rows + kTileRows - 1) / kTileRows;
+  a.cams = d_cams;
+  a.labels = ctx->d_eval_labels;
+  a.ent_slot = d_ent_slot;
+  a.ent_col = d_ent_col;
+  a.n_ent = n_ent;
+  a.tile_ebeg = d_tile_ebeg;
+  a.probe_slot = d_probe_slot;
+  a.ld = ld;
+  a.counts = d_counts;
+  a.wbase = wbase;
+  a.wstride = wstride;
+  a.w2t = sh.w2t;
+  a.w2t_bytes = w2t_bytes(g);
+  a.nl = 2 * g.num_classes <= 128 ? 2 : 1;
+  a.dbg_logits = dbg_logits;
+  const size_t fixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)a.w2t_bytes + 1024;
+  const size_t max_smem = 232448 - 1024;  // opt-in limit minus the static barriers
+  a.stages = (int)std::min<size_t>(kMaxStages, (max_smem - fixed) / kBoxBytes);
+  ECCO_REQUIRE(a.stages >= 2, "fused eval: shared memory too small for the pipeline");
+  const size_t smem = fixed + (size_t)a.stages * kBoxBytes;
+  static bool attr = false;
+  if (!attr) {
+    ECCO_CUDA(cudaFuncSetAttribute(k_eval_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)max_smem));
+    attr = true;
+  }
+  const int grid = std::min(a.n_tiles, sm_count(g.device));
+  if (a.n_tiles == 0 || n_ent == 0) return;
+  const double flops = 2.0 * live_pairs * g.eval_samples *
+                       ((double)g.feat_dim * g.hidden_dim + (double)g.hidden_dim * g.num_classes);
+  const double bytes = live_pairs * g.eval_samples * 0.0 + (double)a.n_rows * g.feat_dim * 2 +
+                       (double)n_ent * (g.feat_dim * g.hidden_dim * 2.0 + a.w2t_bytes) +
+                       4.0 * live_pairs;
+  ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_HIDDEN, flops, bytes,
+             (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
+                                                                  *(const CUtensorMap*)sh.map_w, a)));
+  ECCO_LAUNCHED(ctx);
+}
+
+void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* d_mask,
+                   double* d_out) {
+  if (!n) return;
+  k_counts_to_acc<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(
+      n, d_counts, ctx->cfg.eval_samples, d_mask, d_out);
+  ECCO_LAUNCHED(ctx);
+}
+
+}  // namespace fused

@@ -538,6 +538,47 @@ void init(ecco_ctx* ctx) {
   k_l_prototypes<<<nblk((size_t)g.C * g.F, 256), 256, 0, ctx->stream>>>(g, ctx->cfg.seed,
                                                                          ctx->d_proto_p, ctx->d_proto_q);
   ECCO_LAUNCHED(ctx);
+  // the tensor-core math evaluates through the fused kernel (eval_kernels.cu)
+  if (ctx->cfg.math == ECCO_MATH_TC_TF32 && fused::supported(ctx)) {
+    fused::init_shadow(ctx, ctx->sh_commit);
+    fused::init_shadow(ctx, ctx->sh_spec);
+    ctx->sh_dirty.assign(ctx->cfg.max_jobs, 1);
+    ctx->fused_eval = true;
+  }
+}
+
+// Refreshes the committed-model shadow for the dirty slots among `slots`.
+static void refresh_committed(ecco_ctx* ctx, const int* slots, int n) {
+  std::vector<int> todo;
+  for (int i = 0; i < n; ++i)
+    if (ctx->sh_dirty[slots[i]]) {
+      ctx->sh_dirty[slots[i]] = 0;
+      todo.push_back(slots[i]);
+    }
+  fused::refresh_shadow(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, todo);
+}
+
+// Fused pairs-mode counts: probe p = camera h_cam/d_cam[p] under slot
+// h_slot[p]; consecutive probes of one slot share 128-row tiles.
+static void pair_counts_fused(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wstride,
+                              int n_pairs, const int* h_slot, const int* d_slot, const int* d_cam,
+                              int* d_counts) {
+  const int S = ctx->cfg.eval_samples;
+  const int n_tiles = (int)(((size_t)n_pairs * S + 127) / 128);
+  std::vector<int> ebeg(n_tiles + 1), ent;
+  for (int m = 0; m < n_tiles; ++m) {
+    ebeg[m] = (int)ent.size();
+    const int p_lo = (int)((size_t)m * 128 / S);
+    const int p_hi = std::min(n_pairs, (int)(((size_t)m * 128 + 127) / S) + 1);
+    for (int p = p_lo; p < p_hi; ++p)
+      if (std::find(ent.begin() + ebeg[m], ent.end(), h_slot[p]) == ent.end()) ent.push_back(h_slot[p]);
+  }
+  ebeg[n_tiles] = (int)ent.size();
+  int* d_ent = ctx->upload(12, ent.data(), ent.size());
+  int* d_ebeg = ctx->upload(13, ebeg.data(), ebeg.size());
+  ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(n_pairs, 1), ctx->stream));
+  fused::eval_counts(ctx, sh, wbase, wstride, n_pairs, d_cam, (int)ent.size(), d_ent, d_ent,
+                     n_tiles, d_ebeg, d_slot, 0, d_counts, nullptr, (double)n_pairs);
 }
 
 void generate_frames(ecco_ctx* ctx, int window) {
@@ -618,8 +659,21 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
 }
 
 void eval_matrix(ecco_ctx* ctx, int n, const int* d_cams, int gj, const int* d_slots,
-                 const uint8_t* d_mask, double* d_out) {
+                 const uint8_t* d_mask, double* d_out, const int* h_slots) {
   if (n == 0 || gj == 0) return;
+  if (ctx->fused_eval && h_slots) {
+    // dense camera x group counts in one fused launch, then acc = count / S
+    refresh_committed(ctx, h_slots, gj);
+    std::vector<int> col(gj);
+    for (int j = 0; j < gj; ++j) col[j] = j;
+    int* d_col = ctx->upload(12, col.data(), gj);
+    int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * (size_t)n * gj);
+    ECCO_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int) * (size_t)n * gj, ctx->stream));
+    fused::eval_counts(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, n, d_cams, gj, d_slots, d_col,
+                       0, nullptr, nullptr, gj, d_cnt, nullptr, (double)n * gj);
+    fused::counts_to_acc(ctx, (size_t)n * gj, d_cnt, d_mask, d_out);
+    return;
+  }
   // host-side pair list (mask applied on the host copy when given)
   const size_t total = (size_t)n * gj;
   std::vector<int> slots(gj), cams(n);
@@ -656,8 +710,38 @@ void eval_matrix(ecco_ctx* ctx, int n, const int* d_cams, int gj, const int* d_s
   ECCO_LAUNCHED(ctx);
 }
 
-void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, double* d_out) {
+void debug_logits(ecco_ctx* ctx, int n, const int* h_cams, int gj, const int* h_slots,
+                  float* out) {
+  const LDims g = dims(ctx);
+  refresh_committed(ctx, h_slots, gj);
+  std::vector<int> col(gj);
+  for (int j = 0; j < gj; ++j) col[j] = j;
+  int* d_cams = ctx->upload(11, h_cams, n);
+  int* d_sl = ctx->upload(12, h_slots, gj);
+  int* d_col = ctx->upload(13, col.data(), gj);
+  const size_t nl = (size_t)n * g.S * gj * g.C;
+  DevBuf cnt, lg;
+  int* d_cnt = (int*)cnt.get(sizeof(int) * (size_t)n * gj);
+  float* d_lg = (float*)lg.get(sizeof(float) * nl);
+  ECCO_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int) * (size_t)n * gj, ctx->stream));
+  fused::eval_counts(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, n, d_cams, gj, d_sl, d_col, 0,
+                     nullptr, nullptr, gj, d_cnt, d_lg, (double)n * gj);
+  ECCO_CUDA(ctx_memcpy(ctx, out, d_lg, sizeof(float) * nl, cudaMemcpyDeviceToHost, ctx->stream));
+  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, double* d_out,
+                const int* h_slots) {
   if (n == 0) return;
+  if (ctx->fused_eval && h_slots) {
+    refresh_committed(ctx, h_slots, n);
+    int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * n);
+    pair_counts_fused(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, n, h_slots, d_slots, d_cams,
+                      d_cnt);
+    fused::counts_to_acc(ctx, (size_t)n, d_cnt, nullptr, d_out);
+    ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
   DevBuf cnt, idx;
   int* d_cnt = (int*)cnt.get(sizeof(int) * n);
   std::vector<int> po(n);
@@ -688,7 +772,8 @@ void route_propose(ecco_ctx* ctx, int n, const int* d_cams, const double* d_req,
 }
 
 static void member_pairs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_mem_off,
-                         const int* d_mem_cam, std::vector<int>& h_off, int** d_ps) {
+                         const int* d_mem_cam, std::vector<int>& h_off, int** d_ps,
+                         std::vector<int>* h_ps = nullptr) {
   h_off.resize(n_jobs + 1);
   std::vector<int> slots(n_jobs);
   ECCO_CUDA(ctx_memcpy(ctx, h_off.data(), d_mem_off, sizeof(int) * (n_jobs + 1), cudaMemcpyDeviceToHost, ctx->stream));
@@ -698,18 +783,25 @@ static void member_pairs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const in
   for (int j = 0; j < n_jobs; ++j)
     for (int m = h_off[j]; m < h_off[j + 1]; ++m) ps[m] = slots[j];
   *d_ps = ctx->upload(0, ps.data(), ps.size());
+  if (h_ps) *h_ps = std::move(ps);
   (void)d_mem_cam;
 }
 
 void eval_jobs(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_mem_off,
                const int* d_mem_cam, double* d_out) {
   if (n_jobs == 0) return;
-  std::vector<int> off;
+  std::vector<int> off, hps;
   int* d_ps = nullptr;
-  member_pairs(ctx, n_jobs, d_slots, d_mem_off, d_mem_cam, off, &d_ps);
+  member_pairs(ctx, n_jobs, d_slots, d_mem_off, d_mem_cam, off, &d_ps, &hps);
   const int np = off[n_jobs];
   int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * std::max(np, 1));
-  if (np) pair_counts(ctx, np, d_ps, d_mem_cam, d_cnt);
+  if (np && ctx->fused_eval) {
+    refresh_committed(ctx, hps.data(), np);
+    pair_counts_fused(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, np, hps.data(), d_ps, d_mem_cam,
+                      d_cnt);
+  } else if (np) {
+    pair_counts(ctx, np, d_ps, d_mem_cam, d_cnt);
+  }
   k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(dims(ctx), n_jobs, d_mem_off, d_cnt,
                                                             ctx->cfg.params.acc_floor, d_out, 1, 0);
   ECCO_LAUNCHED(ctx);
@@ -730,9 +822,9 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   for (int j = 0; j < n_jobs; ++j) max_steps = std::max(max_steps, h_steps[j]);
   int* d_steps = ctx->upload(1, h_steps, n_jobs);
   // member pairs for evaluate
-  std::vector<int> off;
+  std::vector<int> off, hps;
   int* d_ps = nullptr;
-  member_pairs(ctx, n_jobs, d_slots, d_mem_off, d_mem_cam, off, &d_ps);
+  member_pairs(ctx, n_jobs, d_slots, d_mem_off, d_mem_cam, off, &d_ps, &hps);
   const int n_mem = off[n_jobs];
   int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * std::max(n_mem, 1));
   // training scratch: rows = n_jobs * B
@@ -771,7 +863,13 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     ECCO_CUDA(ctx_memcpy(ctx, d_tiles, tiles.data(), sizeof(TcTile) * tiles.size(), cudaMemcpyHostToDevice, ctx->stream));
   }
   // acc[:, 0] from the committed models
-  if (n_mem) pair_counts(ctx, n_mem, d_ps, d_mem_cam, d_cnt);
+  if (n_mem && ctx->fused_eval) {
+    refresh_committed(ctx, hps.data(), n_mem);
+    pair_counts_fused(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, n_mem, hps.data(), d_ps,
+                      d_mem_cam, d_cnt);
+  } else if (n_mem) {
+    pair_counts(ctx, n_mem, d_ps, d_mem_cam, d_cnt);
+  }
   k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
                                                             ctx->cfg.params.acc_floor, d_out, depth + 1, 0);
   ECCO_LAUNCHED(ctx);
@@ -836,7 +934,17 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
           g, n_jobs, d_slots, d_steps, step, loss_rows, ctx->d_losses, T, t - 1);
       ECCO_LAUNCHED(ctx);
     }
-    // evaluate state t: temporarily point the pair evaluation at the snapshot
+    // evaluate state t
+    if (n_mem && ctx->fused_eval) {
+      fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots);
+      pair_counts_fused(ctx, ctx->sh_spec, wt, spec_stride, n_mem, hps.data(), d_ps, d_mem_cam,
+                        d_cnt);
+      k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
+                                                                ctx->cfg.params.acc_floor, d_out, depth + 1, t);
+      ECCO_LAUNCHED(ctx);
+      continue;
+    }
+    // (exact path) temporarily point the pair evaluation at the snapshot
     float* saved = ctx->d_w;
     const size_t saved_np = ctx->n_params;
     ctx->d_w = wt;
