@@ -46,7 +46,7 @@ namespace {
 constexpr int kTileRows = 128;
 constexpr int kKC = 64;               // K per TMA box / pipeline stage (one 128-B swizzle atom)
 constexpr int kHalf = 128;            // N of the hidden-layer MMA
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // 2 control warps + 8 epilogue warps
 constexpr uint32_t kBoxBytes = kHalf * 128;   // one W1^T stage: 128 rows x 64 bf16
 constexpr uint32_t kAChunk = kTileRows * 128; // one X K-chunk: 128 rows x 64 bf16
 constexpr int kMaxStages = 8;
@@ -71,7 +71,9 @@ struct EvalArgs {
   const float* wbase;    // fp32 masters: b1 at +F*H, b2 at +F*H+H+H*C
   size_t wstride;
   const uint8_t* w2t;    // per slot: W2^T bf16 K-major 128B-swizzled image
-  uint32_t w2t_bytes;
+  uint32_t w2t_bytes;    // W2^T part of the per-slot image
+  uint32_t img_bytes;    // whole image: W2^T | b1 (H fp32) | b2 (C fp32)
+  uint32_t img_stride;   // smem stride of the two image buffers (1024-aligned)
   int stages;
   int nl;                // logits buffers (1 or 2)
   float* dbg_logits;     // optional: [n_rows][n_ent][C] logits + b2 (dense mode tests)
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nh = a.H / kHalf;
   uint8_t* sA = smem;                                   // nkc x 16 KB
   uint8_t* sB = sA + nkc * kAChunk;                     // stages x 16 KB
-  uint8_t* sW2 = sB + a.stages * kBoxBytes;             // 2 x w2t_bytes
+  uint8_t* sW2 = sB + a.stages * kBoxBytes;             // 2 x img_stride
   __shared__ __align__(8) uint64_t a_full, a_empty;
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ __align__(8) uint64_t w2_full[2], w2_empty[2];
@@ -113,10 +115,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&w2_full[b], 1);
-      mbar_init(&w2_empty[b], 1);
+      mbar_init(&w2_empty[b], 1 + 4);  // MMA commit + the 4 logits warps
       mbar_init(&z_full[b], 1);
-      mbar_init(&z_empty[b], 4);
-      mbar_init(&r_full[b], 4);
+      mbar_init(&z_empty[b], 8);
+      mbar_init(&r_full[b], 8);
       mbar_init(&r_empty[b], 1);
       mbar_init(&l_full[b], 1);
       mbar_init(&l_empty[b], 4);
@@ -131,12 +133,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t sph = 0;
-      uint32_t u = 0, t = 0;
-      for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x, ++t) {
-        if (t > 0) mbar_wait(&a_empty, (t - 1) & 1);
+    // (whole warp walks the schedule; one elected lane issues)
+    int stage = 0;
+    uint32_t sph = 0;
+    uint32_t u = 0, t = 0;
+    for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x, ++t) {
+      if (t > 0) mbar_wait(&a_empty, (t - 1) & 1);
+      if (elect_one()) {
         mbar_expect_tx(&a_full, (uint32_t)nkc * kAChunk);
         for (int h2 = 0; h2 < 2; ++h2) {
           int b = m * 2 + h2;
@@ -146,24 +149,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kc = 0; kc < nkc; ++kc)
             tma_load_2d(sA + kc * kAChunk + h2 * (kAChunk / 2), &map_x, kc * kKC, row, &a_full);
         }
-        const int e1 = tile_ent_end(a, m);
-        for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
-          const int slot = a.ent_slot[e];
-          const int wb = u & 1;
-          mbar_wait(&w2_empty[wb], ((u >> 1) & 1) ^ 1);
-          mbar_expect_tx(&w2_full[wb], a.w2t_bytes);
-          bulk_load(sW2 + wb * a.w2t_bytes, a.w2t + (size_t)slot * a.w2t_bytes, a.w2t_bytes,
+      }
+      __syncwarp();
+      const int e1 = tile_ent_end(a, m);
+      for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
+        const int slot = a.ent_slot[e];
+        const int wb = u & 1;
+        mbar_wait(&w2_empty[wb], ((u >> 1) & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(&w2_full[wb], a.img_bytes);
+          bulk_load(sW2 + wb * a.img_stride, a.w2t + (size_t)slot * a.img_bytes, a.img_bytes,
                     &w2_full[wb]);
-          for (int hf = 0; hf < nh; ++hf) {
-            for (int kc = 0; kc < nkc; ++kc) {
-              mbar_wait(&empty[stage], sph ^ 1);
+        }
+        __syncwarp();
+        for (int hf = 0; hf < nh; ++hf) {
+          for (int kc = 0; kc < nkc; ++kc) {
+            mbar_wait(&empty[stage], sph ^ 1);
+            if (elect_one()) {
               mbar_expect_tx(&full[stage], kBoxBytes);
               tma_load_2d(sB + stage * kBoxBytes, &map_w, kc * kKC, slot * a.H + hf * kHalf,
                           &full[stage]);
-              if (++stage == a.stages) {
-                stage = 0;
-                sph ^= 1;
-              }
+            }
+            __syncwarp();
+            if (++stage == a.stages) {
+              stage = 0;
+              sph ^= 1;
             }
           }
         }
@@ -171,75 +181,88 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
-      const uint32_t id1 = idesc(kTileRows, kHalf, kFmtBF16);
-      const uint32_t id2 = idesc(kTileRows, a.C, kFmtBF16);
-      int stage = 0;
-      uint32_t sph = 0;
-      uint32_t u = 0, t = 0;
-      long prev = -1;  // pending layer-2 for sequence index prev (v = u * nh + hf)
-      auto layer2 = [&](uint32_t w) {
-        const uint32_t uw = w / nh, hw = w % nh;
-        const uint32_t rb = w & 1, lb = uw % a.nl, wb = uw & 1;
-        if (hw == 0) {
-          mbar_wait(&w2_full[wb], (uw >> 1) & 1);
-          mbar_wait(&l_empty[lb], ((uw / a.nl) & 1) ^ 1);
-        }
-        mbar_wait(&r_full[rb], (w >> 1) & 1);
-        tc_fence_after();
-        const uint32_t w2addr = smem_u32(sW2 + wb * a.w2t_bytes);
-#pragma unroll 1
+    // Descriptors are built once; K steps and pipeline stages only add their
+    // byte offset (>> 4) to the start-address field.
+    const uint32_t id1 = idesc(kTileRows, kHalf, kFmtBF16);
+    const uint32_t id2 = idesc(kTileRows, a.C, kFmtBF16);
+    const uint64_t dA0 = desc_kmajor_sw128(smem_u32(sA));
+    const uint64_t dB0 = desc_kmajor_sw128(smem_u32(sB));
+    const uint64_t dW0 = desc_kmajor_sw128(smem_u32(sW2));
+    int stage = 0;
+    uint32_t sph = 0;
+    uint32_t u = 0, t = 0;
+    long prev = -1;  // pending layer-2 for sequence index prev (v = u * nh + hf)
+    auto layer2 = [&](uint32_t w) {
+      const uint32_t uw = w / nh, hw = w % nh;
+      const uint32_t rb = w & 1, lb = uw % a.nl, wb = uw & 1;
+      if (hw == 0) {
+        mbar_wait(&w2_full[wb], (uw >> 1) & 1);
+        mbar_wait(&l_empty[lb], ((uw / a.nl) & 1) ^ 1);
+      }
+      mbar_wait(&r_full[rb], (w >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t dW = dW0 + ((wb * a.img_stride) >> 4);
+#pragma unroll
         for (int k16 = 0; k16 < kHalf / 16; ++k16) {
           const int kg = hw * kHalf + k16 * 16;  // K index into H
-          const uint32_t baddr = w2addr + (kg / 64) * (a.C * 128) + (kg % 64) * 2;
           mma_bf16_ts(tmem + kTmemL + lb * a.C, tmem + kTmemR + rb * 64 + k16 * 8,
-                      desc_kmajor_sw128(baddr), id2, (hw | k16) != 0);
+                      dW + (((kg / 64) * (a.C * 128) + (kg % 64) * 2) >> 4), id2,
+                      (hw | k16) != 0);
         }
         mma_commit(&r_empty[rb]);
         if (hw == (uint32_t)nh - 1) {
           mma_commit(&l_full[lb]);
           mma_commit(&w2_empty[wb]);
         }
-      };
-      for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x, ++t) {
-        mbar_wait(&a_full, t & 1);
-        tc_fence_after();
-        const int e1 = tile_ent_end(a, m);
-        for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
-          for (int hf = 0; hf < nh; ++hf) {
-            const uint32_t v = u * nh + hf, zb = v & 1;
-            mbar_wait(&z_empty[zb], ((v >> 1) & 1) ^ 1);
+      }
+      __syncwarp();
+    };
+    for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x, ++t) {
+      mbar_wait(&a_full, t & 1);
+      tc_fence_after();
+      const int e1 = tile_ent_end(a, m);
+      for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
+        for (int hf = 0; hf < nh; ++hf) {
+          const uint32_t v = u * nh + hf, zb = v & 1;
+          mbar_wait(&z_empty[zb], ((v >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t dz = tmem + kTmemZ + zb * kHalf;
+          for (int kc = 0; kc < nkc; ++kc) {
+            mbar_wait(&full[stage], sph);
             tc_fence_after();
-            for (int kc = 0; kc < nkc; ++kc) {
-              mbar_wait(&full[stage], sph);
-              tc_fence_after();
-              const uint32_t aaddr = smem_u32(sA + kc * kAChunk);
-              const uint32_t baddr = smem_u32(sB + stage * kBoxBytes);
+            if (elect_one()) {
+              const uint64_t da = dA0 + ((kc * kAChunk) >> 4);
+              const uint64_t db = dB0 + ((stage * kBoxBytes) >> 4);
 #pragma unroll
               for (int kk = 0; kk < kKC / 16; ++kk)
-                mma_bf16_ss(tmem + kTmemZ + zb * kHalf, desc_kmajor_sw128(aaddr + kk * 32),
-                            desc_kmajor_sw128(baddr + kk * 32), id1, (kc | kk) != 0);
+                mma_bf16_ss(dz, da + kk * 2, db + kk * 2, id1, (kc | kk) != 0);
               mma_commit(&empty[stage]);
-              if (++stage == a.stages) {
-                stage = 0;
-                sph ^= 1;
-              }
             }
-            mma_commit(&z_full[zb]);
-            if (prev >= 0) layer2((uint32_t)prev);
-            prev = v;
+            __syncwarp();
+            if (++stage == a.stages) {
+              stage = 0;
+              sph ^= 1;
+            }
           }
+          if (elect_one()) mma_commit(&z_full[zb]);
+          __syncwarp();
+          if (prev >= 0) layer2((uint32_t)prev);
+          prev = v;
         }
-        mma_commit(&a_empty);
       }
-      if (prev >= 0) layer2((uint32_t)prev);
+      if (elect_one()) mma_commit(&a_empty);
+      __syncwarp();
     }
+    if (prev >= 0) layer2((uint32_t)prev);
   } else {
     // ----------------------------------------------------------- epilogue --
+    // 8 warps: two per TMEM lane quadrant, each converting 64 of a half's
+    // 128 Z columns; the cp == 0 warp of each quadrant also reads the logits.
     const int q = warp & 3;
+    const int cp = (warp - 2) >> 2;
     const int row = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    const size_t fh = (size_t)a.F * a.H;
     uint32_t u = 0;
     for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x) {
       const int R = m * kTileRows + row;
@@ -249,33 +272,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int pslot = (valid && a.probe_slot) ? a.probe_slot[p] : -1;
       const int e1 = tile_ent_end(a, m);
       for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
-        const int slot = a.ent_slot[e];
-        const float* W = a.wbase + (size_t)slot * a.wstride;
-        const float* b1 = W + fh;
+        const uint32_t wb = u & 1;
+        const uint8_t* img = sW2 + wb * a.img_stride;
+        const float* b1 = reinterpret_cast<const float*>(img + a.w2t_bytes);
+        const float* b2 = b1 + a.H;
+        mbar_wait(&w2_full[wb], (u >> 1) & 1);  // b1 / b2 of this model are in smem
         for (int hf = 0; hf < nh; ++hf) {
           const uint32_t v = u * nh + hf, zb = v & 1;
+          const int c0 = cp * 64;
           mbar_wait(&z_full[zb], (v >> 1) & 1);
           mbar_wait(&r_empty[zb], ((v >> 1) & 1) ^ 1);
           tc_fence_after();
-#pragma unroll 1
-          for (int c0 = 0; c0 < kHalf; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0, r);
-            tmem_ld_wait();
-            const float4* bb = reinterpret_cast<const float4*>(b1 + hf * kHalf + c0);
-            uint32_t pk[16];
+          uint32_t r[64];
+          tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0, r);
+          tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0 + 32, r + 32);
+          tmem_ld_wait();
+          const float4* bb = reinterpret_cast<const float4*>(b1 + hf * kHalf + c0);
+          uint32_t pk[32];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 b = __ldg(bb + i);
-              const float z0 = fmaxf(__uint_as_float(r[4 * i + 0]) + b.x, 0.0f);
-              const float z1 = fmaxf(__uint_as_float(r[4 * i + 1]) + b.y, 0.0f);
-              const float z2 = fmaxf(__uint_as_float(r[4 * i + 2]) + b.z, 0.0f);
-              const float z3 = fmaxf(__uint_as_float(r[4 * i + 3]) + b.w, 0.0f);
-              pk[2 * i] = pack_bf16x2(z0, z1);
-              pk[2 * i + 1] = pack_bf16x2(z2, z3);
-            }
-            tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2, pk);
+          for (int i = 0; i < 16; ++i) {
+            const float4 b = bb[i];
+            const float z0 = fmaxf(__uint_as_float(r[4 * i + 0]) + b.x, 0.0f);
+            const float z1 = fmaxf(__uint_as_float(r[4 * i + 1]) + b.y, 0.0f);
+            const float z2 = fmaxf(__uint_as_float(r[4 * i + 2]) + b.z, 0.0f);
+            const float z3 = fmaxf(__uint_as_float(r[4 * i + 3]) + b.w, 0.0f);
+            pk[2 * i] = pack_bf16x2(z0, z1);
+            pk[2 * i + 1] = pack_bf16x2(z2, z3);
           }
+          tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2, pk);
+          tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2 + 16, pk + 16);
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
@@ -284,11 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&r_full[zb]);
           }
         }
+        if (cp != 0) continue;
         // logits of pair (tile row, entry e)
+        const int slot = a.ent_slot[e];
         const uint32_t lb = u % a.nl;
         mbar_wait(&l_full[lb], (u / a.nl) & 1);
         tc_fence_after();
-        const float* b2 = b1 + a.H + (size_t)a.H * a.C;
         int best = 0;
         float bestv = 0.0f;
         for (int c0 = 0; c0 < a.C; c0 += 16) {
@@ -297,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float l = __uint_as_float(r[i]) + __ldg(b2 + c0 + i);
+            const float l = __uint_as_float(r[i]) + b2[c0 + i];
             if ((c0 | i) == 0 || l > bestv) {
               bestv = l;
               best = c0 + i;
@@ -308,7 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&l_empty[lb]);
+        if (lane == 0) {
+          mbar_arrive(&l_empty[lb]);
+          mbar_arrive(&w2_empty[wb]);  // b2 (and b1) of this buffer no longer read
+        }
         const bool ok = valid && best == label && (pslot < 0 || pslot == slot);
         const unsigned bal = __ballot_sync(0xffffffffu, ok);
         if (lane == 0 && bal) {
@@ -346,10 +375,15 @@ __global__ void k_shadow_w1t(int F, int H, const int* slots, const float* wbase,
 // elements; atom kb of row n at kb*(C*128) + n*128, 16-byte chunk j of the
 // row stored at chunk j ^ (n % 8).
 __global__ void k_shadow_w2t(int F, int H, int C, const int* slots, const float* wbase,
-                             size_t wstride, uint8_t* w2t, uint32_t w2t_bytes) {
+                             size_t wstride, uint8_t* w2t, uint32_t img_bytes) {
   const int slot = slots[blockIdx.x];
-  const float* W2 = wbase + (size_t)slot * wstride + (size_t)F * H + H;
-  uint8_t* img = w2t + (size_t)slot * w2t_bytes;
+  const float* b1 = wbase + (size_t)slot * wstride + (size_t)F * H;
+  const float* W2 = b1 + H;
+  const float* b2 = W2 + (size_t)H * C;
+  uint8_t* img = w2t + (size_t)slot * img_bytes;
+  float* ib = reinterpret_cast<float*>(img + (size_t)C * H * 2);
+  for (int i = threadIdx.x; i < H; i += blockDim.x) ib[i] = b1[i];
+  for (int i = threadIdx.x; i < C; i += blockDim.x) ib[H + i] = b2[i];
   for (int idx = threadIdx.x; idx < H * C; idx += blockDim.x) {
     const int n = idx % C, k = idx / C;  // W2[k][n]
     const int kb = k / 64, kw = k % 64;
@@ -406,14 +440,19 @@ int sm_count(int device) {
 
 namespace fused {
 
+uint32_t w2t_bytes(const ecco_config& g) { return (uint32_t)g.num_classes * g.hidden_dim * 2; }
+uint32_t img_bytes(const ecco_config& g) {
+  return (w2t_bytes(g) + 4u * (g.hidden_dim + g.num_classes) + 15u) & ~15u;
+}
+
 bool supported(const ecco_ctx* ctx) {
   const ecco_config& g = ctx->cfg;
   return g.feat_dim % 64 == 0 && g.feat_dim <= 512 && g.hidden_dim % kHalf == 0 &&
          g.num_classes % 16 == 0 && g.num_classes <= 64 &&
-         (size_t)g.num_classes * g.hidden_dim * 2 <= 16384 && g.eval_samples % 64 == 0;
+         (size_t)g.num_classes * g.hidden_dim * 2 <= 16384 && g.eval_samples % 64 == 0 &&
+         g.feat_dim / 64 * 16384 + 2 * ((img_bytes(g) + 1023) / 1024 * 1024) + 1024 + 2 * 16384 <= 231424;
 }
 
-uint32_t w2t_bytes(const ecco_config& g) { return (uint32_t)g.num_classes * g.hidden_dim * 2; }
 
 void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
                     const std::vector<int>& slots) {
@@ -425,7 +464,7 @@ void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstrid
       g.feat_dim, g.hidden_dim, d_sl, wbase, wstride, sh.w1t);
   ECCO_LAUNCHED(ctx);
   k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_sl, wbase,
-                                           wstride, sh.w2t, w2t_bytes(g));
+                                           wstride, sh.w2t, img_bytes(g));
   ECCO_LAUNCHED(ctx);
 }
 
@@ -433,7 +472,7 @@ void init_shadow(ecco_ctx* ctx, Shadow& sh) {
   const ecco_config& g = ctx->cfg;
   const size_t slots = g.max_jobs;
   ECCO_CUDA(cudaMalloc((void**)&sh.w1t, slots * g.hidden_dim * g.feat_dim * 2));
-  ECCO_CUDA(cudaMalloc((void**)&sh.w2t, slots * w2t_bytes(g)));
+  ECCO_CUDA(cudaMalloc((void**)&sh.w2t, slots * img_bytes(g)));
   sh.map_w = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, kHalf));
 }
 
@@ -472,9 +511,11 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
   a.wstride = wstride;
   a.w2t = sh.w2t;
   a.w2t_bytes = w2t_bytes(g);
+  a.img_bytes = img_bytes(g);
+  a.img_stride = (a.img_bytes + 1023u) & ~1023u;
   a.nl = 2 * g.num_classes <= 128 ? 2 : 1;
   a.dbg_logits = dbg_logits;
-  const size_t fixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)a.w2t_bytes + 1024;
+  const size_t fixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)a.img_stride + 1024;
   const size_t max_smem = 232448 - 1024;  // opt-in limit minus the static barriers
   a.stages = (int)std::min<size_t>(kMaxStages, (max_smem - fixed) / kBoxBytes);
   ECCO_REQUIRE(a.stages >= 2, "fused eval: shared memory too small for the pipeline");
