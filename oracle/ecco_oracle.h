@@ -3,9 +3,10 @@
  *
  * A plain-C restatement of the reference's group-retraining arithmetic
  * (parametric backend: every function cites the reference file:line it
- * follows) and the specification of the learned backend (no reference
- * counterpart; parity there is pinned to this restatement only, see
- * DESIGN.md).  Only tests/, __graft_entry__.smoke() and bench.py's
+ * follows) and the specification of the learned backend.  The learned
+ * backend has no reference counterpart: its parity is UNPINNED by the
+ * reference ("parity unpinned") -- this restatement is
+ * its specification.  Only tests/, __graft_entry__.smoke() and bench.py's
  * cpu_baseline / reference legs may load it.  The product never does.
  */
 #ifndef ECCO_ORACLE_H_
