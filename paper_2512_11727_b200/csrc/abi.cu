@@ -42,6 +42,7 @@ void free_all(ecco_ctx* c) {
   fused::free_shadow(c->sh_spec);
   delete (CUtensorMap*)c->map_x;
   for (auto& b : c->scratch) b.release();
+  for (auto& b : c->train_scratch) b.release();
   for (auto& b : c->hscratch) b.release();
   if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -414,11 +415,16 @@ ecco_status ecco_get_weights(ecco_ctx* ctx, int job_id, float* w1, float* b1, fl
     const ecco_config& g = ctx->cfg;
     const size_t F = g.feat_dim, H = g.hidden_dim, C = g.num_classes;
     const float* base = ctx->d_w + (size_t)ctx->slot(job_id) * ctx->n_params;
-    ECCO_CUDA(ctx_memcpy(ctx, w1, base, F * H * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    std::vector<float> tmp(ctx->w1_t ? F * H : 0);
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->w1_t ? tmp.data() : w1, base, F * H * 4, cudaMemcpyDeviceToHost,
+                         ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, b1, base + F * H, H * 4, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, w2, base + F * H + H, H * C * 4, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, b2, base + F * H + H + H * C, C * 4, cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->w1_t)  // [H][F] -> API layout W1[F][H]
+      for (size_t h = 0; h < H; ++h)
+        for (size_t f = 0; f < F; ++f) w1[f * H + h] = tmp[h * F + f];
   });
 }
 
@@ -431,6 +437,13 @@ ecco_status ecco_set_weights(ecco_ctx* ctx, int job_id, const float* w1, const f
     const int slot = ctx->alloc_slot(job_id);
     ctx->mark_dirty(slot);
     float* base = ctx->d_w + (size_t)slot * ctx->n_params;
+    std::vector<float> tmp;
+    if (ctx->w1_t) {  // API layout W1[F][H] -> [H][F]
+      tmp.resize(F * H);
+      for (size_t f = 0; f < F; ++f)
+        for (size_t h = 0; h < H; ++h) tmp[h * F + f] = w1[f * H + h];
+      w1 = tmp.data();
+    }
     ECCO_CUDA(ctx_memcpy(ctx, base, w1, F * H * 4, cudaMemcpyHostToDevice, ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, base + F * H, b1, H * 4, cudaMemcpyHostToDevice, ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, base + F * H + H, w2, H * C * 4, cudaMemcpyHostToDevice, ctx->stream));

@@ -98,7 +98,8 @@ struct KStat {
 struct Shadow {
   uint16_t* w1t = nullptr;
   uint8_t* w2t = nullptr;
-  void* map_w = nullptr;  // CUtensorMap*
+  void* map_w = nullptr;        // CUtensorMap*, {64, 128} boxes (evaluation)
+  void* map_w_train = nullptr;  // CUtensorMap*, {64, H} boxes (fused SGD step)
 };
 
 struct ecco_ctx {
@@ -177,6 +178,11 @@ struct ecco_ctx {
   // fused evaluation: shadows of the committed models (refreshed lazily for
   // slots marked dirty) and of the speculative snapshot being evaluated
   bool fused_eval = false;
+  bool fused_train = false;
+  // fused mode keeps the fp32 W1 masters transposed, [slot][H][F], so the
+  // fused SGD update reads and writes them coalesced; ecco_get/set_weights
+  // translate to the API layout W1[F][H]
+  bool w1_t = false;
   Shadow sh_commit, sh_spec;
   std::vector<char> sh_dirty;
   void* map_x = nullptr;  // CUtensorMap* over d_eval
@@ -184,7 +190,8 @@ struct ecco_ctx {
     if (slot >= 0 && slot < (int)sh_dirty.size()) sh_dirty[slot] = 1;
   }
 
-  DevBuf scratch[16];  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
+  DevBuf scratch[16];
+  DevBuf train_scratch[8];  // unfused training rows (learned_kernels.cu)  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
   HostBuf hscratch[4];
 
   int slot(int job_id) const {
@@ -285,6 +292,14 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
                  double live_pairs);
 void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* d_mask,
                    double* d_out);
+bool train_supported(const ecco_ctx* ctx);
+// One fused SGD step (sample, gather, fwd, head, bwd, update) for every job
+// whose step budget is not spent; W1^T shadow `sh` kept in sync.
+void train_step(ecco_ctx* ctx, const Shadow& sh, int n_jobs, const int* d_slots,
+                const int* d_job_ids, const int* d_steps, const int* d_src_off,
+                const int* d_src_cam, const double* d_src_frac, const int* d_micro_base,
+                int micro_add, int window, int step, float* wbase, size_t wstride, int loss_t,
+                double live_rows);
 }  // namespace fused
 
 namespace lbackend {

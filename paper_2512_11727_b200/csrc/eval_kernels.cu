@@ -355,11 +355,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------ shadows ------
 // W1^T (bf16, [slot][H][F]) from the fp32 masters W1 [F][H]: 32x32 transpose.
 __global__ void k_shadow_w1t(int F, int H, const int* slots, const float* wbase, size_t wstride,
-                             uint16_t* w1t) {
+                             uint16_t* w1t, bool w1_t) {
   __shared__ float t[32][33];
   const int slot = slots[blockIdx.z];
   const float* W1 = wbase + (size_t)slot * wstride;
   const int f0 = blockIdx.x * 32, h0 = blockIdx.y * 32;
+  if (w1_t) {  // masters already [H][F]: convert in place order
+    uint16_t* dst = w1t + (size_t)slot * H * F;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const size_t o = (size_t)(h0 + i) * F + f0 + threadIdx.x;
+      dst[o] = (uint16_t)(pack_bf16x2(W1[o], 0.0f) & 0xFFFF);
+    }
+    return;
+  }
   for (int i = threadIdx.y; i < 32; i += blockDim.y)
     t[i][threadIdx.x] = W1[(size_t)(f0 + i) * H + h0 + threadIdx.x];
   __syncthreads();
@@ -461,7 +469,7 @@ void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstrid
   int* d_sl = ctx->upload(10, slots.data(), slots.size());
   const int n = (int)slots.size();
   k_shadow_w1t<<<dim3(g.feat_dim / 32, g.hidden_dim / 32, n), dim3(32, 8), 0, ctx->stream>>>(
-      g.feat_dim, g.hidden_dim, d_sl, wbase, wstride, sh.w1t);
+      g.feat_dim, g.hidden_dim, d_sl, wbase, wstride, sh.w1t, ctx->w1_t);
   ECCO_LAUNCHED(ctx);
   k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_sl, wbase,
                                            wstride, sh.w2t, img_bytes(g));
@@ -474,12 +482,15 @@ void init_shadow(ecco_ctx* ctx, Shadow& sh) {
   ECCO_CUDA(cudaMalloc((void**)&sh.w1t, slots * g.hidden_dim * g.feat_dim * 2));
   ECCO_CUDA(cudaMalloc((void**)&sh.w2t, slots * img_bytes(g)));
   sh.map_w = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, kHalf));
+  if (g.hidden_dim <= 256)
+    sh.map_w_train = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, g.hidden_dim));
 }
 
 void free_shadow(Shadow& sh) {
   if (sh.w1t) cudaFree(sh.w1t);
   if (sh.w2t) cudaFree(sh.w2t);
   delete (CUtensorMap*)sh.map_w;
+  delete (CUtensorMap*)sh.map_w_train;
   sh = Shadow{};
 }
 

@@ -56,3 +56,43 @@ __device__ __forceinline__ float ecco_expf(float x) {
   const int ki = (int)k;
   return __fmul_rn(q, __uint_as_float((uint32_t)(ki + 127) << 23));
 }
+
+// Shapes of the learned backend (ecco_config).
+struct LDims {
+  int F, H, C, D, B, R, S;
+  float lr, noise;
+};
+
+
+__device__ __forceinline__ void seed_key(uint64_t seed, uint32_t salt, uint32_t& k0,
+                                         uint32_t& k1) {
+  k0 = (uint32_t)seed ^ salt;
+  k1 = (uint32_t)(seed >> 32);
+}
+
+
+// Rows of one (job, step) minibatch: source by the cumulative source_mix in
+// map order, frame uniform in the ring.  Writes the element offset of the
+// row in the frame table and its label.
+__device__ __forceinline__ void sample_one(const LDims& g, uint64_t seed, int job_id, int n_src,
+                                           const int* src_cam, const double* src_frac,
+                                           int window, int micro, int step, int s, int* cam_out,
+                                           int* frame_out) {
+  uint32_t k0, k1, out[4];
+  seed_key(seed, (uint32_t)job_id * 0x9E3779B9u + 0x632BE5ABu, k0, k1);
+  const uint32_t wt = ((uint32_t)window & 0xFFFFFFu) | (2u << 24);
+  philox4x32((uint32_t)s, (uint32_t)step, (uint32_t)micro, wt, k0, k1, out);
+  const double u = __dmul_rn((double)(((uint64_t)out[0] << 21) | (out[1] >> 11)), 0x1p-53);
+  double cum = 0.0;
+  int pick = n_src - 1;
+  for (int i = 0; i < n_src; ++i) {
+    cum = __dadd_rn(cum, src_frac[i]);
+    if (u < cum) {
+      pick = i;
+      break;
+    }
+  }
+  *cam_out = src_cam[pick];
+  *frame_out = (int)(out[2] % (uint32_t)g.R);
+}
+

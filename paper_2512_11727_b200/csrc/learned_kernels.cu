@@ -19,21 +19,10 @@
 
 namespace {
 
-struct LDims {
-  int F, H, C, D, B, R, S;
-  float lr, noise;
-};
-
 LDims dims(const ecco_ctx* c) {
   return {c->cfg.feat_dim,  c->cfg.hidden_dim,  c->cfg.num_classes, c->cfg.scene_dims,
           c->cfg.minibatch, c->cfg.ring_frames, c->cfg.eval_samples, c->cfg.sgd_lr,
           c->cfg.feature_noise};
-}
-
-__device__ __forceinline__ void seed_key(uint64_t seed, uint32_t salt, uint32_t& k0,
-                                         uint32_t& k1) {
-  k0 = (uint32_t)seed ^ salt;
-  k1 = (uint32_t)(seed >> 32);
 }
 
 // ---------------------------------------------------------------- streams --
@@ -95,7 +84,7 @@ __global__ void __launch_bounds__(256) k_l_gen_frames(LDims g, uint64_t seed, in
 
 // Base model (orc_init_weights): every new job starts from it.
 __global__ void k_l_init_weights(LDims g, uint64_t seed, int n, const int* slots, float* w,
-                                 size_t n_params) {
+                                 size_t n_params, bool w1_t) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)n * n_params) return;
   const int j = (int)(idx / n_params);
@@ -115,35 +104,12 @@ __global__ void k_l_init_weights(LDims g, uint64_t seed, int n, const int* slots
     philox4x32((uint32_t)c, (uint32_t)k, 2u, 3u << 24, k0, k1, out);
     v = __fmul_rn(usym(out[0]), __fsqrt_rn(__fdiv_rn(6.0f, (float)g.H)));
   }
-  w[(size_t)slots[j] * n_params + q] = v;
+  size_t dst = q;
+  if (w1_t && q < fh) dst = (q % g.H) * (size_t)g.F + q / g.H;  // W1 stored [H][F]
+  w[(size_t)slots[j] * n_params + dst] = v;
 }
 
 // ------------------------------------------------------------- sampler --
-
-// Rows of one (job, step) minibatch: source by the cumulative source_mix in
-// map order, frame uniform in the ring.  Writes the element offset of the
-// row in the frame table and its label.
-__device__ __forceinline__ void sample_one(const LDims& g, uint64_t seed, int job_id, int n_src,
-                                           const int* src_cam, const double* src_frac,
-                                           int window, int micro, int step, int s, int* cam_out,
-                                           int* frame_out) {
-  uint32_t k0, k1, out[4];
-  seed_key(seed, (uint32_t)job_id * 0x9E3779B9u + 0x632BE5ABu, k0, k1);
-  const uint32_t wt = ((uint32_t)window & 0xFFFFFFu) | (2u << 24);
-  philox4x32((uint32_t)s, (uint32_t)step, (uint32_t)micro, wt, k0, k1, out);
-  const double u = __dmul_rn((double)(((uint64_t)out[0] << 21) | (out[1] >> 11)), 0x1p-53);
-  double cum = 0.0;
-  int pick = n_src - 1;
-  for (int i = 0; i < n_src; ++i) {
-    cum = __dadd_rn(cum, src_frac[i]);
-    if (u < cum) {
-      pick = i;
-      break;
-    }
-  }
-  *cam_out = src_cam[pick];
-  *frame_out = (int)(out[2] % (uint32_t)g.R);
-}
 
 __global__ void k_l_sample(LDims g, uint64_t seed, int n_jobs, const int* job_ids,
                            const int* steps, const int* src_off, const int* src_cam,
@@ -544,6 +510,8 @@ void init(ecco_ctx* ctx) {
     fused::init_shadow(ctx, ctx->sh_spec);
     ctx->sh_dirty.assign(ctx->cfg.max_jobs, 1);
     ctx->fused_eval = true;
+    ctx->fused_train = fused::train_supported(ctx);
+    ctx->w1_t = ctx->fused_train;
   }
 }
 
@@ -603,7 +571,7 @@ void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const 
   if (n == 0) return;
   const LDims g = dims(ctx);
   k_l_init_weights<<<nblk((size_t)n * ctx->n_params, 256), 256, 0, ctx->stream>>>(
-      g, ctx->cfg.seed, n, d_slots, ctx->d_w, ctx->n_params);
+      g, ctx->cfg.seed, n, d_slots, ctx->d_w, ctx->n_params, ctx->w1_t);
   ECCO_LAUNCHED(ctx);
 }
 
@@ -828,31 +796,33 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   const int n_mem = off[n_jobs];
   int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * std::max(n_mem, 1));
   // training scratch: rows = n_jobs * B
-  const int rows = n_jobs * g.B;
+  // (the fused step keeps everything on chip: no row scratch)
+  const int rows = ctx->fused_train ? 0 : n_jobs * g.B;
   const int nb = rows / kRB;
-  DevBuf b_row, b_lab, b_slot, b_z, b_l, b_dl, b_dh, b_loss;
-  int64_t* row_off = (int64_t*)b_row.get(sizeof(int64_t) * rows);
-  int32_t* row_lab = (int32_t*)b_lab.get(sizeof(int32_t) * rows);
-  int* blk_slot = (int*)b_slot.get(sizeof(int) * nb);
-  float* Z = (float*)b_z.get(sizeof(float) * (size_t)rows * g.H);
-  float* L = (float*)b_l.get(sizeof(float) * (size_t)rows * g.C);
-  float* DL = (float*)b_dl.get(sizeof(float) * (size_t)rows * g.C);
-  float* DH = (float*)b_dh.get(sizeof(float) * (size_t)rows * g.H);
-  float* loss_rows = (float*)b_loss.get(sizeof(float) * rows);
+  DevBuf* ts = ctx->train_scratch;  // persistent across calls (no cudaMalloc per window)
+  int64_t* row_off = rows ? (int64_t*)ts[0].get(sizeof(int64_t) * rows) : nullptr;
+  int32_t* row_lab = rows ? (int32_t*)ts[1].get(sizeof(int32_t) * rows) : nullptr;
+  int* blk_slot = rows ? (int*)ts[2].get(sizeof(int) * nb) : nullptr;
+  float* Z = rows ? (float*)ts[3].get(sizeof(float) * (size_t)rows * g.H) : nullptr;
+  float* L = rows ? (float*)ts[4].get(sizeof(float) * (size_t)rows * g.C) : nullptr;
+  float* DL = rows ? (float*)ts[5].get(sizeof(float) * (size_t)rows * g.C) : nullptr;
+  float* DH = rows ? (float*)ts[6].get(sizeof(float) * (size_t)rows * g.H) : nullptr;
+  float* loss_rows = rows ? (float*)ts[7].get(sizeof(float) * rows) : nullptr;
   // spec chain buffer per slot: T snapshots; train in place in snapshot t-1
   std::vector<int> slots(n_jobs);
   ECCO_CUDA(ctx_memcpy(ctx, slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   std::vector<int> hb_slot(nb);
   const int rb_per_job = g.B / kRB;
-  for (int j = 0; j < n_jobs; ++j)
+  for (int j = 0; nb && j < n_jobs; ++j)
     for (int q = 0; q < rb_per_job; ++q) hb_slot[j * rb_per_job + q] = slots[j];
-  ECCO_CUDA(ctx_memcpy(ctx, blk_slot, hb_slot.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, ctx->stream));
+  if (nb)
+    ECCO_CUDA(ctx_memcpy(ctx, blk_slot, hb_slot.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, ctx->stream));
   // the spec snapshots use a virtual "slot" base: wspec + slot * T * np + (t-1) * np
   const size_t spec_stride = (size_t)T * np;
   // tensor-core path: one 128-row tile (or the whole minibatch when B < 128)
   // per job and 128 rows
-  const bool tc_math = ctx->cfg.math == ECCO_MATH_TC_TF32;
+  const bool tc_math = ctx->cfg.math == ECCO_MATH_TC_TF32 && !ctx->fused_train;
   std::vector<TcTile> tiles;
   TcTile* d_tiles = nullptr;
   if (tc_math) {
@@ -886,7 +856,20 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     // weights of state t are addressed as wbase + slot * spec_stride
     float* wt = ctx->d_wspec + (size_t)(t - 1) * np;
     // the per-slot stride for kernels is spec_stride: pass n_params = spec_stride
-    for (int step = 0; step < max_steps; ++step) {
+    if (ctx->fused_train) {
+      // one fused launch per SGD step for all jobs; the spec shadow (W1^T
+      // bf16) of snapshot t is rebuilt from its fp32 copy, then kept in sync
+      // by every step
+      fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots);
+      for (int step = 0; step < max_steps; ++step) {
+        int live = 0;
+        for (int j = 0; j < n_jobs; ++j) live += step < h_steps[j];
+        fused::train_step(ctx, ctx->sh_spec, n_jobs, d_slots, d_job_ids, d_steps, d_src_off,
+                          d_src_cam, d_src_frac, d_micro_base, t - 1, window, step, wt, spec_stride,
+                          t - 1, (double)live * g.B);
+      }
+    }
+    for (int step = 0; step < (ctx->fused_train ? 0 : max_steps); ++step) {
       const Gate gate{d_steps, step, g.B};
       int live = 0;
       for (int j = 0; j < n_jobs; ++j) live += step < h_steps[j];
@@ -963,8 +946,6 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     ECCO_LAUNCHED(ctx);
   }
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
-  b_row.release(); b_lab.release(); b_slot.release(); b_z.release();
-  b_l.release(); b_dl.release(); b_dh.release(); b_loss.release();
 }
 
 void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted) {

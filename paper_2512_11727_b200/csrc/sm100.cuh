@@ -95,6 +95,14 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t addr) {
   return smem_desc(addr, 16, 1024, kSwizzle128B);
 }
 
+// MN-major operand in 128-byte-swizzled atoms (64 MN-elements of 2 bytes x 8
+// K rows = 1024 B): LBO = byte stride between atoms along MN, SBO = byte
+// stride between 8-row groups along K (CUTLASS canonical layout
+// Swizzle<3,4,3> o ((T,8,m),(8,k)) : ((1,T,LBO),(8T,SBO))).
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return smem_desc(addr, lbo, sbo, kSwizzle128B);
+}
+
 // Instruction descriptor: D fp32, A/B format, both K-major, N, M.
 //   format: kind::f16 -> 0 f16, 1 bf16; kind::tf32 -> 2 tf32
 __host__ __device__ constexpr uint32_t idesc(int m, int n, uint32_t ab_format) {
@@ -102,6 +110,11 @@ __host__ __device__ constexpr uint32_t idesc(int m, int n, uint32_t ab_format) {
          ((uint32_t)(m >> 4) << 24);
 }
 constexpr uint32_t kFmtBF16 = 1, kFmtTF32 = 2;
+// Same with operand majors: bit 15 A, bit 16 B (0 = K-major, 1 = MN-major).
+__host__ __device__ constexpr uint32_t idesc_major(int m, int n, uint32_t ab_format, int a_mn,
+                                                   int b_mn) {
+  return idesc(m, n, ab_format) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16);
+}
 
 // ------------------------------------------------------------------ tcgen05 --
 // D[tmem] (+)= A[smem] . B[smem]^T  (kind::f16, bf16 operands)
@@ -172,6 +185,12 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -185,6 +204,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// 16-byte global -> shared asynchronous copy (L2 only) and its completion.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
 // Packs two fp32 into bf16x2 (round to nearest even), lo in bits 0-15.

@@ -154,22 +154,61 @@ def test_learned_simulation_runs_and_groups():
     assert summ["windows_run"] == 2
 
 
-# ---------------------------------------------------------------- TC_TF32 --
-# Tolerance of the tensor-core path.  tcgen05 kind::tf32 reads the top 19
-# bits of each fp32 operand (truncation to a 10-bit mantissa).  X is exact
-# (bf16 frames); W1 in the forward contraction and X^T, dH in the W1-gradient
-# contraction are truncated.  Two checks:
+# ------------------------------------------------------- tensor-core math --
+# Tolerance of the tensor-core path (fused SGD step, train_kernels.cu).  The
+# two contractions run tcgen05 kind::f16: X is exact (bf16 frames); W1 is the
+# bf16 (round-to-nearest-even) shadow of the fp32 master in the forward, and
+# dH is rounded to bf16 for dW1 = X^T . dH; accumulation and the head are
+# fp32.  Two checks:
 #  * against a float64 restatement of the SGD step that applies exactly that
-#    truncation (_step_tf32 below): agreement to 1e-3 of the update proves
-#    the layouts, descriptors and epilogues (measured: 2e-5);
-#  * against the fp32 oracle: the truncated W1 perturbs Z and therefore the
-#    ReLU mask and dH, which moves one step's W1 update by up to ~7% of its
-#    size (measured 6.7% for W1, 5.0% for b1, 4e-4 for the head), so the
-#    documented tolerance is 1e-1 of the update for one step and 1.5e-1 for
-#    a 3-step chain.
+#    rounding (_step_emulated below): agreement to 1e-3 of the update (measured
+#    7e-5) proves
+#    the layouts, descriptors and epilogues (a layout error is O(1));
+#  * against the fp32 oracle: the bf16 W1 perturbs Z and therefore the ReLU
+#    mask and dH; one step's W1 update moves by ~10% of its size (measured
+#    10.1% one step, 6.3% after a 3-step chain), so
+#    the documented tolerance is 2.5e-1 of the update for one step and for a
+#    3-step chain.
 TC_TOL_EMULATED = 1e-3
-TC_TOL_ONE_STEP = 1e-1
-TC_TOL_CHAIN = 1.5e-1
+TC_TOL_ONE_STEP = 2.5e-1
+TC_TOL_CHAIN = 2.5e-1
+
+
+def _bf16(a):
+    a = np.asarray(a, np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16 << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def _step_emulated(x, y, w, lr):
+    """One SGD step (orc_sgd_step's math) in float64 with the MMA operands
+    rounded to bf16 as the fused kernel feeds the tensor cores."""
+    w1, b1, w2, b2 = [np.asarray(t, np.float64) for t in w]
+    B, F = x.shape
+    H, Cc = b1.size, b2.size
+    W1, W2 = w1.reshape(F, H), w2.reshape(H, Cc)
+    X = x.astype(np.float64)
+    Z = X @ _bf16(W1.astype(np.float32)) + b1
+    R = np.maximum(Z, 0)
+    L = R @ W2 + b2
+    P = np.exp(L - L.max(1, keepdims=True))
+    P /= P.sum(1, keepdims=True)
+    P[np.arange(B), y] -= 1
+    DL = P / B
+    DH = (DL @ W2.T) * (Z > 0)
+    return [W1 - lr * (X.T @ _bf16(DH.astype(np.float32))), b1 - lr * DH.sum(0),
+            W2 - lr * (R.T @ DL), b2 - lr * DL.sum(0)]
+
+
+# The unfused tensor-core kernels (tc_kernels.cu, kind::tf32) still serve
+# shapes the fused step does not (minibatch != 128): tf32 reads the top 19
+# bits of each fp32 operand (truncation); measured agreement with the
+# emulation 2e-5 of the update, 6.7% vs the fp32 oracle after one step.
+TF32_TOL_EMULATED = 1e-3
+TF32_TOL_ONE_STEP = 1e-1
+TF32_TOL_CHAIN = 1.5e-1
+FUSED = dict(feat_dim=256, hidden_dim=256, minibatch=128, ring_frames=128)
 
 
 def _tf32(a):
@@ -198,8 +237,8 @@ def _step_tf32(x, y, w, lr):
             b2 - lr * DL.sum(0)]
 
 
-def _tc_weights_error(steps_one):
-    ctx, orc, rng = setup(seed=5, math=ecco.TC_TF32)
+def _tc_weights_error(steps_one, fused):
+    ctx, orc, rng = setup(seed=5, math=ecco.TC_TF32, **(FUSED if fused else {}))
     ids = [1, 2, 3, 4, 5]
     ctx.seed_models(ids)
     for j in ids:
@@ -225,7 +264,8 @@ def _tc_weights_error(steps_one):
             orc.L.orc_sample(orc.cp, jid, len(sources[j]), np.array(sources[j], np.int32),
                              np.array(fracs[j]), 3, 0, 0, cams, frames)
             x = (orc.frames[cams, frames].astype(np.uint32) << 16).view(np.float32)
-            emul = _step_tf32(x, orc.labels[cams, frames], base, orc.c.lr)
+            emul = (_step_emulated if fused else _step_tf32)(x, orc.labels[cams, frames], base,
+                                                             orc.c.lr)
         for k, (g, want, b0) in enumerate(zip(got, orc.models[jid], base)):
             upd = np.abs(want - b0).max()
             assert upd > 0
@@ -235,18 +275,22 @@ def _tc_weights_error(steps_one):
     return worst, worst_emul
 
 
-def test_tc_single_step_weights_within_tolerance():
-    vs_oracle, vs_emulated = _tc_weights_error(True)
-    assert vs_emulated <= TC_TOL_EMULATED
-    assert vs_oracle <= TC_TOL_ONE_STEP
+@pytest.mark.parametrize("fused", [True, False])
+def test_tc_single_step_weights_within_tolerance(fused):
+    vs_oracle, vs_emulated = _tc_weights_error(True, fused)
+    assert vs_emulated <= (TC_TOL_EMULATED if fused else TF32_TOL_EMULATED), vs_emulated
+    assert vs_oracle <= (TC_TOL_ONE_STEP if fused else TF32_TOL_ONE_STEP), vs_oracle
 
 
-def test_tc_chain_weights_within_tolerance():
-    assert _tc_weights_error(False)[0] <= TC_TOL_CHAIN
+@pytest.mark.parametrize("fused", [True, False])
+def test_tc_chain_weights_within_tolerance(fused):
+    err = _tc_weights_error(False, fused)[0]
+    assert err <= (TC_TOL_CHAIN if fused else TF32_TOL_CHAIN), err
 
 
-def test_tc_eval_counts_close_and_decisions_reported():
-    ctx, orc, rng = setup(seed=6, math=ecco.TC_TF32)
+@pytest.mark.parametrize("fused", [True, False])
+def test_tc_eval_counts_close_and_decisions_reported(fused):
+    ctx, orc, rng = setup(seed=6, math=ecco.TC_TF32, **(FUSED if fused else {}))
     ids = [1, 2, 3]
     ctx.seed_models(ids)
     for j in ids:
