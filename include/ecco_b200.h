@@ -141,6 +141,17 @@ ecco_status ecco_generate_frames(ecco_ctx* ctx, int window);
 ecco_status ecco_upload_frames(ecco_ctx* ctx, int n_cams, const uint16_t* frames,
                                const int32_t* labels, const uint16_t* eval_frames,
                                const int32_t* eval_labels);
+/* Double-buffered window ingest, for overlapping the next window's upload
+ * with the current window's kernels: ecco_stage_frames copies host frames
+ * (same layouts as ecco_upload_frames; pinned memory for a truly
+ * asynchronous DMA) into a back buffer on a separate copy stream and returns
+ * immediately; ecco_swap_frames makes them current (the context stream
+ * waits for the copy; no host synchronisation).  Kernels enqueued before the
+ * swap keep reading the previous frames. */
+ecco_status ecco_stage_frames(ecco_ctx* ctx, int n_cams, const uint16_t* frames,
+                              const int32_t* labels, const uint16_t* eval_frames,
+                              const int32_t* eval_labels);
+ecco_status ecco_swap_frames(ecco_ctx* ctx);
 /* Copies the first n_cams cameras' resident frames back to the host (same
  * layouts as ecco_upload_frames; any pointer may be NULL). */
 ecco_status ecco_read_frames(ecco_ctx* ctx, int n_cams, uint16_t* frames, int32_t* labels,

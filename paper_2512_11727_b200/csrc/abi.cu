@@ -35,7 +35,8 @@ void free_all(ecco_ctx* c) {
                   c->d_cl,     c->d_prof,   c->d_cen,     c->d_sk,      c->d_sclen,
                   c->d_scl,    c->d_sprof,  c->d_scen,    c->d_status,  c->d_w,
                   c->d_wspec,  c->d_proto_p, c->d_proto_q, c->d_frames, c->d_labels,
-                  c->d_eval,   c->d_eval_labels, c->d_losses};
+                  c->d_eval,   c->d_eval_labels, c->d_losses, c->b_frames, c->b_labels,
+                  c->b_eval,   c->b_eval_labels};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   fused::free_shadow(c->sh_commit);
@@ -44,6 +45,9 @@ void free_all(ecco_ctx* c) {
   for (auto& b : c->scratch) b.release();
   for (auto& b : c->train_scratch) b.release();
   for (auto& b : c->hscratch) b.release();
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->copy_done) cudaEventDestroy(c->copy_done);
+  if (c->back_free) cudaEventDestroy(c->back_free);
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -309,6 +313,54 @@ ecco_status ecco_upload_frames(ecco_ctx* ctx, int n, const uint16_t* frames, con
   return guarded(ctx, [&] {
     upload_frames_impl(ctx, n, frames, labels, eval, eval_labels, cudaMemcpyHostToDevice);
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+ecco_status ecco_stage_frames(ecco_ctx* ctx, int n, const uint16_t* frames, const int32_t* labels,
+                              const uint16_t* eval, const int32_t* eval_labels) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(learned(ctx), "stage_frames: learned backend only");
+    ECCO_REQUIRE(n >= 0 && n <= ctx->n_cams, "stage_frames: camera count");
+    ECCO_REQUIRE(!ctx->staged, "stage_frames: previous staging not swapped in");
+    const ecco_config& g = ctx->cfg;
+    if (!ctx->copy_stream) {
+      ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->back_free, cudaEventDisableTiming));
+      const size_t fr = (size_t)g.max_cameras * g.ring_frames, ev = (size_t)g.max_cameras * g.eval_samples;
+      dalloc(&ctx->b_frames, fr * g.feat_dim);
+      dalloc(&ctx->b_labels, fr);
+      dalloc(&ctx->b_eval, ev * g.feat_dim);
+      dalloc(&ctx->b_eval_labels, ev);
+    }
+    // the back buffer may still be read by kernels of the previous window
+    if (ctx->back_busy) ECCO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->back_free, 0));
+    const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n * g.eval_samples;
+    const cudaMemcpyKind k = cudaMemcpyHostToDevice;
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_frames, frames, fr * g.feat_dim * 2, k, ctx->copy_stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels, labels, fr * 4, k, ctx->copy_stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream));
+    ECCO_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+    ctx->staged = true;
+  });
+}
+
+ecco_status ecco_swap_frames(ecco_ctx* ctx) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(ctx->staged, "swap_frames: nothing staged");
+    ECCO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
+    std::swap(ctx->d_frames, ctx->b_frames);
+    std::swap(ctx->d_labels, ctx->b_labels);
+    std::swap(ctx->d_eval, ctx->b_eval);
+    std::swap(ctx->d_eval_labels, ctx->b_eval_labels);
+    delete (CUtensorMap*)ctx->map_x;  // rebuilt over the new eval buffer on next use
+    ctx->map_x = nullptr;
+    // kernels enqueued so far read the old front (now back): the next
+    // staging copy waits for them
+    ECCO_CUDA(cudaEventRecord(ctx->back_free, ctx->stream));
+    ctx->back_busy = true;
+    ctx->staged = false;
   });
 }
 

@@ -174,6 +174,15 @@ struct ecco_ctx {
   int32_t* d_eval_labels = nullptr;
   float* d_losses = nullptr;     // slots * max_depth
   int frames_window = -1;
+  // back buffers of the double-buffered window ingest (ecco_stage_frames /
+  // ecco_swap_frames), allocated on first use; copies run on copy_stream
+  uint16_t* b_frames = nullptr;
+  int32_t* b_labels = nullptr;
+  uint16_t* b_eval = nullptr;
+  int32_t* b_eval_labels = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_done = nullptr, back_free = nullptr;
+  bool staged = false, back_busy = false;
 
   // fused evaluation: shadows of the committed models (refreshed lazily for
   // slots marked dirty) and of the speculative snapshot being evaluated

@@ -304,16 +304,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       *reinterpret_cast<uint4*>(sWB + hc * 16384 + s * 128 + ((c16 ^ (s & 7)) << 4)) = pk;
     }
     __syncthreads();
-    if (tid < kHC * kC) {  // W2 rows h0..h0+7 (their dH is done): sequential over s
-      const int hi = tid / kC, c = tid % kC, h = h0 + hi;
-      float acc = 0.0f;
-      for (int q = 0; q < kB; ++q) acc = __fmaf_rn(sR[q * kHC + hi], sDL[q * kC + c], acc);
-      sW2[h * kC + c] = __fmaf_rn(-lr, acc, sW2[h * kC + c]);
-    } else if (tid < kHC * kC + kHC) {  // b1
-      const int hi = tid - kHC * kC, h = h0 + hi;
-      float acc = 0.0f;
-      for (int q = 0; q < kB; ++q) acc = __fadd_rn(acc, sDH[q * kHC + hi]);
-      b1[h] = __fmaf_rn(-lr, acc, b1[h]);
+    // dW2 rows h0..h0+7 (their dH is done) and db1: 136 sums over the 128
+    // rows, each split across the two halves of a warp (lanes l, l+16 take
+    // rows of opposite parity) with 4 independent accumulators, combined by
+    // one shuffle.  Warps 0-7 x 16 lane pairs = 128 dW2 outputs; the 8 db1
+    // outputs go to warps 0-7 as a second item.
+    {
+      const int half = lane >> 4, li = lane & 15;
+      for (int item = 0; item < 2; ++item) {
+        const int o = item == 0 ? warp * 16 + li : kHC * kC + warp;  // output id
+        const bool active = item == 0 || li == 0;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+        if (active) {
+          if (o < kHC * kC) {
+            const int hi = o / kC, c = o % kC;
+#pragma unroll 4
+            for (int q = half; q < kB; q += 8) {
+              a0 = __fmaf_rn(sR[q * kHC + hi], sDL[q * kC + c], a0);
+              a1 = __fmaf_rn(sR[(q + 2) * kHC + hi], sDL[(q + 2) * kC + c], a1);
+              a2 = __fmaf_rn(sR[(q + 4) * kHC + hi], sDL[(q + 4) * kC + c], a2);
+              a3 = __fmaf_rn(sR[(q + 6) * kHC + hi], sDL[(q + 6) * kC + c], a3);
+            }
+          } else {
+            const int hi = o - kHC * kC;
+#pragma unroll 4
+            for (int q = half; q < kB; q += 8) {
+              a0 += sDH[q * kHC + hi];
+              a1 += sDH[(q + 2) * kHC + hi];
+              a2 += sDH[(q + 4) * kHC + hi];
+              a3 += sDH[(q + 6) * kHC + hi];
+            }
+          }
+        }
+        float acc = (a0 + a1) + (a2 + a3);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+        if (active && half == 0) {
+          if (o < kHC * kC) {
+            const int h = h0 + o / kC, c = o % kC;
+            sW2[h * kC + c] = __fmaf_rn(-lr, acc, sW2[h * kC + c]);
+          } else {
+            const int h = h0 + (o - kHC * kC);
+            b1[h] = __fmaf_rn(-lr, acc, b1[h]);
+          }
+        }
+      }
     }
     __syncthreads();
   }

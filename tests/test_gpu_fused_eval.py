@@ -165,3 +165,29 @@ def test_fused_route_matrix_argmax():
         assert best[i].item() == bc
         if bc >= 0:
             assert acc[i].item() == ba
+
+
+def test_staged_frames_swap_in_and_match_upload():
+    """ecco_stage_frames + ecco_swap_frames (double-buffered ingest) leave
+    the same resident frames and the same evaluation as ecco_upload_frames."""
+    import torch
+    n_cams, ids = 6, [0, 1, 2]
+    ctx, rng = _ctx(ecco.TC_TF32, n_cams, 7)
+    _random_models(ctx, rng, ids)
+    fr, lb, ev, el = ctx.read_frames(n_cams)
+    M0 = ctx.eval_matrix(ids, cams=np.arange(n_cams))
+    # stage a permuted window (cameras reversed), swap, compare
+    pf = [torch.from_numpy(np.ascontiguousarray(a[::-1])).pin_memory() for a in (fr, lb, ev, el)]
+    ctx.stage_frames_host_ptr(n_cams, *[t.data_ptr() for t in pf])
+    ctx.swap_frames()
+    fr2, lb2, ev2, el2 = ctx.read_frames(n_cams)
+    assert fr2.tobytes() == fr[::-1].tobytes() and el2.tobytes() == el[::-1].tobytes()
+    M1 = ctx.eval_matrix(ids, cams=np.arange(n_cams))
+    assert M1.tobytes() == M0[::-1].tobytes()
+    # and back again through the other buffer
+    pf = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in (fr, lb, ev, el)]
+    ctx.stage_frames_host_ptr(n_cams, *[t.data_ptr() for t in pf])
+    ctx.swap_frames()
+    assert ctx.eval_matrix(ids, cams=np.arange(n_cams)).tobytes() == M0.tobytes()
+    with pytest.raises(ecco.InvalidArgument):
+        ctx.swap_frames()  # nothing staged
