@@ -129,6 +129,31 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def _red_device():
+    import torch
+    nccl = os.environ.get("ECCO_DIST_BACKEND", "nccl") == "nccl"
+    return torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+
+
+def reduce_max(dist, values):
+    """Max over ranks (device times: the slowest rank bounds the job)."""
+    if dist is None:
+        return list(values)
+    import torch
+    t = torch.tensor(values, dtype=torch.float64, device=_red_device())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def reduce_sum(dist, value):
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_red_device())
+    dist.all_reduce(t)
+    return t.item()
+
+
 # ------------------------------------------------------------------ workload --
 
 class Workload:
@@ -139,9 +164,9 @@ class Workload:
         self.N, self.G = CONFIGS[config]
         self.per = self.N // self.G
         self.rank, self.world = rank, world
-        self.gb = -(-self.G // world)  # column block per rank (last may be partial)
-        lo, hi = rank * self.gb, min(self.G, (rank + 1) * self.gb)
-        self.local = list(range(lo, hi))
+        from paper_2512_11727_b200 import shard
+        self.gb = shard.block_size(self.G, world)  # column block per rank (last may be ragged)
+        self.local = shard.rank_groups(self.G, world, rank)
         side = 10
         self.scenes = np.array([[0.1 * ((c // self.per) % side), 0.1 * ((c // self.per // side) % side)]
                                 for c in range(self.N)], np.float64)
@@ -159,12 +184,21 @@ class Workload:
 def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2512_11727_b200 as ecco
+    from paper_2512_11727_b200 import shard
 
+    # ECCO_DIST_BACKEND=gloo (testing only) runs N ranks on however many GPUs
+    # the box has, gathering through host memory; the product path is NCCL
+    backend = os.environ.get("ECCO_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     wl = Workload(args.config, rank, world)
     math = ecco.TC_TF32 if args.math == "tf32" else ecco.FFMA_EXACT
     ctx = ecco.Context(backend=ecco.LEARNED, device=local_rank, math=math,
@@ -181,7 +215,6 @@ def run_b200(args, rank, world, local_rank):
     stream = torch.cuda.ExternalStream(ctx.stream)
     dev = torch.device("cuda", local_rank)
     M_local = torch.full((wl.N, wl.gb), float("nan"), dtype=torch.float64, device=dev)
-    M_all = torch.empty((world, wl.N, wl.gb), dtype=torch.float64, device=dev)
     M_part = None if len(wl.local) == wl.gb else torch.empty((wl.N, max(1, len(wl.local))),
                                                              dtype=torch.float64, device=dev)
     best = torch.empty(wl.N, dtype=torch.int32, device=dev)
@@ -200,11 +233,10 @@ def run_b200(args, rank, world, local_rank):
                 else:  # ragged last block: columns beyond the rank's groups stay NaN
                     ctx.eval_matrix_dev(wl.local, M_part.data_ptr(), cams=cams)
                     M_local[:, :len(wl.local)].copy_(M_part)
-            if world > 1:
-                dist.all_gather_into_tensor(M_all, M_local)
-                M = M_all
+            if backend == "nccl":
+                M = shard.gather_blocks(M_local, world, dist)  # NCCL all-gather of column blocks
             else:
-                M = M_local
+                M = shard.gather_blocks(M_local.cpu(), world, dist).to(dev)
             ctx.route_matrix_dev(wl.N, wl.gb, M.data_ptr(), best.data_ptr(), best_acc.data_ptr(),
                                  n_blocks=world)
             if timed:
@@ -246,15 +278,8 @@ def run_b200(args, rank, world, local_rank):
     kst = {name: ctx.kernel_stat(getattr(ecco, "KSTAT_" + name)) for name in
            ("EVAL_HIDDEN", "EVAL_HEAD", "TRAIN_FWD", "TRAIN_DW1", "TRAIN_HEAD")}
     ctx.profile(False)
-    t = torch.tensor([ms, phase["regroup"], phase["retrain"]], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, regroup_ms, retrain_ms = t.tolist()
-    samples = wl.samples_per_step_local() * args.steps
-    if dist is not None:
-        s = torch.tensor([samples], dtype=torch.float64, device=dev)
-        dist.all_reduce(s)
-        samples = s.item()
+    ms, regroup_ms, retrain_ms = reduce_max(dist, [ms, phase["regroup"], phase["retrain"]])
+    samples = reduce_sum(dist, wl.samples_per_step_local() * args.steps)
 
     # ---- e2e: same step through the public API, frames from pinned host memory
     e2e = None if args.no_e2e else run_e2e(args, ctx, wl, step, torch, dist, stream, best)
@@ -366,15 +391,8 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev):
     el_s = time.perf_counter() - t0
     h1, d1 = ctx.transfer_bytes()
     d1 += steps * best_host.numel() * 4
-    t = torch.tensor([el_s], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    el_s = t.item()
-    samples = wl.samples_per_step_local() * steps
-    if dist is not None:
-        s = torch.tensor([samples], dtype=torch.float64, device=t.device)
-        dist.all_reduce(s)
-        samples = s.item()
+    el_s = reduce_max(dist, [el_s])[0]
+    samples = reduce_sum(dist, wl.samples_per_step_local() * steps)
     return {"value": samples / el_s, "unit": "samples/s",
             "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
             "ms_per_step": el_s * 1e3 / steps, "steps": steps,
