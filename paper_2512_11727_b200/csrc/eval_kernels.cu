@@ -52,6 +52,15 @@ constexpr uint32_t kAChunk = kTileRows * 128; // one X K-chunk: 128 rows x 64 bf
 constexpr int kMaxStages = 8;
 constexpr uint32_t kTmemZ = 0, kTmemR = 256, kTmemL = 384;
 
+struct EvalBars {
+  uint64_t a_full, a_empty;
+  uint64_t full[kMaxStages], empty[kMaxStages];
+  uint64_t w2_full[2], w2_empty[2];
+  uint64_t z_full[2], z_empty[2], r_full[2], r_empty[2];
+  uint64_t l_full[2], l_empty[2];
+  uint32_t tmem_base;
+};
+
 struct EvalArgs {
   int n_rows;            // n_probes * S
   int S;
@@ -73,7 +82,8 @@ struct EvalArgs {
   const uint8_t* w2t;    // per slot: W2^T bf16 K-major 128B-swizzled image
   uint32_t w2t_bytes;    // W2^T part of the per-slot image
   uint32_t img_bytes;    // whole image: W2^T | b1 (H fp32) | b2 (C fp32)
-  uint32_t img_stride;   // smem stride of the two image buffers (1024-aligned)
+  uint32_t w2t_stride;   // smem stride of the two W2^T buffers (1024-aligned)
+  uint32_t bias_bytes;   // b1 | b2 part of the image (smem stride of its buffers)
   int stages;
   int nl;                // logits buffers (1 or 2)
   float* dbg_logits;     // optional: [n_rows][n_ent][C] logits + b2 (dense mode tests)
@@ -89,22 +99,33 @@ __device__ __forceinline__ int tile_ent_end(const EvalArgs& a, int m) {
 __global__ void __launch_bounds__(kThreads, 1)
     k_eval_fused(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                  EvalArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // everything lives in dynamic shared memory (no static smem), so the base
+  // is 1 KB aligned as the 128B-swizzle atoms require (checked below)
+  extern __shared__ __align__(1024) uint8_t smem[];
   const int nkc = a.F / kKC;
   const int nh = a.H / kHalf;
   uint8_t* sA = smem;                                   // nkc x 16 KB
   uint8_t* sB = sA + nkc * kAChunk;                     // stages x 16 KB
-  uint8_t* sW2 = sB + a.stages * kBoxBytes;             // 2 x img_stride
-  __shared__ __align__(8) uint64_t a_full, a_empty;
-  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
-  __shared__ __align__(8) uint64_t w2_full[2], w2_empty[2];
-  __shared__ __align__(8) uint64_t z_full[2], z_empty[2], r_full[2], r_empty[2];
-  __shared__ __align__(8) uint64_t l_full[2], l_empty[2];
-  __shared__ uint32_t tmem_base;
+  uint8_t* sW2 = sB + a.stages * kBoxBytes;             // 2 x w2t_stride (W2^T images)
+  uint8_t* sBias = sW2 + 2 * a.w2t_stride;              // 2 x bias_bytes (b1 | b2)
+  EvalBars* bars = reinterpret_cast<EvalBars*>(sBias + 2 * a.bias_bytes);
+  uint64_t& a_full = bars->a_full;
+  uint64_t& a_empty = bars->a_empty;
+  uint64_t* full = bars->full;
+  uint64_t* empty = bars->empty;
+  uint64_t* w2_full = bars->w2_full;
+  uint64_t* w2_empty = bars->w2_empty;
+  uint64_t* z_full = bars->z_full;
+  uint64_t* z_empty = bars->z_empty;
+  uint64_t* r_full = bars->r_full;
+  uint64_t* r_empty = bars->r_empty;
+  uint64_t* l_full = bars->l_full;
+  uint64_t* l_empty = bars->l_empty;
+  uint32_t& tmem_base = bars->tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
     tma_prefetch(&map_x);
     tma_prefetch(&map_w);
     mbar_init(&a_full, 1);
@@ -157,9 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int wb = u & 1;
         mbar_wait(&w2_empty[wb], ((u >> 1) & 1) ^ 1);
         if (elect_one()) {
+          const uint8_t* img = a.w2t + (size_t)slot * a.img_bytes;
           mbar_expect_tx(&w2_full[wb], a.img_bytes);
-          bulk_load(sW2 + wb * a.img_stride, a.w2t + (size_t)slot * a.img_bytes, a.img_bytes,
-                    &w2_full[wb]);
+          bulk_load(sW2 + wb * a.w2t_stride, img, a.w2t_bytes, &w2_full[wb]);
+          bulk_load(sBias + wb * a.bias_bytes, img + a.w2t_bytes, a.bias_bytes, &w2_full[wb]);
         }
         __syncwarp();
         for (int hf = 0; hf < nh; ++hf) {
@@ -202,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&r_full[rb], (w >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint64_t dW = dW0 + ((wb * a.img_stride) >> 4);
+        const uint64_t dW = dW0 + ((wb * a.w2t_stride) >> 4);
 #pragma unroll
         for (int k16 = 0; k16 < kHalf / 16; ++k16) {
           const int kg = hw * kHalf + k16 * 16;  // K index into H
@@ -273,8 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int e1 = tile_ent_end(a, m);
       for (int e = tile_ent_begin(a, m); e < e1; ++e, ++u) {
         const uint32_t wb = u & 1;
-        const uint8_t* img = sW2 + wb * a.img_stride;
-        const float* b1 = reinterpret_cast<const float*>(img + a.w2t_bytes);
+        const float* b1 = reinterpret_cast<const float*>(sBias + wb * a.bias_bytes);
         const float* b2 = b1 + a.H;
         mbar_wait(&w2_full[wb], (u >> 1) & 1);  // b1 / b2 of this model are in smem
         for (int hf = 0; hf < nh; ++hf) {
@@ -458,7 +479,8 @@ bool supported(const ecco_ctx* ctx) {
   return g.feat_dim % 64 == 0 && g.feat_dim <= 512 && g.hidden_dim % kHalf == 0 &&
          g.num_classes % 16 == 0 && g.num_classes <= 64 &&
          (size_t)g.num_classes * g.hidden_dim * 2 <= 16384 && g.eval_samples % 64 == 0 &&
-         g.feat_dim / 64 * 16384 + 2 * ((img_bytes(g) + 1023) / 1024 * 1024) + 1024 + 2 * 16384 <= 231424;
+         g.feat_dim / 64 * 16384 + 2 * ((w2t_bytes(g) + 1023) / 1024 * 1024) +
+                 2 * (img_bytes(g) - w2t_bytes(g)) + sizeof(EvalBars) + 2 * 16384 <= 232448;
 }
 
 
@@ -523,11 +545,13 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
   a.w2t = sh.w2t;
   a.w2t_bytes = w2t_bytes(g);
   a.img_bytes = img_bytes(g);
-  a.img_stride = (a.img_bytes + 1023u) & ~1023u;
+  a.w2t_stride = (a.w2t_bytes + 1023u) & ~1023u;
+  a.bias_bytes = a.img_bytes - a.w2t_bytes;
   a.nl = 2 * g.num_classes <= 128 ? 2 : 1;
   a.dbg_logits = dbg_logits;
-  const size_t fixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)a.img_stride + 1024;
-  const size_t max_smem = 232448 - 1024;  // opt-in limit minus the static barriers
+  const size_t fixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)a.w2t_stride +
+                       2 * (size_t)a.bias_bytes + sizeof(EvalBars);
+  const size_t max_smem = 232448;  // opt-in per-block limit (no static smem)
   a.stages = (int)std::min<size_t>(kMaxStages, (max_smem - fixed) / kBoxBytes);
   ECCO_REQUIRE(a.stages >= 2, "fused eval: shared memory too small for the pipeline");
   const size_t smem = fixed + (size_t)a.stages * kBoxBytes;
