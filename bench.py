@@ -320,7 +320,12 @@ def run_b200(args, rank, world, local_rank):
                         for k, v in kst.items()},
         }
         if not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(args, wl.N, wl.G)
+            line["cpu_baseline"] = cpu_sample(wl.N, wl.G)
+        if world == 1 and not args.no_parametric:
+            try:
+                line["parametric"] = parametric_leg(args)
+            except Exception as e:  # reported, never fatal for the headline line
+                line["parametric"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -479,6 +484,95 @@ def cpu_sample(N, G, budget_s=12.0):
             "window_s": window_s}
 
 
+def parametric_leg(args):
+    """The reference-pinned backend against the UNMODIFIED reference library
+    (oracle/_ref, compiled from /root/reference; shipped prebuilt to the GPU
+    box): (a) the camera x group eval matrix (K1, `eval` per pair,
+    accuracy_model.cpp:60-67) at C4 size on the GPU vs the reference's own loop
+    on a bounded sample, bit-exact check included; (b) Simulation::step_window
+    (orchestrator.cpp:211-413) at C3 on the GPU window driver vs the reference,
+    per-window wall time and byte-identical trace."""
+    import ctypes as C
+
+    import torch
+
+    import oracle
+    import paper_2512_11727_b200 as ecco
+    from paper_2512_11727_b200 import scenarios
+
+    if not oracle.have_ref():
+        return {"unavailable": "oracle/_ref/libecco_ref.so not built"}
+    R = oracle.ref()
+    out = {}
+    # (a) eval matrix, C4: 10,000 scenes x 500 models of K=3 clusters, D=2
+    rng = np.random.default_rng(7)
+    N, G, K, D = 10000, 500, 3, 2
+    params = oracle.params_array(oracle.default_params())
+    scenes = np.round(rng.random((N, D)), 2)
+    ks = np.full(G, K, np.int32)
+    cl = np.round(rng.random((G, K, D)), 2)
+    pr = rng.random((G, K))
+    ce = cl.mean(1)
+    clen = np.full(G, D, np.int32)
+    ctx = ecco.Context(backend=ecco.PARAMETRIC, max_jobs=G, max_cameras=N, max_clusters=K)
+    ids = list(range(G))
+    ctx.put_models(ids, ks, cl, pr, ce, clen)
+    dM = torch.empty((N, G), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    for _ in range(3):
+        ctx.eval_matrix_dev(ids, dM.data_ptr(), scenes=scenes)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+    for _ in range(reps):
+        ctx.eval_matrix_dev(ids, dM.data_ptr(), scenes=scenes)
+    with torch.cuda.stream(stream):
+        ev1.record(stream)
+    ev1.synchronize()
+    gpu_s = ev0.elapsed_time(ev1) / 1e3 / reps
+    ns = 1000  # bounded CPU sample: 1,000 scenes x 500 models
+    want = np.zeros((ns, G))
+    cpu_s = R.ref_eval_matrix(ns, np.ascontiguousarray(scenes[:ns]), G, ks,
+                              np.ascontiguousarray(cl.reshape(-1)), np.ascontiguousarray(pr.reshape(-1)),
+                              clen, np.ascontiguousarray(ce.reshape(-1)), K, D, params, want)
+    got = dM[:ns].cpu().numpy()
+    out["eval_matrix"] = {
+        "workload": f"{N} scenes x {G} models (K={K}, D={D}), fp64",
+        "gpu_pairs_per_s": N * G / gpu_s, "gpu_ms": gpu_s * 1e3,
+        "reference_pairs_per_s": ns * G / cpu_s, "reference_cores": 1,
+        "reference_sample": f"{ns} x {G} pairs through the reference's eval()",
+        "bit_exact_vs_reference": bool(got.tobytes() == want.tobytes()),
+        "speedup": (N * G / gpu_s) / (ns * G / cpu_s)}
+    ctx.close()
+    # (b) window driver, C3 (1,000 cameras / 50 clusters, W = 100 micro-windows)
+    sc = json.dumps(scenarios.config("c3", windows=4, seed=1))  # (seed 3 makes the reference itself
+    # raise set_aimd_params for a zero-gain job, and the GPU driver raises the same)
+    sim = ecco.Simulation(sc, backend=ecco.PARAMETRIC)
+    wins, regroup = [], []
+    while True:
+        t = time.perf_counter()
+        if not sim.step_window():
+            break
+        wins.append(time.perf_counter() - t)
+        regroup.append(sim.last_timings()["regroup_ms"])
+    ref_s = np.zeros(8)
+    n_run = C.c_int()
+    R.ref_time_windows(sc.encode(), 8, ref_s, C.byref(n_run))
+    ref_s = ref_s[:n_run.value]
+    tcap = 1 << 26
+    tb, sb = C.create_string_buffer(tcap), C.create_string_buffer(1 << 20)
+    tl, sl = C.c_size_t(), C.c_size_t()
+    R.ref_run_scenario(sc.encode(), -1, tb, tcap, C.byref(tl), sb, 1 << 20, C.byref(sl))
+    out["window"] = {
+        "workload": "c3 scenario (scenarios.config('c3', seed=1), 4 windows), parametric backend",
+        "gpu_window_ms": [w * 1e3 for w in wins], "gpu_regroup_ms": regroup,
+        "reference_window_ms": [w * 1e3 for w in ref_s], "reference_cores": 1,
+        "trace_identical_to_reference": sim.trace_csv() == tb.raw[:tl.value].decode()}
+    sim.close()
+    return out
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -525,6 +619,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
+    ap.add_argument("--no-parametric", action="store_true",
+                    help="skip the parametric-backend vs reference-library leg")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
