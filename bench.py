@@ -276,7 +276,7 @@ def run_b200(args, rank, world, local_rank):
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
     kst = {name: ctx.kernel_stat(getattr(ecco, "KSTAT_" + name)) for name in
-           ("EVAL_HIDDEN", "EVAL_HEAD", "TRAIN_FWD", "TRAIN_DW1", "TRAIN_HEAD")}
+           ("EVAL_MATRIX", "EVAL_PAIRS", "TRAIN_STEP", "TRAIN_DW1", "TRAIN_HEAD")}
     ctx.profile(False)
     ms, regroup_ms, retrain_ms = reduce_max(dist, [ms, phase["regroup"], phase["retrain"]])
     samples = reduce_sum(dist, wl.samples_per_step_local() * args.steps)
@@ -350,8 +350,8 @@ def roofline(kst, pk, pk_kind, args):
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(name)
-        except (OSError, ValueError):
+            traffic = json.load(open(tpath)).get(args.config, {}).get(name)
+        except (OSError, ValueError, AttributeError):
             traffic = None
     return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": achieved / peak, "peak_source": how,

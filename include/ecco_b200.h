@@ -103,11 +103,11 @@ uint64_t ecco_kernel_launches(const ecco_ctx* ctx);
  * launches, summed device milliseconds and the algorithmic flops and bytes of
  * those launches (units in DESIGN.md). */
 typedef enum {
-  ECCO_KSTAT_TRAIN_FWD = 0,    /* learned: hidden layer of the SGD minibatch   */
-  ECCO_KSTAT_TRAIN_DW1 = 1,    /* learned: W1 gradient + SGD update            */
-  ECCO_KSTAT_TRAIN_HEAD = 2,   /* learned: logits/softmax/dh/W2 update         */
-  ECCO_KSTAT_EVAL_HIDDEN = 3,  /* learned: eval-matrix hidden layer            */
-  ECCO_KSTAT_EVAL_HEAD = 4,    /* learned: eval logits + correct counts        */
+  ECCO_KSTAT_TRAIN_STEP = 0,   /* learned: fused SGD step (unfused math: hidden layer) */
+  ECCO_KSTAT_TRAIN_DW1 = 1,    /* learned, unfused math: W1 gradient + SGD update   */
+  ECCO_KSTAT_TRAIN_HEAD = 2,   /* learned, unfused math: logits/softmax/dH/W2       */
+  ECCO_KSTAT_EVAL_MATRIX = 3,  /* learned: dense camera x group evaluation matrix   */
+  ECCO_KSTAT_EVAL_PAIRS = 4,   /* learned: (camera, job) pair lists (chains, jobs)  */
   ECCO_KSTAT_P_EVAL = 5,       /* parametric eval matrix / pairs               */
   ECCO_KSTAT_P_TRAJ = 6,       /* parametric trajectories                      */
   ECCO_KSTAT_P_PROFILE = 7,    /* parametric profile tables                    */

@@ -25,7 +25,7 @@ OK, INVALID_ARGUMENT, LOGIC, INFEASIBLE, SCHEMA, CUDA, RUNTIME = range(7)
 PARAMETRIC, LEARNED = 0, 1
 FFMA_EXACT, TC_TF32 = 0, 1
 # ecco_kstat (include/ecco_b200.h)
-(KSTAT_TRAIN_FWD, KSTAT_TRAIN_DW1, KSTAT_TRAIN_HEAD, KSTAT_EVAL_HIDDEN, KSTAT_EVAL_HEAD,
+(KSTAT_TRAIN_STEP, KSTAT_TRAIN_DW1, KSTAT_TRAIN_HEAD, KSTAT_EVAL_MATRIX, KSTAT_EVAL_PAIRS,
  KSTAT_P_EVAL, KSTAT_P_TRAJ, KSTAT_P_PROFILE, KSTAT_FRAMES) = range(9)
 
 

@@ -568,7 +568,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
   const double bytes = live_pairs * g.eval_samples * 0.0 + (double)a.n_rows * g.feat_dim * 2 +
                        (double)n_ent * (g.feat_dim * g.hidden_dim * 2.0 + a.w2t_bytes) +
                        4.0 * live_pairs;
-  ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_HIDDEN, flops, bytes,
+  ECCO_TIMED(ctx, d_tile_ebeg ? ECCO_KSTAT_EVAL_PAIRS : ECCO_KSTAT_EVAL_MATRIX, flops, bytes,
              (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
                                                                   *(const CUtensorMap*)sh.map_w, a)));
   ECCO_LAUNCHED(ctx);

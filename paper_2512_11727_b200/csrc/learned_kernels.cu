@@ -609,14 +609,14 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
       tc::fwd_hidden(ctx, ctx->d_eval, row_off, d_tiles, (int)tiles.size(), nullptr, 0, ctx->d_w,
                      ctx->n_params, Z, (double)rows);
     } else {
-      ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_HIDDEN, 2.0 * rows * g.F * g.H,
+      ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_MATRIX, 2.0 * rows * g.F * g.H,
                  (double)rows * g.F * 2 + (double)g.F * g.H * 4,
                  (k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
                      g, ctx->d_eval, row_off, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w,
                      ctx->n_params, Z)));
       ECCO_LAUNCHED(ctx);
     }
-    ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_HEAD, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
+    ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
                (k_l_logits<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
                    g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L)));
     ECCO_LAUNCHED(ctx);
@@ -882,7 +882,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
         tc::fwd_hidden(ctx, ctx->d_frames, row_off, d_tiles, (int)tiles.size(), d_steps, step, wt,
                        spec_stride, Z, lrows);
       } else {
-        ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_FWD, 2.0 * lrows * g.F * g.H,
+        ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_STEP, 2.0 * lrows * g.F * g.H,
                    lrows * g.F * 2 + (double)live * g.F * g.H * 4,
                    (k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
                        g, ctx->d_frames, row_off, blk_slot, gate, wt, spec_stride, Z)));

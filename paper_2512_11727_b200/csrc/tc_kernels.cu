@@ -363,7 +363,7 @@ void fwd_hidden(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, co
     ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 + 2 * 256 * kKC * 4));
     attr = true;
   }
-  const int kind = steps ? ECCO_KSTAT_TRAIN_FWD : ECCO_KSTAT_EVAL_HIDDEN;
+  const int kind = steps ? ECCO_KSTAT_TRAIN_STEP : ECCO_KSTAT_EVAL_MATRIX;
   ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 4,
              (k_tc_fwd<<<dim3(n_tiles, H / NT), kThreads, sm, ctx->stream>>>(a)));
   ECCO_LAUNCHED(ctx);

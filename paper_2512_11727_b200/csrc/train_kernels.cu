@@ -479,7 +479,7 @@ void train_step(ecco_ctx* ctx, const Shadow& sh, int n_jobs, const int* d_slots,
   const double F = c.feat_dim, H = c.hidden_dim, C = c.num_classes;
   const double flops = live_rows * (4.0 * F * H + 6.0 * H * C);
   const double bytes = live_rows * F * 2.0 + live_rows / kB * (F * H * (4.0 + 4.0 + 2.0 + 2.0));
-  ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_FWD, flops, bytes,
+  ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_STEP, flops, bytes,
              (k_train_step<<<n_jobs, kThreads, smem, ctx->stream>>>(
                  *(const CUtensorMap*)sh.map_w_train, a)));
   ECCO_LAUNCHED(ctx);
