@@ -100,6 +100,8 @@ struct Shadow {
   uint8_t* w2t = nullptr;
   void* map_w = nullptr;        // CUtensorMap*, {64, 128} boxes (evaluation)
   void* map_w_train = nullptr;  // CUtensorMap*, {64, H} boxes (fused SGD step)
+  void* map_w_pair = nullptr;   // CUtensorMap*, {64, 64} boxes (CTA-pair evaluation)
+  void* map_w2_pair = nullptr;  // CUtensorMap*, 5-D view of the W2^T images per CTA half
 };
 
 struct ecco_ctx {

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -373,6 +374,292 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (dense matrices): two SMs of a cluster run the hidden
+// layer as M = 256 tcgen05 MMAs (cta_group::2).  Each CTA keeps its own 128
+// eval rows resident and streams only HALF of every W1^T box (64 of the 128
+// hidden columns): the W1^T bytes per FLOP per SM halve, which doubles the
+// work buffered by the same 5 shared-memory stages -- the v4 kernel was bound
+// by exactly that (TMA latency x bytes in flight, profiles/r01_summary.md).
+// The pair leader issues every MMA; the follower's TMA loads complete on the
+// leader's barriers (cp.async.bulk.tensor .cta_group::2); MMA commits are
+// multicast to both CTAs; epilogue warps of both CTAs arrive on the leader's
+// barriers.  The second layer (logits, N = C = 16) is also a pair MMA with A
+// (bf16 relu(Z + b1)) from each CTA's TMEM and W2^T split 8 + 8 rows.
+constexpr uint32_t kPairBox = 64 * 128;  // W1^T half box: 64 rows x 64 bf16
+constexpr int kMaxPairStages = 12;
+
+struct PairBars {
+  uint64_t a_full, a_empty;
+  uint64_t full[kMaxPairStages], empty[kMaxPairStages];
+  uint64_t w2_full[2], w2_empty[2];
+  uint64_t bias_full[2], bias_empty[2];
+  uint64_t z_full[2], z_empty[2], r_full[2], r_empty[2];
+  uint64_t l_full[2], l_empty[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_eval_pair(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                const __grid_constant__ CUtensorMap map_w2, EvalArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int nkc = a.F / kKC;
+  const int nh = a.H / kHalf;
+  const uint32_t w2h = (uint32_t)(a.H / 64) * 1024u;  // this CTA's W2^T half: 8 rows per atom
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + nkc * kAChunk;
+  uint8_t* sW2 = sB + a.stages * kPairBox;
+  uint8_t* sBias = sW2 + 2 * w2h;
+  PairBars* bars = reinterpret_cast<PairBars*>(sBias + 2 * a.bias_bytes);
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  auto lead = [&](uint64_t* bar) { return mapa_shared(smem_u32(bar), 0); };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
+
+  if (warp == 0 && lane == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    tma_prefetch(&map_x);
+    tma_prefetch(&map_w);
+    tma_prefetch(&map_w2);
+    mbar_init(&bars->a_full, 1);
+    mbar_init(&bars->a_empty, 1);
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&bars->full[s], 1);
+      mbar_init(&bars->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->w2_full[b], 1);
+      mbar_init(&bars->w2_empty[b], 1);
+      mbar_init(&bars->bias_full[b], 1);
+      mbar_init(&bars->bias_empty[b], 4);
+      mbar_init(&bars->z_full[b], 1);
+      mbar_init(&bars->z_empty[b], 16);
+      mbar_init(&bars->r_full[b], 16);
+      mbar_init(&bars->r_empty[b], 1);
+      mbar_init(&bars->l_full[b], 1);
+      mbar_init(&bars->l_empty[b], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair(&bars->tmem_base, 512);
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers and TMEM are live before any cross-CTA use
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    int stage = 0;
+    uint32_t sph = 0, u = 0, t = 0;
+    for (int m = pair; m < n_super; m += npairs, ++t) {
+      if (t > 0) mbar_wait(&bars->a_empty, (t - 1) & 1);
+      if (elect_one()) {
+        if (leader) mbar_expect_tx(&bars->a_full, 2u * nkc * kAChunk);
+        for (int h2 = 0; h2 < 2; ++h2) {
+          int b = m * 4 + (int)rank * 2 + h2;
+          if (b * 64 >= a.n_rows) b = 0;  // padding rows: any valid box, masked later
+          const int p = (b * 64) / a.S, soff = (b * 64) % a.S;
+          const int row = a.cams[p] * a.S + soff;
+          for (int kc = 0; kc < nkc; ++kc)
+            tma_load_2d_pair(sA + kc * kAChunk + h2 * (kAChunk / 2), &map_x, kc * kKC, row,
+                             lead(&bars->a_full));
+        }
+      }
+      __syncwarp();
+      for (int e = 0; e < a.n_ent; ++e, ++u) {
+        const int slot = a.ent_slot[e];
+        const int wb = u & 1;
+        mbar_wait(&bars->w2_empty[wb], ((u >> 1) & 1) ^ 1);
+        mbar_wait(&bars->bias_empty[wb], ((u >> 1) & 1) ^ 1);
+        if (elect_one()) {
+          if (leader) mbar_expect_tx(&bars->w2_full[wb], 2u * w2h);
+          tma_load_5d_pair(sW2 + wb * w2h, &map_w2, 0, 0, (int)rank, 0, slot,
+                           lead(&bars->w2_full[wb]));
+          mbar_expect_tx(&bars->bias_full[wb], a.bias_bytes);
+          bulk_load(sBias + wb * a.bias_bytes, a.w2t + (size_t)slot * a.img_bytes + a.w2t_bytes,
+                    a.bias_bytes, &bars->bias_full[wb]);
+        }
+        __syncwarp();
+        for (int hf = 0; hf < nh; ++hf) {
+          for (int kc = 0; kc < nkc; ++kc) {
+            mbar_wait(&bars->empty[stage], sph ^ 1);
+            if (elect_one()) {
+              if (leader) mbar_expect_tx(&bars->full[stage], 2u * kPairBox);
+              tma_load_2d_pair(sB + stage * kPairBox, &map_w, kc * kKC,
+                               slot * a.H + hf * kHalf + (int)rank * 64, lead(&bars->full[stage]));
+            }
+            __syncwarp();
+            if (++stage == a.stages) {
+              stage = 0;
+              sph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------- MMA issuer (leader) ----
+    if (leader) {
+      const uint32_t id1 = idesc(2 * kTileRows, kHalf, kFmtBF16);
+      const uint32_t id2 = idesc(2 * kTileRows, a.C, kFmtBF16);
+      const uint64_t dA0 = desc_kmajor_sw128(smem_u32(sA));
+      const uint64_t dB0 = desc_kmajor_sw128(smem_u32(sB));
+      const uint64_t dW0 = desc_kmajor_sw128(smem_u32(sW2));
+      int stage = 0;
+      uint32_t sph = 0, u = 0, t = 0;
+      long prev = -1;
+      auto layer2 = [&](uint32_t w) {
+        const uint32_t uw = w / nh, hw = w % nh;
+        const uint32_t rb = w & 1, lb = uw % a.nl, wb = uw & 1;
+        if (hw == 0) {
+          mbar_wait(&bars->w2_full[wb], (uw >> 1) & 1);
+          mbar_wait(&bars->l_empty[lb], ((uw / a.nl) & 1) ^ 1);
+        }
+        mbar_wait(&bars->r_full[rb], (w >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t dW = dW0 + ((wb * w2h) >> 4);
+#pragma unroll
+          for (int k16 = 0; k16 < kHalf / 16; ++k16) {
+            const int kg = hw * kHalf + k16 * 16;
+            mma2_bf16_ts(tmem + kTmemL + lb * a.C, tmem + kTmemR + rb * 64 + k16 * 8,
+                         dW + (((kg / 64) * 1024 + (kg % 64) * 2) >> 4), id2, (hw | k16) != 0);
+          }
+          mma2_commit_mc(&bars->r_empty[rb], 3);
+          if (hw == (uint32_t)nh - 1) {
+            mma2_commit_mc(&bars->l_full[lb], 3);
+            mma2_commit_mc(&bars->w2_empty[wb], 3);
+          }
+        }
+        __syncwarp();
+      };
+      for (int m = pair; m < n_super; m += npairs, ++t) {
+        mbar_wait(&bars->a_full, t & 1);
+        tc_fence_after();
+        for (int e = 0; e < a.n_ent; ++e, ++u) {
+          for (int hf = 0; hf < nh; ++hf) {
+            const uint32_t v = u * nh + hf, zb = v & 1;
+            mbar_wait(&bars->z_empty[zb], ((v >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dz = tmem + kTmemZ + zb * kHalf;
+            for (int kc = 0; kc < nkc; ++kc) {
+              mbar_wait(&bars->full[stage], sph);
+              tc_fence_after();
+              if (elect_one()) {
+                const uint64_t da = dA0 + ((kc * kAChunk) >> 4);
+                const uint64_t db = dB0 + ((stage * kPairBox) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < kKC / 16; ++kk)
+                  mma2_bf16_ss(dz, da + kk * 2, db + kk * 2, id1, (kc | kk) != 0);
+                mma2_commit_mc(&bars->empty[stage], 3);
+              }
+              __syncwarp();
+              if (++stage == a.stages) {
+                stage = 0;
+                sph ^= 1;
+              }
+            }
+            if (elect_one()) mma2_commit_mc(&bars->z_full[zb], 3);
+            __syncwarp();
+            if (prev >= 0) layer2((uint32_t)prev);
+            prev = v;
+          }
+        }
+        if (elect_one()) mma2_commit_mc(&bars->a_empty, 3);
+        __syncwarp();
+      }
+      if (prev >= 0) layer2((uint32_t)prev);
+    }
+  } else {
+    // ---------------------------------------------- epilogue (both CTAs) --
+    const int q = warp & 3;
+    const int cp = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t u = 0;
+    for (int m = pair; m < n_super; m += npairs) {
+      const int R = m * 2 * kTileRows + (int)rank * kTileRows + row;
+      const bool valid = R < a.n_rows;
+      const int p = valid ? R / a.S : 0;
+      const int label = valid ? a.labels[(size_t)a.cams[p] * a.S + (R % a.S)] : -1;
+      for (int e = 0; e < a.n_ent; ++e, ++u) {
+        const uint32_t wb = u & 1;
+        const float* b1 = reinterpret_cast<const float*>(sBias + wb * a.bias_bytes);
+        const float* b2 = b1 + a.H;
+        mbar_wait(&bars->bias_full[wb], (u >> 1) & 1);
+        for (int hf = 0; hf < nh; ++hf) {
+          const uint32_t v = u * nh + hf, zb = v & 1;
+          const int c0 = cp * 64;
+          mbar_wait(&bars->z_full[zb], (v >> 1) & 1);
+          mbar_wait(&bars->r_empty[zb], ((v >> 1) & 1) ^ 1);
+          tc_fence_after();
+          uint32_t r[64];
+          tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0, r);
+          tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0 + 32, r + 32);
+          tmem_ld_wait();
+          const float4* bb = reinterpret_cast<const float4*>(b1 + hf * kHalf + c0);
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float4 b = bb[i];
+            const float z0 = fmaxf(__uint_as_float(r[4 * i + 0]) + b.x, 0.0f);
+            const float z1 = fmaxf(__uint_as_float(r[4 * i + 1]) + b.y, 0.0f);
+            const float z2 = fmaxf(__uint_as_float(r[4 * i + 2]) + b.z, 0.0f);
+            const float z3 = fmaxf(__uint_as_float(r[4 * i + 3]) + b.w, 0.0f);
+            pk[2 * i] = pack_bf16x2(z0, z1);
+            pk[2 * i + 1] = pack_bf16x2(z2, z3);
+          }
+          tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2, pk);
+          tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2 + 16, pk + 16);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive_cluster(lead(&bars->z_empty[zb]));
+            mbar_arrive_cluster(lead(&bars->r_full[zb]));
+          }
+        }
+        if (cp != 0) continue;
+        const uint32_t lb = u % a.nl;
+        mbar_wait(&bars->l_full[lb], (u / a.nl) & 1);
+        tc_fence_after();
+        int best = 0;
+        float bestv = 0.0f;
+        for (int c0 = 0; c0 < a.C; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tmem + lane_base + kTmemL + lb * a.C + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float l = __uint_as_float(r[i]) + b2[c0 + i];
+            if ((c0 | i) == 0 || l > bestv) {
+              bestv = l;
+              best = c0 + i;
+            }
+            if (a.dbg_logits && valid)
+              a.dbg_logits[((size_t)R * a.n_ent + e) * a.C + c0 + i] = l;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_cluster(lead(&bars->l_empty[lb]));
+          mbar_arrive(&bars->bias_empty[wb]);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, valid && best == label);
+        if (lane == 0 && bal) atomicAdd(a.counts + (size_t)p * a.ld + a.ent_col[e], __popc(bal));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the leader's MMAs into the follower's TMEM are all complete
+  if (warp == 1) tmem_dealloc_pair(tmem, 512);
+}
+
 // ------------------------------------------------------------ shadows ------
 // W1^T (bf16, [slot][H][F]) from the fp32 masters W1 [F][H]: 32x32 transpose.
 __global__ void k_shadow_w1t(int F, int H, const int* slots, const float* wbase, size_t wstride,
@@ -459,6 +746,30 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
   return m;
 }
 
+// 5-D view of the per-slot W2^T images for the CTA-pair kernel: (64 bf16 of
+// a 128-byte row, 8 rows, 2 halves, H/64 atoms, slots); one box = one CTA's
+// half (8 rows of every atom), copied as-is (the image is pre-swizzled).
+CUtensorMap make_w2_pair_map(const void* base, uint64_t slots, int H, int C, uint32_t img_bytes) {
+  CUtensorMap m;
+  const cuuint64_t dims[5] = {64, 8, 2, (cuuint64_t)(H / 64), slots};
+  const cuuint64_t strides[4] = {128, 1024, (cuuint64_t)C * 128, img_bytes};
+  const cuuint32_t box[5] = {64, 8, 1, (cuuint32_t)(H / 64), 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base),
+                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) ecco_throw(ECCO_ERR_CUDA, "cuTensorMapEncodeTiled (W2^T pair view) failed");
+  return m;
+}
+
+// The CTA-pair kernel serves dense matrices with C == 16; ECCO_EVAL_PAIR=0
+// forces the single-CTA kernel (tests run both).
+bool pair_enabled(const ecco_config& g) {
+  const char* e = getenv("ECCO_EVAL_PAIR");
+  return g.num_classes == 16 && !(e && e[0] == '0');
+}
+
 int sm_count(int device) {
   static int n = 0;
   if (!n) ECCO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
@@ -506,6 +817,10 @@ void init_shadow(ecco_ctx* ctx, Shadow& sh) {
   sh.map_w = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, kHalf));
   if (g.hidden_dim <= 256)
     sh.map_w_train = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, g.hidden_dim));
+  sh.map_w_pair = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, 64));
+  if (g.num_classes == 16)
+    sh.map_w2_pair = new CUtensorMap(make_w2_pair_map(sh.w2t, slots, g.hidden_dim, g.num_classes,
+                                                      img_bytes(g)));
 }
 
 void free_shadow(Shadow& sh) {
@@ -513,6 +828,8 @@ void free_shadow(Shadow& sh) {
   if (sh.w2t) cudaFree(sh.w2t);
   delete (CUtensorMap*)sh.map_w;
   delete (CUtensorMap*)sh.map_w_train;
+  delete (CUtensorMap*)sh.map_w_pair;
+  delete (CUtensorMap*)sh.map_w2_pair;
   sh = Shadow{};
 }
 
@@ -561,14 +878,37 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
                                    (int)max_smem));
     attr = true;
   }
-  const int grid = std::min(a.n_tiles, sm_count(g.device));
   if (a.n_tiles == 0 || n_ent == 0) return;
   const double flops = 2.0 * live_pairs * g.eval_samples *
                        ((double)g.feat_dim * g.hidden_dim + (double)g.hidden_dim * g.num_classes);
-  const double bytes = live_pairs * g.eval_samples * 0.0 + (double)a.n_rows * g.feat_dim * 2 +
-                       (double)n_ent * (g.feat_dim * g.hidden_dim * 2.0 + a.w2t_bytes) +
+  const double bytes = (double)a.n_rows * g.feat_dim * 2 +
+                       (double)n_ent * (g.feat_dim * g.hidden_dim * 2.0 + a.img_bytes) +
                        4.0 * live_pairs;
-  ECCO_TIMED(ctx, d_tile_ebeg ? ECCO_KSTAT_EVAL_PAIRS : ECCO_KSTAT_EVAL_MATRIX, flops, bytes,
+  const int kind = d_tile_ebeg ? ECCO_KSTAT_EVAL_PAIRS : ECCO_KSTAT_EVAL_MATRIX;
+  if (!d_tile_ebeg && !d_probe_slot && sh.map_w2_pair && pair_enabled(g)) {
+    // CTA-pair kernel: 256-row super tiles, half a W1^T box per CTA per stage
+    const size_t pfixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)(a.H / 64) * 1024 +
+                          2 * (size_t)a.bias_bytes + sizeof(PairBars);
+    a.stages = (int)std::min<size_t>(kMaxPairStages, (max_smem - pfixed) / kPairBox);
+    ECCO_REQUIRE(a.stages >= 2, "fused eval (pair): shared memory too small for the pipeline");
+    const size_t psmem = pfixed + (size_t)a.stages * kPairBox;
+    static bool pattr = false;
+    if (!pattr) {
+      ECCO_CUDA(cudaFuncSetAttribute(k_eval_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)max_smem));
+      pattr = true;
+    }
+    const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
+    const int pairs = std::min(n_super, sm_count(g.device) / 2);
+    ECCO_TIMED(ctx, kind, flops, bytes,
+               (k_eval_pair<<<2 * pairs, kThreads, psmem, ctx->stream>>>(
+                   *(const CUtensorMap*)ctx->map_x, *(const CUtensorMap*)sh.map_w_pair,
+                   *(const CUtensorMap*)sh.map_w2_pair, a)));
+    ECCO_LAUNCHED(ctx);
+    return;
+  }
+  const int grid = std::min(a.n_tiles, sm_count(g.device));
+  ECCO_TIMED(ctx, kind, flops, bytes,
              (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
                                                                   *(const CUtensorMap*)sh.map_w, a)));
   ECCO_LAUNCHED(ctx);

@@ -20,6 +20,14 @@ import paper_2512_11727_b200 as ecco
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(params=["pair", "single"], autouse=True)
+def eval_kernel(request, monkeypatch):
+    """Every test runs on both dense-matrix kernels: the CTA-pair
+    (cta_group::2) kernel and the single-CTA kernel (ECCO_EVAL_PAIR=0)."""
+    monkeypatch.setenv("ECCO_EVAL_PAIR", "0" if request.param == "single" else "1")
+    return request.param
+
 DIMS = dict(feat_dim=512, hidden_dim=256, num_classes=16, minibatch=128, ring_frames=64,
             eval_samples=64)
 
