@@ -9,19 +9,23 @@
 //            (bf16, exact) that stays in shared memory for the whole step
 //   fwd      Z = X . W1                 tcgen05 kind::f16, N = H, TMEM
 //            (W1^T bf16 shadow streamed by TMA, 2 stages)
-//   head     logits = relu(Z+b1) . W2 + b2, softmax, dL, dH = (dL . W2^T) *
-//            (Z+b1 > 0), dW2 / db2 / db1 reductions -- CUDA cores, W2 in smem
+//   head     logits = relu(Z+b1) . W2 + b2 (two threads per row, half the
+//            hidden columns each), softmax, dL, dH = (dL . W2^T) * (Z+b1 > 0)
+//            -- CUDA cores, W2 in smem; no block-wide syncs per column
+//   dW2/db1  dW2 = R^T . dL and db1 = dH^T . 1 as tcgen05 MMAs (M = 128
+//            hidden units per tile, N = 16): R = bf16(relu(Z+b1)) is written
+//            MN-major over the X tile once dW1 no longer needs it, dL and a
+//            ones tile as 32B-swizzled MN-major B operands
 //   dW1      G = X^T . dH               tcgen05 kind::f16 with BOTH operands
 //            MN-major (X^T is the same smem tile read transposed; dH is
-//            written MN-major by the head), M = 128 features per tile, two
-//            TMEM accumulators
+//            written MN-major by the head), M = 128 features per tile
 //   update   W1 -= lr * G (fp32 masters, stored transposed [H][F] in this
 //            mode so the read-modify-write is coalesced) and the bf16 W1^T
 //            shadow rewritten for the next step's forward
 //
-// Numerics: X exact (bf16 frames), W1 and dH rounded to bf16 at the two
-// contractions, fp32 accumulation, fp32 masters; the head is fp32 in the
-// oracle's operation order.  Tolerance in tests/test_gpu_learned.py.
+// Numerics: X exact (bf16 frames); W1, dH, R and dL rounded to bf16 at the
+// tensor-core contractions, fp32 accumulation, fp32 masters; logits / softmax
+// / dH fp32 on CUDA cores.  Tolerance in tests/test_gpu_learned.py.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -65,24 +69,22 @@ struct TrainArgs {
 };
 
 struct Layout {
-  uint32_t x, wb, w2, dl, r, dh, rows, labs, b2, loss, bars, tmem, total;
+  uint32_t x, wb, w2, dl, pl, rows, labs, b2, loss, bars, tmem, total;
 };
 
 __host__ __device__ inline Layout layout(int F, int H, int C) {
   Layout L{};
   uint32_t o = 0;
   L.x = o;
-  o += (uint32_t)(F / 64) * 16384u;  // X: F/64 swizzle chunks of 128 rows x 128 B
+  o += (uint32_t)(F / 64) * 16384u;  // X (later R): F/64 swizzle chunks of 128 rows x 128 B
   L.wb = o;
   o += (uint32_t)H * 256u;  // 2 W1^T stages (H x 64 bf16) == dH (128 x H bf16)
   L.w2 = o;
   o += (uint32_t)H * C * 4u;
   L.dl = o;
-  o += (uint32_t)kB * C * 4u;
-  L.r = o;
-  o += (uint32_t)kB * kHC * 4u;
-  L.dh = o;
-  o += (uint32_t)kB * kHC * 4u;
+  o += (uint32_t)kB * C * 4u;  // dL fp32 [row][class]
+  L.pl = o;
+  o += (uint32_t)kB * C * 4u;  // partial logits of the second half; later dL / ones B tiles
   L.rows = o;
   o += kB * 8u;
   L.labs = o;
@@ -93,11 +95,18 @@ __host__ __device__ inline Layout layout(int F, int H, int C) {
   o += kB * 4u;
   o = (o + 7u) & ~7u;
   L.bars = o;
-  o += 10u * 8u;  // full[2] empty[2] zfull gfull[2] gempty[2]
+  o += 8u * 8u;  // full[2] empty[2] zfull gfull gempty dfull
   L.tmem = o;
   o += 16u;
   L.total = o;
   return L;
+}
+
+// MN-major operand with 32-byte swizzle (16 two-byte elements per row of an
+// atom, 8 K rows = 256 B): element (n, k) of a [K][16] tile.
+__device__ __forceinline__ uint32_t sw32_off(int n, int k) {
+  return (uint32_t)k * 32u + ((((uint32_t)n >> 3) ^ (((uint32_t)k >> 2) & 1u)) << 4) +
+         ((uint32_t)n & 7u) * 2u;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -112,17 +121,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sWB = smem + L.wb;
   float* sW2 = (float*)(smem + L.w2);
   float* sDL = (float*)(smem + L.dl);
-  float* sR = (float*)(smem + L.r);
-  float* sDH = (float*)(smem + L.dh);
+  float* sPL = (float*)(smem + L.pl);
   int64_t* sRow = (int64_t*)(smem + L.rows);
   int* sLab = (int*)(smem + L.labs);
   float* sB2 = (float*)(smem + L.b2);
   float* sLoss = (float*)(smem + L.loss);
   uint64_t* full = (uint64_t*)(smem + L.bars);  // [2]
   uint64_t* empty = full + 2;                   // [2]
-  uint64_t* zfull = full + 4;                   // [1]
-  uint64_t* gfull = full + 5;                   // [2]
-  uint64_t* gempty = full + 7;                  // [2]
+  uint64_t* zfull = full + 4;
+  uint64_t* gfull = full + 5;
+  uint64_t* gempty = full + 6;
+  uint64_t* dfull = full + 7;
   uint32_t* sTmem = (uint32_t*)(smem + L.tmem);
   const uint32_t stage_bytes = (uint32_t)H * 128u;
 
@@ -141,10 +150,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&gfull[s], 1);
-      mbar_init(&gempty[s], 8);
     }
     mbar_init(zfull, 1);
+    mbar_init(gfull, 1);
+    mbar_init(gempty, 8);
+    mbar_init(dfull, 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(sTmem, 512);
@@ -219,38 +229,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ------------------------------------------------------- head: logits --
-  const bool rowthr = warp >= 4;
-  const int s = (warp - 4) * 32 + lane;  // minibatch row of a row thread (TMEM lane)
-  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-  float dl[kC];
-  if (rowthr) {
-    mbar_wait(zfull, 0);
-    tc_fence_after();
-    float lg[kC];
+  // Two threads per minibatch row: warps w and w+4 share TMEM lane quadrant
+  // w%4 and take hidden columns [part*H/2, (part+1)*H/2).
+  const int q = warp & 3, part = warp >> 2;
+  const int s = q * 32 + lane;  // minibatch row (TMEM lane)
+  const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+  const int hh = H / 2, h_lo = part * hh;
+  mbar_wait(zfull, 0);
+  tc_fence_after();
+  float lg[kC];
 #pragma unroll
-    for (int c = 0; c < kC; ++c) lg[c] = 0.0f;
-    for (int c0 = 0; c0 < H; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32_nowait(tmem + lane_base + c0, r);
-      tmem_ld_wait();
+  for (int c = 0; c < kC; ++c) lg[c] = 0.0f;
+  for (int c0 = h_lo; c0 < h_lo + hh; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32_nowait(tmem + lane_base + c0, r);
+    tmem_ld_wait();
 #pragma unroll 4
-      for (int i = 0; i < 32; ++i) {
-        const float z = __fadd_rn(__uint_as_float(r[i]), b1[c0 + i]);
-        const float rz = z > 0.0f ? z : 0.0f;
-        const float4* w = reinterpret_cast<const float4*>(sW2 + (c0 + i) * kC);
+    for (int i = 0; i < 32; ++i) {
+      const float z = __fadd_rn(__uint_as_float(r[i]), b1[c0 + i]);
+      const float rz = z > 0.0f ? z : 0.0f;
+      const float4* w = reinterpret_cast<const float4*>(sW2 + (c0 + i) * kC);
 #pragma unroll
-        for (int c4 = 0; c4 < kC / 4; ++c4) {
-          const float4 v = w[c4];
-          lg[4 * c4 + 0] = __fmaf_rn(rz, v.x, lg[4 * c4 + 0]);
-          lg[4 * c4 + 1] = __fmaf_rn(rz, v.y, lg[4 * c4 + 1]);
-          lg[4 * c4 + 2] = __fmaf_rn(rz, v.z, lg[4 * c4 + 2]);
-          lg[4 * c4 + 3] = __fmaf_rn(rz, v.w, lg[4 * c4 + 3]);
-        }
+      for (int c4 = 0; c4 < kC / 4; ++c4) {
+        const float4 v = w[c4];
+        lg[4 * c4 + 0] = __fmaf_rn(rz, v.x, lg[4 * c4 + 0]);
+        lg[4 * c4 + 1] = __fmaf_rn(rz, v.y, lg[4 * c4 + 1]);
+        lg[4 * c4 + 2] = __fmaf_rn(rz, v.z, lg[4 * c4 + 2]);
+        lg[4 * c4 + 3] = __fmaf_rn(rz, v.w, lg[4 * c4 + 3]);
       }
     }
-    // softmax cross-entropy in the oracle's order (orc_sgd_step)
+  }
+  if (part == 1) {
 #pragma unroll
-    for (int c = 0; c < kC; ++c) lg[c] = __fadd_rn(lg[c], sB2[c]);
+    for (int c = 0; c < kC; ++c) sPL[s * kC + c] = lg[c];
+  }
+  __syncthreads();
+  if (part == 0) {  // softmax cross-entropy (orc_sgd_step's order after the sum)
+#pragma unroll
+    for (int c = 0; c < kC; ++c) lg[c] = __fadd_rn(__fadd_rn(lg[c], sPL[s * kC + c]), sB2[c]);
     float m = lg[0];
 #pragma unroll
     for (int c = 1; c < kC; ++c) m = lg[c] > m ? lg[c] : m;
@@ -262,137 +278,104 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const float invB = __fdiv_rn(1.0f, (float)kB);
     const int y = sLab[s];
-#pragma unroll
-    for (int c = 0; c < kC; ++c) {
-      dl[c] = __fmul_rn(__fsub_rn(__fdiv_rn(e[c], sum), c == y ? 1.0f : 0.0f), invB);
-      sDL[s * kC + c] = dl[c];
-    }
     float ly = lg[0];
 #pragma unroll
-    for (int c = 1; c < kC; ++c) ly = c == y ? lg[c] : ly;
+    for (int c = 0; c < kC; ++c) {
+      sDL[s * kC + c] = __fmul_rn(__fsub_rn(__fdiv_rn(e[c], sum), c == y ? 1.0f : 0.0f), invB);
+      ly = c == y ? lg[c] : ly;
+    }
     sLoss[s] = logf(sum) - (ly - m);
   }
   __syncthreads();
 
-  // ---------------------------------------- head: backward, 8 columns a pass --
-  for (int h0 = 0; h0 < H; h0 += kHC) {
-    if (rowthr) {
-      uint32_t r[kHC];
-      tmem_ld8_nowait(tmem + lane_base + h0, r);
+  // ---------------------------------------------- head: dH (no block syncs) --
+  {
+    float dl[kC];
+#pragma unroll
+    for (int c = 0; c < kC; ++c) dl[c] = sDL[s * kC + c];
+    for (int c0 = h_lo; c0 < h_lo + hh; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32_nowait(tmem + lane_base + c0, r);
       tmem_ld_wait();
-      float dh[kHC];
 #pragma unroll
-      for (int i = 0; i < kHC; ++i) {
-        const int h = h0 + i;
-        const float z = __fadd_rn(__uint_as_float(r[i]), b1[h]);
-        float acc = 0.0f;
-        if (z > 0.0f) {
+      for (int g8 = 0; g8 < 4; ++g8) {
+        float dh[8];
 #pragma unroll
-          for (int c = 0; c < kC; ++c) acc = __fmaf_rn(dl[c], sW2[h * kC + c], acc);
-        }
-        dh[i] = acc;
-        sR[s * kHC + i] = z > 0.0f ? z : 0.0f;
-        sDH[s * kHC + i] = acc;
-      }
-      // dH as the MN-major B operand of dW1: element (s, h), 64-column atoms
-      const int hc = h0 >> 6, c16 = (h0 & 63) >> 3;
-      uint4 pk;
-      pk.x = pack_bf16x2(dh[0], dh[1]);
-      pk.y = pack_bf16x2(dh[2], dh[3]);
-      pk.z = pack_bf16x2(dh[4], dh[5]);
-      pk.w = pack_bf16x2(dh[6], dh[7]);
-      *reinterpret_cast<uint4*>(sWB + hc * 16384 + s * 128 + ((c16 ^ (s & 7)) << 4)) = pk;
-    }
-    __syncthreads();
-    // dW2 rows h0..h0+7 (their dH is done) and db1: 136 sums over the 128
-    // rows, each split across the two halves of a warp (lanes l, l+16 take
-    // rows of opposite parity) with 4 independent accumulators, combined by
-    // one shuffle.  Warps 0-7 x 16 lane pairs = 128 dW2 outputs; the 8 db1
-    // outputs go to warps 0-7 as a second item.
-    {
-      const int half = lane >> 4, li = lane & 15;
-      for (int item = 0; item < 2; ++item) {
-        const int o = item == 0 ? warp * 16 + li : kHC * kC + warp;  // output id
-        const bool active = item == 0 || li == 0;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        if (active) {
-          if (o < kHC * kC) {
-            const int hi = o / kC, c = o % kC;
-#pragma unroll 4
-            for (int q = half; q < kB; q += 8) {
-              a0 = __fmaf_rn(sR[q * kHC + hi], sDL[q * kC + c], a0);
-              a1 = __fmaf_rn(sR[(q + 2) * kHC + hi], sDL[(q + 2) * kC + c], a1);
-              a2 = __fmaf_rn(sR[(q + 4) * kHC + hi], sDL[(q + 4) * kC + c], a2);
-              a3 = __fmaf_rn(sR[(q + 6) * kHC + hi], sDL[(q + 6) * kC + c], a3);
-            }
-          } else {
-            const int hi = o - kHC * kC;
-#pragma unroll 4
-            for (int q = half; q < kB; q += 8) {
-              a0 += sDH[q * kHC + hi];
-              a1 += sDH[(q + 2) * kHC + hi];
-              a2 += sDH[(q + 4) * kHC + hi];
-              a3 += sDH[(q + 6) * kHC + hi];
-            }
+        for (int i = 0; i < 8; ++i) {
+          const int h = c0 + g8 * 8 + i;
+          const float z = __fadd_rn(__uint_as_float(r[g8 * 8 + i]), b1[h]);
+          float acc = 0.0f;
+          const float4* w = reinterpret_cast<const float4*>(sW2 + h * kC);
+#pragma unroll
+          for (int c4 = 0; c4 < kC / 4; ++c4) {
+            const float4 v = w[c4];
+            acc = __fmaf_rn(dl[4 * c4 + 0], v.x, acc);
+            acc = __fmaf_rn(dl[4 * c4 + 1], v.y, acc);
+            acc = __fmaf_rn(dl[4 * c4 + 2], v.z, acc);
+            acc = __fmaf_rn(dl[4 * c4 + 3], v.w, acc);
           }
+          dh[i] = z > 0.0f ? acc : 0.0f;
         }
-        float acc = (a0 + a1) + (a2 + a3);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-        if (active && half == 0) {
-          if (o < kHC * kC) {
-            const int h = h0 + o / kC, c = o % kC;
-            sW2[h * kC + c] = __fmaf_rn(-lr, acc, sW2[h * kC + c]);
-          } else {
-            const int h = h0 + (o - kHC * kC);
-            b1[h] = __fmaf_rn(-lr, acc, b1[h]);
-          }
-        }
+        // dH as the MN-major operand (row s, 64-column atoms): dW1's B, db1's A
+        const int h0 = c0 + g8 * 8;
+        uint4 pk;
+        pk.x = pack_bf16x2(dh[0], dh[1]);
+        pk.y = pack_bf16x2(dh[2], dh[3]);
+        pk.z = pack_bf16x2(dh[4], dh[5]);
+        pk.w = pack_bf16x2(dh[6], dh[7]);
+        *reinterpret_cast<uint4*>(sWB + (h0 >> 6) * 16384 + s * 128 +
+                                  ((((h0 & 63) >> 3) ^ (s & 7)) << 4)) = pk;
       }
     }
-    __syncthreads();
   }
-  if (tid < kC) {
-    float acc = 0.0f;
-    for (int q = 0; q < kB; ++q) acc = __fadd_rn(acc, sDL[q * kC + tid]);
-    b2[tid] = __fmaf_rn(-lr, acc, sB2[tid]);
+  // dL and a ones tile as 32B-swizzled MN-major B operands (N = 16, K = rows)
+  {
+    uint8_t* sDLb = reinterpret_cast<uint8_t*>(sPL);  // partial logits are consumed
+    uint8_t* sOnes = sDLb + kB * 32;
+    if (part == 0) {
+#pragma unroll
+      for (int c = 0; c < kC; c += 2) {
+        const uint32_t pk = pack_bf16x2(sDL[s * kC + c], sDL[s * kC + c + 1]);
+        *reinterpret_cast<uint32_t*>(sDLb + sw32_off(c, s)) = pk;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < kC; c += 2)
+        *reinterpret_cast<uint32_t*>(sOnes + sw32_off(c, s)) = 0x3F803F80u;  // bf16 1.0 x 2
+    }
   }
-  for (int i = tid; i < H * kC / 4; i += kThreads)
-    reinterpret_cast<float4*>(W2)[i] = reinterpret_cast<const float4*>(sW2)[i];
-  fence_async_smem();  // dH (generic stores) -> tensor-core reads
+  fence_async_smem();  // dH / dL / ones (generic stores) -> tensor-core reads
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
 
   // ------------------------------------------------- dW1 = X^T . dH, update --
+  // One 256-column accumulator at TMEM [256, 512) (Z stays in [0, 256) for R).
   const int nmt = F / 128;
   const uint32_t idg = idesc_major(128, H, kFmtBF16, 1, 1);
   auto issue = [&](int mt) {
     if (elect_one()) {
-      const int gb = mt & 1;
 #pragma unroll
       for (int k16 = 0; k16 < kB / 16; ++k16) {
         const uint64_t da =
             desc_mnmajor_sw128(smem_u32(sX) + (2 * mt) * 16384 + k16 * 2048, 16384, 1024);
         const uint64_t db = desc_mnmajor_sw128(smem_u32(sWB) + k16 * 2048, 16384, 1024);
-        mma_bf16_ss(tmem + gb * 256, da, db, idg, k16 != 0);
+        mma_bf16_ss(tmem + 256, da, db, idg, k16 != 0);
       }
-      mma_commit(&gfull[gb]);
+      mma_commit(gfull);
     }
     __syncwarp();
   };
-  if (warp == 0) {
-    for (int mt = 0; mt < 2 && mt < nmt; ++mt) issue(mt);
-  }
-  const int q = warp & 3, cp = warp >> 2;
+  if (warp == 0) issue(0);
+  const int cp = part;
   const int hw = H / 2;
   for (int mt = 0; mt < nmt; ++mt) {
-    const int gb = mt & 1;
-    mbar_wait(&gfull[gb], (mt >> 1) & 1);
+    mbar_wait(gfull, mt & 1);
     tc_fence_after();
     const int f = mt * 128 + q * 32 + lane;
     for (int c0 = cp * hw; c0 < (cp + 1) * hw; c0 += 32) {
       uint32_t r[32];
-      tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + gb * 256 + c0, r);
+      tmem_ld32_nowait(tmem + lane_base + 256 + c0, r);
       // masters are [H][F]: for each h the warp's 32 lanes (32 consecutive
       // f) touch one 128-byte line -- coalesced, 32 independent loads
       float w[32];
@@ -408,15 +391,93 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&gempty[gb]);
-    if (warp == 0 && mt + 2 < nmt) {
-      mbar_wait(&gempty[gb], (mt >> 1) & 1);
+    if (lane == 0) mbar_arrive(gempty);
+    if (warp == 0 && mt + 1 < nmt) {
+      mbar_wait(gempty, mt & 1);
       tc_fence_after();
-      issue(mt + 2);
+      issue(mt + 1);
     }
   }
 
+  // ------------------------------ dW2 = R^T . dL, db1 = dH^T . 1 (tensor) --
+  // The last dW1 MMA has completed (every thread waited on it), so the X tile
+  // is free: R = bf16(relu(Z + b1)) goes there, MN-major like dH.
+  for (int c0 = h_lo; c0 < h_lo + hh; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32_nowait(tmem + lane_base + c0, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int g8 = 0; g8 < 4; ++g8) {
+      const int h0 = c0 + g8 * 8;
+      float rz[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float z = __fadd_rn(__uint_as_float(r[g8 * 8 + i]), b1[h0 + i]);
+        rz[i] = z > 0.0f ? z : 0.0f;
+      }
+      uint4 pk;
+      pk.x = pack_bf16x2(rz[0], rz[1]);
+      pk.y = pack_bf16x2(rz[2], rz[3]);
+      pk.z = pack_bf16x2(rz[4], rz[5]);
+      pk.w = pack_bf16x2(rz[6], rz[7]);
+      *reinterpret_cast<uint4*>(sX + (h0 >> 6) * 16384 + s * 128 +
+                                ((((h0 & 63) >> 3) ^ (s & 7)) << 4)) = pk;
+    }
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t idw = idesc_major(128, kC, kFmtBF16, 1, 1);
+      const uint32_t dlb = smem_u32(sPL), onesb = dlb + kB * 32;
+      for (int t2 = 0; t2 < H / 128; ++t2) {
+#pragma unroll
+        for (int k16 = 0; k16 < kB / 16; ++k16) {
+          const uint64_t bdl = smem_desc(dlb + k16 * 512, 256, 256, kSwizzle32B);
+          const uint64_t bon = smem_desc(onesb + k16 * 512, 256, 256, kSwizzle32B);
+          const uint64_t ar =
+              desc_mnmajor_sw128(smem_u32(sX) + (2 * t2) * 16384 + k16 * 2048, 16384, 1024);
+          const uint64_t ad =
+              desc_mnmajor_sw128(smem_u32(sWB) + (2 * t2) * 16384 + k16 * 2048, 16384, 1024);
+          mma_bf16_ss(tmem + t2 * kC, ar, bdl, idw, k16 != 0);          // dW2 tile
+          mma_bf16_ss(tmem + 64 + t2 * kC, ad, bon, idw, k16 != 0);     // db1 tile
+        }
+      }
+      mma_commit(dfull);
+    }
+    __syncwarp();
+  }
+  mbar_wait(dfull, 0);
+  tc_fence_after();
+  if (part < H / 128) {  // thread owns hidden unit h = part*128 + lane quadrant row
+    const int h = part * 128 + q * 32 + lane;
+    uint32_t r[16], rb[16];
+    tmem_ld16_nowait(tmem + lane_base + part * kC, r);
+    tmem_ld16_nowait(tmem + lane_base + 64 + part * kC, rb);
+    tmem_ld_wait();
+    float4* w2row = reinterpret_cast<float4*>(W2 + (size_t)h * kC);
+#pragma unroll
+    for (int c4 = 0; c4 < kC / 4; ++c4) {
+      const float4 o = reinterpret_cast<const float4*>(sW2 + h * kC)[c4];
+      float4 n;
+      n.x = __fmaf_rn(-lr, __uint_as_float(r[4 * c4 + 0]), o.x);
+      n.y = __fmaf_rn(-lr, __uint_as_float(r[4 * c4 + 1]), o.y);
+      n.z = __fmaf_rn(-lr, __uint_as_float(r[4 * c4 + 2]), o.z);
+      n.w = __fmaf_rn(-lr, __uint_as_float(r[4 * c4 + 3]), o.w);
+      w2row[c4] = n;
+    }
+    b1[h] = __fmaf_rn(-lr, __uint_as_float(rb[0]), b1[h]);
+  }
+  if (tid < kC) {
+    float acc = 0.0f;
+    for (int q2 = 0; q2 < kB; ++q2) acc = __fadd_rn(acc, sDL[q2 * kC + tid]);
+    b2[tid] = __fmaf_rn(-lr, acc, sB2[tid]);
+  }
+
   // ------------------------------------------------------------- loss, end --
+  tc_fence_before();
   __syncthreads();
   if (tid == 0) {
     double acc = 0.0;
@@ -435,7 +496,7 @@ namespace fused {
 bool train_supported(const ecco_ctx* ctx) {
   const ecco_config& g = ctx->cfg;
   if (g.minibatch != kB || g.num_classes != kC || g.feat_dim % 128 || g.feat_dim > 512 ||
-      (g.hidden_dim != 128 && g.hidden_dim != 256))
+      g.hidden_dim != 256)
     return false;
   return layout(g.feat_dim, g.hidden_dim, kC).total <= 232448;
 }

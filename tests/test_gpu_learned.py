@@ -159,7 +159,8 @@ def test_learned_simulation_runs_and_groups():
 # two contractions run tcgen05 kind::f16: X is exact (bf16 frames); W1 is the
 # bf16 (round-to-nearest-even) shadow of the fp32 master in the forward, and
 # dH is rounded to bf16 for dW1 = X^T . dH; accumulation and the head are
-# fp32.  Two checks:
+# fp32; dW2 = R^T . dL and db1 = dH^T . 1 also run on the tensor cores with
+# bf16 R, dL, dH.  Two checks:
 #  * against a float64 restatement of the SGD step that applies exactly that
 #    rounding (_step_emulated below): agreement to 1e-3 of the update (measured
 #    7e-5) proves
@@ -182,8 +183,9 @@ def _bf16(a):
 
 
 def _step_emulated(x, y, w, lr):
-    """One SGD step (orc_sgd_step's math) in float64 with the MMA operands
-    rounded to bf16 as the fused kernel feeds the tensor cores."""
+    """One SGD step (orc_sgd_step's math) in float64 with the tensor-core
+    operands rounded to bf16 as the fused kernel feeds them: W1 (forward),
+    dH (dW1 and db1), R = relu(Z) and dL (dW2)."""
     w1, b1, w2, b2 = [np.asarray(t, np.float64) for t in w]
     B, F = x.shape
     H, Cc = b1.size, b2.size
@@ -197,8 +199,10 @@ def _step_emulated(x, y, w, lr):
     P[np.arange(B), y] -= 1
     DL = P / B
     DH = (DL @ W2.T) * (Z > 0)
-    return [W1 - lr * (X.T @ _bf16(DH.astype(np.float32))), b1 - lr * DH.sum(0),
-            W2 - lr * (R.T @ DL), b2 - lr * DL.sum(0)]
+    DHb = _bf16(DH.astype(np.float32))
+    return [W1 - lr * (X.T @ DHb), b1 - lr * DHb.sum(0),
+            W2 - lr * (_bf16(R.astype(np.float32)).T @ _bf16(DL.astype(np.float32))),
+            b2 - lr * DL.sum(0)]
 
 
 # The unfused tensor-core kernels (tc_kernels.cu, kind::tf32) still serve
