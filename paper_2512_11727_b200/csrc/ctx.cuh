@@ -99,7 +99,6 @@ struct Shadow {
   uint16_t* w1t = nullptr;
   uint8_t* w2t = nullptr;
   void* map_w = nullptr;        // CUtensorMap*, {64, 128} boxes (evaluation)
-  void* map_w_train = nullptr;  // CUtensorMap*, {64, H} boxes (fused SGD step)
   void* map_w_pair = nullptr;   // CUtensorMap*, {64, 64} boxes (CTA-pair evaluation)
   void* map_w2_pair = nullptr;  // CUtensorMap*, 5-D view of the W2^T images per CTA half
 };
@@ -304,13 +303,14 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
 void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* d_mask,
                    double* d_out);
 bool train_supported(const ecco_ctx* ctx);
-// One fused SGD step (sample, gather, fwd, head, bwd, update) for every job
-// whose step budget is not spent; W1^T shadow `sh` kept in sync.
-void train_step(ecco_ctx* ctx, const Shadow& sh, int n_jobs, const int* d_slots,
-                const int* d_job_ids, const int* d_steps, const int* d_src_off,
-                const int* d_src_cam, const double* d_src_frac, const int* d_micro_base,
-                int micro_add, int window, int step, float* wbase, size_t wstride, int loss_t,
-                double live_rows);
+// Fused SGD chain (train_kernels.cu): every job's steps[j] SGD steps of one
+// micro-window in ONE launch, one thread-block cluster per job with the fp32
+// masters resident in TMEM; writes the bf16 W1^T shadow `sh` (if given).
+void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,
+                 const int* d_job_ids, const int* d_steps, const int* h_steps,
+                 const int* d_src_off, const int* d_src_cam, const double* d_src_frac,
+                 const int* d_micro_base, int micro_add, int window, float* wbase, size_t wstride,
+                 int loss_t);
 }  // namespace fused
 
 namespace lbackend {

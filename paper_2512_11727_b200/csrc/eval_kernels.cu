@@ -815,8 +815,6 @@ void init_shadow(ecco_ctx* ctx, Shadow& sh) {
   ECCO_CUDA(cudaMalloc((void**)&sh.w1t, slots * g.hidden_dim * g.feat_dim * 2));
   ECCO_CUDA(cudaMalloc((void**)&sh.w2t, slots * img_bytes(g)));
   sh.map_w = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, kHalf));
-  if (g.hidden_dim <= 256)
-    sh.map_w_train = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, g.hidden_dim));
   sh.map_w_pair = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, 64));
   if (g.num_classes == 16)
     sh.map_w2_pair = new CUtensorMap(make_w2_pair_map(sh.w2t, slots, g.hidden_dim, g.num_classes,
@@ -827,7 +825,6 @@ void free_shadow(Shadow& sh) {
   if (sh.w1t) cudaFree(sh.w1t);
   if (sh.w2t) cudaFree(sh.w2t);
   delete (CUtensorMap*)sh.map_w;
-  delete (CUtensorMap*)sh.map_w_train;
   delete (CUtensorMap*)sh.map_w_pair;
   delete (CUtensorMap*)sh.map_w2_pair;
   sh = Shadow{};

@@ -856,19 +856,10 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     // weights of state t are addressed as wbase + slot * spec_stride
     float* wt = ctx->d_wspec + (size_t)(t - 1) * np;
     // the per-slot stride for kernels is spec_stride: pass n_params = spec_stride
-    if (ctx->fused_train) {
-      // one fused launch per SGD step for all jobs; the spec shadow (W1^T
-      // bf16) of snapshot t is rebuilt from its fp32 copy, then kept in sync
-      // by every step
-      fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots);
-      for (int step = 0; step < max_steps; ++step) {
-        int live = 0;
-        for (int j = 0; j < n_jobs; ++j) live += step < h_steps[j];
-        fused::train_step(ctx, ctx->sh_spec, n_jobs, d_slots, d_job_ids, d_steps, d_src_off,
-                          d_src_cam, d_src_frac, d_micro_base, t - 1, window, step, wt, spec_stride,
-                          t - 1, (double)live * g.B);
-      }
-    }
+    if (ctx->fused_train)  // one launch: every job's whole micro-window on chip
+      fused::train_chain(ctx, &ctx->sh_spec, n_jobs, d_slots, d_job_ids, d_steps, h_steps,
+                         d_src_off, d_src_cam, d_src_frac, d_micro_base, t - 1, window, wt,
+                         spec_stride, t - 1);
     for (int step = 0; step < (ctx->fused_train ? 0 : max_steps); ++step) {
       const Gate gate{d_steps, step, g.B};
       int live = 0;
