@@ -7,24 +7,26 @@
 //
 // Cluster of H/64 CTAs; CTA r owns hidden units [64r, 64r+64):
 //   TMEM     fp32 master slice W1[:, 64r:64r+64] (F/128 tiles of 128 lanes x
-//            64 columns) and the dW1 accumulator of the same shape; the
-//            forward accumulator Z (128 rows x 64) aliases dW1's first tile
+//            64 columns), the forward / dH accumulators (128 x 64), the
+//            partial logits (128 x 16), dW2 (64 x 16) and dW1 (up to two
+//            128 x 64 tiles per pass)
 //   smem     X tile (128 sampled rows, bf16, 128B-swizzled K-major; also read
-//            MN-major as X^T), the bf16 W1^T operand built from the master,
-//            W2/b1 slices, b2, dL
-//   step     sample + gather X (cp.async, overlapped with the previous
-//            step's update) -> Z = X.W1 (tcgen05 kind::f16, N = 64) ->
-//            partial logits relu(Z+b1).W2 of the CTA's 64 hidden units, sent
-//            to the CTA owning the row block over DSMEM -> owner sums the
-//            partials in fixed order, softmax, dL, broadcasts dL rows to the
-//            cluster -> dH = (dL.W2^T)*(Z>0) -> dW1 = X^T.dH (tcgen05, both
-//            operands MN-major) while dW2 = R^T.dL, db1, db2 run on the CUDA
-//            cores -> master update in TMEM, bf16 operand rewritten
+//            MN-major as X^T), the bf16 W1 operand built from the master, the
+//            bf16 W2 slice image, R / dH / dL operands, fp32 W2/b1 slices, b2
+//   step     Z = X.W1 (tcgen05 kind::f16, N = 64) -> R = relu(Z+b1) ->
+//            partial logits R.W2 (tcgen05, N = 16) sent to the CTA owning the
+//            row block by st.async over DSMEM -> owner (4 threads per row)
+//            sums the partials in fixed order, softmax, dL, broadcasts dL
+//            rows -> dL.W2^T and dW2 = R^T.dL (tcgen05) -> dH =
+//            (dL.W2^T)*(Z>0) -> dW1 = X^T.dH and db1 = dH^T.1 (tcgen05, in
+//            two passes at F = 512) -> master update in TMEM, bf16 operands
+//            rewritten; the next step's rows are prefetched to L2 while dL is
+//            in flight and gathered (cp.async) into each X chunk as soon as
+//            the dW1 pass reading it completes
 //
-// Numerics: X exact (bf16 frames); W1 rounded to bf16 for the forward and dH
-// rounded to bf16 for dW1 and db1; fp32 accumulation, fp32 masters; the head
-// (logits, softmax, dL, dH) and dW2 = R^T.dL are fp32 on CUDA cores.
-// Tolerance in tests/test_gpu_learned.py.
+// Numerics: X exact (bf16 frames); every tensor-core operand bf16 (W1, R,
+// W2, dL, dH), fp32 accumulation, fp32 masters; bias adds, softmax, dL and
+// db2 fp32 on CUDA cores.  Tolerance in tests/test_gpu_learned.py.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -80,29 +82,37 @@ __global__ void k_chain_rows(LDims g, uint64_t seed, const int* job_ids, const i
 }
 
 struct Layout {
-  uint32_t x, sc, recv, dl, w2, b1, b2, rows, labs, loss, bars, tmem, total;
+  uint32_t x, sc, dlb, ones, w2i, dl, recv, w2, b1, b2, b2p, rows, labs, loss, bars, tmem, total;
 };
 
-// sc: the bf16 W1 operand (MN-major: F rows of 64 hidden units, 128 B); between
-// the forward MMA and the update it holds dH (MN-major, 16 KB) and R (fp32,
-// 32 KB) instead.
+// sc: the bf16 W1 operand (MN-major: F rows of 64 hidden units, 128 B); R
+// (bf16, 128 x 64) and dH (bf16, MN-major over rows) occupy its last 32 KB
+// between the forward MMA and the update of the last dW1 pass.
 __host__ __device__ inline Layout layout(int F) {
   Layout L{};
   uint32_t o = 0;
   L.x = o;
   o += (uint32_t)(F / 64) * 16384u;
   L.sc = o;
-  o += std::max((uint32_t)F * 128u, 49152u);
-  L.recv = o;
-  o += 2u * kB * kC * 4u;  // [src rank][half][row of the owner block][class]
+  o += std::max((uint32_t)F * 128u, 32768u);
+  L.dlb = o;
+  o += kB * 32u;  // bf16 dL [row][16], 32B-swizzled
+  L.ones = o;
+  o += kB * 32u;  // bf16 1.0 [row][16]: db1 = dH^T . 1 on the tensor core
+  L.w2i = o;
+  o += kC * 128u;  // bf16 W2 slice image [class][64 hidden], 128B-swizzled
   L.dl = o;
   o += kB * kC * 4u;
+  L.recv = o;
+  o += kB * kC * 4u;  // [src rank][row of the owner block][class]
   L.w2 = o;
   o += kHS * kC * 4u;
   L.b1 = o;
   o += kHS * 4u;
   L.b2 = o;
   o += kC * 4u;
+  L.b2p = o;
+  o += 8u * kC * 4u;  // db2 partial sums of 8 row blocks
   L.rows = o;
   o += 2u * kB * 8u;
   L.labs = o;
@@ -111,19 +121,21 @@ __host__ __device__ inline Layout layout(int F) {
   o += kB * 4u;
   o = (o + 7u) & ~7u;
   L.bars = o;
-  o += 4u * 8u;
+  o += 8u * 8u;
   L.tmem = o;
   o += 16u;
   L.total = o;
   return L;
 }
 
-__host__ __device__ inline uint32_t tmem_cols(int F) {
-  uint32_t n = (uint32_t)(F / 128) * 128u;  // master + dW1
-  uint32_t a = 32;
-  while (a < n) a <<= 1;
-  return a;
+// TMEM columns: master [0, 64*NM), Z / dL.W2^T [A, A+64), partial logits
+// [A+64, A+80), dW2 [A+80, A+96) with A = 64*NM, dW1 tiles from A+128.
+__host__ __device__ inline int dw1_tiles_per_pass(int F) {
+  const int nm = F / 128;
+  return std::min(2, std::min(nm, (512 - (nm * 64 + 128)) / 64));
 }
+
+__host__ __device__ inline uint32_t tmem_cols(int) { return 512; }
 
 // Remote (or own) shared-memory store whose bytes complete_tx on the
 // destination CTA's mbarrier.
@@ -141,12 +153,6 @@ __device__ __forceinline__ void st_async_f32(uint32_t addr, float a, uint32_t mb
                : "memory");
 }
 
-// R[s][h] (fp32, 64 per row) with the 16-byte chunk index XORed by the row:
-// the head's row-per-lane float4 stores spread over all banks.
-__device__ __forceinline__ int r_idx(int s, int h) {
-  return s * kHS + ((((h >> 2) ^ s) & 15) << 2) + (h & 3);
-}
-
 // 32 fp32 -> bf16 into row `row` (128 B) of an MN-major 128B-swizzled operand
 // of 64 columns, columns [32p, 32p+32).
 __device__ __forceinline__ void put_row32(uint8_t* base, int row, int p, const uint32_t (&w)[32]) {
@@ -162,6 +168,34 @@ __device__ __forceinline__ void put_row32(uint8_t* base, int row, int p, const u
   }
 }
 
+// ecco_expf (learned_common.cuh) without its early-out branches: the same
+// result for every argument, as straight-line code for the 16 classes.
+__device__ __forceinline__ float expf_nb(float x) {
+  const float xc = fminf(fmaxf(x, -87.0f), 88.0f);
+  const float k = rintf(__fmul_rn(xc, 0x1.715476p+0f));
+  float r = __fmaf_rn(k, -0x1.62e400p-1f, xc);
+  r = __fmaf_rn(k, -0x1.7f7d1cp-20f, r);
+  float q = 0x1.6c16c2p-10f;
+  q = __fmaf_rn(q, r, 0x1.111112p-7f);
+  q = __fmaf_rn(q, r, 0x1.555556p-5f);
+  q = __fmaf_rn(q, r, 0x1.555556p-3f);
+  q = __fmaf_rn(q, r, 0.5f);
+  q = __fmaf_rn(q, r, 1.0f);
+  q = __fmaf_rn(q, r, 1.0f);
+  const float e = __fmul_rn(q, __uint_as_float((uint32_t)((int)k + 127) << 23));
+  return x < -87.0f ? 0.0f : e;
+}
+
+
+
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -174,7 +208,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&w)[32
       : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
+// bf16 dL row (16 classes, 32 B) of the 32B-swizzled tile: K-major A of
+// dL.W2^T and MN-major B of dW2 = R^T.dL share it.
+__device__ __forceinline__ uint32_t dlb_off(int row, int chunk) {
+  return (uint32_t)row * 32u + ((uint32_t)(chunk ^ ((row >> 2) & 1)) << 4);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_train_chain(ChainArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const LDims g = a.g;
   const int F = g.F, H = g.H;
@@ -184,22 +225,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
   const int nsteps = a.steps[j];
   if (nsteps <= 0) return;  // the whole cluster (same job) leaves
   const Layout L = layout(F);
+  const uint32_t SC = std::max((uint32_t)F * 128u, 32768u);
   uint8_t* sX = smem + L.x;
-  uint8_t* sSC = smem + L.sc;                   // W1 operand, MN-major [f][64 hidden]
-  uint8_t* sDH = sSC;                           // MN-major dH, 128 rows x 128 B
-  float* sR = (float*)(sSC + 16384);            // relu(Z + b1), fp32 [128][64] swizzled
-  float* sRecv = (float*)(smem + L.recv);
+  uint8_t* sSC = smem + L.sc;                 // W1 operand, MN-major [f][64 hidden]
+  uint8_t* sR = sSC + SC - 32768u;            // bf16 R [row][64], K-major / MN-major
+  uint8_t* sDH = sSC + SC - 16384u;           // bf16 dH [row][64], MN-major over rows
+  uint8_t* sDLb = smem + L.dlb;
+  uint8_t* sW2i = smem + L.w2i;
+  uint8_t* sOnes = smem + L.ones;
+  float* sB2p = (float*)(smem + L.b2p);
   float* sDL = (float*)(smem + L.dl);
+  float* sRecv = (float*)(smem + L.recv);
   float* sW2 = (float*)(smem + L.w2);
   float* sB1 = (float*)(smem + L.b1);
   float* sB2 = (float*)(smem + L.b2);
-  int64_t* sRow = (int64_t*)(smem + L.rows);    // [2][kB] element offsets
-  int* sLab = (int*)(smem + L.labs);            // [2][kB]
+  int* sRow = (int*)(smem + L.rows);          // [2][kB] frame-table rows
+  int* sLab = (int*)(smem + L.labs);          // [2][kB]
   float* sLoss = (float*)(smem + L.loss);
   uint64_t* zfull = (uint64_t*)(smem + L.bars);
-  uint64_t* gfull = zfull + 1;
-  uint64_t* recv_full = zfull + 2;  // owner rows' partial logits arrived (st.async)
-  uint64_t* dl_full = zfull + 3;    // every dL row (and, on rank 0, every loss) arrived
+  uint64_t* plfull = zfull + 1;
+  uint64_t* dhfull = zfull + 2;  // dL.W2^T and dW2 accumulated
+  uint64_t* gfull = zfull + 3;   // one dW1 pass accumulated
+  uint64_t* gfree = zfull + 4;   // every warp has read the pass's dW1 tiles
+  uint64_t* recv_full = zfull + 5;  // owner rows' partial logits arrived (st.async)
+  uint64_t* dl_full = zfull + 6;    // every dL row (and, on rank 0, every loss) arrived
+  uint64_t* w2full = zfull + 7;     // dW2 accumulated
   uint32_t* sTmem = (uint32_t*)(smem + L.tmem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -208,7 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
   const uint32_t lane_base = (uint32_t)(q * 32) << 16;
   const int RP = kB / cs;       // rows owned per CTA for the softmax
   const int NM = F / 128;       // master / dW1 tiles
-  const uint32_t gcol = (uint32_t)NM * 64u;  // dW1 accumulator (and Z) column base
+  const int GT = dw1_tiles_per_pass(F);
+  const int NP = (NM + GT - 1) / GT;  // dW1 passes per step
+  const int nkc = F / 64;
+  const uint32_t acol = (uint32_t)NM * 64u;  // Z / dL.W2^T
+  const uint32_t plcol = acol + 64u, w2col = acol + 80u, gcol = acol + 128u;
   const int slot = a.slots[j];
   float* W1 = a.wbase + (size_t)slot * a.wstride;
   float* b1 = W1 + (size_t)F * H;
@@ -218,16 +272,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
   const int h0 = r * kHS;  // first hidden unit of this CTA
   const int32_t* jrows = a.rows + (size_t)j * a.max_steps * kB;
   const int32_t* jlabs = a.labs + (size_t)j * a.max_steps * kB;
-  const uint32_t recv_bytes = 2u * kB * kC * 4u;
+  const uint32_t recv_bytes = kB * kC * 4u;
   const uint32_t dl_bytes = kB * kC * 4u + (r == 0 ? kB * 4u : 0u);
 
-  // rows of buffer `buf` -> X tile: row i, 16-byte piece c16 -> chunk c16/8
-  auto gather = [&](int buf) {
-    const int per_row = F / 8;
-    for (int i = warp; i < kB; i += kThreads / 32) {
-      const uint16_t* src = a.frames + sRow[buf * kB + i];
-      for (int c16 = lane; c16 < per_row; c16 += 32)
-        cp_async16(sX + (c16 >> 3) * 16384 + i * 128 + (((c16 & 7) ^ (i & 7)) << 4), src + c16 * 8);
+  // rows of buffer `buf`, 16-byte pieces [c0, c0 + n) of each row (n a power
+  // of two) -> X tile, by threads [t0, kThreads); a warp covers consecutive
+  // pieces of one row, piece c16 lands in chunk c16/8
+  const uint32_t xsm = smem_u32(sX);
+  auto gather = [&](int buf, int c0, int n, int t0) {
+    const int* rows = sRow + buf * kB;
+    const int lsh = 31 - __clz(n);
+#pragma unroll 4
+    for (int pc = tid - t0; pc < kB * n; pc += kThreads - t0) {
+      const int i = pc >> lsh, c16 = c0 + (pc & (n - 1));
+      cp_async16_s(xsm + (c16 >> 3) * 16384 + i * 128 + (((c16 & 7) ^ (i & 7)) << 4),
+                   a.frames + (int64_t)rows[i] * F + c16 * 8);
+    }
+  };
+  // db2 partial sums: thread (block of 16 rows, class), threads kB..
+  auto db2_partial = [&]() {
+    if (tid >= kB) {
+      const int c = tid & (kC - 1), blk = (tid - kB) >> 4;
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc = __fadd_rn(acc, sDL[(blk * 16 + i) * kC + c]);
+      sB2p[blk * kC + c] = acc;
+    }
+  };
+  auto build_w2i = [&]() {
+    for (int e = tid; e < kC * kHS / 8; e += kThreads) {
+      const int c = e >> 3, hc = e & 7;
+      const float* w = sW2 + hc * 8 * kC + c;
+      uint4 pk;
+      pk.x = pack_bf16x2(w[0 * kC], w[1 * kC]);
+      pk.y = pack_bf16x2(w[2 * kC], w[3 * kC]);
+      pk.z = pack_bf16x2(w[4 * kC], w[5 * kC]);
+      pk.w = pack_bf16x2(w[6 * kC], w[7 * kC]);
+      *reinterpret_cast<uint4*>(sW2i + c * 128 + ((hc ^ (c & 7)) << 4)) = pk;
     }
   };
 
@@ -235,14 +316,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
   if (tid == 0) {
     if (smem_u32(smem) & 1023u) __trap();  // 128B-swizzle atoms need 1 KB alignment
     mbar_init(zfull, 1);
+    mbar_init(plfull, 1);
+    mbar_init(dhfull, 1);
     mbar_init(gfull, 1);
+    mbar_init(gfree, kThreads / 32);
     mbar_init(recv_full, 1);
     mbar_init(dl_full, 1);
+    mbar_init(w2full, 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(sTmem, tmem_cols(F));
   if (tid < kB) {
-    sRow[tid] = (int64_t)jrows[tid] * F;
+    sRow[tid] = jrows[tid];
   } else {
     sLab[tid - kB] = jlabs[tid - kB];
   }
@@ -254,7 +339,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *sTmem;
-  gather(0);
+  gather(0, 0, F / 8, 0);
+  build_w2i();
+  for (int i = tid; i < kB * 32 / 16; i += kThreads)
+    reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   // master slice -> TMEM; its bf16 image -> the W1 operand
   for (int mt = 0; mt < NM; ++mt) {
     const int f = mt * 128 + s;
@@ -269,158 +357,189 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // every CTA of the cluster is running before any DSMEM store
+  cluster_sync();  // every CTA of the cluster is running before any DSMEM traffic
   tc_fence_after();
 
-  const uint32_t idf = idesc_major(kB, kHS, kFmtBF16, 0, 1);
-  const uint32_t idg = idesc_major(128, kHS, kFmtBF16, 1, 1);
+  const uint32_t idf = idesc_major(kB, kHS, kFmtBF16, 0, 1);     // X . W1
+  const uint32_t idl = idesc(kB, kC, kFmtBF16);                  // R . W2
+  const uint32_t idh = idesc_major(kB, kHS, kFmtBF16, 0, 1);     // dL . W2^T
+  const uint32_t idw2 = idesc_major(128, kC, kFmtBF16, 1, 1);    // R^T . dL (rows 64+ alias)
+  const uint32_t idg = idesc_major(128, kHS, kFmtBF16, 1, 1);    // X^T . dH
+  const uint32_t idb = idesc_major(128, kC, kFmtBF16, 1, 1);     // dH^T . 1 (rows 64+ alias)
   const uint64_t dX = desc_kmajor_sw128(smem_u32(sX));
-  const int nkc = F / 64;
+  auto issue_fwd = [&](int kc0, int kc1) {  // Z (+)= X[:, chunks kc0..kc1) . W1
+    for (int kc = kc0; kc < kc1; ++kc)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16_ss(tmem + acol, dX + ((kc * 16384 + kk * 32) >> 4),
+                    desc_mnmajor_sw128(smem_u32(sSC) + (kc * 4 + kk) * 2048, 16384, 1024), idf,
+                    (kc | kk) != 0);
+  };
+  uint32_t gph = 0, fph = 0;  // gfull / gfree phases completed
 
   for (int step = 0; step < nsteps; ++step) {
     const int cur = step & 1;
     const uint32_t ph = (uint32_t)step & 1u;
+    const bool more = step + 1 < nsteps;
     if (tid == 0) {  // this step's incoming DSMEM bytes
       mbar_expect_tx(recv_full, recv_bytes);
       mbar_expect_tx(dl_full, dl_bytes);
     }
     // ------------------------------------------------------ forward MMA --
+    // (with two dW1 passes the first feature half was issued at the end of
+    // the previous step; the rest waits for the last gathered rows)
     if (warp == 0) {
       if (elect_one()) {
-        for (int kc = 0; kc < nkc; ++kc)
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_bf16_ss(tmem + gcol, dX + ((kc * 16384 + kk * 32) >> 4),
-                        desc_mnmajor_sw128(smem_u32(sSC) + (kc * 4 + kk) * 2048, 16384, 1024), idf,
-                        (kc | kk) != 0);
+        issue_fwd(0, nkc);
         mma_commit(zfull);
       }
       __syncwarp();
     }
     // next step's rows: loads in flight across the forward and the head
     int32_t nxt = 0;
-    const bool more = step + 1 < nsteps;
     if (more) nxt = tid < kB ? jrows[(step + 1) * kB + tid] : jlabs[(step + 1) * kB + tid - kB];
     mbar_wait(zfull, ph);
     tc_fence_after();
 
-    // ------------------------------- head: partial logits of 64 hidden --
-    float rz[32];
+    // ---------------------------- R = relu(Z + b1) -> partial logits MMA --
+    uint32_t mask;  // bit i: Z + b1 > 0 for hidden unit p*32 + i
     {
       uint32_t zr[32];
-      tmem_ld32_nowait(tmem + lane_base + gcol + p * 32, zr);
+      tmem_ld32_nowait(tmem + lane_base + acol + p * 32, zr);
       tmem_ld_wait();
+      mask = 0;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float z = __fadd_rn(__uint_as_float(zr[i]), sB1[p * 32 + i]);
-        rz[i] = z > 0.0f ? z : 0.0f;
+        mask |= (z > 0.0f ? 1u : 0u) << i;
+        zr[i] = __float_as_uint(z > 0.0f ? z : 0.0f);
       }
+      put_row32(sR, s, p, zr);
     }
-    {
-      float pl[kC];
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+      if (elect_one()) {
 #pragma unroll
-      for (int c = 0; c < kC; ++c) pl[c] = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float4* w = reinterpret_cast<const float4*>(sW2 + (p * 32 + i) * kC);
-#pragma unroll
-        for (int c4 = 0; c4 < kC / 4; ++c4) {
-          const float4 v = w[c4];
-          pl[4 * c4 + 0] = __fmaf_rn(rz[i], v.x, pl[4 * c4 + 0]);
-          pl[4 * c4 + 1] = __fmaf_rn(rz[i], v.y, pl[4 * c4 + 1]);
-          pl[4 * c4 + 2] = __fmaf_rn(rz[i], v.z, pl[4 * c4 + 2]);
-          pl[4 * c4 + 3] = __fmaf_rn(rz[i], v.w, pl[4 * c4 + 3]);
-        }
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16_ss(tmem + plcol, desc_kmajor_sw128(smem_u32(sR) + kk * 32),
+                      desc_kmajor_sw128(smem_u32(sW2i) + kk * 32), idl, kk != 0);
+        mma_commit(plfull);
       }
-      // partials -> the CTA owning row s
+      __syncwarp();
+    }
+    mbar_wait(plfull, ph);
+    tc_fence_after();
+    if (p == 0) {  // partials -> the CTA owning row s
+      uint32_t pl[kC];
+      tmem_ld16_nowait(tmem + lane_base + plcol, pl);
+      tmem_ld_wait();
       const uint32_t o = (uint32_t)(s / RP);
-      const uint32_t dst = mapa_shared(smem_u32(sRecv + ((r * 2 + p) * RP + (s % RP)) * kC), o);
+      const uint32_t dst = mapa_shared(smem_u32(sRecv + (r * RP + (s % RP)) * kC), o);
       const uint32_t bar = mapa_shared(smem_u32(recv_full), o);
 #pragma unroll
       for (int c4 = 0; c4 < kC / 4; ++c4)
-        st_async_v4(dst + c4 * 16, pl[4 * c4], pl[4 * c4 + 1], pl[4 * c4 + 2], pl[4 * c4 + 3], bar);
-      // R for dW2 (the W1 operand is dead once the forward completed)
-#pragma unroll
-      for (int i = 0; i < 32; i += 4)
-        *reinterpret_cast<float4*>(sR + r_idx(s, p * 32 + i)) =
-            make_float4(rz[i], rz[i + 1], rz[i + 2], rz[i + 3]);
+        st_async_v4(dst + c4 * 16, __uint_as_float(pl[4 * c4]), __uint_as_float(pl[4 * c4 + 1]),
+                    __uint_as_float(pl[4 * c4 + 2]), __uint_as_float(pl[4 * c4 + 3]), bar);
     }
 
     // ----------------------- owner rows: logits, softmax, dL broadcast --
-    if (tid < RP) {
+    // four threads per owned row (warps 4..), one class quad each
+    if (tid >= kB && tid < kB + 4 * RP) {
       mbar_wait(recv_full, ph);
-      const int row = r * RP + tid;
-      float lg[kC];
-#pragma unroll
-      for (int c = 0; c < kC; ++c) lg[c] = sRecv[tid * kC + c];
-      for (int sh = 1; sh < 2 * cs; ++sh) {
-        const float* pr = sRecv + (sh * RP + tid) * kC;
-#pragma unroll
-        for (int c = 0; c < kC; ++c) lg[c] = __fadd_rn(lg[c], pr[c]);
+      const int t = (tid - kB) >> 2, cq = tid & 3, row = r * RP + t;
+      const float4* rv = reinterpret_cast<const float4*>(sRecv);
+      float4 lg = rv[t * 4 + cq];
+      for (int src = 1; src < cs; ++src) {
+        const float4 v = rv[(src * RP + t) * 4 + cq];
+        lg = make_float4(__fadd_rn(lg.x, v.x), __fadd_rn(lg.y, v.y), __fadd_rn(lg.z, v.z),
+                         __fadd_rn(lg.w, v.w));
       }
-#pragma unroll
-      for (int c = 0; c < kC; ++c) lg[c] = __fadd_rn(lg[c], sB2[c]);
-      float m = lg[0];
-#pragma unroll
-      for (int c = 1; c < kC; ++c) m = lg[c] > m ? lg[c] : m;
-      float e[kC], sum = 0.0f;
-#pragma unroll
-      for (int c = 0; c < kC; ++c) {
-        e[c] = ecco_expf(__fsub_rn(lg[c], m));
-        sum = __fadd_rn(sum, e[c]);
+      const float4 bb = reinterpret_cast<const float4*>(sB2)[cq];
+      lg = make_float4(__fadd_rn(lg.x, bb.x), __fadd_rn(lg.y, bb.y), __fadd_rn(lg.z, bb.z),
+                       __fadd_rn(lg.w, bb.w));
+      float m = fmaxf(fmaxf(lg.x, lg.y), fmaxf(lg.z, lg.w));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      const float4 e = make_float4(expf_nb(__fsub_rn(lg.x, m)), expf_nb(__fsub_rn(lg.y, m)),
+                                   expf_nb(__fsub_rn(lg.z, m)), expf_nb(__fsub_rn(lg.w, m)));
+      float sum = __fadd_rn(__fadd_rn(e.x, e.y), __fadd_rn(e.z, e.w));
+      sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, 1));
+      sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, 2));
+      constexpr float invB = 1.0f / kB;  // exact (power of two)
+      const float inv = __frcp_rn(sum);
+      const int y = sLab[cur * kB + row] - cq * 4;  // class within this quad (0..3 if mine)
+      const float4 dl = make_float4(__fmul_rn(__fsub_rn(__fmul_rn(e.x, inv), y == 0 ? 1.0f : 0.0f), invB),
+                                    __fmul_rn(__fsub_rn(__fmul_rn(e.y, inv), y == 1 ? 1.0f : 0.0f), invB),
+                                    __fmul_rn(__fsub_rn(__fmul_rn(e.z, inv), y == 2 ? 1.0f : 0.0f), invB),
+                                    __fmul_rn(__fsub_rn(__fmul_rn(e.w, inv), y == 3 ? 1.0f : 0.0f), invB));
+      for (int d = 0; d < cs; ++d)
+        st_async_v4(mapa_shared(smem_u32(sDL + row * kC + cq * 4), (uint32_t)d), dl.x, dl.y, dl.z,
+                    dl.w, mapa_shared(smem_u32(dl_full), (uint32_t)d));
+      if (y >= 0 && y < 4) {
+        const float ly = y == 0 ? lg.x : y == 1 ? lg.y : y == 2 ? lg.z : lg.w;
+        st_async_f32(mapa_shared(smem_u32(sLoss + row), 0u), __logf(sum) - (ly - m),
+                     mapa_shared(smem_u32(dl_full), 0u));
       }
-      const float invB = __fdiv_rn(1.0f, (float)kB);
-      const int y = sLab[cur * kB + row];
-      float ly = lg[0], dl[kC];
-#pragma unroll
-      for (int c = 0; c < kC; ++c) {
-        dl[c] = __fmul_rn(__fsub_rn(__fdiv_rn(e[c], sum), c == y ? 1.0f : 0.0f), invB);
-        ly = c == y ? lg[c] : ly;
-      }
-      for (int d = 0; d < cs; ++d) {
-        const uint32_t dst = mapa_shared(smem_u32(sDL + row * kC), (uint32_t)d);
-        const uint32_t bar = mapa_shared(smem_u32(dl_full), (uint32_t)d);
-#pragma unroll
-        for (int c4 = 0; c4 < kC / 4; ++c4)
-          st_async_v4(dst + c4 * 16, dl[4 * c4], dl[4 * c4 + 1], dl[4 * c4 + 2], dl[4 * c4 + 3], bar);
-      }
-      st_async_f32(mapa_shared(smem_u32(sLoss + row), 0u), logf(sum) - (ly - m),
-                   mapa_shared(smem_u32(dl_full), 0u));
     }
     if (more) {  // next step's rows into the other buffer
       if (tid < kB)
-        sRow[(cur ^ 1) * kB + tid] = (int64_t)nxt * F;
+        sRow[(cur ^ 1) * kB + tid] = nxt;
       else
         sLab[(cur ^ 1) * kB + tid - kB] = nxt;
     }
+    if (more && tid < kB) {  // next rows -> L2 (this CTA's block of them), while dL is in flight
+      const int lpr = F / 64;  // 128-byte lines per row
+      for (int li = tid; li < RP * lpr; li += kB) {
+        const int row = r * RP + li / lpr;
+        prefetch_l2(a.frames + (int64_t)jrows[(step + 1) * kB + row] * F + (li % lpr) * 64);
+      }
+    }
     mbar_wait(dl_full, ph);
 
-    // --------------------------------------------- dH = (dL.W2^T)*(Z>0) --
+    // ------------------------------ bf16 dL -> dL.W2^T and dW2 = R^T.dL --
+    if (p == 0) {
+      const float4* d4 = reinterpret_cast<const float4*>(sDL + s * kC);
+#pragma unroll
+      for (int ch = 0; ch < 2; ++ch) {
+        const float4 u = d4[2 * ch], v = d4[2 * ch + 1];
+        uint4 pk;
+        pk.x = pack_bf16x2(u.x, u.y);
+        pk.y = pack_bf16x2(u.z, u.w);
+        pk.z = pack_bf16x2(v.x, v.y);
+        pk.w = pack_bf16x2(v.z, v.w);
+        *reinterpret_cast<uint4*>(sDLb + dlb_off(s, ch)) = pk;
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+      if (elect_one()) {
+        mma_bf16_ss(tmem + acol, smem_desc(smem_u32(sDLb), 16, 256, kSwizzle32B),
+                    desc_mnmajor_sw128(smem_u32(sW2i), 16384, 1024), idh, 0);
+        mma_commit(dhfull);
+#pragma unroll
+        for (int k16 = 0; k16 < kB / 16; ++k16)
+          mma_bf16_ss(tmem + w2col, desc_mnmajor_sw128(smem_u32(sR) + k16 * 2048, 0, 1024),
+                      smem_desc(smem_u32(sDLb) + k16 * 512, 256, 256, kSwizzle32B), idw2, k16 != 0);
+        mma_commit(w2full);
+      }
+      __syncwarp();
+    }
+    mbar_wait(dhfull, ph);
+    tc_fence_after();
+
+    // ------------------------------------------------ dH = (dL.W2^T)*(Z>0) --
     {
-      float dl[kC];
-#pragma unroll
-      for (int c4 = 0; c4 < kC / 4; ++c4) {
-        const float4 v = reinterpret_cast<const float4*>(sDL + s * kC)[c4];
-        dl[4 * c4] = v.x;
-        dl[4 * c4 + 1] = v.y;
-        dl[4 * c4 + 2] = v.z;
-        dl[4 * c4 + 3] = v.w;
-      }
       uint32_t dh[32];
+      tmem_ld32_nowait(tmem + lane_base + acol + p * 32, dh);
+      tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float4* w = reinterpret_cast<const float4*>(sW2 + (p * 32 + i) * kC);
-        float acc = 0.0f;
-#pragma unroll
-        for (int c4 = 0; c4 < kC / 4; ++c4) {
-          const float4 v = w[c4];
-          acc = __fmaf_rn(dl[4 * c4 + 0], v.x, acc);
-          acc = __fmaf_rn(dl[4 * c4 + 1], v.y, acc);
-          acc = __fmaf_rn(dl[4 * c4 + 2], v.z, acc);
-          acc = __fmaf_rn(dl[4 * c4 + 3], v.w, acc);
-        }
-        dh[i] = __float_as_uint(rz[i] > 0.0f ? acc : 0.0f);
-      }
+      for (int i = 0; i < 32; ++i) dh[i] = (mask >> i) & 1u ? dh[i] : 0u;
       put_row32(sDH, s, p, dh);  // MN-major over rows: dW1's B operand
     }
     fence_async_smem();  // dH (generic stores) -> tensor-core reads
@@ -428,73 +547,110 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_chain(ChainArgs a) {
     __syncthreads();
     tc_fence_after();
 
-    // ------------------------------------------- dW1 = X^T . dH (tensor) --
-    if (warp == 0) {
-      if (elect_one()) {
-        for (int mt = 0; mt < NM; ++mt)
+    // ------------------------ dW1 = X^T . dH in passes, master update (TMEM) --
+    for (int pass = 0; pass < NP; ++pass) {
+      const int mt0 = pass * GT, mt1 = std::min(NM, mt0 + GT);
+      if (warp == 0) {
+        if (pass > 0) {
+          mbar_wait(gfree, fph & 1u);  // previous pass's tiles read by every warp
+          ++fph;
+          tc_fence_after();
+        }
+        if (elect_one()) {
+          for (int mt = mt0; mt < mt1; ++mt)
 #pragma unroll
-          for (int k16 = 0; k16 < kB / 16; ++k16)
-            mma_bf16_ss(tmem + gcol + mt * 64,
-                        desc_mnmajor_sw128(smem_u32(sX) + (2 * mt) * 16384 + k16 * 2048, 16384, 1024),
-                        desc_mnmajor_sw128(smem_u32(sDH) + k16 * 2048, 16384, 1024), idg, k16 != 0);
-        mma_commit(gfull);
+            for (int k16 = 0; k16 < kB / 16; ++k16)
+              mma_bf16_ss(tmem + gcol + (mt - mt0) * 64,
+                          desc_mnmajor_sw128(smem_u32(sX) + (2 * mt) * 16384 + k16 * 2048, 16384, 1024),
+                          desc_mnmajor_sw128(smem_u32(sDH) + k16 * 2048, 16384, 1024), idg, k16 != 0);
+          if (pass == NP - 1)  // db1 into the (consumed) partial-logit columns
+#pragma unroll
+            for (int k16 = 0; k16 < kB / 16; ++k16)
+              mma_bf16_ss(tmem + plcol, desc_mnmajor_sw128(smem_u32(sDH) + k16 * 2048, 0, 1024),
+                          smem_desc(smem_u32(sOnes) + k16 * 512, 256, 256, kSwizzle32B), idb,
+                          k16 != 0);
+          mma_commit(gfull);
+        }
+        __syncwarp();
       }
-      __syncwarp();
-    }
-
-    // -------------------- dW2 = R^T.dL, db1 = dH^T.1, db2 = dL^T.1 (fp32) --
-    {
-      const int h = tid >> 2, cq = tid & 3;  // hidden unit, class quad
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 16
-      for (int i = 0; i < kB; ++i) {
-        const float rv = sR[r_idx(i, h)];
-        const float4 d = reinterpret_cast<const float4*>(sDL + i * kC)[cq];
-        acc.x = __fmaf_rn(rv, d.x, acc.x);
-        acc.y = __fmaf_rn(rv, d.y, acc.y);
-        acc.z = __fmaf_rn(rv, d.z, acc.z);
-        acc.w = __fmaf_rn(rv, d.w, acc.w);
+      if (pass == 0 && p == 0 && q < 2) {  // dW2 row h = s (TMEM lanes 0-63)
+        mbar_wait(w2full, ph);
+        tc_fence_after();
+        uint32_t w2r[kC];
+        tmem_ld16_nowait(tmem + lane_base + w2col, w2r);
+        tmem_ld_wait();
+        float4* w = reinterpret_cast<float4*>(sW2 + s * kC);
+#pragma unroll
+        for (int c4 = 0; c4 < kC / 4; ++c4) {
+          const float4 o = w[c4];
+          w[c4] = make_float4(__fmaf_rn(-lr, __uint_as_float(w2r[4 * c4]), o.x),
+                              __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 1]), o.y),
+                              __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 2]), o.z),
+                              __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 3]), o.w));
+        }
       }
-      float4* w = reinterpret_cast<float4*>(sW2 + h * kC) + cq;
-      const float4 o = *w;
-      *w = make_float4(__fmaf_rn(-lr, acc.x, o.x), __fmaf_rn(-lr, acc.y, o.y),
-                       __fmaf_rn(-lr, acc.z, o.z), __fmaf_rn(-lr, acc.w, o.w));
-    }
-    if (tid < kHS) {  // db1 from the bf16 dH operand (as the dW1 contraction sees it)
-      const int hc = tid >> 3, hw = tid & 7;
-      float acc = 0.0f;
-#pragma unroll 16
-      for (int i = 0; i < kB; ++i)
-        acc = __fadd_rn(acc, bf16_to_f32(*reinterpret_cast<const uint16_t*>(
-                                 sDH + i * 128 + ((hc ^ (i & 7)) << 4) + hw * 2)));
-      sB1[tid] = __fmaf_rn(-lr, acc, sB1[tid]);
-    } else if (tid >= 2 * kHS && tid < 2 * kHS + kC) {
-      const int c = tid - 2 * kHS;
-      float acc = 0.0f;
-#pragma unroll 16
-      for (int i = 0; i < kB; ++i) acc = __fadd_rn(acc, sDL[i * kC + c]);
-      sB2[c] = __fmaf_rn(-lr, acc, sB2[c]);
-    }
-
-    // ------------------ next rows in flight, then the master update (TMEM) --
-    mbar_wait(gfull, ph);
-    tc_fence_after();
-    __syncthreads();  // R / dH reads done: the W1 operand may be rewritten
-    if (more) gather(cur ^ 1);  // X is free once dW1 completed
-    for (int mt = 0; mt < NM; ++mt) {
-      uint32_t wr[32], gr[32];
-      tmem_ld32_nowait(tmem + lane_base + mt * 64 + p * 32, wr);
-      tmem_ld32_nowait(tmem + lane_base + gcol + mt * 64 + p * 32, gr);
+      mbar_wait(gfull, gph & 1u);
+      tc_fence_after();
+      if (pass == NP - 1 && p == 1 && q < 2) {  // db1 row h = s (TMEM lanes 0-63)
+        uint32_t v[8];
+        tmem_ld8_nowait(tmem + lane_base + plcol, v);
+        tmem_ld_wait();
+        sB1[s] = __fmaf_rn(-lr, __uint_as_float(v[0]), sB1[s]);
+      }
+      const bool last = pass == NP - 1;
+      // this pass's X chunks are read: release them to the cluster (warp 1
+      // gathers the next rows' features there once every CTA has, below)
+      // this pass's X chunks are read: the next rows' features there (all
+      // threads on the last pass; after the update, without warp 0, otherwise)
+      if (more && last) gather(cur ^ 1, mt0 * 16, (mt1 - mt0) * 16, 0);
+      if (NP == 1) db2_partial();
+      if (last) {
+        __syncthreads();  // dH / R / sW2 readers done, db2 partials written
+        build_w2i();
+        if (tid >= 32 && tid < 32 + kC) {
+          const int c = tid - 32;
+          float acc = sB2p[c];
+#pragma unroll
+          for (int b = 1; b < 8; ++b) acc = __fadd_rn(acc, sB2p[b * kC + c]);
+          sB2[c] = __fmaf_rn(-lr, acc, sB2[c]);
+        }
+      }
+      // master update; on a gating pass the dW1 tiles are read first and the
+      // next pass released before the arithmetic
+      uint32_t g0[32], g1[32];
+      tmem_ld32_nowait(tmem + lane_base + gcol + p * 32, g0);
+      if (mt1 - mt0 > 1) tmem_ld32_nowait(tmem + lane_base + gcol + 64 + p * 32, g1);
       tmem_ld_wait();
+      if (!last) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(gfree);
+      }
+      for (int mt = mt0; mt < mt1; ++mt) {
+        uint32_t wr[32];
+        tmem_ld32_nowait(tmem + lane_base + mt * 64 + p * 32, wr);
+        tmem_ld_wait();
+        if (mt == mt0) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        wr[i] = __float_as_uint(__fmaf_rn(-lr, __uint_as_float(gr[i]), __uint_as_float(wr[i])));
-      tmem_st32(tmem + lane_base + mt * 64 + p * 32, wr);
-      put_row32(sSC, mt * 128 + s, p, wr);
+          for (int i = 0; i < 32; ++i)
+            wr[i] = __float_as_uint(__fmaf_rn(-lr, __uint_as_float(g0[i]), __uint_as_float(wr[i])));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            wr[i] = __float_as_uint(__fmaf_rn(-lr, __uint_as_float(g1[i]), __uint_as_float(wr[i])));
+        }
+        tmem_st32(tmem + lane_base + mt * 64 + p * 32, wr);
+        put_row32(sSC, mt * 128 + s, p, wr);
+      }
+      if (!last) {
+        if (more && warp > 0) gather(cur ^ 1, mt0 * 16, (mt1 - mt0) * 16, 32);
+        if (pass == 0) db2_partial();
+      }
+      ++gph;
     }
     tmem_st_wait();
     cp_async_wait_all();
-    fence_async_smem();  // X rows + W1 operand -> next forward
+    fence_async_smem();  // X rows, W1 / W2 operands -> next step's MMAs
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -535,7 +691,8 @@ namespace fused {
 bool train_supported(const ecco_ctx* ctx) {
   const ecco_config& g = ctx->cfg;
   if (g.minibatch != kB || g.num_classes != kC || g.feat_dim % 128 || g.feat_dim > 512 ||
-      g.hidden_dim % kHS || g.hidden_dim / kHS > kMaxCluster || g.hidden_dim / kHS < 1)
+      (g.feat_dim & (g.feat_dim - 1)) ||
+      (g.hidden_dim != 4 * kHS && g.hidden_dim != 8 * kHS))
     return false;
   return layout(g.feat_dim).total <= 232448;
 }
