@@ -152,6 +152,15 @@ ecco_status ecco_stage_frames(ecco_ctx* ctx, int n_cams, const uint16_t* frames,
                               const int32_t* labels, const uint16_t* eval_frames,
                               const int32_t* eval_labels);
 ecco_status ecco_swap_frames(ecco_ctx* ctx);
+/* Group-sharded variant of ecco_stage_frames: the frame rings of cameras
+ * [ring_first, ring_first + ring_n) only (the members of this rank's groups:
+ * a job trains on its own members' frames, orchestrator.cpp:52-62, 282-309)
+ * and the eval sets of cameras [0, eval_n) (every camera is scored against
+ * this rank's groups).  `frames` / `labels` point at camera ring_first's
+ * ring.  Rings outside the range are left as they were in the back buffer. */
+ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int ring_first, int ring_n,
+                                    const uint16_t* frames, const int32_t* labels, int eval_n,
+                                    const uint16_t* eval_frames, const int32_t* eval_labels);
 /* Copies the first n_cams cameras' resident frames back to the host (same
  * layouts as ecco_upload_frames; any pointer may be NULL). */
 ecco_status ecco_read_frames(ecco_ctx* ctx, int n_cams, uint16_t* frames, int32_t* labels,

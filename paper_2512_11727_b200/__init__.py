@@ -98,7 +98,7 @@ EXPORTS = [
     "ecco_default_config", "ecco_create", "ecco_destroy", "ecco_last_error",
     "ecco_kernel_launches", "ecco_profile", "ecco_kernel_stat", "ecco_transfer_bytes", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
     "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
-    "ecco_read_frames", "ecco_stage_frames", "ecco_swap_frames",
+    "ecco_read_frames", "ecco_stage_frames", "ecco_stage_frames_range", "ecco_swap_frames",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
@@ -271,6 +271,15 @@ class Context:
         self._check(lib().ecco_stage_frames(self._h, int(n_cams), C.c_void_p(frames_ptr),
                                             C.c_void_p(labels_ptr), C.c_void_p(eval_ptr),
                                             C.c_void_p(eval_labels_ptr)))
+
+    def stage_frames_range_host_ptr(self, ring_first, ring_n, frames_ptr, labels_ptr, eval_n,
+                                    eval_ptr, eval_labels_ptr):
+        """ecco_stage_frames_range: the rings of cameras [ring_first, ring_first
+        + ring_n) (pointers at camera ring_first) and the eval sets of cameras
+        [0, eval_n), asynchronously into the back buffer."""
+        self._check(lib().ecco_stage_frames_range(
+            self._h, int(ring_first), int(ring_n), C.c_void_p(frames_ptr), C.c_void_p(labels_ptr),
+            int(eval_n), C.c_void_p(eval_ptr), C.c_void_p(eval_labels_ptr)))
 
     def swap_frames(self):
         self._check(lib().ecco_swap_frames(self._h))

@@ -318,9 +318,16 @@ ecco_status ecco_upload_frames(ecco_ctx* ctx, int n, const uint16_t* frames, con
 
 ecco_status ecco_stage_frames(ecco_ctx* ctx, int n, const uint16_t* frames, const int32_t* labels,
                               const uint16_t* eval, const int32_t* eval_labels) {
+  return ecco_stage_frames_range(ctx, 0, n, frames, labels, n, eval, eval_labels);
+}
+
+ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint16_t* frames,
+                                    const int32_t* labels, int n_eval, const uint16_t* eval,
+                                    const int32_t* eval_labels) {
   return guarded(ctx, [&] {
     ECCO_REQUIRE(learned(ctx), "stage_frames: learned backend only");
-    ECCO_REQUIRE(n >= 0 && n <= ctx->n_cams, "stage_frames: camera count");
+    ECCO_REQUIRE(first >= 0 && n >= 0 && first + n <= ctx->n_cams, "stage_frames: camera range");
+    ECCO_REQUIRE(n_eval >= 0 && n_eval <= ctx->n_cams, "stage_frames: eval camera count");
     ECCO_REQUIRE(!ctx->staged, "stage_frames: previous staging not swapped in");
     const ecco_config& g = ctx->cfg;
     if (!ctx->copy_stream) {
@@ -335,10 +342,12 @@ ecco_status ecco_stage_frames(ecco_ctx* ctx, int n, const uint16_t* frames, cons
     }
     // the back buffer may still be read by kernels of the previous window
     if (ctx->back_busy) ECCO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->back_free, 0));
-    const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n * g.eval_samples;
+    const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n_eval * g.eval_samples;
+    const size_t f0 = (size_t)first * g.ring_frames;
     const cudaMemcpyKind k = cudaMemcpyHostToDevice;
-    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_frames, frames, fr * g.feat_dim * 2, k, ctx->copy_stream));
-    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels, labels, fr * 4, k, ctx->copy_stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_frames + f0 * g.feat_dim, frames, fr * g.feat_dim * 2, k,
+                         ctx->copy_stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels + f0, labels, fr * 4, k, ctx->copy_stream));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream));
     ECCO_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
