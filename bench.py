@@ -44,11 +44,18 @@ CONFIGS = {
     "c2": (100, 10),
     "c3": (1000, 50),
     "c4": (10000, 500),
+    "c5": (10000, 500),  # detection head (DET_DIMS), allocator marginal-gain probes only
 }
 DIMS = dict(feat_dim=512, hidden_dim=256, num_classes=16, minibatch=128, ring_frames=512,
             eval_samples=64)
 DEPTH = 2             # micro-windows granted per group per window (initial pass + 1 greedy)
 STEPS = 16            # SGD steps per micro-window
+# configs[4]: the detection-head variant (larger per-group model and frame
+# features).  Its window is the allocator's marginal-gain probing (every
+# group's speculative chain + member evaluations); the full camera x group
+# matrix at this shape has no fused kernel yet and is left out of the step.
+DET_DIMS = dict(feat_dim=1024, hidden_dim=1024, num_classes=96)
+MATRIX = True         # the regroup matrix is part of the step (False for c5)
 GPU_S = 1.0           # GPU-seconds per micro-window; steps = floor(GPU_S * STEPS)
 BATCH = (30.0, 1080.0, 1.0)  # delivered fps, resolution, quality: sufficiency 1
 THROUGHPUT = 8.192e6  # CameraState.gpu_pixel_throughput default
@@ -214,8 +221,9 @@ def run_b200(args, rank, world, local_rank):
     cams = np.arange(wl.N, dtype=np.int32)
     stream = torch.cuda.ExternalStream(ctx.stream)
     dev = torch.device("cuda", local_rank)
-    M_local = torch.full((wl.N, wl.gb), float("nan"), dtype=torch.float64, device=dev)
-    M_part = None if len(wl.local) == wl.gb else torch.empty((wl.N, max(1, len(wl.local))),
+    M_local = torch.full((wl.N if MATRIX else 1, wl.gb), float("nan"), dtype=torch.float64,
+                         device=dev)
+    M_part = None if len(wl.local) == wl.gb or not MATRIX else torch.empty((wl.N, max(1, len(wl.local))),
                                                              dtype=torch.float64, device=dev)
     best = torch.empty(wl.N, dtype=torch.int32, device=dev)
     best_acc = torch.empty(wl.N, dtype=torch.float64, device=dev)
@@ -227,18 +235,21 @@ def run_b200(args, rank, world, local_rank):
         with torch.cuda.stream(stream):
             if timed:
                 ev["a"].record(stream)
-            if wl.local:
+            if not MATRIX:
+                pass
+            elif wl.local:
                 if M_part is None:
                     ctx.eval_matrix_dev(wl.local, M_local.data_ptr(), cams=cams)
                 else:  # ragged last block: columns beyond the rank's groups stay NaN
                     ctx.eval_matrix_dev(wl.local, M_part.data_ptr(), cams=cams)
                     M_local[:, :len(wl.local)].copy_(M_part)
-            if backend == "nccl":
-                M = shard.gather_blocks(M_local, world, dist)  # NCCL all-gather of column blocks
-            else:
-                M = shard.gather_blocks(M_local.cpu(), world, dist).to(dev)
-            ctx.route_matrix_dev(wl.N, wl.gb, M.data_ptr(), best.data_ptr(), best_acc.data_ptr(),
-                                 n_blocks=world)
+            if MATRIX:
+                if backend == "nccl":
+                    M = shard.gather_blocks(M_local, world, dist)  # NCCL all-gather of column blocks
+                else:
+                    M = shard.gather_blocks(M_local.cpu(), world, dist).to(dev)
+                ctx.route_matrix_dev(wl.N, wl.gb, M.data_ptr(), best.data_ptr(),
+                                     best_acc.data_ptr(), n_blocks=world)
             if timed:
                 ev["b"].record(stream)
             if wl.local:
@@ -308,7 +319,9 @@ def run_b200(args, rank, world, local_rank):
                             f"F{DIMS['feat_dim']}-H{DIMS['hidden_dim']}-C{DIMS['num_classes']}, "
                             f"B={DIMS['minibatch']}, S={DIMS['eval_samples']} eval frames/camera, "
                             f"R={DIMS['ring_frames']} ring frames/camera, depth {DEPTH} x "
-                            f"{STEPS} SGD steps per group per window, full camera x group matrix",
+                            f"{STEPS} SGD steps per group per window, "
+                            + ("full camera x group matrix" if MATRIX else
+                               "marginal-gain probes only (no regroup matrix)"),
                 "cameras": wl.N, "groups": wl.G, "groups_per_rank": wl.gb,
                 "parallelism": f"groups sharded over {world} rank(s); eval matrix all-gather",
                 "l2": "inputs larger than L2 (frames "
@@ -502,7 +515,7 @@ def cpu_sample(N, G, budget_s=12.0):
         step_rate = n_steps * cores / (time.perf_counter() - t)
     per = N // G
     steps_window = G * DEPTH * int(GPU_S * STEPS)
-    pairs_window = N * G + G * (DEPTH + 1) * per  # regroup matrix + chain evaluations
+    pairs_window = (N * G if MATRIX else 0) + G * (DEPTH + 1) * per  # regroup matrix + chain evaluations
     window_s = pairs_window / pair_rate + steps_window / step_rate
     samples = steps_window * B
     return {"value": samples / window_s, "unit": "samples/s", "cores": cores, "kind": "port",
@@ -651,6 +664,10 @@ def main():
     ap.add_argument("--no-parametric", action="store_true",
                     help="skip the parametric-backend vs reference-library leg")
     args = ap.parse_args()
+    global MATRIX
+    if args.config == "c5":
+        DIMS.update(DET_DIMS)
+        MATRIX = False
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank)

@@ -340,6 +340,26 @@ int64_t ecco_sim_last_samples(const ecco_sim* sim);
 size_t ecco_sim_trace_csv(const ecco_sim* sim, char* buf, size_t cap);
 size_t ecco_sim_summary_json(const ecco_sim* sim, char* buf, size_t cap);
 ecco_ctx* ecco_sim_context(ecco_sim* sim);
+/* Timings of the last window, up to n of: the five of ecco_sim_last_timings,
+ * [5] netsim (simulate_window), [6] profile tables (first use of cameras),
+ * [7] drift events, [8] routing of pending requests, [9] shares + config
+ * selection + batch assembly (netsim and profiles excluded), [10] end-of-
+ * window rows and statistics.  Returns the number written. */
+int ecco_sim_last_timings_ex(const ecco_sim* sim, double* out, int n);
+
+/* ---- network model (host, no device) ---------------------------------------
+ * simulate_window's per-flow mean rates (core/src/netsim.cpp:64-94 with
+ * aimd_step :45-62; replaces ecco::simulate_window's mean_rate_bps for the
+ * window driver): n flows with additive increase alpha
+ * (bits/s per RTT, > 0), decrease factor beta (in (0,1)) and local cap (<= 0
+ * = uncapped, resolve_caps :33-40) over one shared bottleneck of `capacity`,
+ * from zero rates for llround(duration_s / rtt_s) steps; mean over the
+ * second half.  Bit-identical to the reference; `exact_steps` (optional)
+ * receives how many steps needed the reference's sequential congestion sum.
+ * Invalid arguments -> ECCO_ERR_INVALID_ARGUMENT (netsim.cpp:17-31). */
+ecco_status ecco_netsim_mean_rates(int n, const double* alpha, const double* beta,
+                                   const double* caps, double capacity, double rtt_s,
+                                   double duration_s, double* mean_rates, int* exact_steps);
 
 #ifdef __cplusplus
 }

@@ -93,6 +93,9 @@ def ref():
         L.ref_profile_table.argtypes = [dp, C.c_int, C.c_double, C.c_int, C.c_int, dp, C.c_int,
                                         dp, dp, C.c_double, C.c_double, C.c_double, C.c_double,
                                         dp, dp, dp, dp, u8p]
+        L.ref_simulate_window.restype = C.c_int
+        L.ref_simulate_window.argtypes = [C.c_int, dp, dp, dp, C.c_double, C.c_double,
+                                          C.c_double, dp]
         L.ref_allocate_trajectories.restype = C.c_int
         L.ref_allocate_trajectories.argtypes = [C.c_int, ip, ip, dp, C.c_int, C.c_double,
                                                 C.c_double, C.c_int, C.c_double, C.c_int,

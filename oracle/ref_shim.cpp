@@ -298,4 +298,30 @@ int ref_time_windows(const char* json, int max_windows, double* out_s, int* n_ru
   }
 }
 
+// ecco::simulate_window (netsim.cpp:64-94) on n flows "f00000".. with local
+// caps (<= 0 = absent); mean rates in flow order.  Returns 0 or the error code.
+int ref_simulate_window(int n, const double* alpha, const double* beta, const double* caps,
+                        double capacity, double rtt_s, double duration_s, double* mean) {
+  try {
+    std::vector<FlowParams> flows(n);
+    NetTopology topo;
+    topo.shared_capacity_bps = capacity;
+    topo.rtt_s = rtt_s;
+    char id[16];
+    for (int i = 0; i < n; ++i) {
+      std::snprintf(id, sizeof(id), "f%05d", i);
+      flows[i].id = id;
+      flows[i].alpha_bps_per_rtt = alpha[i];
+      flows[i].beta = beta[i];
+      if (caps[i] > 0.0) topo.local_caps_bps[id] = caps[i];
+    }
+    const FlowTrace t = simulate_window(flows, topo, duration_s);
+    for (int i = 0; i < n; ++i) mean[i] = t.mean_rate_bps.at(flows[i].id);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
 }  // extern "C"

@@ -107,7 +107,24 @@ EXPORTS = [
     "ecco_profile_tables", "ecco_sim_default_options", "ecco_sim_create", "ecco_sim_destroy",
     "ecco_sim_last_error", "ecco_sim_step_window", "ecco_sim_last_timings",
     "ecco_sim_last_samples", "ecco_sim_trace_csv", "ecco_sim_summary_json", "ecco_sim_context",
+    "ecco_sim_last_timings_ex", "ecco_netsim_mean_rates",
 ]
+
+
+def netsim_mean_rates(alpha, beta, caps, capacity, rtt_s, duration_s):
+    """simulate_window's per-flow mean rates (netsim.cpp:64-94), host code of
+    libecco_b200.so: returns (mean rates, steps that needed the sequential
+    congestion sum).  Raises InvalidArgument as the reference does."""
+    a = np.ascontiguousarray(alpha, np.float64)
+    b = np.ascontiguousarray(beta, np.float64)
+    c = np.ascontiguousarray(caps, np.float64)
+    out = np.zeros(a.size)
+    ex = C.c_int()
+    st = lib().ecco_netsim_mean_rates(a.size, a, b, c, float(capacity), float(rtt_s),
+                                      float(duration_s), out, C.byref(ex))
+    if st:
+        raise _ERRORS.get(st, EccoError)(st, "netsim: invalid argument")
+    return out, ex.value
 
 
 def lib():
@@ -127,6 +144,8 @@ def lib():
         L.ecco_kernel_launches.restype = C.c_uint64
         L.ecco_kernel_launches.argtypes = [vp]
         L.ecco_stream.restype = vp
+        L.ecco_netsim_mean_rates.argtypes = [C.c_int] + [np.ctypeslib.ndpointer(np.float64)] * 3 + [
+            C.c_double] * 3 + [np.ctypeslib.ndpointer(np.float64), C.POINTER(C.c_int)]
         L.ecco_stream.argtypes = [vp]
         L.ecco_sim_default_options.argtypes = [C.POINTER(SimOptions)]
         L.ecco_sim_create.argtypes = [C.c_char_p, C.POINTER(SimOptions), C.POINTER(vp),
@@ -544,9 +563,11 @@ class Simulation:
             pass
 
     def last_timings(self):
-        t = (C.c_double * 5)()
-        lib().ecco_sim_last_timings(self._h, t)
-        return dict(zip(("window_ms", "regroup_ms", "train_ms", "window_end_ms", "replay_ms"), list(t)))
+        t = (C.c_double * 11)()
+        n = lib().ecco_sim_last_timings_ex(self._h, t, 11)
+        return dict(zip(("window_ms", "regroup_ms", "train_ms", "window_end_ms", "replay_ms",
+                         "netsim_ms", "profile_ms", "events_ms", "route_ms", "shares_configs_ms",
+                         "rows_ms"), list(t)[:n]))
 
     def last_samples(self):
         return lib().ecco_sim_last_samples(self._h)

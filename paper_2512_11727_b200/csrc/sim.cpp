@@ -21,6 +21,8 @@
 // The transmission controller, AIMD network model, trace and summary stay
 // scalar host code with the reference's arithmetic, so the trace of a
 // parametric run is byte-identical to the reference's.
+#include <immintrin.h>
+
 #include <algorithm>
 #include <chrono>
 #include <climits>
@@ -58,6 +60,108 @@ struct SimError {
 void check(ecco_ctx* ctx, ecco_status st) {
   if (st != ECCO_OK) fail(st, ecco_last_error(ctx));
 }
+
+// ------------------------------------------------------------- netsim --
+namespace ecco_netsim {
+
+// simulate_window's per-flow mean rates (netsim.cpp:64-94, aimd_step
+// :45-62), bit-identical to the reference.  The only cross-flow coupling is
+// the congestion test `sum(rates) >= capacity` with the sum taken
+// sequentially in flow order; that sum is computed here with eight
+// interleaved accumulators (vectorisable) and the sequential sum is redone
+// only when the two could fall on different sides of the capacity: both
+// differ from the exact sum by at most (n + n/8 + 3) u sum(|rate|) (rates
+// are non-negative), so outside a 2.5 n u sum margin the decision is the
+// reference's.  Returns the number of steps that needed the sequential sum.
+// One pass over the flows per RTT: the previous decision's update, the
+// measurement sum, then this step's clamp to the local cap and its partial
+// sums (accumulator k takes flows f = k mod 8) -- per flow, exactly
+// aimd_step's operations in its order.  An AVX2 version (IEEE add / mul / min
+// lanes, no contraction) and a scalar one compute the same bits.
+template <bool kCongested>
+void netsim_pass(size_t n, double* r, const double* alpha, const double* beta,
+                 const double* caps, double* mean, bool meas, double acc[8]) {
+  for (size_t f = 0; f < n; ++f) {
+    double x = kCongested ? r[f] * beta[f] : std::min(r[f] + alpha[f], caps[f]);
+    if (meas) mean[f] += x;
+    x = std::min(x, caps[f]);
+    r[f] = x;
+    acc[f & 7] += x;
+  }
+}
+
+template <bool kCongested>
+__attribute__((target("avx2"))) void netsim_pass_avx2(size_t n, double* r, const double* alpha,
+                                                      const double* beta, const double* caps,
+                                                      double* mean, bool meas, double acc[8]) {
+  __m256d a0 = _mm256_loadu_pd(acc), a1 = _mm256_loadu_pd(acc + 4);
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    for (int h = 0; h < 2; ++h) {
+      const size_t f = i + 4 * h;
+      const __m256d c = _mm256_loadu_pd(caps + f);
+      __m256d x = _mm256_loadu_pd(r + f);
+      // std::min(a, b) == (b < a) ? b : a == _mm256_min_pd(b, a)'s pick for non-NaN
+      x = kCongested ? _mm256_mul_pd(x, _mm256_loadu_pd(beta + f))
+                     : _mm256_min_pd(c, _mm256_add_pd(x, _mm256_loadu_pd(alpha + f)));
+      if (meas) _mm256_storeu_pd(mean + f, _mm256_add_pd(_mm256_loadu_pd(mean + f), x));
+      x = _mm256_min_pd(c, x);
+      _mm256_storeu_pd(r + f, x);
+      if (h == 0)
+        a0 = _mm256_add_pd(a0, x);
+      else
+        a1 = _mm256_add_pd(a1, x);
+    }
+  }
+  _mm256_storeu_pd(acc, a0);
+  _mm256_storeu_pd(acc + 4, a1);
+  if (i < n) netsim_pass<kCongested>(n - i, r + i, alpha + i, beta + i, caps + i, mean + i, meas, acc);
+}
+
+int mean_rates(size_t n, const double* alpha, const double* beta, const double* caps,
+               double capacity, int steps, double* mean) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  std::vector<double> rates(n, 0.0);  // the current step's rates, clamped to the caps
+  for (size_t i = 0; i < n; ++i) mean[i] = 0.0;
+  const int from = steps / 2;
+  const double margin_per = 2.5 * (double)n * 0x1p-53;
+  int exact = 0;
+  double par = 0.0;  // their sum, eight interleaved accumulators (step 0: all zero)
+  for (int s = 0; s < steps; ++s) {
+    const double margin = margin_per * par;
+    bool congested;
+    if (par - capacity > margin) {
+      congested = true;
+    } else if (capacity - par > margin) {
+      congested = false;
+    } else {  // too close to call: the reference's sequential sum
+      double total = 0.0;
+      for (size_t k = 0; k < n; ++k) total += rates[k];
+      congested = total >= capacity;
+      ++exact;
+    }
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const bool meas = s >= from;
+    double* r = rates.data();
+    if (avx2) {
+      if (congested)
+        netsim_pass_avx2<true>(n, r, alpha, beta, caps, mean, meas, acc);
+      else
+        netsim_pass_avx2<false>(n, r, alpha, beta, caps, mean, meas, acc);
+    } else {
+      if (congested)
+        netsim_pass<true>(n, r, alpha, beta, caps, mean, meas, acc);
+      else
+        netsim_pass<false>(n, r, alpha, beta, caps, mean, meas, acc);
+    }
+    par = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  }
+  const int measured = std::max(1, steps - from);
+  for (size_t k = 0; k < n; ++k) mean[k] = mean[k] / measured;
+  return exact;
+}
+
+}  // namespace ecco_netsim
 
 // ------------------------------------------------------------ scenario --
 // Restatement of the strict schema of proj/core/src/scenario.cpp:80-357.
@@ -423,13 +527,15 @@ struct ecco_sim {
   std::vector<int> membership;  // camera -> job or -1
   std::map<int, Batch> batches;
   std::vector<std::optional<std::vector<ProfRow>>> profiles;
+  std::vector<uint8_t> prof_sorted;  // budgets non-decreasing: select_config by bisection
+  std::vector<double> sel_f, sel_q, rate_of;  // per-camera scratch of a window
   std::vector<Event> events;
   size_t next_event = 0;
   std::vector<Request> pending;
   int next_job_id = 0;
   int window = 0;
   std::vector<Row> rows;
-  double timings[5] = {0, 0, 0, 0, 0};
+  double timings[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   int64_t samples = 0;
   int D = 2;
 
@@ -835,25 +941,10 @@ struct ecco_sim {
       if (!(beta[i] > 0.0 && beta[i] < 1.0)) fail(ECCO_ERR_INVALID_ARGUMENT, "netsim: beta must be in (0,1)");
     }
     const int steps = (int)std::llround(cfg.T() / cfg.rtt);
-    std::vector<double> rates(n, 0.0), sums(n, 0.0);
+    std::vector<double> sums(n, 0.0);
     if (n == 0) return sums;
-    const int from = steps / 2;
-    for (int s = 0; s < steps; ++s) {
-      double total = 0.0;
-      for (size_t i = 0; i < n; ++i) {
-        rates[i] = std::min(rates[i], caps[i]);
-        total += rates[i];
-      }
-      if (total >= cfg.capacity) {
-        for (size_t i = 0; i < n; ++i) rates[i] *= beta[i];
-      } else {
-        for (size_t i = 0; i < n; ++i) rates[i] = std::min(rates[i] + alpha[i], caps[i]);
-      }
-      if (s >= from)
-        for (size_t i = 0; i < n; ++i) sums[i] += rates[i];
-    }
-    const int measured = std::max(1, steps - from);
-    for (size_t i = 0; i < n; ++i) sums[i] = sums[i] / measured;
+    ecco_netsim::mean_rates(n, alpha.data(), beta.data(), caps.data(), cfg.capacity, steps,
+                            sums.data());
     return sums;
   }
 
@@ -883,6 +974,10 @@ struct ecco_sim {
         const size_t o = i * levels.size() + l;
         t.push_back({ob[o], of[o], oq[o], fe[o] != 0});
       }
+      bool sorted = true;
+      for (size_t l = 1; l < t.size(); ++l) sorted = sorted && !(t[l].budget < t[l - 1].budget);
+      if (prof_sorted.size() < profiles.size()) prof_sorted.resize(profiles.size(), 0);
+      prof_sorted[need[i]] = sorted;
       profiles[need[i]] = std::move(t);
     }
   }
@@ -899,10 +994,12 @@ struct ecco_sim {
     const double T = cfg.T();
     const double t0 = window * T, t1 = t0 + T;
     apply_due_events(t0);
+    const auto w_events = clk::now();
     if (learned() && !opt.host_frames) check(ctx, ecco_generate_frames(ctx, window));
     route_pending(t0);
     const auto w_routed = clk::now();
     double route_ms = ms(w0, w_routed);
+    double net_ms = 0.0, prof_ms = 0.0, sel_ms = 0.0;
     struct Stats {
       int members = 0;
       double p = 0, c = 0, delivered = 0;
@@ -969,12 +1066,15 @@ struct ecco_sim {
             if (!profiles[m.cam]) need.push_back(m.cam);
         std::sort(need.begin(), need.end());
         need.erase(std::unique(need.begin(), need.end()), need.end());
+        const auto p0 = clk::now();
         build_profiles(need);
+        prof_ms += ms(p0, clk::now());
       }
       // configs and flows (orchestrator.cpp:253-278)
       std::vector<double> fa, fb, fcap;
       std::vector<int> flow_cam;
-      std::map<int, std::pair<double, double>> selected;
+      sel_f.assign(cams.size(), 0.0);  // (frame rate, resolution) per camera this window
+      sel_q.assign(cams.size(), 0.0);
       for (int k = 0; k < J; ++k) {
         const Job& j = jobs.at(ids[k]);
         Stats& st = wstats[ids[k]];
@@ -989,15 +1089,25 @@ struct ecco_sim {
             q = cfg.fixed_q;
           } else {
             // select_config, transmission.cpp:120-138
+            // (the LAST row within budget; with non-decreasing budgets the rows
+            // within budget are a prefix, so bisection finds the same row)
             const auto& t = *profiles[m.cam];
+            const double lim = c[k] * (1.0 + 1e-12) + 1e-12;
             const ProfRow* row = nullptr;
-            for (const auto& r : t)
-              if (r.budget <= c[k] * (1.0 + 1e-12) + 1e-12) row = &r;
+            if (prof_sorted[m.cam]) {
+              const auto it = std::partition_point(
+                  t.begin(), t.end(), [lim](const ProfRow& r) { return r.budget <= lim; });
+              if (it != t.begin()) row = &*(it - 1);
+            } else {
+              for (const auto& r : t)
+                if (r.budget <= lim) row = &r;
+            }
             if (!row) row = &t.front();
             f = row->f / nm;
             q = row->q;
           }
-          selected[m.cam] = {f, q};
+          sel_f[m.cam] = f;
+          sel_q[m.cam] = q;
           const Cam& cm = cams[m.cam];
           fcap.push_back(cm.cap > 0.0 ? cm.cap : std::numeric_limits<double>::infinity());
           if (cfg.equal_bw) {
@@ -1024,16 +1134,18 @@ struct ecco_sim {
         }
       }
       if (!(cfg.rtt > 0.0)) fail(ECCO_ERR_INVALID_ARGUMENT, "netsim: rtt must be positive");
+      const auto n0 = clk::now();
       const std::vector<double> mean_rate = simulate(fa, fb, fcap);
-      std::map<int, double> rate_of;
+      net_ms += ms(n0, clk::now());
+      rate_of.assign(cams.size(), 0.0);
       for (size_t i = 0; i < flow_cam.size(); ++i) rate_of[flow_cam[i]] = mean_rate[i];
       // batch assembly (orchestrator.cpp:282-309)
       for (int k = 0; k < J; ++k) {
         const Job& j = jobs.at(ids[k]);
         double tf = 0, rs = 0, ql = 0, dl = 0;
         for (const auto& m : j.members) {
-          const auto [f, q] = selected.at(m.cam);
-          const double rate = rate_of.at(m.cam);
+          const double f = sel_f[m.cam], q = sel_q[m.cam];
+          const double rate = rate_of[m.cam];
           // adapt_compression, transmission.cpp:151-166
           double quality = 0.0;
           if (rate < 0.0) fail(ECCO_ERR_INVALID_ARGUMENT, "adapt_compression: negative rate");
@@ -1054,7 +1166,7 @@ struct ecco_sim {
           b.quality = ql / tf;
           for (const auto& m : j.members) {
             b.src.push_back(m.cam);
-            b.frac.push_back(selected.at(m.cam).first / tf);
+            b.frac.push_back(sel_f[m.cam] / tf);
           }
           batches[ids[k]] = b;
         }
@@ -1062,6 +1174,7 @@ struct ecco_sim {
       }
       // ---- remaining micro-windows: speculative chains + host replay
       const auto r0 = clk::now();
+      sel_ms = ms(a1, r0);
       if (budget > 0) {
         std::vector<Batch> bs;
         for (int id : ids) {
@@ -1184,6 +1297,12 @@ struct ecco_sim {
     timings[2] = train_ms;
     timings[3] = ms(e0, e1);
     timings[4] = replay_ms;
+    timings[5] = net_ms;
+    timings[6] = prof_ms;
+    timings[7] = ms(w0, w_events);
+    timings[8] = ms(w_events, w_routed);
+    timings[9] = sel_ms - net_ms - prof_ms;
+    timings[10] = ms(e1, w1);
     return true;
   }
 
@@ -1491,3 +1610,28 @@ size_t ecco_sim_summary_json(const ecco_sim* s, char* buf, size_t cap) {
 ecco_ctx* ecco_sim_context(ecco_sim* s) { return s->ctx; }
 
 }  // extern "C"
+
+ecco_status ecco_netsim_mean_rates(int n, const double* alpha, const double* beta,
+                                   const double* caps, double capacity, double rtt_s,
+                                   double duration_s, double* mean_rates, int* exact_steps) {
+  if (!(capacity > 0.0) || !(rtt_s > 0.0) || !(duration_s > 0.0) || n < 0)
+    return ECCO_ERR_INVALID_ARGUMENT;
+  for (int i = 0; i < n; ++i)
+    if (!(alpha[i] > 0.0) || !(beta[i] > 0.0 && beta[i] < 1.0)) return ECCO_ERR_INVALID_ARGUMENT;
+  std::vector<double> c(caps, caps + n);
+  for (double& x : c)
+    if (!(x > 0.0)) x = std::numeric_limits<double>::infinity();  // resolve_caps (netsim.cpp:33-40)
+  const int steps = (int)std::llround(duration_s / rtt_s);
+  const int ex = n ? ecco_netsim::mean_rates((size_t)n, alpha, beta, c.data(), capacity, steps,
+                                             mean_rates)
+                   : 0;
+  if (exact_steps) *exact_steps = ex;
+  return ECCO_OK;
+}
+
+int ecco_sim_last_timings_ex(const ecco_sim* s, double* out, int n) {
+  if (!s || !out) return 0;
+  const int k = std::min(n, 11);
+  for (int i = 0; i < k; ++i) out[i] = s->timings[i];
+  return k;
+}

@@ -307,3 +307,43 @@ def test_tc_eval_counts_close_and_decisions_reported(fused):
     M = ctx.eval_matrix(ids, cams=np.arange(6))
     W = np.array([[orc.count(orc.models[j], c) / 64 for j in ids] for c in range(6)])
     assert np.abs(M - W).max() <= 4.0 / 64
+
+
+# ------------------------------------------- detection-head shape (C5) --
+# BASELINE.json configs[4]: the larger per-group model (F=1024 -> H=1024 ->
+# C=96).  Shapes outside the fused kernels run the general tensor-core
+# (kind::tf32) training kernels and the exact pair evaluation; the FFMA path
+# stays bit-exact at this shape too.
+DET = dict(feat_dim=1024, hidden_dim=1024, num_classes=96, minibatch=128, ring_frames=64,
+           eval_samples=64, steps_per_gpu_s=0.5)
+
+
+@pytest.mark.parametrize("math", ["ffma", "tc"])
+def test_detection_head_shape(math):
+    m = ecco.FFMA_EXACT if math == "ffma" else ecco.TC_TF32
+    ctx, orc, rng = setup(seed=9, math=m, **DET)
+    ids = [1, 2]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members, sources, fracs, batches = _jobs(rng, len(ids), 6)
+    got = ctx.train_trajectories(ids, batches, sources, fracs, members, 4.0, 1, window=3)
+    want = orc.trajectories(ids, batches, sources, fracs, members, 4.0, 1)
+    ctx.commit(ids, [1, 1])
+    orc.commit(ids, [1, 1])
+    base = orc.base_weights()
+    if math == "ffma":
+        assert got.tobytes() == want.tobytes()
+        for j in ids:
+            for a, b in zip(ctx.get_weights(j), orc.models[j]):
+                assert a.reshape(-1).tobytes() == b.tobytes(), j
+    else:
+        assert np.abs(got - want).max() <= 4.0 / 64
+        for j in ids:
+            for a, b, b0 in zip(ctx.get_weights(j), orc.models[j], base):
+                upd = np.abs(b - b0).max()
+                assert upd > 0
+                assert np.abs(a.reshape(-1) - b).max() <= TF32_TOL_CHAIN * upd
+    M = ctx.eval_matrix(ids, cams=np.arange(6))
+    W = np.array([[orc.count(orc.models[j], c) / 64 for j in ids] for c in range(6)])
+    assert np.abs(M - W).max() <= (0 if math == "ffma" else 4.0 / 64)
