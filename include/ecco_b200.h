@@ -347,6 +347,23 @@ ecco_ctx* ecco_sim_context(ecco_sim* sim);
  * window rows and statistics.  Returns the number written. */
 int ecco_sim_last_timings_ex(const ecco_sim* sim, double* out, int n);
 
+/* ---- allocator decisions (host, no device) --------------------------------
+ * WindowAllocation (core/src/gpu_allocator.cpp:100-181: initial pass in job-id
+ * order, then greedy pick_next / round robin until the micro-window budget is
+ * spent) driven by fixed per-job accuracy trajectories -- the decision replay
+ * the window driver runs on the device's speculative trajectories (SURVEY.md
+ * H4/H8).  traj: n_jobs rows of traj_len accuracies in job_ids order (a job
+ * trained i times reads traj[min(i, traj_len-1)]).  policy 0 ecco, 1 naive,
+ * 2 total_acc_greedy.  Writes micro_windows records (job, acc before, after)
+ * and, unless naive, the initial scores in ascending job id.  Errors as the
+ * reference: invalid config -> ECCO_ERR_INVALID_ARGUMENT, no jobs or more
+ * jobs than micro-windows -> ECCO_ERR_INFEASIBLE. */
+ecco_status ecco_allocate_trajectories(int n_jobs, const int* job_ids, const int* members,
+                                       const double* traj, int traj_len, double alpha, double beta,
+                                       int micro_windows, double micro_s, int gpu_count, int bonus,
+                                       int policy, int* out_job, double* out_before,
+                                       double* out_after, double* out_initial_scores);
+
 /* ---- network model (host, no device) ---------------------------------------
  * simulate_window's per-flow mean rates (core/src/netsim.cpp:64-94 with
  * aimd_step :45-62; replaces ecco::simulate_window's mean_rate_bps for the

@@ -107,7 +107,7 @@ EXPORTS = [
     "ecco_profile_tables", "ecco_sim_default_options", "ecco_sim_create", "ecco_sim_destroy",
     "ecco_sim_last_error", "ecco_sim_step_window", "ecco_sim_last_timings",
     "ecco_sim_last_samples", "ecco_sim_trace_csv", "ecco_sim_summary_json", "ecco_sim_context",
-    "ecco_sim_last_timings_ex", "ecco_netsim_mean_rates",
+    "ecco_sim_last_timings_ex", "ecco_netsim_mean_rates", "ecco_allocate_trajectories",
 ]
 
 
@@ -125,6 +125,27 @@ def netsim_mean_rates(alpha, beta, caps, capacity, rtt_s, duration_s):
     if st:
         raise _ERRORS.get(st, EccoError)(st, "netsim: invalid argument")
     return out, ex.value
+
+
+def allocate_trajectories(job_ids, members, traj, alpha=1.0, beta=1.0, micro_windows=10,
+                          micro_s=6.0, gpu_count=1, bonus=True, policy=0):
+    """The window driver's allocator decisions (WindowAllocation,
+    gpu_allocator.cpp:100-181) on fixed accuracy trajectories: returns
+    (jobs, before, after, initial scores)."""
+    ids = np.ascontiguousarray(job_ids, np.int32)
+    mem = np.ascontiguousarray(members, np.int32)
+    t = np.ascontiguousarray(traj, np.float64)
+    n, L = t.shape
+    job = np.zeros(micro_windows, np.int32)
+    b, a, init = np.zeros(micro_windows), np.zeros(micro_windows), np.zeros(n)
+    vp = C.c_void_p
+    st = lib().ecco_allocate_trajectories(
+        n, vp(ids.ctypes.data), vp(mem.ctypes.data), vp(t.ctypes.data), L, C.c_double(alpha),
+        C.c_double(beta), micro_windows, C.c_double(micro_s), gpu_count, int(bonus), policy,
+        vp(job.ctypes.data), vp(b.ctypes.data), vp(a.ctypes.data), vp(init.ctypes.data))
+    if st:
+        raise _ERRORS.get(st, EccoError)(st, "allocate_trajectories")
+    return job, b, a, init
 
 
 def lib():

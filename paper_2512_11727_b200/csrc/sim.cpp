@@ -163,6 +163,64 @@ int mean_rates(size_t n, const double* alpha, const double* beta, const double* 
 
 }  // namespace ecco_netsim
 
+// ----------------------------------------------------------- allocator --
+namespace ecco_alloc {
+
+// cal_objective_gain, gpu_allocator.cpp:49-76 (jobs ascending by id).  The
+// size weights are fixed within a window: coef[k] = alpha * w_k / ws with
+// w_k = members_k^beta and ws summed in job order -- the reference's
+// `alpha * w / ws * gain` evaluates left to right, so coef[k] * gain[k] is the
+// same double.  They are computed once per window (the reference recomputes
+// them, pow() included, on every greedy pick: O(J) pow per micro-window).
+void size_coef(const std::vector<int>& members, double alpha, double beta,
+               std::vector<double>& coef) {
+  coef.resize(members.size());
+  double ws = 0.0;
+  for (int n : members) ws += std::pow((double)n, beta);
+  for (size_t k = 0; k < members.size(); ++k)
+    coef[k] = alpha * std::pow((double)members[k], beta) / ws;
+}
+
+// current_scores (gpu_allocator.cpp:137-144): total_acc_greedy scores
+// member_count * gain, otherwise the objective gain with the fairness bonus
+// on the least-accurate job (strict <, lowest id on ties).
+void scores(bool total_acc, bool bonus, const std::vector<double>& coef,
+            const std::vector<int>& ids, const std::vector<int>& members,
+            const std::vector<double>& acc, const std::vector<double>& gain,
+            std::vector<double>& out) {
+  out.resize(ids.size());
+  if (total_acc) {
+    for (size_t k = 0; k < ids.size(); ++k) out[k] = members[k] * gain[k];
+    return;
+  }
+  int min_k = 0;
+  double min_acc = acc[0];
+  for (size_t k = 0; k < ids.size(); ++k) {
+    out[k] = coef[k] * gain[k];
+    const double a = acc[k];
+    if (a < min_acc || (a == min_acc && ids[k] < ids[min_k])) {
+      min_acc = a;
+      min_k = (int)k;
+    }
+  }
+  if (bonus) out[min_k] += gain[min_k];
+}
+
+// pick_next (gpu_allocator.cpp:146-158): highest score, strict >, so the
+// lowest id wins ties.
+int argmax(const std::vector<double>& sc) {
+  int k = 0;
+  double b = sc[0];
+  for (size_t q = 1; q < sc.size(); ++q)
+    if (sc[q] > b) {
+      b = sc[q];
+      k = (int)q;
+    }
+  return k;
+}
+
+}  // namespace ecco_alloc
+
 // ------------------------------------------------------------ scenario --
 // Restatement of the strict schema of proj/core/src/scenario.cpp:80-357.
 
@@ -529,6 +587,7 @@ struct ecco_sim {
   std::vector<std::optional<std::vector<ProfRow>>> profiles;
   std::vector<uint8_t> prof_sorted;  // budgets non-decreasing: select_config by bisection
   std::vector<double> sel_f, sel_q, rate_of;  // per-camera scratch of a window
+  std::vector<double> coef;                    // objective size weights of a window
   std::vector<Event> events;
   size_t next_event = 0;
   std::vector<Request> pending;
@@ -898,36 +957,13 @@ struct ecco_sim {
     double before, after;
   };
 
-  // cal_objective_gain, gpu_allocator.cpp:49-76 (jobs ascending by id).
-  std::vector<double> objective_gain(const std::vector<int>& ids, const std::vector<int>& members,
-                                     const std::vector<double>& acc,
-                                     const std::vector<double>& gain) const {
-    double ws = 0.0;
-    for (int n : members) ws += std::pow((double)n, cfg.beta);
-    std::vector<double> obj(ids.size());
-    int min_k = 0;
-    double min_acc = acc[0];
-    for (size_t k = 0; k < ids.size(); ++k) {
-      const double w = std::pow((double)members[k], cfg.beta);
-      obj[k] = cfg.alpha * w / ws * gain[k];
-      const double a = acc[k];
-      if (a < min_acc || (a == min_acc && ids[k] < ids[min_k])) {
-        min_acc = a;
-        min_k = (int)k;
-      }
-    }
-    if (cfg.bonus) obj[min_k] += gain[min_k];
-    return obj;
+  void prepare_scores(const std::vector<int>& members) {
+    ecco_alloc::size_coef(members, cfg.alpha, cfg.beta, coef);
   }
-
-  std::vector<double> scores(const std::vector<int>& ids, const std::vector<int>& members,
-                             const std::vector<double>& acc, const std::vector<double>& gain) const {
-    if (cfg.policy == kTotalAcc) {
-      std::vector<double> s(ids.size());
-      for (size_t k = 0; k < ids.size(); ++k) s[k] = members[k] * gain[k];
-      return s;
-    }
-    return objective_gain(ids, members, acc, gain);
+  void scores(const std::vector<int>& ids, const std::vector<int>& members,
+              const std::vector<double>& acc, const std::vector<double>& gain,
+              std::vector<double>& s) const {
+    ecco_alloc::scores(cfg.policy == kTotalAcc, cfg.bonus, coef, ids, members, acc, gain, s);
   }
 
   // ------------------------------------------------------------ netsim --
@@ -1047,7 +1083,10 @@ struct ecco_sim {
       train_ms += ms(a0, a1);
       std::vector<double> init_scores;
       if (cfg.policy == kNaive) init_scores.assign(J, 1.0);
-      else init_scores = scores(ids, members, acc, gain);
+      else {
+        prepare_scores(members);
+        scores(ids, members, acc, gain, init_scores);
+      }
       // estimate_shares (gpu_allocator.cpp:78-98)
       const double total_gpu_s = cfg.gpus * T;
       double total = 0.0;
@@ -1187,20 +1226,15 @@ struct ecco_sim {
         auto chains = trajectories(ids, bs, mb, std::min(d0, budget));
         std::vector<int> used(J, 0), depth_of(J, std::min(d0, budget)), base(J, 1);
         int rr = 0;
+        std::vector<double> sc;
         while (budget > 0) {
           int k;
           if (cfg.policy == kNaive) {
             k = rr % J;
             ++rr;
           } else {
-            const auto sc = scores(ids, members, acc, gain);
-            k = 0;
-            double bsc = sc[0];
-            for (int q = 0; q < J; ++q)
-              if (sc[q] > bsc) {
-                bsc = sc[q];
-                k = q;
-              }
+            scores(ids, members, acc, gain, sc);
+            k = ecco_alloc::argmax(sc);
           }
           if (used[k] + 1 >= (int)chains[k].size()) {
             // chain exhausted: commit it and extend this job (depth doubling)
@@ -1634,4 +1668,63 @@ int ecco_sim_last_timings_ex(const ecco_sim* s, double* out, int n) {
   const int k = std::min(n, 11);
   for (int i = 0; i < k; ++i) out[i] = s->timings[i];
   return k;
+}
+
+ecco_status ecco_allocate_trajectories(int n_jobs, const int* job_ids, const int* members,
+                                       const double* traj, int traj_len, double alpha, double beta,
+                                       int micro_windows, double micro_s, int gpu_count, int bonus,
+                                       int policy, int* out_job, double* out_before,
+                                       double* out_after, double* out_initial_scores) {
+  // AllocatorConfig::validate (gpu_allocator.cpp:19-30) and the
+  // WindowAllocation constructor's checks (:100-123)
+  if (alpha < 0.0 || beta > 1.0 || micro_windows < 1 || !(micro_s > 0.0) || gpu_count < 1 ||
+      n_jobs < 0 || traj_len < 1 || policy < 0 || policy > 2)
+    return ECCO_ERR_INVALID_ARGUMENT;
+  std::vector<int> order(n_jobs);
+  for (int j = 0; j < n_jobs; ++j) order[j] = j;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return job_ids[a] < job_ids[b]; });
+  std::vector<int> ids(n_jobs), mem(n_jobs);
+  for (int k = 0; k < n_jobs; ++k) {
+    ids[k] = job_ids[order[k]];
+    mem[k] = members[order[k]];
+    if (mem[k] < 1) return ECCO_ERR_INVALID_ARGUMENT;
+    if (k && ids[k] == ids[k - 1]) return ECCO_ERR_INVALID_ARGUMENT;
+  }
+  if (n_jobs == 0 || n_jobs > micro_windows) return ECCO_ERR_INFEASIBLE;
+  std::vector<int> cursor(n_jobs, 0);
+  std::vector<double> acc(n_jobs, 0.0), gain(n_jobs, 0.0), coef, sc;
+  ecco_alloc::size_coef(mem, alpha, beta, coef);
+  int budget = micro_windows, rec = 0;
+  auto at = [&](int k, int c) { return traj[(size_t)order[k] * traj_len + std::min(c, traj_len - 1)]; };
+  auto run_micro = [&](int k) {  // run_micro (:125-135) over the trajectory backend
+    const double before = at(k, cursor[k]);
+    ++cursor[k];
+    const double after = at(k, cursor[k]);
+    --budget;
+    acc[k] = after;
+    gain[k] = after - before;
+    out_job[rec] = ids[k];
+    out_before[rec] = before;
+    out_after[rec] = after;
+    ++rec;
+  };
+  for (int k = 0; k < n_jobs; ++k) run_micro(k);  // run_initial_pass (:160-166)
+  if (policy != 1) {
+    ecco_alloc::scores(policy == 2, bonus != 0, coef, ids, mem, acc, gain, sc);
+    if (out_initial_scores)
+      for (int k = 0; k < n_jobs; ++k) out_initial_scores[k] = sc[k];
+  }
+  int rr = 0;
+  while (budget > 0) {  // run_remaining (:168-181)
+    int k;
+    if (policy == 1) {
+      k = rr % n_jobs;
+      ++rr;
+    } else {
+      ecco_alloc::scores(policy == 2, bonus != 0, coef, ids, mem, acc, gain, sc);
+      k = ecco_alloc::argmax(sc);
+    }
+    run_micro(k);
+  }
+  return ECCO_OK;
 }

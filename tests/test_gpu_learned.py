@@ -347,3 +347,40 @@ def test_detection_head_shape(math):
     M = ctx.eval_matrix(ids, cams=np.arange(6))
     W = np.array([[orc.count(orc.models[j], c) / 64 for j in ids] for c in range(6)])
     assert np.abs(M - W).max() <= (0 if math == "ffma" else 4.0 / 64)
+
+
+# ------------------------------------- allocator decisions on the device --
+# the allocator's decisions are a function of the accuracy
+# trajectories.  (i) on the device's trajectories the window driver's
+# decision replay equals the reference's WindowAllocation bit for bit; (iii)
+# on the FFMA path the trajectories equal the oracle's, so the decisions do.
+@pytest.mark.parametrize("math", ["ffma", "tc"])
+def test_allocator_decisions_on_device_trajectories(math):
+    import oracle
+    if not oracle.have_ref():
+        pytest.skip("oracle/_ref not built")
+    m = ecco.FFMA_EXACT if math == "ffma" else ecco.TC_TF32
+    kw = {} if math == "ffma" else FUSED
+    ctx, orc, rng = setup(seed=21, math=m, **kw)
+    ids = [3, 5, 8, 9]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members, sources, fracs, batches = _jobs(rng, len(ids), 6)
+    depth = 3
+    got = ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, depth, window=3)
+    sizes = [len(x) for x in members]
+    W = 2 * len(ids) + 2
+    mine = ecco.allocate_trajectories(ids, sizes, got, 1.0, 1.0, W, 6.0, 1, True, 0)
+    n, L = got.shape
+    rj, rb, ra, ri = np.zeros(W, np.int32), np.zeros(W), np.zeros(W), np.zeros(n)
+    st = oracle.ref().ref_allocate_trajectories(n, np.array(ids, np.int32), np.array(sizes, np.int32),
+                                                np.ascontiguousarray(got), L, 1.0, 1.0, W, 6.0, 1, 1,
+                                                0, rj, rb, ra, ri)
+    assert st == 0
+    assert (mine[0] == rj).all() and mine[1].tobytes() == rb.tobytes()
+    assert mine[2].tobytes() == ra.tobytes() and mine[3].tobytes() == ri.tobytes()
+    if math == "ffma":
+        want = orc.trajectories(ids, batches, sources, fracs, members, 6.0, depth)
+        theirs = ecco.allocate_trajectories(ids, sizes, want, 1.0, 1.0, W, 6.0, 1, True, 0)
+        assert (theirs[0] == mine[0]).all() and theirs[2].tobytes() == mine[2].tobytes()
