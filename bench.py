@@ -405,7 +405,7 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev):
     evl.numpy()[...] = el
     del f, l, e, el
     best_host = torch.empty(wl.N, dtype=torch.int32, pin_memory=True)
-    steps = max(10, args.steps)  # amortises the pipeline fill (window 0's upload is not overlapped)
+    steps = max(16, args.steps)  # amortises the pipeline fill (window 0's upload is not overlapped)
     h0, d0 = ctx.transfer_bytes()
     torch.cuda.synchronize()
     if dist is not None:
@@ -606,6 +606,25 @@ def parametric_leg(args):
     tb, sb = C.create_string_buffer(tcap), C.create_string_buffer(1 << 20)
     tl, sl = C.c_size_t(), C.c_size_t()
     R.ref_run_scenario(sc.encode(), -1, tb, tcap, C.byref(tl), sb, 1 << 20, C.byref(sl))
+    # (c) the window driver at C4 (10,000 cameras / 500 jobs, W = 1000): GPU
+    # only -- the reference needs ~40 s for window 0 there; its numbers, from
+    # the same scenario on the same kind of box, are in
+    # profiles/r01c_param_window_c4.json (tools/param_window_probe.py)
+    sc4 = json.dumps(scenarios.config("c4", windows=2, seed=1))
+    sim4 = ecco.Simulation(sc4, backend=ecco.PARAMETRIC)
+    w4 = []
+    while sim4.step_window():
+        w4.append({k: round(v, 3) for k, v in sim4.last_timings().items()})
+    sim4.close()
+    ref4 = None
+    try:
+        ref4 = json.load(open(os.path.join(ROOT, "profiles", "r01c_param_window_c4.json")))
+        ref4 = ref4.get("reference_window_ms")
+    except (OSError, ValueError):
+        pass
+    out["window_c4"] = {"workload": "c4 scenario (scenarios.config('c4', windows=2, seed=1)), "
+                                    "parametric backend; window 0 builds 10,000 profile tables",
+                        "gpu_windows": w4, "reference_window_ms_recorded": ref4}
     out["window"] = {
         "workload": "c3 scenario (scenarios.config('c3', seed=1), 4 windows), parametric backend",
         "gpu_window_ms": [w * 1e3 for w in wins], "gpu_regroup_ms": regroup,

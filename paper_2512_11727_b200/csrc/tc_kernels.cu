@@ -156,11 +156,11 @@ struct FwdArgs {
   int F, H, NT;
 };
 
+template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
   const TcTile tile = a.tiles[blockIdx.x];
   if (a.steps && a.step >= a.steps[tile.job]) return;
-  const int n0 = blockIdx.y * a.NT;
-  const int NT = a.NT;
+  const int n0 = blockIdx.y * NT;
   extern __shared__ __align__(1024) uint8_t smem[];
   float* sA[2] = {(float*)smem, (float*)(smem + 16384)};
   float* sB[2] = {(float*)(smem + 32768), (float*)(smem + 32768 + NT * kKC * 4)};
@@ -182,24 +182,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
   const float* W1 = a.wbase + (size_t)tile.slot * a.wstride;
   const int nk = a.F / kKC;
   const uint32_t idesc = idesc_tf32(kM, NT, 0, 0);
+  // per thread and chunk: kA groups of 4 X features, kB 16-byte W1 vectors;
+  // the next chunk's loads are in flight while this chunk's MMAs run
+  constexpr int kA = kM * (kKC / 4) / kThreads, kBv = kKC * (NT / 4) / kThreads;
+  uint2 ra[kA];
+  float4 rb[kBv];
+  auto load = [&](int kc) {
+    const int k0 = kc * kKC;
+#pragma unroll
+    for (int u = 0; u < kA; ++u) {
+      const int e = tid + u * kThreads, r = e >> 3, c = e & 7;
+      ra[u] = rows[r] >= 0 ? *reinterpret_cast<const uint2*>(a.xbase + rows[r] + k0 + c * 4)
+                           : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kBv; ++u) {
+      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
+      rb[u] = *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + k) * a.H + n0 + n4 * 4);
+    }
+  };
+  load(0);
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
     if (kc >= 2) mbar_wait(&bar[s], ((kc - 2) >> 1) & 1);
-    const int k0 = kc * kKC;
-    // A: 128 rows x 32 k, one 4-element (8-byte bf16) group per item
-    for (int e = tid; e < kM * (kKC / 4); e += kThreads) {
-      const int r = e >> 3, c = e & 7;  // c: 4-k chunk
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rows[r] >= 0) v = bf16x4_to_f32(*reinterpret_cast<const uint2*>(a.xbase + rows[r] + k0 + c * 4));
-      *reinterpret_cast<float4*>((uint8_t*)sA[s] + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
+#pragma unroll
+    for (int u = 0; u < kA; ++u) {
+      const int e = tid + u * kThreads, r = e >> 3, c = e & 7;
+      *reinterpret_cast<float4*>((uint8_t*)sA[s] + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) =
+          bf16x4_to_f32(ra[u]);
     }
-    // B: 32 k rows of W1 x NT columns, read as 16-byte vectors along n and
-    // scattered into the K-major tile (element (n, k))
-    for (int e = tid; e < kKC * (NT / 4); e += kThreads) {
-      const int k = e / (NT / 4), n4 = e % (NT / 4);
-      const float4 v = *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + k) * a.H + n0 + n4 * 4);
-      kmajor_put4(sB[s], n4 * 4, k, v);
+#pragma unroll
+    for (int u = 0; u < kBv; ++u) {
+      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
+      kmajor_put4(sB[s], n4 * 4, k, rb[u]);
     }
+    if (kc + 1 < nk) load(kc + 1);
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -256,11 +273,11 @@ struct Dw1Args {
   float lr;
 };
 
+template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   const int j = blockIdx.z;
   if (a.step >= a.steps[j]) return;
-  const int f0 = blockIdx.x * kM, n0 = blockIdx.y * a.NT;
-  const int NT = a.NT;
+  const int f0 = blockIdx.x * kM, n0 = blockIdx.y * NT;
   extern __shared__ __align__(1024) uint8_t smem[];
   float* sA[2] = {(float*)smem, (float*)(smem + 16384)};
   float* sB[2] = {(float*)(smem + 32768), (float*)(smem + 32768 + NT * kKC * 4)};
@@ -280,24 +297,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   const size_t r0 = (size_t)j * a.B;
   const int nk = a.B / kKC;
   const uint32_t idesc = idesc_tf32(kM, NT, 0, 0);
+  constexpr int kA = kKC * (kM / 4) / kThreads, kBv = kKC * (NT / 4) / kThreads;
+  uint2 ra[kA];
+  float4 rb[kBv];
+  auto load = [&](int kc) {
+    const int k0 = kc * kKC;
+#pragma unroll
+    for (int u = 0; u < kA; ++u) {
+      const int e = tid + u * kThreads, k = e / (kM / 4), m4 = e % (kM / 4);
+      ra[u] = *reinterpret_cast<const uint2*>(a.xbase + a.row_off[r0 + k0 + k] + f0 + m4 * 4);
+    }
+#pragma unroll
+    for (int u = 0; u < kBv; ++u) {
+      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
+      rb[u] = *reinterpret_cast<const float4*>(a.DH + (r0 + k0 + k) * a.H + n0 + n4 * 4);
+    }
+  };
+  load(0);
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
     if (kc >= 2) mbar_wait(&bar[s], ((kc - 2) >> 1) & 1);
-    const int k0 = kc * kKC;
-    // A = X^T: 32 sample rows x 128 features (bf16 -> fp32), scattered
-    // K-major (element (f, s))
-    for (int e = tid; e < kKC * (kM / 4); e += kThreads) {
-      const int k = e / (kM / 4), m4 = e % (kM / 4);
-      const float4 v = bf16x4_to_f32(
-          *reinterpret_cast<const uint2*>(a.xbase + a.row_off[r0 + k0 + k] + f0 + m4 * 4));
-      kmajor_put4(sA[s], m4 * 4, k, v);
+    // A = X^T (element (f, s)), B = dH^T (element (h, s)), both K-major
+#pragma unroll
+    for (int u = 0; u < kA; ++u) {
+      const int e = tid + u * kThreads, k = e / (kM / 4), m4 = e % (kM / 4);
+      kmajor_put4(sA[s], m4 * 4, k, bf16x4_to_f32(ra[u]));
     }
-    // B = dH^T: 32 sample rows x NT hidden columns, K-major (element (h, s))
-    for (int e = tid; e < kKC * (NT / 4); e += kThreads) {
-      const int k = e / (NT / 4), n4 = e % (NT / 4);
-      const float4 v = *reinterpret_cast<const float4*>(a.DH + (r0 + k0 + k) * a.H + n0 + n4 * 4);
-      kmajor_put4(sB[s], n4 * 4, k, v);
+#pragma unroll
+    for (int u = 0; u < kBv; ++u) {
+      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
+      kmajor_put4(sB[s], n4 * 4, k, rb[u]);
     }
+    if (kc + 1 < nk) load(kc + 1);
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -345,6 +376,19 @@ int pick_nt(int H, int ctas_per_nt1) {
 
 size_t smem_bytes(int NT) { return 32768 + 2 * (size_t)NT * kKC * 4; }
 
+void set_smem_attrs() {
+  static bool done = false;
+  if (done) return;
+  const int mx = (int)smem_bytes(256);
+  ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  done = true;
+}
+
 }  // namespace
 
 namespace tc {
@@ -357,15 +401,13 @@ void fwd_hidden(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, co
   const int NT = pick_nt(H, n_tiles);
   FwdArgs a{xbase, row_off, tiles, steps, step, wbase, wstride, Z, F, H, NT};
   const size_t sm = smem_bytes(NT);
-  static bool attr = false;
-  if (!attr) {
-    ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 + 2 * 256 * kKC * 4));
-    ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 + 2 * 256 * kKC * 4));
-    attr = true;
-  }
+  set_smem_attrs();
   const int kind = steps ? ECCO_KSTAT_TRAIN_STEP : ECCO_KSTAT_EVAL_MATRIX;
+  const dim3 grid(n_tiles, H / NT);
   ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 4,
-             (k_tc_fwd<<<dim3(n_tiles, H / NT), kThreads, sm, ctx->stream>>>(a)));
+             (NT == 256   ? k_tc_fwd<256><<<grid, kThreads, sm, ctx->stream>>>(a)
+              : NT == 128 ? k_tc_fwd<128><<<grid, kThreads, sm, ctx->stream>>>(a)
+                          : k_tc_fwd<64><<<grid, kThreads, sm, ctx->stream>>>(a)));
   ECCO_LAUNCHED(ctx);
 }
 
@@ -377,9 +419,12 @@ void dw1_update(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, co
   const int NT = pick_nt(H, n_jobs * (F / kM));
   Dw1Args a{xbase, row_off, slots, steps, step, wbase, wstride, DH, F, H, B, NT, ctx->cfg.sgd_lr};
   const size_t sm = smem_bytes(NT);
+  set_smem_attrs();
   ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_DW1, 2.0 * live_jobs * F * H * B,
              (double)live_jobs * (B * F * 2.0 + B * H * 4.0 + 2.0 * F * H * 4),
-             (k_tc_dw1<<<dim3(F / kM, H / NT, n_jobs), kThreads, sm, ctx->stream>>>(a)));
+             (NT == 256   ? k_tc_dw1<256><<<dim3(F / kM, H / NT, n_jobs), kThreads, sm, ctx->stream>>>(a)
+              : NT == 128 ? k_tc_dw1<128><<<dim3(F / kM, H / NT, n_jobs), kThreads, sm, ctx->stream>>>(a)
+                          : k_tc_dw1<64><<<dim3(F / kM, H / NT, n_jobs), kThreads, sm, ctx->stream>>>(a)));
   ECCO_LAUNCHED(ctx);
 }
 
