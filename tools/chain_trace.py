@@ -1,0 +1,84 @@
+"""Per-phase clock64 trace of the fused SGD chain (k_train_chain), for tuning.
+
+  python tools/chain_trace.py on    # instrument paper_2512_11727_b200/csrc/train_kernels.cu
+  (build, then on the GPU box: ECCO_CHAIN_TRACE=1 python bench.py --steps 1 --warmup 1 ...
+   prints "chain step s: k:cycles ..." for steps 0-3 of CTA 0, relative to the step start)
+  python tools/chain_trace.py off   # restore the saved clean source
+
+Each probe is `TS(k, tid)`: thread `tid` of CTA 0 records clock64() at point k."""
+import os
+import re
+import shutil
+import sys
+
+SRC = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                   "paper_2512_11727_b200", "csrc", "train_kernels.cu")
+SAVE = SRC + ".clean"
+
+# (anchor text, probe inserted AFTER the anchor)
+PROBES = [
+    ("    const bool more = step + 1 < nsteps;\n", "    TS(0, 0)\n"),
+    ("    mbar_wait(zfull, ph);\n    tc_fence_after();\n", "    TS(1, 0)\n"),
+    ("    mbar_wait(plfull, ph);\n    tc_fence_after();\n", "    TS(2, 0)\n"),
+    ("      mbar_wait(recv_full, ph);\n", "      TS(3, 128)\n"),
+    ("      TS(13, 128)\n", None),
+    ("    mbar_wait(dl_full, ph);\n", "    TS(4, 0)\n"),
+    ("    mbar_wait(dhfull, ph);\n    tc_fence_after();\n", "    TS(5, 0)\n"),
+    ("    // ------------------------ dW1 = X^T . dH in passes, master update (TMEM) --\n",
+     "    TS(6, 0)\n"),
+    ("      mbar_wait(gfull, gph & 1u);\n      tc_fence_after();\n", "      TS(7 + 2 * pass, 0)\n"),
+    ("        build_w2i();\n", "        TS(12, 0)\n"),
+    ("      if (!last) {\n        tc_fence_before();\n", None),
+    ("    tmem_st_wait();\n    cp_async_wait_all();\n", "    TS(13, 0)\n"),
+    ("    fence_async_smem();  // X rows, W1 / W2 operands -> next step's MMAs\n"
+     "    tc_fence_before();\n    __syncthreads();\n    tc_fence_after();\n", "    TS(14, 0)\n"),
+]
+
+HOST = '''  if (getenv("ECCO_CHAIN_TRACE")) {
+    static long long* dbg = nullptr;
+    if (!dbg) cudaMalloc(&dbg, 64 * 8);
+    cudaMemsetAsync(dbg, 0, 64 * 8, ctx->stream);
+    a.dbg = dbg;
+  }
+'''
+HOST_AFTER = '''  if (a.dbg) {
+    long long h[64];
+    cudaStreamSynchronize(ctx->stream);
+    cudaMemcpy(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    for (int st = 0; st < 4; ++st) {
+      fprintf(stderr, "chain step %d:", st);
+      for (int k = 1; k < 16; ++k)
+        if (h[st * 16 + k]) fprintf(stderr, " %d:%lld", k, h[st * 16 + k] - h[st * 16]);
+      fprintf(stderr, "\\n");
+    }
+  }
+'''
+
+
+def on():
+    s = open(SRC).read()
+    shutil.copy(SRC, SAVE)
+    s = s.replace("#include <vector>\n", "#include <vector>\n#include <cstdio>\n#include <cstdlib>\n", 1)
+    s = s.replace("  int loss_T, loss_t;\n};", "  int loss_T, loss_t;\n  long long* dbg;\n};", 1)
+    s = s.replace("__global__ void __launch_bounds__(kThreads, 1)\n    k_train_chain(",
+                  "#define TS(k, t) if (a.dbg && blockIdx.x == 0 && tid == (t) && step < 4) "
+                  "a.dbg[step * 16 + (k)] = clock64();\n"
+                  "__global__ void __launch_bounds__(kThreads, 1)\n    k_train_chain(", 1)
+    for anchor, probe in PROBES:
+        if probe is None:
+            continue
+        assert anchor in s, anchor
+        s = s.replace(anchor, anchor + probe)
+    s = s.replace("  const uint32_t smem = layout(c.feat_dim).total;\n",
+                  HOST + "  const uint32_t smem = layout(c.feat_dim).total;\n", 1)
+    i = s.rindex("  ECCO_LAUNCHED(ctx);\n}")
+    s = s[:i] + "  ECCO_LAUNCHED(ctx);\n" + HOST_AFTER + "}" + s[i + len("  ECCO_LAUNCHED(ctx);\n}"):]
+    open(SRC, "w").write(s)
+
+
+def off():
+    shutil.move(SAVE, SRC)
+
+
+if __name__ == "__main__":
+    {"on": on, "off": off}[sys.argv[1]]()
