@@ -625,6 +625,24 @@ def parametric_leg(args):
     out["window_c4"] = {"workload": "c4 scenario (scenarios.config('c4', windows=2, seed=1)), "
                                     "parametric backend; window 0 builds 10,000 profile tables",
                         "gpu_windows": w4, "reference_window_ms_recorded": ref4}
+    # (d) the same window driver with the LEARNED backend at C4: routing and
+    # regroup on the device evaluation matrix, every micro-window's SGD chain,
+    # the netsim and allocator replay on the host (no reference counterpart:
+    # the reference has no learned trainer)
+    scl = json.dumps(scenarios.config("c4", windows=2, seed=1, local_acc=0.0))
+    siml = ecco.Simulation(scl, backend=ecco.LEARNED, math=ecco.TC_TF32, full_matrix=1,
+                           steps_per_gpu_s=5000.0)
+    wl_ = []
+    while siml.step_window():
+        d = {k: round(v, 3) for k, v in siml.last_timings().items()}
+        d["samples"] = siml.last_samples()
+        d["samples_per_s"] = d["samples"] / (d["window_ms"] / 1e3)
+        wl_.append(d)
+    siml.close()
+    out["learned_window_c4"] = {
+        "workload": "c4 scenario, local_model_acc 0 (fresh group models accept joins), learned "
+                    "F512-H256-C16 classifier, tf32/bf16 tensor-core math, steps_per_gpu_s 5000",
+        "gpu_windows": wl_}
     out["window"] = {
         "workload": "c3 scenario (scenarios.config('c3', seed=1), 4 windows), parametric backend",
         "gpu_window_ms": [w * 1e3 for w in wins], "gpu_regroup_ms": regroup,
