@@ -1,0 +1,273 @@
+/* ecco_b200_dropin.hpp -- the reference-side C++ binding of the B200 path.
+ *
+ * Header-only; a maintainer adds it to the reference build (it includes the
+ * reference's own headers "ecco/*.hpp" from proj/core/include) and links
+ * libecco_b200.so.  It implements the reference's callback interfaces over
+ * the C-ABI of ecco_b200.h, so the reference call sites stay unchanged:
+ *
+ *   ecco::TrainingBackend  (core/include/ecco/gpu_allocator.hpp:37-42)
+ *       CudaTrainingBackend replaces JobTrainingBackend
+ *       (core/src/orchestrator.cpp:31-70): every job's speculative chain of
+ *       micro-windows is computed in one batched device call; evaluate() /
+ *       train() replay it as WindowAllocation::run_micro
+ *       (core/src/gpu_allocator.cpp:125-135) consumes it, and finish() commits
+ *       the granted prefixes and writes the trained models back into the
+ *       reference's JobMap.
+ *   ecco::ModelEvalFn      (core/include/ecco/grouping.hpp:23)
+ *       make_eval_fn replaces eval_job_on_scene (orchestrator.cpp:186-191).
+ *
+ * Parametric backend (the reference's accuracy model, bit-identical).  The
+ * status -> exception mapping mirrors core/include/ecco/types.hpp:29-48.
+ * Verified by oracle/dropin_test.cpp against the unmodified reference.
+ */
+#ifndef ECCO_B200_DROPIN_HPP_
+#define ECCO_B200_DROPIN_HPP_
+
+#include <algorithm>
+#include <functional>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ecco/accuracy_model.hpp"
+#include "ecco/gpu_allocator.hpp"
+#include "ecco/grouping.hpp"
+#include "ecco/job.hpp"
+#include "ecco/types.hpp"
+#include "ecco_b200.h"
+
+namespace ecco_b200 {
+
+inline void check(ecco_ctx* c, ecco_status s, int window = 0) {
+  switch (s) {
+    case ECCO_OK:
+      return;
+    case ECCO_ERR_INVALID_ARGUMENT:
+      throw std::invalid_argument(ecco_last_error(c));
+    case ECCO_ERR_LOGIC:
+      throw std::logic_error(ecco_last_error(c));
+    case ECCO_ERR_INFEASIBLE:
+      throw ecco::InfeasibleScheduleError(window, ecco_last_error(c));
+    case ECCO_ERR_SCHEMA:
+      throw ecco::SchemaError("", ecco_last_error(c));
+    default:
+      throw std::runtime_error(ecco_last_error(c));
+  }
+}
+
+// A parametric device context plus the CameraId <-> index table and the
+// job models it holds.
+class Device {
+ public:
+  Device(const ecco::ModelParams& p, int scene_dims, int max_clusters, int max_jobs,
+         int max_cameras, int device = 0)
+      : D_(scene_dims), P_(max_clusters) {
+    ecco_config c;
+    ecco_default_config(&c);
+    c.backend = ECCO_BACKEND_PARAMETRIC;
+    c.device = device;
+    c.scene_dims = scene_dims;
+    c.max_clusters = max_clusters;
+    c.max_jobs = max_jobs;
+    c.max_cameras = max_cameras;
+    c.params = {p.learning_rate_k, p.similarity_lambda, p.acc_floor, p.acc_ceil,
+                p.cluster_similarity_threshold};
+    c.max_depth = 64;
+    check(nullptr, ecco_create(&c, &ctx_));
+  }
+  ~Device() { ecco_destroy(ctx_); }
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+
+  ecco_ctx* ctx() const { return ctx_; }
+  int dims() const { return D_; }
+
+  // CameraState table (accuracy_model.hpp:27-34): scenes and pixel throughput,
+  // indexed in std::map (CameraId string) order.
+  void set_cameras(const std::map<ecco::CameraId, ecco::CameraState>& cams) {
+    index_.clear();
+    std::vector<double> scenes, tp;
+    for (const auto& [id, c] : cams) {
+      if ((int)c.scene.size() != D_) throw std::invalid_argument("camera scene dimension");
+      index_[id] = (int)index_.size();
+      scenes.insert(scenes.end(), c.scene.begin(), c.scene.end());
+      tp.push_back(c.gpu_pixel_throughput);
+    }
+    check(ctx_, ecco_set_cameras(ctx_, (int)tp.size(), scenes.data(), tp.data()));
+  }
+  int cam(const ecco::CameraId& id) const { return index_.at(id); }
+
+  // RetrainJob::model <-> device slot.
+  void put_model(ecco::JobId id, const ecco::ModelState& m) {
+    const int k = (int)m.clusters.size();
+    if (k > P_) throw std::invalid_argument("model has more clusters than max_clusters");
+    std::vector<double> cl((size_t)P_ * D_, 0.0), pr(P_, 0.0), ce(D_, 0.0);
+    for (int i = 0; i < k; ++i) {
+      std::copy(m.clusters[i].begin(), m.clusters[i].end(), cl.begin() + (size_t)i * D_);
+      pr[i] = m.proficiency[i];
+    }
+    std::copy(m.centroid.begin(), m.centroid.end(), ce.begin());
+    const int clen = (int)m.centroid.size();
+    check(ctx_, ecco_put_models(ctx_, 1, &id, &k, cl.data(), pr.data(), ce.data(), &clen));
+  }
+  ecco::ModelState get_model(ecco::JobId id) const {
+    int k = 0, clen = 0;
+    std::vector<double> cl((size_t)P_ * D_), pr(P_), ce(D_);
+    check(ctx_, ecco_get_models(ctx_, 1, &id, &k, cl.data(), pr.data(), ce.data(), &clen));
+    ecco::ModelState m;
+    for (int i = 0; i < k; ++i) {
+      m.clusters.emplace_back(cl.begin() + (size_t)i * D_, cl.begin() + (size_t)(i + 1) * D_);
+      m.proficiency.push_back(pr[i]);
+    }
+    m.centroid.assign(ce.begin(), ce.begin() + clen);
+    return m;
+  }
+
+ private:
+  ecco_ctx* ctx_ = nullptr;
+  int D_, P_;
+  std::map<ecco::CameraId, int> index_;
+};
+
+// JobTrainingBackend (orchestrator.cpp:31-70) on the device.  Construct it
+// where the reference constructs JobTrainingBackend, with the same JobMap,
+// batches and bootstrap function; every train() must be for `micro_gpu_s`
+// (the allocator's gpu_count * micro_window_duration_s, gpu_allocator.cpp:127).
+class CudaTrainingBackend final : public ecco::TrainingBackend {
+ public:
+  CudaTrainingBackend(Device& dev, ecco::JobMap& jobs,
+                      const std::map<ecco::JobId, ecco::TrainingBatchStats>& batches,
+                      std::function<ecco::TrainingBatchStats(const ecco::RetrainJob&)> bootstrap,
+                      double micro_gpu_s, int depth = 4, int window = 0)
+      : dev_(dev), jobs_(jobs), gpu_s_(micro_gpu_s), depth_(std::max(1, depth)),
+        window_(window) {
+    for (auto& [id, job] : jobs_) {
+      dev_.put_model(id, job.model);
+      Chain c;
+      const auto it = batches.find(id);
+      const ecco::TrainingBatchStats b = it != batches.end() ? it->second : bootstrap(job);
+      c.batch = {b.delivered_frame_rate, b.resolution, b.quality_factor};
+      for (const auto& [cam, frac] : b.source_mix) {  // std::map order, as train_step
+        c.src.push_back(dev_.cam(cam));
+        c.frac.push_back(frac);
+      }
+      for (const auto& m : job.members) c.mem.push_back(dev_.cam(m.camera));
+      chains_[id] = std::move(c);
+    }
+  }
+
+  double evaluate(ecco::JobId id) override {
+    prepare();
+    Chain& c = chain(id);
+    return c.acc[c.used];
+  }
+
+  void train(ecco::JobId id, double gpu_seconds) override {
+    if (gpu_seconds != gpu_s_)
+      throw std::invalid_argument("CudaTrainingBackend: micro-window GPU time changed");
+    prepare();
+    Chain& c = chain(id);
+    if (c.used + 1 >= (int)c.acc.size()) {  // chain spent: commit it, extend (depth doubling)
+      const int next = std::min(64, 2 * ((int)c.acc.size() - 1));
+      commit(id);
+      run(id, next);
+    }
+    ++c.used;
+  }
+
+  // After run_remaining: commits every granted prefix and writes the trained
+  // models into the JobMap (what JobTrainingBackend::train did in place).
+  void finish() {
+    for (auto& [id, c] : chains_) {
+      commit(id);
+      jobs_.at(id).model = dev_.get_model(id);
+    }
+    prepared_ = false;
+  }
+
+ private:
+  struct Chain {
+    ecco_batch batch{};
+    std::vector<int> src, mem;
+    std::vector<double> frac, acc;
+    int used = 0, base = 0;
+  };
+
+  Chain& chain(ecco::JobId id) { return chains_.at(id); }
+
+  // Every job's chain in one batched device call (the first evaluate()).
+  void prepare() {
+    if (prepared_) return;
+    prepared_ = true;
+    std::vector<int> ids, so{0}, mo{0}, src, mem, base;
+    std::vector<double> frac;
+    std::vector<ecco_batch> bs;
+    for (auto& [id, c] : chains_) {
+      ids.push_back(id);
+      bs.push_back(c.batch);
+      src.insert(src.end(), c.src.begin(), c.src.end());
+      frac.insert(frac.end(), c.frac.begin(), c.frac.end());
+      mem.insert(mem.end(), c.mem.begin(), c.mem.end());
+      so.push_back((int)src.size());
+      mo.push_back((int)mem.size());
+      base.push_back(c.base);
+    }
+    std::vector<double> acc(ids.size() * (depth_ + 1));
+    check(dev_.ctx(), ecco_train_trajectories(dev_.ctx(), (int)ids.size(), ids.data(), bs.data(),
+                                              so.data(), src.data(), frac.data(), mo.data(),
+                                              mem.data(), base.data(), window_, gpu_s_, depth_,
+                                              acc.data()));
+    for (size_t j = 0; j < ids.size(); ++j) {
+      Chain& c = chain(ids[j]);
+      c.acc.assign(acc.begin() + j * (depth_ + 1), acc.begin() + (j + 1) * (depth_ + 1));
+      c.used = 0;
+    }
+  }
+
+  void run(ecco::JobId id, int depth) {
+    Chain& c = chain(id);
+    const int so[2] = {0, (int)c.src.size()}, mo[2] = {0, (int)c.mem.size()};
+    c.acc.assign(depth + 1, 0.0);
+    check(dev_.ctx(), ecco_train_trajectories(dev_.ctx(), 1, &id, &c.batch, so, c.src.data(),
+                                              c.frac.data(), mo, c.mem.data(), &c.base,
+                                              window_, gpu_s_, depth, c.acc.data()));
+    c.used = 0;
+  }
+
+  void commit(ecco::JobId id) {
+    Chain& c = chain(id);
+    if (c.acc.empty()) return;
+    check(dev_.ctx(), ecco_commit(dev_.ctx(), 1, &id, &c.used));
+    c.base += c.used;
+    c.acc.clear();
+    c.used = 0;
+  }
+
+  Device& dev_;
+  ecco::JobMap& jobs_;
+  double gpu_s_;
+  int depth_;
+  int window_;
+  std::map<ecco::JobId, Chain> chains_;
+  bool prepared_ = false;
+};
+
+// eval_job_on_scene (orchestrator.cpp:186-191) on the device: eval(job.model,
+// probe with `scene`).  Per call it ships the job's model and evaluates one
+// pair; a routing pass that knows all its requests up front batches them
+// with ecco_eval_matrix / ecco_route_propose instead.
+inline ecco::ModelEvalFn make_eval_fn(Device& dev) {
+  return [&dev](const ecco::RetrainJob& job, const ecco::SceneVector& scene) {
+    if ((int)scene.size() != dev.dims()) throw std::invalid_argument("scene dimension");
+    dev.put_model(job.id, job.model);
+    double out = 0.0;
+    check(dev.ctx(),
+          ecco_eval_matrix(dev.ctx(), 1, scene.data(), nullptr, 1, &job.id, nullptr, &out));
+    return out;
+  };
+}
+
+}  // namespace ecco_b200
+
+#endif  // ECCO_B200_DROPIN_HPP_

@@ -37,6 +37,8 @@ def build(ref=True):
     targets = ["oracle"]
     if ref and os.path.isdir(REFERENCE_ROOT):
         targets.append("ref")
+        if os.path.exists(os.path.join(HERE, "..", "paper_2512_11727_b200", "libecco_b200.so")):
+            targets.append("dropin")
     subprocess.run(["make", "-s", "-C", HERE, "-j8"] + targets, check=True)
 
 

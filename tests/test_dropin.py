@@ -1,0 +1,25 @@
+"""The reference-side C++ binding (include/ecco_b200_dropin.hpp) inside the
+UNMODIFIED reference library: the reference's own WindowAllocation and
+group_request, driven once by its JobTrainingBackend / eval_job_on_scene
+semantics and once by ecco_b200::CudaTrainingBackend / make_eval_fn on the
+GPU, must produce identical schedules, trained models and assignments
+(oracle/dropin_test.cpp, built by oracle/Makefile where /root/reference
+exists and shipped prebuilt)."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+BIN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                   "dropin_test")
+
+
+@pytest.mark.skipif(not os.path.exists(BIN), reason="oracle/_ref/dropin_test not built")
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_reference_allocator_and_router_over_the_dropin(seed):
+    r = subprocess.run([BIN, str(seed), "9"], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [x for x in r.stdout.splitlines() if x.startswith("trial")]
+    assert len(lines) == 9 and all(x.endswith("identical") for x in lines)
