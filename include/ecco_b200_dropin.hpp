@@ -15,6 +15,10 @@
  *       reference's JobMap.
  *   ecco::ModelEvalFn      (core/include/ecco/grouping.hpp:23)
  *       make_eval_fn replaces eval_job_on_scene (orchestrator.cpp:186-191).
+ *   ecco::ProbeFn          (core/include/ecco/transmission.hpp:46)
+ *       build_profile_tables replaces build_profile_table driven by
+ *       make_accuracy_probe (transmission.cpp:52-118) for many cameras at
+ *       once (Simulation::profile, orchestrator.cpp:94-116).
  *
  * Parametric backend (the reference's accuracy model, bit-identical).  The
  * status -> exception mapping mirrors core/include/ecco/types.hpp:29-48.
@@ -34,6 +38,7 @@
 #include "ecco/gpu_allocator.hpp"
 #include "ecco/grouping.hpp"
 #include "ecco/job.hpp"
+#include "ecco/transmission.hpp"
 #include "ecco/types.hpp"
 #include "ecco_b200.h"
 
@@ -266,6 +271,53 @@ inline ecco::ModelEvalFn make_eval_fn(Device& dev) {
           ecco_eval_matrix(dev.ctx(), 1, scene.data(), nullptr, 1, &job.id, nullptr, &out));
     return out;
   };
+}
+
+// build_profile_table(camera, budget_levels, grid, make_accuracy_probe(camera,
+// params, reference_rate_bps, bpp_ref), opts) for every camera in one device
+// launch (every grid probe of every level, the tie_epsilon / bias tie-break
+// fused).  The cameras must be in the Device's camera table; the params are
+// the Device's.
+inline std::vector<ecco::ProfileTable> build_profile_tables(
+    Device& dev, const std::vector<ecco::CameraState>& cameras,
+    const std::vector<double>& budget_levels, const std::vector<ecco::SamplingConfig>& grid,
+    const ecco::ProfilerOptions& opts, double reference_rate_bps, double bpp_ref) {
+  if (grid.empty()) throw std::invalid_argument("build_profile_table: empty config grid");
+  if (budget_levels.empty()) throw std::invalid_argument("build_profile_table: no budget levels");
+  std::vector<double> levels = budget_levels;
+  std::sort(levels.begin(), levels.end());  // rows in ascending budget order
+  std::vector<int> idx, bias;
+  for (const auto& c : cameras) {
+    idx.push_back(dev.cam(c.id));
+    bias.push_back(opts.bias == ecco::ProfileBias::frame_rate ? 1 : 0);
+  }
+  std::vector<double> gf, gr;
+  for (const auto& g : grid) {
+    gf.push_back(g.frame_rate);
+    gr.push_back(g.resolution);
+  }
+  const size_t n = cameras.size() * levels.size();
+  std::vector<double> ob(n), of(n), oq(n);
+  std::vector<uint8_t> fe(n);
+  check(dev.ctx(), ecco_profile_tables(dev.ctx(), (int)cameras.size(), idx.data(), bias.data(),
+                                       (int)levels.size(), levels.data(), (int)grid.size(),
+                                       gf.data(), gr.data(), opts.window_duration_s,
+                                       opts.tie_epsilon, reference_rate_bps, bpp_ref, ob.data(),
+                                       of.data(), oq.data(), fe.data()));
+  std::vector<ecco::ProfileTable> out(cameras.size());
+  for (size_t i = 0; i < cameras.size(); ++i) {
+    out[i].camera = cameras[i].id;
+    for (size_t l = 0; l < levels.size(); ++l) {
+      const size_t o = i * levels.size() + l;
+      ecco::ProfileRow r;
+      r.budget_gpu_s = ob[o];
+      r.config.frame_rate = of[o];
+      r.config.resolution = oq[o];
+      r.feasible = fe[o] != 0;
+      out[i].rows.push_back(r);
+    }
+  }
+  return out;
 }
 
 }  // namespace ecco_b200

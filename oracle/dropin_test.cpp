@@ -12,7 +12,9 @@
 // (every micro-window record) and the trained models must be identical bit
 // for bit.  The reference's group_request (core/src/grouping.cpp:18-62) is
 // then run with the reference's eval_job_on_scene and with
-// ecco_b200::make_eval_fn; the assignments must be identical.
+// ecco_b200::make_eval_fn, and every camera's profile table is built by the
+// reference's build_profile_table + make_accuracy_probe and by
+// ecco_b200::build_profile_tables; assignments and rows must be identical.
 //
 // Built by oracle/Makefile (target `dropin`, where /root/reference exists)
 // into oracle/_ref/dropin_test; run by tests/test_dropin.py on the GPU box.
@@ -30,6 +32,7 @@
 #include "ecco/gpu_allocator.hpp"
 #include "ecco/grouping.hpp"
 #include "ecco/job.hpp"
+#include "ecco/transmission.hpp"
 #include "ecco_b200_dropin.hpp"
 
 using namespace ecco;
@@ -209,8 +212,34 @@ int main(int argc, char** argv) {
       if (a.job != b.job || a.created != b.created || !same(a.acc, b.acc)) ++bad;
       ++routed;
     }
-    std::printf("trial %d: %zu micro-windows, %d jobs, %d routed requests, policy %d: %s\n", trial,
-                ra.size(), n_jobs, routed, (int)pol, bad ? "MISMATCH" : "identical");
+    // ProbeFn: the profile tables of every camera (Simulation::profile's grid
+    // and levels, orchestrator.cpp:94-116), reference vs one device launch
+    std::vector<double> levels;
+    for (int k = 1; k <= cfg.micro_windows; ++k)
+      levels.push_back(k * cfg.gpu_count * cfg.micro_window_duration_s);
+    const auto grid_cfgs = make_config_grid({1, 2, 5, 10, 15}, {360, 480, 720, 960});
+    ProfilerOptions popts;
+    popts.window_duration_s = cfg.micro_windows * cfg.micro_window_duration_s;
+    popts.bias = trial % 2 ? ProfileBias::frame_rate : ProfileBias::resolution;
+    std::vector<CameraState> cam_list;
+    for (const auto& [id, c] : cams) cam_list.push_back(c);
+    const auto tables = ecco_b200::build_profile_tables(dev, cam_list, levels, grid_cfgs, popts,
+                                                        1e6, 0.1);
+    int rows = 0;
+    for (size_t i = 0; i < cam_list.size(); ++i) {
+      const ProfileTable want = build_profile_table(
+          cam_list[i], levels, grid_cfgs, make_accuracy_probe(cam_list[i], params, 1e6, 0.1), popts);
+      if (want.rows.size() != tables[i].rows.size()) ++bad;
+      for (size_t l = 0; l < want.rows.size() && l < tables[i].rows.size(); ++l, ++rows) {
+        const auto &w = want.rows[l], &g = tables[i].rows[l];
+        if (!same(w.budget_gpu_s, g.budget_gpu_s) || !same(w.config.frame_rate, g.config.frame_rate) ||
+            !same(w.config.resolution, g.config.resolution) || w.feasible != g.feasible)
+          ++bad;
+      }
+    }
+    std::printf("trial %d: %zu micro-windows, %d jobs, %d routed requests, %d profile rows, "
+                "policy %d: %s\n", trial, ra.size(), n_jobs, routed, rows, (int)pol,
+                bad ? "MISMATCH" : "identical");
     failures += bad != 0;
   }
   return failures ? 1 : 0;

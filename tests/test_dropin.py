@@ -23,3 +23,4 @@ def test_reference_allocator_and_router_over_the_dropin(seed):
     assert r.returncode == 0, r.stdout + r.stderr
     lines = [x for x in r.stdout.splitlines() if x.startswith("trial")]
     assert len(lines) == 9 and all(x.endswith("identical") for x in lines)
+    assert all("profile rows" in x for x in lines)
