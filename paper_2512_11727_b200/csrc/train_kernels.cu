@@ -734,9 +734,9 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
   a.loss_t = loss_t;
   const uint32_t smem = layout(c.feat_dim).total;
   static bool attr = false;
-  if (!attr) {
+  if (!attr) {  // the opt-in maximum once: every supported shape fits under it
     ECCO_CUDA(cudaFuncSetAttribute(k_train_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+                                   232448));
     attr = true;
   }
   const int cs = c.hidden_dim / kHS;

@@ -238,8 +238,9 @@ def _step_tf32(x, y, w, lr):
             b2 - lr * DL.sum(0)]
 
 
-def _tc_weights_error(steps_one, fused):
-    ctx, orc, rng = setup(seed=5, math=ecco.TC_TF32, **(FUSED if fused else {}))
+def _tc_weights_error(steps_one, fused, shape=None):
+    ctx, orc, rng = setup(seed=5, math=ecco.TC_TF32,
+                          **(shape if shape else FUSED if fused else {}))
     ids = [1, 2, 3, 4, 5]
     ctx.seed_models(ids)
     for j in ids:
@@ -281,6 +282,20 @@ def test_tc_single_step_weights_within_tolerance(fused):
     vs_oracle, vs_emulated = _tc_weights_error(True, fused)
     assert vs_emulated <= (TC_TOL_EMULATED if fused else TF32_TOL_EMULATED), vs_emulated
     assert vs_oracle <= (TC_TOL_ONE_STEP if fused else TF32_TOL_ONE_STEP), vs_oracle
+
+
+# Other shapes of the fused chain: cluster of 8 (H = 512), one dW1 pass
+# (F = 128), the bench's F = 512 (two dW1 passes).
+@pytest.mark.parametrize("shape", [dict(feat_dim=128, hidden_dim=256),
+                                   dict(feat_dim=512, hidden_dim=256),
+                                   dict(feat_dim=256, hidden_dim=512)])
+def test_fused_chain_shapes_within_tolerance(shape):
+    cfg = dict(FUSED)
+    cfg.update(shape)
+    vs_oracle, vs_emulated = _tc_weights_error(True, True, cfg)
+    assert vs_emulated <= TC_TOL_EMULATED, vs_emulated
+    assert vs_oracle <= TC_TOL_ONE_STEP, vs_oracle
+    assert _tc_weights_error(False, True, cfg)[0] <= TC_TOL_CHAIN
 
 
 @pytest.mark.parametrize("fused", [True, False])
