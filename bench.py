@@ -286,11 +286,17 @@ def run_b200(args, rank, world, local_rank):
     launches = ctx.launches - l0
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
-    # TRAIN_CHAIN: the fused SGD chain (ECCO_KSTAT_TRAIN_STEP); DW1 / HEAD are
-    # the unfused tensor-core / FFMA kernels (other shapes, --math ffma)
+    # ECCO_KSTAT_TRAIN_STEP is the fused SGD chain where it applies
+    # (train_kernels.cu: tensor-core math, B = 128, C = 16, F a power of two
+    # <= 512, H = 256 / 512), else the unfused forward; DW1 / HEAD are the
+    # unfused tensor-core / FFMA kernels (other shapes, --math ffma)
+    F, H = DIMS["feat_dim"], DIMS["hidden_dim"]
+    chain = (args.math == "tf32" and DIMS["minibatch"] == 128 and DIMS["num_classes"] == 16
+             and F <= 512 and F % 128 == 0 and F & (F - 1) == 0 and H in (256, 512))
     kst = {name: ctx.kernel_stat(getattr(ecco, "KSTAT_" + stat)) for name, stat in
            (("EVAL_MATRIX", "EVAL_MATRIX"), ("EVAL_PAIRS", "EVAL_PAIRS"),
-            ("TRAIN_CHAIN", "TRAIN_STEP"), ("TRAIN_DW1", "TRAIN_DW1"), ("TRAIN_HEAD", "TRAIN_HEAD"))}
+            ("TRAIN_CHAIN" if chain else "TRAIN_FWD", "TRAIN_STEP"), ("TRAIN_DW1", "TRAIN_DW1"),
+            ("TRAIN_HEAD", "TRAIN_HEAD"))}
     ctx.profile(False)
     ms, regroup_ms, retrain_ms = reduce_max(dist, [ms, phase["regroup"], phase["retrain"]])
     samples = reduce_sum(dist, wl.samples_per_step_local() * args.steps)
