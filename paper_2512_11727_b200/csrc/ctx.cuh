@@ -299,7 +299,10 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
                  int n_probes, const int* d_cams, int n_ent, const int* d_ent_slot,
                  const int* d_ent_col, int n_tiles_override, const int* d_tile_ebeg,
                  const int* d_probe_slot, int ld, int* d_counts, float* dbg_logits,
-                 double live_pairs);
+                 double live_pairs, bool pair_tiles = false);
+// The CTA-pair evaluation kernel applies (C == 16, not disabled): pair lists
+// may then be cut into 256-row super tiles (pair_tiles = true).
+bool pair_supported(const ecco_ctx* ctx);
 void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* d_mask,
                    double* d_out);
 bool train_supported(const ecco_ctx* ctx);

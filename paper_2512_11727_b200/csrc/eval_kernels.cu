@@ -469,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
-      for (int e = 0; e < a.n_ent; ++e, ++u) {
+      for (int e = tile_ent_begin(a, m), e1 = tile_ent_end(a, m); e < e1; ++e, ++u) {
         const int slot = a.ent_slot[e];
         const int wb = u & 1;
         mbar_wait(&bars->w2_empty[wb], ((u >> 1) & 1) ^ 1);
@@ -539,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int m = pair; m < n_super; m += npairs, ++t) {
         mbar_wait(&bars->a_full, t & 1);
         tc_fence_after();
-        for (int e = 0; e < a.n_ent; ++e, ++u) {
+        for (int e = tile_ent_begin(a, m), e1 = tile_ent_end(a, m); e < e1; ++e, ++u) {
           for (int hf = 0; hf < nh; ++hf) {
             const uint32_t v = u * nh + hf, zb = v & 1;
             mbar_wait(&bars->z_empty[zb], ((v >> 1) & 1) ^ 1);
@@ -585,8 +585,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const bool valid = R < a.n_rows;
       const int p = valid ? R / a.S : 0;
       const int label = valid ? a.labels[(size_t)a.cams[p] * a.S + (R % a.S)] : -1;
-      for (int e = 0; e < a.n_ent; ++e, ++u) {
+      for (int e = tile_ent_begin(a, m), e1 = tile_ent_end(a, m); e < e1; ++e, ++u) {
         const uint32_t wb = u & 1;
+        const int slot = a.ent_slot[e];
         const float* b1 = reinterpret_cast<const float*>(sBias + wb * a.bias_bytes);
         const float* b2 = b1 + a.H;
         mbar_wait(&bars->bias_full[wb], (u >> 1) & 1);
@@ -649,8 +650,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_arrive_cluster(lead(&bars->l_empty[lb]));
           mbar_arrive(&bars->bias_empty[wb]);
         }
-        const unsigned bal = __ballot_sync(0xffffffffu, valid && best == label);
-        if (lane == 0 && bal) atomicAdd(a.counts + (size_t)p * a.ld + a.ent_col[e], __popc(bal));
+        // pairs mode: a row counts only under its probe's own slot
+        const bool ok = valid && best == label && (!a.probe_slot || a.probe_slot[p] == slot);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0 && bal) {
+          const size_t idx = a.probe_slot ? (size_t)p : (size_t)p * a.ld + a.ent_col[e];
+          atomicAdd(a.counts + idx, __popc(bal));
+        }
       }
     }
   }
@@ -785,6 +791,10 @@ uint32_t img_bytes(const ecco_config& g) {
   return (w2t_bytes(g) + 4u * (g.hidden_dim + g.num_classes) + 15u) & ~15u;
 }
 
+bool pair_supported(const ecco_ctx* ctx) {
+  return pair_enabled(ctx->cfg);
+}
+
 bool supported(const ecco_ctx* ctx) {
   const ecco_config& g = ctx->cfg;
   return g.feat_dim % 64 == 0 && g.feat_dim <= 512 && g.hidden_dim % kHalf == 0 &&
@@ -834,7 +844,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
                  int n_probes, const int* d_cams, int n_ent, const int* d_ent_slot,
                  const int* d_ent_col, int n_tiles_override, const int* d_tile_ebeg,
                  const int* d_probe_slot, int ld, int* d_counts, float* dbg_logits,
-                 double live_pairs) {
+                 double live_pairs, bool pair_tiles) {
   const ecco_config& g = ctx->cfg;
   if (!ctx->map_x) ctx->map_x = new CUtensorMap(make_map(ctx->d_eval, (uint64_t)g.max_cameras * g.eval_samples,
                                                          g.feat_dim, 64));
@@ -882,7 +892,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
                        (double)n_ent * (g.feat_dim * g.hidden_dim * 2.0 + a.img_bytes) +
                        4.0 * live_pairs;
   const int kind = d_tile_ebeg ? ECCO_KSTAT_EVAL_PAIRS : ECCO_KSTAT_EVAL_MATRIX;
-  if (!d_tile_ebeg && !d_probe_slot && sh.map_w2_pair && pair_enabled(g)) {
+  if ((pair_tiles || (!d_tile_ebeg && !d_probe_slot)) && sh.map_w2_pair && pair_enabled(g)) {
     // CTA-pair kernel: 256-row super tiles, half a W1^T box per CTA per stage
     const size_t pfixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)(a.H / 64) * 1024 +
                           2 * (size_t)a.bias_bytes + sizeof(PairBars);

@@ -685,12 +685,16 @@ static void pair_counts_fused(ecco_ctx* ctx, const Shadow& sh, const float* wbas
                               int n_pairs, const int* h_slot, const int* d_slot, const int* d_cam,
                               int* d_counts) {
   const int S = ctx->cfg.eval_samples;
-  const int n_tiles = (int)(((size_t)n_pairs * S + 127) / 128);
+  // 128-row tiles, or 256-row super tiles for the CTA-pair kernel (half the
+  // W1^T stream per FLOP): each tile walks the distinct slots of its pairs
+  const bool pair = fused::pair_supported(ctx);
+  const int TR = pair ? 256 : 128;
+  const int n_tiles = (int)(((size_t)n_pairs * S + TR - 1) / TR);
   std::vector<int> ebeg(n_tiles + 1), ent;
   for (int m = 0; m < n_tiles; ++m) {
     ebeg[m] = (int)ent.size();
-    const int p_lo = (int)((size_t)m * 128 / S);
-    const int p_hi = std::min(n_pairs, (int)(((size_t)m * 128 + 127) / S) + 1);
+    const int p_lo = (int)((size_t)m * TR / S);
+    const int p_hi = std::min(n_pairs, (int)(((size_t)m * TR + TR - 1) / S) + 1);
     for (int p = p_lo; p < p_hi; ++p)
       if (std::find(ent.begin() + ebeg[m], ent.end(), h_slot[p]) == ent.end()) ent.push_back(h_slot[p]);
   }
@@ -699,7 +703,7 @@ static void pair_counts_fused(ecco_ctx* ctx, const Shadow& sh, const float* wbas
   int* d_ebeg = ctx->upload(13, ebeg.data(), ebeg.size());
   ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(n_pairs, 1), ctx->stream));
   fused::eval_counts(ctx, sh, wbase, wstride, n_pairs, d_cam, (int)ent.size(), d_ent, d_ent,
-                     n_tiles, d_ebeg, d_slot, 0, d_counts, nullptr, (double)n_pairs);
+                     n_tiles, d_ebeg, d_slot, 0, d_counts, nullptr, (double)n_pairs, pair);
 }
 
 void generate_frames(ecco_ctx* ctx, int window) {
