@@ -249,84 +249,39 @@ __global__ void __launch_bounds__(256) k_l_logits(LDims g, int n_rows, const int
 // stop W2 / Z / DL being re-read from L2 once per output.
 constexpr int kHT = 32;  // reduction chunk of the tiled head kernels
 
-// logits: 64 rows x 32 classes per block, 4 rows x 2 classes per thread.
-__global__ void __launch_bounds__(256) k_l_logits_t(LDims g, int n_rows, const int* blk_slot,
+// logits: 64 rows x 32 classes per block, 4 rows x 4 classes per thread.
+__global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const int* blk_slot,
                                                     Gate gate, const float* wbase,
                                                     size_t n_params, const float* Z, float* L) {
   const int blk = blockIdx.x, c0 = blockIdx.y * 32;
   if (!gate.live_row((size_t)blk * kRB)) return;
   const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
   const float* b2 = W2 + (size_t)g.H * g.C;
-  __shared__ float Zs[kHT][kRB + 1];
-  __shared__ float Ws[kHT][32];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  float acc[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  __shared__ __align__(16) float Zs[kHT][kRB + 4];
+  __shared__ __align__(16) float Ws[kHT][32 + 4];
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  float acc[4][4] = {};
   const size_t r0 = (size_t)blk * kRB;
   for (int k0 = 0; k0 < g.H; k0 += kHT) {
-    for (int e = tid; e < kRB * kHT; e += 256) {
+    for (int e = tid; e < kRB * kHT; e += 128) {
       const int r = e / kHT, k = e % kHT;
       const float z = Z[(r0 + r) * g.H + k0 + k];
       Zs[k][r] = z > 0.0f ? z : 0.0f;
     }
-    for (int e = tid; e < kHT * 32; e += 256) {
+    for (int e = tid; e < kHT * 32; e += 128) {
       const int k = e / 32, c = e % 32;
       Ws[k][c] = c0 + c < g.C ? W2[(size_t)(k0 + k) * g.C + c0 + c] : 0.0f;
     }
     __syncthreads();
 #pragma unroll 8
     for (int k = 0; k < kHT; ++k) {
-      const float w0 = Ws[k][tx * 2], w1 = Ws[k][tx * 2 + 1];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float z = Zs[k][ty * 4 + i];
-        acc[i][0] = __fmaf_rn(z, w0, acc[i][0]);
-        acc[i][1] = __fmaf_rn(z, w1, acc[i][1]);
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int c = c0 + tx * 2 + q;
-      if (c < g.C) L[(r0 + ty * 4 + i) * g.C + c] = __fadd_rn(acc[i][q], b2[c]);
-    }
-}
-
-// dH: 64 rows x 64 hidden units per block, 4 x 4 per thread; c ascending.
-__global__ void __launch_bounds__(256) k_l_dh_t(LDims g, int n_rows, const int* blk_slot,
-                                                Gate gate, const float* wbase, size_t n_params,
-                                                const float* Z, const float* DL, float* DH) {
-  const int blk = blockIdx.x, h0 = blockIdx.y * 64;
-  if (!gate.live_row((size_t)blk * kRB)) return;
-  const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
-  __shared__ float Ds[kHT][kRB + 1];
-  __shared__ float Ws[kHT][64 + 1];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  float acc[4][4] = {};
-  const size_t r0 = (size_t)blk * kRB;
-  for (int c0 = 0; c0 < g.C; c0 += kHT) {
-    const int nc = min(kHT, g.C - c0);
-    for (int e = tid; e < kRB * kHT; e += 256) {
-      const int r = e / kHT, c = e % kHT;
-      Ds[c][r] = c < nc ? DL[(r0 + r) * g.C + c0 + c] : 0.0f;
-    }
-    for (int e = tid; e < 64 * kHT; e += 256) {
-      const int h = e / kHT, c = e % kHT;
-      Ws[c][h] = c < nc ? W2[(size_t)(h0 + h) * g.C + c0 + c] : 0.0f;
-    }
-    __syncthreads();
-    for (int c = 0; c < nc; ++c) {
-      float w[4], d[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = Ws[c][tx * 4 + q];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) d[i] = Ds[c][ty * 4 + i];
+      const float4 z = *reinterpret_cast<const float4*>(&Zs[k][ty * 4]);
+      const float4 w = *reinterpret_cast<const float4*>(&Ws[k][tx * 4]);
+      const float zv[4] = {z.x, z.y, z.z, z.w}, wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[i][q] = __fmaf_rn(d[i], w[q], acc[i][q]);
+        for (int q = 0; q < 4; ++q) acc[i][q] = __fmaf_rn(zv[i], wv[q], acc[i][q]);
     }
     __syncthreads();
   }
@@ -334,15 +289,60 @@ __global__ void __launch_bounds__(256) k_l_dh_t(LDims g, int n_rows, const int* 
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const size_t o = (r0 + ty * 4 + i) * g.H + h0 + tx * 4 + q;
+      const int c = c0 + tx * 4 + q;
+      if (c < g.C) L[(r0 + ty * 4 + i) * g.C + c] = __fadd_rn(acc[i][q], b2[c]);
+    }
+}
+
+// dH: 64 rows x 64 hidden units per block, 8 rows x 4 units per thread; c ascending.
+__global__ void __launch_bounds__(128) k_l_dh_t(LDims g, int n_rows, const int* blk_slot,
+                                                Gate gate, const float* wbase, size_t n_params,
+                                                const float* Z, const float* DL, float* DH) {
+  const int blk = blockIdx.x, h0 = blockIdx.y * 64;
+  if (!gate.live_row((size_t)blk * kRB)) return;
+  const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
+  __shared__ __align__(16) float Ds[kHT][kRB + 4];
+  __shared__ __align__(16) float Ws[kHT][64 + 4];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  float acc[8][4] = {};
+  const size_t r0 = (size_t)blk * kRB;
+  for (int c0 = 0; c0 < g.C; c0 += kHT) {
+    const int nc = min(kHT, g.C - c0);
+    for (int e = tid; e < kRB * kHT; e += 128) {
+      const int r = e / kHT, c = e % kHT;
+      Ds[c][r] = c < nc ? DL[(r0 + r) * g.C + c0 + c] : 0.0f;
+    }
+    for (int e = tid; e < 64 * kHT; e += 128) {
+      const int h = e / kHT, c = e % kHT;
+      Ws[c][h] = c < nc ? W2[(size_t)(h0 + h) * g.C + c0 + c] : 0.0f;
+    }
+    __syncthreads();
+    for (int c = 0; c < nc; ++c) {
+      const float4 w = *reinterpret_cast<const float4*>(&Ws[c][tx * 4]);
+      const float4 d0 = *reinterpret_cast<const float4*>(&Ds[c][ty * 8]);
+      const float4 d1 = *reinterpret_cast<const float4*>(&Ds[c][ty * 8 + 4]);
+      const float wv[4] = {w.x, w.y, w.z, w.w};
+      const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = __fmaf_rn(dv[i], wv[q], acc[i][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const size_t o = (r0 + ty * 8 + i) * g.H + h0 + tx * 4 + q;
       DH[o] = Z[o] > 0.0f ? acc[i][q] : 0.0f;
     }
 }
 
-// W2 / b2 update of one job: 64 hidden units x 32 classes per block, 4 x 2
+// W2 / b2 update of one job: 64 hidden units x 32 classes per block, 4 x 4
 // per thread; rows s ascending.  Blocks of the first hidden tile also sum
 // the b2 gradient of their classes.
-__global__ void __launch_bounds__(256) k_l_update2_t(LDims g, int n_jobs, const int* slots,
+__global__ void __launch_bounds__(128) k_l_update2_t(LDims g, int n_jobs, const int* slots,
                                                      const int* steps, int step, float* wbase,
                                                      size_t n_params, const float* Z,
                                                      const float* DL) {
@@ -350,32 +350,32 @@ __global__ void __launch_bounds__(256) k_l_update2_t(LDims g, int n_jobs, const 
   if (step >= steps[j]) return;
   float* W2 = wbase + (size_t)slots[j] * n_params + (size_t)g.F * g.H + g.H;
   float* b2 = W2 + (size_t)g.H * g.C;
-  __shared__ float Zs[kHT][64 + 1];
-  __shared__ float Ds[kHT][32 + 1];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  float acc[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  __shared__ __align__(16) float Zs[kHT][64 + 4];
+  __shared__ __align__(16) float Ds[kHT][32 + 4];
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  float acc[4][4] = {};
   float bacc = 0.0f;
   const size_t r0 = (size_t)j * g.B;
   for (int s0 = 0; s0 < g.B; s0 += kHT) {
     const int ns = min(kHT, g.B - s0);
-    for (int e = tid; e < kHT * 64; e += 256) {
+    for (int e = tid; e < kHT * 64; e += 128) {
       const int s = e / 64, h = e % 64;
       const float z = s < ns ? Z[(r0 + s0 + s) * g.H + h0 + h] : 0.0f;
       Zs[s][h] = z > 0.0f ? z : 0.0f;
     }
-    for (int e = tid; e < kHT * 32; e += 256) {
+    for (int e = tid; e < kHT * 32; e += 128) {
       const int s = e / 32, c = e % 32;
       Ds[s][c] = s < ns && c0 + c < g.C ? DL[(r0 + s0 + s) * g.C + c0 + c] : 0.0f;
     }
     __syncthreads();
     for (int s = 0; s < ns; ++s) {
-      const float d0 = Ds[s][tx * 2], d1 = Ds[s][tx * 2 + 1];
+      const float4 z = *reinterpret_cast<const float4*>(&Zs[s][ty * 4]);
+      const float4 d = *reinterpret_cast<const float4*>(&Ds[s][tx * 4]);
+      const float zv[4] = {z.x, z.y, z.z, z.w}, dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float z = Zs[s][ty * 4 + i];
-        acc[i][0] = __fmaf_rn(z, d0, acc[i][0]);
-        acc[i][1] = __fmaf_rn(z, d1, acc[i][1]);
-      }
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = __fmaf_rn(zv[i], dv[q], acc[i][q]);
     }
     if (blockIdx.y == 0 && tid < 32)
       for (int s = 0; s < ns; ++s) bacc = __fadd_rn(bacc, Ds[s][tid]);
@@ -384,8 +384,8 @@ __global__ void __launch_bounds__(256) k_l_update2_t(LDims g, int n_jobs, const 
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int c = c0 + tx * 2 + q;
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + tx * 4 + q;
       if (c < g.C) {
         float* w = W2 + (size_t)(h0 + ty * 4 + i) * g.C + c;
         *w = __fmaf_rn(-g.lr, acc[i][q], *w);
@@ -774,7 +774,7 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
       ECCO_LAUNCHED(ctx);
     }
     ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
-               (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 256, 0, ctx->stream>>>(
+               (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
                    g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L)));
     ECCO_LAUNCHED(ctx);
     k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, L, ctx->d_eval_labels,
@@ -1037,13 +1037,13 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
         ECCO_LAUNCHED(ctx);
       }
       ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_HEAD, 8.0 * lrows * g.H * g.C, lrows * g.H * 12,
-                 ((k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 256, 0, ctx->stream>>>(
+                 ((k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
                       g, rows, blk_slot, gate, wt, spec_stride, Z, L)),
                   (k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(
                       g, rows, gate, L, row_lab, DL, loss_rows)),
-                  (k_l_dh_t<<<dim3(rows / kRB, g.H / 64), 256, 0, ctx->stream>>>(
+                  (k_l_dh_t<<<dim3(rows / kRB, g.H / 64), 128, 0, ctx->stream>>>(
                       g, rows, blk_slot, gate, wt, spec_stride, Z, DL, DH)),
-                  (k_l_update2_t<<<dim3(n_jobs, g.H / 64, (g.C + 31) / 32), 256, 0,
+                  (k_l_update2_t<<<dim3(n_jobs, g.H / 64, (g.C + 31) / 32), 128, 0,
                                    ctx->stream>>>(g, n_jobs, d_slots, d_steps, step, wt,
                                                   spec_stride, Z, DL))));
       ctx->launches += 3;
