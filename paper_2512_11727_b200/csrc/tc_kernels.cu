@@ -345,21 +345,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   }
   mbar_wait(&bar[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
   tc_fence_after();
+  // epilogue: each warp's 32 feature rows x 32 gradient columns go through a
+  // shared-memory transpose so the W1 read-modify-write runs along rows
+  // (128-byte coalesced) instead of one 16-byte piece per feature row
   float* W1 = a.wbase + (size_t)a.slots[j] * a.wstride;
-  const int f = f0 + warp * 32 + (tid & 31);
+  const int lane = tid & 31;
+  float* tr = reinterpret_cast<float*>(smem) + warp * 32 * 33;  // operand stages are free
   for (int c0 = 0; c0 < NT; c0 += 32) {
     float v[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-    float* wr = W1 + (size_t)f * a.H + n0 + c0;
 #pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      float4 w = *reinterpret_cast<float4*>(wr + i);
-      w.x = fmaf(-a.lr, v[i], w.x);
-      w.y = fmaf(-a.lr, v[i + 1], w.y);
-      w.z = fmaf(-a.lr, v[i + 2], w.z);
-      w.w = fmaf(-a.lr, v[i + 3], w.w);
-      *reinterpret_cast<float4*>(wr + i) = w;
-    }
+    for (int i = 0; i < 32; ++i) tr[i * 33 + lane] = v[i];  // tr[col][row]
+    __syncwarp();
+    float* wcol = W1 + (size_t)(f0 + warp * 32) * a.H + n0 + c0 + lane;
+    float wv[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) wv[r] = wcol[(size_t)r * a.H];  // 32 loads in flight
+#pragma unroll
+    for (int r = 0; r < 32; ++r) wcol[(size_t)r * a.H] = fmaf(-a.lr, tr[lane * 33 + r], wv[r]);
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
