@@ -159,27 +159,31 @@ struct Gate {
 constexpr int kHB = 128;  // hidden columns per block
 constexpr int kKT = 32;   // k tile
 
+// HB hidden units per block (128, or 32 when the grid would not fill the
+// GPU); a thread owns 4 rows x HB/16 columns; k sequential per output.
+template <int HB>
 __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* xbase,
                                                        const int64_t* row_off,
                                                        const int* blk_slot, Gate gate,
                                                        const float* wbase, size_t n_params,
                                                        float* Z) {
+  constexpr int NC = HB / 16;
   const int blk = blockIdx.x;
   if (!gate.live_row((size_t)blk * kRB)) return;
-  const int h0 = blockIdx.y * kHB;
+  const int h0 = blockIdx.y * HB;
   const float* W1 = wbase + (size_t)blk_slot[blk] * n_params;
   const float* b1 = W1 + (size_t)g.F * g.H;
   __shared__ float As[kKT][kRB + 4];
-  __shared__ __align__(16) float Bs[kKT][kHB];
+  __shared__ __align__(16) float Bs[kKT][HB];
   __shared__ int64_t rows[kRB];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   if (tid < kRB) rows[tid] = row_off[(size_t)blk * kRB + tid];
   __syncthreads();
-  float acc[4][8];
+  float acc[4][NC];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < NC; ++j) acc[i][j] = 0.0f;
   for (int k0 = 0; k0 < g.F; k0 += kKT) {
     // X tile: 64 rows x 32 k (bf16 pairs), transposed into As[k][row]
     for (int e = tid; e < kRB * kKT / 2; e += 256) {
@@ -188,25 +192,23 @@ __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* 
       As[kk][r] = __uint_as_float(two << 16);
       As[kk + 1][r] = __uint_as_float(two & 0xFFFF0000u);
     }
-    for (int e = tid; e < kKT * kHB / 4; e += 256) {
-      const int kk = e / (kHB / 4), c4 = (e % (kHB / 4)) * 4;
+    for (int e = tid; e < kKT * HB / 4; e += 256) {
+      const int kk = e / (HB / 4), c4 = (e % (HB / 4)) * 4;
       *reinterpret_cast<float4*>(&Bs[kk][c4]) =
           *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + kk) * g.H + h0 + c4);
     }
     __syncthreads();
 #pragma unroll 8
     for (int kk = 0; kk < kKT; ++kk) {
-      float a[4], b[8];
+      float a[4], b[NC];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8]);
-      const float4 b4 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8 + 4]);
-      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-      b[4] = b4.x; b[5] = b4.y; b[6] = b4.z; b[7] = b4.w;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) b[j] = Bs[kk][tx * NC + j];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < NC; ++j) acc[i][j] = __fmaf_rn(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -214,11 +216,23 @@ __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* 
   for (int i = 0; i < 4; ++i) {
     const size_t r = (size_t)blk * kRB + ty * 4 + i;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int h = h0 + tx * 8 + j;
+    for (int j = 0; j < NC; ++j) {
+      const int h = h0 + tx * NC + j;
       Z[r * g.H + h] = __fadd_rn(acc[i][j], b1[h]);
     }
   }
+}
+
+// Launches the hidden layer with the widest tile that still fills the GPU.
+static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint16_t* xbase,
+                               const int64_t* row_off, const int* blk_slot, Gate gate,
+                               const float* wbase, size_t n_params, float* Z) {
+  if ((long)nb * (g.H / kHB) >= 2 * 148)
+    k_l_hidden_ffma<kHB><<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(g, xbase, row_off, blk_slot,
+                                                                       gate, wbase, n_params, Z);
+  else
+    k_l_hidden_ffma<32><<<dim3(nb, g.H / 32), 256, 0, ctx->stream>>>(g, xbase, row_off, blk_slot,
+                                                                     gate, wbase, n_params, Z);
 }
 
 // logits[row, c] = sum_k relu(Z[row,k]) * W2[k,c] (sequential k) + b2[c].
@@ -768,9 +782,8 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
     } else {
       ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_MATRIX, 2.0 * rows * g.F * g.H,
                  (double)rows * g.F * 2 + (double)g.F * g.H * 4,
-                 (k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
-                     g, ctx->d_eval, row_off, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w,
-                     ctx->n_params, Z)));
+                 launch_hidden_ffma(ctx, nb, g, ctx->d_eval, row_off, blk_slot,
+                                    Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z));
       ECCO_LAUNCHED(ctx);
     }
     ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
@@ -1032,8 +1045,8 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
       } else {
         ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_STEP, 2.0 * lrows * g.F * g.H,
                    lrows * g.F * 2 + (double)live * g.F * g.H * 4,
-                   (k_l_hidden_ffma<<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(
-                       g, ctx->d_frames, row_off, blk_slot, gate, wt, spec_stride, Z)));
+                   launch_hidden_ffma(ctx, nb, g, ctx->d_frames, row_off, blk_slot, gate, wt,
+                                      spec_stride, Z));
         ECCO_LAUNCHED(ctx);
       }
       ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_HEAD, 8.0 * lrows * g.H * g.C, lrows * g.H * 12,
