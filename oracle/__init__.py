@@ -38,7 +38,7 @@ def build(ref=True):
     if ref and os.path.isdir(REFERENCE_ROOT):
         targets.append("ref")
         if os.path.exists(os.path.join(HERE, "..", "paper_2512_11727_b200", "libecco_b200.so")):
-            targets.append("dropin")
+            targets += ["dropin", "unit"]
     subprocess.run(["make", "-s", "-C", HERE, "-j8"] + targets, check=True)
 
 
