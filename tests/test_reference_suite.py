@@ -35,3 +35,17 @@ def test_reference_unit_suite_on_the_reference():
 @pytest.mark.gpu
 def test_reference_unit_suite_on_the_b200_build():
     _run("unit_tests_b200")
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_on_the_b200_build():
+    """acceptance_main.cpp's ten criteria (equivalence to the reference
+    allocator on 120 instances, Fig. 7 regroup, determinism, ..., #10 runs
+    unit_tests_b200) with the device arithmetic."""
+    path = os.path.join(REF, "acceptance_b200")
+    if not os.path.exists(path):
+        pytest.skip("oracle/_ref/acceptance_b200 not built")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "FAIL" not in r.stdout
