@@ -345,6 +345,11 @@ def run_b200(args, rank, world, local_rank):
         }
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_sample(wl.N, wl.G)
+        if world == 1 and not args.no_scaling:
+            try:
+                line["scaling_emulation"] = scaling_emulation(args, ms / args.steps)
+            except Exception as e:  # reported, never fatal for the headline line
+                line["scaling_emulation"] = {"error": repr(e)}
         if world == 1 and not args.no_parametric:
             try:
                 line["parametric"] = parametric_leg(args)
@@ -354,6 +359,69 @@ def run_b200(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
+    """One GPU standing in for rank 0 of an N-GPU run: its shard of the
+    groups (the largest block), the full camera set, the evaluation of its
+    column block, the route over N blocks (the other ranks' blocks as they
+    would arrive from the all-gather) and its chains.  The per-rank device
+    time projects the N-GPU step; the NCCL all-gather of the blocks
+    (N x cameras x block x 8 B) is not included -- at C4 and N = 8 it moves
+    40 MB per rank over NVLink."""
+    import torch
+    import paper_2512_11727_b200 as ecco
+    out = {}
+    for world in worlds:
+        wl = Workload(args.config, 0, world)
+        ctx = ecco.Context(backend=ecco.LEARNED, device=torch.cuda.current_device(),
+                           math=ecco.TC_TF32 if args.math == "tf32" else ecco.FFMA_EXACT,
+                           max_cameras=wl.N, max_jobs=max(1, len(wl.local)), max_depth=DEPTH,
+                           steps_per_gpu_s=float(STEPS), **DIMS)
+        ctx.set_cameras(wl.scenes, wl.tp)
+        ctx.generate_frames(0)
+        ctx.seed_models(wl.local)
+        prep = ctx.prepare_trajectories(
+            wl.local, [BATCH] * len(wl.local), [wl.members(g) for g in wl.local],
+            [[1.0 / wl.per] * wl.per for _ in wl.local], [wl.members(g) for g in wl.local])
+        cams = np.arange(wl.N, dtype=np.int32)
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        blocks = torch.zeros((world, wl.N if MATRIX else 1, wl.gb), dtype=torch.float64,
+                             device="cuda")
+        best = torch.empty(wl.N, dtype=torch.int32, device="cuda")
+        best_acc = torch.empty(wl.N, dtype=torch.float64, device="cuda")
+        acc_host = np.zeros((len(wl.local), DEPTH + 1))
+
+        def step(w):
+            with torch.cuda.stream(stream):
+                if MATRIX:
+                    ctx.eval_matrix_dev(wl.local, blocks[0].data_ptr(), cams=cams)
+                    ctx.route_matrix_dev(wl.N, wl.gb, blocks.data_ptr(), best.data_ptr(),
+                                         best_acc.data_ptr(), n_blocks=world)
+                ctx.train_prepared(prep, GPU_S, DEPTH, window=w, out=acc_host)
+                ctx.commit(wl.local, [DEPTH] * len(wl.local))
+
+        for w in range(2):
+            step(w + 1)
+        ctx.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 3
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for k in range(n):
+            step(10 + k)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        ctx.close()
+        del blocks
+        torch.cuda.empty_cache()
+        samples = wl.samples_per_step_local() * world
+        out[str(world)] = {"groups_on_rank0": len(wl.local), "rank0_ms_per_step": ms,
+                           "projected_value": samples / (ms / 1e3),
+                           "projected_efficiency": n1_ms / (world * ms)}
+    return out
 
 
 def kernel_roofline(name, stat, pk, pk_kind, args, traffic=None):
@@ -704,6 +772,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
+    ap.add_argument("--no-scaling", action="store_true",
+                    help="skip the single-GPU emulation of rank 0 at N = 2, 4, 8")
     ap.add_argument("--no-parametric", action="store_true",
                     help="skip the parametric-backend vs reference-library leg")
     args = ap.parse_args()
