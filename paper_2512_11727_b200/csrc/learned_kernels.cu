@@ -235,32 +235,13 @@ static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint
                                                                      gate, wbase, n_params, Z);
 }
 
-// logits[row, c] = sum_k relu(Z[row,k]) * W2[k,c] (sequential k) + b2[c].
-__global__ void __launch_bounds__(256) k_l_logits(LDims g, int n_rows, const int* blk_slot,
-                                                  Gate gate, const float* wbase,
-                                                  size_t n_params, const float* Z, float* L) {
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (size_t)n_rows * g.C) return;
-  const int r = (int)(idx / g.C), c = (int)(idx % g.C);
-  const int blk = r / kRB;
-  if (!gate.live_row((size_t)blk * kRB)) return;
-  const float* W = wbase + (size_t)blk_slot[blk] * n_params;
-  const float* W2 = W + (size_t)g.F * g.H + g.H;
-  const float* b2 = W2 + (size_t)g.H * g.C;
-  const float* z = Z + (size_t)r * g.H;
-  float a = 0.0f;
-  for (int k = 0; k < g.H; ++k) {
-    const float zk = z[k];
-    a = __fmaf_rn(zk > 0.0f ? zk : 0.0f, W2[(size_t)k * g.C + c], a);
-  }
-  L[idx] = __fadd_rn(a, b2[c]);
-}
-
-// Shared-memory tiled forms of the head contractions (used for every shape;
-// the naive one-thread-per-output kernels above are their specification).
-// Each output keeps ITS sequential accumulation order (k, c or s ascending,
-// one __fmaf_rn per term), so the results are the same bits; the tiles only
-// stop W2 / Z / DL being re-read from L2 once per output.
+// The head contractions of the general path, shared-memory tiled:
+//   logits[row, c] = sum_k relu(Z[row, k]) * W2[k, c] (k ascending) + b2[c]
+//   dH[row, k]     = Z[row, k] > 0 ? sum_c DL[row, c] * W2[k, c] (c ascending) : 0
+//   W2[k, c]      -= lr * sum_s relu(Z[s, k]) * DL[s, c] (s ascending); b2 likewise
+// Every output keeps that sequential accumulation order (one __fmaf_rn per
+// term, orc_sgd_step's order), so the FFMA math stays bit-exact with the
+// oracle; the tiles only stop W2 / Z / DL being re-read per output.
 constexpr int kHT = 32;  // reduction chunk of the tiled head kernels
 
 // logits: 64 rows x 32 classes per block, 4 rows x 4 classes per thread.
@@ -427,52 +408,6 @@ __global__ void k_l_softmax_grad(LDims g, int n_rows, Gate gate, const float* L,
     DL[(size_t)r * g.C + c] = __fmul_rn(__fsub_rn(p, c == y ? 1.0f : 0.0f), invB);
   }
   loss_rows[r] = logf(sum) - (l[y] - m);
-}
-
-// dh[row, k] = Z > 0 ? sum_c DL[row,c] * W2[k,c] : 0 (pre-update W2).
-__global__ void __launch_bounds__(256) k_l_dh(LDims g, int n_rows, const int* blk_slot,
-                                              Gate gate, const float* wbase,
-                                              size_t n_params, const float* Z, const float* DL,
-                                              float* DH) {
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (size_t)n_rows * g.H) return;
-  const int r = (int)(idx / g.H), k = (int)(idx % g.H);
-  const int blk = r / kRB;
-  if (!gate.live_row((size_t)blk * kRB)) return;
-  const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
-  float a = 0.0f;
-  if (Z[idx] > 0.0f)
-    for (int c = 0; c < g.C; ++c) a = __fmaf_rn(DL[(size_t)r * g.C + c], W2[(size_t)k * g.C + c], a);
-  DH[idx] = a;
-}
-
-// W2[k,c] -= lr * sum_s relu(Z[s,k]) * DL[s,c]; b2[c] -= lr * sum_s DL[s,c].
-// One job = B rows starting at job * B.
-__global__ void __launch_bounds__(256) k_l_update2(LDims g, int n_jobs, const int* slots,
-                                                   const int* steps, int step, float* wbase,
-                                                   size_t n_params, const float* Z,
-                                                   const float* DL) {
-  const int per = g.H * g.C + g.C;
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (size_t)n_jobs * per) return;
-  const int j = (int)(idx / per), q = (int)(idx % per);
-  if (step >= steps[j]) return;
-  float* W2 = wbase + (size_t)slots[j] * n_params + (size_t)g.F * g.H + g.H;
-  float* b2 = W2 + (size_t)g.H * g.C;
-  const size_t r0 = (size_t)j * g.B;
-  float a = 0.0f;
-  if (q < g.H * g.C) {
-    const int k = q / g.C, c = q % g.C;
-    for (int s = 0; s < g.B; ++s) {
-      const float zk = Z[(r0 + s) * g.H + k];
-      a = __fmaf_rn(zk > 0.0f ? zk : 0.0f, DL[(r0 + s) * g.C + c], a);
-    }
-    W2[q] = __fmaf_rn(-g.lr, a, W2[q]);
-  } else {
-    const int c = q - g.H * g.C;
-    for (int s = 0; s < g.B; ++s) a = __fadd_rn(a, DL[(r0 + s) * g.C + c]);
-    b2[c] = __fmaf_rn(-g.lr, a, b2[c]);
-  }
 }
 
 // W1[f,h] -= lr * sum_s x[s,f] * dh[s,h] (sequential s).  Tile 64 f x 128 h.
