@@ -24,6 +24,7 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <charconv>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -516,11 +517,22 @@ struct Row {
 };
 
 // format_value, metrics.cpp:42-47.
-std::string fmt(double v) {
-  if (v == 0.0) return "0";
+// format_value (metrics.cpp:42-47): "%.9g", with -0 written as 0.
+// std::to_chars(general, 9) is specified as printf's %.9g in the C locale
+// (same digits, exponent form and rounding) at a fraction of the cost.
+void fmt_to(std::string& out, double v) {
+  if (v == 0.0) {
+    out += '0';
+    return;
+  }
   char buf[32];
-  std::snprintf(buf, sizeof buf, "%.9g", v);
-  return buf;
+  const auto r = std::to_chars(buf, buf + sizeof buf, v, std::chars_format::general, 9);
+  out.append(buf, r.ptr);
+}
+std::string fmt(double v) {
+  std::string s;
+  fmt_to(s, v);
+  return s;
 }
 
 // ---------------------------------------------------------------- state --
@@ -1428,19 +1440,33 @@ struct ecco_sim {
   }
 
   // -------------------------------------------------------------- output --
-  std::string trace_csv() const {
-    std::string s = "record,window,time_s,camera,job,v1,v2,v3,v4,v5\n";
-    for (const auto& r : rows) {
+  // trace.csv (metrics.cpp:49-59).  Rows are formatted once, incrementally:
+  // a call formats only the rows appended since the previous one.
+  const std::string& trace_csv() const {
+    if (trace_text.empty()) trace_text = "record,window,time_s,camera,job,v1,v2,v3,v4,v5\n";
+    char ib[24];
+    for (; trace_rows < rows.size(); ++trace_rows) {
+      const Row& r = rows[trace_rows];
+      std::string& s = trace_text;
       s += kind_name(r.kind);
-      s += ',' + std::to_string(r.window) + ',' + fmt(r.t) + ',';
+      s += ',';
+      s.append(ib, std::to_chars(ib, ib + sizeof ib, r.window).ptr);
+      s += ',';
+      fmt_to(s, r.t);
+      s += ',';
       if (r.cam >= 0) s += cams[r.cam].id;
       s += ',';
-      if (r.job >= 0) s += std::to_string(r.job);
-      for (int k = 0; k < 5; ++k) s += ',' + fmt(r.v[k]);
+      if (r.job >= 0) s.append(ib, std::to_chars(ib, ib + sizeof ib, r.job).ptr);
+      for (int k = 0; k < 5; ++k) {
+        s += ',';
+        fmt_to(s, r.v[k]);
+      }
       s += '\n';
     }
-    return s;
+    return trace_text;
   }
+  mutable std::string trace_text;
+  mutable size_t trace_rows = 0;
 
   std::string summary_json() const {
     json j;
@@ -1630,7 +1656,7 @@ ecco_status ecco_sim_last_timings(const ecco_sim* s, double* out5) {
 int64_t ecco_sim_last_samples(const ecco_sim* s) { return s->samples; }
 
 size_t ecco_sim_trace_csv(const ecco_sim* s, char* buf, size_t cap) {
-  const std::string t = s->trace_csv();
+  const std::string& t = s->trace_csv();
   if (buf && cap) std::memcpy(buf, t.data(), std::min(cap, t.size()));
   return t.size();
 }
