@@ -1,5 +1,6 @@
 // Internal state of an ecco_ctx and the helpers shared by the .cu files.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -201,7 +202,7 @@ struct ecco_ctx {
   }
 
   DevBuf scratch[16];
-  DevBuf train_scratch[8];  // unfused training rows (learned_kernels.cu)  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
+  DevBuf train_scratch[10];  // [8]: bf16 W1^T shadow of the general tensor-core training path  // unfused training rows (learned_kernels.cu)  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
   HostBuf hscratch[4];
 
   int slot(int job_id) const {
@@ -303,6 +304,11 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
 // The CTA-pair evaluation kernel applies (C == 16, not disabled): pair lists
 // may then be cut into 256-row super tiles (pair_tiles = true).
 bool pair_supported(const ecco_ctx* ctx);
+// bf16 W1^T [slot][H][F] of the fp32 masters of `n` device slots.
+void shadow_w1t(ecco_ctx* ctx, const int* d_slots, int n, const float* wbase, size_t wstride,
+                uint16_t* w1t);
+// 2-D bf16 [rows][cols] tensor map, {64, box_rows} boxes, 128-byte swizzle.
+CUtensorMap tensor_map_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* d_mask,
                    double* d_out);
 bool train_supported(const ecco_ctx* ctx);

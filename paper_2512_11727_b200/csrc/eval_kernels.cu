@@ -791,6 +791,10 @@ uint32_t img_bytes(const ecco_config& g) {
   return (w2t_bytes(g) + 4u * (g.hidden_dim + g.num_classes) + 15u) & ~15u;
 }
 
+CUtensorMap tensor_map_bf16(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return make_map(base, rows, cols, box_rows);
+}
+
 bool pair_supported(const ecco_ctx* ctx) {
   return pair_enabled(ctx->cfg);
 }
@@ -816,6 +820,15 @@ void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstrid
   ECCO_LAUNCHED(ctx);
   k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_sl, wbase,
                                            wstride, sh.w2t, img_bytes(g));
+  ECCO_LAUNCHED(ctx);
+}
+
+void shadow_w1t(ecco_ctx* ctx, const int* d_slots, int n, const float* wbase, size_t wstride,
+                uint16_t* w1t) {
+  if (n == 0) return;
+  const ecco_config& g = ctx->cfg;
+  k_shadow_w1t<<<dim3(g.feat_dim / 32, g.hidden_dim / 32, n), dim3(32, 8), 0, ctx->stream>>>(
+      g.feat_dim, g.hidden_dim, d_slots, wbase, wstride, w1t, ctx->w1_t);
   ECCO_LAUNCHED(ctx);
 }
 

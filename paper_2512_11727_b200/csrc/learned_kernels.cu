@@ -712,8 +712,21 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
       }
       TcTile* d_tiles = (TcTile*)ctx->scratch[8].get(sizeof(TcTile) * tiles.size());
       ECCO_CUDA(ctx_memcpy(ctx, d_tiles, tiles.data(), sizeof(TcTile) * tiles.size(), cudaMemcpyHostToDevice, ctx->stream));
-      tc::fwd_hidden(ctx, ctx->d_eval, row_off, d_tiles, (int)tiles.size(), nullptr, 0, ctx->d_w,
-                     ctx->n_params, Z, (double)rows);
+      if (g.H % 256 == 0) {  // bf16 against a W1^T shadow of the evaluated models
+        std::vector<int> us(hslot);
+        std::sort(us.begin(), us.end());
+        us.erase(std::unique(us.begin(), us.end()), us.end());
+        int* d_us = ctx->upload(14, us.data(), us.size());  // scratch 14: this use only
+        uint16_t* w1t =
+            (uint16_t*)ctx->train_scratch[9].get((size_t)ctx->cfg.max_jobs * g.H * g.F * 2);
+        fused::shadow_w1t(ctx, d_us, (int)us.size(), ctx->d_w, ctx->n_params, w1t);
+        tc::fwd_hidden_bf16(ctx, ctx->d_eval, row_off, d_tiles, (int)tiles.size(), nullptr, 0,
+                            w1t, (size_t)ctx->cfg.max_jobs, ctx->d_w, ctx->n_params, Z,
+                            (double)rows);
+      } else {
+        tc::fwd_hidden(ctx, ctx->d_eval, row_off, d_tiles, (int)tiles.size(), nullptr, 0, ctx->d_w,
+                       ctx->n_params, Z, (double)rows);
+      }
     } else {
       ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_MATRIX, 2.0 * rows * g.F * g.H,
                  (double)rows * g.F * 2 + (double)g.F * g.H * 4,
@@ -928,6 +941,11 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   // tensor-core path: one 128-row tile (or the whole minibatch when B < 128)
   // per job and 128 rows
   const bool tc_math = ctx->cfg.math == ECCO_MATH_TC_TF32 && !ctx->fused_train;
+  // 128-row minibatches with H a multiple of 256 run the forward in bf16
+  // against a W1^T shadow the dW1 update keeps current (tc_kernels.cu)
+  const bool tc_bf16 = tc_math && g.B % 128 == 0 && g.H % 256 == 0;
+  uint16_t* w1t_train =
+      tc_bf16 ? (uint16_t*)ts[8].get((size_t)ctx->cfg.max_jobs * g.H * g.F * 2) : nullptr;
   std::vector<TcTile> tiles;
   TcTile* d_tiles = nullptr;
   if (tc_math) {
@@ -965,6 +983,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
       fused::train_chain(ctx, &ctx->sh_spec, n_jobs, d_slots, d_job_ids, d_steps, h_steps,
                          d_src_off, d_src_cam, d_src_frac, d_micro_base, t - 1, window, wt,
                          spec_stride, t - 1);
+    if (tc_bf16) fused::shadow_w1t(ctx, d_slots, n_jobs, wt, spec_stride, w1t_train);
     for (int step = 0; step < (ctx->fused_train ? 0 : max_steps); ++step) {
       const Gate gate{d_steps, step, g.B};
       int live = 0;
@@ -974,7 +993,10 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
           g, ctx->cfg.seed, n_jobs, d_job_ids, d_steps, d_src_off, d_src_cam, d_src_frac,
           d_micro_base, window, t - 1, step, ctx->d_labels, row_off, row_lab);
       ECCO_LAUNCHED(ctx);
-      if (tc_math) {
+      if (tc_bf16) {
+        tc::fwd_hidden_bf16(ctx, ctx->d_frames, row_off, d_tiles, (int)tiles.size(), d_steps, step,
+                            w1t_train, (size_t)ctx->cfg.max_jobs, wt, spec_stride, Z, lrows);
+      } else if (tc_math) {
         tc::fwd_hidden(ctx, ctx->d_frames, row_off, d_tiles, (int)tiles.size(), d_steps, step, wt,
                        spec_stride, Z, lrows);
       } else {
@@ -998,7 +1020,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
       ECCO_LAUNCHED(ctx);
       if (tc_math) {
         tc::dw1_update(ctx, ctx->d_frames, row_off, d_slots, d_steps, step, n_jobs, wt, spec_stride,
-                       DH, live);
+                       DH, live, w1t_train);
       } else {
         ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_DW1, 2.0 * lrows * g.F * g.H,
                    (double)live * (g.B * g.F * 2.0 + g.B * g.H * 4.0 + 2.0 * g.F * g.H * 4),

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "ctx.cuh"
+#include "sm100.cuh"
 #include "tc_kernels.cuh"
 
 namespace {
@@ -271,6 +272,7 @@ struct Dw1Args {
   const float* DH;
   int F, H, B, NT;
   float lr;
+  uint16_t* w1t;  // nullable: bf16 W1^T shadow [slot][H][F]
 };
 
 template <int NT>
@@ -362,12 +364,140 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
 #pragma unroll
     for (int r = 0; r < 32; ++r) wv[r] = wcol[(size_t)r * a.H];  // 32 loads in flight
 #pragma unroll
-    for (int r = 0; r < 32; ++r) wcol[(size_t)r * a.H] = fmaf(-a.lr, tr[lane * 33 + r], wv[r]);
+    for (int r = 0; r < 32; ++r) {
+      const float nw = fmaf(-a.lr, tr[lane * 33 + r], wv[r]);
+      wcol[(size_t)r * a.H] = nw;
+      tr[lane * 33 + r] = nw;  // (h = lane, f = r), for the shadow below
+    }
+    __syncwarp();
+    if (a.w1t) {  // shadow rows h, 32 consecutive features per warp: 64-byte stores
+      uint16_t* sh = a.w1t + (size_t)a.slots[j] * a.H * a.F + (size_t)(n0 + c0) * a.F + f0 +
+                     warp * 32 + lane;
+#pragma unroll 8
+      for (int h = 0; h < 32; ++h)
+        sh[(size_t)h * a.F] = (uint16_t)(sm100::pack_bf16x2(tr[h * 33 + lane], 0.0f) & 0xFFFF);
+    }
     __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, (uint32_t)NT);
+}
+
+// --------------------------------------------------------------------------
+// fwd, bf16: one CTA per (128-row training tile, 256 hidden columns).  A = X
+// rows gathered by cp.async into a 128B-swizzled K-major stage (bf16, exact),
+// B = the bf16 W1^T shadow by TMA ({64, 256} boxes), kind::f16 MMAs (M 128,
+// N 256, K 16) into TMEM, 4 stages of K = 64.
+constexpr int kBfNT = 256, kBfStages = 4;
+constexpr uint32_t kBfA = 128 * 128, kBfB = kBfNT * 128;  // bytes per stage
+
+struct FwdBfArgs {
+  const uint16_t* xbase;
+  const int64_t* row_off;
+  const TcTile* tiles;
+  const int* steps;
+  int step;
+  const float* wbase;  // b1 at + F*H
+  size_t wstride;
+  float* Z;
+  int F, H;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_tc_fwd_bf16(const __grid_constant__ CUtensorMap map_w, FwdBfArgs a) {
+  const TcTile tile = a.tiles[blockIdx.x];
+  if (a.steps && a.step >= a.steps[tile.job]) return;
+  const int n0 = blockIdx.y * kBfNT;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kBfStages * kBfA;
+  __shared__ uint64_t full[kBfStages], empty[kBfStages], done;
+  __shared__ uint32_t tmem_base;
+  __shared__ int64_t rows[kM];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  rows[tid] = tile.nrows > tid ? a.row_off[tile.row0 + tid] : a.row_off[tile.row0];
+  if (warp == 0) tmem_alloc(&tmem_base, (uint32_t)kBfNT);
+  if (tid == 0) {
+    if (sm100::smem_u32(smem) & 1023u) __trap();
+    for (int s = 0; s < kBfStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const int nk = a.F / 64;
+  const int brow = tile.slot * a.H + n0;  // first W1^T row of this CTA
+  // A gather: thread tid owns row tid, its 8 16-byte pieces of the chunk
+  auto load = [&](int kc) {
+    const int s = kc % kBfStages;
+    const uint32_t dst = sm100::smem_u32(sA + s * kBfA) + tid * 128;
+    const uint16_t* src = a.xbase + rows[tid] + kc * 64;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + ((c ^ (tid & 7)) << 4)),
+                   "l"(src + c * 8)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (tid == 0) {
+      sm100::mbar_expect_tx(&full[s], kBfB);
+      sm100::tma_load_2d(sB + s * kBfB, &map_w, kc * 64, brow, &full[s]);
+    }
+  };
+  for (int kc = 0; kc < kBfStages - 1 && kc < nk; ++kc) load(kc);
+  const uint32_t idf = sm100::idesc(kM, kBfNT, sm100::kFmtBF16);
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc % kBfStages;
+    const int nx = kc + kBfStages - 1;
+    if (nx < nk) {
+      if (nx >= kBfStages) mbar_wait(&empty[nx % kBfStages], ((nx / kBfStages) - 1) & 1);
+      load(nx);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kBfStages - 1) : "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(&full[s], (kc / kBfStages) & 1);
+      tc_fence_after();
+      const uint64_t da = sm100::desc_kmajor_sw128(sm100::smem_u32(sA + s * kBfA));
+      const uint64_t db = sm100::desc_kmajor_sw128(sm100::smem_u32(sB + s * kBfB));
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        sm100::mma_bf16_ss(tmem, da + kk * 2, db + kk * 2, idf, (kc | kk) != 0);
+      sm100::mma_commit(&empty[s]);
+      if (kc == nk - 1) sm100::mma_commit(&done);
+    }
+  }
+  mbar_wait(&done, 0);
+  tc_fence_after();
+  const int r = warp * 32 + lane;
+  const float* b1 = a.wbase + (size_t)tile.slot * a.wstride + (size_t)a.F * a.H;
+  for (int c0 = 0; c0 < kBfNT; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    if (r < tile.nrows) {
+      float* zr = a.Z + (size_t)(tile.row0 + r) * a.H + n0 + c0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        float4 o;
+        o.x = v[i] + b1[n0 + c0 + i];
+        o.y = v[i + 1] + b1[n0 + c0 + i + 1];
+        o.z = v[i + 2] + b1[n0 + c0 + i + 2];
+        o.w = v[i + 3] + b1[n0 + c0 + i + 3];
+        *reinterpret_cast<float4*>(zr + i) = o;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, (uint32_t)kBfNT);
 }
 
 int pick_nt(int H, int ctas_per_nt1) {
@@ -415,13 +545,35 @@ void fwd_hidden(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, co
   ECCO_LAUNCHED(ctx);
 }
 
+void fwd_hidden_bf16(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off,
+                     const TcTile* tiles, int n_tiles, const int* steps, int step,
+                     const uint16_t* w1t, size_t n_slots, const float* wbase, size_t wstride,
+                     float* Z, double live_rows) {
+  if (n_tiles == 0) return;
+  const int F = ctx->cfg.feat_dim, H = ctx->cfg.hidden_dim;
+  ECCO_REQUIRE(H % kBfNT == 0 && F % 64 == 0, "bf16 forward: H % 256 and F % 64");
+  const CUtensorMap map = fused::tensor_map_bf16(w1t, n_slots * H, F, kBfNT);
+  FwdBfArgs a{xbase, row_off, tiles, steps, step, wbase, wstride, Z, F, H};
+  const size_t sm = kBfStages * (size_t)(kBfA + kBfB);
+  static bool attr = false;
+  if (!attr) {
+    ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm));
+    attr = true;
+  }
+  const int kind = steps ? ECCO_KSTAT_TRAIN_STEP : ECCO_KSTAT_EVAL_MATRIX;
+  ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 2,
+             (k_tc_fwd_bf16<<<dim3(n_tiles, H / kBfNT), kThreads, sm, ctx->stream>>>(map, a)));
+  ECCO_LAUNCHED(ctx);
+}
+
 void dw1_update(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, const int* slots,
                 const int* steps, int step, int n_jobs, float* wbase, size_t wstride,
-                const float* DH, int live_jobs) {
+                const float* DH, int live_jobs, uint16_t* w1t) {
   if (n_jobs == 0) return;
   const int F = ctx->cfg.feat_dim, H = ctx->cfg.hidden_dim, B = ctx->cfg.minibatch;
   const int NT = pick_nt(H, n_jobs * (F / kM));
-  Dw1Args a{xbase, row_off, slots, steps, step, wbase, wstride, DH, F, H, B, NT, ctx->cfg.sgd_lr};
+  Dw1Args a{xbase, row_off, slots, steps, step, wbase, wstride, DH, F, H, B, NT, ctx->cfg.sgd_lr, w1t};
   const size_t sm = smem_bytes(NT);
   set_smem_attrs();
   ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_DW1, 2.0 * live_jobs * F * H * B,
