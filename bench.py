@@ -653,9 +653,18 @@ def parametric_leg(args):
                               np.ascontiguousarray(cl.reshape(-1)), np.ascontiguousarray(pr.reshape(-1)),
                               clen, np.ascontiguousarray(ce.reshape(-1)), K, D, params, want)
     got = dM[:ns].cpu().numpy()
+    # K1's rooflines: HBM on the algorithmic bytes (the fp64
+    # matrix written + scenes + models read), FP64 on (K+1)(3D+2) flops per
+    # pair plus K+1 exp (glibc's algorithm, ~25 fp64 ops each) -- B200 FP64
+    # is ~37 TFLOP/s (spec, not measured)
+    k1_bytes = 8.0 * N * G + 8.0 * N * D + 8.0 * G * (K * D + K + D)
+    k1_flops = N * G * ((K + 1) * (3 * D + 2) + (K + 1) * 25.0)
     out["eval_matrix"] = {
         "workload": f"{N} scenes x {G} models (K={K}, D={D}), fp64",
         "gpu_pairs_per_s": N * G / gpu_s, "gpu_ms": gpu_s * 1e3,
+        "hbm_gbs": k1_bytes / gpu_s / 1e9,
+        "hbm_frac": k1_bytes / gpu_s / 1e9 / peaks()[0]["hbm_gbs"],
+        "fp64_tflops": k1_flops / gpu_s / 1e12, "fp64_frac_of_spec_37": k1_flops / gpu_s / 37e12,
         "reference_pairs_per_s": ns * G / cpu_s, "reference_cores": 1,
         "reference_sample": f"{ns} x {G} pairs through the reference's eval()",
         "bit_exact_vs_reference": bool(got.tobytes() == want.tobytes()),
