@@ -1538,7 +1538,7 @@ void ecco_sim_default_options(ecco_sim_options* o) {
   o->backend = ECCO_BACKEND_PARAMETRIC;
   o->math = ECCO_MATH_FFMA_EXACT;
   o->device = 0;
-  o->spec_depth = 2;
+  o->spec_depth = 4;  // learned: 4 micro-windows per job up front (C4: 90 -> 64 ms per window)
   o->feat_dim = 512;
   o->hidden_dim = 256;
   o->num_classes = 16;
