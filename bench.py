@@ -11,7 +11,11 @@ synthetic camera streams ("Measurement"):
   retrain   every group's speculative micro-window chain: evaluate, then
             DEPTH x (STEPS SGD steps of B sampled frames, evaluate)
             (ecco_train_trajectories, the allocator's TrainingBackend probes of
-            gpu_allocator.cpp:125-135), then ecco_commit of the granted chain.
+            gpu_allocator.cpp:125-135); the chains' accuracy trajectories
+            all-gathered across ranks, the reference's greedy allocation
+            (WindowAllocation, ecco_allocate_trajectories) replayed over every
+            group on the host with W = DEPTH x G micro-windows, and
+            ecco_commit of each group's granted prefix.
 
 value = retrain samples of all ranks / max-over-ranks device time of the
 whole step (regroup included), in samples/s.  Groups are sharded across ranks
@@ -217,7 +221,6 @@ def run_b200(args, rank, world, local_rank):
     prep = ctx.prepare_trajectories(
         wl.local, [BATCH] * len(wl.local), [wl.members(g) for g in wl.local],
         [[1.0 / wl.per] * wl.per for _ in wl.local], [wl.members(g) for g in wl.local])
-    granted = [DEPTH] * len(wl.local)
     cams = np.arange(wl.N, dtype=np.int32)
     stream = torch.cuda.ExternalStream(ctx.stream)
     dev = torch.device("cuda", local_rank)
@@ -230,6 +233,20 @@ def run_b200(args, rank, world, local_rank):
     acc_host = np.zeros((len(wl.local), DEPTH + 1))
     ev = {k: torch.cuda.Event(enable_timing=True) for k in ("a", "b", "c")}
     phase = {"regroup": 0.0, "retrain": 0.0}
+
+    def gather_trajectories(acc):
+        """[gb, DEPTH+1] per rank -> [world*gb, DEPTH+1] (group-major)."""
+        blk = np.zeros((wl.gb, DEPTH + 1))
+        blk[:len(wl.local)] = acc
+        if dist is None:
+            return blk
+        t = torch.from_numpy(blk).to(_red_device())
+        out = torch.empty((world, wl.gb, DEPTH + 1), dtype=t.dtype, device=t.device)
+        if t.is_cuda:
+            dist.all_gather_into_tensor(out, t)
+        else:
+            dist.all_gather(list(out.unbind(0)), t)
+        return out.reshape(world * wl.gb, DEPTH + 1).cpu().numpy()
 
     def step(w, timed=False):
         with torch.cuda.stream(stream):
@@ -254,7 +271,18 @@ def run_b200(args, rank, world, local_rank):
                 ev["b"].record(stream)
             if wl.local:
                 ctx.train_prepared(prep, GPU_S, DEPTH, window=w, out=acc_host)
-                ctx.commit(wl.local, granted)
+            # the allocator's decisions over EVERY group: trajectories
+            # all-gathered (G x (DEPTH+1) fp64), the reference's greedy
+            # (WindowAllocation, gpu_allocator.cpp:100-181) replayed on the
+            # host with W = DEPTH x G micro-windows, each rank commits the
+            # granted prefixes of its own groups
+            traj = gather_trajectories(acc_host)
+            jobs, _, _, _ = ecco.allocate_trajectories(
+                np.arange(wl.G, dtype=np.int32), np.full(wl.G, wl.per, np.int32), traj[:wl.G],
+                1.0, 1.0, DEPTH * wl.G, GPU_S, 1, True, 0)
+            counts = np.bincount(jobs, minlength=wl.G)
+            if wl.local:
+                ctx.commit(wl.local, np.minimum(counts[wl.local], DEPTH).astype(np.int32))
             if timed:
                 ev["c"].record(stream)
                 ev["c"].synchronize()
@@ -399,7 +427,15 @@ def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
                     ctx.route_matrix_dev(wl.N, wl.gb, blocks.data_ptr(), best.data_ptr(),
                                          best_acc.data_ptr(), n_blocks=world)
                 ctx.train_prepared(prep, GPU_S, DEPTH, window=w, out=acc_host)
-                ctx.commit(wl.local, [DEPTH] * len(wl.local))
+                # the allocator replay over all groups (other ranks' rows as
+                # the all-gather would deliver them; here zeros)
+                traj = np.zeros((world * wl.gb, DEPTH + 1))
+                traj[:len(wl.local)] = acc_host
+                jobs, _, _, _ = ecco.allocate_trajectories(
+                    np.arange(wl.G, dtype=np.int32), np.full(wl.G, wl.per, np.int32),
+                    traj[:wl.G], 1.0, 1.0, DEPTH * wl.G, GPU_S, 1, True, 0)
+                counts = np.bincount(jobs, minlength=wl.G)
+                ctx.commit(wl.local, np.minimum(counts[wl.local], DEPTH).astype(np.int32))
 
         for w in range(2):
             step(w + 1)
