@@ -140,6 +140,26 @@ def test_uploaded_frames_equal_generated():
     assert fr.tobytes() == orc.frames.tobytes() and el.tobytes() == orc.eval_labels.tobytes()
 
 
+def test_staged_frame_range_and_swap():
+    """ecco_stage_frames_range (group-sharded ingest): the rings of a camera
+    range plus every eval set land in the back buffer and become current on
+    swap; rings outside the range keep the back buffer's previous contents."""
+    ctx, orc, rng = setup(seed=7)
+    import ctypes as C
+    fr = np.ascontiguousarray(orc.frames)
+    lb = np.ascontiguousarray(orc.labels)
+    ev = np.ascontiguousarray(orc.eval)
+    el = np.ascontiguousarray(orc.eval_labels)
+    first, n = 2, 3
+    ctx.stage_frames_range_host_ptr(first, n, fr[first].ctypes.data, lb[first].ctypes.data, 6,
+                                    ev.ctypes.data, el.ctypes.data)
+    ctx.swap_frames()
+    gf, gl, ge, gel = ctx.read_frames(6)
+    assert gf[first:first + n].tobytes() == fr[first:first + n].tobytes()
+    assert gl[first:first + n].tobytes() == lb[first:first + n].tobytes()
+    assert ge.tobytes() == ev.tobytes() and gel.tobytes() == el.tobytes()
+
+
 def test_learned_simulation_runs_and_groups():
     from paper_2512_11727_b200 import scenarios
     sc = scenarios.synthetic(24, 3, windows=2, micro_windows=8, drift_frac=0.1, local_acc=0.0, seed=3)
