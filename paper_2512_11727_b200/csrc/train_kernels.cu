@@ -8,8 +8,7 @@
 // Cluster of H/64 CTAs; CTA r owns hidden units [64r, 64r+64):
 //   TMEM     fp32 master slice W1[:, 64r:64r+64] (F/128 tiles of 128 lanes x
 //            64 columns), the forward / dH accumulators (128 x 64), the
-//            partial logits (128 x 16), dW2 (64 x 16) and dW1 (up to two
-//            128 x 64 tiles per pass)
+//            partial logits (128 x 16) and dW2 (64 x 16)
 //   smem     X tile (128 sampled rows, bf16, 128B-swizzled K-major; also read
 //            MN-major as X^T), the bf16 W1 operand built from the master, the
 //            bf16 W2 slice image, R / dH / dL operands, fp32 W2/b1 slices, b2
@@ -18,15 +17,16 @@
 //            row block by st.async over DSMEM -> owner (4 threads per row)
 //            sums the partials in fixed order, softmax, dL, broadcasts dL
 //            rows -> dL.W2^T and dW2 = R^T.dL (tcgen05) -> dH =
-//            (dL.W2^T)*(Z>0) -> dW1 = X^T.dH and db1 = dH^T.1 (tcgen05, in
-//            two passes at F = 512) -> master update in TMEM, bf16 operands
-//            rewritten; the next step's rows are prefetched to L2 while dL is
-//            in flight and gathered (cp.async) into each X chunk as soon as
-//            the dW1 pass reading it completes
+//            (dL.W2^T)*(Z>0) -> the master ACCUMULATES X^T.(-lr dH) on the
+//            tensor core (D += A.B into the TMEM master, one commit per
+//            128-feature tile) and -lr db1 = (-lr dH)^T.1 -> bf16 W1 operand
+//            rows rebuilt from each finished tile; the next step's rows are
+//            prefetched to L2 while dL is in flight and gathered (cp.async)
+//            into each X chunk as soon as the tile reading it completes
 //
 // Numerics: X exact (bf16 frames); every tensor-core operand bf16 (W1, R,
-// W2, dL, dH), fp32 accumulation, fp32 masters; bias adds, softmax, dL and
-// db2 fp32 on CUDA cores.  Tolerance in tests/test_gpu_learned.py.
+// W2, dL, -lr dH), fp32 accumulation, fp32 masters (W1 += X^T.bf16(-lr dH)
+// in the accumulator); bias adds, softmax, dL and db2 fp32 on CUDA cores.  Tolerance in tests/test_gpu_learned.py.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -121,20 +121,16 @@ __host__ __device__ inline Layout layout(int F) {
   o += kB * 4u;
   o = (o + 7u) & ~7u;
   L.bars = o;
-  o += 8u * 8u;
+  o += 12u * 8u;
   L.tmem = o;
   o += 16u;
   L.total = o;
   return L;
 }
 
-// TMEM columns: master [0, 64*NM), Z / dL.W2^T [A, A+64), partial logits
-// [A+64, A+80), dW2 [A+80, A+96) with A = 64*NM, dW1 tiles from A+128.
-__host__ __device__ inline int dw1_tiles_per_pass(int F) {
-  const int nm = F / 128;
-  return std::min(2, std::min(nm, (512 - (nm * 64 + 128)) / 64));
-}
-
+// TMEM columns: master [0, 64*NM) (the dW1 MMAs accumulate into it), Z /
+// dL.W2^T [A, A+64), partial logits / -lr db1 [A+64, A+80), dW2 [A+80, A+96)
+// with A = 64*NM.
 __host__ __device__ inline uint32_t tmem_cols(int) { return 512; }
 
 // Remote (or own) shared-memory store whose bytes complete_tx on the
@@ -245,11 +241,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* zfull = (uint64_t*)(smem + L.bars);
   uint64_t* plfull = zfull + 1;
   uint64_t* dhfull = zfull + 2;  // dL.W2^T and dW2 accumulated
-  uint64_t* gfull = zfull + 3;   // one dW1 pass accumulated
-  uint64_t* gfree = zfull + 4;   // every warp has read the pass's dW1 tiles
   uint64_t* recv_full = zfull + 5;  // owner rows' partial logits arrived (st.async)
   uint64_t* dl_full = zfull + 6;    // every dL row (and, on rank 0, every loss) arrived
   uint64_t* w2full = zfull + 7;     // dW2 accumulated
+  uint64_t* gt = zfull + 8;         // [NM] dW1 tile mt accumulated into the master
   uint32_t* sTmem = (uint32_t*)(smem + L.tmem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -258,11 +253,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane_base = (uint32_t)(q * 32) << 16;
   const int RP = kB / cs;       // rows owned per CTA for the softmax
   const int NM = F / 128;       // master / dW1 tiles
-  const int GT = dw1_tiles_per_pass(F);
-  const int NP = (NM + GT - 1) / GT;  // dW1 passes per step
   const int nkc = F / 64;
   const uint32_t acol = (uint32_t)NM * 64u;  // Z / dL.W2^T
-  const uint32_t plcol = acol + 64u, w2col = acol + 80u, gcol = acol + 128u;
+  const uint32_t plcol = acol + 64u, w2col = acol + 80u;
   const int slot = a.slots[j];
   float* W1 = a.wbase + (size_t)slot * a.wstride;
   float* b1 = W1 + (size_t)F * H;
@@ -318,8 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(zfull, 1);
     mbar_init(plfull, 1);
     mbar_init(dhfull, 1);
-    mbar_init(gfull, 1);
-    mbar_init(gfree, kThreads / 32);
+    for (int mt = 0; mt < NM; ++mt) mbar_init(gt + mt, 1);
     mbar_init(recv_full, 1);
     mbar_init(dl_full, 1);
     mbar_init(w2full, 1);
@@ -375,7 +367,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     desc_mnmajor_sw128(smem_u32(sSC) + (kc * 4 + kk) * 2048, 16384, 1024), idf,
                     (kc | kk) != 0);
   };
-  uint32_t gph = 0, fph = 0;  // gfull / gfree phases completed
 
   for (int step = 0; step < nsteps; ++step) {
     const int cur = step & 1;
@@ -539,116 +530,79 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32_nowait(tmem + lane_base + acol + p * 32, dh);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) dh[i] = (mask >> i) & 1u ? dh[i] : 0u;
-      put_row32(sDH, s, p, dh);  // MN-major over rows: dW1's B operand
+      for (int i = 0; i < 32; ++i)
+        dh[i] = (mask >> i) & 1u ? __float_as_uint(__fmul_rn(-lr, __uint_as_float(dh[i]))) : 0u;
+      put_row32(sDH, s, p, dh);  // -lr dH, MN-major over rows: dW1's B operand
     }
     fence_async_smem();  // dH (generic stores) -> tensor-core reads
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
 
-    // ------------------------ dW1 = X^T . dH in passes, master update (TMEM) --
-    for (int pass = 0; pass < NP; ++pass) {
-      const int mt0 = pass * GT, mt1 = std::min(NM, mt0 + GT);
-      if (warp == 0) {
-        if (pass > 0) {
-          mbar_wait(gfree, fph & 1u);  // previous pass's tiles read by every warp
-          ++fph;
-          tc_fence_after();
-        }
-        if (elect_one()) {
-          for (int mt = mt0; mt < mt1; ++mt)
+    // ---------- dW1: the master accumulates X^T . (-lr dH) on the tensor core --
+    // one commit per 128-feature tile: its bf16 operand rows are rebuilt and
+    // the next rows' X chunks gathered while the later tiles' MMAs run
+    if (warp == 0) {
+      if (elect_one()) {
+        for (int mt = 0; mt < NM; ++mt) {
 #pragma unroll
-            for (int k16 = 0; k16 < kB / 16; ++k16)
-              mma_bf16_ss(tmem + gcol + (mt - mt0) * 64,
-                          desc_mnmajor_sw128(smem_u32(sX) + (2 * mt) * 16384 + k16 * 2048, 16384, 1024),
-                          desc_mnmajor_sw128(smem_u32(sDH) + k16 * 2048, 16384, 1024), idg, k16 != 0);
-          if (pass == NP - 1)  // db1 into the (consumed) partial-logit columns
+          for (int k16 = 0; k16 < kB / 16; ++k16)
+            mma_bf16_ss(tmem + mt * 64,
+                        desc_mnmajor_sw128(smem_u32(sX) + (2 * mt) * 16384 + k16 * 2048, 16384, 1024),
+                        desc_mnmajor_sw128(smem_u32(sDH) + k16 * 2048, 16384, 1024), idg, 1);
+          if (mt == NM - 1)  // -lr db1 into the (consumed) partial-logit columns
 #pragma unroll
             for (int k16 = 0; k16 < kB / 16; ++k16)
               mma_bf16_ss(tmem + plcol, desc_mnmajor_sw128(smem_u32(sDH) + k16 * 2048, 0, 1024),
                           smem_desc(smem_u32(sOnes) + k16 * 512, 256, 256, kSwizzle32B), idb,
                           k16 != 0);
-          mma_commit(gfull);
-        }
-        __syncwarp();
-      }
-      if (pass == 0 && p == 0 && q < 2) {  // dW2 row h = s (TMEM lanes 0-63)
-        mbar_wait(w2full, ph);
-        tc_fence_after();
-        uint32_t w2r[kC];
-        tmem_ld16_nowait(tmem + lane_base + w2col, w2r);
-        tmem_ld_wait();
-        float4* w = reinterpret_cast<float4*>(sW2 + s * kC);
-#pragma unroll
-        for (int c4 = 0; c4 < kC / 4; ++c4) {
-          const float4 o = w[c4];
-          w[c4] = make_float4(__fmaf_rn(-lr, __uint_as_float(w2r[4 * c4]), o.x),
-                              __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 1]), o.y),
-                              __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 2]), o.z),
-                              __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 3]), o.w));
+          mma_commit(gt + mt);
         }
       }
-      mbar_wait(gfull, gph & 1u);
-      tc_fence_after();
-      if (pass == NP - 1 && p == 1 && q < 2) {  // db1 row h = s (TMEM lanes 0-63)
-        uint32_t v[8];
-        tmem_ld8_nowait(tmem + lane_base + plcol, v);
-        tmem_ld_wait();
-        sB1[s] = __fmaf_rn(-lr, __uint_as_float(v[0]), sB1[s]);
-      }
-      const bool last = pass == NP - 1;
-      // this pass's X chunks are read: release them to the cluster (warp 1
-      // gathers the next rows' features there once every CTA has, below)
-      // this pass's X chunks are read: the next rows' features there (all
-      // threads on the last pass; after the update, without warp 0, otherwise)
-      if (more && last) gather(cur ^ 1, mt0 * 16, (mt1 - mt0) * 16, 0);
-      if (NP == 1) db2_partial();
-      if (last) {
-        __syncthreads();  // dH / R / sW2 readers done, db2 partials written
-        build_w2i();
-        if (tid >= 32 && tid < 32 + kC) {
-          const int c = tid - 32;
-          float acc = sB2p[c];
-#pragma unroll
-          for (int b = 1; b < 8; ++b) acc = __fadd_rn(acc, sB2p[b * kC + c]);
-          sB2[c] = __fmaf_rn(-lr, acc, sB2[c]);
-        }
-      }
-      // master update; on a gating pass the dW1 tiles are read first and the
-      // next pass released before the arithmetic
-      uint32_t g0[32], g1[32];
-      tmem_ld32_nowait(tmem + lane_base + gcol + p * 32, g0);
-      if (mt1 - mt0 > 1) tmem_ld32_nowait(tmem + lane_base + gcol + 64 + p * 32, g1);
-      tmem_ld_wait();
-      if (!last) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(gfree);
-      }
-      for (int mt = mt0; mt < mt1; ++mt) {
-        uint32_t wr[32];
-        tmem_ld32_nowait(tmem + lane_base + mt * 64 + p * 32, wr);
-        tmem_ld_wait();
-        if (mt == mt0) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            wr[i] = __float_as_uint(__fmaf_rn(-lr, __uint_as_float(g0[i]), __uint_as_float(wr[i])));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            wr[i] = __float_as_uint(__fmaf_rn(-lr, __uint_as_float(g1[i]), __uint_as_float(wr[i])));
-        }
-        tmem_st32(tmem + lane_base + mt * 64 + p * 32, wr);
-        put_row32(sSC, mt * 128 + s, p, wr);
-      }
-      if (!last) {
-        if (more && warp > 0) gather(cur ^ 1, mt0 * 16, (mt1 - mt0) * 16, 32);
-        if (pass == 0) db2_partial();
-      }
-      ++gph;
+      __syncwarp();
     }
-    tmem_st_wait();
+    if (p == 0 && q < 2) {  // dW2 row h = s (TMEM lanes 0-63)
+      mbar_wait(w2full, ph);
+      tc_fence_after();
+      uint32_t w2r[kC];
+      tmem_ld16_nowait(tmem + lane_base + w2col, w2r);
+      tmem_ld_wait();
+      float4* w = reinterpret_cast<float4*>(sW2 + s * kC);
+#pragma unroll
+      for (int c4 = 0; c4 < kC / 4; ++c4) {
+        const float4 o = w[c4];
+        w[c4] = make_float4(__fmaf_rn(-lr, __uint_as_float(w2r[4 * c4]), o.x),
+                            __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 1]), o.y),
+                            __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 2]), o.z),
+                            __fmaf_rn(-lr, __uint_as_float(w2r[4 * c4 + 3]), o.w));
+      }
+    }
+    // (tile 2's rows overwrite R, tile 3's dH: both read by MMAs its commit covers)
+    for (int mt = 0; mt < NM; ++mt) {
+      mbar_wait(gt + mt, ph);
+      tc_fence_after();
+      uint32_t wr[32];
+      tmem_ld32_nowait(tmem + lane_base + mt * 64 + p * 32, wr);
+      tmem_ld_wait();
+      put_row32(sSC, mt * 128 + s, p, wr);
+      if (more) gather(cur ^ 1, mt * 16, 16, 0);  // this tile's X chunks are read
+    }
+    if (p == 1 && q < 2) {  // db1 row h = s (TMEM lanes 0-63), already scaled by -lr
+      uint32_t v[8];
+      tmem_ld8_nowait(tmem + lane_base + plcol, v);
+      tmem_ld_wait();
+      sB1[s] = __fadd_rn(sB1[s], __uint_as_float(v[0]));
+    }
+    db2_partial();
+    __syncthreads();  // sW2 updated, db2 partials written
+    build_w2i();
+    if (tid >= 32 && tid < 32 + kC) {
+      const int c = tid - 32;
+      float acc = sB2p[c];
+#pragma unroll
+      for (int b = 1; b < 8; ++b) acc = __fadd_rn(acc, sB2p[b * kC + c]);
+      sB2[c] = __fmaf_rn(-lr, acc, sB2[c]);
+    }
     cp_async_wait_all();
     fence_async_smem();  // X rows, W1 / W2 operands -> next step's MMAs
     tc_fence_before();

@@ -179,8 +179,9 @@ def test_learned_simulation_runs_and_groups():
 # five contractions run tcgen05 kind::f16 with bf16 operands and fp32
 # accumulation: Z = X.W1 (X exact, W1 the bf16 image of the fp32 master),
 # logits = R.W2, dL.W2^T, dW2 = R^T.dL and dW1 = X^T.dH, with R = relu(Z+b1),
-# W2, dL and dH rounded to bf16 where they enter; bias adds, softmax, dL, db2
-# and the masters are fp32, db1 the fp32 sum of the bf16 dH.  Two checks:
+# W2, dL and -lr dH rounded to bf16 where they enter (the W1 master
+# accumulates X^T.bf16(-lr dH) in the MMA accumulator); bias adds, softmax,
+# dL, db2 and the masters are fp32, db1 the fp32 sum of bf16(-lr dH).  Two checks:
 #  * against a float64 restatement of the SGD step that applies exactly that
 #    rounding (_step_emulated below): agreement to 1e-3 of the update proves
 #    the layouts, descriptors and epilogues (a layout error is O(1));
@@ -201,7 +202,7 @@ def _bf16(a):
 
 def _step_emulated(x, y, w, lr):
     """One SGD step (orc_sgd_step's math) in float64 with the tensor-core
-    operands rounded to bf16 as the fused chain feeds them: W1, R, W2, dL, dH."""
+    operands rounded to bf16 as the fused chain feeds them: W1, R, W2, dL, -lr dH."""
     w1, b1, w2, b2 = [np.asarray(t, np.float64) for t in w]
     B, F = x.shape
     H, Cc = b1.size, b2.size
@@ -217,8 +218,8 @@ def _step_emulated(x, y, w, lr):
     DL = P / B
     DLb = _bf16(DL.astype(np.float32))
     DH = (DLb @ W2b.T) * (Z > 0)
-    DHb = _bf16(DH.astype(np.float32))
-    return [W1 - lr * (X.T @ DHb), b1 - lr * DHb.sum(0), W2 - lr * (Rb.T @ DLb),
+    DHs = _bf16(np.float32(-lr) * DH.astype(np.float32))  # the operand: bf16(-lr dH)
+    return [W1 + X.T @ DHs, b1 + DHs.sum(0), W2 - lr * (Rb.T @ DLb),
             b2 - lr * DL.sum(0)]
 
 

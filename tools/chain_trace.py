@@ -21,15 +21,16 @@ PROBES = [
     ("    mbar_wait(zfull, ph);\n    tc_fence_after();\n", "    TS(1, 0)\n"),
     ("    mbar_wait(plfull, ph);\n    tc_fence_after();\n", "    TS(2, 0)\n"),
     ("      mbar_wait(recv_full, ph);\n", "      TS(3, 128)\n"),
-    ("      TS(13, 128)\n", None),
     ("    mbar_wait(dl_full, ph);\n", "    TS(4, 0)\n"),
     ("    mbar_wait(dhfull, ph);\n    tc_fence_after();\n", "    TS(5, 0)\n"),
-    ("    // ------------------------ dW1 = X^T . dH in passes, master update (TMEM) --\n",
+    ("    // ---------- dW1: the master accumulates X^T . (-lr dH) on the tensor core --\n",
      "    TS(6, 0)\n"),
-    ("      mbar_wait(gfull, gph & 1u);\n      tc_fence_after();\n", "      TS(7 + 2 * pass, 0)\n"),
-    ("        build_w2i();\n", "        TS(12, 0)\n"),
-    ("      if (!last) {\n        tc_fence_before();\n", None),
-    ("    tmem_st_wait();\n", "    TS(13, 0)\n"),
+    ("      mbar_wait(gt + mt, ph);\n      tc_fence_after();\n", "      TS(7 + mt, 0)\n"),
+    ("    __syncthreads();  // sW2 updated, db2 partials written\n", "    TS(11, 0)\n"),
+    ("    cp_async_wait_all();\n    fence_async_smem();  // X rows, W1 / W2 operands -> next step's MMAs\n",
+     "    TS(12, 0)\n"),
+    ("    TS(12, 0)\n    tc_fence_before();\n    __syncthreads();\n    tc_fence_after();\n",
+     "    TS(13, 0)\n"),
 ]
 
 HOST = '''  if (getenv("ECCO_CHAIN_TRACE")) {
