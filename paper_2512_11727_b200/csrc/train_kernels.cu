@@ -561,7 +561,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     }
-    if (p == 0 && q < 2) {  // dW2 row h = s (TMEM lanes 0-63)
+    // warp 0 is held by the MMA queue until the dW1 MMAs drain: the other
+    // warps take its share (warp 4 both column halves of lane quadrant 0)
+    if (p == 1 && q < 2) {  // dW2 row h = s (TMEM lanes 0-63)
       mbar_wait(w2full, ph);
       tc_fence_after();
       uint32_t w2r[kC];
@@ -578,14 +580,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     // (tile 2's rows overwrite R, tile 3's dH: both read by MMAs its commit covers)
-    for (int mt = 0; mt < NM; ++mt) {
-      mbar_wait(gt + mt, ph);
-      tc_fence_after();
-      uint32_t wr[32];
-      tmem_ld32_nowait(tmem + lane_base + mt * 64 + p * 32, wr);
-      tmem_ld_wait();
-      put_row32(sSC, mt * 128 + s, p, wr);
-      if (more) gather(cur ^ 1, mt * 16, 16, 0);  // this tile's X chunks are read
+    if (warp > 0) {
+      for (int mt = 0; mt < NM; ++mt) {
+        mbar_wait(gt + mt, ph);
+        tc_fence_after();
+        uint32_t wr[32];
+        tmem_ld32_nowait(tmem + lane_base + mt * 64 + p * 32, wr);
+        if (warp == 4) {
+          uint32_t w0[32];
+          tmem_ld32_nowait(tmem + lane_base + mt * 64, w0);
+          tmem_ld_wait();
+          put_row32(sSC, mt * 128 + s, 0, w0);
+        } else {
+          tmem_ld_wait();
+        }
+        put_row32(sSC, mt * 128 + s, p, wr);
+        if (more) gather(cur ^ 1, mt * 16, 16, 32);  // this tile's X chunks are read
+      }
     }
     if (p == 1 && q < 2) {  // db1 row h = s (TMEM lanes 0-63), already scaled by -lr
       uint32_t v[8];

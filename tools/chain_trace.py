@@ -1,8 +1,8 @@
 """Per-phase clock64 trace of the fused SGD chain (k_train_chain), for tuning.
 
   python tools/chain_trace.py on    # instrument paper_2512_11727_b200/csrc/train_kernels.cu
-  (build, then on the GPU box: ECCO_CHAIN_TRACE=1 python bench.py --steps 1 --warmup 1 ...
-   prints "chain step s: k:cycles ..." for steps 0-3 of CTA 0, relative to the step start)
+  (build, then on the GPU box: ECCO_CHAIN_TRACE=<block> python bench.py --steps 1 --warmup 1 ...
+   prints "chain step s: k:cycles ..." for steps 0-3 of CTA <block>, relative to the step start)
   python tools/chain_trace.py off   # restore the saved clean source
 
 Each probe is `TS(k, tid)`: thread `tid` of CTA 0 records clock64() at point k."""
@@ -25,7 +25,8 @@ PROBES = [
     ("    mbar_wait(dhfull, ph);\n    tc_fence_after();\n", "    TS(5, 0)\n"),
     ("    // ---------- dW1: the master accumulates X^T . (-lr dH) on the tensor core --\n",
      "    TS(6, 0)\n"),
-    ("      mbar_wait(gt + mt, ph);\n      tc_fence_after();\n", "      TS(7 + mt, 0)\n"),
+    ("          mma_commit(gt + mt);\n        }\n      }\n      __syncwarp();\n    }\n", "    TS(14, 0)\n"),
+    ("        mbar_wait(gt + mt, ph);\n        tc_fence_after();\n", "        TS(7 + mt, 32)\n"),
     ("    __syncthreads();  // sW2 updated, db2 partials written\n", "    TS(11, 0)\n"),
     ("    cp_async_wait_all();\n    fence_async_smem();  // X rows, W1 / W2 operands -> next step's MMAs\n",
      "    TS(12, 0)\n"),
@@ -38,6 +39,7 @@ HOST = '''  if (getenv("ECCO_CHAIN_TRACE")) {
     if (!dbg) cudaMalloc(&dbg, 64 * 8);
     cudaMemsetAsync(dbg, 0, 64 * 8, ctx->stream);
     a.dbg = dbg;
+    a.dbg_block = atoi(getenv("ECCO_CHAIN_TRACE"));
   }
 '''
 HOST_AFTER = '''  if (a.dbg) {
@@ -58,9 +60,9 @@ def on():
     s = open(SRC).read()
     src0 = s
     s = s.replace("#include <vector>\n", "#include <vector>\n#include <cstdio>\n#include <cstdlib>\n", 1)
-    s = s.replace("  int loss_T, loss_t;\n};", "  int loss_T, loss_t;\n  long long* dbg;\n};", 1)
+    s = s.replace("  int loss_T, loss_t;\n};", "  int loss_T, loss_t;\n  long long* dbg;\n  int dbg_block;\n};", 1)
     s = s.replace("__global__ void __launch_bounds__(kThreads, 1)\n    k_train_chain(",
-                  "#define TS(k, t) if (a.dbg && blockIdx.x == 0 && tid == (t) && step < 4) "
+                  "#define TS(k, t) if (a.dbg && blockIdx.x == a.dbg_block && tid == (t) && step < 4) "
                   "a.dbg[step * 16 + (k)] = clock64();\n"
                   "__global__ void __launch_bounds__(kThreads, 1)\n    k_train_chain(", 1)
     for anchor, probe in PROBES:
