@@ -34,16 +34,33 @@ PROBES = [
      "    TS(13, 0)\n"),
 ]
 
+# globaltimer stamps of CTA <block>'s thread 0: entry, after setup, after the
+# step loop, after the write-back (dbg[64..67])
+PHASES = [
+    "  if (nsteps <= 0) return;  // the whole cluster (same job) leaves\n",
+    "  cluster_sync();  // every CTA of the cluster is running before any DSMEM traffic\n",
+    None,  # before the write-back banner
+    "  if (warp == 0) tmem_dealloc(tmem, tmem_cols(F));\n",
+]
+WB = "  // ------------------------------------------------------------ write back --\n"
+
+
+def _stamp(k):
+    return ("  { if (a.dbg && blockIdx.x == a.dbg_block && threadIdx.x == 0) { unsigned long long t_; "
+            "asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(t_)); a.dbg[64 + K] = (long long)t_; } }\n"
+            ).replace("64 + K", "64 + %d" % k)
+
+
 HOST = '''  if (getenv("ECCO_CHAIN_TRACE")) {
     static long long* dbg = nullptr;
-    if (!dbg) cudaMalloc(&dbg, 64 * 8);
-    cudaMemsetAsync(dbg, 0, 64 * 8, ctx->stream);
+    if (!dbg) cudaMalloc(&dbg, 72 * 8);
+    cudaMemsetAsync(dbg, 0, 72 * 8, ctx->stream);
     a.dbg = dbg;
     a.dbg_block = atoi(getenv("ECCO_CHAIN_TRACE"));
   }
 '''
 HOST_AFTER = '''  if (a.dbg) {
-    long long h[64];
+    long long h[72];
     cudaStreamSynchronize(ctx->stream);
     cudaMemcpy(h, a.dbg, sizeof(h), cudaMemcpyDeviceToHost);
     for (int st = 0; st < 4; ++st) {
@@ -52,6 +69,8 @@ HOST_AFTER = '''  if (a.dbg) {
         if (h[st * 16 + k]) fprintf(stderr, " %d:%lld", k, h[st * 16 + k] - h[st * 16]);
       fprintf(stderr, "\\n");
     }
+    fprintf(stderr, "chain block %d: setup %lld ns, steps %lld ns, writeback %lld ns\\n", a.dbg_block,
+            h[65] - h[64], h[66] - h[65], h[67] - h[66]);
   }
 '''
 
@@ -70,6 +89,13 @@ def on():
             continue
         assert anchor in s, anchor
         s = s.replace(anchor, anchor + probe)
+    for k, anchor in enumerate(PHASES):
+        if anchor is None:
+            assert WB in s
+            s = s.replace(WB, _stamp(k) + WB, 1)
+        else:
+            assert anchor in s, anchor
+            s = s.replace(anchor, anchor + _stamp(k), 1)
     s = s.replace("  const uint32_t smem = layout(c.feat_dim).total;\n",
                   HOST + "  const uint32_t smem = layout(c.feat_dim).total;\n", 1)
     i = s.rindex("  ECCO_LAUNCHED(ctx);\n}")
