@@ -79,7 +79,7 @@ def on():
     s = open(SRC).read()
     src0 = s
     s = s.replace("#include <vector>\n", "#include <vector>\n#include <cstdio>\n#include <cstdlib>\n", 1)
-    s = s.replace("  int loss_T, loss_t;\n};", "  int loss_T, loss_t;\n  long long* dbg;\n  int dbg_block;\n};", 1)
+    s = s.replace("  int loss_T, loss_t;\n", "  int loss_T, loss_t;\n  long long* dbg;\n  int dbg_block;\n", 1)
     s = s.replace("__global__ void __launch_bounds__(kThreads, 1)\n    k_train_chain(",
                   "#define TS(k, t) if (a.dbg && blockIdx.x == a.dbg_block && tid == (t) && step < 4) "
                   "a.dbg[step * 16 + (k)] = clock64();\n"
