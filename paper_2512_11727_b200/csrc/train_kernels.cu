@@ -121,7 +121,7 @@ __host__ __device__ inline Layout layout(int F) {
   o += kB * 4u;
   o = (o + 7u) & ~7u;
   L.bars = o;
-  o += 12u * 8u;
+  o += 16u * 8u;
   L.tmem = o;
   o += 16u;
   L.total = o;
@@ -187,6 +187,11 @@ __device__ __forceinline__ float expf_nb(float x) {
 __device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -245,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dl_full = zfull + 6;    // every dL row (and, on rank 0, every loss) arrived
   uint64_t* w2full = zfull + 7;     // dW2 accumulated
   uint64_t* gt = zfull + 8;         // [NM] dW1 tile mt accumulated into the master
+  uint64_t* xready = zfull + 12;    // [NM] tile mt's W1 operand rows and next X chunks in smem
   uint32_t* sTmem = (uint32_t*)(smem + L.tmem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -311,7 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(zfull, 1);
     mbar_init(plfull, 1);
     mbar_init(dhfull, 1);
-    for (int mt = 0; mt < NM; ++mt) mbar_init(gt + mt, 1);
+    for (int mt = 0; mt < NM; ++mt) {
+      mbar_init(gt + mt, 1);
+      mbar_init(xready + mt, kThreads - 32);
+    }
     mbar_init(recv_full, 1);
     mbar_init(dl_full, 1);
     mbar_init(w2full, 1);
@@ -377,9 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_expect_tx(dl_full, dl_bytes);
     }
     // ------------------------------------------------------ forward MMA --
-    // (with two dW1 passes the first feature half was issued at the end of
-    // the previous step; the rest waits for the last gathered rows)
-    if (warp == 0) {
+    // (steps after the first: issued tile by tile at the end of the
+    // previous step, as the W1 operand rows and the gathered rows land)
+    if (step == 0 && warp == 0) {
       if (elect_one()) {
         issue_fwd(0, nkc);
         mma_commit(zfull);
@@ -580,6 +589,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     // (tile 2's rows overwrite R, tile 3's dH: both read by MMAs its commit covers)
+    // Tile mt's operand rows and next X chunks are published on xready[mt]
+    // (each thread: its copies of the tile complete -> proxy fence ->
+    // arrive, one tile behind the issue); warp 0 issues the next step's
+    // forward chunks 2mt, 2mt+1 as each tile is published.
     if (warp > 0) {
       for (int mt = 0; mt < NM; ++mt) {
         mbar_wait(gt + mt, ph);
@@ -595,7 +608,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
         }
         put_row32(sSC, mt * 128 + s, p, wr);
-        if (more) gather(cur ^ 1, mt * 16, 16, 32);  // this tile's X chunks are read
+        if (more) {
+          gather(cur ^ 1, mt * 16, 16, 32);  // this tile's X chunks are read
+          cp_async_commit();
+          if (mt > 0) {
+            cp_async_wait_group<1>();
+            fence_async_smem();
+            mbar_arrive(xready + mt - 1);
+          }
+        }
+      }
+      if (more) {
+        cp_async_wait_group<0>();
+        fence_async_smem();
+        mbar_arrive(xready + NM - 1);
+      }
+    } else if (more) {
+      for (int mt = 0; mt < NM; ++mt) {
+        mbar_wait(xready + mt, ph);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_fwd(2 * mt, 2 * mt + 2);
+          if (mt == NM - 1) mma_commit(zfull);
+        }
+        __syncwarp();
       }
     }
     if (p == 1 && q < 2) {  // db1 row h = s (TMEM lanes 0-63), already scaled by -lr
@@ -614,8 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int b = 1; b < 8; ++b) acc = __fadd_rn(acc, sB2p[b * kC + c]);
       sB2[c] = __fmaf_rn(-lr, acc, sB2[c]);
     }
-    cp_async_wait_all();
-    fence_async_smem();  // X rows, W1 / W2 operands -> next step's MMAs
+    fence_async_smem();  // the W2 operand -> next step's MMAs
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
