@@ -27,11 +27,11 @@ PROBES = [
      "    TS(6, 0)\n"),
     ("          mma_commit(gt + mt);\n        }\n      }\n      __syncwarp();\n    }\n", "    TS(14, 0)\n"),
     ("        mbar_wait(gt + mt, ph);\n        tc_fence_after();\n", "        TS(7 + mt, 32)\n"),
-    ("    __syncthreads();  // sW2 updated, db2 partials written\n", "    TS(11, 0)\n"),
-    ("    cp_async_wait_all();\n    fence_async_smem();  // X rows, W1 / W2 operands -> next step's MMAs\n",
-     "    TS(12, 0)\n"),
-    ("    TS(12, 0)\n    tc_fence_before();\n    __syncthreads();\n    tc_fence_after();\n",
-     "    TS(13, 0)\n"),
+    ("        mbar_wait(xready + mt, ph);\n        tc_fence_after();\n",
+     "        if (mt == 0) { TS(11, 0) }\n        if (mt == NM - 1) { TS(12, 0) }\n"),
+    ("    __syncthreads();  // sW2 updated, db2 partials written\n", "    TS(15, 0)\n"),
+    ("    fence_async_smem();  // the W2 operand -> next step's MMAs\n    tc_fence_before();\n"
+     "    __syncthreads();\n    tc_fence_after();\n", "    TS(13, 0)\n"),
 ]
 
 # globaltimer stamps of CTA <block>'s thread 0: entry, after setup, after the
