@@ -220,6 +220,42 @@ int argmax(const std::vector<double>& sc) {
   return k;
 }
 
+// Tournament tree over per-job keys for the greedy's repeated picks: after a
+// micro-window only the granted job's acc / gain change, so each pick is
+// O(log J) instead of the O(J) rescan.  `better(a, b)` is the scan's strict
+// comparison (b replaces the running winner a only if strictly better), so
+// the winner is the lowest index among the best keys -- the same job the
+// linear scans above return whenever no key is NaN (callers check).
+template <class Better>
+struct Tourney {
+  int n = 0, P = 1;
+  std::vector<int> t;  // t[P + k] = k; internal nodes hold the subtree winner (-1: empty)
+  Better better;
+  explicit Tourney(int n_, Better b) : n(n_), better(b) {
+    while (P < n) P <<= 1;
+    t.assign(2 * P, -1);
+    for (int k = 0; k < n; ++k) t[P + k] = k;
+    for (int i = P - 1; i >= 1; --i) t[i] = pick(t[2 * i], t[2 * i + 1]);
+  }
+  int pick(int a, int b) const {
+    if (a < 0) return b;
+    if (b < 0) return a;
+    return better(b, a) ? b : a;  // a has the lower index
+  }
+  void update(int k) {
+    for (int i = (P + k) >> 1; i >= 1; i >>= 1) t[i] = pick(t[2 * i], t[2 * i + 1]);
+  }
+  int best() const { return t[1]; }
+  int best_except(int x) const {  // winner over every index but x
+    int w = -1;
+    for (int i = P + x; i > 1; i >>= 1) {  // siblings along x's path, in index order
+      const int sib = i ^ 1;
+      w = (sib < i) ? pick(t[sib], w) : pick(w, t[sib]);
+    }
+    return w;
+  }
+};
+
 }  // namespace ecco_alloc
 
 // ------------------------------------------------------------ scenario --
@@ -1741,16 +1777,45 @@ ecco_status ecco_allocate_trajectories(int n_jobs, const int* job_ids, const int
       for (int k = 0; k < n_jobs; ++k) out_initial_scores[k] = sc[k];
   }
   int rr = 0;
-  while (budget > 0) {  // run_remaining (:168-181)
-    int k;
-    if (policy == 1) {
-      k = rr % n_jobs;
-      ++rr;
-    } else {
-      ecco_alloc::scores(policy == 2, bonus != 0, coef, ids, mem, acc, gain, sc);
-      k = ecco_alloc::argmax(sc);
+  bool finite = true;  // the trees reproduce the scans' picks when no key is NaN
+  for (size_t i = 0; i < (size_t)n_jobs * traj_len; ++i) finite = finite && !std::isnan(traj[i]);
+  if (policy == 1 || !finite) {
+    while (budget > 0) {  // run_remaining (:168-181)
+      int k;
+      if (policy == 1) {
+        k = rr % n_jobs;
+        ++rr;
+      } else {
+        ecco_alloc::scores(policy == 2, bonus != 0, coef, ids, mem, acc, gain, sc);
+        k = ecco_alloc::argmax(sc);
+      }
+      run_micro(k);
+    }
+    return ECCO_OK;
+  }
+  // the same greedy, each pick from two tournament trees: the bonus-free
+  // score (coef * gain, or members * gain for total_acc) and, for the
+  // fairness bonus, the least-accurate job (lowest id on ties)
+  std::vector<double> base(n_jobs);
+  auto base_of = [&](int k) { return policy == 2 ? mem[k] * gain[k] : coef[k] * gain[k]; };
+  for (int k = 0; k < n_jobs; ++k) base[k] = base_of(k);
+  auto hi = [&](int a, int b) { return base[a] > base[b]; };
+  auto lo = [&](int a, int b) { return acc[a] < acc[b]; };
+  ecco_alloc::Tourney<decltype(hi)> top(n_jobs, hi);
+  ecco_alloc::Tourney<decltype(lo)> low(n_jobs, lo);
+  const bool with_bonus = policy == 0 && bonus != 0;
+  while (budget > 0) {
+    int k = top.best();
+    if (with_bonus) {
+      const int m = low.best();
+      const double boosted = base[m] + gain[m];
+      const int v = top.best_except(m);
+      k = v < 0 || boosted > base[v] || (boosted == base[v] && m < v) ? m : v;
     }
     run_micro(k);
+    base[k] = base_of(k);
+    top.update(k);
+    low.update(k);
   }
   return ECCO_OK;
 }

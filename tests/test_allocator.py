@@ -56,6 +56,26 @@ def test_decisions_bit_identical(policy, quantized):
             assert gi.tobytes() == ri.tobytes()
 
 
+# The driver's picks come from tournament trees (O(log J) per micro-window);
+# at the bench's scale (J = 500, W = 1000) and with NaN trajectories (which
+# fall back to the scans) they must still be the reference's.
+@pytest.mark.parametrize("policy", [0, 2])
+@pytest.mark.parametrize("quantized", [False, True])
+def test_decisions_bit_identical_at_scale(policy, quantized):
+    rng = np.random.default_rng(91 + policy + quantized)
+    for trial in range(3):
+        n, L = 500, 3
+        ids, members, traj = _case(rng, n, L, quantized)
+        if trial == 2:
+            traj[rng.integers(0, n, 3), rng.integers(0, L, 3)] = np.nan
+        for bonus in (True, False):
+            st, rj, rb, ra, ri = _ref(ids, members, traj, 1.0, 0.5, 2 * n, 1.0, 1, bonus, policy)
+            assert st == 0
+            gj, gb, ga, gi = ecco.allocate_trajectories(ids, members, traj, 1.0, 0.5, 2 * n, 1.0,
+                                                        1, bonus, policy)
+            assert (gj == rj).all() and gb.tobytes() == rb.tobytes() and ga.tobytes() == ra.tobytes()
+
+
 def test_reference_kat_sequences():
     # test_gpu_allocator.cpp:155-176: three equal jobs, one better trajectory
     ids = np.array([1, 2, 3], np.int32)
