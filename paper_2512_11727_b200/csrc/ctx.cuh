@@ -290,8 +290,10 @@ namespace fused {
 bool supported(const ecco_ctx* ctx);
 void init_shadow(ecco_ctx* ctx, Shadow& sh);
 void free_shadow(Shadow& sh);
+// bf16 images of the models in `slots` (W1^T only for `w1t_slots` when
+// given: the fused SGD chain writes the W1^T image of every model it trained)
 void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
-                    const std::vector<int>& slots);
+                    const std::vector<int>& slots, const std::vector<int>* w1t_slots = nullptr);
 // Correct-prediction counts of (probe camera, model slot) pairs.  Dense mode
 // (d_tile_ebeg == nullptr): every probe under every entry, counts[p*ld+col].
 // Pairs mode: tile m walks entries [tile_ebeg[m], tile_ebeg[m+1]) and a probe

@@ -810,14 +810,18 @@ bool supported(const ecco_ctx* ctx) {
 
 
 void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
-                    const std::vector<int>& slots) {
+                    const std::vector<int>& slots, const std::vector<int>* w1t_slots) {
   if (slots.empty()) return;
   const ecco_config& g = ctx->cfg;
   int* d_sl = ctx->upload(10, slots.data(), slots.size());
   const int n = (int)slots.size();
-  k_shadow_w1t<<<dim3(g.feat_dim / 32, g.hidden_dim / 32, n), dim3(32, 8), 0, ctx->stream>>>(
-      g.feat_dim, g.hidden_dim, d_sl, wbase, wstride, sh.w1t, ctx->w1_t);
-  ECCO_LAUNCHED(ctx);
+  const std::vector<int>& s1 = w1t_slots ? *w1t_slots : slots;
+  if (!s1.empty()) {
+    const int* d_s1 = w1t_slots ? ctx->upload(15, s1.data(), s1.size()) : d_sl;
+    k_shadow_w1t<<<dim3(g.feat_dim / 32, g.hidden_dim / 32, (unsigned)s1.size()), dim3(32, 8), 0,
+                   ctx->stream>>>(g.feat_dim, g.hidden_dim, d_s1, wbase, wstride, sh.w1t, ctx->w1_t);
+    ECCO_LAUNCHED(ctx);
+  }
   k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_sl, wbase,
                                            wstride, sh.w2t, img_bytes(g));
   ECCO_LAUNCHED(ctx);

@@ -983,7 +983,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
       fused::train_chain(ctx, &ctx->sh_spec, n_jobs, d_slots, d_job_ids, d_steps, h_steps,
                          d_src_off, d_src_cam, d_src_frac, d_micro_base, t - 1, window, wt,
                          spec_stride, t - 1);
-    if (tc_bf16) fused::shadow_w1t(ctx, d_slots, n_jobs, wt, spec_stride, w1t_train);
+    if (tc_bf16 && !ctx->fused_train) fused::shadow_w1t(ctx, d_slots, n_jobs, wt, spec_stride, w1t_train);
     for (int step = 0; step < (ctx->fused_train ? 0 : max_steps); ++step) {
       const Gate gate{d_steps, step, g.B};
       int live = 0;
@@ -1037,7 +1037,14 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     }
     // evaluate state t
     if (n_mem && ctx->fused_eval) {
-      fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots);
+      if (ctx->fused_train) {  // the chain wrote the W1^T image of every job it trained
+        std::vector<int> idle;
+        for (int j = 0; j < n_jobs; ++j)
+          if (h_steps[j] <= 0) idle.push_back(slots[j]);
+        fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots, &idle);
+      } else {
+        fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots);
+      }
       pair_counts_fused(ctx, ctx->sh_spec, wt, spec_stride, n_mem, hps.data(), d_ps, d_mem_cam,
                         d_cnt);
       k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
