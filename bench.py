@@ -346,7 +346,12 @@ def run_b200(args, rank, world, local_rank):
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "tf32" if args.math == "tf32" else "f32",
+            # operand type of the tensor-core contractions (fp32 accumulation
+            # and fp32 masters throughout): the fused chain and the evaluation
+            # kernels run kind::f16 bf16; shapes outside the chain train with
+            # a bf16 forward and a tf32 dW1; --math ffma is fp32 on CUDA cores
+            "dtype": ("f32" if args.math != "tf32" else "bf16" if chain
+                      else "bf16+tf32" if DIMS["minibatch"] % 128 == 0 and H % 256 == 0 else "tf32"),
             "data": "synthetic (counter-RNG camera streams, random-init group MLPs)",
             "config": {
                 "workload": f"{args.config}: {wl.N} cameras / {wl.G} groups, learned classifier "
