@@ -281,6 +281,26 @@ ecco_status ecco_train_trajectories(
     const int* member_offsets /* n_jobs+1 */, const int* member_cams,
     const int* micro_base, int window, double gpu_seconds, int depth,
     double* out_acc /* n_jobs*(depth+1) */);
+
+/* Sampled-row variant of the staged ingest (the e2e path): the SGD draws of
+ * the NEXT ecco_train_trajectories call (same job / batch / source-mix /
+ * micro_base / window / gpu_s / depth arguments) are marked on the device,
+ * and only those ring rows are read from `frames` (the full
+ * [n_cams][R][F] table, which must be PINNED host memory: the copy stream
+ * reads it zero-copy over PCIe) into the back buffer; all labels and the
+ * first n_eval cameras' eval sets are copied as in ecco_stage_frames.  Rows
+ * the trajectories never draw are not transferred (their back-buffer slots
+ * are stale), so the trajectories' results equal a full upload's.  Counts
+ * the rows read into ecco_transfer_bytes.  While such a fetch may run, the
+ * persistent evaluation kernels leave two SMs free.  Replaces, for the
+ * learned path, the per-window frame delivery the reference models as
+ * TrainingBatchStats (accuracy_model.hpp:36-44). */
+ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_ids,
+                                      const ecco_batch* batches, const int* src_off,
+                                      const int* src_cams, const double* src_fracs,
+                                      const int* micro_base, int window, double gpu_s, int depth,
+                                      const uint16_t* frames, const int32_t* labels, int n_eval,
+                                      const uint16_t* eval_frames, const int32_t* eval_labels);
 /* Makes the snapshot after granted[j] steps of the last chain (0 = keep the
  * committed model) the committed model. */
 ecco_status ecco_commit(ecco_ctx* ctx, int n_jobs, const int* job_ids, const int* granted);

@@ -98,7 +98,8 @@ EXPORTS = [
     "ecco_default_config", "ecco_create", "ecco_destroy", "ecco_last_error",
     "ecco_kernel_launches", "ecco_profile", "ecco_kernel_stat", "ecco_transfer_bytes", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
     "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
-    "ecco_read_frames", "ecco_stage_frames", "ecco_stage_frames_range", "ecco_swap_frames",
+    "ecco_read_frames", "ecco_stage_frames", "ecco_stage_frames_range", "ecco_stage_sampled_frames",
+    "ecco_swap_frames",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
@@ -320,6 +321,20 @@ class Context:
         self._check(lib().ecco_stage_frames_range(
             self._h, int(ring_first), int(ring_n), C.c_void_p(frames_ptr), C.c_void_p(labels_ptr),
             int(eval_n), C.c_void_p(eval_ptr), C.c_void_p(eval_labels_ptr)))
+
+    def stage_sampled_host_ptr(self, p, gpu_seconds, depth, window, frames_ptr, labels_ptr,
+                               eval_n, eval_ptr, eval_labels_ptr, micro_base=None):
+        """ecco_stage_sampled_frames for the prepare_trajectories() batch `p`:
+        the ring rows that train_prepared(p, gpu_seconds, depth, window,
+        micro_base) will draw are read zero-copy from the PINNED full frame
+        table at frames_ptr ([n_cams][R][F] bf16 bits) into the back buffer,
+        with every label and the eval sets of cameras [0, eval_n)."""
+        mb = p["mb0"] if micro_base is None else np.ascontiguousarray(micro_base, np.int32)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        self._check(lib().ecco_stage_sampled_frames(
+            self._h, p["n"], vp(p["ids"]), p["bt"], vp(p["so"]), vp(p["sc"]), vp(p["sf"]), vp(mb),
+            C.c_int(window), C.c_double(gpu_seconds), C.c_int(depth), C.c_void_p(frames_ptr),
+            C.c_void_p(labels_ptr), int(eval_n), C.c_void_p(eval_ptr), C.c_void_p(eval_labels_ptr)))
 
     def swap_frames(self):
         self._check(lib().ecco_swap_frames(self._h))

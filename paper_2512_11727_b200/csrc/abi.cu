@@ -36,7 +36,7 @@ void free_all(ecco_ctx* c) {
                   c->d_scl,    c->d_sprof,  c->d_scen,    c->d_status,  c->d_w,
                   c->d_wspec,  c->d_proto_p, c->d_proto_q, c->d_frames, c->d_labels,
                   c->d_eval,   c->d_eval_labels, c->d_losses, c->b_frames, c->b_labels,
-                  c->b_eval,   c->b_eval_labels};
+                  c->b_eval,   c->b_eval_labels, c->d_zc_rows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   fused::free_shadow(c->sh_commit);
@@ -45,6 +45,8 @@ void free_all(ecco_ctx* c) {
   for (auto& b : c->scratch) b.release();
   for (auto& b : c->train_scratch) b.release();
   for (auto& b : c->hscratch) b.release();
+  for (auto& b : c->zc_args) b.release();
+  c->zc_flags.release();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->copy_done) cudaEventDestroy(c->copy_done);
   if (c->back_free) cudaEventDestroy(c->back_free);
@@ -253,6 +255,13 @@ ecco_status ecco_kernel_stat(ecco_ctx* ctx, int which, uint64_t* launches, doubl
 ecco_status ecco_transfer_bytes(const ecco_ctx* ctx, uint64_t* h2d, uint64_t* d2h) {
   *h2d = ctx->h2d_bytes;
   *d2h = ctx->d2h_bytes;
+  if (ctx->d_zc_rows) {  // + rows read from pinned host memory by the sampled-row fetch
+    unsigned long long n = 0;
+    if (cudaStreamSynchronize(ctx->copy_stream) != cudaSuccess ||
+        cudaMemcpy(&n, ctx->d_zc_rows, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return ECCO_ERR_CUDA;
+    *h2d += n * (uint64_t)ctx->cfg.feat_dim * 2;
+  }
   return ECCO_OK;
 }
 
@@ -321,6 +330,24 @@ ecco_status ecco_stage_frames(ecco_ctx* ctx, int n, const uint16_t* frames, cons
   return ecco_stage_frames_range(ctx, 0, n, frames, labels, n, eval, eval_labels);
 }
 
+// Back buffers + copy stream of the double-buffered ingest (first use); the
+// copy stream then waits until kernels of the previous window stop reading
+// the back buffer.
+void open_back_buffers(ecco_ctx* ctx) {
+  const ecco_config& g = ctx->cfg;
+  if (!ctx->copy_stream) {
+    ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    ECCO_CUDA(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+    ECCO_CUDA(cudaEventCreateWithFlags(&ctx->back_free, cudaEventDisableTiming));
+    const size_t fr = (size_t)g.max_cameras * g.ring_frames, ev = (size_t)g.max_cameras * g.eval_samples;
+    dalloc(&ctx->b_frames, fr * g.feat_dim);
+    dalloc(&ctx->b_labels, fr);
+    dalloc(&ctx->b_eval, ev * g.feat_dim);
+    dalloc(&ctx->b_eval_labels, ev);
+  }
+  if (ctx->back_busy) ECCO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->back_free, 0));
+}
+
 ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint16_t* frames,
                                     const int32_t* labels, int n_eval, const uint16_t* eval,
                                     const int32_t* eval_labels) {
@@ -330,18 +357,7 @@ ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint1
     ECCO_REQUIRE(n_eval >= 0 && n_eval <= ctx->n_cams, "stage_frames: eval camera count");
     ECCO_REQUIRE(!ctx->staged, "stage_frames: previous staging not swapped in");
     const ecco_config& g = ctx->cfg;
-    if (!ctx->copy_stream) {
-      ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
-      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->back_free, cudaEventDisableTiming));
-      const size_t fr = (size_t)g.max_cameras * g.ring_frames, ev = (size_t)g.max_cameras * g.eval_samples;
-      dalloc(&ctx->b_frames, fr * g.feat_dim);
-      dalloc(&ctx->b_labels, fr);
-      dalloc(&ctx->b_eval, ev * g.feat_dim);
-      dalloc(&ctx->b_eval_labels, ev);
-    }
-    // the back buffer may still be read by kernels of the previous window
-    if (ctx->back_busy) ECCO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->back_free, 0));
+    open_back_buffers(ctx);
     const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n_eval * g.eval_samples;
     const size_t f0 = (size_t)first * g.ring_frames;
     const cudaMemcpyKind k = cudaMemcpyHostToDevice;
@@ -351,6 +367,71 @@ ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint1
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream));
     ECCO_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+    ctx->staged = true;
+  });
+}
+
+ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_ids,
+                                      const ecco_batch* batches, const int* src_off,
+                                      const int* src_cams, const double* src_fracs,
+                                      const int* micro_base, int window, double gpu_s, int depth,
+                                      const uint16_t* frames, const int32_t* labels, int n_eval,
+                                      const uint16_t* eval, const int32_t* eval_labels) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(learned(ctx), "stage_sampled_frames: learned backend only");
+    ECCO_REQUIRE(!ctx->staged, "stage_sampled_frames: previous staging not swapped in");
+    ECCO_REQUIRE(n_jobs >= 0 && depth >= 1 && depth <= ctx->cfg.max_depth,
+                 "stage_sampled_frames: depth must be in [1, max_depth]");
+    ECCO_REQUIRE(n_eval >= 0 && n_eval <= ctx->n_cams, "stage_sampled_frames: eval camera count");
+    ECCO_REQUIRE(n_jobs == 0 || src_off[0] == 0, "CSR offsets must start at 0");
+    for (int j = 0; j < n_jobs; ++j)
+      validate_batch(ctx, j, gpu_s, src_off[j + 1] - src_off[j], src_cams + src_off[j],
+                     src_fracs + src_off[j]);
+    const ecco_config& g = ctx->cfg;
+    void* fdev = nullptr;  // the device address of the pinned ring table
+    ECCO_REQUIRE(cudaHostGetDevicePointer(&fdev, (void*)frames, 0) == cudaSuccess,
+                 "stage_sampled_frames: frames must be pinned (mapped) host memory");
+    open_back_buffers(ctx);
+    cudaStream_t st = ctx->copy_stream;
+    if (!ctx->d_zc_rows) {
+      dalloc(&ctx->d_zc_rows, 1);
+      ECCO_CUDA(cudaDeviceSynchronize());
+    }
+    const cudaMemcpyKind k = cudaMemcpyHostToDevice;
+    const size_t rows = (size_t)ctx->n_cams * g.ring_frames, words = (rows + 31) / 32;
+    uint32_t* flags = (uint32_t*)ctx->zc_flags.get(words * 4);
+    ECCO_CUDA(cudaMemsetAsync(flags, 0, words * 4, st));
+    if (n_jobs > 0) {
+      std::vector<int> steps(n_jobs), mb(n_jobs, 0);
+      int max_steps = 0;
+      for (int j = 0; j < n_jobs; ++j) {
+        steps[j] = learned_steps(ctx, batches[j], gpu_s, src_off[j + 1] - src_off[j],
+                                 src_cams + src_off[j]);
+        max_steps = std::max(max_steps, steps[j]);
+      }
+      if (micro_base) mb.assign(micro_base, micro_base + n_jobs);
+      const size_t nsrc = std::max(src_off[n_jobs], 1);
+      auto up = [&](int i, const void* h, size_t bytes) {
+        void* d = ctx->zc_args[i].get(bytes);
+        ECCO_CUDA(ctx_memcpy(ctx, d, h, bytes, k, st));
+        return d;
+      };
+      const int* d_j = (const int*)up(0, job_ids, sizeof(int) * n_jobs);
+      const int* d_st = (const int*)up(1, steps.data(), sizeof(int) * n_jobs);
+      const int* d_so = (const int*)up(2, src_off, sizeof(int) * (n_jobs + 1));
+      const int* d_sc = (const int*)up(3, src_cams, sizeof(int) * nsrc);
+      const double* d_sf = (const double*)up(4, src_fracs, sizeof(double) * nsrc);
+      const int* d_mb = (const int*)up(5, mb.data(), sizeof(int) * n_jobs);
+      stage::mark_sampled(ctx, st, n_jobs, d_j, d_st, max_steps, d_so, d_sc, d_sf, d_mb, depth,
+                          window, flags);
+    }
+    ctx->sm_reserve = 2;  // from now on the persistent kernels leave room for the fetch
+    stage::fetch_rows(ctx, st, (const uint16_t*)fdev, ctx->b_frames, flags, words, ctx->d_zc_rows);
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels, labels, rows * 4, k, st));
+    const size_t ev = (size_t)n_eval * g.eval_samples;
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, st));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, st));
+    ECCO_CUDA(cudaEventRecord(ctx->copy_done, st));
     ctx->staged = true;
   });
 }

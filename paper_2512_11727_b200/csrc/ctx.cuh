@@ -185,6 +185,14 @@ struct ecco_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t copy_done = nullptr, back_free = nullptr;
   bool staged = false, back_busy = false;
+  // sampled-row ingest (ecco_stage_sampled_frames): the window's job
+  // arguments on the copy stream, the bitmap of drawn ring rows, and the
+  // running count of rows read from host memory over PCIe (zero-copy)
+  DevBuf zc_args[6], zc_flags;
+  unsigned long long* d_zc_rows = nullptr;
+  // SMs left free by the persistent evaluation kernels while a zero-copy
+  // row fetch may be streaming on copy_stream
+  int sm_reserve = 0;
 
   // fused evaluation: shadows of the committed models (refreshed lazily for
   // slots marked dirty) and of the speculative snapshot being evaluated
@@ -323,6 +331,21 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
                  const int* d_micro_base, int micro_add, int window, float* wbase, size_t wstride,
                  int loss_t);
 }  // namespace fused
+
+// Sampled-row ingest (stage_kernels.cu), on the given stream.
+namespace stage {
+// Marks, in a bitmap over ring rows (cam * R + frame), every row the fused
+// or general SGD path will draw for micro-windows micro_base[j] + t,
+// t < depth (the same counter-RNG draws as k_chain_rows / k_l_sample).
+void mark_sampled(ecco_ctx* ctx, cudaStream_t st, int n_jobs, const int* d_job_ids,
+                  const int* d_steps, int max_steps, const int* d_src_off, const int* d_src_cam,
+                  const double* d_src_frac, const int* d_micro_base, int depth, int window,
+                  uint32_t* d_flags);
+// Copies every marked row (F bf16) from mapped pinned host memory into dst
+// (same [row][F] layout), counting the rows into *d_count.
+void fetch_rows(ecco_ctx* ctx, cudaStream_t st, const uint16_t* host_dev, uint16_t* dst,
+                const uint32_t* d_flags, size_t n_words, unsigned long long* d_count);
+}  // namespace stage
 
 namespace lbackend {
 void init(ecco_ctx* ctx);

@@ -923,7 +923,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
       pattr = true;
     }
     const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
-    const int pairs = std::min(n_super, sm_count(g.device) / 2);
+    const int pairs = std::min(n_super, (sm_count(g.device) - ctx->sm_reserve) / 2);
     ECCO_TIMED(ctx, kind, flops, bytes,
                (k_eval_pair<<<2 * pairs, kThreads, psmem, ctx->stream>>>(
                    *(const CUtensorMap*)ctx->map_x, *(const CUtensorMap*)sh.map_w_pair,
@@ -931,7 +931,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
     ECCO_LAUNCHED(ctx);
     return;
   }
-  const int grid = std::min(a.n_tiles, sm_count(g.device));
+  const int grid = std::min(a.n_tiles, sm_count(g.device) - ctx->sm_reserve);
   ECCO_TIMED(ctx, kind, flops, bytes,
              (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
                                                                   *(const CUtensorMap*)sh.map_w, a)));

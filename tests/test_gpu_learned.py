@@ -160,6 +160,48 @@ def test_staged_frame_range_and_swap():
     assert ge.tobytes() == ev.tobytes() and gel.tobytes() == el.tobytes()
 
 
+@pytest.mark.parametrize("math", [ecco.FFMA_EXACT, ecco.TC_TF32])
+def test_sampled_staging_equals_full_frames(math):
+    """ecco_stage_sampled_frames (the e2e ingest): only the ring rows the next
+    trajectories draw are read from pinned host memory into a back buffer that
+    was POISONED (NaN frames) beforehand; trajectories and committed weights
+    must equal, bit for bit, those of a context holding every frame -- so
+    every row the SGD path reads was fetched -- and the fetched byte count is
+    reported."""
+    import torch
+    kw = {} if math == ecco.FFMA_EXACT else dict(FUSED)
+    ids = [1, 2, 3, 4]
+    res = []
+    for sampled in (False, True):
+        ctx, orc, rng = setup(seed=11, math=math, **kw)
+        ctx.seed_models(ids)
+        members, sources, fracs, batches = _jobs(rng, len(ids), 6)
+        p = ctx.prepare_trajectories(ids, batches, sources, fracs, members)
+        if sampled:
+            fr = torch.from_numpy(np.ascontiguousarray(orc.frames).view(np.int16)).pin_memory()
+            lb = torch.from_numpy(np.ascontiguousarray(orc.labels)).pin_memory()
+            ev = torch.from_numpy(np.ascontiguousarray(orc.eval).view(np.int16)).pin_memory()
+            el = torch.from_numpy(np.ascontiguousarray(orc.eval_labels)).pin_memory()
+            poison = torch.full_like(fr, 0x7FC0)  # bf16 NaN in every ring row
+            for _ in range(2):  # both halves of the double buffer
+                ctx.stage_frames_range_host_ptr(0, 6, poison.data_ptr(), lb.data_ptr(), 6,
+                                                ev.data_ptr(), el.data_ptr())
+                ctx.swap_frames()
+            h0, _ = ctx.transfer_bytes()
+            ctx.stage_sampled_host_ptr(p, 6.0, 2, 3, fr.data_ptr(), lb.data_ptr(), 6, ev.data_ptr(),
+                                       el.data_ptr())
+            ctx.swap_frames()
+            h1, _ = ctx.transfer_bytes()
+            ring = orc.frames.nbytes
+            fetched = h1 - h0 - orc.labels.nbytes - orc.eval.nbytes - orc.eval_labels.nbytes
+            assert 0 < fetched < ring  # (plus a few hundred bytes of job arguments)
+        acc = ctx.train_prepared(p, 6.0, 2, window=3)
+        ctx.commit(ids, [2] * len(ids))
+        res.append((acc.tobytes(), [w.tobytes() for j in ids for w in ctx.get_weights(j)]))
+    assert res[0][0] == res[1][0]
+    assert res[0][1] == res[1][1]
+
+
 def test_learned_simulation_runs_and_groups():
     from paper_2512_11727_b200 import scenarios
     sc = scenarios.synthetic(24, 3, windows=2, micro_windows=8, drift_frac=0.1, local_acc=0.0, seed=3)
