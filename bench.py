@@ -330,7 +330,7 @@ def run_b200(args, rank, world, local_rank):
     samples = reduce_sum(dist, wl.samples_per_step_local() * args.steps)
 
     # ---- e2e: same step through the public API, frames from pinned host memory
-    e2e = None if args.no_e2e else run_e2e(args, ctx, wl, step, torch, dist, stream, best)
+    e2e = None if args.no_e2e else run_e2e(args, ctx, wl, step, torch, dist, stream, best, prep)
 
     if rank == 0:
         pk, pk_kind = peaks()
@@ -505,7 +505,7 @@ def roofline(kst, pk, pk_kind, args):
     return head, every
 
 
-def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev):
+def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev, prep):
     """Frames uploaded from pinned host memory and results read back every step."""
     import paper_2512_11727_b200 as ecco  # noqa: F401
     R, S, F = DIMS["ring_frames"], DIMS["eval_samples"], DIMS["feat_dim"]
@@ -526,22 +526,30 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev):
     if dist is not None:
         dist.barrier()
     t0 = time.perf_counter()
-    # this rank's groups train on their members' rings only: upload those
-    # (a contiguous camera range) plus every camera's eval set
+    # this rank's groups train on their members' rings only.  Default: the
+    # ring rows the window's SGD steps draw (marked on the device from the
+    # same counter-RNG draws, read zero-copy from the pinned table); with
+    # --e2e-full-rings every ring of the rank's camera range is copied.  Both
+    # add every camera's eval set and all labels.
     c0, c1 = (wl.local[0] * wl.per, (wl.local[-1] + 1) * wl.per) if wl.local else (0, 0)
     ptrs = (fr[c0].data_ptr() if c1 > c0 else fr.data_ptr(), lb[c0].data_ptr() if c1 > c0 else lb.data_ptr(),
             wl.N, evf.data_ptr(), evl.data_ptr())
 
-    def stage():
-        ctx.stage_frames_range_host_ptr(c0, c1 - c0, *ptrs)
+    def stage(w):
+        if args.e2e_full_rings or not wl.local:
+            ctx.stage_frames_range_host_ptr(c0, c1 - c0, *ptrs)
+        else:
+            ctx.stage_sampled_host_ptr(prep, GPU_S, DEPTH, w, fr.data_ptr(), lb.data_ptr(), wl.N,
+                                       evf.data_ptr(), evl.data_ptr())
 
-    # double-buffered ingest: window k+1's frames stream in on the copy engine
-    # while window k's kernels run (every window's copy is inside the region)
-    stage()
+    # double-buffered ingest: window k+1's frames stream in on the copy
+    # stream while window k's kernels run (every window's copy is inside the
+    # region)
+    stage(10_000)
     ctx.swap_frames()
     for k in range(steps):
         if k + 1 < steps:
-            stage()
+            stage(10_000 + k + 1)
         step(10_000 + k)
         with torch.cuda.stream(stream):
             best_host.copy_(best_dev, non_blocking=True)  # group assignments back to the host
@@ -556,11 +564,16 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev):
     return {"value": samples / el_s, "unit": "samples/s",
             "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
             "ms_per_step": el_s * 1e3 / steps, "steps": steps,
-            "how": "every window's frames copied from pinned host buffers (ecco_stage_frames_range "
-                   "on a copy stream: the rings of this rank's group members and every camera's "
-                   "eval set; double-buffered so window k+1 uploads while window k computes; "
-                   "ecco_swap_frames) + the step + assignments/accuracies read back; wall clock "
-                   "with a device synchronize at the end, window 0's unoverlapped upload included",
+            "how": ("every window's frames from pinned host buffers on a copy stream, "
+                    + ("ecco_stage_frames_range: the full rings of this rank's group members"
+                       if args.e2e_full_rings else
+                       "ecco_stage_sampled_frames: the ring rows this rank's SGD steps draw, marked "
+                       "on the device and read zero-copy over PCIe (rows never drawn are not "
+                       "transferred)")
+                    + ", all labels and every camera's eval set; double-buffered so window k+1 "
+                    "uploads while window k computes (ecco_swap_frames) + the step + "
+                    "assignments/accuracies read back; wall clock with a device synchronize at the "
+                    "end, window 0's unoverlapped upload included"),
             "pcie_gbs": (h1 - h0) / steps / (el_s / steps) / 1e9}
 
 
@@ -822,6 +835,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
+    ap.add_argument("--e2e-full-rings", action="store_true",
+                    help="e2e ingest copies every ring of the rank's cameras, not only the drawn rows")
     ap.add_argument("--no-scaling", action="store_true",
                     help="skip the single-GPU emulation of rank 0 at N = 2, 4, 8")
     ap.add_argument("--no-parametric", action="store_true",
