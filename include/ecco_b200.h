@@ -212,7 +212,8 @@ ecco_status ecco_eval_jobs(ecco_ctx* ctx, int n_jobs, const int* job_ids,
 ecco_status ecco_eval_matrix(ecco_ctx* ctx, int n_probes, const double* scenes,
                              const int* cam_idx, int n_jobs, const int* job_ids,
                              const uint8_t* mask, double* out);
-/* Device-resident variant: out_dev is an n_probes*n_jobs fp64 device buffer. */
+/* Device-resident variant: out_dev is an n_probes*n_jobs fp64 device buffer;
+ * stream-ordered on the context stream, returns without host synchronisation. */
 ecco_status ecco_eval_matrix_dev(ecco_ctx* ctx, int n_probes, const double* scenes,
                                  const int* cam_idx, int n_jobs, const int* job_ids,
                                  const uint8_t* mask, void* out_dev);

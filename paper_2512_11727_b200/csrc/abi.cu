@@ -46,6 +46,8 @@ void free_all(ecco_ctx* c) {
   for (auto& b : c->train_scratch) b.release();
   for (auto& b : c->hscratch) b.release();
   for (auto& b : c->zc_args) b.release();
+  for (auto& b : c->traj_args) b.release();
+  for (auto& b : c->em_args) b.release();
   c->zc_flags.release();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->copy_done) cudaEventDestroy(c->copy_done);
@@ -633,7 +635,9 @@ static void eval_matrix_impl(ecco_ctx* ctx, int n, const double* scenes, const i
                              int g, const int* job_ids, const uint8_t* mask, double* d_out) {
   if (n == 0 || g == 0) return;
   auto s = slots_of(ctx, g, job_ids);
-  DevBuf bs, bp, bm;
+  DevBuf& bs = ctx->em_args[0];  // kept across calls: no cudaMalloc/cudaFree per window
+  DevBuf& bp = ctx->em_args[1];
+  DevBuf& bm = ctx->em_args[2];
   int* d_s = (int*)bs.get(sizeof(int) * g);
   ECCO_CUDA(ctx_memcpy(ctx, d_s, s.data(), sizeof(int) * g, cudaMemcpyHostToDevice, ctx->stream));
   uint8_t* d_m = nullptr;
@@ -654,10 +658,6 @@ static void eval_matrix_impl(ecco_ctx* ctx, int n, const double* scenes, const i
     ECCO_CUDA(ctx_memcpy(ctx, d_sc, scenes, sizeof(double) * n * D, cudaMemcpyHostToDevice, ctx->stream));
     pbackend::eval_matrix(ctx, n, d_sc, g, d_s, d_m, d_out);
   }
-  ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
-  bs.release();
-  bp.release();
-  bm.release();
 }
 
 ecco_status ecco_eval_matrix(ecco_ctx* ctx, int n, const double* scenes, const int* cam_idx, int g,
@@ -667,6 +667,7 @@ ecco_status ecco_eval_matrix(ecco_ctx* ctx, int n, const double* scenes, const i
     DevBuf o;
     double* d_out = (double*)o.get(sizeof(double) * (size_t)n * g);
     eval_matrix_impl(ctx, n, scenes, cam_idx, g, job_ids, mask, d_out);
+    ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
     ECCO_CUDA(cudaMemcpy(out, d_out, sizeof(double) * (size_t)n * g, cudaMemcpyDeviceToHost));
     o.release();
   });
@@ -798,7 +799,7 @@ ecco_status ecco_train_trajectories(ecco_ctx* ctx, int n_jobs, const int* job_id
     check_cams(ctx, mem_off[n_jobs], mem_cams, "train_trajectories members");
     auto s = slots_of(ctx, n_jobs, job_ids);
     const size_t nsrc = std::max(src_off[n_jobs], 1), nmem = std::max(mem_off[n_jobs], 1);
-    DevBuf b[9];
+    DevBuf* b = ctx->traj_args;  // kept across calls: no cudaMalloc/cudaFree per window
     auto up = [&](int i, const void* h, size_t bytes) {
       void* d = b[i].get(bytes);
       ECCO_CUDA(ctx_memcpy(ctx, d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -834,7 +835,6 @@ ecco_status ecco_train_trajectories(ecco_ctx* ctx, int n_jobs, const int* job_id
     }
     ECCO_CUDA(ctx_memcpy(ctx, out_acc, d_out, sizeof(double) * n_jobs * (depth + 1), cudaMemcpyDeviceToHost, ctx->stream));
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (auto& x : b) x.release();
   });
 }
 

@@ -189,6 +189,8 @@ struct ecco_ctx {
   // arguments on the copy stream, the bitmap of drawn ring rows, and the
   // running count of rows read from host memory over PCIe (zero-copy)
   DevBuf zc_args[6], zc_flags;
+  DevBuf traj_args[9];  // ecco_train_trajectories' uploaded arguments
+  DevBuf em_args[3];    // ecco_eval_matrix(_dev)'s uploaded arguments
   unsigned long long* d_zc_rows = nullptr;
   // SMs left free by the persistent evaluation kernels while a zero-copy
   // row fetch may be streaming on copy_stream
