@@ -299,6 +299,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   const size_t r0 = (size_t)j * a.B;
   const int nk = a.B / kKC;
   const uint32_t idesc = idesc_tf32(kM, NT, 0, 0);
+  {  // the W1 tile the epilogue read-modify-writes -> L2 while the MMAs run
+    const float* wt = a.wbase + (size_t)a.slots[j] * a.wstride + (size_t)f0 * a.H + n0;
+    constexpr int kLines = kM * NT / 32;  // 128-byte lines of the tile
+    for (int li = tid; li < kLines; li += kThreads)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(wt + (size_t)(li / (NT / 32)) * a.H +
+                                                     (li % (NT / 32)) * 32));
+  }
   constexpr int kA = kKC * (kM / 4) / kThreads, kBv = kKC * (NT / 4) / kThreads;
   uint2 ra[kA];
   float4 rb[kBv];

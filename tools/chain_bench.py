@@ -1,11 +1,13 @@
-"""A/B timing of the fused SGD chain alone at the C4 shape (500 groups x 20
-members, F512-H256-C16, B = 128, 2 micro-windows x 16 steps), for tuning:
+"""A/B timing of the learned trajectories alone, for tuning:
 
-  python tools/chain_bench.py [reps]
+  python tools/chain_bench.py [reps] [c4|c5]
 
-Runs the bench's trajectories (train_prepared) `reps` times after warm-up and
-prints the median / min CUDA-event time of the chain kernel per launch
-(ECCO_KSTAT_TRAIN_STEP) and the median SM clock sampled meanwhile."""
+c4 (default): the fused SGD chain at the C4 shape (500 groups x 20 members,
+F512-H256-C16, B = 128, 2 micro-windows x 16 steps); prints the median / min
+CUDA-event time of the chain kernel per launch (ECCO_KSTAT_TRAIN_STEP).
+c5: the detection-head shape (F1024-H1024-C96) through the general
+tensor-core path; prints the per-window time of every kernel family.
+Both print the median SM clock sampled meanwhile."""
 import os
 import statistics
 import subprocess
@@ -23,10 +25,14 @@ import paper_2512_11727_b200 as ecco  # noqa: E402
 
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-    wl = bench.Workload("c4", 0, 1)
+    cfg = sys.argv[2] if len(sys.argv) > 2 else "c4"
+    dims = dict(bench.DIMS)
+    if cfg == "c5":
+        dims.update(bench.DET_DIMS)
+    wl = bench.Workload(cfg, 0, 1)
     ctx = ecco.Context(backend=ecco.LEARNED, device=0, math=ecco.TC_TF32, max_cameras=wl.N,
                        max_jobs=len(wl.local), max_depth=bench.DEPTH,
-                       steps_per_gpu_s=float(bench.STEPS), **bench.DIMS)
+                       steps_per_gpu_s=float(bench.STEPS), **dims)
     ctx.set_cameras(wl.scenes, wl.tp)
     ctx.generate_frames(0)
     ctx.seed_models(wl.local)
@@ -48,17 +54,26 @@ def main():
 
     th = threading.Thread(target=sample)
     th.start()
-    per = []
+    fams = ["TRAIN_STEP", "TRAIN_DW1", "TRAIN_HEAD", "EVAL_MATRIX", "EVAL_PAIRS"]
+    per, fam = [], {f: [] for f in fams}
     for k in range(reps):
         ctx.profile(True)
         ctx.train_prepared(prep, bench.GPU_S, bench.DEPTH, window=10 + k, out=acc)
         n, ms = ctx.kernel_stat(ecco.KSTAT_TRAIN_STEP)[:2]
+        for f in fams:
+            fam[f].append(ctx.kernel_stat(getattr(ecco, "KSTAT_" + f))[1])
         ctx.profile(False)
         per.append(ms / max(n, 1))
     stop.set()
     th.join()
-    print(f"chain ms/launch: median {statistics.median(per):.4f} min {min(per):.4f} "
-          f"(reps {reps}, sm clock median {statistics.median(clocks) if clocks else 0} MHz)")
+    clk = statistics.median(clocks) if clocks else 0
+    if cfg == "c4":
+        print(f"chain ms/launch: median {statistics.median(per):.4f} min {min(per):.4f} "
+              f"(reps {reps}, sm clock median {clk} MHz)")
+    else:
+        parts = " ".join(f"{f} {statistics.median(v):.2f}" for f, v in fam.items())
+        tot = statistics.median([sum(v[i] for v in fam.values()) for i in range(reps)])
+        print(f"c5 ms/window: total {tot:.2f} | {parts} (reps {reps}, sm clock median {clk} MHz)")
 
 
 if __name__ == "__main__":
