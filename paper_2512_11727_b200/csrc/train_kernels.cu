@@ -82,7 +82,7 @@ __global__ void k_chain_rows(LDims g, uint64_t seed, const int* job_ids, const i
 }
 
 struct Layout {
-  uint32_t x, sc, dlb, ones, w2i, dl, recv, w2, b1, b2, b2p, rows, labs, loss, bars, tmem, total;
+  uint32_t x, sc, dlb, ones, w2i, dl, recv, w2, b1, b2, rows, labs, loss, bars, tmem, total;
 };
 
 // sc: the bf16 W1 operand (MN-major: F rows of 64 hidden units, 128 B); R
@@ -111,8 +111,6 @@ __host__ __device__ inline Layout layout(int F) {
   o += kHS * 4u;
   L.b2 = o;
   o += kC * 4u;
-  L.b2p = o;
-  o += 8u * kC * 4u;  // db2 partial sums of 8 row blocks
   L.rows = o;
   o += 2u * kB * 8u;
   L.labs = o;
@@ -141,6 +139,12 @@ __device__ __forceinline__ void st_async_v4(uint32_t addr, float a, float b, flo
       "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
           addr),
       "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void st_async_v2b32(uint32_t addr, uint32_t a, uint32_t b, uint32_t mbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+      "r"(a), "r"(b), "r"(mbar)
       : "memory");
 }
 __device__ __forceinline__ void st_async_f32(uint32_t addr, float a, uint32_t mbar) {
@@ -234,8 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sDLb = smem + L.dlb;
   uint8_t* sW2i = smem + L.w2i;
   uint8_t* sOnes = smem + L.ones;
-  float* sB2p = (float*)(smem + L.b2p);
-  float* sDL = (float*)(smem + L.dl);
+  float* sB2r = (float*)(smem + L.dl);  // [kB / 8][kC] db2 partial sums of 8-row blocks
   float* sRecv = (float*)(smem + L.recv);
   float* sW2 = (float*)(smem + L.w2);
   float* sB1 = (float*)(smem + L.b1);
@@ -272,7 +275,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int32_t* jrows = a.rows + (size_t)j * a.max_steps * kB;
   const int32_t* jlabs = a.labs + (size_t)j * a.max_steps * kB;
   const uint32_t recv_bytes = kB * kC * 4u;
-  const uint32_t dl_bytes = kB * kC * 4u + (r == 0 ? kB * 4u : 0u);
+  // bf16 dL rows + the 8-row db2 partials (+ every row's loss on rank 0)
+  const uint32_t dl_bytes = kB * 32u + (kB / 8) * kC * 4u + (r == 0 ? kB * 4u : 0u);
 
   // rows of buffer `buf`, 16-byte pieces [c0, c0 + n) of each row (n a power
   // of two) -> X tile, by threads [t0, kThreads); a warp covers consecutive
@@ -286,16 +290,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int i = pc >> lsh, c16 = c0 + (pc & (n - 1));
       cp_async16_s(xsm + (c16 >> 3) * 16384 + i * 128 + (((c16 & 7) ^ (i & 7)) << 4),
                    a.frames + (int64_t)rows[i] * F + c16 * 8);
-    }
-  };
-  // db2 partial sums: thread (block of 16 rows, class), threads kB..
-  auto db2_partial = [&]() {
-    if (tid >= kB) {
-      const int c = tid & (kC - 1), blk = (tid - kB) >> 4;
-      float acc = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) acc = __fadd_rn(acc, sDL[(blk * 16 + i) * kC + c]);
-      sB2p[blk * kC + c] = acc;
     }
   };
   auto build_w2i = [&]() {
@@ -475,9 +469,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     __fmul_rn(__fsub_rn(__fmul_rn(e.y, inv), y == 1 ? 1.0f : 0.0f), invB),
                                     __fmul_rn(__fsub_rn(__fmul_rn(e.z, inv), y == 2 ? 1.0f : 0.0f), invB),
                                     __fmul_rn(__fsub_rn(__fmul_rn(e.w, inv), y == 3 ? 1.0f : 0.0f), invB));
-      for (int d = 0; d < cs; ++d)
-        st_async_v4(mapa_shared(smem_u32(sDL + row * kC + cq * 4), (uint32_t)d), dl.x, dl.y, dl.z,
-                    dl.w, mapa_shared(smem_u32(dl_full), (uint32_t)d));
+      // bf16 dL straight into every CTA's MMA operand tile, and the fp32 db2
+      // partial of this warp's 8 rows (fixed butterfly over the row lanes)
+      const uint32_t lo = pack_bf16x2(dl.x, dl.y), hi = pack_bf16x2(dl.z, dl.w);
+      float4 b2s = dl;
+#pragma unroll
+      for (int x = 4; x < 32; x <<= 1)
+        b2s = make_float4(__fadd_rn(b2s.x, __shfl_xor_sync(0xffffffffu, b2s.x, x)),
+                          __fadd_rn(b2s.y, __shfl_xor_sync(0xffffffffu, b2s.y, x)),
+                          __fadd_rn(b2s.z, __shfl_xor_sync(0xffffffffu, b2s.z, x)),
+                          __fadd_rn(b2s.w, __shfl_xor_sync(0xffffffffu, b2s.w, x)));
+      const uint32_t dlo = dlb_off(row, cq >> 1) + (cq & 1) * 8u;
+      for (int d = 0; d < cs; ++d) {
+        const uint32_t bar = mapa_shared(smem_u32(dl_full), (uint32_t)d);
+        st_async_v2b32(mapa_shared(smem_u32(sDLb) + dlo, (uint32_t)d), lo, hi, bar);
+        if ((lane >> 2) == 0)
+          st_async_v4(mapa_shared(smem_u32(sB2r + (row >> 3) * kC + cq * 4), (uint32_t)d), b2s.x,
+                      b2s.y, b2s.z, b2s.w, bar);
+      }
       if (y >= 0 && y < 4) {
         const float ly = y == 0 ? lg.x : y == 1 ? lg.y : y == 2 ? lg.z : lg.w;
         st_async_f32(mapa_shared(smem_u32(sLoss + row), 0u), __logf(sum) - (ly - m),
@@ -499,25 +508,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(dl_full, ph);
 
-    // ------------------------------ bf16 dL -> dL.W2^T and dW2 = R^T.dL --
-    if (p == 0) {
-      const float4* d4 = reinterpret_cast<const float4*>(sDL + s * kC);
-#pragma unroll
-      for (int ch = 0; ch < 2; ++ch) {
-        const float4 u = d4[2 * ch], v = d4[2 * ch + 1];
-        uint4 pk;
-        pk.x = pack_bf16x2(u.x, u.y);
-        pk.y = pack_bf16x2(u.z, u.w);
-        pk.z = pack_bf16x2(v.x, v.y);
-        pk.w = pack_bf16x2(v.z, v.w);
-        *reinterpret_cast<uint4*>(sDLb + dlb_off(s, ch)) = pk;
-      }
-    }
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+    // ------------------------------------- dL.W2^T and dW2 = R^T.dL --
+    // (the owners wrote the bf16 dL tile with st.async: no local pass)
     if (warp == 0) {
+      fence_async_smem();
+      tc_fence_after();
       if (elect_one()) {
         mma_bf16_ss(tmem + acol, smem_desc(smem_u32(sDLb), 16, 256, kSwizzle32B),
                     desc_mnmajor_sw128(smem_u32(sW2i), 16384, 1024), idh, 0);
@@ -640,14 +635,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       sB1[s] = __fadd_rn(sB1[s], __uint_as_float(v[0]));
     }
-    db2_partial();
-    __syncthreads();  // sW2 updated, db2 partials written
+    __syncthreads();  // sW2 updated
     build_w2i();
     if (tid >= 32 && tid < 32 + kC) {
       const int c = tid - 32;
-      float acc = sB2p[c];
+      float acc = sB2r[c];
 #pragma unroll
-      for (int b = 1; b < 8; ++b) acc = __fadd_rn(acc, sB2p[b * kC + c]);
+      for (int b = 1; b < kB / 8; ++b) acc = __fadd_rn(acc, sB2r[b * kC + c]);
       sB2[c] = __fmaf_rn(-lr, acc, sB2[c]);
     }
     fence_async_smem();  // the W2 operand -> next step's MMAs
