@@ -248,7 +248,7 @@ def run_b200(args, rank, world, local_rank):
             dist.all_gather(list(out.unbind(0)), t)
         return out.reshape(world * wl.gb, DEPTH + 1).cpu().numpy()
 
-    def step(w, timed=False):
+    def step(w, timed=False, mid=None):
         with torch.cuda.stream(stream):
             if timed:
                 ev["a"].record(stream)
@@ -269,6 +269,8 @@ def run_b200(args, rank, world, local_rank):
                                      best_acc.data_ptr(), n_blocks=world)
             if timed:
                 ev["b"].record(stream)
+            if mid is not None:
+                mid()  # (e2e: this window's rings become current here)
             if wl.local:
                 ctx.train_prepared(prep, GPU_S, DEPTH, window=w, out=acc_host)
             # the allocator's decisions over EVERY group: trajectories
@@ -507,7 +509,7 @@ def roofline(kst, pk, pk_kind, args):
 
 def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev, prep):
     """Frames uploaded from pinned host memory and results read back every step."""
-    import paper_2512_11727_b200 as ecco  # noqa: F401
+    import paper_2512_11727_b200 as ecco
     R, S, F = DIMS["ring_frames"], DIMS["eval_samples"], DIMS["feat_dim"]
     fr = torch.empty((wl.N, R, F), dtype=torch.int16, pin_memory=True)
     lb = torch.empty((wl.N, R), dtype=torch.int32, pin_memory=True)
@@ -535,26 +537,36 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev, prep):
     ptrs = (fr[c0].data_ptr() if c1 > c0 else fr.data_ptr(), lb[c0].data_ptr() if c1 > c0 else lb.data_ptr(),
             wl.N, evf.data_ptr(), evl.data_ptr())
 
-    def stage(w):
-        if args.e2e_full_rings or not wl.local:
-            ctx.stage_frames_range_host_ptr(c0, c1 - c0, *ptrs)
-        else:
-            ctx.stage_sampled_host_ptr(prep, GPU_S, DEPTH, w, fr.data_ptr(), lb.data_ptr(), wl.N,
-                                       evf.data_ptr(), evl.data_ptr())
+    def stage_eval():
+        ctx.stage_frames_range_host_ptr(0, 0, fr.data_ptr(), lb.data_ptr(), wl.N, evf.data_ptr(),
+                                        evl.data_ptr())
 
-    # double-buffered ingest: window k+1's frames stream in on the copy
-    # stream while window k's kernels run (every window's copy is inside the
-    # region)
-    stage(10_000)
-    ctx.swap_frames()
+    def stage_rings(w):
+        if args.e2e_full_rings or not wl.local:
+            ctx.stage_frames_range_host_ptr(c0, c1 - c0, ptrs[0], ptrs[1], 0, 0, 0)
+        else:
+            ctx.stage_sampled_host_ptr(prep, GPU_S, DEPTH, w, fr.data_ptr(), lb.data_ptr(), 0, 0, 0)
+
+    # double-buffered ingest in two parts on the copy stream: window k+1's
+    # eval sets stream in during window k and become current at window k+1's
+    # start (its regroup reads them); its rings (the drawn rows) stream in
+    # during window k+1's regroup and become current between that regroup
+    # and its SGD chains.  Window 0's eval sets are the only unoverlapped copy.
+    stage_eval()
+    ctx.swap_frame_parts(ecco.FRAMES_EVAL)
+    stage_rings(10_000)
     for k in range(steps):
         if k + 1 < steps:
-            stage(10_000 + k + 1)
-        step(10_000 + k)
+            stage_eval()
+        step(10_000 + k, mid=lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS))
+        if k + 1 < steps:
+            stage_rings(10_000 + k + 1)
+        if os.environ.get("ECCO_E2E_TRACE"):
+            print(f"e2e window {k}: host {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
         with torch.cuda.stream(stream):
             best_host.copy_(best_dev, non_blocking=True)  # group assignments back to the host
         if k + 1 < steps:
-            ctx.swap_frames()
+            ctx.swap_frame_parts(ecco.FRAMES_EVAL)
     ctx.synchronize()
     el_s = time.perf_counter() - t0
     h1, d1 = ctx.transfer_bytes()
@@ -570,10 +582,12 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev, prep):
                        "ecco_stage_sampled_frames: the ring rows this rank's SGD steps draw, marked "
                        "on the device and read zero-copy over PCIe (rows never drawn are not "
                        "transferred)")
-                    + ", all labels and every camera's eval set; double-buffered so window k+1 "
-                    "uploads while window k computes (ecco_swap_frames) + the step + "
-                    "assignments/accuracies read back; wall clock with a device synchronize at the "
-                    "end, window 0's unoverlapped upload included"),
+                    + ", all labels and every camera's eval set; double-buffered in two parts "
+                    "(ecco_swap_frame_parts): window k+1's eval sets upload during window k and "
+                    "its rings from window k's mid-point, current at window k+1's start / before "
+                    "its SGD chains + the step + assignments/accuracies read back; wall clock with "
+                    "a device synchronize at the end, window 0's unoverlapped eval-set upload "
+                    "included"),
             "pcie_gbs": (h1 - h0) / steps / (el_s / steps) / 1e9}
 
 

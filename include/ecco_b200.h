@@ -152,6 +152,14 @@ ecco_status ecco_stage_frames(ecco_ctx* ctx, int n_cams, const uint16_t* frames,
                               const int32_t* labels, const uint16_t* eval_frames,
                               const int32_t* eval_labels);
 ecco_status ecco_swap_frames(ecco_ctx* ctx);
+/* The two parts of the staged ingest swap independently: bit 0 the frame
+ * rings + their labels (what the SGD steps read), bit 1 the eval sets + their
+ * labels (what the evaluation matrix and member evaluations read).  A staging
+ * call stages the parts it copies (rings when ring cameras or sampled rows
+ * are given, eval when n_eval > 0); ecco_swap_frames swaps every staged part,
+ * ecco_swap_frame_parts the requested ones, so a window's eval sets can
+ * become current for the regroup while its rings still stream in. */
+ecco_status ecco_swap_frame_parts(ecco_ctx* ctx, int parts);
 /* Group-sharded variant of ecco_stage_frames: the frame rings of cameras
  * [ring_first, ring_first + ring_n) only (the members of this rank's groups:
  * a job trains on its own members' frames, orchestrator.cpp:52-62, 282-309)

@@ -94,12 +94,15 @@ class SimOptions(C.Structure):
 _lib = None
 
 # Every symbol include/ecco_b200.h declares (checked by tests/test_abi.py).
+# ecco_swap_frame_parts masks
+FRAMES_RINGS, FRAMES_EVAL = 1, 2
+
 EXPORTS = [
     "ecco_default_config", "ecco_create", "ecco_destroy", "ecco_last_error",
     "ecco_kernel_launches", "ecco_profile", "ecco_kernel_stat", "ecco_transfer_bytes", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
     "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
     "ecco_read_frames", "ecco_stage_frames", "ecco_stage_frames_range", "ecco_stage_sampled_frames",
-    "ecco_swap_frames",
+    "ecco_swap_frames", "ecco_swap_frame_parts",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
@@ -338,6 +341,11 @@ class Context:
 
     def swap_frames(self):
         self._check(lib().ecco_swap_frames(self._h))
+
+    def swap_frame_parts(self, parts):
+        """ecco_swap_frame_parts: FRAMES_RINGS (rings + labels) and/or
+        FRAMES_EVAL (eval sets + labels) of the staged ingest become current."""
+        self._check(lib().ecco_swap_frame_parts(self._h, int(parts)))
 
     def upload_frames_dev(self, n_cams, frames_ptr, labels_ptr, eval_ptr, eval_labels_ptr):
         self._check(lib().ecco_upload_frames_dev(self._h, int(n_cams), C.c_void_p(frames_ptr),

@@ -1,6 +1,7 @@
 // C-ABI of include/ecco_b200.h: argument validation with the reference's
 // error semantics, host <-> device staging, and dispatch to the parametric
 // (param_kernels.cu) or learned (learned_kernels.cu, tc_kernels.cu) backend.
+#include <cstring>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <string.h>
@@ -46,12 +47,16 @@ void free_all(ecco_ctx* c) {
   for (auto& b : c->train_scratch) b.release();
   for (auto& b : c->hscratch) b.release();
   for (auto& b : c->zc_args) b.release();
+  c->zc_host.release();
+  if (c->zc_host_free) cudaEventDestroy(c->zc_host_free);
   for (auto& b : c->traj_args) b.release();
   for (auto& b : c->em_args) b.release();
   c->zc_flags.release();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-  if (c->copy_done) cudaEventDestroy(c->copy_done);
-  if (c->back_free) cudaEventDestroy(c->back_free);
+  for (int i = 0; i < 2; ++i) {
+    if (c->copy_done[i]) cudaEventDestroy(c->copy_done[i]);
+    if (c->back_free[i]) cudaEventDestroy(c->back_free[i]);
+  }
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -334,20 +339,36 @@ ecco_status ecco_stage_frames(ecco_ctx* ctx, int n, const uint16_t* frames, cons
 
 // Back buffers + copy stream of the double-buffered ingest (first use); the
 // copy stream then waits until kernels of the previous window stop reading
-// the back buffer.
-void open_back_buffers(ecco_ctx* ctx) {
+// the back buffers of the parts about to be staged (bit 0 rings, bit 1 eval).
+void open_back_buffers(ecco_ctx* ctx, int parts) {
   const ecco_config& g = ctx->cfg;
   if (!ctx->copy_stream) {
     ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-    ECCO_CUDA(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
-    ECCO_CUDA(cudaEventCreateWithFlags(&ctx->back_free, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->copy_done[i], cudaEventDisableTiming));
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->back_free[i], cudaEventDisableTiming));
+    }
     const size_t fr = (size_t)g.max_cameras * g.ring_frames, ev = (size_t)g.max_cameras * g.eval_samples;
     dalloc(&ctx->b_frames, fr * g.feat_dim);
     dalloc(&ctx->b_labels, fr);
     dalloc(&ctx->b_eval, ev * g.feat_dim);
     dalloc(&ctx->b_eval_labels, ev);
   }
-  if (ctx->back_busy) ECCO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->back_free, 0));
+  for (int i = 0; i < 2; ++i) {
+    if (!((parts >> i) & 1)) continue;
+    ECCO_REQUIRE(!ctx->staged[i], i == 0 ? "stage_frames: staged rings not swapped in yet"
+                                         : "stage_frames: staged eval sets not swapped in yet");
+    if (ctx->back_busy[i]) ECCO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->back_free[i], 0));
+  }
+}
+
+// Marks `parts` staged once the copies enqueued so far on the copy stream land.
+void staged_parts(ecco_ctx* ctx, int parts) {
+  for (int i = 0; i < 2; ++i)
+    if ((parts >> i) & 1) {
+      ECCO_CUDA(cudaEventRecord(ctx->copy_done[i], ctx->copy_stream));
+      ctx->staged[i] = true;
+    }
 }
 
 ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint16_t* frames,
@@ -357,9 +378,9 @@ ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint1
     ECCO_REQUIRE(learned(ctx), "stage_frames: learned backend only");
     ECCO_REQUIRE(first >= 0 && n >= 0 && first + n <= ctx->n_cams, "stage_frames: camera range");
     ECCO_REQUIRE(n_eval >= 0 && n_eval <= ctx->n_cams, "stage_frames: eval camera count");
-    ECCO_REQUIRE(!ctx->staged, "stage_frames: previous staging not swapped in");
     const ecco_config& g = ctx->cfg;
-    open_back_buffers(ctx);
+    const int parts = (n > 0 || n_eval == 0 ? 1 : 0) | (n_eval > 0 ? 2 : 0);
+    open_back_buffers(ctx, parts);
     const size_t fr = (size_t)n * g.ring_frames, ev = (size_t)n_eval * g.eval_samples;
     const size_t f0 = (size_t)first * g.ring_frames;
     const cudaMemcpyKind k = cudaMemcpyHostToDevice;
@@ -368,8 +389,7 @@ ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint1
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels + f0, labels, fr * 4, k, ctx->copy_stream));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream));
-    ECCO_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
-    ctx->staged = true;
+    staged_parts(ctx, parts);
   });
 }
 
@@ -381,7 +401,6 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
                                       const uint16_t* eval, const int32_t* eval_labels) {
   return guarded(ctx, [&] {
     ECCO_REQUIRE(learned(ctx), "stage_sampled_frames: learned backend only");
-    ECCO_REQUIRE(!ctx->staged, "stage_sampled_frames: previous staging not swapped in");
     ECCO_REQUIRE(n_jobs >= 0 && depth >= 1 && depth <= ctx->cfg.max_depth,
                  "stage_sampled_frames: depth must be in [1, max_depth]");
     ECCO_REQUIRE(n_eval >= 0 && n_eval <= ctx->n_cams, "stage_sampled_frames: eval camera count");
@@ -393,7 +412,8 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
     void* fdev = nullptr;  // the device address of the pinned ring table
     ECCO_REQUIRE(cudaHostGetDevicePointer(&fdev, (void*)frames, 0) == cudaSuccess,
                  "stage_sampled_frames: frames must be pinned (mapped) host memory");
-    open_back_buffers(ctx);
+    const int parts = 1 | (n_eval > 0 ? 2 : 0);
+    open_back_buffers(ctx, parts);
     cudaStream_t st = ctx->copy_stream;
     if (!ctx->d_zc_rows) {
       dalloc(&ctx->d_zc_rows, 1);
@@ -413,9 +433,22 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
       }
       if (micro_base) mb.assign(micro_base, micro_base + n_jobs);
       const size_t nsrc = std::max(src_off[n_jobs], 1);
+      // the arguments go through a pinned buffer: a pageable copy would make
+      // the host wait for the copy stream (which waits for the previous
+      // window's kernels); the previous call's copies have long read it
+      if (!ctx->zc_host_free)
+        ECCO_CUDA(cudaEventCreateWithFlags(&ctx->zc_host_free, cudaEventDisableTiming));
+      else
+        ECCO_CUDA(cudaEventSynchronize(ctx->zc_host_free));
+      const size_t words_i = 4 * (size_t)n_jobs + 1 + nsrc, bytes_h = words_i * 4 + nsrc * 8 + 64;
+      uint8_t* hb = (uint8_t*)ctx->zc_host.get(bytes_h);
+      size_t ho = 0;
       auto up = [&](int i, const void* h, size_t bytes) {
         void* d = ctx->zc_args[i].get(bytes);
-        ECCO_CUDA(ctx_memcpy(ctx, d, h, bytes, k, st));
+        ho = (ho + 7) & ~(size_t)7;
+        std::memcpy(hb + ho, h, bytes);
+        ECCO_CUDA(ctx_memcpy(ctx, d, hb + ho, bytes, k, st));
+        ho += bytes;
         return d;
       };
       const int* d_j = (const int*)up(0, job_ids, sizeof(int) * n_jobs);
@@ -426,33 +459,52 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
       const int* d_mb = (const int*)up(5, mb.data(), sizeof(int) * n_jobs);
       stage::mark_sampled(ctx, st, n_jobs, d_j, d_st, max_steps, d_so, d_sc, d_sf, d_mb, depth,
                           window, flags);
+      ECCO_CUDA(cudaEventRecord(ctx->zc_host_free, st));
     }
-    ctx->sm_reserve = 2;  // from now on the persistent kernels leave room for the fetch
+    ctx->sm_reserve = 4;  // from now on the persistent kernels leave room for the fetch
     stage::fetch_rows(ctx, st, (const uint16_t*)fdev, ctx->b_frames, flags, words, ctx->d_zc_rows);
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels, labels, rows * 4, k, st));
     const size_t ev = (size_t)n_eval * g.eval_samples;
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, st));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, st));
-    ECCO_CUDA(cudaEventRecord(ctx->copy_done, st));
-    ctx->staged = true;
+    staged_parts(ctx, parts);
   });
+}
+
+static void swap_parts(ecco_ctx* ctx, int parts) {
+  for (int i = 0; i < 2; ++i) {
+    if (!((parts >> i) & 1)) continue;
+    ECCO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->copy_done[i], 0));
+    if (i == 0) {
+      std::swap(ctx->d_frames, ctx->b_frames);
+      std::swap(ctx->d_labels, ctx->b_labels);
+    } else {
+      std::swap(ctx->d_eval, ctx->b_eval);
+      std::swap(ctx->d_eval_labels, ctx->b_eval_labels);
+      delete (CUtensorMap*)ctx->map_x;  // rebuilt over the new eval buffer on next use
+      ctx->map_x = nullptr;
+    }
+    // kernels enqueued so far read the old front (now back): the next
+    // staging copy of this part waits for them
+    ECCO_CUDA(cudaEventRecord(ctx->back_free[i], ctx->stream));
+    ctx->back_busy[i] = true;
+    ctx->staged[i] = false;
+  }
 }
 
 ecco_status ecco_swap_frames(ecco_ctx* ctx) {
   return guarded(ctx, [&] {
-    ECCO_REQUIRE(ctx->staged, "swap_frames: nothing staged");
-    ECCO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->copy_done, 0));
-    std::swap(ctx->d_frames, ctx->b_frames);
-    std::swap(ctx->d_labels, ctx->b_labels);
-    std::swap(ctx->d_eval, ctx->b_eval);
-    std::swap(ctx->d_eval_labels, ctx->b_eval_labels);
-    delete (CUtensorMap*)ctx->map_x;  // rebuilt over the new eval buffer on next use
-    ctx->map_x = nullptr;
-    // kernels enqueued so far read the old front (now back): the next
-    // staging copy waits for them
-    ECCO_CUDA(cudaEventRecord(ctx->back_free, ctx->stream));
-    ctx->back_busy = true;
-    ctx->staged = false;
+    ECCO_REQUIRE(ctx->staged[0] || ctx->staged[1], "swap_frames: nothing staged");
+    swap_parts(ctx, (ctx->staged[0] ? 1 : 0) | (ctx->staged[1] ? 2 : 0));
+  });
+}
+
+ecco_status ecco_swap_frame_parts(ecco_ctx* ctx, int parts) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(parts >= 1 && parts <= 3, "swap_frame_parts: parts is a mask of 1 (rings), 2 (eval)");
+    ECCO_REQUIRE(!(parts & 1) || ctx->staged[0], "swap_frame_parts: rings not staged");
+    ECCO_REQUIRE(!(parts & 2) || ctx->staged[1], "swap_frame_parts: eval sets not staged");
+    swap_parts(ctx, parts);
   });
 }
 

@@ -183,12 +183,16 @@ struct ecco_ctx {
   uint16_t* b_eval = nullptr;
   int32_t* b_eval_labels = nullptr;
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t copy_done = nullptr, back_free = nullptr;
-  bool staged = false, back_busy = false;
+  // per part (0: rings + labels, 1: eval sets + labels): the staged copy's
+  // completion, and the point after which the back buffer is no longer read
+  cudaEvent_t copy_done[2] = {nullptr, nullptr}, back_free[2] = {nullptr, nullptr};
+  bool staged[2] = {false, false}, back_busy[2] = {false, false};
   // sampled-row ingest (ecco_stage_sampled_frames): the window's job
   // arguments on the copy stream, the bitmap of drawn ring rows, and the
   // running count of rows read from host memory over PCIe (zero-copy)
   DevBuf zc_args[6], zc_flags;
+  HostBuf zc_host;                   // pinned staging of those arguments (truly async copies)
+  cudaEvent_t zc_host_free = nullptr;  // the previous argument copy has read zc_host
   DevBuf traj_args[9];  // ecco_train_trajectories' uploaded arguments
   DevBuf em_args[3];    // ecco_eval_matrix(_dev)'s uploaded arguments
   unsigned long long* d_zc_rows = nullptr;

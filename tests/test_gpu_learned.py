@@ -202,6 +202,32 @@ def test_sampled_staging_equals_full_frames(math):
     assert res[0][1] == res[1][1]
 
 
+def test_frame_parts_swap_independently():
+    """ecco_swap_frame_parts: eval sets staged and swapped alone leave the
+    current rings untouched, and rings staged afterwards become current
+    without touching the eval sets."""
+    ctx, orc, rng = setup(seed=8)
+    fr = np.ascontiguousarray(orc.frames)
+    lb = np.ascontiguousarray(orc.labels)
+    ev = np.ascontiguousarray(orc.eval)
+    el = np.ascontiguousarray(orc.eval_labels)
+    z_fr = np.ascontiguousarray(fr ^ np.uint16(1))  # distinct rings and labels
+    z_lb = np.ascontiguousarray((lb + 1) % orc.c.C).astype(lb.dtype)
+    ev2 = np.ascontiguousarray(ev ^ np.uint16(1))  # different eval bits
+    ctx.stage_frames_range_host_ptr(0, 0, fr.ctypes.data, lb.ctypes.data, 6, ev2.ctypes.data,
+                                    el.ctypes.data)
+    with pytest.raises(ecco.EccoError):
+        ctx.swap_frame_parts(ecco.FRAMES_RINGS)  # rings were not staged
+    ctx.swap_frame_parts(ecco.FRAMES_EVAL)
+    gf, gl, ge, gel = ctx.read_frames(6)
+    assert gf.tobytes() == fr.tobytes() and ge.tobytes() == ev2.tobytes()
+    ctx.stage_frames_range_host_ptr(0, 6, z_fr.ctypes.data, z_lb.ctypes.data, 0, 0, 0)
+    ctx.swap_frame_parts(ecco.FRAMES_RINGS)
+    gf, gl, ge, gel = ctx.read_frames(6)
+    assert gf.tobytes() == z_fr.tobytes() and gl.tobytes() == z_lb.tobytes()
+    assert ge.tobytes() == ev2.tobytes() and gel.tobytes() == el.tobytes()
+
+
 def test_learned_simulation_runs_and_groups():
     from paper_2512_11727_b200 import scenarios
     sc = scenarios.synthetic(24, 3, windows=2, micro_windows=8, drift_frac=0.1, local_acc=0.0, seed=3)
