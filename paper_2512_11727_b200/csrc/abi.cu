@@ -410,8 +410,10 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
                      src_fracs + src_off[j]);
     const ecco_config& g = ctx->cfg;
     void* fdev = nullptr;  // the device address of the pinned ring table
-    ECCO_REQUIRE(cudaHostGetDevicePointer(&fdev, (void*)frames, 0) == cudaSuccess,
-                 "stage_sampled_frames: frames must be pinned (mapped) host memory");
+    if (cudaHostGetDevicePointer(&fdev, (void*)frames, 0) != cudaSuccess) {
+      (void)cudaGetLastError();  // not sticky: clear it so later launch checks do not see it
+      ECCO_REQUIRE(false, "stage_sampled_frames: frames must be pinned (mapped) host memory");
+    }
     const int parts = 1 | (n_eval > 0 ? 2 : 0);
     open_back_buffers(ctx, parts);
     cudaStream_t st = ctx->copy_stream;

@@ -228,6 +228,29 @@ def test_frame_parts_swap_independently():
     assert ge.tobytes() == ev2.tobytes() and gel.tobytes() == el.tobytes()
 
 
+def test_sampled_staging_edges():
+    """ecco_stage_sampled_frames rejects a pageable frame table, stages
+    nothing for an empty job list (no rows fetched), and a second staging of
+    a part before its swap is refused."""
+    import torch
+    ctx, orc, rng = setup(seed=12)
+    fr = np.ascontiguousarray(orc.frames)
+    lb = torch.from_numpy(np.ascontiguousarray(orc.labels)).pin_memory()
+    empty = ctx.prepare_trajectories([], [], [], [], [])
+    with pytest.raises(ecco.EccoError, match="pinned"):
+        ctx.stage_sampled_host_ptr(empty, 6.0, 1, 3, fr.ctypes.data, lb.data_ptr(), 0, 0, 0)
+    frp = torch.from_numpy(fr.view(np.int16)).pin_memory()
+    h0, _ = ctx.transfer_bytes()
+    ctx.stage_sampled_host_ptr(empty, 6.0, 1, 3, frp.data_ptr(), lb.data_ptr(), 0, 0, 0)
+    with pytest.raises(ecco.EccoError, match="not swapped"):
+        ctx.stage_sampled_host_ptr(empty, 6.0, 1, 3, frp.data_ptr(), lb.data_ptr(), 0, 0, 0)
+    ctx.swap_frame_parts(ecco.FRAMES_RINGS)
+    h1, _ = ctx.transfer_bytes()
+    assert h1 - h0 == orc.labels.nbytes  # labels only: no row was drawn
+    with pytest.raises(ecco.EccoError, match="nothing staged"):
+        ctx.swap_frames()
+
+
 def test_learned_simulation_runs_and_groups():
     from paper_2512_11727_b200 import scenarios
     sc = scenarios.synthetic(24, 3, windows=2, micro_windows=8, drift_frac=0.1, local_acc=0.0, seed=3)
