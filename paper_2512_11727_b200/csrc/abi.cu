@@ -24,9 +24,11 @@ ecco_status guarded(ecco_ctx* ctx, F&& f) {
     return ECCO_OK;
   } catch (const EccoError& e) {
     if (ctx) ctx->err = e.msg;
+    (void)cudaGetLastError();  // a non-sticky CUDA error must not surface in the next call
     return e.code;
   } catch (const std::exception& e) {
     if (ctx) ctx->err = e.what();
+    (void)cudaGetLastError();
     return ECCO_ERR_RUNTIME;
   }
 }
