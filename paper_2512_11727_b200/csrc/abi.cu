@@ -53,6 +53,7 @@ void free_all(ecco_ctx* c) {
   if (c->zc_host_free) cudaEventDestroy(c->zc_host_free);
   for (auto& b : c->traj_args) b.release();
   for (auto& b : c->em_args) b.release();
+  c->tile_ctr.release();
   c->zc_flags.release();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -465,7 +466,8 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
                           window, flags);
       ECCO_CUDA(cudaEventRecord(ctx->zc_host_free, st));
     }
-    ctx->sm_reserve = 4;  // from now on the persistent kernels leave room for the fetch
+    // (the CTA-pair evaluation kernel schedules its super tiles dynamically:
+    // pairs that cannot start beside the fetch simply take fewer tiles)
     stage::fetch_rows(ctx, st, (const uint16_t*)fdev, ctx->b_frames, flags, words, ctx->d_zc_rows);
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels, labels, rows * 4, k, st));
     const size_t ev = (size_t)n_eval * g.eval_samples;

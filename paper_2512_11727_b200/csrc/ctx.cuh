@@ -195,6 +195,7 @@ struct ecco_ctx {
   cudaEvent_t zc_host_free = nullptr;  // the previous argument copy has read zc_host
   DevBuf traj_args[9];  // ecco_train_trajectories' uploaded arguments
   DevBuf em_args[3];    // ecco_eval_matrix(_dev)'s uploaded arguments
+  DevBuf tile_ctr;      // the CTA-pair evaluation kernel's dynamic super-tile counter
   unsigned long long* d_zc_rows = nullptr;
   // SMs left free by the persistent evaluation kernels while a zero-copy
   // row fetch may be streaming on copy_stream

@@ -88,6 +88,7 @@ struct EvalArgs {
   int stages;
   int nl;                // logits buffers (1 or 2)
   float* dbg_logits;     // optional: [n_rows][n_ent][C] logits + b2 (dense mode tests)
+  int* tile_ctr;         // pair kernel: next super tile (zeroed before the launch)
 };
 
 __device__ __forceinline__ int tile_ent_begin(const EvalArgs& a, int m) {
@@ -397,8 +398,20 @@ struct PairBars {
   uint64_t bias_full[2], bias_empty[2];
   uint64_t z_full[2], z_empty[2], r_full[2], r_empty[2];
   uint64_t l_full[2], l_empty[2];
+  // dynamic super-tile queue: the leader's producer takes the next tile from
+  // a global counter and publishes it to both CTAs (the follower's copy by
+  // st.async); every role walks the queue in order; the leader's tq_empty
+  // collects the releases of both CTAs' consumers
+  uint64_t tq_full[4], tq_empty[4];
+  int tq[4];
   uint32_t tmem_base;
 };
+
+__device__ __forceinline__ void st_async_s32(uint32_t addr, int v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.s32 [%0], %1, [%2];" ::"r"(addr),
+               "r"(v), "r"(mbar)
+               : "memory");
+}
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_eval_pair(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
@@ -442,6 +455,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bars->l_full[b], 1);
       mbar_init(&bars->l_empty[b], 8);
     }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&bars->tq_full[i], 1);
+      mbar_init(&bars->tq_empty[i], 1 + 8 + 8 + 1);  // MMA, 2 x 8 epilogue warps, follower producer
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_pair(&bars->tmem_base, 512);
@@ -453,8 +470,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
     int stage = 0;
-    uint32_t sph = 0, u = 0, t = 0;
-    for (int m = pair; m < n_super; m += npairs, ++t) {
+    uint32_t sph = 0, u = 0;
+    for (uint32_t t = 0;; ++t) {
+      const int qs = t & 3;
+      int m;
+      if (leader) {
+        if (t >= 4) mbar_wait(&bars->tq_empty[qs], ((t >> 2) - 1) & 1);
+        if (lane == 0) {
+          const int g = atomicAdd(a.tile_ctr, 1);
+          m = g < n_super ? g : -1;
+          bars->tq[qs] = m;
+          st_async_s32(mapa_shared(smem_u32(&bars->tq[qs]), 1), m,
+                       mapa_shared(smem_u32(&bars->tq_full[qs]), 1));
+          mbar_arrive(&bars->tq_full[qs]);
+        }
+        m = __shfl_sync(0xffffffffu, m, 0);
+      } else {
+        if (lane == 0) mbar_expect_tx(&bars->tq_full[qs], 4);
+        mbar_wait(&bars->tq_full[qs], (t >> 2) & 1);
+        m = bars->tq[qs];
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(lead(&bars->tq_empty[qs]));
+      }
+      if (m < 0) break;
       if (t > 0) mbar_wait(&bars->a_empty, (t - 1) & 1);
       if (elect_one()) {
         if (leader) mbar_expect_tx(&bars->a_full, 2u * nkc * kAChunk);
@@ -536,7 +574,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       };
-      for (int m = pair; m < n_super; m += npairs, ++t) {
+      for (;; ++t) {
+        const int qs = t & 3;
+        mbar_wait(&bars->tq_full[qs], (t >> 2) & 1);
+        const int m = bars->tq[qs];
+        if (m < 0) break;
         mbar_wait(&bars->a_full, t & 1);
         tc_fence_after();
         for (int e = tile_ent_begin(a, m), e1 = tile_ent_end(a, m); e < e1; ++e, ++u) {
@@ -570,6 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (elect_one()) mma2_commit_mc(&bars->a_empty, 3);
         __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->tq_empty[qs]);
       }
       if (prev >= 0) layer2((uint32_t)prev);
     }
@@ -580,7 +623,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int row = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     uint32_t u = 0;
-    for (int m = pair; m < n_super; m += npairs) {
+    for (uint32_t t = 0;; ++t) {
+      const int qs = t & 3;
+      mbar_wait(&bars->tq_full[qs], (t >> 2) & 1);
+      const int m = bars->tq[qs];
+      if (m < 0) break;
       const int R = m * 2 * kTileRows + (int)rank * kTileRows + row;
       const bool valid = R < a.n_rows;
       const int p = valid ? R / a.S : 0;
@@ -657,6 +704,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const size_t idx = a.probe_slot ? (size_t)p : (size_t)p * a.ld + a.ent_col[e];
           atomicAdd(a.counts + idx, __popc(bal));
         }
+      }
+      __syncwarp();
+      if (lane == 0) {  // this warp is done with the tile's queue slot
+        if (leader)
+          mbar_arrive(&bars->tq_empty[qs]);
+        else
+          mbar_arrive_cluster(lead(&bars->tq_empty[qs]));
       }
     }
   }
@@ -924,6 +978,8 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
     }
     const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
     const int pairs = std::min(n_super, (sm_count(g.device) - ctx->sm_reserve) / 2);
+    a.tile_ctr = (int*)ctx->tile_ctr.get(sizeof(int));
+    ECCO_CUDA(cudaMemsetAsync(a.tile_ctr, 0, sizeof(int), ctx->stream));
     ECCO_TIMED(ctx, kind, flops, bytes,
                (k_eval_pair<<<2 * pairs, kThreads, psmem, ctx->stream>>>(
                    *(const CUtensorMap*)ctx->map_x, *(const CUtensorMap*)sh.map_w_pair,

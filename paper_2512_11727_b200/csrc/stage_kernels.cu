@@ -98,9 +98,9 @@ void fetch_rows(ecco_ctx* ctx, cudaStream_t st, const uint16_t* host_dev, uint16
   if (n_words == 0) return;
   ECCO_REQUIRE(n_words * 32 * (ctx->cfg.feat_dim / 8) < (1ull << 32),
                "sampled-row fetch: ring table too large for 32-bit piece offsets");
-  // two CTAs (64 warps, 6 pieces in flight per lane): whatever two SMs they
-  // land on, the CTA-pair evaluation kernel keeps 72 whole TPCs
-  // (ctx->sm_reserve = 4 while a fetch may run, eval_kernels.cu)
+  // two CTAs (64 warps, 6 pieces in flight per lane) beside whatever runs;
+  // the CTA-pair evaluation kernel takes its super tiles from a counter, so
+  // a pair that starts late (its TPC hosts a fetch CTA) just takes fewer
   k_fetch_rows<<<2, 1024, 0, st>>>(reinterpret_cast<const uint4*>(host_dev),
                                    reinterpret_cast<uint4*>(dst), d_flags, n_words,
                                    ctx->cfg.feat_dim / 8, d_count);
