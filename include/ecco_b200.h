@@ -300,8 +300,9 @@ ecco_status ecco_train_trajectories(
  * first n_eval cameras' eval sets are copied as in ecco_stage_frames.  Rows
  * the trajectories never draw are not transferred (their back-buffer slots
  * are stale), so the trajectories' results equal a full upload's.  Counts
- * the rows read into ecco_transfer_bytes.  While such a fetch may run, the
- * persistent evaluation kernels leave two SMs free.  Replaces, for the
+ * the rows read into ecco_transfer_bytes.  The fetch runs as two CTAs
+ * beside the window's kernels (the CTA-pair evaluation kernel schedules its
+ * tiles dynamically around them).  Replaces, for the
  * learned path, the per-window frame delivery the reference models as
  * TrainingBatchStats (accuracy_model.hpp:36-44). */
 ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_ids,

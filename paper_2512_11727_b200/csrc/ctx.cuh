@@ -197,9 +197,6 @@ struct ecco_ctx {
   DevBuf em_args[3];    // ecco_eval_matrix(_dev)'s uploaded arguments
   DevBuf tile_ctr;      // the CTA-pair evaluation kernel's dynamic super-tile counter
   unsigned long long* d_zc_rows = nullptr;
-  // SMs left free by the persistent evaluation kernels while a zero-copy
-  // row fetch may be streaming on copy_stream
-  int sm_reserve = 0;
 
   // fused evaluation: shadows of the committed models (refreshed lazily for
   // slots marked dirty) and of the speculative snapshot being evaluated

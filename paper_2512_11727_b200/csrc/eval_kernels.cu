@@ -977,7 +977,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
       pattr = true;
     }
     const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
-    const int pairs = std::min(n_super, (sm_count(g.device) - ctx->sm_reserve) / 2);
+    const int pairs = std::min(n_super, sm_count(g.device) / 2);
     a.tile_ctr = (int*)ctx->tile_ctr.get(sizeof(int));
     ECCO_CUDA(cudaMemsetAsync(a.tile_ctr, 0, sizeof(int), ctx->stream));
     ECCO_TIMED(ctx, kind, flops, bytes,
@@ -987,7 +987,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
     ECCO_LAUNCHED(ctx);
     return;
   }
-  const int grid = std::min(a.n_tiles, sm_count(g.device) - ctx->sm_reserve);
+  const int grid = std::min(a.n_tiles, sm_count(g.device));
   ECCO_TIMED(ctx, kind, flops, bytes,
              (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
                                                                   *(const CUtensorMap*)sh.map_w, a)));
