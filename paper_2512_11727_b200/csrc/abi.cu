@@ -20,6 +20,9 @@ namespace {
 template <class F>
 ecco_status guarded(ecco_ctx* ctx, F&& f) {
   try {
+    // every call runs on the context's device, whatever the calling thread
+    // had current (several contexts on different GPUs in one process)
+    if (ctx) ECCO_CUDA(cudaSetDevice(ctx->cfg.device));
     f();
     return ECCO_OK;
   } catch (const EccoError& e) {

@@ -950,11 +950,11 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
   a.stages = (int)std::min<size_t>(kMaxStages, (max_smem - fixed) / kBoxBytes);
   ECCO_REQUIRE(a.stages >= 2, "fused eval: shared memory too small for the pipeline");
   const size_t smem = fixed + (size_t)a.stages * kBoxBytes;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned attr = 0;  // per device: the attribute applies to the current device
+  if (!((attr >> (g.device & 31)) & 1u)) {
     ECCO_CUDA(cudaFuncSetAttribute(k_eval_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)max_smem));
-    attr = true;
+    attr |= 1u << (g.device & 31);
   }
   if (a.n_tiles == 0 || n_ent == 0) return;
   const double flops = 2.0 * live_pairs * g.eval_samples *
@@ -970,11 +970,11 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
     a.stages = (int)std::min<size_t>(kMaxPairStages, (max_smem - pfixed) / kPairBox);
     ECCO_REQUIRE(a.stages >= 2, "fused eval (pair): shared memory too small for the pipeline");
     const size_t psmem = pfixed + (size_t)a.stages * kPairBox;
-    static bool pattr = false;
-    if (!pattr) {
+    static unsigned pattr = 0;
+    if (!((pattr >> (g.device & 31)) & 1u)) {
       ECCO_CUDA(cudaFuncSetAttribute(k_eval_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)max_smem));
-      pattr = true;
+      pattr |= 1u << (g.device & 31);
     }
     const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
     const int pairs = std::min(n_super, sm_count(g.device) / 2);

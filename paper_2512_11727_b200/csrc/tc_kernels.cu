@@ -517,9 +517,9 @@ int pick_nt(int H, int ctas_per_nt1) {
 
 size_t smem_bytes(int NT) { return 32768 + 2 * (size_t)NT * kKC * 4; }
 
-void set_smem_attrs() {
-  static bool done = false;
-  if (done) return;
+void set_smem_attrs(int device) {  // per device: the attribute applies to the current device
+  static unsigned done = 0;
+  if ((done >> (device & 31)) & 1u) return;
   const int mx = (int)smem_bytes(256);
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -527,7 +527,7 @@ void set_smem_attrs() {
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  done = true;
+  done |= 1u << (device & 31);
 }
 
 }  // namespace
@@ -542,7 +542,7 @@ void fwd_hidden(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, co
   const int NT = pick_nt(H, n_tiles);
   FwdArgs a{xbase, row_off, tiles, steps, step, wbase, wstride, Z, F, H, NT};
   const size_t sm = smem_bytes(NT);
-  set_smem_attrs();
+  set_smem_attrs(ctx->cfg.device);
   const int kind = steps ? ECCO_KSTAT_TRAIN_STEP : ECCO_KSTAT_EVAL_MATRIX;
   const dim3 grid(n_tiles, H / NT);
   ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 4,
@@ -562,11 +562,11 @@ void fwd_hidden_bf16(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_of
   const CUtensorMap map = fused::tensor_map_bf16(w1t, n_slots * H, F, kBfNT);
   FwdBfArgs a{xbase, row_off, tiles, steps, step, wbase, wstride, Z, F, H};
   const size_t sm = kBfStages * (size_t)(kBfA + kBfB);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned attr = 0;  // per device
+  if (!((attr >> (ctx->cfg.device & 31)) & 1u)) {
     ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
-    attr = true;
+    attr |= 1u << (ctx->cfg.device & 31);
   }
   const int kind = steps ? ECCO_KSTAT_TRAIN_STEP : ECCO_KSTAT_EVAL_MATRIX;
   ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 2,
@@ -582,7 +582,7 @@ void dw1_update(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_off, co
   const int NT = pick_nt(H, n_jobs * (F / kM));
   Dw1Args a{xbase, row_off, slots, steps, step, wbase, wstride, DH, F, H, B, NT, ctx->cfg.sgd_lr, w1t};
   const size_t sm = smem_bytes(NT);
-  set_smem_attrs();
+  set_smem_attrs(ctx->cfg.device);
   ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_DW1, 2.0 * live_jobs * F * H * B,
              (double)live_jobs * (B * F * 2.0 + B * H * 4.0 + 2.0 * F * H * 4),
              (NT == 256   ? k_tc_dw1<256><<<dim3(F / kM, H / NT, n_jobs), kThreads, sm, ctx->stream>>>(a)
