@@ -309,16 +309,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   constexpr int kA = kKC * (kM / 4) / kThreads, kBv = kKC * (NT / 4) / kThreads;
   uint2 ra[kA];
   float4 rb[kBv];
+  // element e -> (K index k, MN group of 4): within a warp the lanes cover
+  // 4 consecutive k x 8 consecutive groups (lane bits 0-1: k, 2-4: group),
+  // so every scalar store of kmajor_put4 hits 8 banks (4-way), not 2
+  // (16-way), and the global loads stay contiguous 64 / 128-byte runs
+  auto kidx = [](int e) { return 4 * ((e >> 5) & 7) + (e & 3); };
+  auto gidx = [](int e) { return 8 * (e >> 8) + 2 * ((e >> 3) & 3) + ((e >> 2) & 1); };
   auto load = [&](int kc) {
     const int k0 = kc * kKC;
 #pragma unroll
     for (int u = 0; u < kA; ++u) {
-      const int e = tid + u * kThreads, k = e / (kM / 4), m4 = e % (kM / 4);
+      const int e = tid + u * kThreads, k = kidx(e), m4 = gidx(e);
       ra[u] = *reinterpret_cast<const uint2*>(a.xbase + a.row_off[r0 + k0 + k] + f0 + m4 * 4);
     }
 #pragma unroll
     for (int u = 0; u < kBv; ++u) {
-      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
+      const int e = tid + u * kThreads, k = kidx(e), n4 = gidx(e);
       rb[u] = *reinterpret_cast<const float4*>(a.DH + (r0 + k0 + k) * a.H + n0 + n4 * 4);
     }
   };
@@ -329,13 +335,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
     // A = X^T (element (f, s)), B = dH^T (element (h, s)), both K-major
 #pragma unroll
     for (int u = 0; u < kA; ++u) {
-      const int e = tid + u * kThreads, k = e / (kM / 4), m4 = e % (kM / 4);
-      kmajor_put4(sA[s], m4 * 4, k, bf16x4_to_f32(ra[u]));
+      const int e = tid + u * kThreads;
+      kmajor_put4(sA[s], gidx(e) * 4, kidx(e), bf16x4_to_f32(ra[u]));
     }
 #pragma unroll
     for (int u = 0; u < kBv; ++u) {
-      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
-      kmajor_put4(sB[s], n4 * 4, k, rb[u]);
+      const int e = tid + u * kThreads;
+      kmajor_put4(sB[s], gidx(e) * 4, kidx(e), rb[u]);
     }
     if (kc + 1 < nk) load(kc + 1);
     fence_async_smem();
