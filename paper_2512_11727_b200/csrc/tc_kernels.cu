@@ -137,6 +137,16 @@ __device__ __forceinline__ void kmajor_put4(float* tile, int r, int k, float4 v)
   }
 }
 
+// Element e of a K-major staging pass (kKC = 32 K indices x groups of 4
+// MN rows) -> (K index, MN group): within a warp the lanes cover 4
+// consecutive K x 8 consecutive groups (lane bits 0-1: K, 2-4: group), so
+// every scalar store of kmajor_put4 hits 8 banks (4-way) instead of 2
+// (16-way), and the global loads stay contiguous 64- / 128-byte runs.
+__device__ __forceinline__ int stage_k(int e) { return 4 * ((e >> 5) & 7) + (e & 3); }
+__device__ __forceinline__ int stage_g(int e) {
+  return 8 * (e >> 8) + 2 * ((e >> 3) & 3) + ((e >> 2) & 1);
+}
+
 __device__ __forceinline__ float4 bf16x4_to_f32(uint2 p) {
   return make_float4(__uint_as_float(p.x << 16), __uint_as_float(p.x & 0xFFFF0000u),
                      __uint_as_float(p.y << 16), __uint_as_float(p.y & 0xFFFF0000u));
@@ -198,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < kBv; ++u) {
-      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
+      const int e = tid + u * kThreads, k = stage_k(e), n4 = stage_g(e);
       rb[u] = *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + k) * a.H + n0 + n4 * 4);
     }
   };
@@ -214,8 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < kBv; ++u) {
-      const int e = tid + u * kThreads, k = e / (NT / 4), n4 = e % (NT / 4);
-      kmajor_put4(sB[s], n4 * 4, k, rb[u]);
+      const int e = tid + u * kThreads;
+      kmajor_put4(sB[s], stage_g(e) * 4, stage_k(e), rb[u]);
     }
     if (kc + 1 < nk) load(kc + 1);
     fence_async_smem();
@@ -309,22 +319,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   constexpr int kA = kKC * (kM / 4) / kThreads, kBv = kKC * (NT / 4) / kThreads;
   uint2 ra[kA];
   float4 rb[kBv];
-  // element e -> (K index k, MN group of 4): within a warp the lanes cover
-  // 4 consecutive k x 8 consecutive groups (lane bits 0-1: k, 2-4: group),
-  // so every scalar store of kmajor_put4 hits 8 banks (4-way), not 2
-  // (16-way), and the global loads stay contiguous 64 / 128-byte runs
-  auto kidx = [](int e) { return 4 * ((e >> 5) & 7) + (e & 3); };
-  auto gidx = [](int e) { return 8 * (e >> 8) + 2 * ((e >> 3) & 3) + ((e >> 2) & 1); };
   auto load = [&](int kc) {
     const int k0 = kc * kKC;
 #pragma unroll
     for (int u = 0; u < kA; ++u) {
-      const int e = tid + u * kThreads, k = kidx(e), m4 = gidx(e);
+      const int e = tid + u * kThreads, k = stage_k(e), m4 = stage_g(e);
       ra[u] = *reinterpret_cast<const uint2*>(a.xbase + a.row_off[r0 + k0 + k] + f0 + m4 * 4);
     }
 #pragma unroll
     for (int u = 0; u < kBv; ++u) {
-      const int e = tid + u * kThreads, k = kidx(e), n4 = gidx(e);
+      const int e = tid + u * kThreads, k = stage_k(e), n4 = stage_g(e);
       rb[u] = *reinterpret_cast<const float4*>(a.DH + (r0 + k0 + k) * a.H + n0 + n4 * 4);
     }
   };
@@ -336,12 +340,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
 #pragma unroll
     for (int u = 0; u < kA; ++u) {
       const int e = tid + u * kThreads;
-      kmajor_put4(sA[s], gidx(e) * 4, kidx(e), bf16x4_to_f32(ra[u]));
+      kmajor_put4(sA[s], stage_g(e) * 4, stage_k(e), bf16x4_to_f32(ra[u]));
     }
 #pragma unroll
     for (int u = 0; u < kBv; ++u) {
       const int e = tid + u * kThreads;
-      kmajor_put4(sB[s], gidx(e) * 4, kidx(e), rb[u]);
+      kmajor_put4(sB[s], stage_g(e) * 4, stage_k(e), rb[u]);
     }
     if (kc + 1 < nk) load(kc + 1);
     fence_async_smem();
