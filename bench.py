@@ -336,7 +336,7 @@ def run_b200(args, rank, world, local_rank):
 
     if rank == 0:
         pk, pk_kind = peaks()
-        roof = roofline(kst, pk, pk_kind, args)
+        roof = roofline(kst, pk, pk_kind, args, fused=chain)
         line = {
             "metric": "group-retrain samples/s (per-window regroup + retrain)",
             "value": samples / (ms / 1e3),
@@ -467,31 +467,40 @@ def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
     return out
 
 
-def kernel_roofline(name, stat, pk, pk_kind, args, traffic=None):
+def kernel_roofline(name, stat, pk, pk_kind, args, traffic=None, fused=True):
     """Roofline of one kernel family from its CUDA-event stats (launches, ms,
-    algorithmic flops, algorithmic bytes).  The tensor-core kernels run bf16
-    kind::f16 MMAs under TC math; a kernel that fills most of a long step is
-    held to the SUSTAINED bf16 peak (MEASURED_PEAKS.json), the burst figure is
-    reported beside it."""
+    algorithmic flops, algorithmic bytes), against the pipe the family runs
+    on: under TC math the fused chain / evaluation kernels and the general
+    bf16 forward run bf16 kind::f16 MMAs (held to the SUSTAINED bf16 peak of
+    MEASURED_PEAKS.json, the kernels run back to back inside a long step;
+    burst beside it), the general dW1 runs kind::tf32 (half that rate), and
+    the general head (TRAIN_HEAD, and EVAL_PAIRS where the fused evaluation
+    does not apply) is fp32 FFMA on the CUDA cores; --math ffma is all FFMA."""
     n, ms, fl, by = stat
     if not n or not ms:
         return None
     achieved = fl / (ms / 1e3) / 1e12
-    if args.math == "tf32":
+    ffma = 148 * 128 * 2 * 1.965e9 / 1e12
+    if args.math != "tf32" or name == "TRAIN_HEAD" or (name == "EVAL_PAIRS" and not fused):
+        peak = burst = ffma
+        bound, how = "fp32", "fp32 FFMA spec (148 SM x 128 lanes x 2 x 1.965 GHz), CUDA cores"
+    else:
         peak, burst = pk.get("bf16_tflops_sustained", pk["bf16_tflops"]), pk["bf16_tflops"]
+        bound = "tensor"
         how = (f"{pk_kind} bf16 dense sustained {peak} TFLOP/s (burst {burst}): the kernel runs "
                "kind::f16 bf16 MMAs back to back inside a long step")
-    else:
-        peak = burst = 148 * 128 * 2 * 1.965e9 / 1e12
-        how = "fp32 FFMA spec (148 SM x 128 lanes x 2 x 1.965 GHz)"
+        if name == "TRAIN_DW1":
+            peak, burst = peak / 2, burst / 2
+            how = (f"half the {pk_kind} bf16 dense peak ({peak:.1f} sustained, {burst:.1f} burst): "
+                   "kind::tf32 MMAs")
     gbs = by / (ms / 1e3) / 1e9
-    return {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": peak,
+    return {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": achieved / peak, "frac_burst": achieved / burst,
             "peak_source": how, "avg_launch_ms": ms / n, "launches": n, "traffic": traffic,
             "algorithmic_gbs": gbs, "hbm_frac": gbs / pk["hbm_gbs"]}
 
 
-def roofline(kst, pk, pk_kind, args):
+def roofline(kst, pk, pk_kind, args, fused=True):
     """The dominant kernel's roofline (the headline `roofline` key) and every
     kernel family's."""
     name = max(kst.items(), key=lambda kv: kv[1][1])[0]
@@ -502,8 +511,8 @@ def roofline(kst, pk, pk_kind, args):
             traffic = json.load(open(tpath)).get(args.config, {}).get(name)
         except (OSError, ValueError, AttributeError):
             traffic = None
-    head = kernel_roofline(name, kst[name], pk, pk_kind, args, traffic)
-    every = {k: kernel_roofline(k, v, pk, pk_kind, args) for k, v in kst.items() if v[0]}
+    head = kernel_roofline(name, kst[name], pk, pk_kind, args, traffic, fused)
+    every = {k: kernel_roofline(k, v, pk, pk_kind, args, fused=fused) for k, v in kst.items() if v[0]}
     return head, every
 
 
