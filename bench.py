@@ -559,17 +559,25 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev, prep):
     # double-buffered ingest in two parts on the copy stream: window k+1's
     # eval sets stream in during window k and become current at window k+1's
     # start (its regroup reads them); its rings (the drawn rows) stream in
-    # during window k+1's regroup and become current between that regroup
-    # and its SGD chains.  Window 0's eval sets are the only unoverlapped copy.
+    # during window k+1's own regroup and become current between that regroup
+    # and its SGD chains (configs without a regroup matrix stage them a whole
+    # window ahead instead).  Window 0's eval sets are the only unoverlapped
+    # copy.
     stage_eval()
     ctx.swap_frame_parts(ecco.FRAMES_EVAL)
     stage_rings(10_000)
     for k in range(steps):
         if k + 1 < steps:
             stage_eval()
-        step(10_000 + k, mid=lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS))
-        if k + 1 < steps:
-            stage_rings(10_000 + k + 1)
+
+        def mid(k=k):  # window k's rings become current
+            ctx.swap_frame_parts(ecco.FRAMES_RINGS)
+            if k + 1 < steps and not MATRIX:
+                stage_rings(10_000 + k + 1)  # no regroup to hide them behind: a window ahead
+
+        step(10_000 + k, mid=mid)
+        if k + 1 < steps and MATRIX:
+            stage_rings(10_000 + k + 1)  # streams during window k+1's regroup
         if os.environ.get("ECCO_E2E_TRACE"):
             print(f"e2e window {k}: host {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
         with torch.cuda.stream(stream):
