@@ -160,6 +160,10 @@ ecco_status ecco_swap_frames(ecco_ctx* ctx);
  * ecco_swap_frame_parts the requested ones, so a window's eval sets can
  * become current for the regroup while its rings still stream in. */
 ecco_status ecco_swap_frame_parts(ecco_ctx* ctx, int parts);
+/* Allocates everything the staged ingest uses (back buffers of the frame
+ * table and eval sets, copy stream, the sampled-row bitmap) up front, so the
+ * first staging call does not pay for gigabytes of fresh device memory. */
+ecco_status ecco_reserve_ingest(ecco_ctx* ctx);
 /* Group-sharded variant of ecco_stage_frames: the frame rings of cameras
  * [ring_first, ring_first + ring_n) only (the members of this rank's groups:
  * a job trains on its own members' frames, orchestrator.cpp:52-62, 282-309)

@@ -102,7 +102,7 @@ EXPORTS = [
     "ecco_kernel_launches", "ecco_profile", "ecco_kernel_stat", "ecco_transfer_bytes", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
     "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
     "ecco_read_frames", "ecco_stage_frames", "ecco_stage_frames_range", "ecco_stage_sampled_frames",
-    "ecco_swap_frames", "ecco_swap_frame_parts",
+    "ecco_swap_frames", "ecco_swap_frame_parts", "ecco_reserve_ingest",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
@@ -341,6 +341,10 @@ class Context:
 
     def swap_frames(self):
         self._check(lib().ecco_swap_frames(self._h))
+
+    def reserve_ingest(self):
+        """ecco_reserve_ingest: allocate the staged ingest's buffers now."""
+        self._check(lib().ecco_reserve_ingest(self._h))
 
     def swap_frame_parts(self, parts):
         """ecco_swap_frame_parts: FRAMES_RINGS (rings + labels) and/or

@@ -399,6 +399,18 @@ ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint1
   });
 }
 
+ecco_status ecco_reserve_ingest(ecco_ctx* ctx) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(learned(ctx), "reserve_ingest: learned backend only");
+    open_back_buffers(ctx, 0);  // the back buffers, copy stream and events
+    if (!ctx->d_zc_rows) dalloc(&ctx->d_zc_rows, 1);
+    const size_t rows = (size_t)ctx->cfg.max_cameras * ctx->cfg.ring_frames;
+    ctx->zc_flags.get((rows + 31) / 32 * 4);
+    ctx->zc_host.get(4096);
+    ECCO_CUDA(cudaDeviceSynchronize());
+  });
+}
+
 ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_ids,
                                       const ecco_batch* batches, const int* src_off,
                                       const int* src_cams, const double* src_fracs,
