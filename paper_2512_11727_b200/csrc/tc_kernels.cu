@@ -370,29 +370,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
   float* W1 = a.wbase + (size_t)a.slots[j] * a.wstride;
   const int lane = tid & 31;
   float* tr = reinterpret_cast<float*>(smem) + warp * 32 * 33;  // operand stages are free
+  // 16-byte accesses: lane = (row group rr = lane / 8, column quad cq =
+  // lane % 8) covers 4 rows x 32 columns per instruction; the shadow lane =
+  // (column group, feature quad) writes 8 bytes; tr reads conflict-free
+  const int rr = lane >> 3, cq = lane & 7;
   for (int c0 = 0; c0 < NT; c0 += 32) {
     float v[32];
     tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
 #pragma unroll
     for (int i = 0; i < 32; ++i) tr[i * 33 + lane] = v[i];  // tr[col][row]
     __syncwarp();
-    float* wcol = W1 + (size_t)(f0 + warp * 32) * a.H + n0 + c0 + lane;
-    float wv[32];
+    float* wrow = W1 + (size_t)(f0 + warp * 32 + rr) * a.H + n0 + c0 + 4 * cq;
+    float4 wv[8];
 #pragma unroll
-    for (int r = 0; r < 32; ++r) wv[r] = wcol[(size_t)r * a.H];  // 32 loads in flight
+    for (int it = 0; it < 8; ++it)  // rows 4 * it + rr: 8 x 16 bytes in flight
+      wv[it] = *reinterpret_cast<const float4*>(wrow + (size_t)(4 * it) * a.H);
 #pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const float nw = fmaf(-a.lr, tr[lane * 33 + r], wv[r]);
-      wcol[(size_t)r * a.H] = nw;
-      tr[lane * 33 + r] = nw;  // (h = lane, f = r), for the shadow below
+    for (int it = 0; it < 8; ++it) {
+      const int r = 4 * it + rr;
+      float* t = tr + (4 * cq) * 33 + r;
+      const float4 nw = make_float4(fmaf(-a.lr, t[0], wv[it].x), fmaf(-a.lr, t[33], wv[it].y),
+                                    fmaf(-a.lr, t[66], wv[it].z), fmaf(-a.lr, t[99], wv[it].w));
+      *reinterpret_cast<float4*>(wrow + (size_t)(4 * it) * a.H) = nw;
+      t[0] = nw.x;  // (col, row) -> the updated value, for the shadow below
+      t[33] = nw.y;
+      t[66] = nw.z;
+      t[99] = nw.w;
     }
     __syncwarp();
-    if (a.w1t) {  // shadow rows h, 32 consecutive features per warp: 64-byte stores
-      uint16_t* sh = a.w1t + (size_t)a.slots[j] * a.H * a.F + (size_t)(n0 + c0) * a.F + f0 +
-                     warp * 32 + lane;
-#pragma unroll 8
-      for (int h = 0; h < 32; ++h)
-        sh[(size_t)h * a.F] = (uint16_t)(sm100::pack_bf16x2(tr[h * 33 + lane], 0.0f) & 0xFFFF);
+    if (a.w1t) {  // shadow [h][f]: lane = (h group, 4 consecutive features), 8-byte stores
+      uint16_t* sh = a.w1t + (size_t)a.slots[j] * a.H * a.F + (size_t)(n0 + c0 + rr) * a.F + f0 +
+                     warp * 32 + 4 * cq;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const float* t = tr + (4 * it + rr) * 33 + 4 * cq;
+        *reinterpret_cast<uint2*>(sh + (size_t)(4 * it) * a.F) =
+            make_uint2(sm100::pack_bf16x2(t[0], t[1]), sm100::pack_bf16x2(t[2], t[3]));
+      }
     }
     __syncwarp();
   }
