@@ -351,18 +351,38 @@ __global__ void __launch_bounds__(128) k_l_update2_t(LDims g, int n_jobs, const 
   float acc[4][4] = {};
   float bacc = 0.0f;
   const size_t r0 = (size_t)j * g.B;
+  // the next chunk's Z / DL values are loaded into registers while this
+  // chunk's products run (the kernel is bound by global-load latency)
+  constexpr int kZ = kHT * 64 / 128, kD = kHT * 32 / 128;
+  float zr[kZ], dr[kD];
+  auto fetch = [&](int s0) {
+    const int ns = min(kHT, g.B - s0);
+#pragma unroll
+    for (int u = 0; u < kZ; ++u) {
+      const int e = tid + u * 128, s = e / 64, h = e % 64;
+      zr[u] = s < ns ? Z[(r0 + s0 + s) * g.H + h0 + h] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kD; ++u) {
+      const int e = tid + u * 128, s = e / 32, c = e % 32;
+      dr[u] = s < ns && c0 + c < g.C ? DL[(r0 + s0 + s) * g.C + c0 + c] : 0.0f;
+    }
+  };
+  fetch(0);
   for (int s0 = 0; s0 < g.B; s0 += kHT) {
     const int ns = min(kHT, g.B - s0);
-    for (int e = tid; e < kHT * 64; e += 128) {
-      const int s = e / 64, h = e % 64;
-      const float z = s < ns ? Z[(r0 + s0 + s) * g.H + h0 + h] : 0.0f;
-      Zs[s][h] = z > 0.0f ? z : 0.0f;
+#pragma unroll
+    for (int u = 0; u < kZ; ++u) {
+      const int e = tid + u * 128;
+      Zs[e / 64][e % 64] = zr[u] > 0.0f ? zr[u] : 0.0f;
     }
-    for (int e = tid; e < kHT * 32; e += 128) {
-      const int s = e / 32, c = e % 32;
-      Ds[s][c] = s < ns && c0 + c < g.C ? DL[(r0 + s0 + s) * g.C + c0 + c] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < kD; ++u) {
+      const int e = tid + u * 128;
+      Ds[e / 32][e % 32] = dr[u];
     }
     __syncthreads();
+    if (s0 + kHT < g.B) fetch(s0 + kHT);
     for (int s = 0; s < ns; ++s) {
       const float4 z = *reinterpret_cast<const float4*>(&Zs[s][ty * 4]);
       const float4 d = *reinterpret_cast<const float4*>(&Ds[s][tx * 4]);
