@@ -257,17 +257,35 @@ __global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const i
   const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
   float acc[4][4] = {};
   const size_t r0 = (size_t)blk * kRB;
-  for (int k0 = 0; k0 < g.H; k0 += kHT) {
-    for (int e = tid; e < kRB * kHT; e += 128) {
-      const int r = e / kHT, k = e % kHT;
-      const float z = Z[(r0 + r) * g.H + k0 + k];
-      Zs[k][r] = z > 0.0f ? z : 0.0f;
+  // next chunk's Z / W2 values prefetched into registers (load-latency bound)
+  constexpr int kZ = kRB * kHT / 128, kW = kHT * 32 / 128;
+  float zr[kZ], wr[kW];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < kZ; ++u) {
+      const int e = tid + u * 128, r = e / kHT, k = e % kHT;
+      zr[u] = Z[(r0 + r) * g.H + k0 + k];
     }
-    for (int e = tid; e < kHT * 32; e += 128) {
-      const int k = e / 32, c = e % 32;
-      Ws[k][c] = c0 + c < g.C ? W2[(size_t)(k0 + k) * g.C + c0 + c] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < kW; ++u) {
+      const int e = tid + u * 128, k = e / 32, c = e % 32;
+      wr[u] = c0 + c < g.C ? W2[(size_t)(k0 + k) * g.C + c0 + c] : 0.0f;
+    }
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < g.H; k0 += kHT) {
+#pragma unroll
+    for (int u = 0; u < kZ; ++u) {
+      const int e = tid + u * 128;
+      Zs[e % kHT][e / kHT] = zr[u] > 0.0f ? zr[u] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kW; ++u) {
+      const int e = tid + u * 128;
+      Ws[e / 32][e % 32] = wr[u];
     }
     __syncthreads();
+    if (k0 + kHT < g.H) fetch(k0 + kHT);
 #pragma unroll 8
     for (int k = 0; k < kHT; ++k) {
       const float4 z = *reinterpret_cast<const float4*>(&Zs[k][ty * 4]);
@@ -301,17 +319,36 @@ __global__ void __launch_bounds__(128) k_l_dh_t(LDims g, int n_rows, const int* 
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   float acc[8][4] = {};
   const size_t r0 = (size_t)blk * kRB;
+  constexpr int kDv = kRB * kHT / 128, kWv = 64 * kHT / 128;
+  float dr[kDv], wr[kWv];
+  auto fetch = [&](int c0) {  // next chunk into registers (load-latency bound)
+    const int nc = min(kHT, g.C - c0);
+#pragma unroll
+    for (int u = 0; u < kDv; ++u) {
+      const int e = tid + u * 128, r = e / kHT, c = e % kHT;
+      dr[u] = c < nc ? DL[(r0 + r) * g.C + c0 + c] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kWv; ++u) {
+      const int e = tid + u * 128, h = e / kHT, c = e % kHT;
+      wr[u] = c < nc ? W2[(size_t)(h0 + h) * g.C + c0 + c] : 0.0f;
+    }
+  };
+  fetch(0);
   for (int c0 = 0; c0 < g.C; c0 += kHT) {
     const int nc = min(kHT, g.C - c0);
-    for (int e = tid; e < kRB * kHT; e += 128) {
-      const int r = e / kHT, c = e % kHT;
-      Ds[c][r] = c < nc ? DL[(r0 + r) * g.C + c0 + c] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < kDv; ++u) {
+      const int e = tid + u * 128;
+      Ds[e % kHT][e / kHT] = dr[u];
     }
-    for (int e = tid; e < 64 * kHT; e += 128) {
-      const int h = e / kHT, c = e % kHT;
-      Ws[c][h] = c < nc ? W2[(size_t)(h0 + h) * g.C + c0 + c] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < kWv; ++u) {
+      const int e = tid + u * 128;
+      Ws[e % kHT][e / kHT] = wr[u];
     }
     __syncthreads();
+    if (c0 + kHT < g.C) fetch(c0 + kHT);
     for (int c = 0; c < nc; ++c) {
       const float4 w = *reinterpret_cast<const float4*>(&Ws[c][tx * 4]);
       const float4 d0 = *reinterpret_cast<const float4*>(&Ds[c][ty * 8]);
