@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
 // rows gathered by cp.async into a 128B-swizzled K-major stage (bf16, exact),
 // B = the bf16 W1^T shadow by TMA ({64, 256} boxes), kind::f16 MMAs (M 128,
 // N 256, K 16) into TMEM, 4 stages of K = 64.
-constexpr int kBfNT = 256, kBfStages = 4;
+constexpr int kBfNT = 256, kBfStages = 2;  // 96 KB: two CTAs per SM
 constexpr uint32_t kBfA = 128 * 128, kBfB = kBfNT * 128;  // bytes per stage
 
 struct FwdBfArgs {
