@@ -419,7 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
 // fwd, bf16: one CTA per (128-row training tile, 256 hidden columns).  A = X
 // rows gathered by cp.async into a 128B-swizzled K-major stage (bf16, exact),
 // B = the bf16 W1^T shadow by TMA ({64, 256} boxes), kind::f16 MMAs (M 128,
-// N 256, K 16) into TMEM, 4 stages of K = 64.
+// N 256, K 16) into TMEM, 2 stages of K = 64 (two CTAs per SM hide the
+// gather latency better than four stages in one).
 constexpr int kBfNT = 256, kBfStages = 2;  // 96 KB: two CTAs per SM
 constexpr uint32_t kBfA = 128 * 128, kBfB = kBfNT * 128;  // bytes per stage
 
