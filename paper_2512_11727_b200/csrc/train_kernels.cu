@@ -320,6 +320,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(w2full, 1);
     fence_barrier_init();
   }
+  // this CTA's master slice (64 rows x F fp32) -> L2 at once: the tile-by-tile
+  // loads below then wait on L2, not on four HBM round trips
+  for (int li = tid; li < kHS * (F / 32); li += kThreads)
+    prefetch_l2(W1 + (size_t)(h0 + li / (F / 32)) * F + (li % (F / 32)) * 32);
   if (warp == 0) tmem_alloc(sTmem, tmem_cols(F));
   if (tid < kB) {
     sRow[tid] = jrows[tid];
