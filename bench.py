@@ -211,7 +211,7 @@ def run_b200(args, rank, world, local_rank):
         else:
             dist.init_process_group(backend)
     wl = Workload(args.config, rank, world)
-    math = ecco.TC_TF32 if args.math == "tf32" else ecco.FFMA_EXACT
+    math = ecco.TC_BF16 if args.math == "tf32" else ecco.FFMA_EXACT
     ctx = ecco.Context(backend=ecco.LEARNED, device=local_rank, math=math,
                        max_cameras=wl.N, max_jobs=max(1, len(wl.local)), max_depth=DEPTH,
                        steps_per_gpu_s=float(STEPS), **DIMS)
@@ -410,7 +410,7 @@ def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
     for world in worlds:
         wl = Workload(args.config, 0, world)
         ctx = ecco.Context(backend=ecco.LEARNED, device=torch.cuda.current_device(),
-                           math=ecco.TC_TF32 if args.math == "tf32" else ecco.FFMA_EXACT,
+                           math=ecco.TC_BF16 if args.math == "tf32" else ecco.FFMA_EXACT,
                            max_cameras=wl.N, max_jobs=max(1, len(wl.local)), max_depth=DEPTH,
                            steps_per_gpu_s=float(STEPS), **DIMS)
         ctx.set_cameras(wl.scenes, wl.tp)
@@ -807,7 +807,7 @@ def parametric_leg(args):
     # the netsim and allocator replay on the host (no reference counterpart:
     # the reference has no learned trainer)
     scl = json.dumps(scenarios.config("c4", windows=2, seed=1, local_acc=0.0))
-    siml = ecco.Simulation(scl, backend=ecco.LEARNED, math=ecco.TC_TF32, full_matrix=1,
+    siml = ecco.Simulation(scl, backend=ecco.LEARNED, math=ecco.TC_BF16, full_matrix=1,
                            steps_per_gpu_s=5000.0)
     wl_ = []
     while siml.step_window():

@@ -51,10 +51,19 @@ typedef enum {
 
 typedef enum { ECCO_BACKEND_PARAMETRIC = 0, ECCO_BACKEND_LEARNED = 1 } ecco_backend;
 
-/* Arithmetic of the learned backend's dense contractions. */
+/* Arithmetic of the learned backend's dense contractions.
+ *
+ * ECCO_MATH_TC_BF16: tcgen05 tensor-core math with fp32 accumulation in TMEM
+ * and fp32 master weights; the operands are bf16 (kind::f16) in the fused
+ * SGD chain (train_kernels.cu, every contraction) and in the fused
+ * evaluation kernels (eval_kernels.cu); shapes outside the fused chain
+ * (tc_kernels.cu) run a bf16 forward and a kind::tf32 W1 gradient.  Results
+ * are within the tolerances stated in DESIGN.md 2, not bit-exact.
+ * ECCO_MATH_TC_TF32 is the round-1 name of the same mode (kept as an alias). */
 typedef enum {
-  ECCO_MATH_FFMA_EXACT = 0, /* fp32 FFMA in the oracle's order: bit-exact   */
-  ECCO_MATH_TC_TF32 = 1     /* tcgen05 kind::tf32 -> fp32 TMEM: tolerance  */
+  ECCO_MATH_FFMA_EXACT = 0, /* fp32 FFMA in the oracle's order: bit-exact        */
+  ECCO_MATH_TC_BF16 = 1,    /* tcgen05, bf16 operands (+tf32 dW1 off the chain)  */
+  ECCO_MATH_TC_TF32 = 1     /* alias of ECCO_MATH_TC_BF16                        */
 } ecco_math;
 
 /* ModelParams (proj/core/include/ecco/accuracy_model.hpp:18-24). */
@@ -269,6 +278,17 @@ ecco_status ecco_route_matrix_dev(ecco_ctx* ctx, int n, int g_block, int n_block
                                   const void* matrix_dev, const void* req_dev, void* best_col_dev,
                                   void* best_acc_dev);
 
+/* Same epilogue with a column -> group id map, for group placements where a
+ * rank's block holds arbitrary groups (the cost-balanced placement of
+ * SURVEY.md 8(e), paper_2512_11727_b200/shard.py): col_ids_dev holds
+ * n_blocks*g_block int32 group ids in gathered column order (< 0 = padding
+ * column, skipped).  best_id_dev receives the winning GROUP ID (-1 = none),
+ * ties going to the lowest id -- group_request's order over jobs in
+ * ascending id (grouping.cpp:30-39) -- whatever rank holds the group. */
+ecco_status ecco_route_matrix_ids_dev(ecco_ctx* ctx, int n, int g_block, int n_blocks,
+                                      const void* matrix_dev, const void* col_ids_dev,
+                                      const void* req_dev, void* best_id_dev, void* best_acc_dev);
+
 /* ---- TrainingBackend::train batches: marginal-gain probes ------------------
  * Batch description = TrainingBatchStats (accuracy_model.hpp:50-56) with the
  * source_mix flattened to CSR (cameras in std::map order). */
@@ -303,7 +323,10 @@ ecco_status ecco_train_trajectories(
  * reads it zero-copy over PCIe) into the back buffer; all labels and the
  * first n_eval cameras' eval sets are copied as in ecco_stage_frames.  Rows
  * the trajectories never draw are not transferred (their back-buffer slots
- * are stale), so the trajectories' results equal a full upload's.  Counts
+ * are stale), so the trajectories' results equal a full upload's; once the
+ * rings are current, a ecco_train_trajectories call that would draw an
+ * unstaged row fails with ECCO_ERR_LOGIC (ecco_fetch_sampled_frames tops
+ * them up).  Counts
  * the rows read into ecco_transfer_bytes.  The fetch runs as two CTAs
  * beside the window's kernels (the CTA-pair evaluation kernel schedules its
  * tiles dynamically around them).  Replaces, for the
@@ -315,6 +338,22 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
                                       const int* micro_base, int window, double gpu_s, int depth,
                                       const uint16_t* frames, const int32_t* labels, int n_eval,
                                       const uint16_t* eval_frames, const int32_t* eval_labels);
+/* Top-up of a sampled ingest: when the CURRENT rings came from
+ * ecco_stage_sampled_frames (only the rows its trajectories draw), reads the
+ * rows that THESE trajectories arguments draw and the rings lack from the
+ * same pinned [n_cams][R][F] table, zero-copy, into the current rings
+ * (stream-ordered on the context stream; returns after the fetch).  For
+ * chains the caller did not foresee at staging time -- e.g. a chain the
+ * allocator replay exhausts and extends (micro_base = micro-windows already
+ * committed).  A no-op when the current rings are complete (generated,
+ * uploaded or staged whole).  ecco_train_trajectories itself checks, when
+ * the current rings are partial, that every row it draws was staged or
+ * fetched, and fails with ECCO_ERR_LOGIC otherwise (no silent stale rows). */
+ecco_status ecco_fetch_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_ids,
+                                      const ecco_batch* batches, const int* src_off,
+                                      const int* src_cams, const double* src_fracs,
+                                      const int* micro_base, int window, double gpu_s, int depth,
+                                      const uint16_t* frames);
 /* Makes the snapshot after granted[j] steps of the last chain (0 = keep the
  * committed model) the committed model. */
 ecco_status ecco_commit(ecco_ctx* ctx, int n_jobs, const int* job_ids, const int* granted);

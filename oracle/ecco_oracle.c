@@ -453,22 +453,35 @@ void orc_init_weights(const orc_lcfg* c, float* w1, float* b1, float* w2, float*
   for (int j = 0; j < c->C; ++j) b2[j] = 0.0f;
 }
 
-/* Forward of one sample: z (pre-activation, H), logits (C). */
+/* The learned step's arithmetic, fixed per output element: every dot
+ * product is an fmaf chain in ascending contraction index from 0.0f, bias
+ * added last; every gradient sum an fmaf (or +) chain in ascending sample
+ * index.  The loops below keep exactly that sequence PER ELEMENT while
+ * running the independent elements of a row in the inner loop (contiguous,
+ * so the compiler vectorizes them with hardware FMA: the rounding of each
+ * fmaf is the same single rounding whichever way it executes).  The device
+ * FFMA path (learned_kernels.cu) follows the same sequences bit for bit. */
+
+/* Forward of one sample: z (pre-activation, H), logits (C); acc: H floats
+ * of scratch. */
 static void fwd1(const orc_lcfg* c, const uint16_t* xs, const float* w1, const float* b1,
                  const float* w2, const float* b2, float* z, float* logit) {
-  for (int h = 0; h < c->H; ++h) {
-    float a = 0.0f;
-    for (int f = 0; f < c->F; ++f) a = fmaf(orc_bf16_to_f32(xs[f]), w1[(long)f * c->H + h], a);
-    z[h] = a + b1[h];
+  const int F = c->F, H = c->H, C = c->C;
+  for (int h = 0; h < H; ++h) z[h] = 0.0f;
+  for (int f = 0; f < F; ++f) {  /* z[h] = fmaf(x[f], W1[f][h], z[h]), f ascending */
+    const float xf = orc_bf16_to_f32(xs[f]);
+    const float* row = w1 + (long)f * H;
+    for (int h = 0; h < H; ++h) z[h] = fmaf(xf, row[h], z[h]);
   }
-  for (int j = 0; j < c->C; ++j) {
-    float a = 0.0f;
-    for (int k = 0; k < c->H; ++k) {
-      const float hk = z[k] > 0.0f ? z[k] : 0.0f;
-      a = fmaf(hk, w2[(long)k * c->C + j], a);
-    }
-    logit[j] = a + b2[j];
+  for (int h = 0; h < H; ++h) z[h] = z[h] + b1[h];
+  float a[1024];
+  for (int j = 0; j < C; ++j) a[j] = 0.0f;
+  for (int k = 0; k < H; ++k) {  /* logit[j] = fmaf(relu(z[k]), W2[k][j], .), k ascending */
+    const float hk = z[k] > 0.0f ? z[k] : 0.0f;
+    const float* row = w2 + (long)k * C;
+    for (int j = 0; j < C; ++j) a[j] = fmaf(hk, row[j], a[j]);
   }
+  for (int j = 0; j < C; ++j) logit[j] = a[j] + b2[j];
 }
 
 float orc_sgd_step(const orc_lcfg* c, const uint16_t* x, const int32_t* y, float* w1, float* b1,
@@ -477,6 +490,9 @@ float orc_sgd_step(const orc_lcfg* c, const uint16_t* x, const int32_t* y, float
   float* z = (float*)malloc(sizeof(float) * B * H);
   float* dl = (float*)malloc(sizeof(float) * B * C);
   float* dh = (float*)malloc(sizeof(float) * B * H);
+  float* w2t = (float*)malloc(sizeof(float) * C * H);
+  float* acc = (float*)malloc(sizeof(float) * (H > C ? H : C));
+  float* xf = (float*)malloc(sizeof(float) * B);
   float logit[1024];
   const float invB = 1.0f / (float)B;
   double loss = 0.0;
@@ -495,45 +511,58 @@ float orc_sgd_step(const orc_lcfg* c, const uint16_t* x, const int32_t* y, float
     }
     loss += (double)(logf(sum) - (logit[y[s]] - m));
   }
-  /* dh with the pre-update W2 */
-  for (int s = 0; s < B; ++s)
-    for (int k = 0; k < H; ++k) {
-      float a = 0.0f;
-      if (z[(long)s * H + k] > 0.0f)
-        for (int j = 0; j < C; ++j) a = fmaf(dl[(long)s * C + j], w2[(long)k * C + j], a);
-      dh[(long)s * H + k] = a;
-    }
-  /* W2, b2 */
+  /* dh[s][k] = relu'(z) * sum_j fmaf(dl[s][j], W2[k][j], .), j ascending, with
+   * the pre-update W2 (transposed once so k runs contiguous) */
   for (int k = 0; k < H; ++k)
+    for (int j = 0; j < C; ++j) w2t[(long)j * H + k] = w2[(long)k * C + j];
+  for (int s = 0; s < B; ++s) {
+    float* d = dh + (long)s * H;
+    for (int k = 0; k < H; ++k) d[k] = 0.0f;
     for (int j = 0; j < C; ++j) {
-      float a = 0.0f;
-      for (int s = 0; s < B; ++s) {
-        const float zk = z[(long)s * H + k];
-        a = fmaf(zk > 0.0f ? zk : 0.0f, dl[(long)s * C + j], a);
-      }
-      w2[(long)k * C + j] = fmaf(-c->lr, a, w2[(long)k * C + j]);
+      const float g = dl[(long)s * C + j];
+      const float* row = w2t + (long)j * H;
+      for (int k = 0; k < H; ++k) d[k] = fmaf(g, row[k], d[k]);
     }
-  for (int j = 0; j < C; ++j) {
-    float a = 0.0f;
-    for (int s = 0; s < B; ++s) a += dl[(long)s * C + j];
-    b2[j] = fmaf(-c->lr, a, b2[j]);
+    const float* zs = z + (long)s * H;
+    for (int k = 0; k < H; ++k) d[k] = zs[k] > 0.0f ? d[k] : 0.0f;
   }
-  /* W1, b1 */
-  for (int f = 0; f < F; ++f)
-    for (int h = 0; h < H; ++h) {
-      float a = 0.0f;
-      for (int s = 0; s < B; ++s)
-        a = fmaf(orc_bf16_to_f32(x[(long)s * F + f]), dh[(long)s * H + h], a);
-      w1[(long)f * H + h] = fmaf(-c->lr, a, w1[(long)f * H + h]);
+  /* W2[k][j] += -lr * sum_s fmaf(relu(z[s][k]), dl[s][j], .), s ascending */
+  for (int k = 0; k < H; ++k) {
+    for (int j = 0; j < C; ++j) acc[j] = 0.0f;
+    for (int s = 0; s < B; ++s) {
+      const float zk = z[(long)s * H + k];
+      const float r = zk > 0.0f ? zk : 0.0f;
+      const float* g = dl + (long)s * C;
+      for (int j = 0; j < C; ++j) acc[j] = fmaf(r, g[j], acc[j]);
     }
-  for (int h = 0; h < H; ++h) {
-    float a = 0.0f;
-    for (int s = 0; s < B; ++s) a += dh[(long)s * H + h];
-    b1[h] = fmaf(-c->lr, a, b1[h]);
+    for (int j = 0; j < C; ++j) w2[(long)k * C + j] = fmaf(-c->lr, acc[j], w2[(long)k * C + j]);
   }
+  for (int j = 0; j < C; ++j) acc[j] = 0.0f;
+  for (int s = 0; s < B; ++s)
+    for (int j = 0; j < C; ++j) acc[j] += dl[(long)s * C + j];
+  for (int j = 0; j < C; ++j) b2[j] = fmaf(-c->lr, acc[j], b2[j]);
+  /* W1[f][h] += -lr * sum_s fmaf(x[s][f], dh[s][h], .), s ascending */
+  for (int f = 0; f < F; ++f) {
+    for (int s = 0; s < B; ++s) xf[s] = orc_bf16_to_f32(x[(long)s * F + f]);
+    for (int h = 0; h < H; ++h) acc[h] = 0.0f;
+    for (int s = 0; s < B; ++s) {
+      const float v = xf[s];
+      const float* d = dh + (long)s * H;
+      for (int h = 0; h < H; ++h) acc[h] = fmaf(v, d[h], acc[h]);
+    }
+    float* row = w1 + (long)f * H;
+    for (int h = 0; h < H; ++h) row[h] = fmaf(-c->lr, acc[h], row[h]);
+  }
+  for (int h = 0; h < H; ++h) acc[h] = 0.0f;
+  for (int s = 0; s < B; ++s)
+    for (int h = 0; h < H; ++h) acc[h] += dh[(long)s * H + h];
+  for (int h = 0; h < H; ++h) b1[h] = fmaf(-c->lr, acc[h], b1[h]);
   free(z);
   free(dl);
   free(dh);
+  free(w2t);
+  free(acc);
+  free(xf);
   return (float)(loss / B);
 }
 

@@ -23,7 +23,8 @@ LIB_PATH = os.path.join(HERE, "libecco_b200.so")
 
 OK, INVALID_ARGUMENT, LOGIC, INFEASIBLE, SCHEMA, CUDA, RUNTIME = range(7)
 PARAMETRIC, LEARNED = 0, 1
-FFMA_EXACT, TC_TF32 = 0, 1
+FFMA_EXACT, TC_BF16 = 0, 1
+TC_TF32 = TC_BF16  # round-1 name of the tensor-core mode (ecco_math in include/ecco_b200.h)
 # ecco_kstat (include/ecco_b200.h)
 (KSTAT_TRAIN_STEP, KSTAT_TRAIN_DW1, KSTAT_TRAIN_HEAD, KSTAT_EVAL_MATRIX, KSTAT_EVAL_PAIRS,
  KSTAT_P_EVAL, KSTAT_P_TRAJ, KSTAT_P_PROFILE, KSTAT_FRAMES) = range(9)
@@ -101,12 +102,12 @@ EXPORTS = [
     "ecco_default_config", "ecco_create", "ecco_destroy", "ecco_last_error",
     "ecco_kernel_launches", "ecco_profile", "ecco_kernel_stat", "ecco_transfer_bytes", "ecco_stream", "ecco_synchronize", "ecco_set_cameras",
     "ecco_update_scenes", "ecco_generate_frames", "ecco_upload_frames", "ecco_upload_frames_dev",
-    "ecco_read_frames", "ecco_stage_frames", "ecco_stage_frames_range", "ecco_stage_sampled_frames",
+    "ecco_read_frames", "ecco_stage_frames", "ecco_stage_frames_range", "ecco_stage_sampled_frames", "ecco_fetch_sampled_frames",
     "ecco_swap_frames", "ecco_swap_frame_parts", "ecco_reserve_ingest",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
     "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
-    "ecco_route_matrix_dev", "ecco_debug_eval_logits",
+    "ecco_route_matrix_dev", "ecco_route_matrix_ids_dev", "ecco_debug_eval_logits",
     "ecco_train_trajectories", "ecco_commit", "ecco_last_losses", "ecco_sample_indices",
     "ecco_profile_tables", "ecco_sim_default_options", "ecco_sim_create", "ecco_sim_destroy",
     "ecco_sim_last_error", "ecco_sim_step_window", "ecco_sim_last_timings",
@@ -339,6 +340,16 @@ class Context:
             C.c_int(window), C.c_double(gpu_seconds), C.c_int(depth), C.c_void_p(frames_ptr),
             C.c_void_p(labels_ptr), int(eval_n), C.c_void_p(eval_ptr), C.c_void_p(eval_labels_ptr)))
 
+    def fetch_sampled_host_ptr(self, p, gpu_seconds, depth, window, frames_ptr, micro_base=None):
+        """ecco_fetch_sampled_frames for the prepare_trajectories() batch `p`:
+        tops the CURRENT (sampled) rings up with the rows train_prepared(p,
+        ...) will draw, from the pinned frame table at frames_ptr."""
+        mb = p["mb0"] if micro_base is None else np.ascontiguousarray(micro_base, np.int32)
+        vp = lambda a: a.ctypes.data_as(C.c_void_p)
+        self._check(lib().ecco_fetch_sampled_frames(
+            self._h, p["n"], vp(p["ids"]), p["bt"], vp(p["so"]), vp(p["sc"]), vp(p["sf"]), vp(mb),
+            C.c_int(window), C.c_double(gpu_seconds), C.c_int(depth), C.c_void_p(frames_ptr)))
+
     def swap_frames(self):
         self._check(lib().ecco_swap_frames(self._h))
 
@@ -480,6 +491,15 @@ class Context:
                                                 C.c_void_p(matrix_ptr),
                                                 C.c_void_p(req_ptr) if req_ptr else None,
                                                 C.c_void_p(best_ptr), C.c_void_p(acc_ptr)))
+
+    def route_matrix_ids_dev(self, n, g_block, matrix_ptr, ids_ptr, best_ptr, acc_ptr,
+                             req_ptr=None, n_blocks=1):
+        """ecco_route_matrix_ids_dev: the same epilogue with a device column ->
+        group id map (int32, < 0 = padding); best_ptr receives group ids."""
+        self._check(lib().ecco_route_matrix_ids_dev(
+            self._h, int(n), int(g_block), int(n_blocks), C.c_void_p(matrix_ptr),
+            C.c_void_p(ids_ptr), C.c_void_p(req_ptr) if req_ptr else None, C.c_void_p(best_ptr),
+            C.c_void_p(acc_ptr)))
 
     # training
     def prepare_trajectories(self, job_ids, batches, sources, fracs, members):

@@ -181,7 +181,7 @@ ecco_status ecco_create(const ecco_config* cfg, ecco_ctx** out) {
       ECCO_REQUIRE(g.eval_samples % 64 == 0 && g.eval_samples > 0,
                    "eval_samples must be a multiple of 64");
       ECCO_REQUIRE(g.ring_frames > 0, "ring_frames must be positive");
-      ECCO_REQUIRE(g.math == ECCO_MATH_FFMA_EXACT || g.math == ECCO_MATH_TC_TF32, "unknown math");
+      ECCO_REQUIRE(g.math == ECCO_MATH_FFMA_EXACT || g.math == ECCO_MATH_TC_BF16, "unknown math");
     }
     ECCO_CUDA(cudaSetDevice(g.device));
     ECCO_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -314,6 +314,7 @@ ecco_status ecco_generate_frames(ecco_ctx* ctx, int window) {
   return guarded(ctx, [&] {
     ECCO_REQUIRE(learned(ctx), "generate_frames: learned backend only");
     lbackend::generate_frames(ctx, window);
+    ctx->ring_partial = false;
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -328,6 +329,7 @@ static void upload_frames_impl(ecco_ctx* ctx, int n, const void* frames, const v
   ECCO_CUDA(ctx_memcpy(ctx, ctx->d_labels, labels, fr * 4, kind, ctx->stream));
   ECCO_CUDA(ctx_memcpy(ctx, ctx->d_eval, eval, ev * g.feat_dim * 2, kind, ctx->stream));
   ECCO_CUDA(ctx_memcpy(ctx, ctx->d_eval_labels, eval_labels, ev * 4, kind, ctx->stream));
+  ctx->ring_partial = false;
 }
 
 ecco_status ecco_upload_frames(ecco_ctx* ctx, int n, const uint16_t* frames, const int32_t* labels,
@@ -396,6 +398,7 @@ ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint1
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream));
     staged_parts(ctx, parts);
+    if (parts & 1) ctx->back_partial = false;  // whole rings (of the caller's range)
   });
 }
 
@@ -489,6 +492,61 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, st));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, st));
     staged_parts(ctx, parts);
+    ctx->back_partial = true;  // only the drawn rows: zc_flags says which
+  });
+}
+
+ecco_status ecco_fetch_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_ids,
+                                      const ecco_batch* batches, const int* src_off,
+                                      const int* src_cams, const double* src_fracs,
+                                      const int* micro_base, int window, double gpu_s, int depth,
+                                      const uint16_t* frames) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(learned(ctx), "fetch_sampled_frames: learned backend only");
+    ECCO_REQUIRE(n_jobs >= 0 && depth >= 1 && depth <= ctx->cfg.max_depth,
+                 "fetch_sampled_frames: depth must be in [1, max_depth]");
+    ECCO_REQUIRE(n_jobs == 0 || src_off[0] == 0, "CSR offsets must start at 0");
+    for (int j = 0; j < n_jobs; ++j)
+      validate_batch(ctx, j, gpu_s, src_off[j + 1] - src_off[j], src_cams + src_off[j],
+                     src_fracs + src_off[j]);
+    if (!ctx->ring_partial || n_jobs == 0) return;  // complete rings: nothing to fetch
+    void* fdev = nullptr;
+    if (cudaHostGetDevicePointer(&fdev, (void*)frames, 0) != cudaSuccess) {
+      (void)cudaGetLastError();
+      ECCO_REQUIRE(false, "fetch_sampled_frames: frames must be pinned (mapped) host memory");
+    }
+    const ecco_config& g = ctx->cfg;
+    cudaStream_t st = ctx->stream;
+    std::vector<int> steps(n_jobs), mb(n_jobs, 0);
+    int max_steps = 0;
+    for (int j = 0; j < n_jobs; ++j) {
+      steps[j] = learned_steps(ctx, batches[j], gpu_s, src_off[j + 1] - src_off[j],
+                               src_cams + src_off[j]);
+      max_steps = std::max(max_steps, steps[j]);
+    }
+    if (micro_base) mb.assign(micro_base, micro_base + n_jobs);
+    const size_t nsrc = std::max(src_off[n_jobs], 1);
+    DevBuf* b = ctx->traj_args;  // stream-ordered before the next trajectories' uploads
+    auto up = [&](int i, const void* h, size_t bytes) {
+      void* d = b[i].get(bytes);
+      ECCO_CUDA(ctx_memcpy(ctx, d, h, bytes, cudaMemcpyHostToDevice, st));
+      return d;
+    };
+    const int* d_j = (const int*)up(7, job_ids, sizeof(int) * n_jobs);
+    const int* d_st = (const int*)up(9, steps.data(), sizeof(int) * n_jobs);
+    const int* d_so = (const int*)up(1, src_off, sizeof(int) * (n_jobs + 1));
+    const int* d_sc = (const int*)up(2, src_cams, sizeof(int) * nsrc);
+    const double* d_sf = (const double*)up(3, src_fracs, sizeof(double) * nsrc);
+    const int* d_mb = (const int*)up(8, mb.data(), sizeof(int) * n_jobs);
+    const size_t rows = (size_t)ctx->n_cams * g.ring_frames, words = (rows + 31) / 32;
+    uint32_t* want = (uint32_t*)ctx->zc_topup.get(words * 4);
+    ECCO_CUDA(cudaMemsetAsync(want, 0, words * 4, st));
+    stage::mark_sampled(ctx, st, n_jobs, d_j, d_st, max_steps, d_so, d_sc, d_sf, d_mb, depth,
+                        window, want);
+    if (!ctx->d_zc_rows) dalloc(&ctx->d_zc_rows, 1);
+    stage::fetch_rows(ctx, st, (const uint16_t*)fdev, ctx->d_frames, want, words, ctx->d_zc_rows,
+                      (uint32_t*)ctx->zc_flags_front.p);
+    ECCO_CUDA(cudaStreamSynchronize(st));  // the caller's arguments are host memory
   });
 }
 
@@ -499,6 +557,9 @@ static void swap_parts(ecco_ctx* ctx, int parts) {
     if (i == 0) {
       std::swap(ctx->d_frames, ctx->b_frames);
       std::swap(ctx->d_labels, ctx->b_labels);
+      std::swap(ctx->zc_flags, ctx->zc_flags_front);
+      ctx->ring_partial = ctx->back_partial;
+      ctx->back_partial = false;
     } else {
       std::swap(ctx->d_eval, ctx->b_eval);
       std::swap(ctx->d_eval_labels, ctx->b_eval_labels);
@@ -817,7 +878,22 @@ ecco_status ecco_route_matrix_dev(ecco_ctx* ctx, int n, int g_block, int n_block
     ECCO_REQUIRE(n == 0 || ((matrix_dev || g_block == 0) && best_col_dev && best_acc_dev),
                  "route_matrix: null buffer");
     lbackend::route_matrix(ctx, n, g_block, n_blocks, (const double*)matrix_dev,
-                           (const double*)req_dev, (int*)best_col_dev, (double*)best_acc_dev);
+                           (const double*)req_dev, nullptr, (int*)best_col_dev,
+                           (double*)best_acc_dev);
+  });
+}
+
+ecco_status ecco_route_matrix_ids_dev(ecco_ctx* ctx, int n, int g_block, int n_blocks,
+                                      const void* matrix_dev, const void* col_ids_dev,
+                                      const void* req_dev, void* best_id_dev, void* best_acc_dev) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(n >= 0 && g_block >= 0 && n_blocks >= 1, "route_matrix_ids: bad size");
+    ECCO_REQUIRE(n == 0 || ((matrix_dev || g_block == 0) && best_id_dev && best_acc_dev &&
+                            (col_ids_dev || g_block == 0)),
+                 "route_matrix_ids: null buffer");
+    lbackend::route_matrix(ctx, n, g_block, n_blocks, (const double*)matrix_dev,
+                           (const double*)req_dev, (const int*)col_ids_dev, (int*)best_id_dev,
+                           (double*)best_acc_dev);
   });
 }
 
@@ -893,6 +969,27 @@ ecco_status ecco_train_trajectories(ecco_ctx* ctx, int n_jobs, const int* job_id
       std::vector<int> mb(n_jobs, 0);
       if (micro_base) mb.assign(micro_base, micro_base + n_jobs);
       int* d_mb = (int*)up(8, mb.data(), sizeof(int) * n_jobs);
+      if (ctx->ring_partial) {
+        // the current rings hold only the rows a sampled staging fetched:
+        // every draw of THIS call must be among them, or its arguments
+        // differ from the staging call's (the chain would read stale rows)
+        int max_steps = 0;
+        for (int v : steps) max_steps = std::max(max_steps, v);
+        int* d_st = (int*)up(9, steps.data(), sizeof(int) * n_jobs);
+        unsigned* d_miss = (unsigned*)ctx->zc_missing.get(sizeof(unsigned));
+        ECCO_CUDA(cudaMemsetAsync(d_miss, 0, sizeof(unsigned), ctx->stream));
+        stage::mark_sampled(ctx, ctx->stream, n_jobs, d_j, d_st, max_steps, d_so, d_sc, d_sf, d_mb,
+                            depth, window, nullptr, (const uint32_t*)ctx->zc_flags_front.p, d_miss);
+        unsigned miss = 0;
+        ECCO_CUDA(ctx_memcpy(ctx, &miss, d_miss, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+        ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+        ECCO_REQUIRE_LOGIC(miss == 0, "train_trajectories: " + std::to_string(miss) +
+                                          " sampled draws read ring rows that "
+                                          "ecco_stage_sampled_frames did not stage (its arguments "
+                                          "differ from this call's): stage them with "
+                                          "ecco_fetch_sampled_frames first");
+      }
       lbackend::trajectories(ctx, n_jobs, job_ids, d_s, d_j, steps.data(), d_so, d_sc, d_sf, d_mo,
                              d_mc, d_mb, window, depth, d_out);
     } else {
@@ -919,9 +1016,8 @@ ecco_status ecco_commit(ecco_ctx* ctx, int n_jobs, const int* job_ids, const int
     auto s = slots_of(ctx, n_jobs, job_ids);
     for (int j = 0; j < n_jobs; ++j)
       if (granted[j] > 0) ctx->mark_dirty(s[j]);
-    DevBuf a, b;
-    int* d_s = (int*)a.get(sizeof(int) * n_jobs);
-    int* d_g = (int*)b.get(sizeof(int) * n_jobs);
+    int* d_s = (int*)ctx->commit_args[0].get(sizeof(int) * n_jobs);
+    int* d_g = (int*)ctx->commit_args[1].get(sizeof(int) * n_jobs);
     ECCO_CUDA(ctx_memcpy(ctx, d_s, s.data(), sizeof(int) * n_jobs, cudaMemcpyHostToDevice, ctx->stream));
     ECCO_CUDA(ctx_memcpy(ctx, d_g, granted, sizeof(int) * n_jobs, cudaMemcpyHostToDevice, ctx->stream));
     if (learned(ctx))
@@ -929,8 +1025,6 @@ ecco_status ecco_commit(ecco_ctx* ctx, int n_jobs, const int* job_ids, const int
     else
       pbackend::commit(ctx, n_jobs, d_s, d_g);
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
-    a.release();
-    b.release();
   });
 }
 

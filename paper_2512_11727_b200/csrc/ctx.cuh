@@ -32,6 +32,10 @@ struct EccoError {
   do {                                                                 \
     if (!(cond)) ecco_throw(ECCO_ERR_INVALID_ARGUMENT, (msg));         \
   } while (0)
+#define ECCO_REQUIRE_LOGIC(cond, msg)                                  \
+  do {                                                                 \
+    if (!(cond)) ecco_throw(ECCO_ERR_LOGIC, (msg));                    \
+  } while (0)
 
 // Growable device scratch buffer.
 struct DevBuf {
@@ -63,6 +67,7 @@ struct HostBuf {
     if (bytes > cap) {
       if (p) cudaFreeHost(p);
       p = nullptr;
+      cap = 0;
       size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
       if (cudaMallocHost(&p, want) != cudaSuccess) ecco_throw(ECCO_ERR_CUDA, "cudaMallocHost");
       cap = want;
@@ -191,9 +196,16 @@ struct ecco_ctx {
   // arguments on the copy stream, the bitmap of drawn ring rows, and the
   // running count of rows read from host memory over PCIe (zero-copy)
   DevBuf zc_args[6], zc_flags;
+  // The bitmap of the rows present in the CURRENT ring buffer when it came
+  // from a sampled staging (ring_partial): ecco_train_trajectories checks
+  // every draw against it, ecco_fetch_sampled_frames tops it up.  Swapped
+  // with zc_flags when the staged rings become current.
+  DevBuf zc_flags_front, zc_topup, zc_missing;
+  bool ring_partial = false, back_partial = false;
   HostBuf zc_host;                   // pinned staging of those arguments (truly async copies)
   cudaEvent_t zc_host_free = nullptr;  // the previous argument copy has read zc_host
-  DevBuf traj_args[9];  // ecco_train_trajectories' uploaded arguments
+  DevBuf traj_args[10];  // ecco_train_trajectories' uploaded arguments
+  DevBuf commit_args[2];  // ecco_commit's
   DevBuf em_args[3];    // ecco_eval_matrix(_dev)'s uploaded arguments
   DevBuf tile_ctr;      // the CTA-pair evaluation kernel's dynamic super-tile counter
   unsigned long long* d_zc_rows = nullptr;
@@ -344,11 +356,14 @@ namespace stage {
 void mark_sampled(ecco_ctx* ctx, cudaStream_t st, int n_jobs, const int* d_job_ids,
                   const int* d_steps, int max_steps, const int* d_src_off, const int* d_src_cam,
                   const double* d_src_frac, const int* d_micro_base, int depth, int window,
-                  uint32_t* d_flags);
+                  uint32_t* d_flags, const uint32_t* d_have = nullptr,
+                  unsigned* d_missing = nullptr);
 // Copies every marked row (F bf16) from mapped pinned host memory into dst
-// (same [row][F] layout), counting the rows into *d_count.
+// (same [row][F] layout), counting the rows into *d_count.  With d_have,
+// rows already marked there are skipped and the copied ones are marked.
 void fetch_rows(ecco_ctx* ctx, cudaStream_t st, const uint16_t* host_dev, uint16_t* dst,
-                const uint32_t* d_flags, size_t n_words, unsigned long long* d_count);
+                const uint32_t* d_flags, size_t n_words, unsigned long long* d_count,
+                uint32_t* d_have = nullptr);
 }  // namespace stage
 
 namespace lbackend {
@@ -372,7 +387,7 @@ void eval_pairs(ecco_ctx* ctx, int n, const int* d_cams, const int* d_slots, dou
                 const int* h_slots = nullptr);
 void debug_logits(ecco_ctx* ctx, int n, const int* h_cams, int gj, const int* h_slots, float* out);
 void route_matrix(ecco_ctx* ctx, int n, int gb, int n_blocks, const double* d_M,
-                  const double* d_req, int* d_best, double* d_best_acc);
+                  const double* d_req, const int* d_ids, int* d_best, double* d_best_acc);
 void sample_indices(ecco_ctx* ctx, int job_id, int n_src, const int* d_src_cam,
                     const double* d_src_frac, int window, int micro, int step, int* d_cam,
                     int* d_frame);

@@ -830,6 +830,16 @@ bool pair_enabled(const ecco_config& g) {
   return g.num_classes == 16 && !(e && e[0] == '0');
 }
 
+// Test knob: caps the persistent grid (CTA pairs / CTAs) so a handful of
+// cameras exercise the multi-tile regime of the production grid (C4: ~34
+// super tiles per pair) -- queue wrap, per-tile barrier phases, TMEM buffer
+// parity across tiles.  Unset or <= 0: no cap.
+int grid_cap(const char* name) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : 0;
+  return v > 0 ? v : (1 << 30);
+}
+
 int sm_count(int device) {
   static int n = 0;
   if (!n) ECCO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
@@ -977,7 +987,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
       pattr |= 1u << (g.device & 31);
     }
     const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
-    const int pairs = std::min(n_super, sm_count(g.device) / 2);
+    const int pairs = std::min({n_super, sm_count(g.device) / 2, grid_cap("ECCO_EVAL_MAX_PAIRS")});
     a.tile_ctr = (int*)ctx->tile_ctr.get(sizeof(int));
     ECCO_CUDA(cudaMemsetAsync(a.tile_ctr, 0, sizeof(int), ctx->stream));
     ECCO_TIMED(ctx, kind, flops, bytes,
@@ -987,7 +997,7 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
     ECCO_LAUNCHED(ctx);
     return;
   }
-  const int grid = std::min(a.n_tiles, sm_count(g.device));
+  const int grid = std::min({a.n_tiles, sm_count(g.device), grid_cap("ECCO_EVAL_MAX_CTAS")});
   ECCO_TIMED(ctx, kind, flops, bytes,
              (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
                                                                   *(const CUtensorMap*)sh.map_w, a)));

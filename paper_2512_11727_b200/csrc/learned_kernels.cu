@@ -604,8 +604,14 @@ __global__ void k_l_job_mean(LDims g, int n_jobs, const int* mem_off, const int*
 // probe row.  The matrix is n_blocks column blocks of gb columns, block b
 // stored row-major at M + b*n*gb (n_blocks = 1: plain n x gb row-major; the
 // all-gathered column blocks of every rank otherwise).
+// group_request's join rule (grouping.cpp:30-39) per camera row, one warp
+// per row: among unmasked columns with acc >= req the highest accuracy, ties
+// to the lowest group id (strict '>' over jobs in ascending id order).  The
+// id of column j is ids[j] when a column -> group map is given (cost-balanced
+// placement: a rank's block holds any groups), else j; ids[j] < 0 marks a
+// padding column.
 __global__ void k_l_route(int n, int gb, int n_blocks, const double* M, const double* req,
-                          int* best_col, double* best_acc) {
+                          const int* ids, int* best_col, double* best_acc) {
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (i >= n) return;
@@ -614,11 +620,13 @@ __global__ void k_l_route(int n, int gb, int n_blocks, const double* M, const do
   const double r = req ? req[i] : 0.0;
   const int g = gb * n_blocks;
   for (int j = lane; j < g; j += 32) {
+    const int id = ids ? ids[j] : j;
+    if (id < 0) continue;
     const int b = j / gb;
     const double a = M[((size_t)b * n + i) * gb + (j - b * gb)];
     if (a != a || a < r) continue;  // masked (NaN) or below the device accuracy
-    if (bc < 0 || a > ba) {
-      bc = j;
+    if (bc < 0 || a > ba || (a == ba && id < bc)) {
+      bc = id;
       ba = a;
     }
   }
@@ -664,7 +672,7 @@ void init(ecco_ctx* ctx) {
                                                                          ctx->d_proto_p, ctx->d_proto_q);
   ECCO_LAUNCHED(ctx);
   // the tensor-core math evaluates through the fused kernel (eval_kernels.cu)
-  if (ctx->cfg.math == ECCO_MATH_TC_TF32 && fused::supported(ctx)) {
+  if (ctx->cfg.math == ECCO_MATH_TC_BF16 && fused::supported(ctx)) {
     fused::init_shadow(ctx, ctx->sh_commit);
     fused::init_shadow(ctx, ctx->sh_spec);
     ctx->sh_dirty.assign(ctx->cfg.max_jobs, 1);
@@ -755,7 +763,7 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
     k_l_pair_rows<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, d_pair_slot + p0,
                                                              d_pair_cam + p0, row_off, blk_slot);
     ECCO_LAUNCHED(ctx);
-    if (ctx->cfg.math == ECCO_MATH_TC_TF32) {
+    if (ctx->cfg.math == ECCO_MATH_TC_BF16) {
       // tensor-core hidden layer: 128-row tiles that never straddle two
       // models (tiles are cut at slot changes of the 64-row pair blocks)
       std::vector<int> hslot(nb);
@@ -908,7 +916,8 @@ void route_propose(ecco_ctx* ctx, int n, const int* d_cams, const double* d_req,
     M = (double*)tmp.get(sizeof(double) * (size_t)n * gj);
     eval_matrix(ctx, n, d_cams, gj, d_slots, d_mask, M);
   }
-  k_l_route<<<nblk((size_t)n * 32, 256), 256, 0, ctx->stream>>>(n, gj, 1, M, d_req, d_best, d_best_acc);
+  k_l_route<<<nblk((size_t)n * 32, 256), 256, 0, ctx->stream>>>(n, gj, 1, M, d_req, nullptr, d_best,
+                                                                 d_best_acc);
   ECCO_LAUNCHED(ctx);
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
   tmp.release();
@@ -997,7 +1006,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   const size_t spec_stride = (size_t)T * np;
   // tensor-core path: one 128-row tile (or the whole minibatch when B < 128)
   // per job and 128 rows
-  const bool tc_math = ctx->cfg.math == ECCO_MATH_TC_TF32 && !ctx->fused_train;
+  const bool tc_math = ctx->cfg.math == ECCO_MATH_TC_BF16 && !ctx->fused_train;
   // 128-row minibatches with H a multiple of 256 run the forward in bf16
   // against a W1^T shadow the dW1 update keeps current (tc_kernels.cu)
   const bool tc_bf16 = tc_math && g.B % 128 == 0 && g.H % 256 == 0;
@@ -1141,10 +1150,10 @@ void commit(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_granted)
 }
 
 void route_matrix(ecco_ctx* ctx, int n, int gb, int n_blocks, const double* d_M,
-                  const double* d_req, int* d_best, double* d_best_acc) {
+                  const double* d_req, const int* d_ids, int* d_best, double* d_best_acc) {
   if (n == 0) return;
   k_l_route<<<nblk((size_t)n * 32, 256), 256, 0, ctx->stream>>>(n, gb, n_blocks, d_M, d_req,
-                                                                 d_best, d_best_acc);
+                                                                 d_ids, d_best, d_best_acc);
   ECCO_LAUNCHED(ctx);
 }
 

@@ -693,20 +693,53 @@ struct ecco_sim {
       ids.push_back(id);
       boxes.push_back(b);
     }
+    // Candidate search over a uniform grid of job boxes (cell = delta): a
+    // job is a candidate for request r only if r lies within delta of its
+    // member box on both axes and within eps of its members' times (else
+    // some member fails correlation_filter).  Pairs come out per request in
+    // ascending job id (the JobMap order group_request walks), pair_off[r]
+    // delimiting request r's run.
     std::vector<int> pair_job;
     std::vector<int> pair_req;
-    for (int r = 0; r < n; ++r) {
-      const Request& q = reqs[r];
+    std::vector<int> pair_off(n + 1, 0);
+    {
+      const double cell = std::max(cfg.delta, 1e-9);
+      auto cidx = [&](double v) { return (long long)std::floor(v / cell); };
+      auto ckey = [](long long gx, long long gy) {
+        return (unsigned long long)(gx * 1000003LL + gy);
+      };
+      std::unordered_map<unsigned long long, std::vector<int>> grid;  // cell -> job positions
+      std::vector<int> wide;  // boxes spanning too many cells: checked against every request
       for (size_t k = 0; k < ids.size(); ++k) {
-        if (ids[k] == exclude[r]) continue;
         const Box& b = boxes[k];
-        const double dx = q.x < b.x0 ? b.x0 - q.x : (q.x > b.x1 ? q.x - b.x1 : 0.0);
-        const double dy = q.y < b.y0 ? b.y0 - q.y : (q.y > b.y1 ? q.y - b.y1 : 0.0);
-        if (dx > cfg.delta || dy > cfg.delta) continue;
-        if (q.t - b.t0 > cfg.eps || b.t1 - q.t > cfg.eps) continue;
-        if (!correlated(jobs.at(ids[k]), q)) continue;
-        pair_job.push_back(ids[k]);
-        pair_req.push_back(r);
+        const long long x0 = cidx(b.x0 - cfg.delta), x1 = cidx(b.x1 + cfg.delta);
+        const long long y0 = cidx(b.y0 - cfg.delta), y1 = cidx(b.y1 + cfg.delta);
+        if ((x1 - x0 + 1) * (y1 - y0 + 1) > 64) {
+          wide.push_back((int)k);
+          continue;
+        }
+        for (long long gx = x0; gx <= x1; ++gx)
+          for (long long gy = y0; gy <= y1; ++gy) grid[ckey(gx, gy)].push_back((int)k);
+      }
+      std::vector<int> cand;
+      for (int r = 0; r < n; ++r) {
+        const Request& q = reqs[r];
+        cand.assign(wide.begin(), wide.end());
+        auto it = grid.find(ckey(cidx(q.x), cidx(q.y)));
+        if (it != grid.end()) cand.insert(cand.end(), it->second.begin(), it->second.end());
+        std::sort(cand.begin(), cand.end());  // positions in ids: ascending job id
+        for (int k : cand) {
+          if (ids[k] == exclude[r]) continue;
+          const Box& b = boxes[k];
+          const double dx = q.x < b.x0 ? b.x0 - q.x : (q.x > b.x1 ? q.x - b.x1 : 0.0);
+          const double dy = q.y < b.y0 ? b.y0 - q.y : (q.y > b.y1 ? q.y - b.y1 : 0.0);
+          if (dx > cfg.delta || dy > cfg.delta) continue;
+          if (q.t - b.t0 > cfg.eps || b.t1 - q.t > cfg.eps) continue;
+          if (!correlated(jobs.at(ids[k]), q)) continue;
+          pair_job.push_back(ids[k]);
+          pair_req.push_back(r);
+        }
+        pair_off[r + 1] = (int)pair_job.size();
       }
     }
     // (b) provisional columns: a job founded by request a can only be a
@@ -769,51 +802,58 @@ struct ecco_sim {
     if (!pj.empty())
       check(ctx, ecco_eval_pairs(ctx, (int)pj.size(), learned() ? nullptr : ps.data(), pc.data(),
                                  pj.data(), vals.data()));
-    std::unordered_map<unsigned long long, double> value;
-    auto vkey = [](int r, int job) {
-      return ((unsigned long long)(unsigned)r << 32) | (unsigned)job;
-    };
-    for (size_t i = 0; i < pair_job.size(); ++i) value[vkey(pair_req[i], pair_job[i])] = vals[i];
     size_t off = pair_job.size();
     std::vector<double> base_val(n, 0.0);
+    std::vector<double> prov_val(prov.size(), 0.0);
     if (!learned()) {
-      for (size_t i = 0; i < prov.size(); ++i)
-        value[vkey(prov[i].second, prov_id[prov[i].first])] = vals[off + i];
+      for (size_t i = 0; i < prov.size(); ++i) prov_val[i] = vals[off + i];
     } else {
       for (int r = 0; r < n; ++r) base_val[r] = vals[off + r];
     }
-    // host commit in request order
+    // founders a < b whose job may be a candidate for b, per b (ascending a:
+    // jobs created in this pass get ascending ids in request order)
+    std::vector<std::vector<int>> prov_of(n);  // indices into prov
+    for (size_t i = 0; i < prov.size(); ++i) prov_of[prov[i].second].push_back((int)i);
+    for (auto& v : prov_of)
+      std::sort(v.begin(), v.end(), [&](int x, int y) { return prov[x].first < prov[y].first; });
+    // camera -> job at batch start, kept current through the commit
+    std::vector<int> mem_of(cams.size(), -1);
+    for (const auto& [id, j] : jobs)
+      for (const auto& m : j.members) mem_of[m.cam] = id;
+    // host commit in request order (group_request, grouping.cpp:18-62): the
+    // candidates are the pairs found above (existing jobs, ascending id; a
+    // job's member set only grows, so correlation_filter is re-checked on the
+    // current members) followed by the jobs this pass created for correlated
+    // earlier requests (larger ids, ascending) -- the same jobs, in the same
+    // order, that a walk over every job would accept
+    std::vector<int> created_by(n, -1);  // request -> job it created
     std::map<int, int> founder;  // new job id -> founding request
     std::vector<int> created_ids, created_prov;
     for (int r = 0; r < n; ++r) {
       Request& q = reqs[r];
-      for (const auto& [id, j] : jobs)
-        if (j.find(q.cam) >= 0)
-          fail(ECCO_ERR_INVALID_ARGUMENT, "group_request: camera " + cams[q.cam].id +
-                                              " is already a member of job " + std::to_string(id));
+      if (mem_of[q.cam] >= 0)
+        fail(ECCO_ERR_INVALID_ARGUMENT, "group_request: camera " + cams[q.cam].id +
+                                            " is already a member of job " +
+                                            std::to_string(mem_of[q.cam]));
       int best = -1;
       double best_acc = 0.0;
-      for (const auto& [id, j] : jobs) {
-        if (exclude[r] >= 0 && id == exclude[r]) continue;
-        if (!correlated(j, q)) continue;
-        double acc;
-        auto f = founder.find(id);
-        if (f == founder.end()) {
-          auto it = value.find(vkey(r, id));
-          if (it == value.end()) fail(ECCO_ERR_LOGIC, "route: missing candidate pair");
-          acc = it->second;
-        } else if (learned()) {
-          acc = base_val[r];
-        } else {
-          auto it = value.find(vkey(r, prov_id[f->second]));
-          if (it == value.end()) fail(ECCO_ERR_LOGIC, "route: missing provisional pair");
-          acc = it->second;
-        }
-        if (acc < q.acc) continue;
+      auto consider = [&](int id, double acc) {
+        if (acc < q.acc) return;
         if (best < 0 || acc > best_acc) {
           best = id;
           best_acc = acc;
         }
+      };
+      for (int i = pair_off[r]; i < pair_off[r + 1]; ++i) {
+        const int id = pair_job[i];
+        if (!correlated(jobs.at(id), q)) continue;
+        consider(id, vals[i]);
+      }
+      for (int pi : prov_of[r]) {
+        const int id = created_by[prov[pi].first];
+        if (id < 0 || (exclude[r] >= 0 && id == exclude[r])) continue;
+        if (!correlated(jobs.at(id), q)) continue;
+        consider(id, learned() ? base_val[r] : prov_val[pi]);
       }
       if (best >= 0) {
         Job& j = jobs.at(best);
@@ -821,6 +861,7 @@ struct ecco_sim {
         const int cam = q.cam;
         j.insert(q);
         j.acc_per_member[cam] = best_acc;
+        mem_of[cam] = best;
         out[r] = {best, false, best_acc};
       } else {
         Job j;
@@ -831,7 +872,9 @@ struct ecco_sim {
         j.insert(q);
         j.acc_per_member[cam] = seed_acc;
         founder[j.id] = r;
+        created_by[r] = j.id;
         created_ids.push_back(j.id);
+        mem_of[cam] = j.id;
         out[r] = {j.id, true, seed_acc};
         jobs.emplace(j.id, std::move(j));
       }

@@ -1,4 +1,4 @@
-// Tensor-core path of the learned backend (ECCO_MATH_TC_TF32): the two dense
+// Tensor-core path of the learned backend (ECCO_MATH_TC_BF16): the two dense
 // contractions of every SGD step and of the evaluation matrix run on the 5th
 // generation tensor cores (tcgen05.mma kind::tf32, fp32 accumulators in TMEM).
 //

@@ -80,7 +80,7 @@ def _frames(ctx, n):
 
 def test_fused_logits_match_bf16_emulation():
     n_cams, ids = 9, [3, 1, 4, 7, 5]  # odd camera count: last tile half padded
-    ctx, rng = _ctx(ecco.TC_TF32, n_cams, 0)
+    ctx, rng = _ctx(ecco.TC_BF16, n_cams, 0)
     models = _random_models(ctx, rng, ids)
     cams = np.arange(n_cams)[::-1].copy()  # arbitrary probe order
     got = ctx.debug_eval_logits(ids, cams)
@@ -94,7 +94,7 @@ def test_fused_logits_match_bf16_emulation():
 
 def test_fused_counts_match_emulated_argmax():
     n_cams, ids = 12, [0, 1, 2, 3, 4, 5, 6]
-    ctx, rng = _ctx(ecco.TC_TF32, n_cams, 1)
+    ctx, rng = _ctx(ecco.TC_BF16, n_cams, 1)
     models = _random_models(ctx, rng, ids)
     M = ctx.eval_matrix(ids, cams=np.arange(n_cams))
     x, el = _frames(ctx, n_cams)
@@ -112,7 +112,7 @@ def test_fused_pairs_equal_dense_matrix():
     """eval_jobs / eval_pairs (pairs-mode tiles) reproduce the dense matrix
     entries bit for bit: every row's arithmetic is independent of its tile."""
     n_cams, ids = 10, [2, 9, 4]
-    ctx, rng = _ctx(ecco.TC_TF32, n_cams, 2)
+    ctx, rng = _ctx(ecco.TC_BF16, n_cams, 2)
     _random_models(ctx, rng, ids)
     M = ctx.eval_matrix(ids, cams=np.arange(n_cams))
     members = [[0, 3, 5], [1, 2, 4, 6, 7], [8, 9]]
@@ -131,7 +131,7 @@ def test_fused_pairs_equal_dense_matrix():
 
 def test_fused_counts_close_to_fp32_oracle_math():
     n_cams, ids = 8, [0, 1, 2, 3]
-    ctx_tc, rng = _ctx(ecco.TC_TF32, n_cams, 3)
+    ctx_tc, rng = _ctx(ecco.TC_BF16, n_cams, 3)
     models = _random_models(ctx_tc, rng, ids)
     ctx_ex, _ = _ctx(ecco.FFMA_EXACT, n_cams, 3)
     ctx_ex.seed_models(ids)
@@ -148,7 +148,7 @@ def test_fused_route_matrix_argmax():
     """ecco_route_matrix_dev over a blocked (all-gather layout) matrix equals
     the host argmax with the reference's tie rule (strict >, lowest index)."""
     import torch
-    ctx, _ = _ctx(ecco.TC_TF32, 4, 4)
+    ctx, _ = _ctx(ecco.TC_BF16, 4, 4)
     rng = np.random.default_rng(5)
     n, gb, nb = 37, 5, 3
     M = np.round(rng.random((nb, n, gb)) * 8) / 8  # many ties
@@ -180,7 +180,7 @@ def test_staged_frames_swap_in_and_match_upload():
     the same resident frames and the same evaluation as ecco_upload_frames."""
     import torch
     n_cams, ids = 6, [0, 1, 2]
-    ctx, rng = _ctx(ecco.TC_TF32, n_cams, 7)
+    ctx, rng = _ctx(ecco.TC_BF16, n_cams, 7)
     _random_models(ctx, rng, ids)
     fr, lb, ev, el = ctx.read_frames(n_cams)
     M0 = ctx.eval_matrix(ids, cams=np.arange(n_cams))
@@ -199,3 +199,85 @@ def test_staged_frames_swap_in_and_match_upload():
     assert ctx.eval_matrix(ids, cams=np.arange(n_cams)).tobytes() == M0.tobytes()
     with pytest.raises(ecco.InvalidArgument):
         ctx.swap_frames()  # nothing staged
+
+
+# ------------------------------------------- the production (multi-tile) regime --
+# At C4 the persistent grid is 74 CTA pairs over 2,500 super tiles (~34 per
+# pair): every role walks the 4-slot tile queue many times, the a_full /
+# a_empty phases and the TMEM Z / R / logits buffers alternate across tiles.
+# ECCO_EVAL_MAX_PAIRS / ECCO_EVAL_MAX_CTAS cap the grid so a few dozen
+# cameras reproduce that regime: 75 cameras = 4,800 eval rows = 19 super
+# tiles (the last one a quarter full) = 38 single-CTA tiles.
+def _cap_env(kernel):
+    return "ECCO_EVAL_MAX_PAIRS" if kernel == "pair" else "ECCO_EVAL_MAX_CTAS"
+
+
+def _emulated_counts(ctx, models, ids, cams):
+    x, el = _frames(ctx, int(max(cams)) + 1)
+    want = np.zeros((len(cams), len(ids)))
+    for jj, j in enumerate(ids):
+        for ii, c in enumerate(cams):
+            want[ii, jj] = (np.argmax(_emulate(x[c], models[j]), 1) == el[c]).sum()
+    return want
+
+
+@pytest.mark.parametrize("cap", [1, 2, 5])
+def test_multi_tile_regime_matches_full_grid_and_emulation(monkeypatch, eval_kernel, cap):
+    n_cams, ids = 75, [4, 0, 8, 2, 6, 1, 7, 3, 5]
+    ctx = ecco.Context(backend=ecco.LEARNED, math=ecco.TC_BF16, max_cameras=80, max_jobs=16,
+                       max_depth=2, **DIMS)
+    rng = np.random.default_rng(40 + cap)
+    ctx.set_cameras(np.round(rng.random((n_cams, 2)), 1), np.full(n_cams, 8.192e6))
+    ctx.generate_frames(2)
+    models = _random_models(ctx, rng, ids)
+    cams = rng.permutation(n_cams)  # arbitrary probe order
+    monkeypatch.delenv(_cap_env(eval_kernel), raising=False)
+    full = ctx.eval_matrix(ids, cams=cams)
+    monkeypatch.setenv(_cap_env(eval_kernel), str(cap))
+    for _ in range(2):  # twice: the tile counter is re-armed per launch
+        capped = ctx.eval_matrix(ids, cams=cams)
+        assert capped.tobytes() == full.tobytes()  # counts are order-independent integers
+    S = DIMS["eval_samples"]
+    want = _emulated_counts(ctx, models, ids, cams)
+    diff = np.abs(full * S - want)
+    assert diff.max() <= 2 and diff.mean() <= 0.2, (diff.max(), diff.mean())
+    # pairs mode (per-tile slot lists) in the same regime: member means equal
+    # the dense matrix's entries
+    members = [sorted(rng.choice(n_cams, 12, replace=False).tolist()) for _ in ids]
+    got = ctx.eval_jobs(ids, members)
+    inv = np.argsort(cams)
+    for jj, m in enumerate(members):
+        acc = 0.0
+        for c in m:
+            acc += full[inv[c], jj]
+        assert got[jj] == acc / len(m)
+
+
+def test_multi_tile_regime_beside_the_sampled_row_fetch(monkeypatch, eval_kernel):
+    """The evaluation kernel shares the GPU with k_fetch_rows (the e2e
+    ingest's zero-copy fetch on the copy stream, enqueued first): its counts
+    are unchanged and the staged rows are the drawn ones."""
+    import torch
+    n_cams, ids = 64, [0, 1, 2, 3, 4, 5]
+    ctx = ecco.Context(backend=ecco.LEARNED, math=ecco.TC_BF16, max_cameras=64, max_jobs=8,
+                       max_depth=2, **dict(DIMS, ring_frames=512))
+    rng = np.random.default_rng(50)
+    ctx.set_cameras(np.round(rng.random((n_cams, 2)), 1), np.full(n_cams, 8.192e6))
+    ctx.generate_frames(2)
+    _random_models(ctx, rng, ids)
+    monkeypatch.setenv(_cap_env(eval_kernel), "2")
+    full = ctx.eval_matrix(ids, cams=np.arange(n_cams))
+    fr, lb, ev, el = ctx.read_frames(n_cams)
+    pf = torch.from_numpy(fr.view(np.int16)).pin_memory()
+    pl = torch.from_numpy(lb).pin_memory()
+    members = [list(range(10 * k, 10 * k + 10)) for k in range(len(ids))]
+    p = ctx.prepare_trajectories(ids, [(30.0, 1080.0, 1.0)] * len(ids), members,
+                                 [[0.1] * 10 for _ in ids], members)
+    ctx.stage_sampled_host_ptr(p, 64.0, 2, 5, pf.data_ptr(), pl.data_ptr(), 0, 0, 0)
+    beside = ctx.eval_matrix(ids, cams=np.arange(n_cams))  # runs while the fetch may
+    assert beside.tobytes() == full.tobytes()
+    ctx.swap_frame_parts(ecco.FRAMES_RINGS)
+    fr2, lb2, _, _ = ctx.read_frames(n_cams)
+    assert lb2.tobytes() == lb.tobytes()
+    drawn = (fr2 == fr).all(-1)
+    assert drawn.any()

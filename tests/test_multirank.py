@@ -91,3 +91,41 @@ def test_block_layout_column_mapping():
     for r in range(world):
         for jb, j in enumerate(shard.rank_groups(g, world, r)):
             assert r * gb + jb == j
+
+
+def test_cost_balanced_placement():
+    """shard.Placement: LPT by members x samples, ties to the
+    lowest rank / lowest group id; new groups by the same rule; drops give
+    the load back; the gathered column map lists every group once."""
+    from paper_2512_11727_b200.shard import Placement
+    sizes = [12, 4, 8, 6, 10, 8, 5, 7]
+    costs = {g: float(n * 64) for g, n in enumerate(sizes)}
+    pl = Placement(2).place(costs)
+    assert pl.owner[0] == 0 and pl.owner[4] == 1  # the two largest first, lowest rank first
+    loads = [sum(costs[g] for g in pl.groups(r)) for r in range(2)]
+    assert loads == pl.load
+    assert abs(loads[0] - loads[1]) <= max(costs.values())
+    assert Placement(2).place(costs).owner == pl.owner  # deterministic
+    least = int(np.argmin(pl.load)) if pl.load[0] != pl.load[1] else 0
+    assert pl.add(99, 1.0) == least
+    pl.drop(99)
+    assert pl.load == loads
+    ids = pl.column_ids()
+    gb = pl.block_size()
+    assert len(ids) == 2 * gb and sorted(ids[ids >= 0].tolist()) == list(range(len(sizes)))
+    for r in range(2):
+        assert ids[r * gb:r * gb + len(pl.groups(r))].tolist() == pl.groups(r)
+    # equal costs: round robin in id order
+    eq = Placement(3).place({g: 1.0 for g in range(7)})
+    assert [eq.owner[g] for g in range(7)] == [0, 1, 2, 0, 1, 2, 0]
+    with pytest.raises(ValueError):
+        eq.add(3, 1.0)
+
+
+def test_first_exhausted_pick():
+    from paper_2512_11727_b200.window import first_exhausted
+    chain = np.array([2, 2, 2])
+    assert first_exhausted(np.array([0, 1, 2, 0, 1, 2]), chain) == -1
+    assert first_exhausted(np.array([0, 1, 0, 2, 0, 1, 1]), chain) == 4  # job 0's third pick
+    assert first_exhausted(np.array([], np.int64), chain) == -1
+    assert first_exhausted(np.array([1, 1, 1]), np.array([2, 5, 2])) == -1

@@ -30,7 +30,7 @@ def main():
     if cfg == "c5":
         dims.update(bench.DET_DIMS)
     wl = bench.Workload(cfg, 0, 1)
-    ctx = ecco.Context(backend=ecco.LEARNED, device=0, math=ecco.TC_TF32, max_cameras=wl.N,
+    ctx = ecco.Context(backend=ecco.LEARNED, device=0, math=ecco.TC_BF16, max_cameras=wl.N,
                        max_jobs=len(wl.local), max_depth=bench.DEPTH,
                        steps_per_gpu_s=float(bench.STEPS), **dims)
     ctx.set_cameras(wl.scenes, wl.tp)

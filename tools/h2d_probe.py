@@ -24,7 +24,7 @@ import numpy as np, sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_11727_b200 as ecco
 N, R, S, F = 2000, 512, 64, 512
-ctx = ecco.Context(backend=ecco.LEARNED, math=ecco.TC_TF32, max_cameras=N, max_jobs=4, max_depth=2)
+ctx = ecco.Context(backend=ecco.LEARNED, math=ecco.TC_BF16, max_cameras=N, max_jobs=4, max_depth=2)
 ctx.set_cameras(np.zeros((N, 2)), np.full(N, 8.192e6))
 fr = torch.empty((N, R, F), dtype=torch.int16, pin_memory=True)
 lb = torch.empty((N, R), dtype=torch.int32, pin_memory=True)

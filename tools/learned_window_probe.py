@@ -16,7 +16,7 @@ wins = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 spg = float(sys.argv[3]) if len(sys.argv) > 3 else 16.0 / 0.06
 spec = int(sys.argv[4]) if len(sys.argv) > 4 else 2
 sc = scenarios.config(cfg, windows=wins, seed=1, local_acc=0.0)  # fresh learned models join
-sim = ecco.Simulation(json.dumps(sc), backend=ecco.LEARNED, math=ecco.TC_TF32, full_matrix=1,
+sim = ecco.Simulation(json.dumps(sc), backend=ecco.LEARNED, math=ecco.TC_BF16, full_matrix=1,
                       steps_per_gpu_s=spg, spec_depth=spec)
 out = {"config": cfg, "windows": wins, "steps_per_gpu_s": spg, "spec_depth": spec, "gpu": []}
 while True:
