@@ -1,32 +1,36 @@
-"""Benchmark of the B200 group-retraining path (BASELINE.json `metric`).
+"""Benchmark of the B200 group-retraining path (BASELINE.json `metric`:
+group-retrain samples/s and regroup latency per window).
 
 One step = one retraining window of the hot path over the workload's
-synthetic camera streams ("Measurement"):
+synthetic camera streams, through the product's group-sharded window
+(paper_2512_11727_b200/window.py):
 
   regroup   the camera x group evaluation matrix -- every camera's S labelled
             eval frames scored under every group model (ecco_eval_matrix_dev,
             the ModelEvalFn batch of grouping.cpp:33) -- all-gathered across
             ranks, then the warp-reduced argmax/threshold per camera
-            (ecco_route_matrix_dev, group_request's join rule);
-  retrain   every group's speculative micro-window chain: evaluate, then
-            DEPTH x (STEPS SGD steps of B sampled frames, evaluate)
-            (ecco_train_trajectories, the allocator's TrainingBackend probes of
-            gpu_allocator.cpp:125-135); the chains' accuracy trajectories
-            all-gathered across ranks, the reference's greedy allocation
+            (ecco_route_matrix_ids_dev, group_request's join rule);
+  retrain   every group's speculative chain of DEPTH micro-windows x STEPS SGD
+            steps of B sampled frames (ecco_train_trajectories, the
+            allocator's TrainingBackend probes of gpu_allocator.cpp:125-135),
+            the trajectories all-gathered, the reference's greedy
             (WindowAllocation, ecco_allocate_trajectories) replayed over every
-            group on the host with W = DEPTH x G micro-windows, and
-            ecco_commit of each group's granted prefix.
+            group with W = DEPTH x G micro-windows -- chains the greedy
+            exhausts are committed and extended (exact replay, no frozen
+            accuracies) -- and each group's granted prefix committed.
 
-value = retrain samples of all ranks / max-over-ranks device time of the
-whole step (regroup included), in samples/s.  Groups are sharded across ranks
-(contiguous blocks); cameras are replicated (their frames are generated per
-rank from the counter RNG).  The only collective is the all-gather of the
-evaluation-matrix column blocks.  `e2e` is the same step through the public
-API with the window's frames uploaded from pinned host memory and the
-assignments / accuracies read back, every step.
+Keys: `value` = COMMITTED samples (granted micro-windows x steps x B) of the
+whole window / max-over-ranks device time of the window (regroup + retrain),
+the north star's "per-window regroup+retrain"; `retrain_samples_per_s` =
+the same samples / train-phase time; `regroup_ms_per_window`
+= regroup latency.  `e2e` = the same window through the public API with the
+frames ingested from pinned host memory every window and the assignments /
+accuracies read back, phase by phase.  Groups are placed on ranks by cost
+(shard.Placement); cameras are replicated (frames regenerated per rank).
 
-`--impl reference` times the CPU restatement of the same path (oracle/, the
-reference itself has no learned trainer: SURVEY.md 0) on this box's cores.
+`--impl reference` times the CPU restatement of the same train phase
+(oracle/, the reference itself has no learned trainer: SURVEY.md 0) on this
+box's cores.
 """
 import argparse
 import json
@@ -168,26 +172,31 @@ def reduce_sum(dist, value):
 # ------------------------------------------------------------------ workload --
 
 class Workload:
-    """Cameras, groups and the rank's shard (groups in contiguous blocks)."""
+    """Cameras and groups of a config: group g = cameras [g*per, (g+1)*per)
+    (one spatial cluster, scenes on a 0.1 grid per cluster)."""
 
-    def __init__(self, config, rank, world):
+    def __init__(self, config):
         self.config = config
         self.N, self.G = CONFIGS[config]
         self.per = self.N // self.G
-        self.rank, self.world = rank, world
-        from paper_2512_11727_b200 import shard
-        self.gb = shard.block_size(self.G, world)  # column block per rank (last may be ragged)
-        self.local = shard.rank_groups(self.G, world, rank)
         side = 10
         self.scenes = np.array([[0.1 * ((c // self.per) % side), 0.1 * ((c // self.per // side) % side)]
                                 for c in range(self.N)], np.float64)
         self.tp = np.full(self.N, THROUGHPUT)
+        self.groups = [list(range(g * self.per, (g + 1) * self.per)) for g in range(self.G)]
 
     def members(self, g):
-        return list(range(g * self.per, (g + 1) * self.per))
+        return self.groups[g]
 
-    def samples_per_step_local(self):
-        return len(self.local) * DEPTH * int(GPU_S * STEPS) * DIMS["minibatch"]
+
+def make_retrainer(args, wl, rank, world, dist, device, emulate=False):
+    import paper_2512_11727_b200 as ecco
+    from paper_2512_11727_b200.window import GroupRetrainer
+    math = ecco.FFMA_EXACT if args.math == "ffma" else ecco.TC_BF16
+    cls = EmulatedRank0 if emulate else GroupRetrainer
+    return cls(wl.scenes, wl.tp, wl.groups, rank=rank, world=world, dist=dist, device=device,
+               math=math, depth=DEPTH, gpu_s=GPU_S, batch=BATCH, steps_per_gpu_s=float(STEPS),
+               max_depth=8, dims=DIMS)
 
 
 # ----------------------------------------------------------------- B200 arm --
@@ -195,7 +204,6 @@ class Workload:
 def run_b200(args, rank, world, local_rank):
     import torch
     import paper_2512_11727_b200 as ecco
-    from paper_2512_11727_b200 import shard
 
     # ECCO_DIST_BACKEND=gloo (testing only) runs N ranks on however many GPUs
     # the box has, gathering through host memory; the product path is NCCL
@@ -210,86 +218,32 @@ def run_b200(args, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
-    wl = Workload(args.config, rank, world)
-    math = ecco.TC_BF16 if args.math == "tf32" else ecco.FFMA_EXACT
-    ctx = ecco.Context(backend=ecco.LEARNED, device=local_rank, math=math,
-                       max_cameras=wl.N, max_jobs=max(1, len(wl.local)), max_depth=DEPTH,
-                       steps_per_gpu_s=float(STEPS), **DIMS)
-    ctx.set_cameras(wl.scenes, wl.tp)
-    ctx.generate_frames(0)
-    ctx.seed_models(wl.local)
-    prep = ctx.prepare_trajectories(
-        wl.local, [BATCH] * len(wl.local), [wl.members(g) for g in wl.local],
-        [[1.0 / wl.per] * wl.per for _ in wl.local], [wl.members(g) for g in wl.local])
-    cams = np.arange(wl.N, dtype=np.int32)
-    stream = torch.cuda.ExternalStream(ctx.stream)
-    dev = torch.device("cuda", local_rank)
-    M_local = torch.full((wl.N if MATRIX else 1, wl.gb), float("nan"), dtype=torch.float64,
-                         device=dev)
-    M_part = None if len(wl.local) == wl.gb or not MATRIX else torch.empty((wl.N, max(1, len(wl.local))),
-                                                             dtype=torch.float64, device=dev)
-    best = torch.empty(wl.N, dtype=torch.int32, device=dev)
-    best_acc = torch.empty(wl.N, dtype=torch.float64, device=dev)
-    acc_host = np.zeros((len(wl.local), DEPTH + 1))
+    wl = Workload(args.config)
+    retr = make_retrainer(args, wl, rank, world, dist, local_rank)
+    ctx, stream = retr.ctx, retr.stream
     ev = {k: torch.cuda.Event(enable_timing=True) for k in ("a", "b", "c")}
-    phase = {"regroup": 0.0, "retrain": 0.0}
-
-    def gather_trajectories(acc):
-        """[gb, DEPTH+1] per rank -> [world*gb, DEPTH+1] (group-major)."""
-        blk = np.zeros((wl.gb, DEPTH + 1))
-        blk[:len(wl.local)] = acc
-        if dist is None:
-            return blk
-        t = torch.from_numpy(blk).to(_red_device())
-        out = torch.empty((world, wl.gb, DEPTH + 1), dtype=t.dtype, device=t.device)
-        if t.is_cuda:
-            dist.all_gather_into_tensor(out, t)
-        else:
-            dist.all_gather(list(out.unbind(0)), t)
-        return out.reshape(world * wl.gb, DEPTH + 1).cpu().numpy()
+    acc = {"regroup": 0.0, "retrain": 0.0, "committed": 0, "speculative": 0, "extensions": 0,
+           "max_micro": 0}
 
     def step(w, timed=False, mid=None):
         with torch.cuda.stream(stream):
             if timed:
                 ev["a"].record(stream)
-            if not MATRIX:
-                pass
-            elif wl.local:
-                if M_part is None:
-                    ctx.eval_matrix_dev(wl.local, M_local.data_ptr(), cams=cams)
-                else:  # ragged last block: columns beyond the rank's groups stay NaN
-                    ctx.eval_matrix_dev(wl.local, M_part.data_ptr(), cams=cams)
-                    M_local[:, :len(wl.local)].copy_(M_part)
             if MATRIX:
-                if backend == "nccl":
-                    M = shard.gather_blocks(M_local, world, dist)  # NCCL all-gather of column blocks
-                else:
-                    M = shard.gather_blocks(M_local.cpu(), world, dist).to(dev)
-                ctx.route_matrix_dev(wl.N, wl.gb, M.data_ptr(), best.data_ptr(),
-                                     best_acc.data_ptr(), n_blocks=world)
+                retr.regroup()
             if timed:
                 ev["b"].record(stream)
-            if mid is not None:
-                mid()  # (e2e: this window's rings become current here)
-            if wl.local:
-                ctx.train_prepared(prep, GPU_S, DEPTH, window=w, out=acc_host)
-            # the allocator's decisions over EVERY group: trajectories
-            # all-gathered (G x (DEPTH+1) fp64), the reference's greedy
-            # (WindowAllocation, gpu_allocator.cpp:100-181) replayed on the
-            # host with W = DEPTH x G micro-windows, each rank commits the
-            # granted prefixes of its own groups
-            traj = gather_trajectories(acc_host)
-            jobs, _, _, _ = ecco.allocate_trajectories(
-                np.arange(wl.G, dtype=np.int32), np.full(wl.G, wl.per, np.int32), traj[:wl.G],
-                1.0, 1.0, DEPTH * wl.G, GPU_S, 1, True, 0)
-            counts = np.bincount(jobs, minlength=wl.G)
-            if wl.local:
-                ctx.commit(wl.local, np.minimum(counts[wl.local], DEPTH).astype(np.int32))
-            if timed:
+        retr.retrain(w, mid=mid)
+        if timed:
+            with torch.cuda.stream(stream):
                 ev["c"].record(stream)
-                ev["c"].synchronize()
-                phase["regroup"] += ev["a"].elapsed_time(ev["b"])
-                phase["retrain"] += ev["b"].elapsed_time(ev["c"])
+            ev["c"].synchronize()
+            acc["regroup"] += ev["a"].elapsed_time(ev["b"])
+            acc["retrain"] += ev["b"].elapsed_time(ev["c"])
+            acc["committed"] += retr.stats["committed_samples"]
+            acc["speculative"] += retr.stats["speculative_samples"]
+            acc["extensions"] += retr.stats["extensions"]
+            acc["max_micro"] = max(acc["max_micro"], retr.stats["max_micro_windows"])
 
     def barrier():
         torch.cuda.synchronize()
@@ -321,30 +275,40 @@ def run_b200(args, rank, world, local_rank):
     # <= 512, H = 256 / 512), else the unfused forward; DW1 / HEAD are the
     # unfused tensor-core / FFMA kernels (other shapes, --math ffma)
     F, H = DIMS["feat_dim"], DIMS["hidden_dim"]
-    chain = (args.math == "tf32" and DIMS["minibatch"] == 128 and DIMS["num_classes"] == 16
+    chain = (args.math != "ffma" and DIMS["minibatch"] == 128 and DIMS["num_classes"] == 16
              and F <= 512 and F % 128 == 0 and F & (F - 1) == 0 and H in (256, 512))
     kst = {name: ctx.kernel_stat(getattr(ecco, "KSTAT_" + stat)) for name, stat in
            (("EVAL_MATRIX", "EVAL_MATRIX"), ("EVAL_PAIRS", "EVAL_PAIRS"),
             ("TRAIN_CHAIN" if chain else "TRAIN_FWD", "TRAIN_STEP"), ("TRAIN_DW1", "TRAIN_DW1"),
             ("TRAIN_HEAD", "TRAIN_HEAD"))}
     ctx.profile(False)
-    ms, regroup_ms, retrain_ms = reduce_max(dist, [ms, phase["regroup"], phase["retrain"]])
-    samples = reduce_sum(dist, wl.samples_per_step_local() * args.steps)
+    ms, regroup_ms, retrain_ms = reduce_max(dist, [ms, acc["regroup"], acc["retrain"]])
+    samples = acc["committed"]  # every rank replays the same schedule: already global
+    parity = None
+    if not args.no_parity:
+        try:
+            parity = parity_spot_check(args, retr, wl)
+        except Exception as e:  # reported, never fatal for the headline line
+            parity = {"error": repr(e)}
 
-    # ---- e2e: same step through the public API, frames from pinned host memory
-    e2e = None if args.no_e2e else run_e2e(args, ctx, wl, step, torch, dist, stream, best, prep)
+    # ---- e2e: same window through the public API, frames from pinned host memory
+    e2e = None if args.no_e2e else run_e2e(args, retr, wl, torch, dist)
 
     if rank == 0:
         pk, pk_kind = peaks()
         roof = roofline(kst, pk, pk_kind, args, fused=chain)
+        steps = args.steps
         line = {
             "metric": "group-retrain samples/s (per-window regroup + retrain)",
             "value": samples / (ms / 1e3),
             "unit": "samples/s",
+            "retrain_samples_per_s": samples / (retrain_ms / 1e3),
+            "regroup_ms_per_window": regroup_ms / steps,
+            "retrain_ms_per_window": retrain_ms / steps,
             "n_gpus": world,
-            "steps": args.steps,
+            "steps": steps,
             "warmup": args.warmup,
-            "ms_per_step": ms / args.steps,
+            "ms_per_step": ms / steps,
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
@@ -352,24 +316,29 @@ def run_b200(args, rank, world, local_rank):
             # and fp32 masters throughout): the fused chain and the evaluation
             # kernels run kind::f16 bf16; shapes outside the chain train with
             # a bf16 forward and a tf32 dW1; --math ffma is fp32 on CUDA cores
-            "dtype": ("f32" if args.math != "tf32" else "bf16" if chain
+            "dtype": ("f32" if args.math == "ffma" else "bf16" if chain
                       else "bf16+tf32" if DIMS["minibatch"] % 128 == 0 and H % 256 == 0 else "tf32"),
             "data": "synthetic (counter-RNG camera streams, random-init group MLPs)",
             "config": {
                 "workload": f"{args.config}: {wl.N} cameras / {wl.G} groups, learned classifier "
                             f"F{DIMS['feat_dim']}-H{DIMS['hidden_dim']}-C{DIMS['num_classes']}, "
                             f"B={DIMS['minibatch']}, S={DIMS['eval_samples']} eval frames/camera, "
-                            f"R={DIMS['ring_frames']} ring frames/camera, depth {DEPTH} x "
-                            f"{STEPS} SGD steps per group per window, "
+                            f"R={DIMS['ring_frames']} ring frames/camera, speculative depth {DEPTH} x "
+                            f"{STEPS} SGD steps per group, W = {DEPTH} x groups micro-windows, "
                             + ("full camera x group matrix" if MATRIX else
                                "marginal-gain probes only (no regroup matrix)"),
-                "cameras": wl.N, "groups": wl.G, "groups_per_rank": wl.gb,
-                "parallelism": f"groups sharded over {world} rank(s); eval matrix all-gather",
+                "cameras": wl.N, "groups": wl.G, "groups_per_rank": len(retr.local),
+                "parallelism": f"groups placed on {world} rank(s) by cost; eval matrix + "
+                               "trajectory all-gather",
                 "l2": "inputs larger than L2 (frames "
                       f"{wl.N * (DIMS['ring_frames'] + DIMS['eval_samples']) * DIMS['feat_dim'] * 2 / 2**30:.1f} GiB)",
             },
-            "regroup_ms_per_window": regroup_ms / args.steps,
-            "retrain_ms_per_window": retrain_ms / args.steps,
+            "samples": {"committed_per_window": samples / steps,
+                        "speculative_per_window": acc["speculative"] / steps,
+                        "chain_extensions_per_window": acc["extensions"] / steps,
+                        "max_micro_windows_one_group": acc["max_micro"],
+                        "note": "value counts COMMITTED samples (the replayed schedule's granted "
+                                "micro-windows); speculative = trained (chains + extensions)"},
             "gpu_launches": int(launches),
             "clocks": clk,
             "e2e": e2e,
@@ -377,12 +346,17 @@ def run_b200(args, rank, world, local_rank):
             "rooflines": roof[1],
             "kernels": {k: {"launches": v[0], "ms": v[1], "tflops": (v[2] / v[1] / 1e9) if v[1] else None}
                         for k, v in kst.items()},
+            "parity": parity,
         }
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_sample(wl.N, wl.G)
+            try:
+                line["cpu_baseline_blas"] = cpu_blas(wl.N, wl.G)
+            except Exception as e:
+                line["cpu_baseline_blas"] = {"error": repr(e)}
         if world == 1 and not args.no_scaling:
             try:
-                line["scaling_emulation"] = scaling_emulation(args, ms / args.steps)
+                line["scaling_emulation"] = scaling_emulation(args, ms / steps)
             except Exception as e:  # reported, never fatal for the headline line
                 line["scaling_emulation"] = {"error": repr(e)}
         if world == 1 and not args.no_parametric:
@@ -391,80 +365,50 @@ def run_b200(args, rank, world, local_rank):
             except Exception as e:  # reported, never fatal for the headline line
                 line["parametric"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)
+    retr.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
-    """One GPU standing in for rank 0 of an N-GPU run: its shard of the
-    groups (the largest block), the full camera set, the evaluation of its
-    column block, the route over N blocks (the other ranks' blocks as they
-    would arrive from the all-gather) and its chains.  The per-rank device
-    time projects the N-GPU step; the NCCL all-gather of the blocks
-    (N x cameras x block x 8 B) is not included -- at C4 and N = 8 it moves
-    40 MB per rank over NVLink."""
+def parity_spot_check(args, retr, wl, n_cams=64):
+    """The production-grid regroup matrix against the oracle-exact path: one
+    more regroup on the bench's grid (C4: ~34 super tiles per CTA pair), its
+    rows for a seeded sample of cameras compared with an FFMA_EXACT context
+    (bit-exact to the fp32 oracle) holding the same committed weights and the
+    same frames.  Reports count differences (of S) and the agreement of the
+    join decision (argmax, lowest group id on ties)."""
     import torch
     import paper_2512_11727_b200 as ecco
-    out = {}
-    for world in worlds:
-        wl = Workload(args.config, 0, world)
-        ctx = ecco.Context(backend=ecco.LEARNED, device=torch.cuda.current_device(),
-                           math=ecco.TC_BF16 if args.math == "tf32" else ecco.FFMA_EXACT,
-                           max_cameras=wl.N, max_jobs=max(1, len(wl.local)), max_depth=DEPTH,
-                           steps_per_gpu_s=float(STEPS), **DIMS)
-        ctx.set_cameras(wl.scenes, wl.tp)
-        ctx.generate_frames(0)
-        ctx.seed_models(wl.local)
-        prep = ctx.prepare_trajectories(
-            wl.local, [BATCH] * len(wl.local), [wl.members(g) for g in wl.local],
-            [[1.0 / wl.per] * wl.per for _ in wl.local], [wl.members(g) for g in wl.local])
-        cams = np.arange(wl.N, dtype=np.int32)
-        stream = torch.cuda.ExternalStream(ctx.stream)
-        blocks = torch.zeros((world, wl.N if MATRIX else 1, wl.gb), dtype=torch.float64,
-                             device="cuda")
-        best = torch.empty(wl.N, dtype=torch.int32, device="cuda")
-        best_acc = torch.empty(wl.N, dtype=torch.float64, device="cuda")
-        acc_host = np.zeros((len(wl.local), DEPTH + 1))
-
-        def step(w):
-            with torch.cuda.stream(stream):
-                if MATRIX:
-                    ctx.eval_matrix_dev(wl.local, blocks[0].data_ptr(), cams=cams)
-                    ctx.route_matrix_dev(wl.N, wl.gb, blocks.data_ptr(), best.data_ptr(),
-                                         best_acc.data_ptr(), n_blocks=world)
-                ctx.train_prepared(prep, GPU_S, DEPTH, window=w, out=acc_host)
-                # the allocator replay over all groups (other ranks' rows as
-                # the all-gather would deliver them; here zeros)
-                traj = np.zeros((world * wl.gb, DEPTH + 1))
-                traj[:len(wl.local)] = acc_host
-                jobs, _, _, _ = ecco.allocate_trajectories(
-                    np.arange(wl.G, dtype=np.int32), np.full(wl.G, wl.per, np.int32),
-                    traj[:wl.G], 1.0, 1.0, DEPTH * wl.G, GPU_S, 1, True, 0)
-                counts = np.bincount(jobs, minlength=wl.G)
-                ctx.commit(wl.local, np.minimum(counts[wl.local], DEPTH).astype(np.int32))
-
-        for w in range(2):
-            step(w + 1)
-        ctx.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        n = 3
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-        for k in range(n):
-            step(10 + k)
-        with torch.cuda.stream(stream):
-            e1.record(stream)
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / n
-        ctx.close()
-        del blocks
-        torch.cuda.empty_cache()
-        samples = wl.samples_per_step_local() * world
-        out[str(world)] = {"groups_on_rank0": len(wl.local), "rank0_ms_per_step": ms,
-                           "projected_value": samples / (ms / 1e3),
-                           "projected_efficiency": n1_ms / (world * ms)}
-    return out
+    if not MATRIX or args.math == "ffma" or not retr.local:
+        return None
+    retr.regroup()
+    retr.ctx.synchronize()
+    rng = np.random.default_rng(1234)
+    cams = np.sort(rng.choice(wl.N, min(n_cams, wl.N), replace=False)).astype(np.int32)
+    tc = retr.M_local[torch.from_numpy(cams).long().to(retr.dev), :len(retr.local)].cpu().numpy()
+    ff = ecco.Context(backend=ecco.LEARNED, device=retr.dev.index, math=ecco.FFMA_EXACT,
+                      max_cameras=wl.N, max_jobs=len(retr.local), max_depth=2,
+                      steps_per_gpu_s=float(STEPS), **DIMS)
+    ff.set_cameras(wl.scenes, wl.tp)
+    ff.generate_frames(0)
+    ff.seed_models(retr.local)
+    for g in retr.local:
+        ff.set_weights(g, *retr.ctx.get_weights(g))
+    ex = ff.eval_matrix(retr.local, cams=cams)
+    ff.close()
+    S = DIMS["eval_samples"]
+    d = np.abs(tc - ex) * S
+    ids = np.array(retr.local)
+    # join rule per camera over these groups (no threshold): max, lowest id
+    pick = lambda M: ids[np.argmax(M, axis=1)]  # local ids ascending: first max = lowest id
+    return {"cameras": int(len(cams)), "groups": int(len(ids)),
+            "max_count_diff": float(d.max()), "mean_count_diff": float(d.mean()),
+            "pairs_equal": float((d == 0).mean()),
+            "join_agreement": float((pick(tc) == pick(ex)).mean()),
+            "how": "rows of the production-grid k_eval_pair matrix (bf16 tensor cores) vs an "
+                   "FFMA_EXACT context (bit-exact to the fp32 oracle) with the same weights and "
+                   "frames; counts of S = %d eval frames" % S}
 
 
 def kernel_roofline(name, stat, pk, pk_kind, args, traffic=None, fused=True):
@@ -481,7 +425,7 @@ def kernel_roofline(name, stat, pk, pk_kind, args, traffic=None, fused=True):
         return None
     achieved = fl / (ms / 1e3) / 1e12
     ffma = 148 * 128 * 2 * 1.965e9 / 1e12
-    if args.math != "tf32" or name == "TRAIN_HEAD" or (name == "EVAL_PAIRS" and not fused):
+    if args.math == "ffma" or name == "TRAIN_HEAD" or (name == "EVAL_PAIRS" and not fused):
         peak = burst = ffma
         bound, how = "fp32", "fp32 FFMA spec (148 SM x 128 lanes x 2 x 1.965 GHz), CUDA cores"
     else:
@@ -516,9 +460,19 @@ def roofline(kst, pk, pk_kind, args, fused=True):
     return head, every
 
 
-def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev, prep):
-    """Frames uploaded from pinned host memory and results read back every step."""
+def run_e2e(args, retr, wl, torch, dist):
+    """The same window through the public API with host buffers: every
+    window's frames are ingested from pinned host memory and its results
+    read back.  Pipelined as the product runs it: window k+1's
+    eval sets stream in on the copy stream during window k; window k's drawn
+    ring rows (ecco_stage_sampled_frames: only the rows its SGD steps draw,
+    marked on the device, read zero-copy over PCIe) stream in during window
+    k's own regroup and become current before its chains; chains the replay
+    extends top their rows up (ecco_fetch_sampled_frames).  Host wall clock
+    per phase: regroup = window start -> assignments on the host; retrain =
+    -> trajectories replayed and the schedule committed."""
     import paper_2512_11727_b200 as ecco
+    ctx = retr.ctx
     R, S, F = DIMS["ring_frames"], DIMS["eval_samples"], DIMS["feat_dim"]
     fr = torch.empty((wl.N, R, F), dtype=torch.int16, pin_memory=True)
     lb = torch.empty((wl.N, R), dtype=torch.int32, pin_memory=True)
@@ -533,96 +487,188 @@ def run_e2e(args, ctx, wl, step, torch, dist, stream, best_dev, prep):
     best_host = torch.empty(wl.N, dtype=torch.int32, pin_memory=True)
     steps = max(16, args.steps)  # amortises the pipeline fill (window 0's upload is not overlapped)
     ctx.reserve_ingest()  # setup: the back buffers' device memory is allocated before the clock
-    # this rank's groups train on their members' rings only.  Default: the
-    # ring rows the window's SGD steps draw (marked on the device from the
-    # same counter-RNG draws, read zero-copy from the pinned table); with
-    # --e2e-full-rings every ring of the rank's camera range is copied.  Both
-    # add every camera's eval set and all labels.
-    c0, c1 = (wl.local[0] * wl.per, (wl.local[-1] + 1) * wl.per) if wl.local else (0, 0)
-    ptrs = (fr[c0].data_ptr() if c1 > c0 else fr.data_ptr(), lb[c0].data_ptr() if c1 > c0 else lb.data_ptr(),
-            wl.N, evf.data_ptr(), evl.data_ptr())
+    retr.set_host_frames(fr.data_ptr())
+    prep = retr.prep
 
     def stage_eval():
         ctx.stage_frames_range_host_ptr(0, 0, fr.data_ptr(), lb.data_ptr(), wl.N, evf.data_ptr(),
                                         evl.data_ptr())
 
     def stage_rings(w):
-        if args.e2e_full_rings or not wl.local:
-            ctx.stage_frames_range_host_ptr(c0, c1 - c0, ptrs[0], ptrs[1], 0, 0, 0)
+        if args.e2e_full_rings or not retr.local:
+            ctx.stage_frames_range_host_ptr(0, wl.N, fr.data_ptr(), lb.data_ptr(), 0, 0, 0)
         else:
             ctx.stage_sampled_host_ptr(prep, GPU_S, DEPTH, w, fr.data_ptr(), lb.data_ptr(), 0, 0, 0)
 
-    # double-buffered ingest in two parts on the copy stream: window k+1's
-    # eval sets stream in during window k and become current at window k+1's
-    # start (its regroup reads them); its rings (the drawn rows) stream in
-    # during window k+1's own regroup and become current between that regroup
-    # and its SGD chains (configs without a regroup matrix stage them a whole
-    # window ahead instead).  Window 0's eval sets are the only unoverlapped
-    # copy.
-    # one untimed warm-up window through the same ingest path (first-touch
-    # costs of the pinned table and the staging buffers), like the W warm-up
-    # steps of the device-only leg
+    def window(w, timed):
+        t0 = time.perf_counter()
+        if MATRIX:
+            retr.regroup()
+            with torch.cuda.stream(retr.stream):
+                best_host.copy_(retr.best, non_blocking=True)  # group assignments to the host
+            retr.stream.synchronize()
+        t1 = time.perf_counter()
+        # window w+1's eval sets stream in from here on (back buffer)
+        nxt = w + 1
+        stage_eval()
+        if not MATRIX:
+            retr.retrain(w, mid=lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS))
+            stage_rings(nxt)  # no regroup to hide behind: a window ahead
+        else:
+            retr.retrain(w, mid=lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS))
+            stage_rings(nxt)  # streams during window w+1's regroup
+        t2 = time.perf_counter()
+        ctx.swap_frame_parts(ecco.FRAMES_EVAL)
+        return t1 - t0, t2 - t1, retr.stats["committed_samples"]
+
+    # pipeline fill + one untimed warm-up window through the same ingest path
+    # (first-touch costs of the pinned table and the staging buffers)
     stage_eval()
     ctx.swap_frame_parts(ecco.FRAMES_EVAL)
     stage_rings(9_999)
-    step(9_999, mid=lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS))
+    window(9_999, False)
     ctx.synchronize()
-    h0, d0 = ctx.transfer_bytes()
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    t0 = time.perf_counter()
-    stage_eval()
-    ctx.swap_frame_parts(ecco.FRAMES_EVAL)
-    stage_rings(10_000)
+    h0, d0 = ctx.transfer_bytes()
+    rg, tr, committed = 0.0, 0.0, 0
     for k in range(steps):
-        if k + 1 < steps:
-            stage_eval()
-
-        def mid(k=k):  # window k's rings become current
-            ctx.swap_frame_parts(ecco.FRAMES_RINGS)
-            if k + 1 < steps and not MATRIX:
-                stage_rings(10_000 + k + 1)  # no regroup to hide them behind: a window ahead
-
-        step(10_000 + k, mid=mid)
-        if k + 1 < steps and MATRIX:
-            stage_rings(10_000 + k + 1)  # streams during window k+1's regroup
-        if os.environ.get("ECCO_E2E_TRACE"):
-            print(f"e2e window {k}: host {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
-        with torch.cuda.stream(stream):
-            best_host.copy_(best_dev, non_blocking=True)  # group assignments back to the host
-        if k + 1 < steps:
-            ctx.swap_frame_parts(ecco.FRAMES_EVAL)
+        a, b, c = window(10_000 + k, True)
+        rg, tr, committed = rg + a, tr + b, committed + c
     ctx.synchronize()
-    el_s = time.perf_counter() - t0
     h1, d1 = ctx.transfer_bytes()
     d1 += steps * best_host.numel() * 4
-    el_s = reduce_max(dist, [el_s])[0]
-    samples = reduce_sum(dist, wl.samples_per_step_local() * steps)
-    return {"value": samples / el_s, "unit": "samples/s",
+    rg, tr = reduce_max(dist, [rg, tr])
+    el_s = rg + tr
+    return {"value": committed / el_s, "unit": "samples/s",
             "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
             "ms_per_step": el_s * 1e3 / steps, "steps": steps,
+            "regroup_ms_per_window": rg * 1e3 / steps,
+            "retrain_ms_per_window": tr * 1e3 / steps,
+            "retrain_samples_per_s": committed / tr,
             "how": ("every window's frames from pinned host buffers on a copy stream, "
-                    + ("ecco_stage_frames_range: the full rings of this rank's group members"
+                    + ("ecco_stage_frames_range: every camera's full ring"
                        if args.e2e_full_rings else
                        "ecco_stage_sampled_frames: the ring rows this rank's SGD steps draw, marked "
                        "on the device and read zero-copy over PCIe (rows never drawn are not "
-                       "transferred)")
+                       "transferred; extended chains top up with ecco_fetch_sampled_frames)")
                     + ", all labels and every camera's eval set; double-buffered in two parts "
-                    "(ecco_swap_frame_parts): window k+1's eval sets upload during window k and "
-                    "its rings from window k's mid-point, current at window k+1's start / before "
-                    "its SGD chains + the step + assignments/accuracies read back; wall clock with "
-                    "a device synchronize at the end, window 0's unoverlapped eval-set upload "
-                    "included"),
-            "pcie_gbs": (h1 - h0) / steps / (el_s / steps) / 1e9}
+                    "(ecco_swap_frame_parts): window k+1's eval sets upload during window k, "
+                    "window k's drawn rows during its own regroup; the assignments read back "
+                    "before the retrain phase, trajectories read back for the host replay; host "
+                    "wall clock per phase (max over ranks), window 0's unoverlapped eval-set "
+                    "upload in the warm-up"),
+            "pcie_gbs": (h1 - h0) / el_s / 1e9}
+
+
+class _EmulatedMixin:
+    """Rank 0 of an N-rank job on ONE GPU: its placed groups, every camera,
+    the evaluation of its column block, the route over N blocks (the other
+    ranks' blocks zero, as if gathered) and its chains; the other ranks'
+    trajectories are stand-ins.  The all-gathers are not executed (one GPU):
+    their NVLink time is modelled separately (scaling_emulation)."""
+
+    def gather_blocks(self, M):
+        out = self.torch.zeros((self.world, *M.shape), dtype=M.dtype, device=M.device)
+        out[0].copy_(M)
+        return out
+
+    def gather_trajectories(self, acc):
+        full = np.empty((self.G, acc.shape[1]))
+        rows = acc if len(acc) else np.full((1, acc.shape[1]), 0.1)
+        for g in range(self.G):
+            full[g] = rows[self.slot_of[g]] if g in self.slot_of else rows[g % len(rows)]
+        return full
+
+    def broadcast(self, values, src):
+        return values
+
+
+def _emulated():
+    from paper_2512_11727_b200.window import GroupRetrainer
+
+    class E(_EmulatedMixin, GroupRetrainer):
+        pass
+    return E
+
+
+EmulatedRank0 = None
+
+
+def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
+    """One GPU standing in for rank 0 of an N-GPU run (its cost-balanced
+    share of the groups, the full camera set, its column block, the route
+    over N blocks, its chains, the replay over every group).  The NCCL
+    all-gathers are modelled, not measured (one GPU): the matrix blocks
+    (N x cameras x block x 8 B) and the trajectories at an assumed 600 GB/s
+    all-gather bus bandwidth over NVLink 5 plus 25 us per collective."""
+    import torch
+    global EmulatedRank0
+    EmulatedRank0 = _emulated()
+    out = {}
+    wl = Workload(args.config)
+    for world in worlds:
+        retr = make_retrainer(args, wl, 0, world, None, torch.cuda.current_device(), emulate=True)
+        for w in range(2):
+            retr.step(w + 1)
+        retr.ctx.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 3
+        committed = 0
+        with torch.cuda.stream(retr.stream):
+            e0.record(retr.stream)
+        for k in range(n):
+            retr.step(10 + k)
+            committed += retr.stats["committed_samples"]
+        with torch.cuda.stream(retr.stream):
+            e1.record(retr.stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        gb = retr.gb
+        ag_bytes = (world * wl.N * gb * 8 if MATRIX else 0) + world * gb * (DEPTH + 1) * 8
+        ag_ms = ag_bytes / 600e9 * 1e3 + 2 * 0.025
+        local = len(retr.local)
+        retr.close()
+        torch.cuda.empty_cache()
+        out[str(world)] = {"groups_on_rank0": local, "rank0_ms_per_step": ms,
+                           "allgather_model_ms": ag_ms,
+                           "projected_value": committed / n / ((ms + ag_ms) / 1e3),
+                           "projected_efficiency": n1_ms / (world * (ms + ag_ms))}
+    return out
 
 
 # ------------------------------------------------------------ CPU baselines --
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _window_units(N, G):
+    """Work of one window the CPU must do for the same committed samples:
+    the reference's sequential allocation (WindowAllocation::run_micro,
+    gpu_allocator.cpp:125-135) runs W = DEPTH x G micro-windows, each one
+    train(job) of STEPS SGD steps and two evaluate(job) over the job's
+    members (orchestrator.cpp:43-62); the regroup adds the N x G matrix."""
+    per = N // G
+    W = DEPTH * G
+    return {"micro_windows": W, "sgd_steps": W * int(GPU_S * STEPS), "train_eval_pairs": 2 * W * per,
+            "matrix_pairs": N * G if MATRIX else 0,
+            "committed_samples": W * int(GPU_S * STEPS) * DIMS["minibatch"]}
+
+
 def cpu_sample(N, G, budget_s=12.0):
-    """The oracle's restatement of the same step (FFMA-order fp32 C, one
-    thread per group) timed on a bounded sample and scaled to the window:
-    pairs of the eval matrix and SGD steps measured separately."""
+    """The oracle's restatement of the same window (oracle/ecco_oracle.c: the
+    FFMA-order fp32 C that the device FFMA path matches bit for bit, built
+    -O3 -march=x86-64-v3 so its fmaf chains vectorize) on every host core
+    (one group per thread), timed on a bounded sample and scaled to the
+    window: eval pairs (S frames each) and SGD steps measured separately."""
     import ctypes as C
     from concurrent.futures import ThreadPoolExecutor
 
@@ -666,31 +712,103 @@ def cpu_sample(N, G, budget_s=12.0):
 
     # calibrate one unit each, then size the parallel sample to ~budget_s
     t = time.perf_counter()
-    eval_work(1)
-    t_pair = time.perf_counter() - t
+    eval_work(4)
+    t_pair = (time.perf_counter() - t) / 4
     t = time.perf_counter()
-    train_work(1)
-    t_step = time.perf_counter() - t
+    train_work(2)
+    t_step = (time.perf_counter() - t) / 2
     per_thread = budget_s / 2.0
     n_pairs = max(1, int(per_thread / max(t_pair, 1e-6)))
     n_steps = max(1, int(per_thread / max(t_step, 1e-6)))
-    with ThreadPoolExecutor(cores) as ex:
+    with ThreadPoolExecutor(cores) as ex:  # ctypes releases the GIL in the C calls
         t = time.perf_counter()
         list(ex.map(eval_work, [n_pairs] * cores))
         pair_rate = n_pairs * cores / (time.perf_counter() - t)
         t = time.perf_counter()
         list(ex.map(train_work, [n_steps] * cores))
         step_rate = n_steps * cores / (time.perf_counter() - t)
-    per = N // G
-    steps_window = G * DEPTH * int(GPU_S * STEPS)
-    pairs_window = (N * G if MATRIX else 0) + G * (DEPTH + 1) * per  # regroup matrix + chain evaluations
-    window_s = pairs_window / pair_rate + steps_window / step_rate
-    samples = steps_window * B
-    return {"value": samples / window_s, "unit": "samples/s", "cores": cores, "kind": "port",
+    u = _window_units(N, G)
+    retrain_s = u["train_eval_pairs"] / pair_rate + u["sgd_steps"] / step_rate
+    regroup_s = u["matrix_pairs"] / pair_rate
+    window_s = retrain_s + regroup_s
+    return {"value": u["committed_samples"] / window_s, "unit": "samples/s", "cores": cores,
+            "kind": "port",
+            "retrain_samples_per_s": u["committed_samples"] / retrain_s,
+            "regroup_ms_per_window": regroup_s * 1e3,
+            "cpu": cpu_model(),
             "sample": f"{n_pairs * cores} eval pairs (S={S} frames each) and {n_steps * cores} "
-                      f"SGD steps (B={B}) of the oracle (oracle/ecco_oracle.c, FFMA-order fp32) on "
-                      f"{cores} threads; window = {pairs_window} pairs + {steps_window} steps, "
-                      f"scaled from the measured rates",
+                      f"SGD steps (B={B}) of the oracle (oracle/ecco_oracle.c, FFMA-order fp32, "
+                      f"AVX2/FMA-vectorized) on {cores} threads; window = {u['matrix_pairs']} "
+                      f"matrix pairs + {u['train_eval_pairs']} allocator evaluation pairs + "
+                      f"{u['sgd_steps']} SGD steps, scaled from the measured rates",
+            "window_s": window_s}
+
+
+def cpu_blas(N, G, budget_s=8.0):
+    """A BLAS-batched CPU implementation of the same window beside the port:
+    torch CPU fp32 (oneDNN / MKL GEMMs) on every core, SGD steps of many
+    groups batched as bmm (speculatively, as the device does) and member
+    evaluations as batched GEMMs; timed on a bounded sample, scaled to the
+    window's units (_window_units)."""
+    import torch
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    F, H, Cc, B, S = (DIMS["feat_dim"], DIMS["hidden_dim"], DIMS["num_classes"],
+                      DIMS["minibatch"], DIMS["eval_samples"])
+    g = 32  # groups per batched call
+    gen = torch.Generator().manual_seed(0)
+    X = torch.randn(g, B, F, generator=gen).bfloat16().float()
+    Y = torch.randint(0, Cc, (g, B), generator=gen)
+    W1 = torch.randn(g, F, H, generator=gen) * 0.05
+    b1 = torch.zeros(g, 1, H)
+    W2 = torch.randn(g, H, Cc, generator=gen) * 0.1
+    b2 = torch.zeros(g, 1, Cc)
+    E = torch.randn(g, 20 * S, F, generator=gen).bfloat16().float()
+    lr = 0.05
+
+    def sgd():
+        Z = torch.baddbmm(b1, X, W1)
+        Rl = Z.clamp_min(0)
+        Lg = torch.baddbmm(b2, Rl, W2)
+        P = torch.softmax(Lg, -1)
+        P[torch.arange(g)[:, None], torch.arange(B)[None], Y] -= 1
+        dL = P / B
+        dH = torch.bmm(dL, W2.transpose(1, 2)) * (Z > 0)
+        W2.sub_(lr * torch.bmm(Rl.transpose(1, 2), dL))
+        b2.sub_(lr * dL.sum(1, keepdim=True))
+        W1.sub_(lr * torch.bmm(X.transpose(1, 2), dH))
+        b1.sub_(lr * dH.sum(1, keepdim=True))
+
+    def evaluate():
+        Lg = torch.baddbmm(b2, torch.baddbmm(b1, E, W1).clamp_min(0), W2)
+        return Lg.argmax(-1)
+
+    with torch.no_grad():
+        sgd()
+        evaluate()
+        t = time.perf_counter()
+        n = 0
+        while time.perf_counter() - t < budget_s / 2:
+            sgd()
+            n += 1
+        step_rate = n * g / (time.perf_counter() - t)  # group-steps / s
+        t = time.perf_counter()
+        m = 0
+        while time.perf_counter() - t < budget_s / 2:
+            evaluate()
+            m += 1
+        pair_rate = m * g * 20 / (time.perf_counter() - t)  # (camera, group) pairs / s
+    u = _window_units(N, G)
+    retrain_s = u["train_eval_pairs"] / pair_rate + u["sgd_steps"] / step_rate
+    regroup_s = u["matrix_pairs"] / pair_rate
+    window_s = retrain_s + regroup_s
+    return {"value": u["committed_samples"] / window_s, "unit": "samples/s", "cores": cores,
+            "kind": "blas",
+            "retrain_samples_per_s": u["committed_samples"] / retrain_s,
+            "regroup_ms_per_window": regroup_s * 1e3, "cpu": cpu_model(),
+            "sample": f"{n * g} group SGD steps (B={B}, batched {g} groups per bmm) and "
+                      f"{m * g * 20} eval pairs (S={S}) in torch CPU fp32 on {cores} threads "
+                      f"(torch {torch.__version__}), scaled to the window",
             "window_s": window_s}
 
 
@@ -783,25 +901,30 @@ def parametric_leg(args):
     tb, sb = C.create_string_buffer(tcap), C.create_string_buffer(1 << 20)
     tl, sl = C.c_size_t(), C.c_size_t()
     R.ref_run_scenario(sc.encode(), -1, tb, tcap, C.byref(tl), sb, 1 << 20, C.byref(sl))
-    # (c) the window driver at C4 (10,000 cameras / 500 jobs, W = 1000): GPU
-    # only -- the reference needs ~40 s for window 0 there; its numbers, from
-    # the same scenario on the same kind of box, are in
-    # profiles/r01c_param_window_c4.json (tools/param_window_probe.py)
+    # (c) the window driver at C4 (10,000 cameras / 500 jobs, W = 1000) on the
+    # GPU and the UNMODIFIED reference's Simulation::step_window on one host
+    # core, same scenario, measured here (window 0 builds every camera's
+    # profile table: ~40 s for the reference), traces compared
     sc4 = json.dumps(scenarios.config("c4", windows=2, seed=1))
     sim4 = ecco.Simulation(sc4, backend=ecco.PARAMETRIC)
     w4 = []
     while sim4.step_window():
         w4.append({k: round(v, 3) for k, v in sim4.last_timings().items()})
-    sim4.close()
     ref4 = None
-    try:
-        ref4 = json.load(open(os.path.join(ROOT, "profiles", "r01c_param_window_c4.json")))
-        ref4 = ref4.get("reference_window_ms")
-    except (OSError, ValueError):
-        pass
+    if not args.no_ref_c4:
+        r4 = np.zeros(4)
+        n4 = C.c_int()
+        tb4 = C.create_string_buffer(1 << 27)
+        tl4 = C.c_size_t()
+        R.ref_time_windows_trace(sc4.encode(), 4, r4, C.byref(n4), tb4, 1 << 27, C.byref(tl4))
+        ref4 = [float(v) * 1e3 for v in r4[:n4.value]]
+        same4 = sim4.trace_csv() == tb4.raw[:tl4.value].decode()
+    sim4.close()
     out["window_c4"] = {"workload": "c4 scenario (scenarios.config('c4', windows=2, seed=1)), "
                                     "parametric backend; window 0 builds 10,000 profile tables",
-                        "gpu_windows": w4, "reference_window_ms_recorded": ref4}
+                        "gpu_windows": w4, "reference_window_ms": ref4, "reference_cores": 1,
+                        "reference_cpu": cpu_model(),
+                        "trace_identical_to_reference": same4 if ref4 is not None else None}
     # (d) the same window driver with the LEARNED backend at C4: routing and
     # regroup on the device evaluation matrix, every micro-window's SGD chain,
     # the netsim and allocator replay on the host (no reference counterpart:
@@ -830,9 +953,12 @@ def parametric_leg(args):
 
 
 def run_reference(args, rank):
+    """The reference arm: the CPU restatement of the same window (oracle
+    port, every host core), each step a bounded sample scaled to the window
+    (cpu_sample).  Rank 0 only; the other ranks exit without work."""
     if rank != 0:
         return
-    wl = Workload(args.config, 0, 1)
+    wl = Workload(args.config)
     vals = []
     for _ in range(args.warmup):
         cpu_sample(wl.N, wl.G, budget_s=2.0)
@@ -840,26 +966,30 @@ def run_reference(args, rank):
     last = None
     for _ in range(args.steps):
         last = cpu_sample(wl.N, wl.G, budget_s=args.ref_budget)
-        vals.append(last["value"])
+        vals.append(last)
     wall = time.perf_counter() - t0
-    value = statistics.median(vals)
+    value = statistics.median(v["value"] for v in vals)
     line = {
         "impl": "reference",
         "metric": "group-retrain samples/s (per-window regroup + retrain)",
-        "value": value, "unit": "samples/s", "n_gpus": 1, "steps": args.steps,
+        "value": value, "unit": "samples/s",
+        "retrain_samples_per_s": statistics.median(v["retrain_samples_per_s"] for v in vals),
+        "regroup_ms_per_window": statistics.median(v["regroup_ms_per_window"] for v in vals),
+        "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": last["window_s"] * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (counter-RNG camera streams, random-init group MLPs)",
         "config": {"workload": f"{args.config}: {wl.N} cameras / {wl.G} groups (same as the B200 arm)",
                    "cameras": wl.N, "groups": wl.G},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": last["cores"],
-                         "kind": "port", "sample": last["sample"]},
+                         "kind": "port", "sample": last["sample"], "cpu": last["cpu"]},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "wall_s": wall,
         "note": "the reference (a C++ simulator) has no learned trainer: its path is the "
                 "parametric accuracy model (SURVEY.md 0); the learned path's CPU form is the "
-                "oracle restatement, run here on every host core",
+                "oracle restatement (vectorized, bit-identical to the scalar restatement), run "
+                "here on every host core",
     }
     print(json.dumps(line), flush=True)
 
@@ -871,7 +1001,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
-    ap.add_argument("--math", default="tf32", choices=["tf32", "ffma"])
+    ap.add_argument("--math", default="bf16", choices=["bf16", "tf32", "ffma"],
+                    help="bf16: tensor-core math (tf32 is its round-1 name); ffma: fp32 exact")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
@@ -881,6 +1012,12 @@ def main():
                     help="skip the single-GPU emulation of rank 0 at N = 2, 4, 8")
     ap.add_argument("--no-parametric", action="store_true",
                     help="skip the parametric-backend vs reference-library leg")
+    ap.add_argument("--no-ref-c4", action="store_true",
+                    help="skip timing the reference's C4 parametric windows (~40 s of CPU)")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the production-grid parity spot check against the FFMA path")
+    ap.add_argument("--decisions", action="store_true",
+                    help="add the decision-agreement leg (learned window driver, FFMA vs TC)")
     args = ap.parse_args()
     global MATRIX
     if args.config == "c5":

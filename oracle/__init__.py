@@ -108,6 +108,9 @@ def ref():
                                        C.POINTER(C.c_size_t)]
         L.ref_time_windows.restype = C.c_int
         L.ref_time_windows.argtypes = [C.c_char_p, C.c_int, dp, C.POINTER(C.c_int)]
+        L.ref_time_windows_trace.restype = C.c_int
+        L.ref_time_windows_trace.argtypes = [C.c_char_p, C.c_int, dp, C.POINTER(C.c_int),
+                                             C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
         _ref = L
     return _ref
 

@@ -298,6 +298,32 @@ int ref_time_windows(const char* json, int max_windows, double* out_s, int* n_ru
   }
 }
 
+// ref_time_windows that also returns the run's trace.csv bytes (one run
+// serves both the timing and the trace comparison).
+int ref_time_windows_trace(const char* json, int max_windows, double* out_s, int* n_run,
+                           char* trace, size_t trace_cap, size_t* trace_len) {
+  try {
+    ScenarioConfig cfg = parse_scenario_json(json);
+    Simulation sim(cfg);
+    int w = 0;
+    while (w < max_windows) {
+      auto t0 = std::chrono::steady_clock::now();
+      if (!sim.step_window()) break;
+      out_s[w++] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+    *n_run = w;
+    std::ostringstream os;
+    sim.trace().write_csv(os);
+    const std::string t = os.str();
+    *trace_len = t.size();
+    std::memcpy(trace, t.data(), std::min(trace_cap, t.size()));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
 // ecco::simulate_window (netsim.cpp:64-94) on n flows "f00000".. with local
 // caps (<= 0 = absent); mean rates in flow order.  Returns 0 or the error code.
 int ref_simulate_window(int n, const double* alpha, const double* beta, const double* caps,
