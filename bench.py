@@ -15,7 +15,7 @@ synthetic camera streams, through the product's group-sharded window
             allocator's TrainingBackend probes of gpu_allocator.cpp:125-135),
             the trajectories all-gathered, the reference's greedy
             (WindowAllocation, ecco_allocate_trajectories) replayed over every
-            group with W = DEPTH x G micro-windows -- chains the greedy
+            group with W = W_PER_GROUP x G micro-windows -- chains the greedy
             exhausts are committed and extended (exact replay, no frozen
             accuracies) -- and each group's granted prefix committed.
 
@@ -56,7 +56,12 @@ CONFIGS = {
 }
 DIMS = dict(feat_dim=512, hidden_dim=256, num_classes=16, minibatch=128, ring_frames=512,
             eval_samples=64)
-DEPTH = 2             # micro-windows granted per group per window (initial pass + 1 greedy)
+W_PER_GROUP = 2       # allocator budget W = 2 x groups micro-windows (C4: W = 1000)
+DEPTH = 1             # speculative chain every group trains up front: the initial pass.  The
+                      # ECCO greedy's fairness bonus goes to the minimum-accuracy group, which on
+                      # these streams absorbs most of the remaining budget; its chain is extended
+                      # by depth doubling (window.py), the other groups' chains are never wasted
+MAX_DEPTH = 64        # deepest extension chain (snapshots: groups x MAX_DEPTH x params in HBM)
 STEPS = 16            # SGD steps per micro-window
 # configs[4]: the detection-head variant (larger per-group model and frame
 # features).  Its window is the allocator's marginal-gain probing (every
@@ -196,7 +201,7 @@ def make_retrainer(args, wl, rank, world, dist, device, emulate=False):
     cls = EmulatedRank0 if emulate else GroupRetrainer
     return cls(wl.scenes, wl.tp, wl.groups, rank=rank, world=world, dist=dist, device=device,
                math=math, depth=DEPTH, gpu_s=GPU_S, batch=BATCH, steps_per_gpu_s=float(STEPS),
-               max_depth=8, dims=DIMS)
+               micro_windows=W_PER_GROUP * wl.G, max_depth=MAX_DEPTH, dims=DIMS)
 
 
 # ----------------------------------------------------------------- B200 arm --
@@ -323,8 +328,9 @@ def run_b200(args, rank, world, local_rank):
                 "workload": f"{args.config}: {wl.N} cameras / {wl.G} groups, learned classifier "
                             f"F{DIMS['feat_dim']}-H{DIMS['hidden_dim']}-C{DIMS['num_classes']}, "
                             f"B={DIMS['minibatch']}, S={DIMS['eval_samples']} eval frames/camera, "
-                            f"R={DIMS['ring_frames']} ring frames/camera, speculative depth {DEPTH} x "
-                            f"{STEPS} SGD steps per group, W = {DEPTH} x groups micro-windows, "
+                            f"R={DIMS['ring_frames']} ring frames/camera, {STEPS} SGD steps per "
+                            f"micro-window, W = {W_PER_GROUP} x groups micro-windows (ECCO policy, "
+                            f"exact replay: speculative depth {DEPTH}, extensions up to {MAX_DEPTH}), "
                             + ("full camera x group matrix" if MATRIX else
                                "marginal-gain probes only (no regroup matrix)"),
                 "cameras": wl.N, "groups": wl.G, "groups_per_rank": len(retr.local),
@@ -653,11 +659,11 @@ def cpu_model():
 def _window_units(N, G):
     """Work of one window the CPU must do for the same committed samples:
     the reference's sequential allocation (WindowAllocation::run_micro,
-    gpu_allocator.cpp:125-135) runs W = DEPTH x G micro-windows, each one
+    gpu_allocator.cpp:125-135) runs W = W_PER_GROUP x G micro-windows, each one
     train(job) of STEPS SGD steps and two evaluate(job) over the job's
     members (orchestrator.cpp:43-62); the regroup adds the N x G matrix."""
     per = N // G
-    W = DEPTH * G
+    W = W_PER_GROUP * G
     return {"micro_windows": W, "sgd_steps": W * int(GPU_S * STEPS), "train_eval_pairs": 2 * W * per,
             "matrix_pairs": N * G if MATRIX else 0,
             "committed_samples": W * int(GPU_S * STEPS) * DIMS["minibatch"]}
@@ -1019,10 +1025,11 @@ def main():
     ap.add_argument("--decisions", action="store_true",
                     help="add the decision-agreement leg (learned window driver, FFMA vs TC)")
     args = ap.parse_args()
-    global MATRIX
+    global MATRIX, MAX_DEPTH
     if args.config == "c5":
         DIMS.update(DET_DIMS)
         MATRIX = False
+        MAX_DEPTH = 8  # 4.2 MB of parameters per snapshot
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank)

@@ -20,9 +20,19 @@
  *       make_accuracy_probe (transmission.cpp:52-118) for many cameras at
  *       once (Simulation::profile, orchestrator.cpp:94-116).
  *
- * Parametric backend (the reference's accuracy model, bit-identical).  The
- * status -> exception mapping mirrors core/include/ecco/types.hpp:29-48.
- * Verified by oracle/dropin_test.cpp against the unmodified reference.
+ * Two backends behind the same classes:
+ *   parametric  the reference's accuracy model, bit-identical: the job's
+ *               ModelState is shipped to the device and written back;
+ *   learned     real per-group MLPs resident on the device (Device(params,
+ *               LearnedShape, ...)): a job's model is its device weights,
+ *               keyed by JobId (seeded on first use), and the probe of a
+ *               routing request is its CAMERA's labelled eval set.
+ * BatchedRouter serves group_request's ModelEvalFn for a whole routing pass
+ * from ONE ecco_eval_matrix call (both backends).
+ * The status -> exception mapping mirrors core/include/ecco/types.hpp:29-48.
+ * Verified against the unmodified reference by oracle/dropin_test.cpp
+ * (parametric) and oracle/dropin_learned_test.cpp (learned, vs the CPU
+ * oracle's trajectories).
  */
 #ifndef ECCO_B200_DROPIN_HPP_
 #define ECCO_B200_DROPIN_HPP_
@@ -30,6 +40,7 @@
 #include <algorithm>
 #include <functional>
 #include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -61,10 +72,22 @@ inline void check(ecco_ctx* c, ecco_status s, int window = 0) {
   }
 }
 
-// A parametric device context plus the CameraId <-> index table and the
-// job models it holds.
+// The learned backend's model and stream shape (ecco_config's learned
+// fields; defaults = ecco_default_config's, SURVEY.md 8(a')).
+struct LearnedShape {
+  int feat_dim = 512, hidden_dim = 256, num_classes = 16, minibatch = 128;
+  int ring_frames = 512, eval_samples = 64, max_depth = 64;
+  float sgd_lr = 0.05f, feature_noise = 1.0f;
+  double steps_per_gpu_s = 4.0;
+  uint64_t seed = 0x5eed0001ULL;
+  int math = ECCO_MATH_FFMA_EXACT;  // or ECCO_MATH_TC_BF16
+};
+
+// A device context plus the CameraId <-> index table and the job models it
+// holds.
 class Device {
  public:
+  // parametric backend
   Device(const ecco::ModelParams& p, int scene_dims, int max_clusters, int max_jobs,
          int max_cameras, int device = 0)
       : D_(scene_dims), P_(max_clusters) {
@@ -80,6 +103,48 @@ class Device {
                 p.cluster_similarity_threshold};
     c.max_depth = 64;
     check(nullptr, ecco_create(&c, &ctx_));
+  }
+  // learned backend
+  Device(const ecco::ModelParams& p, const LearnedShape& shape, int scene_dims, int max_jobs,
+         int max_cameras, int device = 0)
+      : D_(scene_dims), P_(1), learned_(true) {
+    ecco_config c;
+    ecco_default_config(&c);
+    c.backend = ECCO_BACKEND_LEARNED;
+    c.device = device;
+    c.scene_dims = scene_dims;
+    c.max_jobs = max_jobs;
+    c.max_cameras = max_cameras;
+    c.params = {p.learning_rate_k, p.similarity_lambda, p.acc_floor, p.acc_ceil,
+                p.cluster_similarity_threshold};
+    c.math = shape.math;
+    c.feat_dim = shape.feat_dim;
+    c.hidden_dim = shape.hidden_dim;
+    c.num_classes = shape.num_classes;
+    c.minibatch = shape.minibatch;
+    c.ring_frames = shape.ring_frames;
+    c.eval_samples = shape.eval_samples;
+    c.max_depth = shape.max_depth;
+    c.sgd_lr = shape.sgd_lr;
+    c.feature_noise = shape.feature_noise;
+    c.steps_per_gpu_s = shape.steps_per_gpu_s;
+    c.seed = shape.seed;
+    check(nullptr, ecco_create(&c, &ctx_));
+  }
+  bool learned() const { return learned_; }
+  // learned: the window's synthetic streams (frame rings + eval sets) of
+  // every camera, from (seed, camera, window, scene)
+  void generate_frames(int window) { check(ctx_, ecco_generate_frames(ctx_, window)); }
+  // learned: a job's device model, seeded on first use (the learned
+  // seed_model: the base model every new job starts from)
+  void ensure_model(ecco::JobId id) {
+    if (seeded_.count(id)) return;
+    check(ctx_, ecco_seed_models(ctx_, 1, &id, nullptr, nullptr));
+    seeded_.insert(id);
+  }
+  void drop_model(ecco::JobId id) {
+    check(ctx_, ecco_drop_models(ctx_, 1, &id));
+    seeded_.erase(id);
   }
   ~Device() { ecco_destroy(ctx_); }
   Device(const Device&) = delete;
@@ -132,7 +197,9 @@ class Device {
  private:
   ecco_ctx* ctx_ = nullptr;
   int D_, P_;
+  bool learned_ = false;
   std::map<ecco::CameraId, int> index_;
+  std::set<ecco::JobId> seeded_;
 };
 
 // JobTrainingBackend (orchestrator.cpp:31-70) on the device.  Construct it
@@ -148,7 +215,10 @@ class CudaTrainingBackend final : public ecco::TrainingBackend {
       : dev_(dev), jobs_(jobs), gpu_s_(micro_gpu_s), depth_(std::max(1, depth)),
         window_(window) {
     for (auto& [id, job] : jobs_) {
-      dev_.put_model(id, job.model);
+      if (dev_.learned())
+        dev_.ensure_model(id);  // the job's weights live on the device
+      else
+        dev_.put_model(id, job.model);
       Chain c;
       const auto it = batches.find(id);
       const ecco::TrainingBatchStats b = it != batches.end() ? it->second : bootstrap(job);
@@ -181,12 +251,13 @@ class CudaTrainingBackend final : public ecco::TrainingBackend {
     ++c.used;
   }
 
-  // After run_remaining: commits every granted prefix and writes the trained
-  // models into the JobMap (what JobTrainingBackend::train did in place).
+  // After run_remaining: commits every granted prefix and, parametric,
+  // writes the trained models into the JobMap (what JobTrainingBackend::train
+  // did in place); learned models stay on the device (ecco_get_weights).
   void finish() {
     for (auto& [id, c] : chains_) {
       commit(id);
-      jobs_.at(id).model = dev_.get_model(id);
+      if (!dev_.learned()) jobs_.at(id).model = dev_.get_model(id);
     }
     prepared_ = false;
   }
@@ -259,10 +330,12 @@ class CudaTrainingBackend final : public ecco::TrainingBackend {
 };
 
 // eval_job_on_scene (orchestrator.cpp:186-191) on the device: eval(job.model,
-// probe with `scene`).  Per call it ships the job's model and evaluates one
-// pair; a routing pass that knows all its requests up front batches them
-// with ecco_eval_matrix / ecco_route_propose instead.
+// probe with `scene`), parametric backend.  Per call it ships the job's model
+// and evaluates one pair; a routing pass that knows all its requests up front
+// uses BatchedRouter (below) instead: one fused launch for the whole pass.
 inline ecco::ModelEvalFn make_eval_fn(Device& dev) {
+  if (dev.learned())
+    throw std::invalid_argument("make_eval_fn: the learned probe is a camera, use BatchedRouter");
   return [&dev](const ecco::RetrainJob& job, const ecco::SceneVector& scene) {
     if ((int)scene.size() != dev.dims()) throw std::invalid_argument("scene dimension");
     dev.put_model(job.id, job.model);
@@ -272,6 +345,95 @@ inline ecco::ModelEvalFn make_eval_fn(Device& dev) {
     return out;
   };
 }
+
+// Batched ModelEvalFn for a whole routing pass.  group_request
+// (grouping.cpp:18-62) calls eval_fn(job, request.subsamples) for every
+// correlated job, one request at a time; a routing pass
+// (route_pending_requests, orchestrator.cpp:158-184, or update_grouping's
+// reroute, grouping.cpp:113-118) knows its requests up front, so:
+//
+//   BatchedRouter router(dev, jobs, pending);  // ONE ecco_eval_matrix call
+//   for (auto& req : pending) {                // in the reference's order
+//     router.route_as(req);
+//     auto a = ecco::group_request(jobs, req, cfg, params, router.eval_fn(), next_id);
+//     if (a.created) router.created(jobs.at(a.job));
+//   }
+//
+// The probe of a request is its scene (parametric: request.subsamples, as
+// eval_job_on_scene, orchestrator.cpp:186-191) or its CAMERA's labelled eval
+// set (learned).  The constructor evaluates every (request, job) pair in one
+// fused launch; jobs created during the pass (seed_model / the learned base
+// model) are evaluated on demand.  Values equal make_eval_fn's bit for bit.
+class BatchedRouter {
+ public:
+  BatchedRouter(Device& dev, const ecco::JobMap& jobs,
+                const std::vector<ecco::RetrainRequest>& requests)
+      : dev_(dev) {
+    std::vector<int> cams, ids;
+    std::vector<double> scenes;
+    for (const auto& r : requests) {
+      if (row_.count(r.camera)) continue;
+      row_[r.camera] = (int)row_.size();
+      if (dev.learned()) cams.push_back(dev.cam(r.camera));  // the probe is its eval set
+      else {
+        if ((int)r.subsamples.size() != dev.dims()) throw std::invalid_argument("scene dimension");
+        scenes.insert(scenes.end(), r.subsamples.begin(), r.subsamples.end());
+      }
+    }
+    for (const auto& [id, j] : jobs) {
+      if (dev.learned())
+        dev.ensure_model(id);
+      else
+        dev.put_model(id, j.model);
+      col_[id] = (int)ids.size();
+      ids.push_back(id);
+    }
+    n_jobs_ = (int)ids.size();
+    m_.assign(row_.size() * ids.size(), 0.0);
+    if (!row_.empty() && !ids.empty())
+      check(dev.ctx(), ecco_eval_matrix(dev.ctx(), (int)row_.size(),
+                                        dev.learned() ? nullptr : scenes.data(),
+                                        dev.learned() ? cams.data() : nullptr, (int)ids.size(),
+                                        ids.data(), nullptr, m_.data()));
+  }
+  void route_as(const ecco::RetrainRequest& request) { cur_ = &request; }
+  // a job group_request created in this pass (it may be a candidate for the
+  // pass's later requests)
+  void created(const ecco::RetrainJob& job) {
+    if (dev_.learned())
+      dev_.ensure_model(job.id);
+    else
+      dev_.put_model(job.id, job.model);
+  }
+  ecco::ModelEvalFn eval_fn() {
+    return [this](const ecco::RetrainJob& job, const ecco::SceneVector& scene) {
+      if (!cur_) throw std::logic_error("BatchedRouter: route_as() before group_request");
+      const auto r = row_.find(cur_->camera);
+      const auto c = col_.find(job.id);
+      if (r != row_.end() && c != col_.end()) return m_[(size_t)r->second * n_jobs_ + c->second];
+      created(job);
+      const int id = job.id;
+      double out = 0.0;
+      if (dev_.learned()) {
+        const int cam = dev_.cam(cur_->camera);
+        check(dev_.ctx(), ecco_eval_pairs(dev_.ctx(), 1, nullptr, &cam, &id, &out));
+      } else {
+        if ((int)scene.size() != dev_.dims()) throw std::invalid_argument("scene dimension");
+        check(dev_.ctx(),
+              ecco_eval_matrix(dev_.ctx(), 1, scene.data(), nullptr, 1, &id, nullptr, &out));
+      }
+      return out;
+    };
+  }
+
+ private:
+  Device& dev_;
+  std::map<ecco::CameraId, int> row_;
+  std::map<ecco::JobId, int> col_;
+  std::vector<double> m_;
+  int n_jobs_ = 0;
+  const ecco::RetrainRequest* cur_ = nullptr;
+};
 
 // build_profile_table(camera, budget_levels, grid, make_accuracy_probe(camera,
 // params, reference_rate_bps, bpp_ref), opts) for every camera in one device

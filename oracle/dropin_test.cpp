@@ -11,8 +11,9 @@
 // on the same randomly generated jobs, batches and cameras; the schedules
 // (every micro-window record) and the trained models must be identical bit
 // for bit.  The reference's group_request (core/src/grouping.cpp:18-62) is
-// then run with the reference's eval_job_on_scene and with
-// ecco_b200::make_eval_fn, and every camera's profile table is built by the
+// then run with the reference's eval_job_on_scene, with
+// ecco_b200::make_eval_fn and with ecco_b200::BatchedRouter (one fused
+// evaluation matrix per routing pass), and every camera's profile table is built by the
 // reference's build_profile_table + make_accuracy_probe and by
 // ecco_b200::build_profile_tables; assignments and rows must be identical.
 //
@@ -199,17 +200,31 @@ int main(int argc, char** argv) {
       return eval(job.model, probe, params);
     };
     const ModelEvalFn eval_b200 = ecco_b200::make_eval_fn(dev);
-    JobMap ga = ja, gb = ja;
-    JobId next_a = 1000, next_b = 1000;
+    JobMap ga = ja, gb = ja, gc = ja;
+    JobId next_a = 1000, next_b = 1000, next_c = 1000;
     int routed = 0;
+    // requests for cameras of the table (the device indexes probes by camera)
+    std::vector<RetrainRequest> pending;
     for (int q = 0; q < 12; ++q) {
       RetrainRequest r;
-      r.camera = "req" + std::to_string(q);
+      r.camera = cam_id((int)(u(rng) * n_cams));
+      bool dup = false;
+      for (const auto& p : pending) dup |= p.camera == r.camera;
+      for (const auto& [id, j] : ga) dup |= j.find_member(r.camera) != nullptr;
+      if (dup) continue;
       r.subsamples = {grid(0.05), grid(0.05)};
       r.acc = 0.1 + 0.3 * u(rng);
+      pending.push_back(r);
+    }
+    ecco_b200::BatchedRouter router(dev, gc, pending);  // one fused matrix for the pass
+    for (const auto& r : pending) {
       const GroupAssignment a = group_request(ga, r, gcfg, params, eval_ref, next_a);
       const GroupAssignment b = group_request(gb, r, gcfg, params, eval_b200, next_b);
+      router.route_as(r);
+      const GroupAssignment c = group_request(gc, r, gcfg, params, router.eval_fn(), next_c);
+      if (c.created) router.created(gc.at(c.job));
       if (a.job != b.job || a.created != b.created || !same(a.acc, b.acc)) ++bad;
+      if (a.job != c.job || a.created != c.created || !same(a.acc, c.acc)) ++bad;
       ++routed;
     }
     // ProbeFn: the profile tables of every camera (Simulation::profile's grid

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -17,12 +18,35 @@
 
 namespace {
 
+// The message of the last failed ecco_create on this thread (there is no
+// context to hold it): ecco_last_error(nullptr) returns it.
+thread_local std::string g_create_error = "no context";
+
+// Makes the context's device current for the call and restores the caller's
+// current device afterwards (several contexts on different GPUs in one
+// process must not move the calling thread's device, e.g. torch's).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) (void)cudaGetLastError();
+    if (cur != dev) {
+      ECCO_CUDA(cudaSetDevice(dev));
+      prev = cur;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 template <class F>
 ecco_status guarded(ecco_ctx* ctx, F&& f) {
   try {
     // every call runs on the context's device, whatever the calling thread
     // had current (several contexts on different GPUs in one process)
-    if (ctx) ECCO_CUDA(cudaSetDevice(ctx->cfg.device));
+    std::optional<DeviceGuard> dg;
+    if (ctx) dg.emplace(ctx->cfg.device);
     f();
     return ECCO_OK;
   } catch (const EccoError& e) {
@@ -58,6 +82,10 @@ void free_all(ecco_ctx* c) {
   for (auto& b : c->em_args) b.release();
   c->tile_ctr.release();
   c->zc_flags.release();
+  c->zc_flags_front.release();
+  c->zc_topup.release();
+  c->zc_missing.release();
+  for (auto& b : c->commit_args) b.release();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (int i = 0; i < 2; ++i) {
     if (c->copy_done[i]) cudaEventDestroy(c->copy_done[i]);
@@ -66,11 +94,18 @@ void free_all(ecco_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
 }
 
+// Zero-initialised device allocation.  The zeroing must be complete before
+// any stream touches the buffer: the context's streams are non-blocking, so a
+// legacy-stream cudaMemset (asynchronous with respect to the host) would NOT
+// be ordered before their kernels -- a kernel could write the buffer (e.g.
+// seed a model into d_w) and the late memset zero it again.  So: memset on
+// the legacy stream and wait for it.
 template <class T>
 void dalloc(T** p, size_t n) {
   if (n == 0) n = 1;
   ECCO_CUDA(cudaMalloc((void**)p, n * sizeof(T)));
   ECCO_CUDA(cudaMemset(*p, 0, n * sizeof(T)));
+  ECCO_CUDA(cudaStreamSynchronize(0));
 }
 
 bool learned(const ecco_ctx* c) { return c->cfg.backend == ECCO_BACKEND_LEARNED; }
@@ -218,8 +253,7 @@ ecco_status ecco_create(const ecco_config* cfg, ecco_ctx** out) {
     ECCO_CUDA(cudaStreamSynchronize(c->stream));
   });
   if (st != ECCO_OK) {
-    static thread_local std::string last;
-    last = c->err;
+    g_create_error = c->err;
     free_all(c);
     delete c;
     return st;
@@ -230,13 +264,18 @@ ecco_status ecco_create(const ecco_config* cfg, ecco_ctx** out) {
 
 void ecco_destroy(ecco_ctx* ctx) {
   if (!ctx) return;
+  int prev = -1;
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
   cudaSetDevice(ctx->cfg.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   free_all(ctx);
   delete ctx;
+  if (prev >= 0) cudaSetDevice(prev);
 }
 
-const char* ecco_last_error(const ecco_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+const char* ecco_last_error(const ecco_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
 
 uint64_t ecco_kernel_launches(const ecco_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
@@ -271,6 +310,7 @@ ecco_status ecco_transfer_bytes(const ecco_ctx* ctx, uint64_t* h2d, uint64_t* d2
   if (ctx->d_zc_rows) {  // + rows read from pinned host memory by the sampled-row fetch
     unsigned long long n = 0;
     if (cudaStreamSynchronize(ctx->copy_stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess ||  // (top-up fetches)
         cudaMemcpy(&n, ctx->d_zc_rows, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess)
       return ECCO_ERR_CUDA;
     *h2d += n * (uint64_t)ctx->cfg.feat_dim * 2;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -56,6 +57,17 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
+  }
+};
+
+// Per-device "attribute already set" flags for cudaFuncSetAttribute (the
+// attribute applies to the current device): thread-safe, and a device past
+// the 64 cached ones is simply set again on every launch.
+struct DeviceFlags {
+  std::atomic<uint64_t> bits{0};
+  bool done(int dev) const { return dev >= 0 && dev < 64 && ((bits.load() >> dev) & 1u); }
+  void mark(int dev) {
+    if (dev >= 0 && dev < 64) bits.fetch_or(1ull << dev);
   }
 };
 

@@ -841,8 +841,8 @@ int grid_cap(const char* name) {
 }
 
 int sm_count(int device) {
-  static int n = 0;
-  if (!n) ECCO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+  int n = 0;
+  ECCO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
   return n;
 }
 
@@ -960,11 +960,11 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
   a.stages = (int)std::min<size_t>(kMaxStages, (max_smem - fixed) / kBoxBytes);
   ECCO_REQUIRE(a.stages >= 2, "fused eval: shared memory too small for the pipeline");
   const size_t smem = fixed + (size_t)a.stages * kBoxBytes;
-  static unsigned attr = 0;  // per device: the attribute applies to the current device
-  if (!((attr >> (g.device & 31)) & 1u)) {
+  static DeviceFlags attr;  // per device: the attribute applies to the current device
+  if (!attr.done(g.device)) {
     ECCO_CUDA(cudaFuncSetAttribute(k_eval_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)max_smem));
-    attr |= 1u << (g.device & 31);
+    attr.mark(g.device);
   }
   if (a.n_tiles == 0 || n_ent == 0) return;
   const double flops = 2.0 * live_pairs * g.eval_samples *
@@ -980,11 +980,11 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
     a.stages = (int)std::min<size_t>(kMaxPairStages, (max_smem - pfixed) / kPairBox);
     ECCO_REQUIRE(a.stages >= 2, "fused eval (pair): shared memory too small for the pipeline");
     const size_t psmem = pfixed + (size_t)a.stages * kPairBox;
-    static unsigned pattr = 0;
-    if (!((pattr >> (g.device & 31)) & 1u)) {
+    static DeviceFlags pattr;
+    if (!pattr.done(g.device)) {
       ECCO_CUDA(cudaFuncSetAttribute(k_eval_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)max_smem));
-      pattr |= 1u << (g.device & 31);
+      pattr.mark(g.device);
     }
     const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
     const int pairs = std::min({n_super, sm_count(g.device) / 2, grid_cap("ECCO_EVAL_MAX_PAIRS")});

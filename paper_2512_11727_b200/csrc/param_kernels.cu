@@ -363,7 +363,8 @@ __global__ void k_p_seed(PTraj t, int n, const int* slots, const double* scenes,
 PDev make_pdev(ecco_ctx* c) {
   PDev m;
   m.p = {c->cfg.params.learning_rate_k, c->cfg.params.similarity_lambda, c->cfg.params.acc_floor,
-         c->cfg.params.acc_ceil, c->cfg.params.cluster_similarity_threshold};
+         c->cfg.params.acc_ceil, c->cfg.params.cluster_similarity_threshold,
+         exact_reciprocal_pow2(c->cfg.params.similarity_lambda)};
   m.d = c->cfg.scene_dims;
   m.kmax = c->cfg.max_clusters;
   m.T = c->cfg.max_depth + 1;

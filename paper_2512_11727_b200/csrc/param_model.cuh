@@ -4,6 +4,7 @@
 // rounding, and exp comes from the bit-exact glibc port in ecco_exp.cuh, so
 // each function returns the same double the reference returns.
 #pragma once
+#include <math.h>
 #include <stdint.h>
 
 #include "ecco_exp.cuh"
@@ -13,17 +14,34 @@
 
 struct PParams {
   double k, lambda, floor, ceil, thr;
+  // 1/lambda when lambda is a power of two (the default 0.5): x / lambda and
+  // x * (1/lambda) are then the correctly rounded value of the same exact
+  // number, so the multiply is bit-identical and skips the fp64 division
+  // (~20 dependent FP64 instructions per similarity); 0 = divide.
+  double inv_lambda_pow2;
 };
+
+// 1/lambda if lambda is a power of two whose reciprocal is a normal double, else 0.
+__host__ inline double exact_reciprocal_pow2(double lambda) {
+  int e = 0;
+  const double m = frexp(lambda, &e);  // lambda = m * 2^e, m in [0.5, 1)
+  if (!(lambda > 0.0) || m != 0.5) return 0.0;
+  const double inv = ldexp(1.0, 1 - e);
+  return (inv > 2.2250738585072014e-308 && inv < 8.98846567431158e307) ? inv : 0.0;
+}
 
 // euclidean + similarity: accuracy_model.cpp:10-17, 28-34.
 __device__ __forceinline__ double p_similarity(const double* a, const double* b, int d,
-                                               double lambda, const uint64_t* tab) {
+                                               const PParams& p, const uint64_t* tab) {
   double sq = 0.0;
   for (int i = 0; i < d; ++i) {
     const double t = __dsub_rn(a[i], b[i]);
     sq = __dadd_rn(sq, __dmul_rn(t, t));
   }
-  return ecco_exp_tab(__ddiv_rn(-__dsqrt_rn(sq), lambda), tab);
+  const double ns = -__dsqrt_rn(sq);
+  const double x = p.inv_lambda_pow2 != 0.0 ? __dmul_rn(ns, p.inv_lambda_pow2)
+                                            : __ddiv_rn(ns, p.lambda);
+  return ecco_exp_tab(x, tab);
 }
 
 // find_cluster: accuracy_model.cpp:36-49 (strict '>' from 0.0, then >= thr).
@@ -32,7 +50,7 @@ __device__ __forceinline__ int p_find_cluster(int k, const double* cl, int d, co
   int best = -1;
   double best_sim = 0.0;
   for (int c = 0; c < k; ++c) {
-    const double s = p_similarity(cl + c * d, scene, d, p.lambda, tab);
+    const double s = p_similarity(cl + c * d, scene, d, p, tab);
     if (s > best_sim) {
       best_sim = s;
       best = c;
@@ -49,7 +67,7 @@ __device__ __forceinline__ double p_eval(int k, const double* cl, const double* 
   if (k == 0 || clen == 0) return p.floor;
   const int c = p_find_cluster(k, cl, d, scene, p, tab);
   const double pr = c < 0 ? 0.0 : prof[c];
-  const double sim = p_similarity(scene, cen, d, p.lambda, tab);
+  const double sim = p_similarity(scene, cen, d, p, tab);
   return __dadd_rn(p.floor, __dmul_rn(__dmul_rn(__dsub_rn(p.ceil, p.floor), pr), sim));
 }
 

@@ -543,8 +543,8 @@ int pick_nt(int H, int ctas_per_nt1) {
 size_t smem_bytes(int NT) { return 32768 + 2 * (size_t)NT * kKC * 4; }
 
 void set_smem_attrs(int device) {  // per device: the attribute applies to the current device
-  static unsigned done = 0;
-  if ((done >> (device & 31)) & 1u) return;
+  static DeviceFlags done;
+  if (done.done(device)) return;
   const int mx = (int)smem_bytes(256);
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -552,7 +552,7 @@ void set_smem_attrs(int device) {  // per device: the attribute applies to the c
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   ECCO_CUDA(cudaFuncSetAttribute(k_tc_dw1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-  done |= 1u << (device & 31);
+  done.mark(device);
 }
 
 }  // namespace
@@ -587,11 +587,11 @@ void fwd_hidden_bf16(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_of
   const CUtensorMap map = fused::tensor_map_bf16(w1t, n_slots * H, F, kBfNT);
   FwdBfArgs a{xbase, row_off, tiles, steps, step, wbase, wstride, Z, F, H};
   const size_t sm = kBfStages * (size_t)(kBfA + kBfB);
-  static unsigned attr = 0;  // per device
-  if (!((attr >> (ctx->cfg.device & 31)) & 1u)) {
+  static DeviceFlags attr;  // per device
+  if (!attr.done(ctx->cfg.device)) {
     ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm));
-    attr |= 1u << (ctx->cfg.device & 31);
+    attr.mark(ctx->cfg.device);
   }
   const int kind = steps ? ECCO_KSTAT_TRAIN_STEP : ECCO_KSTAT_EVAL_MATRIX;
   ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 2,

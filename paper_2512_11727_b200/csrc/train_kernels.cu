@@ -731,11 +731,11 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
   a.loss_T = c.max_depth;
   a.loss_t = loss_t;
   const uint32_t smem = layout(c.feat_dim).total;
-  static unsigned attr = 0;  // per device: the attribute applies to the current device
-  if (!((attr >> (c.device & 31)) & 1u)) {  // the opt-in maximum: every supported shape fits
+  static DeviceFlags attr;  // per device: the attribute applies to the current device
+  if (!attr.done(c.device)) {  // the opt-in maximum: every supported shape fits
     ECCO_CUDA(cudaFuncSetAttribute(k_train_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    232448));
-    attr |= 1u << (c.device & 31);
+    attr.mark(c.device);
   }
   const int cs = c.hidden_dim / kHS;
   cudaLaunchConfig_t lc{};

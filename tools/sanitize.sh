@@ -1,0 +1,31 @@
+#!/bin/bash
+# compute-sanitizer over the product's kernels (memcheck,
+# synccheck and racecheck on every kernel).  Run on the GPU box from the repo
+# root: bash tools/sanitize.sh [out_dir]; writes one log per (tool, target)
+# and a summary (the ERROR SUMMARY line of each) to $OUT/summary.txt.
+OUT=${1:-gpurun_out/sanitize}
+mkdir -p "$OUT"
+CS=/usr/local/cuda/bin/compute-sanitizer
+SUM="$OUT/summary.txt"
+: > "$SUM"
+run() {  # tool name timeout cmd...
+  local tool=$1 name=$2 to=$3
+  shift 3
+  local log="$OUT/${tool}_${name}.log"
+  timeout "$to" "$CS" --tool "$tool" --target-processes all --print-limit 50 "$@" > "$log" 2>&1
+  local rc=$?
+  local errs
+  errs=$(grep -h "ERROR SUMMARY" "$log" | tr '\n' ';')
+  echo "$tool $name rc=$rc ${errs:-no summary line}" >> "$SUM"
+}
+PYT="python -m pytest -q -p no:cacheprovider -m gpu -x"
+for tool in memcheck synccheck racecheck; do
+  run $tool smoke 900 python __graft_entry__.py
+done
+for tool in memcheck synccheck; do
+  run $tool parametric 1500 $PYT tests/test_gpu_parametric.py -k "not exp_port"
+  run $tool learned 1800 $PYT tests/test_gpu_learned.py -k "not detection and not bench_shape"
+  run $tool fused_eval 1500 $PYT tests/test_gpu_fused_eval.py -k "pair and (multi_tile_regime_matches and 2 or pairs_equal or route or staged)"
+  run $tool sim 900 $PYT tests/test_gpu_sim.py -k "c1_ten or drift_recovery"
+done
+cat "$SUM"
