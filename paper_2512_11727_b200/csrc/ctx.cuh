@@ -237,7 +237,7 @@ struct ecco_ctx {
     if (slot >= 0 && slot < (int)sh_dirty.size()) sh_dirty[slot] = 1;
   }
 
-  DevBuf scratch[16];
+  DevBuf scratch[20];
   DevBuf train_scratch[10];  // [8]: bf16 W1^T shadow of the general tensor-core training path  // unfused training rows (learned_kernels.cu)  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
   HostBuf hscratch[4];
 
@@ -328,6 +328,10 @@ void init_shadow(ecco_ctx* ctx, Shadow& sh);
 void free_shadow(Shadow& sh);
 // bf16 images of the models in `slots` (W1^T only for `w1t_slots` when
 // given: the fused SGD chain writes the W1^T image of every model it trained)
+// Same from device slot lists (no host upload: stream-ordered, the host
+// does not wait), W1^T images for d_w1t_slots[0..n1) only.
+void refresh_shadow_dev(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
+                        const int* d_slots, int n, const int* d_w1t_slots, int n1);
 void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
                     const std::vector<int>& slots, const std::vector<int>* w1t_slots = nullptr);
 // Correct-prediction counts of (probe camera, model slot) pairs.  Dense mode

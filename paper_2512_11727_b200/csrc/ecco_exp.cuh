@@ -77,6 +77,47 @@ ECCO_HD double specialcase(double tmp, uint64_t sbits, uint64_t ki) {
 
 }  // namespace ecco_exp_detail
 
+// exp(x) bit-identical to glibc 2.39's x86-64 FMA variant, with the table
+// behind an accessor: tab.tail(i) / tab.sbits(i) are entries 2i / 2i+1 of the
+// 256-entry table of exp_table.inc (i = ki & 127), wherever they live.
+template <class Tab>
+ECCO_HD double ecco_exp_with(double x, const Tab& tab) {
+  using namespace ecco_exp_detail;
+  uint64_t ix = as_u(x);
+  uint32_t abstop = (uint32_t)((ix >> 52) & 0x7ff);
+  bool special = false;
+  if (abstop - 0x3c9u >= 0x3fu) {
+    if ((int32_t)(abstop - 0x3c9u) < 0) return add(x, 1.0);  // |x| < 2^-54
+    if (abstop >= 0x409u) {                                   // |x| >= 1024
+      if (ix == 0xfff0000000000000ULL) return 0.0;            // -inf
+      if (abstop >= 0x7ffu) return add(x, 1.0);               // inf or nan
+      return (ix >> 63) ? 0.0 : as_d(0x7ff0000000000000ULL);  // under/overflow
+    }
+    special = true;  // large |x| that may still be representable
+  }
+  double kd = fmad(x, as_d(ECCO_EXP_INVLN2N), as_d(ECCO_EXP_SHIFT));
+  uint64_t ki = as_u(kd);
+  kd = sub(kd, as_d(ECCO_EXP_SHIFT));
+  double r = fmad(kd, as_d(ECCO_EXP_NEGLN2HIN), x);
+  r = fmad(kd, as_d(ECCO_EXP_NEGLN2LON), r);
+  const uint32_t i = (uint32_t)(ki & 127u);
+  uint64_t tail_bits, sbits0;
+  tab.get(i, tail_bits, sbits0);
+  uint64_t top = ki << 45;
+  double tail = as_d(tail_bits);
+  uint64_t sbits = sbits0 + top;
+  double p23 = fmad(r, as_d(ECCO_EXP_C3), as_d(ECCO_EXP_C2));
+  double rt = add(r, tail);
+  double r2 = mul(r, r);
+  double p45 = fmad(r, as_d(ECCO_EXP_C5), as_d(ECCO_EXP_C4));
+  double tmp = fmad(p23, r2, rt);
+  double r4 = mul(r2, r2);
+  tmp = fmad(r4, p45, tmp);
+  if (special) return specialcase(tmp, sbits, ki);
+  double scale = as_d(sbits);
+  return fmad(scale, tmp, scale);
+}
+
 // exp(x) bit-identical to glibc 2.39's x86-64 FMA variant. `tab` is the 256-entry
 // table from exp_table.inc (global, constant or shared memory).
 ECCO_HD double ecco_exp_tab(double x, const uint64_t* tab) {

@@ -891,6 +891,21 @@ void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstrid
   ECCO_LAUNCHED(ctx);
 }
 
+void refresh_shadow_dev(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstride,
+                        const int* d_slots, int n, const int* d_w1t_slots, int n1) {
+  if (n == 0) return;
+  const ecco_config& g = ctx->cfg;
+  if (n1 > 0) {
+    k_shadow_w1t<<<dim3(g.feat_dim / 32, g.hidden_dim / 32, (unsigned)n1), dim3(32, 8), 0,
+                   ctx->stream>>>(g.feat_dim, g.hidden_dim, d_w1t_slots, wbase, wstride, sh.w1t,
+                                  ctx->w1_t);
+    ECCO_LAUNCHED(ctx);
+  }
+  k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_slots, wbase,
+                                           wstride, sh.w2t, img_bytes(g));
+  ECCO_LAUNCHED(ctx);
+}
+
 void shadow_w1t(ecco_ctx* ctx, const int* d_slots, int n, const float* wbase, size_t wstride,
                 uint16_t* w1t) {
   if (n == 0) return;

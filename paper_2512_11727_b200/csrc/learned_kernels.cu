@@ -693,6 +693,50 @@ static void refresh_committed(ecco_ctx* ctx, const int* slots, int n) {
   fused::refresh_shadow(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, todo);
 }
 
+// The tile plan of a pairs-mode evaluation (which slots each 128/256-row
+// tile walks), uploaded once: a chain of micro-windows evaluates the same
+// (member, slot) pairs after every micro-window, so it reuses the plan and
+// the host never waits for the stream inside the chain (a pageable upload
+// would drain it first).
+struct PairsPlan {
+  int n_pairs = 0, n_tiles = 0, n_ent = 0;
+  bool pair = false;
+  const int* d_ent = nullptr;
+  const int* d_ebeg = nullptr;
+};
+
+static PairsPlan plan_pairs(ecco_ctx* ctx, int n_pairs, const int* h_slot, int ent_buf,
+                            int ebeg_buf) {
+  const int S = ctx->cfg.eval_samples;
+  PairsPlan pl;
+  pl.n_pairs = n_pairs;
+  pl.pair = fused::pair_supported(ctx);
+  const int TR = pl.pair ? 256 : 128;
+  pl.n_tiles = (int)(((size_t)n_pairs * S + TR - 1) / TR);
+  std::vector<int> ebeg(pl.n_tiles + 1), ent;
+  for (int m = 0; m < pl.n_tiles; ++m) {
+    ebeg[m] = (int)ent.size();
+    const int p_lo = (int)((size_t)m * TR / S);
+    const int p_hi = std::min(n_pairs, (int)(((size_t)m * TR + TR - 1) / S) + 1);
+    for (int p = p_lo; p < p_hi; ++p)
+      if (std::find(ent.begin() + ebeg[m], ent.end(), h_slot[p]) == ent.end()) ent.push_back(h_slot[p]);
+  }
+  ebeg[pl.n_tiles] = (int)ent.size();
+  pl.n_ent = (int)ent.size();
+  pl.d_ent = ctx->upload(ent_buf, ent.data(), ent.size());
+  pl.d_ebeg = ctx->upload(ebeg_buf, ebeg.data(), ebeg.size());
+  return pl;
+}
+
+static void pair_counts_planned(ecco_ctx* ctx, const Shadow& sh, const float* wbase,
+                                size_t wstride, const PairsPlan& pl, const int* d_slot,
+                                const int* d_cam, int* d_counts) {
+  ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(pl.n_pairs, 1), ctx->stream));
+  fused::eval_counts(ctx, sh, wbase, wstride, pl.n_pairs, d_cam, pl.n_ent, pl.d_ent, pl.d_ent,
+                     pl.n_tiles, pl.d_ebeg, d_slot, 0, d_counts, nullptr, (double)pl.n_pairs,
+                     pl.pair);
+}
+
 // Fused pairs-mode counts: probe p = camera h_cam/d_cam[p] under slot
 // h_slot[p]; consecutive probes of one slot share 128-row tiles.
 static void pair_counts_fused(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wstride,
@@ -1021,11 +1065,23 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     d_tiles = (TcTile*)ctx->scratch[9].get(sizeof(TcTile) * tiles.size());
     ECCO_CUDA(ctx_memcpy(ctx, d_tiles, tiles.data(), sizeof(TcTile) * tiles.size(), cudaMemcpyHostToDevice, ctx->stream));
   }
+  // the per-micro-window evaluation plan and idle-job list, uploaded once
+  PairsPlan spec_plan;
+  const int* d_idle = nullptr;
+  int n_idle = 0;
+  if (n_mem && ctx->fused_eval) {
+    spec_plan = plan_pairs(ctx, n_mem, hps.data(), 16, 17);
+    std::vector<int> idle;
+    for (int j = 0; j < n_jobs; ++j)
+      if (h_steps[j] <= 0) idle.push_back(slots[j]);
+    n_idle = (int)idle.size();
+    d_idle = ctx->upload(18, idle.data(), idle.size());
+  }
   // acc[:, 0] from the committed models
   if (n_mem && ctx->fused_eval) {
     refresh_committed(ctx, hps.data(), n_mem);
-    pair_counts_fused(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, n_mem, hps.data(), d_ps,
-                      d_mem_cam, d_cnt);
+    pair_counts_planned(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, spec_plan, d_ps, d_mem_cam,
+                        d_cnt);
   } else if (n_mem) {
     pair_counts(ctx, n_mem, d_ps, d_mem_cam, d_cnt);
   }
@@ -1103,16 +1159,12 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     }
     // evaluate state t
     if (n_mem && ctx->fused_eval) {
-      if (ctx->fused_train) {  // the chain wrote the W1^T image of every job it trained
-        std::vector<int> idle;
-        for (int j = 0; j < n_jobs; ++j)
-          if (h_steps[j] <= 0) idle.push_back(slots[j]);
-        fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots, &idle);
-      } else {
-        fused::refresh_shadow(ctx, ctx->sh_spec, wt, spec_stride, slots);
-      }
-      pair_counts_fused(ctx, ctx->sh_spec, wt, spec_stride, n_mem, hps.data(), d_ps, d_mem_cam,
-                        d_cnt);
+      // the chain wrote the W1^T image of every job it trained: only idle
+      // jobs' images are rebuilt (all of them on the unfused path)
+      fused::refresh_shadow_dev(ctx, ctx->sh_spec, wt, spec_stride, d_slots, n_jobs,
+                                ctx->fused_train ? d_idle : d_slots,
+                                ctx->fused_train ? n_idle : n_jobs);
+      pair_counts_planned(ctx, ctx->sh_spec, wt, spec_stride, spec_plan, d_ps, d_mem_cam, d_cnt);
       k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
                                                                 ctx->cfg.params.acc_floor, d_out, depth + 1, t);
       ECCO_LAUNCHED(ctx);

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "ctx.cuh"
 #include "param_model.cuh"
 
@@ -60,6 +62,62 @@ __global__ void __launch_bounds__(256) k_p_eval_matrix(PDev m, int n, const doub
   double sc[ECCO_PMAX_D];
   for (int t = 0; t < m.d; ++t) sc[t] = scenes[(size_t)i * m.d + t];
   out[o] = eval_slot(m, slots[j], sc, s_tab);
+}
+
+// K1 for a compile-time scene dimension D (every fixture and BASELINE
+// config has D = 2).  Block = 32 jobs x 8 probe rows; each block keeps its 32
+// models and the 8-way replicated exp table in shared memory and walks probe
+// rows i = blockIdx.y*8 + ty, stepping 8*gridDim.y (the table is loaded once
+// per block, not once per 8 probes).  A warp writes 32 consecutive doubles of
+// one output row.  Same arithmetic as k_p_eval_matrix, bit for bit (p_eval_t).
+template <int D>
+__global__ void __launch_bounds__(256) k_p_eval_matrix_t(PDev m, int n, const double* scenes,
+                                                         int g, const int* slots,
+                                                         const uint8_t* mask, double* out) {
+  extern __shared__ __align__(16) uint8_t psm[];
+  ulonglong2* s_rep = reinterpret_cast<ulonglong2*>(psm);      // 128 x 8 x 16 B
+  const int K = m.kmax;
+  const int stride = K * D + K + D;                             // doubles per model
+  double* s_mod = reinterpret_cast<double*>(psm + 128 * 8 * 16);  // 32 models
+  int* s_kc = reinterpret_cast<int*>(s_mod + 32 * stride);       // [32][2] k, clen
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < 128 * 8; e += 256) {
+    const int i = e >> 3;
+    s_rep[e] = make_ulonglong2(g_exp_tab[2 * i], g_exp_tab[2 * i + 1]);
+  }
+  const int j0 = blockIdx.x * 32;
+  for (int e = tid; e < 32 * stride; e += 256) {
+    const int jj = e / stride, q = e % stride;
+    if (j0 + jj >= g) continue;
+    const int slot = slots[j0 + jj];
+    double v;
+    if (q < K * D) v = m.cl[(size_t)slot * K * D + q];
+    else if (q < K * D + K) v = m.prof[(size_t)slot * K + q - K * D];
+    else v = m.cen[(size_t)slot * D + q - K * D - K];
+    s_mod[e] = v;
+  }
+  if (tid < 32 && j0 + tid < g) {
+    const int slot = slots[j0 + tid];
+    s_kc[2 * tid] = m.k[slot];
+    s_kc[2 * tid + 1] = m.clen[slot];
+  }
+  __syncthreads();
+  const int j = j0 + threadIdx.x;
+  if (j >= g) return;
+  const double* md = s_mod + threadIdx.x * stride;
+  const int k = s_kc[2 * threadIdx.x], clen = s_kc[2 * threadIdx.x + 1];
+  const RepTab tab{s_rep, (uint32_t)(threadIdx.x & 7)};
+  for (int i = blockIdx.y * 8 + threadIdx.y; i < n; i += 8 * gridDim.y) {
+    const size_t o = (size_t)i * g + j;
+    if (mask && !mask[o]) {
+      out[o] = __longlong_as_double(0x7ff8000000000000LL);
+      continue;
+    }
+    double sc[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) sc[t] = scenes[(size_t)i * D + t];
+    out[o] = p_eval_t<D>(k, md, md + K * D, clen, md + K * D + K, sc, m.p, tab);
+  }
 }
 
 // Sparse pairs: out[p] = eval(model(slot[p]), scene of probe p).
@@ -402,8 +460,21 @@ namespace pbackend {
 void eval_matrix(ecco_ctx* ctx, int n, const double* scenes, int g, const int* slots,
                  const uint8_t* mask, double* out) {
   if (n == 0 || g == 0) return;
-  dim3 grid((g + 31) / 32, (n + 7) / 8), block(32, 8);
-  k_p_eval_matrix<<<grid, block, 0, ctx->stream>>>(make_pdev(ctx), n, scenes, g, slots, mask, out);
+  const PDev m = make_pdev(ctx);
+  if (m.d == 2) {
+    // ~8 resident blocks per SM (16 KB table + 32 models each); enough probe
+    // rows per block to amortise loading them
+    int sms = 0;
+    ECCO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device));
+    const int gx = (g + 31) / 32;
+    const int gy = std::max(1, std::min((n + 7) / 8, (sms * 8 + gx - 1) / gx));
+    const size_t smem = 128 * 8 * 16 + 32 * (size_t)(m.kmax * 2 + m.kmax + 2) * 8 + 32 * 2 * 4;
+    k_p_eval_matrix_t<2><<<dim3(gx, gy), dim3(32, 8), smem, ctx->stream>>>(m, n, scenes, g, slots,
+                                                                            mask, out);
+  } else {
+    dim3 grid((g + 31) / 32, (n + 7) / 8), block(32, 8);
+    k_p_eval_matrix<<<grid, block, 0, ctx->stream>>>(m, n, scenes, g, slots, mask, out);
+  }
   ECCO_LAUNCHED(ctx);
 }
 

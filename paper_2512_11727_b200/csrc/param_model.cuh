@@ -44,6 +44,60 @@ __device__ __forceinline__ double p_similarity(const double* a, const double* b,
   return ecco_exp_tab(x, tab);
 }
 
+// The exp table in shared memory, replicated 8 times with the (tail, sbits)
+// pair of entry i of copy c at [i * 8 + c] (16 bytes): a 16-byte load is
+// served 8 lanes per wavefront, and lane l reading copy l % 8 makes every
+// wavefront bank-conflict-free whatever entries the lanes need (a single
+// copy costs ~2.5x the wavefronts on random indices; ncu r2_k1).
+struct RepTab {
+  const ulonglong2* t;
+  uint32_t c;
+  __device__ __forceinline__ void get(uint32_t i, uint64_t& tail, uint64_t& sbits) const {
+    const ulonglong2 v = t[i * 8u + c];
+    tail = v.x;
+    sbits = v.y;
+  }
+};
+
+// similarity with a compile-time scene dimension (the scene stays in
+// registers); same operation order as p_similarity.
+template <int D, class Tab>
+__device__ __forceinline__ double p_similarity_t(const double* a, const double* b,
+                                                 const PParams& p, const Tab& tab) {
+  double sq = 0.0;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const double t = __dsub_rn(a[i], b[i]);
+    sq = __dadd_rn(sq, __dmul_rn(t, t));
+  }
+  const double ns = -__dsqrt_rn(sq);
+  const double x = p.inv_lambda_pow2 != 0.0 ? __dmul_rn(ns, p.inv_lambda_pow2)
+                                            : __ddiv_rn(ns, p.lambda);
+  return ecco_exp_with(x, tab);
+}
+
+// eval (accuracy_model.cpp:60-67) with find_cluster (:36-49) inlined, scene
+// dimension D at compile time: bit-identical to p_eval.
+template <int D, class Tab>
+__device__ __forceinline__ double p_eval_t(int k, const double* cl, const double* prof, int clen,
+                                           const double* cen, const double* scene,
+                                           const PParams& p, const Tab& tab) {
+  if (k == 0 || clen == 0) return p.floor;
+  int best = -1;
+  double best_sim = 0.0;
+  for (int c = 0; c < k; ++c) {
+    const double s = p_similarity_t<D>(cl + c * D, scene, p, tab);
+    if (s > best_sim) {
+      best_sim = s;
+      best = c;
+    }
+  }
+  const int c = (best >= 0 && best_sim >= p.thr) ? best : -1;
+  const double pr = c < 0 ? 0.0 : prof[c];
+  const double sim = p_similarity_t<D>(scene, cen, p, tab);
+  return __dadd_rn(p.floor, __dmul_rn(__dmul_rn(__dsub_rn(p.ceil, p.floor), pr), sim));
+}
+
 // find_cluster: accuracy_model.cpp:36-49 (strict '>' from 0.0, then >= thr).
 __device__ __forceinline__ int p_find_cluster(int k, const double* cl, int d, const double* scene,
                                               const PParams& p, const uint64_t* tab) {

@@ -78,6 +78,32 @@ def test_eval_matrix_bit_exact(orc):
     assert gm[mask == 1].tobytes() == want[mask == 1].tobytes()
 
 
+@pytest.mark.parametrize("lam", [0.3, 0.25, 1.0])
+def test_eval_matrix_bit_exact_any_lambda(orc, lam):
+    """similarity's -sqrt(d)/lambda: a power-of-two lambda runs as an exact
+    multiply by 1/lambda (param_model.cuh), any other as the division; both
+    equal the oracle (and so the reference) bit for bit, over a matrix large
+    enough that every block walks several probe rows."""
+    rng = np.random.default_rng(11)
+    ctx = make_ctx(params=dict(similarity_lambda=lam))
+    g, n = 45, 1500
+    models = random_models(rng, g)
+    ids = np.arange(g, dtype=np.int32)
+    ctx.put_models(ids, *models)
+    scenes = rng.random((n, 2))
+    for i in range(0, n, 3):
+        j = rng.integers(0, g)
+        if models[0][j]:
+            scenes[i] = models[1][j, rng.integers(0, models[0][j])] + rng.normal(0, 0.01, 2)
+    got = ctx.eval_matrix(ids, scenes=scenes)
+    ks, cl, pr, ce, clen = models
+    want = np.zeros(n * g)
+    orc.orc_eval_matrix(n, np.ascontiguousarray(scenes).reshape(-1), g, ks, cl.reshape(-1),
+                        pr.reshape(-1), clen, ce.reshape(-1), 8, 2,
+                        oracle.orc_params(dict(P, similarity_lambda=lam)), want)
+    assert got.tobytes() == want.tobytes()
+
+
 def test_route_propose_matches_sequential_scan(orc):
     rng = np.random.default_rng(2)
     ctx = make_ctx()

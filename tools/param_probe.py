@@ -61,11 +61,18 @@ def main():
                                  "hbm_gbs_on_output": N * G * 8 / ms / 1e6}
     if which in ("k2", "all"):
         per = N // G
+        # every job's members share one cluster scene (C4 layout): train_step
+        # finds / adds one cluster per distinct scene
+        ctx2 = ecco.Context(backend=ecco.PARAMETRIC, max_jobs=G, max_cameras=N, max_clusters=8,
+                            max_depth=8)
+        sc2 = np.repeat(np.round(rng.random((G, D)), 2), per, axis=0)
+        ctx2.set_cameras(sc2, np.full(N, 8.192e6))
+        ctx2.seed_models(ids, scenes=sc2[::per], device_acc=np.full(G, 0.2))
         members = [list(range(g * per, (g + 1) * per)) for g in ids]
         fr = [[1.0 / per] * per for _ in ids]
-        p = ctx.prepare_trajectories(ids, [(15.0 * per, 720.0, 1.0)] * G, members, fr, members)
+        p = ctx2.prepare_trajectories(ids, [(15.0 * per, 720.0, 1.0)] * G, members, fr, members)
         acc = np.zeros((G, 5))
-        ms = timed(ctx, lambda: ctx.train_prepared(p, 0.06, 4, out=acc), reps)
+        ms = timed(ctx2, lambda: ctx2.train_prepared(p, 0.06, 4, out=acc), reps)
         out["k2_trajectories"] = {"jobs": G, "depth": 4, "sources": per, "ms_per_call": ms}
     if which in ("k3", "all"):
         n = 1000
