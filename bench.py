@@ -289,6 +289,12 @@ def run_b200(args, rank, world, local_rank):
     ctx.profile(False)
     ms, regroup_ms, retrain_ms = reduce_max(dist, [ms, acc["regroup"], acc["retrain"]])
     samples = acc["committed"]  # every rank replays the same schedule: already global
+    probes = None
+    if not args.no_probes:
+        try:
+            probes = probe_leg(retr, torch, dist)
+        except Exception as e:  # reported, never fatal for the headline line
+            probes = {"error": repr(e)}
     parity = None
     if not args.no_parity:
         try:
@@ -353,6 +359,7 @@ def run_b200(args, rank, world, local_rank):
             "kernels": {k: {"launches": v[0], "ms": v[1], "tflops": (v[2] / v[1] / 1e9) if v[1] else None}
                         for k, v in kst.items()},
             "parity": parity,
+            "probes": probes,
         }
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_sample(wl.N, wl.G)
@@ -375,6 +382,41 @@ def run_b200(args, rank, world, local_rank):
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+PROBE_DEPTH = 2
+
+
+def probe_leg(retr, torch, dist, reps=5):
+    """The allocator's marginal-gain probes as concurrent batched kernels
+    (the north star's third subsystem): every group's speculative chain of
+    PROBE_DEPTH micro-windows in ONE ecco_train_trajectories call (the
+    evaluate / train / evaluate probes of WindowAllocation::run_micro,
+    gpu_allocator.cpp:125-135, for all groups at once), nothing committed.
+    This is the throughput regime of the fused SGD chain (every group's
+    cluster busy); the window's exact schedule above is the latency regime
+    (the ECCO greedy serialises most of the budget on one group)."""
+    if not retr.local:
+        return None
+    ctx = retr.ctx
+    acc = np.zeros((len(retr.local), PROBE_DEPTH + 1))
+    ctx.train_prepared(retr.prep, retr.gpu_s, PROBE_DEPTH, window=77, out=acc)
+    ctx.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(retr.stream):
+        e0.record(retr.stream)
+    for k in range(reps):
+        ctx.train_prepared(retr.prep, retr.gpu_s, PROBE_DEPTH, window=78 + k, out=acc)
+    with torch.cuda.stream(retr.stream):
+        e1.record(retr.stream)
+    e1.synchronize()
+    ms = reduce_max(dist, [e0.elapsed_time(e1) / reps])[0]
+    samples = reduce_sum(dist, float(PROBE_DEPTH * int(retr.steps[retr.local].sum()) * retr.B))
+    return {"value": samples / (ms / 1e3), "unit": "samples/s", "ms_per_call": ms,
+            "depth": PROBE_DEPTH, "groups": int(retr.G),
+            "how": f"every group's {PROBE_DEPTH}-micro-window speculative chain in one "
+                   "ecco_train_trajectories call (member evaluations included, nothing "
+                   "committed), CUDA events on the context stream, max over ranks"}
 
 
 def parity_spot_check(args, retr, wl, n_cams=64):
@@ -1020,6 +1062,8 @@ def main():
                     help="skip the parametric-backend vs reference-library leg")
     ap.add_argument("--no-ref-c4", action="store_true",
                     help="skip timing the reference's C4 parametric windows (~40 s of CPU)")
+    ap.add_argument("--no-probes", action="store_true",
+                    help="skip the batched marginal-gain probe leg")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the production-grid parity spot check against the FFMA path")
     ap.add_argument("--decisions", action="store_true",

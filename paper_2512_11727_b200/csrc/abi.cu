@@ -71,6 +71,12 @@ void free_all(ecco_ctx* c) {
     if (p) cudaFree(p);
   fused::free_shadow(c->sh_commit);
   fused::free_shadow(c->sh_spec);
+  fused::free_shadow(c->sh_spec2);
+  if (c->eval_stream) cudaStreamDestroy(c->eval_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_chain[i]) cudaEventDestroy(c->ev_chain[i]);
+    if (c->ev_eval[i]) cudaEventDestroy(c->ev_eval[i]);
+  }
   delete (CUtensorMap*)c->map_x;
   for (auto& b : c->scratch) b.release();
   for (auto& b : c->train_scratch) b.release();

@@ -230,7 +230,9 @@ struct ecco_ctx {
   // fused SGD update reads and writes them coalesced; ecco_get/set_weights
   // translate to the API layout W1[F][H]
   bool w1_t = false;
-  Shadow sh_commit, sh_spec;
+  Shadow sh_commit, sh_spec, sh_spec2;  // (sh_spec / sh_spec2: alternate micro-windows)
+  cudaStream_t eval_stream = nullptr;    // member evaluations of a chain, beside its training
+  cudaEvent_t ev_chain[2] = {nullptr, nullptr}, ev_eval[2] = {nullptr, nullptr};
   std::vector<char> sh_dirty;
   void* map_x = nullptr;  // CUtensorMap* over d_eval
   void mark_dirty(int slot) {
@@ -356,11 +358,16 @@ void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* 
 bool train_supported(const ecco_ctx* ctx);
 // Fused SGD chain (train_kernels.cu): every job's steps[j] SGD steps of one
 // micro-window in ONE launch, one thread-block cluster per job with the fp32
-// masters resident in TMEM; writes the bf16 W1^T shadow `sh` (if given).
+// masters resident in TMEM, starting from the models at wsrc and leaving them
+// at wbase (a snapshot); writes the bf16 W1^T shadow `sh` (if given).
+// chain_rows() first draws the sampled rows of all n_micro micro-windows of
+// the call (micro-window `micro` of them is trained by train_chain).
+void chain_rows(ecco_ctx* ctx, int n_jobs, const int* d_job_ids, const int* d_steps,
+                const int* h_steps, const int* d_src_off, const int* d_src_cam,
+                const double* d_src_frac, const int* d_micro_base, int n_micro, int window);
 void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,
-                 const int* d_job_ids, const int* d_steps, const int* h_steps,
-                 const int* d_src_off, const int* d_src_cam, const double* d_src_frac,
-                 const int* d_micro_base, int micro_add, int window, float* wbase, size_t wstride,
+                 const int* d_steps, const int* h_steps, int micro, int n_micro,
+                 const float* wsrc, size_t wsrc_stride, float* wbase, size_t wstride,
                  int loss_t);
 }  // namespace fused
 

@@ -675,6 +675,14 @@ void init(ecco_ctx* ctx) {
   if (ctx->cfg.math == ECCO_MATH_TC_BF16 && fused::supported(ctx)) {
     fused::init_shadow(ctx, ctx->sh_commit);
     fused::init_shadow(ctx, ctx->sh_spec);
+    if (fused::train_supported(ctx)) {  // chains evaluate on a side stream, alternating shadows
+      fused::init_shadow(ctx, ctx->sh_spec2);
+      ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->eval_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        ECCO_CUDA(cudaEventCreateWithFlags(&ctx->ev_chain[i], cudaEventDisableTiming));
+        ECCO_CUDA(cudaEventCreateWithFlags(&ctx->ev_eval[i], cudaEventDisableTiming));
+      }
+    }
     ctx->sh_dirty.assign(ctx->cfg.max_jobs, 1);
     ctx->fused_eval = true;
     ctx->fused_train = fused::train_supported(ctx);
@@ -1088,23 +1096,60 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
                                                             ctx->cfg.params.acc_floor, d_out, depth + 1, 0);
   ECCO_LAUNCHED(ctx);
+  // Fused chains: the sampled rows of all `depth` micro-windows are drawn in
+  // one launch, each micro-window's chain reads state t-1 and leaves state t
+  // (no copy), and -- with a side stream -- the member evaluation of state t
+  // runs beside the chain of state t+1 (the two alternate between the two
+  // speculative shadows: chain t+2 rewrites the shadow eval t reads, so it
+  // waits for it).
+  const bool side = ctx->fused_train && ctx->eval_stream && n_mem > 0 && ctx->fused_eval;
+  if (ctx->fused_train)
+    fused::chain_rows(ctx, n_jobs, d_job_ids, d_steps, h_steps, d_src_off, d_src_cam, d_src_frac,
+                      d_micro_base, depth, window);
+  if (side) {  // the side stream sees everything enqueued so far (acc[:, 0], plans, rows)
+    ECCO_CUDA(cudaEventRecord(ctx->ev_chain[0], ctx->stream));
+    ECCO_CUDA(cudaStreamWaitEvent(ctx->eval_stream, ctx->ev_chain[0], 0));
+  }
   for (int t = 1; t <= depth; ++t) {
-    // state t starts as a copy of state t-1
-    if (t == 1)
-      k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(n_jobs, d_slots, ctx->d_w, np, 0,
-                                                                  ctx->d_wspec, spec_stride, 0, np, nullptr);
-    else
-      k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(
-          n_jobs, d_slots, ctx->d_wspec, spec_stride, (size_t)(t - 2) * np, ctx->d_wspec,
-          spec_stride, (size_t)(t - 1) * np, np, nullptr);
-    ECCO_LAUNCHED(ctx);
     // weights of state t are addressed as wbase + slot * spec_stride
     float* wt = ctx->d_wspec + (size_t)(t - 1) * np;
-    // the per-slot stride for kernels is spec_stride: pass n_params = spec_stride
-    if (ctx->fused_train)  // one launch: every job's whole micro-window on chip
-      fused::train_chain(ctx, &ctx->sh_spec, n_jobs, d_slots, d_job_ids, d_steps, h_steps,
-                         d_src_off, d_src_cam, d_src_frac, d_micro_base, t - 1, window, wt,
-                         spec_stride, t - 1);
+    if (ctx->fused_train) {  // one launch: every job's whole micro-window on chip
+      const float* src = t == 1 ? ctx->d_w : ctx->d_wspec + (size_t)(t - 2) * np;
+      Shadow* sh = (t & 1) ? &ctx->sh_spec : &ctx->sh_spec2;
+      if (side && t >= 3) ECCO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_eval[t & 1], 0));
+      fused::train_chain(ctx, sh, n_jobs, d_slots, d_steps, h_steps, t - 1, depth, src,
+                         t == 1 ? np : spec_stride, wt, spec_stride, t - 1);
+      if (side) {
+        ECCO_CUDA(cudaEventRecord(ctx->ev_chain[t & 1], ctx->stream));
+        ECCO_CUDA(cudaStreamWaitEvent(ctx->eval_stream, ctx->ev_chain[t & 1], 0));
+        cudaStream_t main_stream = ctx->stream;
+        ctx->stream = ctx->eval_stream;  // the evaluation of state t, on the side stream
+        try {
+          fused::refresh_shadow_dev(ctx, *sh, wt, spec_stride, d_slots, n_jobs, d_idle, n_idle);
+          pair_counts_planned(ctx, *sh, wt, spec_stride, spec_plan, d_ps, d_mem_cam, d_cnt);
+          k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(
+              g, n_jobs, d_mem_off, d_cnt, ctx->cfg.params.acc_floor, d_out, depth + 1, t);
+          ECCO_LAUNCHED(ctx);
+        } catch (...) {
+          ctx->stream = main_stream;
+          throw;
+        }
+        ctx->stream = main_stream;
+        ECCO_CUDA(cudaEventRecord(ctx->ev_eval[t & 1], ctx->eval_stream));
+        continue;
+      }
+    } else {
+      // state t starts as a copy of state t-1
+      if (t == 1)
+        k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(n_jobs, d_slots, ctx->d_w, np,
+                                                                    0, ctx->d_wspec, spec_stride, 0,
+                                                                    np, nullptr);
+      else
+        k_l_copy_weights<<<dim3(64, n_jobs), 256, 0, ctx->stream>>>(
+            n_jobs, d_slots, ctx->d_wspec, spec_stride, (size_t)(t - 2) * np, ctx->d_wspec,
+            spec_stride, (size_t)(t - 1) * np, np, nullptr);
+      ECCO_LAUNCHED(ctx);
+    }
     if (tc_bf16 && !ctx->fused_train) fused::shadow_w1t(ctx, d_slots, n_jobs, wt, spec_stride, w1t_train);
     for (int step = 0; step < (ctx->fused_train ? 0 : max_steps); ++step) {
       const Gate gate{d_steps, step, g.B};
@@ -1187,6 +1232,10 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
                                                               ctx->cfg.params.acc_floor, d_out, depth + 1, t);
     ECCO_LAUNCHED(ctx);
+  }
+  if (side) {  // the context stream (the caller's copy of d_out) waits for the last evaluation
+    ECCO_CUDA(cudaEventRecord(ctx->ev_eval[0], ctx->eval_stream));
+    ECCO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_eval[0], 0));
   }
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
 }

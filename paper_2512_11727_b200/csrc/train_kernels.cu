@@ -55,8 +55,12 @@ struct ChainArgs {
   const int32_t* rows;  // [job][max_steps][kB] frame-table row of every sampled frame
   const int32_t* labs;  // [job][max_steps][kB] its label
   int max_steps;
+  int row_step0;        // first row step of this micro-window in rows / labs
+  int rows_T;           // row steps per job in rows / labs (micro-windows x max_steps)
   const uint16_t* frames;
-  float* wbase;  // fp32 masters being trained (W1 stored [H][F])
+  const float* wsrc;    // fp32 masters the micro-window starts from (W1 stored [H][F])
+  size_t wsrc_stride;
+  float* wbase;         // ... and where it leaves them (a snapshot; may equal wsrc)
   size_t wstride;
   uint16_t* w1t;  // bf16 W1^T evaluation shadow [slot][H][F], written at the end
   float* losses;  // losses[slot * loss_T + loss_t] = mean loss of the last step
@@ -65,18 +69,21 @@ struct ChainArgs {
 
 // Every (job, step, row) draw of the micro-window, ahead of the chain
 // (sample_one: the same draws as k_l_sample and the oracle's orc_sample).
+// (grid.y covers n_micro x max_steps row steps: micro-window micro_add + y /
+// max_steps, step y % max_steps; rows laid out [job][micro][step][kB])
 __global__ void k_chain_rows(LDims g, uint64_t seed, const int* job_ids, const int* steps,
                              const int* src_off, const int* src_cam, const double* src_frac,
                              const int* micro_base, int micro_add, int window, int max_steps,
                              const int32_t* labels, int32_t* rows, int32_t* labs) {
-  const int j = blockIdx.x, step = blockIdx.y, s = threadIdx.x;
+  const int j = blockIdx.x, step = blockIdx.y % max_steps, mi = blockIdx.y / max_steps;
+  const int s = threadIdx.x;
   if (step >= steps[j]) return;
   int cam, frame;
   const int s0 = src_off[j];
   sample_one(g, seed, job_ids[j], src_off[j + 1] - s0, src_cam + s0, src_frac + s0, window,
-             micro_base[j] + micro_add, step, s, &cam, &frame);
+             micro_base[j] + micro_add + mi, step, s, &cam, &frame);
   const int32_t row = cam * g.R + frame;
-  const size_t o = ((size_t)j * max_steps + step) * kB + s;
+  const size_t o = ((size_t)j * gridDim.y + blockIdx.y) * kB + s;
   rows[o] = row;
   labs[o] = labels[row];
 }
@@ -228,7 +235,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int j = blockIdx.x / cs;
   const int r = (int)cluster_ctarank();
   const int nsteps = a.steps[j];
-  if (nsteps <= 0) return;  // the whole cluster (same job) leaves
+  if (nsteps <= 0) {  // no step: the snapshot is the starting model (the cluster copies it)
+    const int slot0 = a.slots[j];
+    const float* src = a.wsrc + (size_t)slot0 * a.wsrc_stride;
+    float* dst = a.wbase + (size_t)slot0 * a.wstride;
+    if (src != dst) {
+      const size_t np = (size_t)g.F * g.H + g.H + (size_t)g.H * g.C + g.C;
+      for (size_t i = (size_t)r * blockDim.x + threadIdx.x; i < np; i += (size_t)cs * blockDim.x)
+        dst[i] = src[i];
+    }
+    return;  // the whole cluster (same job) leaves
+  }
   const Layout L = layout(F);
   const uint32_t SC = std::max((uint32_t)F * 128u, 32768u);
   uint8_t* sX = smem + L.x;
@@ -270,10 +287,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* b1 = W1 + (size_t)F * H;
   float* W2 = b1 + H;
   float* b2 = W2 + (size_t)H * kC;
+  const float* sW1 = a.wsrc + (size_t)slot * a.wsrc_stride;  // the starting model
+  const float* sb1 = sW1 + (size_t)F * H;
+  const float* sW2g = sb1 + H;
+  const float* sb2 = sW2g + (size_t)H * kC;
   const float lr = g.lr;
   const int h0 = r * kHS;  // first hidden unit of this CTA
-  const int32_t* jrows = a.rows + (size_t)j * a.max_steps * kB;
-  const int32_t* jlabs = a.labs + (size_t)j * a.max_steps * kB;
+  const int32_t* jrows = a.rows + ((size_t)j * a.rows_T + a.row_step0) * kB;
+  const int32_t* jlabs = a.labs + ((size_t)j * a.rows_T + a.row_step0) * kB;
   const uint32_t recv_bytes = kB * kC * 4u;
   // bf16 dL rows + the 8-row db2 partials (+ every row's loss on rank 0)
   const uint32_t dl_bytes = kB * 32u + (kB / 8) * kC * 4u + (r == 0 ? kB * 4u : 0u);
@@ -323,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // this CTA's master slice (64 rows x F fp32) -> L2 at once: the tile-by-tile
   // loads below then wait on L2, not on four HBM round trips
   for (int li = tid; li < kHS * (F / 32); li += kThreads)
-    prefetch_l2(W1 + (size_t)(h0 + li / (F / 32)) * F + (li % (F / 32)) * 32);
+    prefetch_l2(sW1 + (size_t)(h0 + li / (F / 32)) * F + (li % (F / 32)) * 32);
   if (warp == 0) tmem_alloc(sTmem, tmem_cols(F));
   if (tid < kB) {
     sRow[tid] = jrows[tid];
@@ -331,9 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     sLab[tid - kB] = jlabs[tid - kB];
   }
   for (int i = tid; i < kHS * kC / 4; i += kThreads)
-    reinterpret_cast<float4*>(sW2)[i] = reinterpret_cast<const float4*>(W2 + (size_t)h0 * kC)[i];
-  if (tid < kHS) sB1[tid] = b1[h0 + tid];
-  if (tid < kC) sB2[tid] = b2[tid];
+    reinterpret_cast<float4*>(sW2)[i] = reinterpret_cast<const float4*>(sW2g + (size_t)h0 * kC)[i];
+  if (tid < kHS) sB1[tid] = sb1[h0 + tid];
+  if (tid < kC) sB2[tid] = sb2[tid];
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -347,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int f = mt * 128 + s;
     uint32_t w[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(W1[(size_t)(h0 + p * 32 + i) * F + f]);
+    for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(sW1[(size_t)(h0 + p * 32 + i) * F + f]);
     tmem_st32(tmem + lane_base + mt * 64 + p * 32, w);
     put_row32(sSC, f, p, w);
   }
@@ -695,12 +716,10 @@ bool train_supported(const ecco_ctx* ctx) {
   return layout(g.feat_dim).total <= 232448;
 }
 
-void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,
-                 const int* d_job_ids, const int* d_steps, const int* h_steps,
-                 const int* d_src_off, const int* d_src_cam, const double* d_src_frac,
-                 const int* d_micro_base, int micro_add, int window, float* wbase, size_t wstride,
-                 int loss_t) {
-  if (n_jobs == 0) return;
+void chain_rows(ecco_ctx* ctx, int n_jobs, const int* d_job_ids, const int* d_steps,
+                const int* h_steps, const int* d_src_off, const int* d_src_cam,
+                const double* d_src_frac, const int* d_micro_base, int n_micro, int window) {
+  if (n_jobs == 0 || n_micro == 0) return;
   const ecco_config& c = ctx->cfg;
   const LDims g{c.feat_dim, c.hidden_dim, c.num_classes, c.scene_dims, c.minibatch,
                 c.ring_frames, c.eval_samples, c.sgd_lr, c.feature_noise};
@@ -709,21 +728,37 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
   if (max_steps == 0) return;
   ECCO_REQUIRE((double)c.max_cameras * c.ring_frames < 2147483647.0,
                "fused SGD chain: frame-table rows must fit int32");
-  const size_t nrows = (size_t)n_jobs * max_steps * kB;
+  const size_t nrows = (size_t)n_jobs * n_micro * max_steps * kB;
   int32_t* rows = (int32_t*)ctx->train_scratch[0].get(nrows * 4);
   int32_t* labs = (int32_t*)ctx->train_scratch[1].get(nrows * 4);
-  k_chain_rows<<<dim3(n_jobs, max_steps), kB, 0, ctx->stream>>>(
-      g, c.seed, d_job_ids, d_steps, d_src_off, d_src_cam, d_src_frac, d_micro_base, micro_add,
-      window, max_steps, ctx->d_labels, rows, labs);
+  k_chain_rows<<<dim3(n_jobs, n_micro * max_steps), kB, 0, ctx->stream>>>(
+      g, c.seed, d_job_ids, d_steps, d_src_off, d_src_cam, d_src_frac, d_micro_base, 0, window,
+      max_steps, ctx->d_labels, rows, labs);
   ECCO_LAUNCHED(ctx);
+}
+
+void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,
+                 const int* d_steps, const int* h_steps, int micro, int n_micro,
+                 const float* wsrc, size_t wsrc_stride, float* wbase, size_t wstride,
+                 int loss_t) {
+  if (n_jobs == 0) return;
+  const ecco_config& c = ctx->cfg;
+  const LDims g{c.feat_dim, c.hidden_dim, c.num_classes, c.scene_dims, c.minibatch,
+                c.ring_frames, c.eval_samples, c.sgd_lr, c.feature_noise};
+  int max_steps = 0;
+  for (int j = 0; j < n_jobs; ++j) max_steps = std::max(max_steps, h_steps[j]);
   ChainArgs a{};
   a.g = g;
   a.slots = d_slots;
   a.steps = d_steps;
-  a.rows = rows;
-  a.labs = labs;
+  a.rows = (const int32_t*)ctx->train_scratch[0].p;  // chain_rows() of this call
+  a.labs = (const int32_t*)ctx->train_scratch[1].p;
   a.max_steps = max_steps;
+  a.row_step0 = micro * max_steps;
+  a.rows_T = n_micro * max_steps;
   a.frames = ctx->d_frames;
+  a.wsrc = wsrc;
+  a.wsrc_stride = wsrc_stride;
   a.wbase = wbase;
   a.wstride = wstride;
   a.w1t = sh ? sh->w1t : nullptr;
