@@ -19,7 +19,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libecco_b200.so")
+# (ECCO_LIB_PATH: an instrumented build for the tools/ probes; never set by tests or bench)
+LIB_PATH = os.environ.get("ECCO_LIB_PATH") or os.path.join(HERE, "libecco_b200.so")
 
 OK, INVALID_ARGUMENT, LOGIC, INFEASIBLE, SCHEMA, CUDA, RUNTIME = range(7)
 PARAMETRIC, LEARNED = 0, 1

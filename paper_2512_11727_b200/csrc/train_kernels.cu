@@ -47,6 +47,7 @@ constexpr int kThreads = 256;  // 8 warps: lane quadrant q = warp % 4, half p = 
 constexpr int kC = 16;         // classes (logits held in registers)
 constexpr int kHS = 64;        // hidden units per CTA of the cluster
 constexpr int kMaxCluster = 8;
+constexpr int kGatherWarps = 4;  // warps 1-4 each issue a quarter of a tile's gather4 copies
 
 struct ChainArgs {
   LDims g;
@@ -126,7 +127,7 @@ __host__ __device__ inline Layout layout(int F) {
   o += kB * 4u;
   o = (o + 7u) & ~7u;
   L.bars = o;
-  o += 16u * 8u;
+  o += 20u * 8u;
   L.tmem = o;
   o += 16u;
   L.total = o;
@@ -226,8 +227,19 @@ __device__ __forceinline__ uint32_t dlb_off(int row, int chunk) {
   return (uint32_t)row * 32u + ((uint32_t)(chunk ^ ((row >> 2) & 1)) << 4);
 }
 
+// TMA gather4 (sm_100a): four rows `r0..r3` of the 2-D frame table, columns
+// [c0, c0 + 64), into four consecutive 128-byte rows of a 128B-swizzled tile.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int c0, int r0,
+                                            int r1, int r2, int r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-    k_train_chain(ChainArgs a) {
+    k_train_chain(const __grid_constant__ CUtensorMap map_rows, ChainArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const LDims g = a.g;
   const int F = g.F, H = g.H;
@@ -270,7 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* dl_full = zfull + 6;    // every dL row (and, on rank 0, every loss) arrived
   uint64_t* w2full = zfull + 7;     // dW2 accumulated
   uint64_t* gt = zfull + 8;         // [NM] dW1 tile mt accumulated into the master
-  uint64_t* xready = zfull + 12;    // [NM] tile mt's W1 operand rows and next X chunks in smem
+  uint64_t* xready = zfull + 12;    // [NM] tile mt's W1 operand rows rebuilt in smem
+  uint64_t* xfull = zfull + 16;     // [NM] tile mt's next-step X chunks landed (TMA gather4)
   uint32_t* sTmem = (uint32_t*)(smem + L.tmem);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -335,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int mt = 0; mt < NM; ++mt) {
       mbar_init(gt + mt, 1);
       mbar_init(xready + mt, kThreads - 32);
+      mbar_init(xfull + mt, kGatherWarps);
     }
     mbar_init(recv_full, 1);
     mbar_init(dl_full, 1);
@@ -609,14 +623,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     // (tile 2's rows overwrite R, tile 3's dH: both read by MMAs its commit covers)
-    // Tile mt's operand rows and next X chunks are published on xready[mt]
-    // (each thread: its copies of the tile complete -> proxy fence ->
-    // arrive, one tile behind the issue); warp 0 issues the next step's
-    // forward chunks 2mt, 2mt+1 as each tile is published.
+    // As soon as tile mt's dW1 MMAs have read its X chunks (gt[mt]), warps
+    // 1-4 each issue a quarter of the next step's rows for those two chunks
+    // as TMA gather4 copies (4 rows x 128 B each, landing 128B-swizzled where
+    // the forward MMA reads them; completion on xfull[mt]), and warps 1-7
+    // rebuild the tile's bf16 W1 operand rows from the TMEM master and publish
+    // them on xready[mt]; warp 0 issues the next step's forward chunks 2mt,
+    // 2mt+1 once both have landed.  The row gather no longer occupies the
+    // warps or the LSU (it was a cp.async loop of 2,048 16-byte pieces per tile).
     if (warp > 0) {
+      const int* nrows = sRow + (cur ^ 1) * kB;
       for (int mt = 0; mt < NM; ++mt) {
         mbar_wait(gt + mt, ph);
         tc_fence_after();
+        if (more && warp <= kGatherWarps) {
+          if (elect_one()) {
+            constexpr int kGroups = kB / 4 / kGatherWarps;  // row groups of 4 per issuing warp
+            mbar_expect_tx(xfull + mt, 2u * kGroups * 512u);
+            const int g0 = (warp - 1) * kGroups;
+            for (int cc = 0; cc < 2; ++cc) {
+              const int kc = 2 * mt + cc;
+              for (int gi = g0; gi < g0 + kGroups; ++gi) {
+                const int i0 = gi * 4;
+                tma_gather4(sX + kc * 16384 + i0 * 128, &map_rows, kc * 64, nrows[i0],
+                            nrows[i0 + 1], nrows[i0 + 2], nrows[i0 + 3], xfull + mt);
+              }
+            }
+          }
+          __syncwarp();
+        }
         uint32_t wr[32];
         tmem_ld32_nowait(tmem + lane_base + mt * 64 + p * 32, wr);
         if (warp == 4) {
@@ -629,23 +664,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         put_row32(sSC, mt * 128 + s, p, wr);
         if (more) {
-          gather(cur ^ 1, mt * 16, 16, 32);  // this tile's X chunks are read
-          cp_async_commit();
-          if (mt > 0) {
-            cp_async_wait_group<1>();
-            fence_async_smem();
-            mbar_arrive(xready + mt - 1);
-          }
+          fence_async_smem();  // the rebuilt rows (generic stores) -> the forward MMA
+          mbar_arrive(xready + mt);
         }
-      }
-      if (more) {
-        cp_async_wait_group<0>();
-        fence_async_smem();
-        mbar_arrive(xready + NM - 1);
       }
     } else if (more) {
       for (int mt = 0; mt < NM; ++mt) {
         mbar_wait(xready + mt, ph);
+        mbar_wait(xfull + mt, ph);
         tc_fence_after();
         if (elect_one()) {
           issue_fwd(2 * mt, 2 * mt + 2);
@@ -796,8 +822,12 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
   const double flops = steps * kB * (4.0 * F * H + 6.0 * H * C);
   const double params = F * H + H + H * C + C;
   const double bytes = steps * kB * F * 2.0 + live * params * 8.0;
+  // the frame table as a 2-D bf16 tensor [camera*R + frame][F]: TMA gather4
+  // rows of 64 columns, 128B swizzle (the forward's X operand layout)
+  const CUtensorMap map_rows =
+      tensor_map_bf16(ctx->d_frames, (uint64_t)ctx->cfg.max_cameras * c.ring_frames, c.feat_dim, 1);
   ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_STEP, flops, bytes,
-             ECCO_CUDA(cudaLaunchKernelEx(&lc, k_train_chain, a)));
+             ECCO_CUDA(cudaLaunchKernelEx(&lc, k_train_chain, map_rows, a)));
   ECCO_LAUNCHED(ctx);
 }
 
