@@ -62,6 +62,7 @@ DEPTH = 1             # speculative chain every group trains up front: the initi
                       # these streams absorbs most of the remaining budget; its chain is extended
                       # by depth doubling (window.py), the other groups' chains are never wasted
 MAX_DEPTH = 64        # deepest extension chain (snapshots: groups x MAX_DEPTH x params in HBM)
+RESERVE_SMS = 8       # SMs the overlapped regroup matrix leaves to the serial extension chains
 STEPS = 16            # SGD steps per micro-window
 # configs[4]: the detection-head variant (larger per-group model and frame
 # features).  Its window is the allocator's marginal-gain probing (every
@@ -230,21 +231,32 @@ def run_b200(args, rank, world, local_rank):
     acc = {"regroup": 0.0, "retrain": 0.0, "committed": 0, "speculative": 0, "extensions": 0,
            "max_micro": 0}
 
-    def step(w, timed=False, mid=None):
+    def mark_b():
         with torch.cuda.stream(stream):
-            if timed:
+            ev["b"].record(stream)
+
+    def step(w, timed=False, mid=None):
+        # the window in the reference's order -- retrain, then the window-end
+        # regroup over the trained models -- with the regroup matrix of the
+        # groups the greedy leaves alone overlapped with its serial extension
+        # chains (GroupRetrainer.window); "retrain" = start -> the schedule
+        # committed, "regroup" = -> the join rule done (what the window still
+        # waits for after the retrain)
+        if timed:
+            with torch.cuda.stream(stream):
                 ev["a"].record(stream)
-            if MATRIX:
-                retr.regroup()
+        if MATRIX:
+            retr.window(w, mid=mid, reserve_sms=RESERVE_SMS, mark=mark_b if timed else None)
+        else:
+            retr.retrain(w, mid=mid)
             if timed:
-                ev["b"].record(stream)
-        retr.retrain(w, mid=mid)
+                mark_b()
         if timed:
             with torch.cuda.stream(stream):
                 ev["c"].record(stream)
             ev["c"].synchronize()
-            acc["regroup"] += ev["a"].elapsed_time(ev["b"])
-            acc["retrain"] += ev["b"].elapsed_time(ev["c"])
+            acc["retrain"] += ev["a"].elapsed_time(ev["b"])
+            acc["regroup"] += ev["b"].elapsed_time(ev["c"])
             acc["committed"] += retr.stats["committed_samples"]
             acc["speculative"] += retr.stats["speculative_samples"]
             acc["extensions"] += retr.stats["extensions"]
@@ -549,30 +561,31 @@ def run_e2e(args, retr, wl, torch, dist):
             ctx.stage_sampled_host_ptr(prep, GPU_S, DEPTH, w, fr.data_ptr(), lb.data_ptr(), 0, 0, 0)
 
     def window(w, timed):
+        """Window w: its rings and eval sets were staged during window w-1 and
+        become current at its start; window w+1's are staged on the copy
+        stream as soon as window w's regroup matrix is enqueued (beside its
+        greedy's chains); the assignments are read back at the end."""
         t0 = time.perf_counter()
+        nxt = w + 1
+
+        def stage_next():
+            stage_eval()
+            stage_rings(nxt)
+
+        swap = lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS | ecco.FRAMES_EVAL)
         if MATRIX:
-            retr.regroup()
+            retr.window(w, mid=swap, reserve_sms=RESERVE_SMS, after_launch=stage_next)
             with torch.cuda.stream(retr.stream):
                 best_host.copy_(retr.best, non_blocking=True)  # group assignments to the host
             retr.stream.synchronize()
-        t1 = time.perf_counter()
-        # window w+1's eval sets stream in from here on (back buffer)
-        nxt = w + 1
-        stage_eval()
-        if not MATRIX:
-            retr.retrain(w, mid=lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS))
-            stage_rings(nxt)  # no regroup to hide behind: a window ahead
         else:
-            retr.retrain(w, mid=lambda: ctx.swap_frame_parts(ecco.FRAMES_RINGS))
-            stage_rings(nxt)  # streams during window w+1's regroup
-        t2 = time.perf_counter()
-        ctx.swap_frame_parts(ecco.FRAMES_EVAL)
-        return t1 - t0, t2 - t1, retr.stats["committed_samples"]
+            retr.retrain(w, mid=swap)
+            stage_next()
+        return time.perf_counter() - t0, retr.stats["committed_samples"]
 
     # pipeline fill + one untimed warm-up window through the same ingest path
     # (first-touch costs of the pinned table and the staging buffers)
     stage_eval()
-    ctx.swap_frame_parts(ecco.FRAMES_EVAL)
     stage_rings(9_999)
     window(9_999, False)
     ctx.synchronize()
@@ -580,33 +593,29 @@ def run_e2e(args, retr, wl, torch, dist):
     if dist is not None:
         dist.barrier()
     h0, d0 = ctx.transfer_bytes()
-    rg, tr, committed = 0.0, 0.0, 0
+    wall, committed = 0.0, 0
     for k in range(steps):
-        a, b, c = window(10_000 + k, True)
-        rg, tr, committed = rg + a, tr + b, committed + c
+        a, c = window(10_000 + k, True)
+        wall, committed = wall + a, committed + c
     ctx.synchronize()
     h1, d1 = ctx.transfer_bytes()
     d1 += steps * best_host.numel() * 4
-    rg, tr = reduce_max(dist, [rg, tr])
-    el_s = rg + tr
+    el_s = reduce_max(dist, [wall])[0]
     return {"value": committed / el_s, "unit": "samples/s",
             "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
             "ms_per_step": el_s * 1e3 / steps, "steps": steps,
-            "regroup_ms_per_window": rg * 1e3 / steps,
-            "retrain_ms_per_window": tr * 1e3 / steps,
-            "retrain_samples_per_s": committed / tr,
             "how": ("every window's frames from pinned host buffers on a copy stream, "
                     + ("ecco_stage_frames_range: every camera's full ring"
                        if args.e2e_full_rings else
                        "ecco_stage_sampled_frames: the ring rows this rank's SGD steps draw, marked "
                        "on the device and read zero-copy over PCIe (rows never drawn are not "
                        "transferred; extended chains top up with ecco_fetch_sampled_frames)")
-                    + ", all labels and every camera's eval set; double-buffered in two parts "
-                    "(ecco_swap_frame_parts): window k+1's eval sets upload during window k, "
-                    "window k's drawn rows during its own regroup; the assignments read back "
-                    "before the retrain phase, trajectories read back for the host replay; host "
-                    "wall clock per phase (max over ranks), window 0's unoverlapped eval-set "
-                    "upload in the warm-up"),
+                    + ", all labels and every camera's eval set; double-buffered: window k+1's "
+                    "rings and eval sets stream in during window k (from its regroup-matrix "
+                    "launch on) and become current at window k+1's start; the assignments read "
+                    "back at the end of every window, trajectories read back for the host "
+                    "replay; host wall clock per window (max over ranks), the pipeline fill in "
+                    "the warm-up"),
             "pcie_gbs": (h1 - h0) / el_s / 1e9}
 
 
@@ -658,8 +667,9 @@ def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
     wl = Workload(args.config)
     for world in worlds:
         retr = make_retrainer(args, wl, 0, world, None, torch.cuda.current_device(), emulate=True)
+        run = (lambda w: retr.window(w, reserve_sms=RESERVE_SMS)) if MATRIX else retr.retrain
         for w in range(2):
-            retr.step(w + 1)
+            run(w + 1)
         retr.ctx.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         n = 3
@@ -667,7 +677,7 @@ def scaling_emulation(args, n1_ms, worlds=(2, 4, 8)):
         with torch.cuda.stream(retr.stream):
             e0.record(retr.stream)
         for k in range(n):
-            retr.step(10 + k)
+            run(10 + k)
             committed += retr.stats["committed_samples"]
         with torch.cuda.stream(retr.stream):
             e1.record(retr.stream)

@@ -238,6 +238,19 @@ ecco_status ecco_eval_matrix(ecco_ctx* ctx, int n_probes, const double* scenes,
 ecco_status ecco_eval_matrix_dev(ecco_ctx* ctx, int n_probes, const double* scenes,
                                  const int* cam_idx, int n_jobs, const int* job_ids,
                                  const uint8_t* mask, void* out_dev);
+/* The same matrix (learned backend, tensor-core math, camera probes)
+ * enqueued on the context's own MATRIX stream, after everything enqueued on
+ * the context stream so far (it evaluates the models committed by then), with
+ * its evaluation grid leaving `reserve_sms` SMs free for the kernels the
+ * context stream launches meanwhile; returns at once.  ecco_matrix_join makes
+ * the context stream wait for it.  A model committed while it runs may be
+ * read half-updated: its column must be re-evaluated after the join (what the
+ * window-end regroup of paper_2512_11727_b200/window.py does for the groups
+ * the allocator trained beyond the initial pass, overlapping the rest of the
+ * matrix with their serial chains). */
+ecco_status ecco_eval_matrix_dev_async(ecco_ctx* ctx, int n_probes, const int* cam_idx, int n_jobs,
+                                       const int* job_ids, void* out_dev, int reserve_sms);
+ecco_status ecco_matrix_join(ecco_ctx* ctx);
 /* Sparse form of the same matrix: out[p] = eval(model(job_ids[p]), probe p)
  * where probe p is scenes[p] (parametric; nullable = the camera's current
  * scene cams[p]) or camera cams[p]'s eval set (learned).  Used for the

@@ -107,7 +107,7 @@ EXPORTS = [
     "ecco_swap_frames", "ecco_swap_frame_parts", "ecco_reserve_ingest",
     "ecco_put_models", "ecco_get_models", "ecco_seed_models", "ecco_drop_models",
     "ecco_get_weights", "ecco_set_weights", "ecco_eval_jobs", "ecco_eval_matrix",
-    "ecco_eval_matrix_dev", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
+    "ecco_eval_matrix_dev", "ecco_eval_matrix_dev_async", "ecco_matrix_join", "ecco_eval_pairs", "ecco_rename_models", "ecco_route_propose",
     "ecco_route_matrix_dev", "ecco_route_matrix_ids_dev", "ecco_debug_eval_logits",
     "ecco_train_trajectories", "ecco_commit", "ecco_last_losses", "ecco_sample_indices",
     "ecco_profile_tables", "ecco_sim_default_options", "ecco_sim_create", "ecco_sim_destroy",
@@ -452,6 +452,17 @@ class Context:
         n = len(c) if c is not None else len(s)
         self._check(lib().ecco_eval_matrix_dev(self._h, n, sp, cp, len(j), jp, mp,
                                                C.c_void_p(out_ptr)))
+
+    def eval_matrix_dev_async(self, job_ids, out_ptr, cams, reserve_sms=8):
+        """ecco_eval_matrix_dev_async: the matrix on the context's matrix stream,
+        leaving reserve_sms SMs for the context stream; join with matrix_join()."""
+        j, jp = _p(job_ids, np.int32)
+        c, cp = _p(cams, np.int32)
+        self._check(lib().ecco_eval_matrix_dev_async(self._h, len(c), cp, len(j), jp,
+                                                     C.c_void_p(out_ptr), int(reserve_sms)))
+
+    def matrix_join(self):
+        self._check(lib().ecco_matrix_join(self._h))
 
     def eval_pairs(self, job_ids, scenes=None, cams=None):
         j, jp = _p(job_ids, np.int32)

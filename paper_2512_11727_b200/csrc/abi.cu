@@ -93,6 +93,12 @@ void free_all(ecco_ctx* c) {
   c->zc_missing.release();
   for (auto& b : c->commit_args) b.release();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (auto& b : c->side_scratch) b.release();
+  for (auto& b : c->side_em_args) b.release();
+  c->side_tile_ctr.release();
+  if (c->matrix_stream) cudaStreamDestroy(c->matrix_stream);
+  if (c->ev_matrix_in) cudaEventDestroy(c->ev_matrix_in);
+  if (c->ev_matrix_done) cudaEventDestroy(c->ev_matrix_done);
   for (int i = 0; i < 2; ++i) {
     if (c->copy_done[i]) cudaEventDestroy(c->copy_done[i]);
     if (c->back_free[i]) cudaEventDestroy(c->back_free[i]);
@@ -856,6 +862,60 @@ ecco_status ecco_eval_matrix(ecco_ctx* ctx, int n, const double* scenes, const i
 ecco_status ecco_eval_matrix_dev(ecco_ctx* ctx, int n, const double* scenes, const int* cam_idx,
                                  int g, const int* job_ids, const uint8_t* mask, void* out_dev) {
   return guarded(ctx, [&] { eval_matrix_impl(ctx, n, scenes, cam_idx, g, job_ids, mask, (double*)out_dev); });
+}
+
+ecco_status ecco_eval_matrix_dev_async(ecco_ctx* ctx, int n, const int* cam_idx, int g,
+                                       const int* job_ids, void* out_dev, int reserve_sms) {
+  return guarded(ctx, [&] {
+    ECCO_REQUIRE(learned(ctx) && ctx->fused_eval,
+                 "eval_matrix_dev_async: learned backend with tensor-core math");
+    ECCO_REQUIRE(reserve_sms >= 0, "eval_matrix_dev_async: reserve_sms must be >= 0");
+    if (n == 0 || g == 0) return;
+    if (!ctx->matrix_stream) {
+      ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->matrix_stream, cudaStreamNonBlocking));
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->ev_matrix_in, cudaEventDisableTiming));
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->ev_matrix_done, cudaEventDisableTiming));
+    }
+    // the committed models' evaluation shadows are rebuilt on the CONTEXT
+    // stream first: the chains that run meanwhile evaluate from the same
+    // shadows, and must not see one half rebuilt by the matrix stream
+    {
+      auto s = slots_of(ctx, g, job_ids);
+      lbackend::refresh_models(ctx, s.data(), g);
+    }
+    // the matrix sees everything the context stream has enqueued (committed models)
+    ECCO_CUDA(cudaEventRecord(ctx->ev_matrix_in, ctx->stream));
+    ECCO_CUDA(cudaStreamWaitEvent(ctx->matrix_stream, ctx->ev_matrix_in, 0));
+    // enqueue with the side buffers swapped in: nothing the context stream
+    // runs meanwhile shares a scratch buffer, argument buffer or tile counter
+    cudaStream_t main_stream = ctx->stream;
+    auto swap_side = [&] {
+      for (int i = 0; i < 20; ++i) std::swap(ctx->scratch[i], ctx->side_scratch[i]);
+      for (int i = 0; i < 3; ++i) std::swap(ctx->em_args[i], ctx->side_em_args[i]);
+      std::swap(ctx->tile_ctr, ctx->side_tile_ctr);
+    };
+    swap_side();
+    ctx->stream = ctx->matrix_stream;
+    ctx->reserve_sms = reserve_sms;
+    try {
+      eval_matrix_impl(ctx, n, nullptr, cam_idx, g, job_ids, nullptr, (double*)out_dev);
+    } catch (...) {
+      ctx->stream = main_stream;
+      ctx->reserve_sms = 0;
+      swap_side();
+      throw;
+    }
+    ctx->stream = main_stream;
+    ctx->reserve_sms = 0;
+    swap_side();
+    ECCO_CUDA(cudaEventRecord(ctx->ev_matrix_done, ctx->matrix_stream));
+  });
+}
+
+ecco_status ecco_matrix_join(ecco_ctx* ctx) {
+  return guarded(ctx, [&] {
+    if (ctx->matrix_stream) ECCO_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_matrix_done, 0));
+  });
 }
 
 ecco_status ecco_eval_pairs(ecco_ctx* ctx, int n, const double* scenes, const int* cams,

@@ -220,6 +220,13 @@ struct ecco_ctx {
   DevBuf commit_args[2];  // ecco_commit's
   DevBuf em_args[3];    // ecco_eval_matrix(_dev)'s uploaded arguments
   DevBuf tile_ctr;      // the CTA-pair evaluation kernel's dynamic super-tile counter
+  // ecco_eval_matrix_dev_async: the matrix runs on its own stream with its own
+  // scratch / argument buffers / tile counter (swapped in for the enqueue),
+  // leaving reserve_sms SMs to what the context stream runs meanwhile
+  cudaStream_t matrix_stream = nullptr;
+  cudaEvent_t ev_matrix_in = nullptr, ev_matrix_done = nullptr;
+  DevBuf side_scratch[20], side_em_args[3], side_tile_ctr;
+  int reserve_sms = 0;
   unsigned long long* d_zc_rows = nullptr;
 
   // fused evaluation: shadows of the committed models (refreshed lazily for
@@ -391,6 +398,9 @@ void fetch_rows(ecco_ctx* ctx, cudaStream_t st, const uint16_t* host_dev, uint16
 
 namespace lbackend {
 void init(ecco_ctx* ctx);
+// Rebuilds the bf16 evaluation shadows of the committed models among the
+// slots that changed since their last refresh (stream-ordered).
+void refresh_models(ecco_ctx* ctx, const int* h_slots, int n);
 void generate_frames(ecco_ctx* ctx, int window);
 void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const int* d_job_ids);
 void eval_matrix(ecco_ctx* ctx, int n_probes, const int* d_cams, int n_jobs, const int* d_slots,

@@ -1002,7 +1002,8 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
       pattr.mark(g.device);
     }
     const int n_super = (a.n_rows + 2 * kTileRows - 1) / (2 * kTileRows);
-    const int pairs = std::min({n_super, sm_count(g.device) / 2, grid_cap("ECCO_EVAL_MAX_PAIRS")});
+    const int pairs = std::max(1, std::min({n_super, (sm_count(g.device) - ctx->reserve_sms) / 2,
+                                            grid_cap("ECCO_EVAL_MAX_PAIRS")}));
     a.tile_ctr = (int*)ctx->tile_ctr.get(sizeof(int));
     ECCO_CUDA(cudaMemsetAsync(a.tile_ctr, 0, sizeof(int), ctx->stream));
     ECCO_TIMED(ctx, kind, flops, bytes,
@@ -1012,7 +1013,8 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
     ECCO_LAUNCHED(ctx);
     return;
   }
-  const int grid = std::min({a.n_tiles, sm_count(g.device), grid_cap("ECCO_EVAL_MAX_CTAS")});
+  const int grid = std::max(1, std::min({a.n_tiles, sm_count(g.device) - ctx->reserve_sms,
+                                         grid_cap("ECCO_EVAL_MAX_CTAS")}));
   ECCO_TIMED(ctx, kind, flops, bytes,
              (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
                                                                   *(const CUtensorMap*)sh.map_w, a)));

@@ -745,6 +745,10 @@ static void pair_counts_planned(ecco_ctx* ctx, const Shadow& sh, const float* wb
                      pl.pair);
 }
 
+void refresh_models(ecco_ctx* ctx, const int* h_slots, int n) {
+  if (ctx->fused_eval && n > 0) refresh_committed(ctx, h_slots, n);
+}
+
 // Fused pairs-mode counts: probe p = camera h_cam/d_cam[p] under slot
 // h_slot[p]; consecutive probes of one slot share 128-row tiles.
 static void pair_counts_fused(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wstride,

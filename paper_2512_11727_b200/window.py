@@ -200,10 +200,15 @@ class GroupRetrainer:
                                           n_blocks=self.world)
         return self.best, self.best_acc
 
-    def retrain(self, window, mid=None):
+    def retrain(self, window, mid=None, after_initial=None):
         """Speculative chains, replay over every group, exact extension of
         exhausted chains, commit.  Returns the committed micro-windows per
-        group (G,)."""
+        group (G,).  With `after_initial`, every local group's first
+        micro-window (the initial pass, which always grants each group
+        exactly one, gpu_allocator.cpp:160-166) is committed as soon as the
+        initial chains have run, and after_initial() is called before the
+        greedy remainder (the window step overlaps the regroup matrix with
+        it)."""
         if mid is not None:
             mid()
         if self.local:
@@ -212,7 +217,13 @@ class GroupRetrainer:
         traj = self.gather_trajectories(self.acc_local)
         chain = np.full(self.G, self.depth, np.int64)   # micro-windows each chain covers
         last_d = np.full(self.G, self.depth, np.int64)
-        committed = np.zeros(self.G, np.int64)         # this window, local groups only
+        # micro-windows committed before the group's LAST chain started (ecco_commit
+        # counts from there); local groups only
+        start = np.zeros(self.G, np.int64)
+        if after_initial is not None:
+            if self.local:
+                self.ctx.commit(self.local, [1] * len(self.local))
+            after_initial()
         rows = [list(t) for t in traj]
         ids = np.arange(self.G, dtype=np.int32)
         extensions, ext_samples = 0, 0
@@ -233,8 +244,8 @@ class GroupRetrainer:
             owner = self.placement.owner[k]
             ext = np.zeros(d + 1)
             if owner == self.rank:
-                self.ctx.commit([k], [int(chain[k] - committed[k])])
-                committed[k] = chain[k]
+                self.ctx.commit([k], [int(chain[k] - start[k])])
+                start[k] = chain[k]
                 mem = self.groups[k]
                 p1 = self.ctx.prepare_trajectories([k], [self.batch], [mem],
                                                    [[1.0 / len(mem)] * len(mem)], [mem])
@@ -253,13 +264,70 @@ class GroupRetrainer:
         self.traj = T  # the trajectories the final replay read (extensions included)
         self.schedule = jobs
         if self.local:
-            self.ctx.commit(self.local, (counts[self.local] - committed[self.local]).astype(np.int32))
+            self.ctx.commit(self.local, (counts[self.local] - start[self.local]).astype(np.int32))
         self.stats = {"extensions": extensions, "extension_samples": ext_samples,
                       "committed_samples": int((counts * self.steps).sum()) * self.B,
                       "speculative_samples": int(self.depth * self.steps.sum()) * self.B + ext_samples,
                       "max_micro_windows": int(counts.max()) if self.G else 0}
         self.counts = counts
         return counts
+
+    def window(self, window, mid=None, reserve_sms=8, after_launch=None, mark=None):
+        """One window in the reference's order -- retrain (initial pass, greedy
+        remainder) then the window-end regroup matrix over the trained models
+        and the join rule -- with the two overlapped where the data allows:
+        once the initial pass is committed, every group's model is final
+        unless the greedy trains it again, so the matrix of all groups runs on
+        the context's matrix stream (ecco_eval_matrix_dev_async, leaving
+        `reserve_sms` SMs) while the greedy's extension chains run on the
+        context stream; afterwards the columns of the groups the greedy
+        trained beyond their first micro-window are re-evaluated on their
+        final models.  The result equals retrain() followed by regroup()
+        (tests/test_gpu_multirank.py checks it bit for bit).  after_launch()
+        runs right after the matrix is enqueued (e.g. the next window's
+        ingest), mark() once the retrain is committed (phase timing).
+        Returns (counts, best group per camera, its accuracy)."""
+        torch = self.torch
+        fused = bool(self.local) and self.ctx.cfg.math == TC_BF16
+
+        def launch_matrix():
+            if self.local and fused:
+                self.ctx.eval_matrix_dev_async(self.local, self._m_target(), self.cams,
+                                               reserve_sms=reserve_sms)
+            if after_launch is not None:
+                after_launch()
+
+        counts = self.retrain(window, mid=mid, after_initial=launch_matrix)
+        if mark is not None:
+            mark()
+        with torch.cuda.stream(self.stream):
+            if self.local:
+                if fused:
+                    self.ctx.matrix_join()
+                    redo = [g for g in self.local if counts[g] > 1]
+                    if redo:
+                        M2 = torch.empty((self.N, len(redo)), dtype=torch.float64, device=self.dev)
+                        self.ctx.eval_matrix_dev(redo, M2.data_ptr(), cams=self.cams)
+                        cols = torch.tensor([self.slot_of[g] for g in redo], device=self.dev)
+                        self._m_view().index_copy_(1, cols, M2)
+                    if self.M_part is not None:
+                        self.M_local[:, :len(self.local)].copy_(self.M_part)
+                else:  # (exact math: no side stream) the matrix after the retrain
+                    self.ctx.eval_matrix_dev(self.local, self._m_target(), cams=self.cams)
+                    if self.M_part is not None:
+                        self.M_local[:, :len(self.local)].copy_(self.M_part)
+            M = self.gather_blocks(self.M_local)
+            self.ctx.route_matrix_ids_dev(self.N, self.gb, M.data_ptr(), self.col_ids.data_ptr(),
+                                          self.best.data_ptr(), self.best_acc.data_ptr(),
+                                          n_blocks=self.world)
+        return counts, self.best, self.best_acc
+
+    def _m_target(self):
+        """Device pointer the local eval matrix is written to ([N, local] contiguous)."""
+        return (self.M_local if self.M_part is None else self.M_part).data_ptr()
+
+    def _m_view(self):
+        return self.M_local if self.M_part is None else self.M_part
 
     def set_host_frames(self, frames_ptr):
         """Registers the pinned frame table the window's rings are staged
@@ -268,8 +336,9 @@ class GroupRetrainer:
         self.host_frames_ptr = int(frames_ptr)
 
     def step(self, window, mid=None):
-        self.regroup()
-        return self.retrain(window, mid=mid)
+        """One window (retrain, then the overlapped window-end regroup);
+        returns the committed micro-windows per group."""
+        return self.window(window, mid=mid)[0]
 
     def local_samples(self, counts=None):
         """Committed samples of this rank's groups."""

@@ -41,7 +41,7 @@ def _layout():
     return groups, scenes, np.full(c, 8.192e6)
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, mode="split"):
     import torch
     dist = None
     if world > 1:
@@ -58,9 +58,12 @@ def _worker(rank, world, port, q):
                            steps_per_gpu_s=4.0, dims=DIMS)
         out = []
         for w in range(WINDOWS):
-            best, acc = r.regroup()
+            if mode == "split":  # retrain, then the window-end regroup, in sequence
+                counts = r.retrain(w + 1)
+                best, acc = r.regroup()
+            else:  # the overlapped window (matrix beside the greedy's extension chains)
+                counts, best, acc = r.window(w + 1)
             torch.cuda.synchronize()
-            counts = r.retrain(w + 1)
             out.append({"best": best.cpu().numpy(), "acc": acc.cpu().numpy(), "counts": counts,
                         "traj": r.traj.copy(), "schedule": r.schedule.copy(),
                         "extensions": r.stats["extensions"]})
@@ -72,12 +75,12 @@ def _worker(rank, world, port, q):
             dist.destroy_process_group()
 
 
-def _spawn(world):
+def _spawn(world, mode="split"):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
@@ -87,12 +90,18 @@ def _spawn(world):
     return res
 
 
-def test_two_ranks_bit_identical_to_one():
+@pytest.mark.parametrize("mode", ["split", "window"])
+def test_two_ranks_bit_identical_to_one(mode):
+    """split: retrain() then regroup() per window, 1 rank vs 2 ranks;
+    window: the overlapped GroupRetrainer.window() on 2 ranks vs the split
+    sequence on 1 rank (the overlap must not change a bit)."""
     one = _spawn(1)[0]
-    two = _spawn(2)
-    owned = sorted(g for _, local, _, _ in two for g in local)
+    two = _spawn(2, mode)
+    if mode == "window":
+        two = two + _spawn(1, mode)  # and the overlapped window on a single rank
+    owned = sorted(g for _, local, _, _ in two[:2] for g in local)
     assert owned == list(range(len(SIZES)))  # every group on exactly one rank
-    assert all(local for _, local, _, _ in two)  # both ranks hold groups
+    assert all(local for _, local, _, _ in two[:2])  # both ranks hold groups
     ext = 0
     for w in range(WINDOWS):
         a = one[2][w]
