@@ -319,7 +319,7 @@ def run_b200(args, rank, world, local_rank):
 
     if rank == 0:
         pk, pk_kind = peaks()
-        roof = roofline(kst, pk, pk_kind, args, fused=chain)
+        roof = roofline(kst, pk, pk_kind, args, fused=chain, window_ms=ms)
         steps = args.steps
         line = {
             "metric": "group-retrain samples/s (per-window regroup + retrain)",
@@ -504,10 +504,16 @@ def kernel_roofline(name, stat, pk, pk_kind, args, traffic=None, fused=True):
             "algorithmic_gbs": gbs, "hbm_frac": gbs / pk["hbm_gbs"]}
 
 
-def roofline(kst, pk, pk_kind, args, fused=True):
+def roofline(kst, pk, pk_kind, args, fused=True, window_ms=None):
     """The dominant kernel's roofline (the headline `roofline` key) and every
-    kernel family's."""
-    name = max(kst.items(), key=lambda kv: kv[1][1])[0]
+    kernel family's.  Dominant = the family carrying most of the window's
+    algorithmic work (FLOPs): at C4 the regroup matrix (~8.7e13 FLOP per
+    window) against the retrain's ~1.1e12 -- the retrain's fused-chain
+    launches take as much device time, but they are one group's serial
+    chain running BESIDE the matrix on the reserved SMs (latency-bound by
+    construction: its number is reported in `rooflines`, with each family's
+    share of the window's device time)."""
+    name = max(kst.items(), key=lambda kv: kv[1][2])[0]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tpath):
@@ -516,7 +522,13 @@ def roofline(kst, pk, pk_kind, args, fused=True):
         except (OSError, ValueError, AttributeError):
             traffic = None
     head = kernel_roofline(name, kst[name], pk, pk_kind, args, traffic, fused)
+    if head is not None:
+        head["selected_by"] = "largest algorithmic FLOPs of the window"
     every = {k: kernel_roofline(k, v, pk, pk_kind, args, fused=fused) for k, v in kst.items() if v[0]}
+    if window_ms:
+        for k, v in every.items():
+            if v is not None:
+                v["device_ms_share_of_window"] = kst[k][1] / window_ms
     return head, every
 
 
