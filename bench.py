@@ -62,7 +62,8 @@ DEPTH = 1             # speculative chain every group trains up front: the initi
                       # these streams absorbs most of the remaining budget; its chain is extended
                       # by depth doubling (window.py), the other groups' chains are never wasted
 MAX_DEPTH = 64        # deepest extension chain (snapshots: groups x MAX_DEPTH x params in HBM)
-RESERVE_SMS = 8       # SMs the overlapped regroup matrix leaves to the serial extension chains
+RESERVE_SMS = int(os.environ.get("ECCO_RESERVE_SMS", "12"))  # SMs the overlapped
+# regroup matrix leaves to the serial extension chains (and the e2e ingest's fetch CTAs)
 STEPS = 16            # SGD steps per micro-window
 # configs[4]: the detection-head variant (larger per-group model and frame
 # features).  Its window is the allocator's marginal-gain probing (every

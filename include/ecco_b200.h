@@ -358,7 +358,9 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
  * (stream-ordered on the context stream; returns after the fetch).  For
  * chains the caller did not foresee at staging time -- e.g. a chain the
  * allocator replay exhausts and extends (micro_base = micro-windows already
- * committed).  A no-op when the current rings are complete (generated,
+ * committed; depth may exceed max_depth -- up to 65535 micro-windows -- to
+ * fetch the rows of chains that will follow).  A no-op when the current
+ * rings are complete (generated,
  * uploaded or staged whole).  ecco_train_trajectories itself checks, when
  * the current rings are partial, that every row it draws was staged or
  * fetched, and fails with ECCO_ERR_LOGIC otherwise (no silent stale rows). */

@@ -555,8 +555,10 @@ ecco_status ecco_fetch_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
                                       const uint16_t* frames) {
   return guarded(ctx, [&] {
     ECCO_REQUIRE(learned(ctx), "fetch_sampled_frames: learned backend only");
-    ECCO_REQUIRE(n_jobs >= 0 && depth >= 1 && depth <= ctx->cfg.max_depth,
-                 "fetch_sampled_frames: depth must be in [1, max_depth]");
+    // (depth only bounds the draws marked: a caller may fetch ahead of the
+    // chains it will run, e.g. a group's whole remaining budget at once)
+    ECCO_REQUIRE(n_jobs >= 0 && depth >= 1 && depth <= 65535,
+                 "fetch_sampled_frames: depth must be in [1, 65535]");
     ECCO_REQUIRE(n_jobs == 0 || src_off[0] == 0, "CSR offsets must start at 0");
     for (int j = 0; j < n_jobs; ++j)
       validate_batch(ctx, j, gpu_s, src_off[j + 1] - src_off[j], src_cams + src_off[j],

@@ -6,6 +6,7 @@
 // so the result is identical to a full upload (tests/test_gpu_learned.py).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -113,10 +114,15 @@ void fetch_rows(ecco_ctx* ctx, cudaStream_t st, const uint16_t* host_dev, uint16
   if (n_words == 0) return;
   ECCO_REQUIRE(n_words * 32 * (ctx->cfg.feat_dim / 8) < (1ull << 32),
                "sampled-row fetch: ring table too large for 32-bit piece offsets");
-  // two CTAs (64 warps, 6 pieces in flight per lane) beside whatever runs;
+  // four CTAs (128 warps, 6 pieces in flight per lane; ECCO_FETCH_CTAS) beside whatever runs;
   // the CTA-pair evaluation kernel takes its super tiles from a counter, so
   // a pair that starts late (its TPC hosts a fetch CTA) just takes fewer
-  k_fetch_rows<<<2, 1024, 0, st>>>(reinterpret_cast<const uint4*>(host_dev),
+  static const int fetch_ctas = [] {
+    const char* e = getenv("ECCO_FETCH_CTAS");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : 4;
+  }();
+  k_fetch_rows<<<fetch_ctas, 1024, 0, st>>>(reinterpret_cast<const uint4*>(host_dev),
                                    reinterpret_cast<uint4*>(dst), d_flags, n_words,
                                    ctx->cfg.feat_dim / 8, d_count, d_have);
   ECCO_LAUNCHED(ctx);

@@ -227,6 +227,7 @@ class GroupRetrainer:
         rows = [list(t) for t in traj]
         ids = np.arange(self.G, dtype=np.int32)
         extensions, ext_samples = 0, 0
+        fetched = set()  # groups whose remaining rows were topped up this window
         while True:
             width = int(chain.max()) + 1
             T = np.empty((self.G, width))
@@ -250,9 +251,14 @@ class GroupRetrainer:
                 p1 = self.ctx.prepare_trajectories([k], [self.batch], [mem],
                                                    [[1.0 / len(mem)] * len(mem)], [mem])
                 mb = [int(chain[k])]
-                if self.host_frames_ptr:  # sampled ingest: the extension's rows were not staged
-                    self.ctx.fetch_sampled_host_ptr(p1, self.gpu_s, d, window,
-                                                    self.host_frames_ptr, micro_base=mb)
+                if self.host_frames_ptr and k not in fetched:
+                    # sampled ingest: the extension's rows were not staged.  The
+                    # group's rows for every micro-window the budget could still
+                    # give it are fetched at once (one top-up per group and
+                    # window, at most its members' rings), not per extension
+                    self.ctx.fetch_sampled_host_ptr(p1, self.gpu_s, int(min(self.W - p, 65535)),
+                                                    window, self.host_frames_ptr, micro_base=mb)
+                    fetched.add(k)
                 ext = self.ctx.train_prepared(p1, self.gpu_s, d, window=window, micro_base=mb)[0]
             ext = self.broadcast(ext, owner)
             rows[k] = rows[k] + list(ext[1:])
