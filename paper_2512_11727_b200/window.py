@@ -131,6 +131,7 @@ class GroupRetrainer:
         self.slot_of = {g: k for k, g in enumerate(self.local)}
         self.stats = {}
         self.host_frames_ptr = 0  # pinned [N][R][F] table of a sampled ingest (set_host_frames)
+        self.prev_counts = np.zeros(self.G, np.int64)  # last window's grants (extension depths)
 
     # ---------------------------------------------------------- collectives --
     def _coll_device(self):
@@ -224,24 +225,31 @@ class GroupRetrainer:
             if self.local:
                 self.ctx.commit(self.local, [1] * len(self.local))
             after_initial()
-        rows = [list(t) for t in traj]
+        # trajectories as the replay reads them: row g holds the chain's
+        # accuracies, padded with its last one (beyond the chain: never read by
+        # the final replay); grown in place as chains are extended
+        T = np.array(traj, dtype=np.float64, copy=True)
         ids = np.arange(self.G, dtype=np.int32)
         extensions, ext_samples = 0, 0
         fetched = set()  # groups whose remaining rows were topped up this window
+        first_ext = set()
         while True:
-            width = int(chain.max()) + 1
-            T = np.empty((self.G, width))
-            for g in range(self.G):
-                r = rows[g]
-                T[g, :len(r)] = r
-                T[g, len(r):] = r[-1]  # beyond the chain: never read by the final replay
             jobs, _, _, _ = allocate_trajectories(ids, self.sizes, T, self.alpha, self.beta,
                                                   self.W, self.gpu_s, 1, self.bonus, self.policy)
             p = first_exhausted(jobs, chain)
             if p < 0:
                 break
             k = int(jobs[p])
-            d = int(min(self.max_depth, max(1, 2 * last_d[k]), self.W - p))
+            d = max(1, 2 * int(last_d[k]))
+            if k not in first_ext:
+                # a group extended last window too is likely to take as many
+                # micro-windows again (the greedy's fairness bonus keeps
+                # feeding the least accurate group): start its doubling there
+                # -- fewer round trips, no effect on the schedule (a chain the
+                # greedy does not use up is simply not committed)
+                first_ext.add(k)
+                d = max(d, int(self.prev_counts[k]) - int(chain[k]))
+            d = int(min(self.max_depth, d, self.W - p))
             owner = self.placement.owner[k]
             ext = np.zeros(d + 1)
             if owner == self.rank:
@@ -261,12 +269,17 @@ class GroupRetrainer:
                     fetched.add(k)
                 ext = self.ctx.train_prepared(p1, self.gpu_s, d, window=window, micro_base=mb)[0]
             ext = self.broadcast(ext, owner)
-            rows[k] = rows[k] + list(ext[1:])
+            need = int(chain[k]) + d + 1
+            if need > T.shape[1]:
+                T = np.concatenate([T, np.repeat(T[:, -1:], need - T.shape[1], axis=1)], axis=1)
+            T[k, int(chain[k]) + 1:need] = ext[1:]
+            T[k, need:] = ext[-1]
             chain[k] += d
             last_d[k] = d
             extensions += 1
             ext_samples += d * int(self.steps[k]) * self.B
         counts = np.bincount(jobs, minlength=self.G)
+        self.prev_counts = counts
         self.traj = T  # the trajectories the final replay read (extensions included)
         self.schedule = jobs
         if self.local:
