@@ -622,7 +622,7 @@ def test_sampled_ingest_refuses_unstaged_draws_and_fetch_tops_up():
         if sampled:  # a fetch ahead of many future micro-windows (depth > max_depth)
             ctx.fetch_sampled_host_ptr(p, 6.0, 40, 3, fr.data_ptr(), micro_base=[3, 3, 3])
         acc3 = ctx.train_prepared(p, 6.0, 2, window=3, micro_base=[20, 20, 20])
-        acc2 = np.concatenate([acc2, acc3])
+        acc2 = np.concatenate([acc2.ravel(), acc3.ravel()])
         res.append((acc.tobytes(), acc2.tobytes(),
                     [w.tobytes() for j in ids for w in ctx.get_weights(j)]))
     assert res[0] == res[1]
