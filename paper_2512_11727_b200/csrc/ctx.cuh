@@ -247,7 +247,7 @@ struct ecco_ctx {
   }
 
   DevBuf scratch[20];
-  DevBuf train_scratch[10];  // [8]: bf16 W1^T shadow of the general tensor-core training path  // unfused training rows (learned_kernels.cu)  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
+  DevBuf train_scratch[11];  // [8]: bf16 W1^T shadow of the general tensor-core training path  // unfused training rows (learned_kernels.cu)  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
   HostBuf hscratch[4];
 
   int slot(int job_id) const {

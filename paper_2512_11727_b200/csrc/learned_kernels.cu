@@ -245,10 +245,19 @@ static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint
 constexpr int kHT = 32;  // reduction chunk of the tiled head kernels
 
 // logits: 64 rows x 32 classes per block, 4 rows x 4 classes per thread.
+// (split-K form, tensor-core math only -- the sum order is not the
+// oracle's: block z covers hidden units [z*kspan, (z+1)*kspan) and writes
+// its partial (no b2) to L + z*n_rows*C; k_l_logits_sum adds the partials in
+// z order and b2.  kspan = H is the exact form.)
 __global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const int* blk_slot,
                                                     Gate gate, const float* wbase,
-                                                    size_t n_params, const float* Z, float* L) {
+                                                    size_t n_params, const float* Z, float* L,
+                                                    int kspan = 0) {
   const int blk = blockIdx.x, c0 = blockIdx.y * 32;
+  const int kb = kspan > 0 ? blockIdx.z * kspan : 0;
+  const int ke = kspan > 0 ? kb + kspan : g.H;
+  const bool part = kspan > 0;
+  if (part) L += (size_t)blockIdx.z * n_rows * g.C;
   if (!gate.live_row((size_t)blk * kRB)) return;
   const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
   const float* b2 = W2 + (size_t)g.H * g.C;
@@ -272,8 +281,8 @@ __global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const i
       wr[u] = c0 + c < g.C ? W2[(size_t)(k0 + k) * g.C + c0 + c] : 0.0f;
     }
   };
-  fetch(0);
-  for (int k0 = 0; k0 < g.H; k0 += kHT) {
+  fetch(kb);
+  for (int k0 = kb; k0 < ke; k0 += kHT) {
 #pragma unroll
     for (int u = 0; u < kZ; ++u) {
       const int e = tid + u * 128;
@@ -285,7 +294,7 @@ __global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const i
       Ws[e / 32][e % 32] = wr[u];
     }
     __syncthreads();
-    if (k0 + kHT < g.H) fetch(k0 + kHT);
+    if (k0 + kHT < ke) fetch(k0 + kHT);
 #pragma unroll 8
     for (int k = 0; k < kHT; ++k) {
       const float4 z = *reinterpret_cast<const float4*>(&Zs[k][ty * 4]);
@@ -303,8 +312,23 @@ __global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const i
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = c0 + tx * 4 + q;
-      if (c < g.C) L[(r0 + ty * 4 + i) * g.C + c] = __fadd_rn(acc[i][q], b2[c]);
+      if (c < g.C) L[(r0 + ty * 4 + i) * g.C + c] = part ? acc[i][q] : __fadd_rn(acc[i][q], b2[c]);
     }
+}
+
+// logits = sum of the ks split-K partials (z ascending) + b2 of the row's model.
+__global__ void k_l_logits_sum(LDims g, int n_rows, int ks, const int* blk_slot, Gate gate,
+                               const float* wbase, size_t n_params, const float* Lp, float* L) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)n_rows * g.C) return;
+  const size_t r = e / g.C;
+  if (!gate.live_row(r)) return;
+  const int c = (int)(e % g.C);
+  const float* b2 = wbase + (size_t)blk_slot[r / kRB] * n_params + (size_t)g.F * g.H + g.H +
+                    (size_t)g.H * g.C;
+  float v = Lp[e];
+  for (int z = 1; z < ks; ++z) v = __fadd_rn(v, Lp[(size_t)z * n_rows * g.C + e]);
+  L[e] = __fadd_rn(v, b2[c]);
 }
 
 // dH: 64 rows x 64 hidden units per block, 8 rows x 4 units per thread; c ascending.
@@ -1048,6 +1072,16 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   float* DL = rows ? (float*)ts[5].get(sizeof(float) * (size_t)rows * g.C) : nullptr;
   float* DH = rows ? (float*)ts[6].get(sizeof(float) * (size_t)rows * g.H) : nullptr;
   float* loss_rows = rows ? (float*)ts[7].get(sizeof(float) * rows) : nullptr;
+  // tensor-core math with few head blocks (one group's chain: the K = H
+  // logits loop is latency bound on a handful of SMs): split-K logits
+  int head_ks = 1;
+  if (rows && ctx->cfg.math == ECCO_MATH_TC_BF16 && !ctx->fused_train) {
+    const int blocks = (rows / kRB) * ((g.C + 31) / 32);
+    while (head_ks < 16 && blocks * head_ks * 2 <= 128 && (g.H / (head_ks * 2)) % kHT == 0)
+      head_ks *= 2;
+  }
+  float* Lp = head_ks > 1 ? (float*)ts[10].get(sizeof(float) * (size_t)head_ks * rows * g.C)
+                          : nullptr;
   // spec chain buffer per slot: T snapshots; train in place in snapshot t-1
   std::vector<int> slots(n_jobs);
   ECCO_CUDA(ctx_memcpy(ctx, slots.data(), d_slots, sizeof(int) * n_jobs, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1178,8 +1212,14 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
         ECCO_LAUNCHED(ctx);
       }
       ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_HEAD, 8.0 * lrows * g.H * g.C, lrows * g.H * 12,
-                 ((k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
-                      g, rows, blk_slot, gate, wt, spec_stride, Z, L)),
+                 ((head_ks > 1
+                       ? (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32, head_ks), 128, 0,
+                                         ctx->stream>>>(g, rows, blk_slot, gate, wt, spec_stride,
+                                                        Z, Lp, g.H / head_ks),
+                          k_l_logits_sum<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
+                              g, rows, head_ks, blk_slot, gate, wt, spec_stride, Lp, L))
+                       : k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
+                             g, rows, blk_slot, gate, wt, spec_stride, Z, L)),
                   (k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(
                       g, rows, gate, L, row_lab, DL, loss_rows)),
                   (k_l_dh_t<<<dim3(rows / kRB, g.H / 64), 128, 0, ctx->stream>>>(

@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_dw1(Dw1Args a) {
 // B = the bf16 W1^T shadow by TMA ({64, 256} boxes), kind::f16 MMAs (M 128,
 // N 256, K 16) into TMEM, 2 stages of K = 64 (two CTAs per SM hide the
 // gather latency better than four stages in one).
-constexpr int kBfNT = 256, kBfStages = 2;  // 96 KB: two CTAs per SM
+constexpr int kBfNT = 256;
 constexpr uint32_t kBfA = 128 * 128, kBfB = kBfNT * 128;  // bytes per stage
 
 struct FwdBfArgs {
@@ -436,6 +436,9 @@ struct FwdBfArgs {
   int F, H;
 };
 
+// STG pipeline stages: 2 (96 KB, two CTAs per SM) for full grids, 4 (192 KB)
+// when the grid is small (a single group's chain: the K loop is latency bound)
+template <int STG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_tc_fwd_bf16(const __grid_constant__ CUtensorMap map_w, FwdBfArgs a) {
   const TcTile tile = a.tiles[blockIdx.x];
@@ -443,8 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n0 = blockIdx.y * kBfNT;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kBfStages * kBfA;
-  __shared__ uint64_t full[kBfStages], empty[kBfStages], done;
+  uint8_t* sB = smem + STG * kBfA;
+  __shared__ uint64_t full[STG], empty[STG], done;
   __shared__ uint32_t tmem_base;
   __shared__ int64_t rows[kM];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) tmem_alloc(&tmem_base, (uint32_t)kBfNT);
   if (tid == 0) {
     if (sm100::smem_u32(smem) & 1023u) __trap();
-    for (int s = 0; s < kBfStages; ++s) {
+    for (int s = 0; s < STG; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -467,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int brow = tile.slot * a.H + n0;  // first W1^T row of this CTA
   // A gather: thread tid owns row tid, its 8 16-byte pieces of the chunk
   auto load = [&](int kc) {
-    const int s = kc % kBfStages;
+    const int s = kc % STG;
     const uint32_t dst = sm100::smem_u32(sA + s * kBfA) + tid * 128;
     const uint16_t* src = a.xbase + rows[tid] + kc * 64;
 #pragma unroll
@@ -481,22 +484,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       sm100::tma_load_2d(sB + s * kBfB, &map_w, kc * 64, brow, &full[s]);
     }
   };
-  for (int kc = 0; kc < kBfStages - 1 && kc < nk; ++kc) load(kc);
+  for (int kc = 0; kc < STG - 1 && kc < nk; ++kc) load(kc);
   const uint32_t idf = sm100::idesc(kM, kBfNT, sm100::kFmtBF16);
   for (int kc = 0; kc < nk; ++kc) {
-    const int s = kc % kBfStages;
-    const int nx = kc + kBfStages - 1;
+    const int s = kc % STG;
+    const int nx = kc + STG - 1;
     if (nx < nk) {
-      if (nx >= kBfStages) mbar_wait(&empty[nx % kBfStages], ((nx / kBfStages) - 1) & 1);
+      if (nx >= STG) mbar_wait(&empty[nx % STG], ((nx / STG) - 1) & 1);
       load(nx);
-      asm volatile("cp.async.wait_group %0;" ::"n"(kBfStages - 1) : "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(STG - 1) : "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
-      mbar_wait(&full[s], (kc / kBfStages) & 1);
+      mbar_wait(&full[s], (kc / STG) & 1);
       tc_fence_after();
       const uint64_t da = sm100::desc_kmajor_sw128(sm100::smem_u32(sA + s * kBfA));
       const uint64_t db = sm100::desc_kmajor_sw128(sm100::smem_u32(sB + s * kBfB));
@@ -586,16 +589,22 @@ void fwd_hidden_bf16(ecco_ctx* ctx, const uint16_t* xbase, const int64_t* row_of
   ECCO_REQUIRE(H % kBfNT == 0 && F % 64 == 0, "bf16 forward: H % 256 and F % 64");
   const CUtensorMap map = fused::tensor_map_bf16(w1t, n_slots * H, F, kBfNT);
   FwdBfArgs a{xbase, row_off, tiles, steps, step, wbase, wstride, Z, F, H};
-  const size_t sm = kBfStages * (size_t)(kBfA + kBfB);
   static DeviceFlags attr;  // per device
   if (!attr.done(ctx->cfg.device)) {
-    ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sm));
+    ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd_bf16<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(2 * (size_t)(kBfA + kBfB))));
+    ECCO_CUDA(cudaFuncSetAttribute(k_tc_fwd_bf16<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(4 * (size_t)(kBfA + kBfB))));
     attr.mark(ctx->cfg.device);
   }
+  int sms = 0;
+  ECCO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device));
+  const bool deep = (long)n_tiles * (H / kBfNT) * 2 <= sms;  // room for one CTA per SM
   const int kind = steps ? ECCO_KSTAT_TRAIN_STEP : ECCO_KSTAT_EVAL_MATRIX;
+  const dim3 grid(n_tiles, H / kBfNT);
   ECCO_TIMED(ctx, kind, 2.0 * live_rows * F * H, live_rows * F * 2.0 + (double)F * H * 2,
-             (k_tc_fwd_bf16<<<dim3(n_tiles, H / kBfNT), kThreads, sm, ctx->stream>>>(map, a)));
+             (deep ? k_tc_fwd_bf16<4><<<grid, kThreads, 4 * (size_t)(kBfA + kBfB), ctx->stream>>>(map, a)
+                   : k_tc_fwd_bf16<2><<<grid, kThreads, 2 * (size_t)(kBfA + kBfB), ctx->stream>>>(map, a)));
   ECCO_LAUNCHED(ctx);
 }
 
