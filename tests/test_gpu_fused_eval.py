@@ -281,3 +281,38 @@ def test_multi_tile_regime_beside_the_sampled_row_fetch(monkeypatch, eval_kernel
     assert lb2.tobytes() == lb.tobytes()
     drawn = (fr2 == fr).all(-1)
     assert drawn.any()
+
+
+def test_async_matrix_equals_sync_and_overlaps_a_chain(eval_kernel):
+    """ecco_eval_matrix_dev_async on the context's matrix stream (grid
+    leaving SMs free) while a fused SGD chain runs on the context stream:
+    after ecco_matrix_join its matrix equals the synchronous one bitwise for
+    every model the chain does not commit (the chain's own column is the
+    only one that may differ and is re-evaluated by the caller)."""
+    import torch
+    n_cams, ids = 40, [0, 1, 2, 3, 4, 5, 6]
+    ctx = ecco.Context(backend=ecco.LEARNED, math=ecco.TC_BF16, max_cameras=n_cams, max_jobs=8,
+                       max_depth=4, **dict(DIMS, ring_frames=128), steps_per_gpu_s=16.0)
+    rng = np.random.default_rng(60)
+    ctx.set_cameras(np.round(rng.random((n_cams, 2)), 1), np.full(n_cams, 8.192e6))
+    ctx.generate_frames(2)
+    _random_models(ctx, rng, ids)
+    cams = np.arange(n_cams, dtype=np.int32)
+    want = ctx.eval_matrix(ids, cams=cams)
+    out = torch.empty((n_cams, len(ids)), dtype=torch.float64, device="cuda")
+    ctx.eval_matrix_dev_async(ids, out.data_ptr(), cams, reserve_sms=16)
+    # meanwhile: job 6's chain on the context stream, committed
+    mem = list(range(8))
+    ctx.train_trajectories([6], [(30.0, 1080.0, 1.0)], [mem], [[1 / 8] * 8], [mem], 1.0, 2,
+                           window=2)
+    ctx.commit([6], [2])
+    ctx.matrix_join()
+    ctx.synchronize()
+    got = out.cpu().numpy()
+    assert got[:, :6].tobytes() == want[:, :6].tobytes()
+    after = ctx.eval_matrix([6], cams=cams)  # the re-evaluated column of the trained job
+    assert np.isfinite(after).all()
+    ffma = ecco.Context(backend=ecco.LEARNED, math=ecco.FFMA_EXACT, max_cameras=4, max_jobs=2,
+                        **DIMS)
+    with pytest.raises(ecco.InvalidArgument):
+        ffma.eval_matrix_dev_async([0], out.data_ptr(), cams[:2])
