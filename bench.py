@@ -290,11 +290,14 @@ def run_b200(args, rank, world, local_rank):
     ms = t0.elapsed_time(t1)
     # ECCO_KSTAT_TRAIN_STEP is the fused SGD chain where it applies
     # (train_kernels.cu: tensor-core math, B = 128, C = 16, F a power of two
-    # <= 512, H = 256 / 512), else the unfused forward; DW1 / HEAD are the
+    # <= 512, H = 256 / 512; wide_kernels.cu: the detection head F = 1024,
+    # C = 96, H = 512 / 1024), else the unfused forward; DW1 / HEAD are the
     # unfused tensor-core / FFMA kernels (other shapes, --math ffma)
     F, H = DIMS["feat_dim"], DIMS["hidden_dim"]
-    chain = (args.math != "ffma" and DIMS["minibatch"] == 128 and DIMS["num_classes"] == 16
-             and F <= 512 and F % 128 == 0 and F & (F - 1) == 0 and H in (256, 512))
+    chain = (args.math != "ffma" and DIMS["minibatch"] == 128 and
+             ((DIMS["num_classes"] == 16 and F <= 512 and F % 128 == 0 and F & (F - 1) == 0
+               and H in (256, 512)) or
+              (DIMS["num_classes"] == 96 and F == 1024 and H in (512, 1024))))
     kst = {name: ctx.kernel_stat(getattr(ecco, "KSTAT_" + stat)) for name, stat in
            (("EVAL_MATRIX", "EVAL_MATRIX"), ("EVAL_PAIRS", "EVAL_PAIRS"),
             ("TRAIN_CHAIN" if chain else "TRAIN_FWD", "TRAIN_STEP"), ("TRAIN_DW1", "TRAIN_DW1"),

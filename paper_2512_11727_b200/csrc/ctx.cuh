@@ -246,8 +246,10 @@ struct ecco_ctx {
     if (slot >= 0 && slot < (int)sh_dirty.size()) sh_dirty[slot] = 1;
   }
 
-  DevBuf scratch[20];
-  DevBuf train_scratch[11];  // [8]: bf16 W1^T shadow of the general tensor-core training path  // unfused training rows (learned_kernels.cu)  // 0-3: ABI staging, 4-7: eval rows, 8-11: tensor-core tiles
+  DevBuf scratch[22];  // 19-20: the general-path evaluation plan of a chain (learned_kernels.cu)
+  // 0-10: general training path (learned_kernels.cu; 0-1 also the fused chains' sampled rows),
+  // 11: the wide chain's gathered minibatch rows (wide_kernels.cu)
+  DevBuf train_scratch[12];
   HostBuf hscratch[4];
 
   int slot(int job_id) const {
@@ -363,6 +365,17 @@ CUtensorMap tensor_map_bf16(const void* base, uint64_t rows, uint64_t cols, uint
 void counts_to_acc(ecco_ctx* ctx, size_t n, const int* d_counts, const uint8_t* d_mask,
                    double* d_out);
 bool train_supported(const ecco_ctx* ctx);
+// Fused SGD chain for wide models (wide_kernels.cu: F <= 1024, H = 512 or
+// 1024, C <= 128, the detection head of BASELINE configs[4]): a cluster of
+// H/64 CTAs per job, fp32 masters read-modify-written in the snapshot (L2)
+// every step.  Same contract as train_chain (which dispatches to it).
+bool wide_supported(const ecco_ctx* ctx);
+// The sampled rows chain_rows() drew, gathered into contiguous minibatches
+// for the wide chain (called by chain_rows for wide shapes).
+void wide_gather(ecco_ctx* ctx, int n_jobs, const int* d_steps, int max_steps, int n_micro);
+void train_wide(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_steps,
+                const int* h_steps, int micro, int n_micro, const float* wsrc, size_t wsrc_stride,
+                float* wbase, size_t wstride, int loss_t);
 // Fused SGD chain (train_kernels.cu): every job's steps[j] SGD steps of one
 // micro-window in ONE launch, one thread-block cluster per job with the fp32
 // masters resident in TMEM, starting from the models at wsrc and leaving them

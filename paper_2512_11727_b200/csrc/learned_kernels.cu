@@ -711,6 +711,16 @@ void init(ecco_ctx* ctx) {
     ctx->fused_eval = true;
     ctx->fused_train = fused::train_supported(ctx);
     ctx->w1_t = ctx->fused_train;
+  } else if (ctx->cfg.math == ECCO_MATH_TC_BF16 && fused::wide_supported(ctx)) {
+    // wide models (detection head): fused chains, members evaluated on the
+    // general path on a side stream beside the next micro-window's chain
+    ctx->fused_train = true;
+    ctx->w1_t = true;  // [H][F]: a CTA's master slice is contiguous
+    ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->eval_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->ev_chain[i], cudaEventDisableTiming));
+      ECCO_CUDA(cudaEventCreateWithFlags(&ctx->ev_eval[i], cudaEventDisableTiming));
+    }
   }
 }
 
@@ -798,6 +808,72 @@ static void pair_counts_fused(ecco_ctx* ctx, const Shadow& sh, const float* wbas
   ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(n_pairs, 1), ctx->stream));
   fused::eval_counts(ctx, sh, wbase, wstride, n_pairs, d_cam, (int)ent.size(), d_ent, d_ent,
                      n_tiles, d_ebeg, d_slot, 0, d_counts, nullptr, (double)n_pairs, pair);
+}
+
+// The general (unfused) tensor-core evaluation of a fixed list of (slot,
+// camera) pairs, planned once: the wide fused chain (detection-head shapes)
+// evaluates the same member pairs after every micro-window, so the 128-row
+// tile list and the evaluated slots are built on the host from the host's
+// pair slots and uploaded ONCE per call -- no device->host read or pageable
+// upload (which would drain the stream) inside the chain.
+struct GeneralPlan {
+  bool ok = false;
+  int n_pairs = 0, n_tiles = 0, n_us = 0;
+  const TcTile* d_tiles = nullptr;
+  const int* d_us = nullptr;
+};
+
+static GeneralPlan plan_general(ecco_ctx* ctx, int n_pairs, const int* h_slot) {
+  const LDims g = dims(ctx);
+  GeneralPlan pl;
+  const int chunk = std::max(1, (int)std::min<size_t>(n_pairs, (size_t)(256u << 20) / ((size_t)g.S * g.H * 4)));
+  if (n_pairs == 0 || n_pairs > chunk || g.S % kRB || g.H % 256 || ctx->cfg.math != ECCO_MATH_TC_BF16)
+    return pl;  // pair_counts (chunked, per-call plan) serves the rest
+  const int nb = n_pairs * g.S / kRB;
+  std::vector<int> hslot(nb);
+  for (int b = 0; b < nb; ++b) hslot[b] = h_slot[(size_t)b * kRB / g.S];
+  std::vector<TcTile> tiles;  // same cut as pair_counts: never straddle two models
+  for (int b = 0; b < nb;) {
+    const int take = (b + 1 < nb && hslot[b + 1] == hslot[b]) ? 2 : 1;
+    tiles.push_back({hslot[b], b * kRB, take * kRB, 0});
+    b += take;
+  }
+  std::vector<int> us(hslot);
+  std::sort(us.begin(), us.end());
+  us.erase(std::unique(us.begin(), us.end()), us.end());
+  pl.d_tiles = ctx->upload(19, tiles.data(), tiles.size());
+  pl.d_us = ctx->upload(20, us.data(), us.size());
+  pl.n_tiles = (int)tiles.size();
+  pl.n_us = (int)us.size();
+  pl.n_pairs = n_pairs;
+  pl.ok = true;
+  return pl;
+}
+
+static void pair_counts_general_planned(ecco_ctx* ctx, const GeneralPlan& pl, const float* wbase,
+                                        size_t wstride, const int* d_pair_slot,
+                                        const int* d_pair_cam, int* d_counts) {
+  const LDims g = dims(ctx);
+  const int np = pl.n_pairs, rows = np * g.S, nb = rows / kRB;
+  ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * np, ctx->stream));
+  int64_t* row_off = (int64_t*)ctx->scratch[4].get(sizeof(int64_t) * rows);
+  int* blk_slot = (int*)ctx->scratch[5].get(sizeof(int) * nb);
+  float* Z = (float*)ctx->scratch[6].get(sizeof(float) * (size_t)rows * g.H);
+  float* L = (float*)ctx->scratch[7].get(sizeof(float) * (size_t)rows * g.C);
+  k_l_pair_rows<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, d_pair_slot, d_pair_cam, row_off,
+                                                           blk_slot);
+  ECCO_LAUNCHED(ctx);
+  uint16_t* w1t = (uint16_t*)ctx->train_scratch[9].get((size_t)ctx->cfg.max_jobs * g.H * g.F * 2);
+  fused::shadow_w1t(ctx, pl.d_us, pl.n_us, wbase, wstride, w1t);
+  tc::fwd_hidden_bf16(ctx, ctx->d_eval, row_off, pl.d_tiles, pl.n_tiles, nullptr, 0, w1t,
+                      (size_t)ctx->cfg.max_jobs, wbase, wstride, Z, (double)rows);
+  ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
+             (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
+                 g, rows, blk_slot, Gate{nullptr, 0, 1}, wbase, wstride, Z, L)));
+  ECCO_LAUNCHED(ctx);
+  k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, L, ctx->d_eval_labels, d_pair_cam,
+                                                       d_counts);
+  ECCO_LAUNCHED(ctx);
 }
 
 void generate_frames(ecco_ctx* ctx, int window) {
@@ -1123,8 +1199,13 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     n_idle = (int)idle.size();
     d_idle = ctx->upload(18, idle.data(), idle.size());
   }
+  // the wide chain's member evaluations: the general path, planned once
+  GeneralPlan gen_plan;
+  if (n_mem && !ctx->fused_eval && ctx->fused_train) gen_plan = plan_general(ctx, n_mem, hps.data());
   // acc[:, 0] from the committed models
-  if (n_mem && ctx->fused_eval) {
+  if (gen_plan.ok) {
+    pair_counts_general_planned(ctx, gen_plan, ctx->d_w, ctx->n_params, d_ps, d_mem_cam, d_cnt);
+  } else if (n_mem && ctx->fused_eval) {
     refresh_committed(ctx, hps.data(), n_mem);
     pair_counts_planned(ctx, ctx->sh_commit, ctx->d_w, ctx->n_params, spec_plan, d_ps, d_mem_cam,
                         d_cnt);
@@ -1140,7 +1221,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   // runs beside the chain of state t+1 (the two alternate between the two
   // speculative shadows: chain t+2 rewrites the shadow eval t reads, so it
   // waits for it).
-  const bool side = ctx->fused_train && ctx->eval_stream && n_mem > 0 && ctx->fused_eval;
+  const bool side = ctx->fused_train && ctx->eval_stream && n_mem > 0 && (ctx->fused_eval || gen_plan.ok);
   if (ctx->fused_train)
     fused::chain_rows(ctx, n_jobs, d_job_ids, d_steps, h_steps, d_src_off, d_src_cam, d_src_frac,
                       d_micro_base, depth, window);
@@ -1163,8 +1244,12 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
         cudaStream_t main_stream = ctx->stream;
         ctx->stream = ctx->eval_stream;  // the evaluation of state t, on the side stream
         try {
-          fused::refresh_shadow_dev(ctx, *sh, wt, spec_stride, d_slots, n_jobs, d_idle, n_idle);
-          pair_counts_planned(ctx, *sh, wt, spec_stride, spec_plan, d_ps, d_mem_cam, d_cnt);
+          if (gen_plan.ok) {  // wide chains: the planned general evaluation of snapshot t
+            pair_counts_general_planned(ctx, gen_plan, wt, spec_stride, d_ps, d_mem_cam, d_cnt);
+          } else {
+            fused::refresh_shadow_dev(ctx, *sh, wt, spec_stride, d_slots, n_jobs, d_idle, n_idle);
+            pair_counts_planned(ctx, *sh, wt, spec_stride, spec_plan, d_ps, d_mem_cam, d_cnt);
+          }
           k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(
               g, n_jobs, d_mem_off, d_cnt, ctx->cfg.params.acc_floor, d_out, depth + 1, t);
           ECCO_LAUNCHED(ctx);
@@ -1254,6 +1339,13 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
                                 ctx->fused_train ? d_idle : d_slots,
                                 ctx->fused_train ? n_idle : n_jobs);
       pair_counts_planned(ctx, ctx->sh_spec, wt, spec_stride, spec_plan, d_ps, d_mem_cam, d_cnt);
+      k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
+                                                                ctx->cfg.params.acc_floor, d_out, depth + 1, t);
+      ECCO_LAUNCHED(ctx);
+      continue;
+    }
+    if (gen_plan.ok) {  // wide chains: no host round trip between micro-windows
+      pair_counts_general_planned(ctx, gen_plan, wt, spec_stride, d_ps, d_mem_cam, d_cnt);
       k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
                                                                 ctx->cfg.params.acc_floor, d_out, depth + 1, t);
       ECCO_LAUNCHED(ctx);

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_learned.py -q -p no:cacheprovider -k "wide or detection" > gpurun_out/r2_t32.log 2>&1; echo rc=$? >> gpurun_out/r2_t32.log
+ECCO_WIDE_TRACE=1 timeout 300 python tools/single_chain.py 2 1 c5 >> gpurun_out/r2_t32.log 2>&1
+timeout 300 python tools/single_chain.py 8 3 c5 >> gpurun_out/r2_t32.log 2>&1
+timeout 1500 python bench.py --config c5 --no-parametric --no-scaling --no-cpu --steps 3 > gpurun_out/r2_b32_c5.json 2> gpurun_out/r2_b32_c5.err; echo rc=$? >> gpurun_out/r2_b32_c5.err
