@@ -65,9 +65,10 @@ constexpr int kThreads = kEpi + 64;       // + warp 8 (gather), warp 9 (MMA)
 constexpr int kMaxNM = 8;                 // 128-feature tiles (F <= 1024)
 constexpr uint32_t kSlot = 32768;         // ring slot: two 64-feature chunks of 128 rows
 constexpr uint32_t kColZ = 0;             // Z, then dL.W2^T (64 columns)
-constexpr uint32_t kColL = 64;            // partial logits (C <= 128)
-constexpr uint32_t kColW2 = 192;          // dW2 (rows 0-63 = hidden units)
-constexpr uint32_t kColB1 = 320;          // -lr db1 (16 columns)
+constexpr uint32_t kColL = 64;            // partial logits (C <= 96)
+constexpr uint32_t kColW2 = 160;          // dW2 (rows 0-63 = hidden units)
+constexpr uint32_t kColW2M = 256;         // the fp32 W2 master slice (rows 0-63)
+constexpr uint32_t kColB1 = 352;          // -lr db1 (16 columns)
 constexpr uint32_t kColD = 384;           // two dW1 tile buffers of 64 columns
 
 struct WideArgs {
@@ -99,6 +100,7 @@ struct WBars {
   uint64_t zfull, r_ready, plfull, recv_full, dl_full, dhfull, w2full, dh_ready, b1full;
   uint64_t dfull[2], dempty[2];  // dW1 tile buffers
   uint64_t fwd_done[2];          // every CTA's forward of step t done (by step parity)
+  uint64_t stage_free;           // the partial logits staged in the ring have been sent
   uint64_t xready[kMaxNM];       // W1 operand tile rebuilt
 };
 
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->full[i], 1);
       mbar_init(&bars->empty[i], 1);
       mbar_init(&bars->dfull[i], 1);
-      mbar_init(&bars->dempty[i], kEpi);
+      mbar_init(&bars->dempty[i], kEpi / 2);
       mbar_init(&bars->fwd_done[i], cs);
     }
     mbar_init(&bars->zfull, 1);
@@ -267,15 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->w2full, 1);
     mbar_init(&bars->dh_ready, kEpi);
     mbar_init(&bars->b1full, 1);
-    for (int mt = 0; mt < kMaxNM; ++mt) mbar_init(&bars->xready[mt], kEpi);
+    mbar_init(&bars->stage_free, 1);
+    for (int mt = 0; mt < kMaxNM; ++mt) mbar_init(&bars->xready[mt], kEpi / 2);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(sTmem, 512);
-  if (src != dst) {  // the starting model's slices -> the snapshot trained in place
+  if (src != dst) {  // the starting W1 slice -> the snapshot trained in place
     const float4* s4 = reinterpret_cast<const float4*>(src + (size_t)h0 * F);
     float4* d4 = reinterpret_cast<float4*>(W1 + (size_t)h0 * F);
     for (int i = tid; i < kHS * F / 4; i += kThreads) d4[i] = s4[i];
-    for (int i = tid; i < kHS * C; i += kThreads) W2[(size_t)h0 * C + i] = sW2s[(size_t)h0 * C + i];
   }
   if (tid < kHS) sB1[tid] = sb1[h0 + tid];
   if (tid < C) sB2[tid] = sb2[tid];
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int e = tid; e < C * kHS / 8; e += kEpi) {  // W2 image
       const int c = e >> 3, hc = e & 7;
-      const float* w = W2 + (size_t)(h0 + hc * 8) * C + c;
+      const float* w = sW2s + (size_t)(h0 + hc * 8) * C + c;
       uint4 pk;
       pk.x = pack_bf16x2(w[0 * C], w[1 * C]);
       pk.y = pack_bf16x2(w[2 * C], w[3 * C]);
@@ -305,12 +307,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       *reinterpret_cast<uint4*>(sW2i + c * 128 + ((hc ^ (c & 7)) << 4)) = pk;
     }
   }
+  tc_fence_before();
+  __syncthreads();  // (the TMEM allocation is visible)
+  tc_fence_after();
+  const uint32_t tmem = *sTmem;
+  if (tid < kEpi && q < 2) {  // the W2 master slice -> TMEM lane s (hidden unit h0 + s)
+    const float* w = sW2s + (size_t)(h0 + s) * C + p * (C / 2);
+    for (int c16 = 0; c16 < C / 32; ++c16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(w[c16 * 16 + i]);
+      tmem_st16(tmem + lane_base + kColW2M + p * (C / 2) + c16 * 16, v);
+    }
+    tmem_st_wait();
+  }
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // every CTA of the cluster is running before any DSMEM traffic
   tc_fence_after();
-  const uint32_t tmem = *sTmem;
   const uint32_t ring_a = smem_u32(ring), w1_a = smem_u32(sW1), w2i_a = smem_u32(sW2i);
   const uint32_t r_a = smem_u32(sR), dl_a = smem_u32(sDL), dh_a = smem_u32(sDH);
 
@@ -328,6 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int sl = (int)(k & 1u);
           const uint32_t u = k >> 1;
           if (u) mbar_wait(&bars->empty[sl], (u - 1) & 1u);
+          // the head stages this step's partial logits in the ring after the
+          // forward: dW1's rows load once they have been sent
+          if (pass == 1 && mt == 0) mbar_wait(&bars->stage_free, (uint32_t)t & 1u);
           if (lane == 0) {
             mbar_expect_tx(&bars->full[sl], kSlot);
             tma_load_2d(ring + sl * kSlot, &map_x, (2 * mt) * 64, row0, &bars->full[sl]);
@@ -465,6 +483,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_cluster(mapa_shared(smem_u32(&bars->fwd_done[t & 1]), (uint32_t)lane));
 
       // ------------------------------ partial logits -> the row owner --
+      // staged in the ring (free between the forward and dW1's row loads)
+      // as [owner][row of its block][class] fp32, 16-byte chunks swizzled
+      // within groups of 8 by the row (conflict-free stores), then one bulk
+      // DSMEM copy per owner into its receive buffer (source block r)
       mbar_wait(&bars->plfull, ph);
       tc_fence_after();
       if (tid == 0) WTS(2);
@@ -475,16 +497,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c16 * 16 < half) tmem_ld16_nowait(tmem + lane_base + kColL + p * half + c16 * 16, pl + c16 * 16);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_wait(&bars->fwd_done[t & 1], (uint32_t)(t >> 1) & 1u);
-        if (tid == 0) WTS(3);
-        const uint32_t o = (uint32_t)(s / RP);
-        const uint32_t da = mapa_shared(smem_u32(sRecv + ((r * RP + s % RP) * C + p * half)), o);
-        const uint32_t bar = mapa_shared(smem_u32(&bars->recv_full), o);
+        const int tr = s % RP;
+        uint8_t* st = ring + (size_t)(s / RP) * RP * C * 4 + (size_t)tr * C * 4;
 #pragma unroll
         for (int c4 = 0; c4 < 16; ++c4)
-          if (c4 * 4 < half)
-            st_async_v4(da + c4 * 16, __uint_as_float(pl[4 * c4]), __uint_as_float(pl[4 * c4 + 1]),
-                      __uint_as_float(pl[4 * c4 + 2]), __uint_as_float(pl[4 * c4 + 3]), bar);
+          if (c4 * 4 < half) {
+            const int ch = p * (half / 4) + c4;
+            *reinterpret_cast<uint4*>(st + ((ch & ~7) | ((ch & 7) ^ (tr & 7))) * 16) =
+                make_uint4(pl[4 * c4], pl[4 * c4 + 1], pl[4 * c4 + 2], pl[4 * c4 + 3]);
+          }
+        fence_async_smem();  // generic stores -> the bulk copies' reads
+      }
+      bar_epi();
+      if (warp == 0) {
+        if (lane < cs) {
+          mbar_wait(&bars->fwd_done[t & 1], (uint32_t)(t >> 1) & 1u);
+          if (lane == 0) WTS(3);
+          const uint32_t blk = (uint32_t)RP * C * 4u;
+          bulk_s2c(mapa_shared(smem_u32(sRecv) + (uint32_t)r * blk, (uint32_t)lane),
+                   smem_u32(ring) + (uint32_t)lane * blk, blk,
+                   mapa_shared(smem_u32(&bars->recv_full), (uint32_t)lane));
+          bulk_commit();
+          bulk_wait_read_all();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->stage_free);
       }
 
       // --------------- owned rows: logits, softmax, dL -> every CTA --
@@ -494,9 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = r * RP + tt;
         const bool act = 4 * lane < C;
         const int c0 = act ? 4 * lane : 0;
-        float4 lg = *reinterpret_cast<const float4*>(sRecv + (size_t)tt * C + c0);
+        const int pc = ((lane & ~7) | ((lane & 7) ^ (tt & 7))) * 4;  // the staged swizzle
+        float4 lg = *reinterpret_cast<const float4*>(sRecv + (size_t)tt * C + (act ? pc : 0));
         for (int sr = 1; sr < cs; ++sr) {
-          const float4 v = *reinterpret_cast<const float4*>(sRecv + ((size_t)sr * RP + tt) * C + c0);
+          const float4 v = *reinterpret_cast<const float4*>(sRecv + ((size_t)sr * RP + tt) * C + (act ? pc : 0));
           lg = make_float4(__fadd_rn(lg.x, v.x), __fadd_rn(lg.y, v.y), __fadd_rn(lg.z, v.z),
                            __fadd_rn(lg.w, v.w));
         }
@@ -546,9 +584,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           st_async_v4(mapa_shared(smem_u32(sDb2 + r * C + 4 * tid), (uint32_t)d), acc.x, acc.y, acc.z,
                       acc.w, mapa_shared(smem_u32(&bars->dl_full), (uint32_t)d));
       }
-      // this thread's first master tile, in flight across the dL exchange
-      float mcur[32];
-      ld_master<F>(W1 + (size_t)(h0 + p * 32) * F + s, mcur);
       mbar_wait(&bars->dl_full, ph);
       if (tid == 0) WTS(6);
       if (tid < C) {  // b2 (identical in every CTA: same partials, same order)
@@ -576,35 +611,45 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       if (tid == 0) WTS(9);
       // -------------- W1 += X^T.(-lr dH): master tiles and operand rows --
-      for (int mt = 0; mt < NM; ++mt, ++nd) {
-        const int b = (int)(nd & 1u);
-        mbar_wait(&bars->dfull[b], (nd >> 1) & 1u);
+      // two tile streams: warps 0-3 (p = 0) take the even tiles (TMEM buffer
+      // 0), warps 4-7 the odd ones (buffer 1), each thread both 32-column
+      // halves of its feature -- one group's TMEM reads overlap the other's
+      // master round trip
+      for (int mt = p; mt < NM; mt += 2, ++nd) {
+        const int f = mt * 128 + s;
+        float m0[32], m1[32];
+        ld_master<F>(W1 + (size_t)h0 * F + f, m0);
+        mbar_wait(&bars->dfull[p], nd & 1u);
         tc_fence_after();
         if (tid == 0) WTS(10 + mt);
-        uint32_t dv[32];
-        tmem_ld32_nowait(tmem + lane_base + kColD + b * 64 + p * 32, dv);
+        uint32_t d0[32], d1[32];
+        tmem_ld32_nowait(tmem + lane_base + kColD + p * 64, d0);
+        tmem_ld32_nowait(tmem + lane_base + kColD + p * 64 + 32, d1);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(&bars->dempty[b]);
-        float mnext[32];
-        if (mt + 1 < NM) ld_master<F>(W1 + (size_t)(h0 + p * 32) * F + (mt + 1) * 128 + s, mnext);
-        float* wm = W1 + (size_t)(h0 + p * 32) * F + mt * 128 + s;
+        mbar_arrive(&bars->dempty[p]);
+        ld_master<F>(W1 + (size_t)(h0 + 32) * F + f, m1);
+        float* wm = W1 + (size_t)h0 * F + f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float w = __fadd_rn(mcur[i], __uint_as_float(dv[i]));
+          const float w = __fadd_rn(m0[i], __uint_as_float(d0[i]));
           wm[(size_t)i * F] = w;
-          dv[i] = __float_as_uint(w);
+          d0[i] = __float_as_uint(w);
         }
-        put_row32(sW1, mt * 128 + s, p, dv);
+        put_row32(sW1, f, 0, d0);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float w = __fadd_rn(m1[i], __uint_as_float(d1[i]));
+          wm[(size_t)(32 + i) * F] = w;
+          d1[i] = __float_as_uint(w);
+        }
+        put_row32(sW1, f, 1, d1);
         fence_async_smem();  // the rebuilt rows (generic stores) -> the next forward
         mbar_arrive(&bars->xready[mt]);
-        if (mt + 1 < NM) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mcur[i] = mnext[i];
-        }
       }
-      // ---------- W2 -= lr dW2 (off the critical path: the next step's
-      // logits read the image only after the end-of-step barrier) --
+      // ---------- W2 -= lr dW2, the master in TMEM (off the critical path:
+      // the next step's logits read the image only after the end-of-step
+      // barrier) --
       if (q < 2) {  // TMEM lanes 0-63 = hidden unit s of this CTA
         mbar_wait(&bars->w2full, ph);
         tc_fence_after();
@@ -613,24 +658,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c16 = 0; c16 < 4; ++c16)
           if (c16 * 16 < half) tmem_ld16_nowait(tmem + lane_base + kColW2 + p * half + c16 * 16, w + c16 * 16);
         tmem_ld_wait();
-        float4* wr = reinterpret_cast<float4*>(W2 + (size_t)(h0 + s) * C + p * half);
-        constexpr int kQ = C / 8;  // float4 of this thread's half row
-        float4 o[kQ];
+        uint32_t m[64];
 #pragma unroll
-        for (int c4 = 0; c4 < kQ; ++c4) o[c4] = wr[c4];
+        for (int c16 = 0; c16 < 4; ++c16)
+          if (c16 * 16 < half) tmem_ld16_nowait(tmem + lane_base + kColW2M + p * half + c16 * 16, m + c16 * 16);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c4 = 0; c4 < kQ; ++c4) {
-          const float4 nw = make_float4(__fmaf_rn(-lr, __uint_as_float(w[4 * c4]), o[c4].x),
-                                        __fmaf_rn(-lr, __uint_as_float(w[4 * c4 + 1]), o[c4].y),
-                                        __fmaf_rn(-lr, __uint_as_float(w[4 * c4 + 2]), o[c4].z),
-                                        __fmaf_rn(-lr, __uint_as_float(w[4 * c4 + 3]), o[c4].w));
-          wr[c4] = nw;
-          const int c = p * half + 4 * c4;
-          *reinterpret_cast<uint16_t*>(sW2i + w2img_off(c, s)) = (uint16_t)(pack_bf16x2(nw.x, 0.0f) & 0xFFFFu);
-          *reinterpret_cast<uint16_t*>(sW2i + w2img_off(c + 1, s)) = (uint16_t)(pack_bf16x2(nw.y, 0.0f) & 0xFFFFu);
-          *reinterpret_cast<uint16_t*>(sW2i + w2img_off(c + 2, s)) = (uint16_t)(pack_bf16x2(nw.z, 0.0f) & 0xFFFFu);
-          *reinterpret_cast<uint16_t*>(sW2i + w2img_off(c + 3, s)) = (uint16_t)(pack_bf16x2(nw.w, 0.0f) & 0xFFFFu);
+        for (int c = 0; c < 64; ++c) {
+          if (c >= half) break;
+          const float nw = __fmaf_rn(-lr, __uint_as_float(w[c]), __uint_as_float(m[c]));
+          m[c] = __float_as_uint(nw);
+          *reinterpret_cast<uint16_t*>(sW2i + w2img_off(p * half + c, s)) =
+              (uint16_t)(pack_bf16x2(nw, 0.0f) & 0xFFFFu);
         }
+#pragma unroll
+        for (int c16 = 0; c16 < 4; ++c16)
+          if (c16 * 16 < half) tmem_st16(tmem + lane_base + kColW2M + p * half + c16 * 16, m + c16 * 16);
+        tmem_st_wait();
       }
 
       if (q < 2 && p == 0) {  // b1 row s, already scaled by -lr
@@ -651,6 +695,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ------------------------------------------------------------ write back --
   tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  if (tid < kEpi && q < 2) {  // the W2 master slice
+    float* w = W2 + (size_t)(h0 + s) * C + p * (C / 2);
+    for (int c16 = 0; c16 < C / 32; ++c16) {
+      uint32_t v[16];
+      tmem_ld16_nowait(tmem + lane_base + kColW2M + p * (C / 2) + c16 * 16, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[c16 * 16 + i] = __uint_as_float(v[i]);
+    }
+  }
   if (tid < kHS) b1[h0 + tid] = sB1[tid];
   if (r == 0 && tid < C) b2[tid] = sB2[tid];
   if (r == 0 && tid == 0) {
