@@ -86,6 +86,9 @@ struct WideArgs {
   float* losses;
   int loss_T, loss_t;
   int trace;  // ECCO_WIDE_TRACE: clock64 stamps of CTA 0, steps 0-3 (g_wide_trace)
+  int st_exchange;  // ECCO_WIDE_ST_ASYNC: partial logits by per-thread st.async
+                    // instead of bulk copies (compute-sanitizer memcheck does
+                    // not model shared::cta -> shared::cluster bulk copies)
 };
 
 // [step][point] cycles since the step start of CTA 0 (tools/wide_trace.md)
@@ -498,30 +501,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         tc_fence_before();
         const int tr = s % RP;
-        uint8_t* st = ring + (size_t)(s / RP) * RP * C * 4 + (size_t)tr * C * 4;
-#pragma unroll
-        for (int c4 = 0; c4 < 16; ++c4)
-          if (c4 * 4 < half) {
-            const int ch = p * (half / 4) + c4;
-            *reinterpret_cast<uint4*>(st + ((ch & ~7) | ((ch & 7) ^ (tr & 7))) * 16) =
-                make_uint4(pl[4 * c4], pl[4 * c4 + 1], pl[4 * c4 + 2], pl[4 * c4 + 3]);
-          }
-        fence_async_smem();  // generic stores -> the bulk copies' reads
-      }
-      bar_epi();
-      if (warp == 0) {
-        if (lane < cs) {
+        if (a.st_exchange) {  // straight into the owner's receive buffer, same layout
           mbar_wait(&bars->fwd_done[t & 1], (uint32_t)(t >> 1) & 1u);
-          if (lane == 0) WTS(3);
-          const uint32_t blk = (uint32_t)RP * C * 4u;
-          bulk_s2c(mapa_shared(smem_u32(sRecv) + (uint32_t)r * blk, (uint32_t)lane),
-                   smem_u32(ring) + (uint32_t)lane * blk, blk,
-                   mapa_shared(smem_u32(&bars->recv_full), (uint32_t)lane));
-          bulk_commit();
-          bulk_wait_read_all();
+          const uint32_t o = (uint32_t)(s / RP);
+          const uint32_t row_a = mapa_shared(smem_u32(sRecv + ((size_t)r * RP + tr) * C), o);
+          const uint32_t bar = mapa_shared(smem_u32(&bars->recv_full), o);
+#pragma unroll
+          for (int c4 = 0; c4 < 16; ++c4)
+            if (c4 * 4 < half) {
+              const int ch = p * (half / 4) + c4;
+              st_async_v4(row_a + ((ch & ~7) | ((ch & 7) ^ (tr & 7))) * 16, __uint_as_float(pl[4 * c4]),
+                          __uint_as_float(pl[4 * c4 + 1]), __uint_as_float(pl[4 * c4 + 2]),
+                          __uint_as_float(pl[4 * c4 + 3]), bar);
+            }
+        } else {
+          uint8_t* st = ring + (size_t)(s / RP) * RP * C * 4 + (size_t)tr * C * 4;
+#pragma unroll
+          for (int c4 = 0; c4 < 16; ++c4)
+            if (c4 * 4 < half) {
+              const int ch = p * (half / 4) + c4;
+              *reinterpret_cast<uint4*>(st + ((ch & ~7) | ((ch & 7) ^ (tr & 7))) * 16) =
+                  make_uint4(pl[4 * c4], pl[4 * c4 + 1], pl[4 * c4 + 2], pl[4 * c4 + 3]);
+            }
+          fence_async_smem();  // generic stores -> the bulk copies' reads
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->stage_free);
+      }
+      if (a.st_exchange) {
+        if (tid == 0) mbar_arrive(&bars->stage_free);
+      } else {
+        bar_epi();
+        if (warp == 0) {
+          if (lane < cs) {
+            mbar_wait(&bars->fwd_done[t & 1], (uint32_t)(t >> 1) & 1u);
+            if (lane == 0) WTS(3);
+            const uint32_t blk = (uint32_t)RP * C * 4u;
+            bulk_s2c(mapa_shared(smem_u32(sRecv) + (uint32_t)r * blk, (uint32_t)lane),
+                     smem_u32(ring) + (uint32_t)lane * blk, blk,
+                     mapa_shared(smem_u32(&bars->recv_full), (uint32_t)lane));
+            bulk_commit();
+            bulk_wait_read_all();
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->stage_free);
+        }
       }
 
       // --------------- owned rows: logits, softmax, dL -> every CTA --
@@ -822,6 +844,7 @@ void train_wide(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_step
   a.loss_T = c.max_depth;
   a.loss_t = loss_t;
   a.trace = getenv("ECCO_WIDE_TRACE") ? 1 : 0;
+  a.st_exchange = getenv("ECCO_WIDE_ST_ASYNC") ? 1 : 0;
   wide_attrs(c.device);
   cudaLaunchAttribute at[1];
   cudaLaunchConfig_t lc = wide_config(c, n_jobs, ctx->stream, at);

@@ -470,6 +470,26 @@ def test_wide_chain_within_tolerance(hidden):
     assert _tc_weights_error(False, True, cfg)[0] <= TC_TOL_CHAIN
 
 
+def test_wide_chain_exchange_variants_bit_identical(monkeypatch):
+    # the partial logits reach their row owner by bulk DSMEM copies (default)
+    # or per-thread st.async (ECCO_WIDE_ST_ASYNC, the compute-sanitizer
+    # memcheck build): same bytes, same summation order -> same models
+    outs = []
+    for st in (False, True):
+        if st:
+            monkeypatch.setenv("ECCO_WIDE_ST_ASYNC", "1")
+        ctx, orc, rng = setup(seed=7, math=ecco.TC_BF16, hidden_dim=1024, **WIDE)
+        ids = [1, 2]
+        ctx.seed_models(ids)
+        members, sources, fracs, batches = _jobs(rng, len(ids), 6)
+        acc = ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, 2, window=3)
+        ctx.commit(ids, [2, 2])
+        outs.append((acc, [w for j in ids for w in ctx.get_weights(j)]))
+    assert outs[0][0].tobytes() == outs[1][0].tobytes()
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert a.tobytes() == b.tobytes()
+
+
 def test_wide_chain_is_one_launch_per_micro_window():
     ctx, orc, rng = setup(seed=4, math=ecco.TC_BF16, hidden_dim=1024, **WIDE)
     ids = [1, 2, 3]
