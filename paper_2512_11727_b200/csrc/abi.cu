@@ -72,6 +72,7 @@ void free_all(ecco_ctx* c) {
   fused::free_shadow(c->sh_commit);
   fused::free_shadow(c->sh_spec);
   fused::free_shadow(c->sh_spec2);
+  fused::free_shadow(c->sh_pool);
   if (c->eval_stream) cudaStreamDestroy(c->eval_stream);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_chain[i]) cudaEventDestroy(c->ev_chain[i]);

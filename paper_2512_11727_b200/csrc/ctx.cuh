@@ -238,6 +238,7 @@ struct ecco_ctx {
   // translate to the API layout W1[F][H]
   bool w1_t = false;
   Shadow sh_commit, sh_spec, sh_spec2;  // (sh_spec / sh_spec2: alternate micro-windows)
+  Shadow sh_pool;  // serial chains: the images of one job's max_depth snapshots
   cudaStream_t eval_stream = nullptr;    // member evaluations of a chain, beside its training
   cudaEvent_t ev_chain[2] = {nullptr, nullptr}, ev_eval[2] = {nullptr, nullptr};
   std::vector<char> sh_dirty;
@@ -246,7 +247,7 @@ struct ecco_ctx {
     if (slot >= 0 && slot < (int)sh_dirty.size()) sh_dirty[slot] = 1;
   }
 
-  DevBuf scratch[22];  // 19-20: the general-path evaluation plan of a chain (learned_kernels.cu)
+  DevBuf scratch[26];  // 19-20: the general-path evaluation plan of a chain, 21-25: a serial chain's (learned_kernels.cu)
   // 0-10: general training path (learned_kernels.cu; 0-1 also the fused chains' sampled rows),
   // 11: the wide chain's gathered minibatch rows (wide_kernels.cu)
   DevBuf train_scratch[12];
@@ -335,7 +336,8 @@ void eval_pairs(ecco_ctx* ctx, int n, const double* d_scenes_in, const int* d_ca
 
 namespace fused {
 bool supported(const ecco_ctx* ctx);
-void init_shadow(ecco_ctx* ctx, Shadow& sh);
+// Evaluation images for `images` model slots (cfg.max_jobs when 0).
+void init_shadow(ecco_ctx* ctx, Shadow& sh, size_t images = 0);
 void free_shadow(Shadow& sh);
 // bf16 images of the models in `slots` (W1^T only for `w1t_slots` when
 // given: the fused SGD chain writes the W1^T image of every model it trained)
@@ -388,7 +390,7 @@ void chain_rows(ecco_ctx* ctx, int n_jobs, const int* d_job_ids, const int* d_st
 void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,
                  const int* d_steps, const int* h_steps, int micro, int n_micro,
                  const float* wsrc, size_t wsrc_stride, float* wbase, size_t wstride,
-                 int loss_t);
+                 int loss_t, int n_launch = 1, size_t wmicro = 0);
 }  // namespace fused
 
 // Sampled-row ingest (stage_kernels.cu), on the given stream.

@@ -915,9 +915,9 @@ void shadow_w1t(ecco_ctx* ctx, const int* d_slots, int n, const float* wbase, si
   ECCO_LAUNCHED(ctx);
 }
 
-void init_shadow(ecco_ctx* ctx, Shadow& sh) {
+void init_shadow(ecco_ctx* ctx, Shadow& sh, size_t images) {
   const ecco_config& g = ctx->cfg;
-  const size_t slots = g.max_jobs;
+  const size_t slots = images ? images : (size_t)g.max_jobs;
   ECCO_CUDA(cudaMalloc((void**)&sh.w1t, slots * g.hidden_dim * g.feat_dim * 2));
   ECCO_CUDA(cudaMalloc((void**)&sh.w2t, slots * img_bytes(g)));
   sh.map_w = new CUtensorMap(make_map(sh.w1t, slots * g.hidden_dim, g.feat_dim, kHalf));

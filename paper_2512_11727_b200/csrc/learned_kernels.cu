@@ -624,6 +624,26 @@ __global__ void k_l_job_mean(LDims g, int n_jobs, const int* mem_off, const int*
   out[(size_t)j * stride + col] = nm == 0 ? floor_acc : __ddiv_rn(sum, (double)nm);
 }
 
+// Serial chains (one job, `depth` snapshots evaluated in one pass): the
+// (snapshot, member) pair list -- pair u * n_mem + m is member m under
+// snapshot u (virtual slot u of the snapshot pool) -- and each snapshot's
+// member mean, in k_l_job_mean's order.
+__global__ void k_l_serial_pairs(int n_mem, int depth, const int* mem_cam, int* pair_slot,
+                                 int* pair_cam) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_mem * depth) return;
+  pair_slot[i] = i / n_mem;
+  pair_cam[i] = mem_cam[i % n_mem];
+}
+__global__ void k_l_serial_mean(LDims g, int n_mem, int depth, const int* counts, double* out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= depth) return;
+  double sum = 0.0;
+  for (int m = 0; m < n_mem; ++m)
+    sum = __dadd_rn(sum, __ddiv_rn((double)counts[(size_t)u * n_mem + m], (double)g.S));
+  out[1 + u] = __ddiv_rn(sum, (double)n_mem);
+}
+
 // Warp-reduced argmax / threshold of group_request (grouping.cpp:30-39) per
 // probe row.  The matrix is n_blocks column blocks of gb columns, block b
 // stored row-major at M + b*n*gb (n_blocks = 1: plain n x gb row-major; the
@@ -701,6 +721,7 @@ void init(ecco_ctx* ctx) {
     fused::init_shadow(ctx, ctx->sh_spec);
     if (fused::train_supported(ctx)) {  // chains evaluate on a side stream, alternating shadows
       fused::init_shadow(ctx, ctx->sh_spec2);
+      fused::init_shadow(ctx, ctx->sh_pool, (size_t)ctx->cfg.max_depth);
       ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->eval_stream, cudaStreamNonBlocking));
       for (int i = 0; i < 2; ++i) {
         ECCO_CUDA(cudaEventCreateWithFlags(&ctx->ev_chain[i], cudaEventDisableTiming));
@@ -1221,6 +1242,41 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   // runs beside the chain of state t+1 (the two alternate between the two
   // speculative shadows: chain t+2 rewrites the shadow eval t reads, so it
   // waits for it).
+  // Serial mode -- one job on the fused chain with >= 2 micro-windows (the
+  // exact replay's extension chains): every micro-window in ONE launch from
+  // on-chip state (no per-micro-window setup, write-back of the starting
+  // model or launch gap), then the member evaluations of all `depth`
+  // snapshots as one batched pass over the snapshot pool's images.
+  // Bit-identical to the per-micro-window launches (same arithmetic; the
+  // masters round-trip exactly), tests/test_gpu_learned.py.
+  const bool serial = ctx->fused_train && fused::train_supported(ctx) && n_jobs == 1 &&
+                      depth >= 2 && n_mem > 0 && ctx->fused_eval && ctx->sh_pool.w1t &&
+                      h_steps[0] > 0 && !getenv("ECCO_NO_SERIAL_CHAIN");
+  if (serial) {
+    fused::chain_rows(ctx, n_jobs, d_job_ids, d_steps, h_steps, d_src_off, d_src_cam, d_src_frac,
+                      d_micro_base, depth, window);
+    float* sbase = ctx->d_wspec + (size_t)slots[0] * spec_stride;  // snapshot t at sbase + (t-1) np
+    fused::train_chain(ctx, nullptr, 1, d_slots, d_steps, h_steps, 0, depth, ctx->d_w, np,
+                       ctx->d_wspec, spec_stride, 0, depth, np);
+    const int n_pairs = n_mem * depth;
+    int* d_vslot = (int*)ctx->scratch[21].get(sizeof(int) * n_pairs);
+    int* d_vcam = (int*)ctx->scratch[22].get(sizeof(int) * n_pairs);
+    int* d_vcnt = (int*)ctx->scratch[23].get(sizeof(int) * n_pairs);
+    k_l_serial_pairs<<<nblk(n_pairs, 256), 256, 0, ctx->stream>>>(n_mem, depth, d_mem_cam, d_vslot,
+                                                                  d_vcam);
+    ECCO_LAUNCHED(ctx);
+    std::vector<int> hv(n_pairs), us(depth);
+    for (int i = 0; i < n_pairs; ++i) hv[i] = i / n_mem;
+    for (int u = 0; u < depth; ++u) us[u] = u;
+    const int* d_us = ctx->upload(24, us.data(), us.size());
+    fused::refresh_shadow_dev(ctx, ctx->sh_pool, sbase, np, d_us, depth, d_us, depth);
+    const PairsPlan vplan = plan_pairs(ctx, n_pairs, hv.data(), 25, 20);
+    pair_counts_planned(ctx, ctx->sh_pool, sbase, np, vplan, d_vslot, d_vcam, d_vcnt);
+    k_l_serial_mean<<<nblk(depth, 64), 64, 0, ctx->stream>>>(g, n_mem, depth, d_vcnt, d_out);
+    ECCO_LAUNCHED(ctx);
+    ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+    return;
+  }
   const bool side = ctx->fused_train && ctx->eval_stream && n_mem > 0 && (ctx->fused_eval || gen_plan.ok);
   if (ctx->fused_train)
     fused::chain_rows(ctx, n_jobs, d_job_ids, d_steps, h_steps, d_src_off, d_src_cam, d_src_frac,

@@ -68,6 +68,11 @@ struct ChainArgs {
   uint16_t* w1t;  // bf16 W1^T evaluation shadow [slot][H][F], written at the end
   float* losses;  // losses[slot * loss_T + loss_t] = mean loss of the last step
   int loss_T, loss_t;
+  // Serial mode (n_micro_launch > 1, one job): the launch trains that many
+  // consecutive micro-windows from on-chip state, leaving micro-window u's
+  // model at wbase + u * wmicro (and its loss at loss_t + u)
+  int n_micro_launch;
+  size_t wmicro;
 };
 
 // Every (job, step, row) draw of the micro-window, ahead of the chain
@@ -319,10 +324,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     (kc | kk) != 0);
   };
 
-  for (int step = 0; step < nsteps; ++step) {
+  // global step index over the launch's micro-windows (serial mode: the
+  // rows of one job's consecutive micro-windows are consecutive row steps)
+  const int total = nsteps * a.n_micro_launch;
+  for (int step = 0; step < total; ++step) {
     const int cur = step & 1;
     const uint32_t ph = (uint32_t)step & 1u;
-    const bool more = step + 1 < nsteps;
+    const bool more = step + 1 < total;
+    // the last step of a micro-window that is not the launch's last: its
+    // model is written out as the rebuild reads it (serial mode)
+    const bool boundary = more && (step + 1) % nsteps == 0;
+    const size_t snap = (size_t)(step / nsteps) * a.wmicro;
     if (tid == 0) {  // this step's incoming DSMEM bytes
       mbar_expect_tx(recv_full, recv_bytes);
       mbar_expect_tx(dl_full, dl_bytes);
@@ -568,10 +580,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32_nowait(tmem + lane_base + mt * 64, w0);
           tmem_ld_wait();
           put_row32(sSC, mt * 128 + s, 0, w0);
+          if (boundary) {
+            float* wo = W1 + snap + (size_t)h0 * F + mt * 128 + s;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) wo[(size_t)i * F] = __uint_as_float(w0[i]);
+          }
         } else {
           tmem_ld_wait();
         }
         put_row32(sSC, mt * 128 + s, p, wr);
+        if (boundary) {
+          float* wo = W1 + snap + (size_t)(h0 + p * 32) * F + mt * 128 + s;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) wo[(size_t)i * F] = __uint_as_float(wr[i]);
+        }
         if (more) {
           fence_async_smem();  // the rebuilt rows (generic stores) -> the forward MMA
           mbar_arrive(xready + mt);
@@ -608,9 +630,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (boundary) {  // the rest of micro-window step / nsteps's model and its loss
+      for (int i = tid; i < kHS * kC / 4; i += kThreads)
+        reinterpret_cast<float4*>(W2 + snap + (size_t)h0 * kC)[i] = reinterpret_cast<const float4*>(sW2)[i];
+      if (tid < kHS) b1[snap + h0 + tid] = sB1[tid];
+      if (r == 0 && tid < kC) b2[snap + tid] = sB2[tid];
+      if (r == 0 && tid == 0) {
+        double acc = 0.0;
+        for (int i = 0; i < kB; ++i) acc += sLoss[i];
+        a.losses[(size_t)slot * a.loss_T + a.loss_t + step / nsteps] = (float)(acc / kB);
+      }
+    }
   }
 
   // ------------------------------------------------------------ write back --
+  // (the launch's last micro-window: snapshot n_micro_launch - 1)
+  const size_t last = (size_t)(a.n_micro_launch - 1) * a.wmicro;
+  W1 += last;
+  b1 += last;
+  W2 += last;
+  b2 += last;
   for (int mt = 0; mt < NM; ++mt) {
     const int f = mt * 128 + s;
     uint32_t wr[32];
@@ -631,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (r == 0 && tid == 0) {
     double acc = 0.0;
     for (int i = 0; i < kB; ++i) acc += sLoss[i];
-    a.losses[(size_t)slot * a.loss_T + a.loss_t] = (float)(acc / kB);
+    a.losses[(size_t)slot * a.loss_T + a.loss_t + a.n_micro_launch - 1] = (float)(acc / kB);
   }
   tc_fence_before();
   __syncthreads();
@@ -676,8 +715,10 @@ void chain_rows(ecco_ctx* ctx, int n_jobs, const int* d_job_ids, const int* d_st
 void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,
                  const int* d_steps, const int* h_steps, int micro, int n_micro,
                  const float* wsrc, size_t wsrc_stride, float* wbase, size_t wstride,
-                 int loss_t) {
+                 int loss_t, int n_launch, size_t wmicro) {
   if (n_jobs == 0) return;
+  ECCO_REQUIRE(n_launch == 1 || (n_jobs == 1 && train_supported(ctx) && !sh),
+               "serial chain: one job, the fused chain shape, no shadow");
   if (!train_supported(ctx)) {  // the detection-head shape: wide_kernels.cu
     train_wide(ctx, n_jobs, d_slots, d_steps, h_steps, micro, n_micro, wsrc, wsrc_stride, wbase,
                wstride, loss_t);
@@ -706,6 +747,8 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
   a.losses = ctx->d_losses;
   a.loss_T = c.max_depth;
   a.loss_t = loss_t;
+  a.n_micro_launch = n_launch;
+  a.wmicro = wmicro;
   const uint32_t smem = layout(c.feat_dim).total;
   static DeviceFlags attr;  // per device: the attribute applies to the current device
   if (!attr.done(c.device)) {  // the opt-in maximum: every supported shape fits
@@ -731,12 +774,12 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
   const double F = c.feat_dim, H = c.hidden_dim, C = c.num_classes;
   double steps = 0, live = 0;
   for (int j = 0; j < n_jobs; ++j) {
-    steps += h_steps[j];
+    steps += (double)h_steps[j] * n_launch;
     live += h_steps[j] > 0;
   }
   const double flops = steps * kB * (4.0 * F * H + 6.0 * H * C);
   const double params = F * H + H + H * C + C;
-  const double bytes = steps * kB * F * 2.0 + live * params * 8.0;
+  const double bytes = steps * kB * F * 2.0 + live * params * 4.0 * (1 + n_launch);
   // the frame table as a 2-D bf16 tensor [camera*R + frame][F]: TMA gather4
   // rows of 64 columns, 128B swizzle (the forward's X operand layout)
   const CUtensorMap map_rows =

@@ -503,6 +503,34 @@ def test_wide_chain_is_one_launch_per_micro_window():
     assert ctx.kernel_stat(ecco.KSTAT_TRAIN_HEAD)[0] == 0
 
 
+def test_serial_chain_equals_per_micro_window_launches(monkeypatch):
+    # one job's chain of micro-windows (the exact replay's extensions) runs
+    # in ONE launch from on-chip state with a batched evaluation of all its
+    # snapshots; the per-micro-window launches (ECCO_NO_SERIAL_CHAIN) give
+    # the same bytes: trajectories, losses and every granted prefix's model
+    outs = []
+    for serial in (True, False):
+        if not serial:
+            monkeypatch.setenv("ECCO_NO_SERIAL_CHAIN", "1")
+        ctx, orc, rng = setup(seed=8, math=ecco.TC_BF16, **FUSED)
+        ids = [3]
+        ctx.seed_models(ids)
+        members, sources, fracs, batches = _jobs(rng, 1, 6)
+        members[0] = [0, 1, 2, 4]  # several members: the batched evaluation spans super tiles
+        ctx.profile(True)
+        acc = ctx.train_trajectories(ids, batches, sources, fracs, members, 6.0, 4, window=3)
+        launches = ctx.kernel_stat(ecco.KSTAT_TRAIN_STEP)[0]
+        assert launches == (1 if serial else 4), launches
+        models = []
+        for grant in (2, 4):  # an intermediate snapshot and the last (the snapshots stay)
+            ctx.commit(ids, [grant])
+            models += [w.copy() for w in ctx.get_weights(3)]
+        outs.append((acc.copy(), models))
+    assert outs[0][0].tobytes() == outs[1][0].tobytes()
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert a.tobytes() == b.tobytes()
+
+
 @pytest.mark.parametrize("fused", [True, False])
 def test_tc_chain_weights_within_tolerance(fused):
     err = _tc_weights_error(False, fused)[0]
