@@ -1104,7 +1104,10 @@ def main():
     if args.config == "c5":
         DIMS.update(DET_DIMS)
         MATRIX = False
-        MAX_DEPTH = 8  # 4.2 MB of parameters per snapshot
+        # 4.4 MB of parameters per snapshot: 500 groups x 32 snapshots = 70 GB
+        # of HBM (of 180), so the least accurate group's ~500 serial
+        # micro-windows take ~16 extension calls (each one launch)
+        MAX_DEPTH = 32
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
         run_reference(args, rank)

@@ -377,7 +377,7 @@ bool wide_supported(const ecco_ctx* ctx);
 void wide_gather(ecco_ctx* ctx, int n_jobs, const int* d_steps, int max_steps, int n_micro);
 void train_wide(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_steps,
                 const int* h_steps, int micro, int n_micro, const float* wsrc, size_t wsrc_stride,
-                float* wbase, size_t wstride, int loss_t);
+                float* wbase, size_t wstride, int loss_t, int n_launch = 1, size_t wmicro = 0);
 // Fused SGD chain (train_kernels.cu): every job's steps[j] SGD steps of one
 // micro-window in ONE launch, one thread-block cluster per job with the fp32
 // masters resident in TMEM, starting from the models at wsrc and leaving them

@@ -844,7 +844,8 @@ struct GeneralPlan {
   const int* d_us = nullptr;
 };
 
-static GeneralPlan plan_general(ecco_ctx* ctx, int n_pairs, const int* h_slot) {
+static GeneralPlan plan_general(ecco_ctx* ctx, int n_pairs, const int* h_slot, int tiles_buf = 19,
+                                int us_buf = 20) {
   const LDims g = dims(ctx);
   GeneralPlan pl;
   const int chunk = std::max(1, (int)std::min<size_t>(n_pairs, (size_t)(256u << 20) / ((size_t)g.S * g.H * 4)));
@@ -862,8 +863,8 @@ static GeneralPlan plan_general(ecco_ctx* ctx, int n_pairs, const int* h_slot) {
   std::vector<int> us(hslot);
   std::sort(us.begin(), us.end());
   us.erase(std::unique(us.begin(), us.end()), us.end());
-  pl.d_tiles = ctx->upload(19, tiles.data(), tiles.size());
-  pl.d_us = ctx->upload(20, us.data(), us.size());
+  pl.d_tiles = ctx->upload(tiles_buf, tiles.data(), tiles.size());
+  pl.d_us = ctx->upload(us_buf, us.data(), us.size());
   pl.n_tiles = (int)tiles.size();
   pl.n_us = (int)us.size();
   pl.n_pairs = n_pairs;
@@ -884,10 +885,12 @@ static void pair_counts_general_planned(ecco_ctx* ctx, const GeneralPlan& pl, co
   k_l_pair_rows<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, d_pair_slot, d_pair_cam, row_off,
                                                            blk_slot);
   ECCO_LAUNCHED(ctx);
-  uint16_t* w1t = (uint16_t*)ctx->train_scratch[9].get((size_t)ctx->cfg.max_jobs * g.H * g.F * 2);
+  // (slots index job models, or the snapshots of a serial chain)
+  const size_t n_img = (size_t)std::max(ctx->cfg.max_jobs, ctx->cfg.max_depth);
+  uint16_t* w1t = (uint16_t*)ctx->train_scratch[9].get(n_img * g.H * g.F * 2);
   fused::shadow_w1t(ctx, pl.d_us, pl.n_us, wbase, wstride, w1t);
-  tc::fwd_hidden_bf16(ctx, ctx->d_eval, row_off, pl.d_tiles, pl.n_tiles, nullptr, 0, w1t,
-                      (size_t)ctx->cfg.max_jobs, wbase, wstride, Z, (double)rows);
+  tc::fwd_hidden_bf16(ctx, ctx->d_eval, row_off, pl.d_tiles, pl.n_tiles, nullptr, 0, w1t, n_img,
+                      wbase, wstride, Z, (double)rows);
   ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
              (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
                  g, rows, blk_slot, Gate{nullptr, 0, 1}, wbase, wstride, Z, L)));
@@ -1249,9 +1252,12 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   // snapshots as one batched pass over the snapshot pool's images.
   // Bit-identical to the per-micro-window launches (same arithmetic; the
   // masters round-trip exactly), tests/test_gpu_learned.py.
-  const bool serial = ctx->fused_train && fused::train_supported(ctx) && n_jobs == 1 &&
-                      depth >= 2 && n_mem > 0 && ctx->fused_eval && ctx->sh_pool.w1t &&
-                      h_steps[0] > 0 && !getenv("ECCO_NO_SERIAL_CHAIN");
+  // (wide chains: the planned general evaluation of all snapshots)
+  const bool wide = ctx->fused_train && !fused::train_supported(ctx);
+  const bool serial = ctx->fused_train && n_jobs == 1 && depth >= 2 && n_mem > 0 &&
+                      h_steps[0] > 0 && !getenv("ECCO_NO_SERIAL_CHAIN") &&
+                      (wide ? gen_plan.ok && (size_t)n_mem * depth * g.S * g.H * 4 <= (256u << 20)
+                            : ctx->fused_eval && ctx->sh_pool.w1t != nullptr);
   if (serial) {
     fused::chain_rows(ctx, n_jobs, d_job_ids, d_steps, h_steps, d_src_off, d_src_cam, d_src_frac,
                       d_micro_base, depth, window);
@@ -1268,10 +1274,16 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     std::vector<int> hv(n_pairs), us(depth);
     for (int i = 0; i < n_pairs; ++i) hv[i] = i / n_mem;
     for (int u = 0; u < depth; ++u) us[u] = u;
-    const int* d_us = ctx->upload(24, us.data(), us.size());
-    fused::refresh_shadow_dev(ctx, ctx->sh_pool, sbase, np, d_us, depth, d_us, depth);
-    const PairsPlan vplan = plan_pairs(ctx, n_pairs, hv.data(), 25, 20);
-    pair_counts_planned(ctx, ctx->sh_pool, sbase, np, vplan, d_vslot, d_vcam, d_vcnt);
+    if (wide) {
+      const GeneralPlan vplan = plan_general(ctx, n_pairs, hv.data(), 24, 25);
+      ECCO_REQUIRE(vplan.ok, "serial wide chain: evaluation plan");
+      pair_counts_general_planned(ctx, vplan, sbase, np, d_vslot, d_vcam, d_vcnt);
+    } else {
+      const int* d_us = ctx->upload(24, us.data(), us.size());
+      fused::refresh_shadow_dev(ctx, ctx->sh_pool, sbase, np, d_us, depth, d_us, depth);
+      const PairsPlan vplan = plan_pairs(ctx, n_pairs, hv.data(), 25, 20);
+      pair_counts_planned(ctx, ctx->sh_pool, sbase, np, vplan, d_vslot, d_vcam, d_vcnt);
+    }
     k_l_serial_mean<<<nblk(depth, 64), 64, 0, ctx->stream>>>(g, n_mem, depth, d_vcnt, d_out);
     ECCO_LAUNCHED(ctx);
     ECCO_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -717,11 +717,10 @@ void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots
                  const float* wsrc, size_t wsrc_stride, float* wbase, size_t wstride,
                  int loss_t, int n_launch, size_t wmicro) {
   if (n_jobs == 0) return;
-  ECCO_REQUIRE(n_launch == 1 || (n_jobs == 1 && train_supported(ctx) && !sh),
-               "serial chain: one job, the fused chain shape, no shadow");
+  ECCO_REQUIRE(n_launch == 1 || (n_jobs == 1 && !sh), "serial chain: one job, no shadow");
   if (!train_supported(ctx)) {  // the detection-head shape: wide_kernels.cu
     train_wide(ctx, n_jobs, d_slots, d_steps, h_steps, micro, n_micro, wsrc, wsrc_stride, wbase,
-               wstride, loss_t);
+               wstride, loss_t, n_launch, wmicro);
     return;
   }
   const ecco_config& c = ctx->cfg;

@@ -86,6 +86,10 @@ struct WideArgs {
   float* losses;
   int loss_T, loss_t;
   int trace;  // ECCO_WIDE_TRACE: clock64 stamps of CTA 0, steps 0-3 (g_wide_trace)
+  // Serial mode (n_micro_launch > 1, one job): the launch trains that many
+  // consecutive micro-windows, micro-window u's model at wbase + u * wmicro
+  int n_micro_launch;
+  size_t wmicro;
   int st_exchange;  // ECCO_WIDE_ST_ASYNC: partial logits by per-thread st.async
                     // instead of bulk copies (compute-sanitizer memcheck does
                     // not model shared::cta -> shared::cluster bulk copies)
@@ -209,7 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cs = H / kHS;
   const int j = blockIdx.x / cs;
   const int r = (int)cluster_ctarank();
-  const int nsteps = a.steps[j];
+  const int nsteps = a.steps[j];  // per micro-window
+  const int total = nsteps * a.n_micro_launch;
   const int slot = a.slots[j];
   const float* src = a.wsrc + (size_t)slot * a.wsrc_stride;
   float* dst = a.wbase + (size_t)slot * a.wstride;
@@ -277,11 +282,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(sTmem, 512);
-  if (src != dst) {  // the starting W1 slice -> the snapshot trained in place
-    const float4* s4 = reinterpret_cast<const float4*>(src + (size_t)h0 * F);
-    float4* d4 = reinterpret_cast<float4*>(W1 + (size_t)h0 * F);
-    for (int i = tid; i < kHS * F / 4; i += kThreads) d4[i] = s4[i];
-  }
   if (tid < kHS) sB1[tid] = sb1[h0 + tid];
   if (tid < C) sB2[tid] = sb2[tid];
   for (int i = tid; i < kB * 32 / 16; i += kThreads)
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid < kEpi) {
     for (int mt = 0; mt < NM; ++mt) {  // bf16 W1 operand from the master slice
       float m[32];
-      ld_master<F>(W1 + (size_t)(h0 + p * 32) * F + mt * 128 + s, m);
+      ld_master<F>(src + (size_t)(h0 + p * 32) * F + mt * 128 + s, m);
       uint32_t w[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(m[i]);
@@ -329,6 +329,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   cluster_sync();  // every CTA of the cluster is running before any DSMEM traffic
   tc_fence_after();
+  // the rest of micro-window u's model (the W2 master slice from TMEM, b1,
+  // b2) and its loss -> snapshot u (epilogue threads, after the step)
+  auto write_rest = [&](int u) {
+    const size_t o = (size_t)u * a.wmicro;
+    if (q < 2) {
+      float* w = W2 + o + (size_t)(h0 + s) * C + p * (C / 2);
+      for (int c16 = 0; c16 < C / 32; ++c16) {
+        uint32_t v[16];
+        tmem_ld16_nowait(tmem + lane_base + kColW2M + p * (C / 2) + c16 * 16, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) w[c16 * 16 + i] = __uint_as_float(v[i]);
+      }
+    }
+    if (tid < kHS) b1[o + h0 + tid] = sB1[tid];
+    if (r == 0 && tid < C) b2[o + tid] = sB2[tid];
+    if (r == 0 && tid == 0) {
+      double acc = 0.0;
+      for (int i = 0; i < kB; ++i) acc += sLoss[i];
+      a.losses[(size_t)slot * a.loss_T + a.loss_t + u] = (float)(acc / kB);
+    }
+  };
   const uint32_t ring_a = smem_u32(ring), w1_a = smem_u32(sW1), w2i_a = smem_u32(sW2i);
   const uint32_t r_a = smem_u32(sR), dl_a = smem_u32(sDL), dh_a = smem_u32(sDH);
 
@@ -337,9 +359,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // per step: the forward's 128-feature slot pairs, then dW1's; each slot
     // is two 64-feature boxes of the step's 128 gathered rows (k_wide_gather)
     uint32_t k = 0;
-    for (int t = 0; t < nsteps; ++t) {
+    for (int t = 0; t < total; ++t) {
       const int row0 = (int)(((size_t)j * a.rows_T + a.row_step0 + t) * kB);
-      if (lane == 0 && t + 1 < nsteps && r < F / 64)  // this CTA's box of the next step -> L2
+      if (lane == 0 && t + 1 < total && r < F / 64)  // this CTA's box of the next step -> L2
         tma_prefetch_2d(&map_x, r * 64, row0 + kB);
       for (int pass = 0; pass < 2; ++pass)
         for (int mt = 0; mt < NM; ++mt, ++k) {
@@ -368,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t idg = idesc_major(128, kHS, kFmtBF16, 1, 1);  // X^T . dH
     const uint32_t idb = idesc_major(128, 16, kFmtBF16, 1, 1);   // dH^T . 1 (rows 64+ alias)
     uint32_t k = 0, nd = 0;
-    for (int t = 0; t < nsteps; ++t) {
+    for (int t = 0; t < total; ++t) {
       const uint32_t ph = (uint32_t)t & 1u;
       for (int mt = 0; mt < NM; ++mt, ++k) {  // Z = X . W1
         const int sl = (int)(k & 1u);
@@ -448,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --------------------------------------------------------- epilogue --
     const int half = C / 2;  // partial-logit / dW2 columns per column half
     uint32_t nd = 0;
-    for (int t = 0; t < nsteps; ++t) {
+    for (int t = 0; t < total; ++t) {
       const uint32_t ph = (uint32_t)t & 1u;
       if (a.trace && blockIdx.x == 0 && t < 4 && tid == 0) g_wide_trace[t * 32 + 31] = clock64();
       if (tid == 0) {  // this step's incoming DSMEM bytes
@@ -637,10 +659,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // 0), warps 4-7 the odd ones (buffer 1), each thread both 32-column
       // halves of its feature -- one group's TMEM reads overlap the other's
       // master round trip
+      // the master is read-modify-written in the snapshot: micro-window u's
+      // first step reads the model it starts from (the source model, or
+      // snapshot u-1 in serial mode) and writes snapshot u -- the copy
+      // rides on the update
+      const int u = t / nsteps;
+      float* W1w = W1 + (size_t)u * a.wmicro;
+      const float* W1r = t % nsteps ? W1w : u == 0 ? src : W1w - a.wmicro;
       for (int mt = p; mt < NM; mt += 2, ++nd) {
         const int f = mt * 128 + s;
         float m0[32], m1[32];
-        ld_master<F>(W1 + (size_t)h0 * F + f, m0);
+        ld_master<F>(W1r + (size_t)h0 * F + f, m0);
         mbar_wait(&bars->dfull[p], nd & 1u);
         tc_fence_after();
         if (tid == 0) WTS(10 + mt);
@@ -650,8 +679,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars->dempty[p]);
-        ld_master<F>(W1 + (size_t)(h0 + 32) * F + f, m1);
-        float* wm = W1 + (size_t)h0 * F + f;
+        ld_master<F>(W1r + (size_t)(h0 + 32) * F + f, m1);
+        float* wm = W1w + (size_t)h0 * F + f;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const float w = __fadd_rn(m0[i], __uint_as_float(d0[i]));
@@ -711,6 +740,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       if (tid == 0) WTS(18);
       bar_epi();
+      if ((t + 1) % nsteps == 0 && t + 1 < total)  // serial mode: micro-window u is done
+        write_rest(u);
     }
   }
 
@@ -718,23 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (tid < kEpi && q < 2) {  // the W2 master slice
-    float* w = W2 + (size_t)(h0 + s) * C + p * (C / 2);
-    for (int c16 = 0; c16 < C / 32; ++c16) {
-      uint32_t v[16];
-      tmem_ld16_nowait(tmem + lane_base + kColW2M + p * (C / 2) + c16 * 16, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) w[c16 * 16 + i] = __uint_as_float(v[i]);
-    }
-  }
-  if (tid < kHS) b1[h0 + tid] = sB1[tid];
-  if (r == 0 && tid < C) b2[tid] = sB2[tid];
-  if (r == 0 && tid == 0) {
-    double acc = 0.0;
-    for (int i = 0; i < kB; ++i) acc += sLoss[i];
-    a.losses[(size_t)slot * a.loss_T + a.loss_t] = (float)(acc / kB);
-  }
+  if (tid < kEpi) write_rest(a.n_micro_launch - 1);
   cluster_sync();  // no CTA leaves while the cluster may still address its shared memory
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, 512);
@@ -820,7 +835,8 @@ bool wide_supported(const ecco_ctx* ctx) {
 
 void train_wide(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_steps,
                 const int* h_steps, int micro, int n_micro, const float* wsrc, size_t wsrc_stride,
-                float* wbase, size_t wstride, int loss_t) {
+                float* wbase, size_t wstride, int loss_t, int n_launch, size_t wmicro) {
+  ECCO_REQUIRE(n_launch == 1 || n_jobs == 1, "serial wide chain: one job");
   if (n_jobs == 0) return;
   const ecco_config& c = ctx->cfg;
   const LDims g{c.feat_dim, c.hidden_dim, c.num_classes, c.scene_dims, c.minibatch,
@@ -843,6 +859,8 @@ void train_wide(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_step
   a.losses = ctx->d_losses;
   a.loss_T = c.max_depth;
   a.loss_t = loss_t;
+  a.n_micro_launch = n_launch;
+  a.wmicro = wmicro;
   a.trace = getenv("ECCO_WIDE_TRACE") ? 1 : 0;
   a.st_exchange = getenv("ECCO_WIDE_ST_ASYNC") ? 1 : 0;
   wide_attrs(c.device);
@@ -851,7 +869,7 @@ void train_wide(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_step
   const double F = c.feat_dim, H = c.hidden_dim, C = c.num_classes;
   double steps = 0, live = 0;
   for (int j = 0; j < n_jobs; ++j) {
-    steps += h_steps[j];
+    steps += (double)h_steps[j] * n_launch;
     live += h_steps[j] > 0;
   }
   // algorithmic work: every live step's forward + backward; bytes: the

@@ -503,7 +503,8 @@ def test_wide_chain_is_one_launch_per_micro_window():
     assert ctx.kernel_stat(ecco.KSTAT_TRAIN_HEAD)[0] == 0
 
 
-def test_serial_chain_equals_per_micro_window_launches(monkeypatch):
+@pytest.mark.parametrize("shape", ["c4", "wide"])
+def test_serial_chain_equals_per_micro_window_launches(monkeypatch, shape):
     # one job's chain of micro-windows (the exact replay's extensions) runs
     # in ONE launch from on-chip state with a batched evaluation of all its
     # snapshots; the per-micro-window launches (ECCO_NO_SERIAL_CHAIN) give
@@ -512,7 +513,8 @@ def test_serial_chain_equals_per_micro_window_launches(monkeypatch):
     for serial in (True, False):
         if not serial:
             monkeypatch.setenv("ECCO_NO_SERIAL_CHAIN", "1")
-        ctx, orc, rng = setup(seed=8, math=ecco.TC_BF16, **FUSED)
+        dims = FUSED if shape == "c4" else dict(WIDE, hidden_dim=1024)
+        ctx, orc, rng = setup(seed=8, math=ecco.TC_BF16, **dims)
         ids = [3]
         ctx.seed_models(ids)
         members, sources, fracs, batches = _jobs(rng, 1, 6)
