@@ -720,6 +720,283 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc_pair(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// Wide variant (F > 512 -- the detection head of BASELINE configs[4], F = 1024,
+// H = 1024, C = 96): a 128-row X tile of F = 1024 bf16 (256 KB) does not fit
+// in shared memory, so X streams WITH the model: every pipeline stage carries
+// the tile's X chunk (128 rows x 64 features: the two 64-row camera boxes)
+// and the W1^T box of the same K chunk (128 hidden x 64 features), both
+// 128B-swizzled K-major, and one MMA step consumes both.  The X chunk is
+// re-read from L2 once per hidden half, the W1^T box once per tile.  W2^T
+// streams per hidden half (C rows x 128 K = two swizzle atoms: one
+// contiguous bulk copy of the slot's image) through two buffers, b1 | b2 per
+// entry through two more.  TMEM, warp roles, epilogue and numerics are those
+// of k_eval_fused (the logits single-buffered when 2 C > 128), so a row's
+// count does not depend on which kernel evaluated it.
+constexpr uint32_t kWideStage = kAChunk + kBoxBytes;  // 32 KB: X chunk | W1^T box
+
+struct WideBars {
+  uint64_t full[kMaxStages], empty[kMaxStages];
+  uint64_t w2_full[2], w2_empty[2];
+  uint64_t bias_full[2], bias_empty[2];
+  uint64_t z_full[2], z_empty[2], r_full[2], r_empty[2];
+  uint64_t l_full[2], l_empty[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_eval_wide(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                EvalArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int nkc = a.F / kKC;
+  const int nh = a.H / kHalf;
+  const uint32_t w2c = (uint32_t)a.C * 256u;  // W2^T of one hidden half: 2 atoms x C rows x 128 B
+  uint8_t* sS = smem;                         // stages x (X chunk | W1^T box)
+  uint8_t* sW2 = sS + a.stages * kWideStage;  // 2 x w2t_stride (W2^T hidden halves)
+  uint8_t* sBias = sW2 + 2 * a.w2t_stride;    // 2 x bias_bytes (b1 | b2)
+  WideBars* bars = reinterpret_cast<WideBars*>(sBias + 2 * a.bias_bytes);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    tma_prefetch(&map_x);
+    tma_prefetch(&map_w);
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&bars->full[s], 1);
+      mbar_init(&bars->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->w2_full[b], 1);
+      mbar_init(&bars->w2_empty[b], 1);    // the layer-2 MMA commit
+      mbar_init(&bars->bias_full[b], 1);
+      mbar_init(&bars->bias_empty[b], 4);  // the 4 logits warps (b2 read last)
+      mbar_init(&bars->z_full[b], 1);
+      mbar_init(&bars->z_empty[b], 8);
+      mbar_init(&bars->r_full[b], 8);
+      mbar_init(&bars->r_empty[b], 1);
+      mbar_init(&bars->l_full[b], 1);
+      mbar_init(&bars->l_empty[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&bars->tmem_base, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    int stage = 0;
+    uint32_t sph = 0, u = 0;
+    for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x) {
+      int xrow[2];
+      for (int h2 = 0; h2 < 2; ++h2) {
+        int b = m * 2 + h2;
+        if (b * 64 >= a.n_rows) b = 0;  // padding rows: any valid box, masked later
+        xrow[h2] = a.cams[(b * 64) / a.S] * a.S + (b * 64) % a.S;
+      }
+      for (int e = tile_ent_begin(a, m), e1 = tile_ent_end(a, m); e < e1; ++e, ++u) {
+        const int slot = a.ent_slot[e];
+        const uint8_t* img = a.w2t + (size_t)slot * a.img_bytes;
+        for (int hf = 0; hf < nh; ++hf) {
+          const uint32_t v = u * nh + hf;
+          for (int kc = 0; kc < nkc; ++kc) {
+            mbar_wait(&bars->empty[stage], sph ^ 1);
+            if (elect_one()) {
+              uint8_t* st = sS + stage * kWideStage;
+              mbar_expect_tx(&bars->full[stage], kWideStage);
+              tma_load_2d(st, &map_x, kc * kKC, xrow[0], &bars->full[stage]);
+              tma_load_2d(st + kAChunk / 2, &map_x, kc * kKC, xrow[1], &bars->full[stage]);
+              tma_load_2d(st + kAChunk, &map_w, kc * kKC, slot * a.H + hf * kHalf,
+                          &bars->full[stage]);
+            }
+            __syncwarp();
+            if (++stage == a.stages) {
+              stage = 0;
+              sph ^= 1;
+            }
+          }
+          // after the half's stages (they pace the tensor cores): the entry's
+          // biases once, then this half's W2^T (read by its layer-2 MMAs,
+          // which the MMA warp issues after the NEXT half's K loop)
+          if (hf == 0) {
+            const uint32_t bb = u & 1;
+            mbar_wait(&bars->bias_empty[bb], ((u >> 1) & 1) ^ 1);
+            if (elect_one()) {
+              mbar_expect_tx(&bars->bias_full[bb], a.bias_bytes);
+              bulk_load(sBias + bb * a.bias_bytes, img + a.w2t_bytes, a.bias_bytes,
+                        &bars->bias_full[bb]);
+            }
+            __syncwarp();
+          }
+          const uint32_t wb = v & 1;
+          mbar_wait(&bars->w2_empty[wb], ((v >> 1) & 1) ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(&bars->w2_full[wb], w2c);
+            bulk_load(sW2 + wb * a.w2t_stride, img + (size_t)hf * w2c, w2c, &bars->w2_full[wb]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer --
+    const uint32_t id1 = idesc(kTileRows, kHalf, kFmtBF16);
+    const uint32_t id2 = idesc(kTileRows, a.C, kFmtBF16);
+    const uint64_t dS0 = desc_kmajor_sw128(smem_u32(sS));
+    const uint64_t dW0 = desc_kmajor_sw128(smem_u32(sW2));
+    int stage = 0;
+    uint32_t sph = 0, u = 0;
+    long prev = -1;  // pending layer-2 for sequence index prev (v = u * nh + hf)
+    auto layer2 = [&](uint32_t w) {
+      const uint32_t uw = w / nh, hw = w % nh;
+      const uint32_t rb = w & 1, wb = w & 1, lb = uw % a.nl;
+      if (hw == 0) mbar_wait(&bars->l_empty[lb], ((uw / a.nl) & 1) ^ 1);
+      mbar_wait(&bars->w2_full[wb], (w >> 1) & 1);
+      mbar_wait(&bars->r_full[rb], (w >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint64_t dW = dW0 + ((wb * a.w2t_stride) >> 4);
+#pragma unroll
+        for (int k16 = 0; k16 < kHalf / 16; ++k16) {
+          const int kg = k16 * 16;  // K index within the hidden half
+          mma_bf16_ts(tmem + kTmemL + lb * a.C, tmem + kTmemR + rb * 64 + k16 * 8,
+                      dW + (((kg / 64) * (a.C * 128) + (kg % 64) * 2) >> 4), id2,
+                      (hw | k16) != 0);
+        }
+        mma_commit(&bars->r_empty[rb]);
+        mma_commit(&bars->w2_empty[wb]);
+        if (hw == (uint32_t)nh - 1) mma_commit(&bars->l_full[lb]);
+      }
+      __syncwarp();
+    };
+    for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x) {
+      for (int e = tile_ent_begin(a, m), e1 = tile_ent_end(a, m); e < e1; ++e, ++u) {
+        for (int hf = 0; hf < nh; ++hf) {
+          const uint32_t v = u * nh + hf, zb = v & 1;
+          mbar_wait(&bars->z_empty[zb], ((v >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t dz = tmem + kTmemZ + zb * kHalf;
+          for (int kc = 0; kc < nkc; ++kc) {
+            mbar_wait(&bars->full[stage], sph);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t da = dS0 + ((stage * kWideStage) >> 4);
+              const uint64_t db = da + (kAChunk >> 4);
+#pragma unroll
+              for (int kk = 0; kk < kKC / 16; ++kk)
+                mma_bf16_ss(dz, da + kk * 2, db + kk * 2, id1, (kc | kk) != 0);
+              mma_commit(&bars->empty[stage]);
+            }
+            __syncwarp();
+            if (++stage == a.stages) {
+              stage = 0;
+              sph ^= 1;
+            }
+          }
+          if (elect_one()) mma_commit(&bars->z_full[zb]);
+          __syncwarp();
+          if (prev >= 0) layer2((uint32_t)prev);
+          prev = v;
+        }
+      }
+    }
+    if (prev >= 0) layer2((uint32_t)prev);
+  } else {
+    // ----------------------------------------------------------- epilogue --
+    // as k_eval_fused: 8 warps, two per TMEM lane quadrant, each converting
+    // 64 of a half's 128 Z columns; the cp == 0 warps also read the logits
+    const int q = warp & 3;
+    const int cp = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t u = 0;
+    for (int m = blockIdx.x; m < a.n_tiles; m += gridDim.x) {
+      const int R = m * kTileRows + row;
+      const bool valid = R < a.n_rows;
+      const int p = valid ? R / a.S : 0;
+      const int label = valid ? a.labels[(size_t)a.cams[p] * a.S + (R % a.S)] : -1;
+      const int pslot = (valid && a.probe_slot) ? a.probe_slot[p] : -1;
+      for (int e = tile_ent_begin(a, m), e1 = tile_ent_end(a, m); e < e1; ++e, ++u) {
+        const uint32_t bb = u & 1;
+        const float* b1 = reinterpret_cast<const float*>(sBias + bb * a.bias_bytes);
+        const float* b2 = b1 + a.H;
+        mbar_wait(&bars->bias_full[bb], (u >> 1) & 1);
+        for (int hf = 0; hf < nh; ++hf) {
+          const uint32_t v = u * nh + hf, zb = v & 1;
+          const int c0 = cp * 64;
+          mbar_wait(&bars->z_full[zb], (v >> 1) & 1);
+          mbar_wait(&bars->r_empty[zb], ((v >> 1) & 1) ^ 1);
+          tc_fence_after();
+          uint32_t r[64];
+          tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0, r);
+          tmem_ld32_nowait(tmem + lane_base + kTmemZ + zb * kHalf + c0 + 32, r + 32);
+          tmem_ld_wait();
+          const float4* bv = reinterpret_cast<const float4*>(b1 + hf * kHalf + c0);
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float4 b = bv[i];
+            const float z0 = fmaxf(__uint_as_float(r[4 * i + 0]) + b.x, 0.0f);
+            const float z1 = fmaxf(__uint_as_float(r[4 * i + 1]) + b.y, 0.0f);
+            const float z2 = fmaxf(__uint_as_float(r[4 * i + 2]) + b.z, 0.0f);
+            const float z3 = fmaxf(__uint_as_float(r[4 * i + 3]) + b.w, 0.0f);
+            pk[2 * i] = pack_bf16x2(z0, z1);
+            pk[2 * i + 1] = pack_bf16x2(z2, z3);
+          }
+          tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2, pk);
+          tmem_st16(tmem + lane_base + kTmemR + zb * 64 + c0 / 2 + 16, pk + 16);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&bars->z_empty[zb]);
+            mbar_arrive(&bars->r_full[zb]);
+          }
+        }
+        if (cp != 0) continue;
+        const int slot = a.ent_slot[e];
+        const uint32_t lb = u % a.nl;
+        mbar_wait(&bars->l_full[lb], (u / a.nl) & 1);
+        tc_fence_after();
+        int best = 0;
+        float bestv = 0.0f;
+        for (int c0 = 0; c0 < a.C; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16_nowait(tmem + lane_base + kTmemL + lb * a.C + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float l = __uint_as_float(r[i]) + b2[c0 + i];
+            if ((c0 | i) == 0 || l > bestv) {
+              bestv = l;
+              best = c0 + i;
+            }
+            if (a.dbg_logits && valid)
+              a.dbg_logits[((size_t)R * a.n_ent + e) * a.C + c0 + i] = l;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&bars->l_empty[lb]);
+          mbar_arrive(&bars->bias_empty[bb]);  // b1 (all halves done) and b2 no longer read
+        }
+        const bool ok = valid && best == label && (pslot < 0 || pslot == slot);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0 && bal) {
+          const size_t idx = a.probe_slot ? (size_t)p : (size_t)p * a.ld + a.ent_col[e];
+          atomicAdd(a.counts + idx, __popc(bal));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 // ------------------------------------------------------------ shadows ------
 // W1^T (bf16, [slot][H][F]) from the fp32 masters W1 [F][H]: 32x32 transpose.
 __global__ void k_shadow_w1t(int F, int H, const int* slots, const float* wbase, size_t wstride,
@@ -827,7 +1104,7 @@ CUtensorMap make_w2_pair_map(const void* base, uint64_t slots, int H, int C, uin
 // forces the single-CTA kernel (tests run both).
 bool pair_enabled(const ecco_config& g) {
   const char* e = getenv("ECCO_EVAL_PAIR");
-  return g.num_classes == 16 && !(e && e[0] == '0');
+  return g.num_classes == 16 && g.feat_dim <= 512 && !(e && e[0] == '0');
 }
 
 // Test knob: caps the persistent grid (CTA pairs / CTAs) so a handful of
@@ -863,13 +1140,34 @@ bool pair_supported(const ecco_ctx* ctx) {
   return pair_enabled(ctx->cfg);
 }
 
-bool supported(const ecco_ctx* ctx) {
-  const ecco_config& g = ctx->cfg;
+// k_eval_fused: the 128-row X tile resident in shared memory (F <= 512)
+static bool resident_supported(const ecco_config& g) {
   return g.feat_dim % 64 == 0 && g.feat_dim <= 512 && g.hidden_dim % kHalf == 0 &&
          g.num_classes % 16 == 0 && g.num_classes <= 64 &&
          (size_t)g.num_classes * g.hidden_dim * 2 <= 16384 && g.eval_samples % 64 == 0 &&
          g.feat_dim / 64 * 16384 + 2 * ((w2t_bytes(g) + 1023) / 1024 * 1024) +
                  2 * (img_bytes(g) - w2t_bytes(g)) + sizeof(EvalBars) + 2 * 16384 <= 232448;
+}
+
+// k_eval_wide: X streamed with the model (any F % 64 == 0; logits C <= 128
+// columns of TMEM beside Z and R), at least 3 pipeline stages.  ECCO_EVAL_WIDE=0
+// leaves wide shapes on the general (unfused) path.
+static uint32_t wide_w2_stride(const ecco_config& g) {
+  return ((uint32_t)g.num_classes * 256u + 1023u) & ~1023u;
+}
+static size_t wide_fixed_smem(const ecco_config& g) {
+  return 2 * (size_t)wide_w2_stride(g) + 2 * (size_t)(img_bytes(g) - w2t_bytes(g)) +
+         sizeof(WideBars);
+}
+static bool wide_eval_supported(const ecco_config& g) {
+  const char* e = getenv("ECCO_EVAL_WIDE");
+  return !(e && e[0] == '0') && g.feat_dim % 64 == 0 && g.hidden_dim % kHalf == 0 &&
+         g.num_classes % 16 == 0 && g.num_classes <= 128 && g.eval_samples % 64 == 0 &&
+         wide_fixed_smem(g) + 3 * (size_t)kWideStage <= 232448;
+}
+
+bool supported(const ecco_ctx* ctx) {
+  return resident_supported(ctx->cfg) || wide_eval_supported(ctx->cfg);
 }
 
 
@@ -972,8 +1270,9 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
   const size_t fixed = (size_t)(a.F / kKC) * kAChunk + 2 * (size_t)a.w2t_stride +
                        2 * (size_t)a.bias_bytes + sizeof(EvalBars);
   const size_t max_smem = 232448;  // opt-in per-block limit (no static smem)
-  a.stages = (int)std::min<size_t>(kMaxStages, (max_smem - fixed) / kBoxBytes);
-  ECCO_REQUIRE(a.stages >= 2, "fused eval: shared memory too small for the pipeline");
+  const bool resident = resident_supported(g);  // else k_eval_wide (X streamed)
+  a.stages = resident ? (int)std::min<size_t>(kMaxStages, (max_smem - fixed) / kBoxBytes) : 0;
+  ECCO_REQUIRE(!resident || a.stages >= 2, "fused eval: shared memory too small for the pipeline");
   const size_t smem = fixed + (size_t)a.stages * kBoxBytes;
   static DeviceFlags attr;  // per device: the attribute applies to the current device
   if (!attr.done(g.device)) {
@@ -1015,6 +1314,25 @@ void eval_counts(ecco_ctx* ctx, const Shadow& sh, const float* wbase, size_t wst
   }
   const int grid = std::max(1, std::min({a.n_tiles, sm_count(g.device) - ctx->reserve_sms,
                                          grid_cap("ECCO_EVAL_MAX_CTAS")}));
+  if (!resident) {
+    // wide shapes: X streams with the model (k_eval_wide)
+    ECCO_REQUIRE(wide_eval_supported(g), "fused eval: unsupported shape");
+    a.w2t_stride = wide_w2_stride(g);
+    const size_t wfixed = wide_fixed_smem(g);
+    a.stages = (int)std::min<size_t>(kMaxStages, (max_smem - wfixed) / kWideStage);
+    const size_t wsmem = wfixed + (size_t)a.stages * kWideStage;
+    static DeviceFlags wattr;
+    if (!wattr.done(g.device)) {
+      ECCO_CUDA(cudaFuncSetAttribute(k_eval_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)max_smem));
+      wattr.mark(g.device);
+    }
+    ECCO_TIMED(ctx, kind, flops, bytes,
+               (k_eval_wide<<<grid, kThreads, wsmem, ctx->stream>>>(
+                   *(const CUtensorMap*)ctx->map_x, *(const CUtensorMap*)sh.map_w, a)));
+    ECCO_LAUNCHED(ctx);
+    return;
+  }
   ECCO_TIMED(ctx, kind, flops, bytes,
              (k_eval_fused<<<grid, kThreads, smem, ctx->stream>>>(*(const CUtensorMap*)ctx->map_x,
                                                                   *(const CUtensorMap*)sh.map_w, a)));

@@ -716,10 +716,13 @@ void init(ecco_ctx* ctx) {
                                                                          ctx->d_proto_p, ctx->d_proto_q);
   ECCO_LAUNCHED(ctx);
   // the tensor-core math evaluates through the fused kernel (eval_kernels.cu)
+  // (wide models -- the detection head -- through k_eval_wide, trained by
+  // the wide fused chain)
   if (ctx->cfg.math == ECCO_MATH_TC_BF16 && fused::supported(ctx)) {
+    const bool chain = fused::train_supported(ctx) || fused::wide_supported(ctx);
     fused::init_shadow(ctx, ctx->sh_commit);
     fused::init_shadow(ctx, ctx->sh_spec);
-    if (fused::train_supported(ctx)) {  // chains evaluate on a side stream, alternating shadows
+    if (chain) {  // chains evaluate on a side stream, alternating shadows
       fused::init_shadow(ctx, ctx->sh_spec2);
       fused::init_shadow(ctx, ctx->sh_pool, (size_t)ctx->cfg.max_depth);
       ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->eval_stream, cudaStreamNonBlocking));
@@ -730,8 +733,8 @@ void init(ecco_ctx* ctx) {
     }
     ctx->sh_dirty.assign(ctx->cfg.max_jobs, 1);
     ctx->fused_eval = true;
-    ctx->fused_train = fused::train_supported(ctx);
-    ctx->w1_t = ctx->fused_train;
+    ctx->fused_train = chain;
+    ctx->w1_t = chain;
   } else if (ctx->cfg.math == ECCO_MATH_TC_BF16 && fused::wide_supported(ctx)) {
     // wide models (detection head): fused chains, members evaluated on the
     // general path on a side stream beside the next micro-window's chain
@@ -1256,8 +1259,8 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   const bool wide = ctx->fused_train && !fused::train_supported(ctx);
   const bool serial = ctx->fused_train && n_jobs == 1 && depth >= 2 && n_mem > 0 &&
                       h_steps[0] > 0 && !getenv("ECCO_NO_SERIAL_CHAIN") &&
-                      (wide ? gen_plan.ok && (size_t)n_mem * depth * g.S * g.H * 4 <= (256u << 20)
-                            : ctx->fused_eval && ctx->sh_pool.w1t != nullptr);
+                      (ctx->fused_eval ? ctx->sh_pool.w1t != nullptr
+                                       : gen_plan.ok && (size_t)n_mem * depth * g.S * g.H * 4 <= (256u << 20));
   if (serial) {
     fused::chain_rows(ctx, n_jobs, d_job_ids, d_steps, h_steps, d_src_off, d_src_cam, d_src_frac,
                       d_micro_base, depth, window);
@@ -1274,7 +1277,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
     std::vector<int> hv(n_pairs), us(depth);
     for (int i = 0; i < n_pairs; ++i) hv[i] = i / n_mem;
     for (int u = 0; u < depth; ++u) us[u] = u;
-    if (wide) {
+    if (!ctx->fused_eval) {
       const GeneralPlan vplan = plan_general(ctx, n_pairs, hv.data(), 24, 25);
       ECCO_REQUIRE(vplan.ok, "serial wide chain: evaluation plan");
       pair_counts_general_planned(ctx, vplan, sbase, np, d_vslot, d_vcam, d_vcnt);
@@ -1315,7 +1318,11 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
           if (gen_plan.ok) {  // wide chains: the planned general evaluation of snapshot t
             pair_counts_general_planned(ctx, gen_plan, wt, spec_stride, d_ps, d_mem_cam, d_cnt);
           } else {
-            fused::refresh_shadow_dev(ctx, *sh, wt, spec_stride, d_slots, n_jobs, d_idle, n_idle);
+            // (the narrow chain wrote its trained jobs' W1^T images itself)
+            if (wide)
+              fused::refresh_shadow_dev(ctx, *sh, wt, spec_stride, d_slots, n_jobs, d_slots, n_jobs);
+            else
+              fused::refresh_shadow_dev(ctx, *sh, wt, spec_stride, d_slots, n_jobs, d_idle, n_idle);
             pair_counts_planned(ctx, *sh, wt, spec_stride, spec_plan, d_ps, d_mem_cam, d_cnt);
           }
           k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(
@@ -1404,8 +1411,8 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
       // the chain wrote the W1^T image of every job it trained: only idle
       // jobs' images are rebuilt (all of them on the unfused path)
       fused::refresh_shadow_dev(ctx, ctx->sh_spec, wt, spec_stride, d_slots, n_jobs,
-                                ctx->fused_train ? d_idle : d_slots,
-                                ctx->fused_train ? n_idle : n_jobs);
+                                ctx->fused_train && !wide ? d_idle : d_slots,
+                                ctx->fused_train && !wide ? n_idle : n_jobs);
       pair_counts_planned(ctx, ctx->sh_spec, wt, spec_stride, spec_plan, d_ps, d_mem_cam, d_cnt);
       k_l_job_mean<<<nblk(n_jobs, 128), 128, 0, ctx->stream>>>(g, n_jobs, d_mem_off, d_cnt,
                                                                 ctx->cfg.params.acc_floor, d_out, depth + 1, t);
