@@ -67,8 +67,9 @@ RESERVE_SMS = int(os.environ.get("ECCO_RESERVE_SMS", "12"))  # SMs the overlappe
 STEPS = 16            # SGD steps per micro-window
 # configs[4]: the detection-head variant (larger per-group model and frame
 # features).  Its window is the allocator's marginal-gain probing (every
-# group's speculative chain + member evaluations); the full camera x group
-# matrix at this shape has no fused kernel yet and is left out of the step.
+# group's speculative chain + member evaluations, as configs[4] states); the
+# full camera x group matrix at this shape (k_eval_wide, 7.3e14 FLOP) is
+# timed beside it as the line's `regroup_matrix` leg.
 DET_DIMS = dict(feat_dim=1024, hidden_dim=1024, num_classes=96)
 MATRIX = True         # the regroup matrix is part of the step (False for c5)
 GPU_S = 1.0           # GPU-seconds per micro-window; steps = floor(GPU_S * STEPS)
@@ -311,6 +312,12 @@ def run_b200(args, rank, world, local_rank):
             probes = probe_leg(retr, torch, dist)
         except Exception as e:  # reported, never fatal for the headline line
             probes = {"error": repr(e)}
+    regroup = None
+    if not MATRIX and not args.no_regroup:
+        try:
+            regroup = regroup_leg(retr, torch, dist, peaks()[0])
+        except Exception as e:  # reported, never fatal for the headline line
+            regroup = {"error": repr(e)}
     parity = None
     if not args.no_parity:
         try:
@@ -377,6 +384,8 @@ def run_b200(args, rank, world, local_rank):
             "parity": parity,
             "probes": probes,
         }
+        if regroup is not None:
+            line["regroup_matrix"] = regroup
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_sample(wl.N, wl.G)
             try:
@@ -433,6 +442,41 @@ def probe_leg(retr, torch, dist, reps=5):
             "how": f"every group's {PROBE_DEPTH}-micro-window speculative chain in one "
                    "ecco_train_trajectories call (member evaluations included, nothing "
                    "committed), CUDA events on the context stream, max over ranks"}
+
+
+def regroup_leg(retr, torch, dist, pk, reps=2):
+    """configs[4]'s window is the allocator's marginal-gain probing; its
+    window-end regroup -- the full camera x group matrix at the
+    detection-head shape (k_eval_wide: X streamed beside the model), the
+    all-gather and group_request's join rule -- is timed here on its own
+    (CUDA events on the context stream, max over ranks; the kernel's own
+    device time from the context's per-family events)."""
+    if not retr.local:
+        return None
+    ctx = retr.ctx
+    retr.regroup()
+    ctx.synchronize()
+    ctx.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(retr.stream):
+        e0.record(retr.stream)
+    for _ in range(reps):
+        retr.regroup()
+    with torch.cuda.stream(retr.stream):
+        e1.record(retr.stream)
+    e1.synchronize()
+    ctx.synchronize()
+    import paper_2512_11727_b200 as ecco
+    n, kms, fl, by = ctx.kernel_stat(ecco.KSTAT_EVAL_MATRIX)
+    ctx.profile(False)
+    ms = reduce_max(dist, [e0.elapsed_time(e1) / reps])[0]
+    tf = fl / kms / 1e9 if kms else None
+    peak = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    return {"ms_per_regroup": ms, "kernel_ms": kms / max(n, 1), "launches_per_regroup": n / reps,
+            "flops": fl / max(n, 1), "achieved_tflops": tf, "peak_tflops": peak,
+            "frac": tf / peak if tf else None,
+            "how": "full camera x group matrix (every camera's S eval frames under every local "
+                   "group), all-gather and join rule, CUDA events on the context stream"}
 
 
 def parity_spot_check(args, retr, wl, n_cams=64):
@@ -1095,6 +1139,8 @@ def main():
                     help="skip timing the reference's C4 parametric windows (~40 s of CPU)")
     ap.add_argument("--no-probes", action="store_true",
                     help="skip the batched marginal-gain probe leg")
+    ap.add_argument("--no-regroup", action="store_true",
+                    help="c5: skip the separately timed regroup-matrix leg")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the production-grid parity spot check against the FFMA path")
     ap.add_argument("--decisions", action="store_true",

@@ -768,8 +768,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars->w2_full[b], 1);
       mbar_init(&bars->w2_empty[b], 1);    // the layer-2 MMA commit
-      mbar_init(&bars->bias_full[b], 1);
-      mbar_init(&bars->bias_empty[b], 4);  // the 4 logits warps (b2 read last)
+      mbar_init(&bars->bias_full[b], 32);  // the producer warp's lanes
+      mbar_init(&bars->bias_empty[b], 8);  // every epilogue warp: b1 read, and b2 by the logits warps
       mbar_init(&bars->z_full[b], 1);
       mbar_init(&bars->z_empty[b], 8);
       mbar_init(&bars->r_full[b], 8);
@@ -820,15 +820,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           // after the half's stages (they pace the tensor cores): the entry's
           // biases once, then this half's W2^T (read by its layer-2 MMAs,
           // which the MMA warp issues after the NEXT half's K loop)
-          if (hf == 0) {
+          if (hf == 0) {  // (4.5 KB: plain warp copies, every lane arrives)
             const uint32_t bb = u & 1;
             mbar_wait(&bars->bias_empty[bb], ((u >> 1) & 1) ^ 1);
-            if (elect_one()) {
-              mbar_expect_tx(&bars->bias_full[bb], a.bias_bytes);
-              bulk_load(sBias + bb * a.bias_bytes, img + a.w2t_bytes, a.bias_bytes,
-                        &bars->bias_full[bb]);
-            }
-            __syncwarp();
+            const uint4* src = reinterpret_cast<const uint4*>(img + a.w2t_bytes);
+            uint4* dst = reinterpret_cast<uint4*>(sBias + bb * a.bias_bytes);
+            for (uint32_t i = lane; i < a.bias_bytes / 16; i += 32) dst[i] = __ldg(src + i);
+            mbar_arrive(&bars->bias_full[bb]);
           }
           const uint32_t wb = v & 1;
           mbar_wait(&bars->w2_empty[wb], ((v >> 1) & 1) ^ 1);
@@ -955,7 +953,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&bars->r_full[zb]);
           }
         }
-        if (cp != 0) continue;
+        if (cp != 0) {  // this warp's last b1 read of the entry is done
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->bias_empty[bb]);
+          continue;
+        }
         const int slot = a.ent_slot[e];
         const uint32_t lb = u % a.nl;
         mbar_wait(&bars->l_full[lb], (u / a.nl) & 1);
@@ -1027,6 +1029,9 @@ __global__ void k_shadow_w1t(int F, int H, const int* slots, const float* wbase,
 // W2^T image: C rows x H (K) bf16, K-major, 128-byte swizzle atoms of 64 K
 // elements; atom kb of row n at kb*(C*128) + n*128, 16-byte chunk j of the
 // row stored at chunk j ^ (n % 8).
+// One block per (slot, 64-wide K atom): the detection head's 96 x 1024 image
+// is 16 blocks' work, not one block's (a serial chain's snapshot images
+// are rebuilt per call, on the evaluation's critical path).
 __global__ void k_shadow_w2t(int F, int H, int C, const int* slots, const float* wbase,
                              size_t wstride, uint8_t* w2t, uint32_t img_bytes) {
   const int slot = slots[blockIdx.x];
@@ -1034,10 +1039,13 @@ __global__ void k_shadow_w2t(int F, int H, int C, const int* slots, const float*
   const float* W2 = b1 + H;
   const float* b2 = W2 + (size_t)H * C;
   uint8_t* img = w2t + (size_t)slot * img_bytes;
-  float* ib = reinterpret_cast<float*>(img + (size_t)C * H * 2);
-  for (int i = threadIdx.x; i < H; i += blockDim.x) ib[i] = b1[i];
-  for (int i = threadIdx.x; i < C; i += blockDim.x) ib[H + i] = b2[i];
-  for (int idx = threadIdx.x; idx < H * C; idx += blockDim.x) {
+  if (blockIdx.y == 0) {
+    float* ib = reinterpret_cast<float*>(img + (size_t)C * H * 2);
+    for (int i = threadIdx.x; i < H; i += blockDim.x) ib[i] = b1[i];
+    for (int i = threadIdx.x; i < C; i += blockDim.x) ib[H + i] = b2[i];
+  }
+  const int k0 = blockIdx.y * 64, k1 = min(H, k0 + 64);
+  for (int idx = k0 * C + threadIdx.x; idx < k1 * C; idx += blockDim.x) {
     const int n = idx % C, k = idx / C;  // W2[k][n]
     const int kb = k / 64, kw = k % 64;
     const int chunk = (kw * 2) / 16, within = (kw * 2) % 16;
@@ -1184,8 +1192,8 @@ void refresh_shadow(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t wstrid
                    ctx->stream>>>(g.feat_dim, g.hidden_dim, d_s1, wbase, wstride, sh.w1t, ctx->w1_t);
     ECCO_LAUNCHED(ctx);
   }
-  k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_sl, wbase,
-                                           wstride, sh.w2t, img_bytes(g));
+  k_shadow_w2t<<<dim3(n, (g.hidden_dim + 63) / 64), 256, 0, ctx->stream>>>(
+      g.feat_dim, g.hidden_dim, g.num_classes, d_sl, wbase, wstride, sh.w2t, img_bytes(g));
   ECCO_LAUNCHED(ctx);
 }
 
@@ -1199,8 +1207,8 @@ void refresh_shadow_dev(ecco_ctx* ctx, Shadow& sh, const float* wbase, size_t ws
                                   ctx->w1_t);
     ECCO_LAUNCHED(ctx);
   }
-  k_shadow_w2t<<<n, 256, 0, ctx->stream>>>(g.feat_dim, g.hidden_dim, g.num_classes, d_slots, wbase,
-                                           wstride, sh.w2t, img_bytes(g));
+  k_shadow_w2t<<<dim3(n, (g.hidden_dim + 63) / 64), 256, 0, ctx->stream>>>(
+      g.feat_dim, g.hidden_dim, g.num_classes, d_slots, wbase, wstride, sh.w2t, img_bytes(g));
   ECCO_LAUNCHED(ctx);
 }
 

@@ -19,6 +19,12 @@ run() {  # tool name timeout cmd...
   echo "$tool $name rc=$rc ${errs:-no summary line}" >> "$SUM"
 }
 PYT="python -m pytest -q -p no:cacheprovider -m gpu -x"
+wide_eval() {  # k_eval_wide (X streamed beside the model): odd shape, pairs mode, capped grid
+  for tool in memcheck synccheck racecheck; do
+    run $tool wide_eval 1500 $PYT tests/test_gpu_wide_eval.py -k "logits and odd or pairs_equal or regime and 2"
+  done
+}
+[ "${SANITIZE_ONLY:-}" = "wide_eval" ] && { : > "$SUM"; wide_eval; cat "$SUM"; exit 0; }
 for tool in memcheck synccheck racecheck; do
   run $tool smoke 900 python __graft_entry__.py
 done
@@ -28,4 +34,5 @@ for tool in memcheck synccheck; do
   run $tool fused_eval 1500 $PYT tests/test_gpu_fused_eval.py -k "pair and (multi_tile_regime_matches and 2 or pairs_equal or route or staged)"
   run $tool sim 900 $PYT tests/test_gpu_sim.py -k "c1_ten or drift_recovery"
 done
+wide_eval
 cat "$SUM"
