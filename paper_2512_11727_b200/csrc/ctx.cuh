@@ -386,7 +386,15 @@ void train_wide(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_step
 // the call (micro-window `micro` of them is trained by train_chain).
 void chain_rows(ecco_ctx* ctx, int n_jobs, const int* d_job_ids, const int* d_steps,
                 const int* h_steps, const int* d_src_off, const int* d_src_cam,
-                const double* d_src_frac, const int* d_micro_base, int n_micro, int window);
+                const double* d_src_frac, const int* d_micro_base, int n_micro, int window,
+                bool wide_rows = true);
+// Fused FP32 SGD chain (ffma_chain.cu): the oracle-exact math of the FFMA
+// path in one launch per micro-window (same contract as train_chain, without
+// shadows), one cluster of H/16 CTAs per job.
+bool ffma_chain_supported(const ecco_ctx* ctx);
+void train_ffma(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_steps,
+                const int* h_steps, int micro, int n_micro, const float* wsrc, size_t wsrc_stride,
+                float* wbase, size_t wstride, int loss_t, int n_launch = 1, size_t wmicro = 0);
 void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,
                  const int* d_steps, const int* h_steps, int micro, int n_micro,
                  const float* wsrc, size_t wsrc_stride, float* wbase, size_t wstride,

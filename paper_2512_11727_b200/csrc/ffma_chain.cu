@@ -1,0 +1,507 @@
+// Fused FP32 (FFMA) SGD chain of the learned backend: the ORACLE-EXACT math
+// (ECCO_MATH_FFMA_EXACT) in one launch per micro-window -- every job's
+// steps[j] SGD steps of gather, forward, softmax cross-entropy, backward and
+// update -- on one thread-block cluster per job, instead of nine kernels per
+// SGD step on a handful of SMs (learned_kernels.cu's general FFMA path,
+// ~115 us per step of a single job's serial chain).
+//
+// Bit-exact with oracle/ecco_oracle.c orc_sgd_step (and so with the general
+// FFMA path): every output is ONE thread's fmaf chain in the oracle's order --
+//   Z[s][h]     = (fmaf over f ascending of x[s][f] W1[f][h], from 0) + b1[h]
+//   L[s][c]     = (fmaf over k ascending of relu(Z[s][k]) W2[k][c]) + b2[c]
+//   softmax     = k_l_softmax_grad's sequence (max, ascending sum of ecco_expf,
+//                 IEEE divide, (p - onehot) * (1/B))
+//   dH[s][k]    = Z[s][k] > 0 ? fmaf over c ascending of dL[s][c] W2[k][c] : 0
+//                 (pre-update W2)
+//   W2[k][c]   <- fmaf(-lr, fmaf over s ascending of relu(Z[s][k]) dL[s][c], W2)
+//   b2[c]      <- fmaf(-lr, sum over s ascending of dL[s][c], b2)
+//   W1[f][h]   <- fmaf(-lr, fmaf over s ascending of x[s][f] dH[s][h], W1)
+//   b1[h]      <- fmaf(-lr, sum over s ascending of dH[s][h], b1)
+// -- so the tiling below changes where each chain runs, never its order.
+//
+// Cluster of H/16 CTAs (16 for H = 256: a non-portable cluster); CTA r owns
+// hidden units [16r, 16r+16) and rows [r RP, r RP + RP) (RP = 128 / cluster):
+//   smem    X (the step's 128 sampled rows, bf16, 16-byte chunks XOR-swizzled
+//           by row pair), the fp32 W1 master slice [F][16] (resident for the
+//           whole micro-window), a full copy of W2 (rows padded to C + 1:
+//           conflict-free both along k and along c), b1 slice, b2, the own
+//           pre-activations Z[128][16], and the exchange buffers below
+//   step    gather X (cp.async) -> Z of own units (FFMA, 2 rows x 4 units per
+//           thread) -> relu rows to the row owners (DSMEM) -> cluster barrier
+//           -> owner: logits of its rows over all H, softmax, dL (to every
+//           CTA), dH of its rows for all units (to each unit's CTA), row
+//           losses (to CTA 0) -> cluster barrier -> own W2 rows (to every
+//           CTA's copy), b2, b1, W1 (FFMA, 4 features x 8 units per thread)
+// Two cluster barriers per step; everything else is CTA-local.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "ctx.cuh"
+#include "learned_common.cuh"
+#include "sm100.cuh"
+
+using namespace sm100;
+
+namespace {
+
+constexpr int kB = 128;        // minibatch rows
+constexpr int kHS = 16;        // hidden units per CTA
+constexpr int kC = 16;         // classes
+constexpr int kThreads = 256;  // 8 warps
+constexpr int kMaxNC = 16;
+
+struct FfmaArgs {
+  LDims g;
+  const int* slots;
+  const int* steps;
+  const int32_t* rows;  // [job][row steps][kB] frame-table row of every sampled frame (chain_rows)
+  const int32_t* labs;  // ... and its label
+  int row_step0, rows_T;
+  const uint16_t* frames;
+  const float* wsrc;  // fp32 models the micro-window starts from (W1 [F][H])
+  size_t wsrc_stride;
+  float* wbase;  // ... and where it leaves them (a snapshot; may equal wsrc)
+  size_t wstride;
+  float* losses;
+  int loss_T, loss_t;
+  // serial mode (n_micro_launch > 1, one job): micro-window u's model is
+  // written to wbase + u * wmicro and its loss to loss_t + u
+  int n_micro_launch;
+  size_t wmicro;
+  int trace;
+};
+
+struct FLayout {
+  uint32_t x, w1, w2, b1, b2, z, rrecv, dl, dh, lown, loss, total;
+};
+
+__host__ __device__ inline FLayout flayout(int F, int H, int nc) {
+  FLayout L{};
+  const int rp = kB / nc;
+  uint32_t o = 0;
+  L.x = o;  // [128][F] bf16, 16-byte chunk j of row s at j ^ ((s >> 1) & 7)
+  o += (uint32_t)kB * F * 2u;
+  L.w1 = o;  // [F][16] fp32
+  o += (uint32_t)F * kHS * 4u;
+  L.w2 = o;  // [H][C + 1] fp32 (full copy)
+  o += (uint32_t)H * (kC + 1) * 4u;
+  o = (o + 15u) & ~15u;
+  L.b1 = o;
+  o += kHS * 4u;
+  L.b2 = o;
+  o += kC * 4u;
+  L.z = o;  // [128][16] fp32 own pre-activations
+  o += kB * kHS * 4u;
+  L.rrecv = o;  // [rp][H] fp32 relu rows of the owned rows, all units
+  o += (uint32_t)rp * H * 4u;
+  L.dl = o;  // [128][C] fp32 dL of every row
+  o += kB * kC * 4u;
+  L.dh = o;  // [128][16] fp32 dH of own units, every row
+  o += kB * kHS * 4u;
+  L.lown = o;  // [rp][C] logits / dL of the owned rows
+  o += (uint32_t)rp * kC * 4u;
+  L.loss = o;  // [128] row losses (CTA 0)
+  o += kB * 4u;
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+// Byte offset of bf16 element (s, f) in the swizzled X tile (row = F * 2 bytes).
+__device__ __forceinline__ uint32_t xoff(int F, int s, int f) {
+  const uint32_t chunk = (uint32_t)(f >> 3) ^ (uint32_t)((s >> 1) & 7);
+  return (uint32_t)s * (uint32_t)F * 2u + (chunk << 4) + (uint32_t)(f & 7) * 2u;
+}
+
+// 4 consecutive bf16 features (f % 4 == 0) of row s as fp32 (exact).
+__device__ __forceinline__ void ld_x4(const uint8_t* xs, int F, int s, int f, float (&x)[4]) {
+  const uint2 v = *reinterpret_cast<const uint2*>(xs + xoff(F, s, f));
+  x[0] = __uint_as_float(v.x << 16);
+  x[1] = __uint_as_float(v.x & 0xFFFF0000u);
+  x[2] = __uint_as_float(v.y << 16);
+  x[3] = __uint_as_float(v.y & 0xFFFF0000u);
+}
+
+// [step][point] clock64 of CTA 0, steps 0-3 (ECCO_FFMA_TRACE)
+__device__ long long g_ffma_trace[4 * 16];
+#define FTS(k)                                                                              \
+  do {                                                                                      \
+    if (a.trace && blockIdx.x == 0 && tid == 0 && t < 4) g_ffma_trace[t * 16 + (k)] = clock64(); \
+  } while (0)
+
+// Packed FP32 FMA (fma.rn.f32x2, sm_100): two IEEE fmaf in one instruction.
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+template <int NC, int F>
+__global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int RP = kB / NC;
+  const int H = a.g.H;
+  constexpr int C = kC;
+  constexpr int CP = kC + 1;  // padded W2 row
+  const FLayout L = flayout(F, H, NC);
+  uint8_t* xs = smem + L.x;
+  float* w1s = reinterpret_cast<float*>(smem + L.w1);
+  float* w2s = reinterpret_cast<float*>(smem + L.w2);
+  float* b1s = reinterpret_cast<float*>(smem + L.b1);
+  float* b2s = reinterpret_cast<float*>(smem + L.b2);
+  float* zs = reinterpret_cast<float*>(smem + L.z);
+  float* rrecv = reinterpret_cast<float*>(smem + L.rrecv);
+  float* dls = reinterpret_cast<float*>(smem + L.dl);
+  float* dhs = reinterpret_cast<float*>(smem + L.dh);
+  float* lown = reinterpret_cast<float*>(smem + L.lown);
+  float* lossv = reinterpret_cast<float*>(smem + L.loss);
+
+  const uint32_t r = cluster_ctarank();
+  const int j = blockIdx.x / NC;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int slot = a.slots[j];
+  const int nsteps = a.steps[j];
+  const int h0 = (int)r * kHS;
+  const float lr = a.g.lr;
+
+  // ---------------------------------------------------------- setup --
+  {
+    const float* src = a.wsrc + (size_t)slot * a.wsrc_stride;
+    for (int e = tid; e < F * kHS; e += kThreads) w1s[e] = src[(size_t)(e / kHS) * H + h0 + e % kHS];
+    const float* b1 = src + (size_t)F * H;
+    const float* W2 = b1 + H;
+    const float* b2 = W2 + (size_t)H * C;
+    for (int e = tid; e < H * C; e += kThreads) w2s[(e / C) * CP + e % C] = W2[e];
+    if (tid < kHS) b1s[tid] = b1[h0 + tid];
+    if (tid < C) b2s[tid] = b2[tid];
+  }
+  __syncthreads();
+
+  const uint32_t rrecv_a = smem_u32(rrecv), dl_a = smem_u32(dls), dh_a = smem_u32(dhs);
+  const uint32_t loss_a = smem_u32(lossv), w2_a = smem_u32(w2s);
+  const int total = nsteps * a.n_micro_launch;
+  for (int t = 0; t < total; ++t) {
+    const int u = t / (nsteps > 0 ? nsteps : 1);
+    const size_t rstep = (size_t)j * a.rows_T + a.row_step0 + t;
+    const int32_t* rows = a.rows + rstep * kB;
+    // ------------------------------------------------------ gather X --
+    FTS(0);
+    {
+      const int cpr = F / 8;  // 16-byte chunks per row
+      for (int e = tid; e < kB * cpr; e += kThreads) {
+        const int s = e / cpr, ch = e % cpr;
+        cp_async16(xs + xoff(F, s, ch * 8), a.frames + (size_t)rows[s] * F + ch * 8);
+      }
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    // ------------------------------ Z = X.W1 + b1 of the own 16 units --
+    FTS(1);
+    float acc[2][4];
+    const int hq = (lane & 3) * 4, s0 = warp * 16 + (lane >> 2) * 2;
+    {
+      float2 ac[2][2] = {};  // (row, unit pair): fma.rn.f32x2, each lane an fmaf chain
+#pragma unroll 2
+      for (int f = 0; f < F; f += 4) {
+        float x0[4], x1[4];
+        ld_x4(xs, F, s0, f, x0);
+        ld_x4(xs, F, s0 + 1, f, x1);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 w = *reinterpret_cast<const float4*>(w1s + (f + i) * kHS + hq);
+          const float2 wa = make_float2(w.x, w.y), wb = make_float2(w.z, w.w);
+          const float2 xa = make_float2(x0[i], x0[i]), xb = make_float2(x1[i], x1[i]);
+          ac[0][0] = fma2(xa, wa, ac[0][0]);
+          ac[0][1] = fma2(xa, wb, ac[0][1]);
+          ac[1][0] = fma2(xb, wa, ac[1][0]);
+          ac[1][1] = fma2(xb, wb, ac[1][1]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        acc[i][0] = ac[i][0].x;
+        acc[i][1] = ac[i][0].y;
+        acc[i][2] = ac[i][1].x;
+        acc[i][3] = ac[i][1].y;
+      }
+    }
+    {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int s = s0 + i;
+        float z[4], rl[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          z[q] = __fadd_rn(acc[i][q], b1s[hq + q]);
+          rl[q] = z[q] > 0.0f ? z[q] : 0.0f;
+        }
+        *reinterpret_cast<float4*>(zs + s * kHS + hq) = make_float4(z[0], z[1], z[2], z[3]);
+        // relu row piece -> the row's owner, at its units' columns
+        const uint32_t dst = rrecv_a + (uint32_t)(((s % RP) * H + h0 + hq) * 4);
+        st_cluster_v4(mapa_shared(dst, (uint32_t)(s / RP)), rl[0], rl[1], rl[2], rl[3]);
+      }
+    }
+    FTS(2);
+    cluster_sync();  // every owned row's relu values are in
+    FTS(3);
+    // ------------------------------------------- owner: logits, dL, dH --
+    {
+      const int rb = (int)r * RP;  // first owned row
+      for (int o = tid; o < RP * C; o += kThreads) {
+        const int sl = o / C, c = o % C;
+        const float* rr = rrecv + sl * H;
+        float acc = 0.0f;
+        for (int k = 0; k < H; ++k) acc = __fmaf_rn(rr[k], w2s[k * CP + c], acc);
+        lown[sl * C + c] = __fadd_rn(acc, b2s[c]);
+      }
+      __syncthreads();
+      if (tid < RP) {  // softmax cross-entropy of owned row rb + tid (k_l_softmax_grad)
+        float* l = lown + tid * C;
+        float m = l[0];
+        for (int c = 1; c < C; ++c) m = l[c] > m ? l[c] : m;
+        float sum = 0.0f;
+        for (int c = 0; c < C; ++c) sum = __fadd_rn(sum, ecco_expf(__fsub_rn(l[c], m)));
+        const float invB = __fdiv_rn(1.0f, (float)kB);
+        const int y = a.labs[rstep * kB + rb + tid];
+        const float loss = logf(sum) - (l[y] - m);
+        float dl[C];
+        for (int c = 0; c < C; ++c) {
+          const float p = __fdiv_rn(ecco_expf(__fsub_rn(l[c], m)), sum);
+          dl[c] = __fmul_rn(__fsub_rn(p, c == y ? 1.0f : 0.0f), invB);
+        }
+        for (int c = 0; c < C; ++c) l[c] = dl[c];
+        const uint32_t drow = dl_a + (uint32_t)((rb + tid) * C * 4);
+        for (uint32_t d = 0; d < (uint32_t)NC; ++d) {
+#pragma unroll
+          for (int c4 = 0; c4 < C; c4 += 4)
+            st_cluster_v4(mapa_shared(drow + c4 * 4, d), dl[c4], dl[c4 + 1], dl[c4 + 2], dl[c4 + 3]);
+        }
+        st_cluster_f32(mapa_shared(loss_a + (uint32_t)((rb + tid) * 4), 0u), loss);
+      }
+      __syncthreads();
+      // dH of the owned rows for every unit (pre-update W2), to the unit's CTA
+      for (int sl = warp; sl < RP; sl += kThreads / 32) {
+        const float* dlr = lown + sl * C;
+        const float* rr = rrecv + sl * H;
+        for (int k = lane; k < H; k += 32) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc = __fmaf_rn(dlr[c], w2s[k * CP + c], acc);
+          const float dh = rr[k] > 0.0f ? acc : 0.0f;
+          st_cluster_f32(mapa_shared(dh_a + (uint32_t)(((rb + sl) * kHS + k % kHS) * 4),
+                                     (uint32_t)(k / kHS)),
+                         dh);
+        }
+      }
+    }
+    FTS(4);
+    cluster_sync();  // every row's dL and every own unit's dH are in
+    FTS(5);
+    // ------------------------------------------------------- updates --
+    {
+      // own W2 rows (one element per thread), to every CTA's copy
+      for (int o = tid; o < kHS * C; o += kThreads) {
+        const int kl = o / C, c = o % C, k = h0 + kl;
+        float acc = 0.0f;
+        for (int s = 0; s < kB; ++s) {
+          const float z = zs[s * kHS + kl];
+          acc = __fmaf_rn(z > 0.0f ? z : 0.0f, dls[s * C + c], acc);
+        }
+        const float w = __fmaf_rn(-lr, acc, w2s[k * CP + c]);
+        const uint32_t wa = w2_a + (uint32_t)((k * CP + c) * 4);
+        for (uint32_t d = 0; d < (uint32_t)NC; ++d) st_cluster_f32(mapa_shared(wa, d), w);
+      }
+      if (tid < C) {  // b2 (every CTA, same inputs, same order)
+        float acc = 0.0f;
+        for (int s = 0; s < kB; ++s) acc = __fadd_rn(acc, dls[s * C + tid]);
+        b2s[tid] = __fmaf_rn(-lr, acc, b2s[tid]);
+      }
+      if (tid >= 32 && tid < 32 + kHS) {  // own b1
+        const int h = tid - 32;
+        float acc = 0.0f;
+        for (int s = 0; s < kB; ++s) acc = __fadd_rn(acc, dhs[s * kHS + h]);
+        b1s[h] = __fmaf_rn(-lr, acc, b1s[h]);
+      }
+      // W1 += -lr X^T dH: 4 features x 8 units per thread, rows ascending
+      for (int fb = tid >> 1; fb < F / 4; fb += kThreads / 2) {
+        const int f0 = fb * 4, hq = (tid & 1) * 8;
+        float2 acc[4][4] = {};  // (feature, unit pair)
+#pragma unroll 2
+        for (int s = 0; s < kB; ++s) {
+          float x[4];
+          ld_x4(xs, F, s, f0, x);
+          const float4 d0 = *reinterpret_cast<const float4*>(dhs + s * kHS + hq);
+          const float4 d1 = *reinterpret_cast<const float4*>(dhs + s * kHS + hq + 4);
+          const float2 d[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w),
+                               make_float2(d1.x, d1.y), make_float2(d1.z, d1.w)};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 xi = make_float2(x[i], x[i]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][q] = fma2(xi, d[q], acc[i][q]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float* w = w1s + (f0 + i) * kHS + hq + 2 * q;
+            w[0] = __fmaf_rn(-lr, acc[i][q].x, w[0]);
+            w[1] = __fmaf_rn(-lr, acc[i][q].y, w[1]);
+          }
+      }
+      if (r == 0 && tid == 64 && ((t + 1) % nsteps == 0)) {  // the micro-window's last step loss
+        double s = 0.0;
+        for (int i = 0; i < kB; ++i) s += lossv[i];
+        a.losses[(size_t)slot * a.loss_T + a.loss_t + u] = (float)(s / kB);
+      }
+    }
+    __syncthreads();
+    FTS(6);
+    // ----------------------------------------- snapshot at micro-window end --
+    if ((t + 1) % nsteps == 0 && (t + 1) < total) {
+      float* dst = a.wbase + (size_t)slot * a.wstride + (size_t)u * a.wmicro;
+      for (int e = tid; e < F * kHS; e += kThreads) dst[(size_t)(e / kHS) * H + h0 + e % kHS] = w1s[e];
+      float* b1 = dst + (size_t)F * H;
+      float* W2 = b1 + H;
+      if (tid < kHS) b1[h0 + tid] = b1s[tid];
+      for (int e = tid; e < kHS * C; e += kThreads) W2[(size_t)h0 * C + e] = w2s[(h0 + e / C) * CP + e % C];
+      if (r == 0 && tid < C) W2[(size_t)H * C + tid] = b2s[tid];
+    }
+  }
+  // ---------------------------------------------------- write-back --
+  // (the other CTAs' W2 rows of the last step arrive by DSMEM; none is read here)
+  const int ulast = a.n_micro_launch - 1;
+  float* dst = a.wbase + (size_t)slot * a.wstride + (size_t)ulast * a.wmicro;
+  for (int e = tid; e < F * kHS; e += kThreads) dst[(size_t)(e / kHS) * H + h0 + e % kHS] = w1s[e];
+  float* b1 = dst + (size_t)F * H;
+  float* W2 = b1 + H;
+  if (tid < kHS) b1[h0 + tid] = b1s[tid];
+  for (int e = tid; e < kHS * C; e += kThreads) W2[(size_t)h0 * C + e] = w2s[(h0 + e / C) * CP + e % C];
+  if (r == 0 && tid < C) W2[(size_t)H * C + tid] = b2s[tid];
+  if (nsteps == 0 && r == 0 && tid == 0)
+    for (int u = 0; u < a.n_micro_launch; ++u)
+      a.losses[(size_t)slot * a.loss_T + a.loss_t + u] = __int_as_float(0x7fc00000);
+  cluster_sync();  // no CTA exits while a peer may still store into its shared memory
+}
+
+template <int NC, int F>
+void launch_nc(const cudaLaunchConfig_t& lc0, const FfmaArgs& a, int device) {
+  static DeviceFlags attr;
+  if (!attr.done(device)) {
+    ECCO_CUDA(cudaFuncSetAttribute(k_train_ffma<NC, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   232448));
+    if (NC > 8)
+      ECCO_CUDA(cudaFuncSetAttribute(k_train_ffma<NC, F>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr.mark(device);
+  }
+  cudaLaunchConfig_t lc = lc0;
+  ECCO_CUDA(cudaLaunchKernelEx(&lc, k_train_ffma<NC, F>, a));
+}
+
+template <int F>
+void launch_f(int nc, const cudaLaunchConfig_t& lc, const FfmaArgs& a, int device) {
+  switch (nc) {
+    case 16: launch_nc<16, F>(lc, a, device); break;
+    case 8: launch_nc<8, F>(lc, a, device); break;
+    case 4: launch_nc<4, F>(lc, a, device); break;
+    default: launch_nc<2, F>(lc, a, device); break;
+  }
+}
+
+}  // namespace
+
+namespace fused {
+
+// B = 128, C = 16, H = 16 x (2, 4, 8, 16), F = 128 / 256 / 512 and
+// the shared-memory layout within the opt-in limit.  ECCO_FFMA_CHAIN=0 keeps
+// the general per-step FFMA kernels (the A/B reference of the tests).
+bool ffma_chain_supported(const ecco_ctx* ctx) {
+  const ecco_config& g = ctx->cfg;
+  const char* e = getenv("ECCO_FFMA_CHAIN");
+  if (e && e[0] == '0') return false;
+  const int nc = g.hidden_dim / kHS;
+  return g.minibatch == kB && g.num_classes == kC && g.hidden_dim % kHS == 0 && nc >= 2 &&
+         nc <= kMaxNC && (nc & (nc - 1)) == 0 &&
+         (g.feat_dim == 128 || g.feat_dim == 256 || g.feat_dim == 512) &&
+         flayout(g.feat_dim, g.hidden_dim, nc).total <= 232448;
+}
+
+void train_ffma(ecco_ctx* ctx, int n_jobs, const int* d_slots, const int* d_steps,
+                const int* h_steps, int micro, int n_micro, const float* wsrc, size_t wsrc_stride,
+                float* wbase, size_t wstride, int loss_t, int n_launch, size_t wmicro) {
+  if (n_jobs == 0) return;
+  ECCO_REQUIRE(n_launch == 1 || n_jobs == 1, "serial FFMA chain: one job");
+  const ecco_config& c = ctx->cfg;
+  int max_steps = 0;
+  for (int j = 0; j < n_jobs; ++j) max_steps = std::max(max_steps, h_steps[j]);
+  FfmaArgs a{};
+  a.g = LDims{c.feat_dim, c.hidden_dim, c.num_classes, c.scene_dims, c.minibatch,
+              c.ring_frames, c.eval_samples, c.sgd_lr, c.feature_noise};
+  a.slots = d_slots;
+  a.steps = d_steps;
+  a.rows = (const int32_t*)ctx->train_scratch[0].p;  // chain_rows() of this call
+  a.labs = (const int32_t*)ctx->train_scratch[1].p;
+  a.row_step0 = micro * max_steps;
+  a.rows_T = n_micro * max_steps;
+  a.frames = ctx->d_frames;
+  a.wsrc = wsrc;
+  a.wsrc_stride = wsrc_stride;
+  a.wbase = wbase;
+  a.wstride = wstride;
+  a.losses = ctx->d_losses;
+  a.loss_T = c.max_depth;
+  a.loss_t = loss_t;
+  a.n_micro_launch = n_launch;
+  a.wmicro = wmicro;
+  const int nc = c.hidden_dim / kHS;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)(nc * n_jobs));
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = flayout(c.feat_dim, c.hidden_dim, nc).total;
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)nc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const double F = c.feat_dim, H = c.hidden_dim, C = c.num_classes;
+  double steps = 0, live = 0;
+  for (int j = 0; j < n_jobs; ++j) {
+    steps += (double)h_steps[j] * n_launch;
+    live += h_steps[j] > 0;
+  }
+  const double flops = steps * kB * (4.0 * F * H + 6.0 * H * C);
+  const double bytes = steps * kB * F * 2.0 + live * (F * H + H + H * C + C) * 8.0;
+  a.trace = getenv("ECCO_FFMA_TRACE") ? 1 : 0;
+  ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_STEP, flops, bytes,
+             (c.feat_dim == 512   ? launch_f<512>(nc, lc, a, c.device)
+              : c.feat_dim == 256 ? launch_f<256>(nc, lc, a, c.device)
+                                  : launch_f<128>(nc, lc, a, c.device)));
+  ECCO_LAUNCHED(ctx);
+  if (a.trace) {  // points: 0 gather, 1 forward, 2 relu sent, 3 barrier 1, 4 head done, 5 barrier 2, 6 updates done
+    long long tr[4 * 16];
+    ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+    ECCO_CUDA(cudaMemcpyFromSymbol(tr, g_ffma_trace, sizeof(tr)));
+    for (int t = 0; t < 4; ++t) {
+      fprintf(stderr, "ffma step %d:", t);
+      for (int k = 1; k < 7; ++k) fprintf(stderr, " %d:%lld", k, tr[t * 16 + k] - tr[t * 16]);
+      fprintf(stderr, "\n");
+    }
+  }
+}
+
+}  // namespace fused

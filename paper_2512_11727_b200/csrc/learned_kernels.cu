@@ -1257,6 +1257,46 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
   // masters round-trip exactly), tests/test_gpu_learned.py.
   // (wide chains: the planned general evaluation of all snapshots)
   const bool wide = ctx->fused_train && !fused::train_supported(ctx);
+  // The oracle-exact math on its fused FFMA chain (ffma_chain.cu): one launch
+  // per micro-window (or one per call in serial mode), the same arithmetic
+  // as the per-step FFMA kernels below bit for bit
+  const bool ffma_chain = !ctx->fused_train && ctx->cfg.math == ECCO_MATH_FFMA_EXACT &&
+                          fused::ffma_chain_supported(ctx);
+  if (ffma_chain) {
+    fused::chain_rows(ctx, n_jobs, d_job_ids, d_steps, h_steps, d_src_off, d_src_cam, d_src_frac,
+                      d_micro_base, depth, window, false);
+    if (n_jobs == 1 && depth >= 2 && n_mem > 0 && h_steps[0] > 0 && !getenv("ECCO_NO_SERIAL_CHAIN")) {
+      // serial: every micro-window in one launch, then the member
+      // evaluations of all snapshots in one batched pass
+      float* sbase = ctx->d_wspec + (size_t)slots[0] * spec_stride;
+      fused::train_ffma(ctx, 1, d_slots, d_steps, h_steps, 0, depth, ctx->d_w, np, ctx->d_wspec,
+                        spec_stride, 0, depth, np);
+      const int n_pairs = n_mem * depth;
+      int* d_vslot = (int*)ctx->scratch[21].get(sizeof(int) * n_pairs);
+      int* d_vcam = (int*)ctx->scratch[22].get(sizeof(int) * n_pairs);
+      int* d_vcnt = (int*)ctx->scratch[23].get(sizeof(int) * n_pairs);
+      k_l_serial_pairs<<<nblk(n_pairs, 256), 256, 0, ctx->stream>>>(n_mem, depth, d_mem_cam, d_vslot,
+                                                                    d_vcam);
+      ECCO_LAUNCHED(ctx);
+      float* saved = ctx->d_w;
+      const size_t saved_np = ctx->n_params;
+      ctx->d_w = sbase;  // snapshot u = "slot" u of the pair evaluation
+      ctx->n_params = np;
+      try {
+        pair_counts(ctx, n_pairs, d_vslot, d_vcam, d_vcnt);
+      } catch (...) {
+        ctx->d_w = saved;
+        ctx->n_params = saved_np;
+        throw;
+      }
+      ctx->d_w = saved;
+      ctx->n_params = saved_np;
+      k_l_serial_mean<<<nblk(depth, 64), 64, 0, ctx->stream>>>(g, n_mem, depth, d_vcnt, d_out);
+      ECCO_LAUNCHED(ctx);
+      ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+  }
   const bool serial = ctx->fused_train && n_jobs == 1 && depth >= 2 && n_mem > 0 &&
                       h_steps[0] > 0 && !getenv("ECCO_NO_SERIAL_CHAIN") &&
                       (ctx->fused_eval ? ctx->sh_pool.w1t != nullptr
@@ -1336,6 +1376,10 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
         ECCO_CUDA(cudaEventRecord(ctx->ev_eval[t & 1], ctx->eval_stream));
         continue;
       }
+    } else if (ffma_chain) {  // state t-1 -> state t in one launch
+      const float* src = t == 1 ? ctx->d_w : ctx->d_wspec + (size_t)(t - 2) * np;
+      fused::train_ffma(ctx, n_jobs, d_slots, d_steps, h_steps, t - 1, depth, src,
+                        t == 1 ? np : spec_stride, wt, spec_stride, t - 1);
     } else {
       // state t starts as a copy of state t-1
       if (t == 1)
@@ -1349,7 +1393,7 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
       ECCO_LAUNCHED(ctx);
     }
     if (tc_bf16 && !ctx->fused_train) fused::shadow_w1t(ctx, d_slots, n_jobs, wt, spec_stride, w1t_train);
-    for (int step = 0; step < (ctx->fused_train ? 0 : max_steps); ++step) {
+    for (int step = 0; step < (ctx->fused_train || ffma_chain ? 0 : max_steps); ++step) {
       const Gate gate{d_steps, step, g.B};
       int live = 0;
       for (int j = 0; j < n_jobs; ++j) live += step < h_steps[j];

@@ -692,7 +692,8 @@ bool train_supported(const ecco_ctx* ctx) {
 
 void chain_rows(ecco_ctx* ctx, int n_jobs, const int* d_job_ids, const int* d_steps,
                 const int* h_steps, const int* d_src_off, const int* d_src_cam,
-                const double* d_src_frac, const int* d_micro_base, int n_micro, int window) {
+                const double* d_src_frac, const int* d_micro_base, int n_micro, int window,
+                bool wide_rows) {
   if (n_jobs == 0 || n_micro == 0) return;
   const ecco_config& c = ctx->cfg;
   const LDims g{c.feat_dim, c.hidden_dim, c.num_classes, c.scene_dims, c.minibatch,
@@ -709,7 +710,7 @@ void chain_rows(ecco_ctx* ctx, int n_jobs, const int* d_job_ids, const int* d_st
       g, c.seed, d_job_ids, d_steps, d_src_off, d_src_cam, d_src_frac, d_micro_base, 0, window,
       max_steps, ctx->d_labels, rows, labs);
   ECCO_LAUNCHED(ctx);
-  if (!train_supported(ctx)) wide_gather(ctx, n_jobs, d_steps, max_steps, n_micro);
+  if (wide_rows && !train_supported(ctx)) wide_gather(ctx, n_jobs, d_steps, max_steps, n_micro);
 }
 
 void train_chain(ecco_ctx* ctx, const Shadow* sh, int n_jobs, const int* d_slots,

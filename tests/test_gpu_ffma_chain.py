@@ -1,0 +1,93 @@
+"""The fused FP32 SGD chain (ffma_chain.cu): the oracle-exact math
+(FFMA_EXACT) in one launch per micro-window on a cluster of H/16 CTAs.
+
+Bar: bit-exact.  Trajectories, committed weights and losses equal the CPU
+oracle's (orc_sgd_step, oracle/ecco_oracle.c) and the general per-step FFMA
+kernels' (ECCO_FFMA_CHAIN=0) bit for bit -- with jobs of unequal step
+budgets (including idle jobs), in serial mode (one job, several
+micro-windows in one launch) and at other shapes (H = 128, F = 128)."""
+import numpy as np
+import pytest
+
+import paper_2512_11727_b200 as ecco
+
+from test_gpu_learned import BENCH, setup
+
+pytestmark = pytest.mark.gpu
+
+
+def _jobs(n, members_per=2, fps=None):
+    ids = list(range(3, 3 + n))
+    members = [[(2 * k + i) % 6 for i in range(members_per)] for k in range(n)]
+    fracs = [[1.0 / members_per] * members_per] * n
+    fps = fps or [30.0] * n
+    batches = [(f, 1080.0, 1.0) for f in fps]
+    return ids, members, fracs, batches
+
+
+def _run(ctx, ids, members, fracs, batches, depth, window=3):
+    ctx.seed_models(ids)
+    got = ctx.train_trajectories(ids, batches, members, fracs, members, 1.0, depth, window=window)
+    losses = ctx.last_losses(ids, depth)
+    ctx.commit(ids, [depth] * len(ids))
+    return got, losses, [ctx.get_weights(j) for j in ids]
+
+
+# fps 30: sufficiency 1 (16 steps); 0.1: 0 steps (idle job); 2.0: 8 steps
+@pytest.mark.parametrize("fps", [[30.0, 30.0, 30.0], [30.0, 0.1, 2.0]], ids=["equal", "unequal"])
+def test_ffma_chain_equals_oracle_and_per_step_kernels(fps, monkeypatch):
+    ids, members, fracs, batches = _jobs(3, fps=fps)
+    ctx, orc, _ = setup(seed=41, **BENCH)
+    got, losses, weights = _run(ctx, ids, members, fracs, batches, 2)
+    # the oracle
+    for j in ids:
+        orc.seed(j)
+    want = orc.trajectories(ids, batches, members, fracs, members, 1.0, 2)
+    assert got.tobytes() == want.tobytes()
+    orc.commit(ids, [2] * len(ids))
+    for j, w in zip(ids, weights):
+        for a, b in zip(w, orc.models[j]):
+            assert a.reshape(-1).tobytes() == b.tobytes(), j
+    # the per-step FFMA kernels (incl. the losses the oracle does not keep)
+    monkeypatch.setenv("ECCO_FFMA_CHAIN", "0")
+    ctx2, _, _ = setup(seed=41, **BENCH)
+    got2, losses2, weights2 = _run(ctx2, ids, members, fracs, batches, 2)
+    assert got.tobytes() == got2.tobytes()
+    assert np.array_equal(losses, losses2, equal_nan=True)
+    for w, w2 in zip(weights, weights2):
+        for a, b in zip(w, w2):
+            assert a.tobytes() == b.tobytes()
+
+
+def test_ffma_serial_chain_equals_per_micro_window_launches(monkeypatch):
+    """One job, depth 4: serial mode (one launch, snapshots written at the
+    micro-window ends, one batched evaluation) vs one launch per
+    micro-window."""
+    ids, members, fracs, batches = _jobs(1, members_per=3)
+    ctx, _, _ = setup(seed=42, **BENCH)
+    got, losses, weights = _run(ctx, ids, members, fracs, batches, 4)
+    monkeypatch.setenv("ECCO_NO_SERIAL_CHAIN", "1")
+    ctx2, _, _ = setup(seed=42, **BENCH)
+    got2, losses2, weights2 = _run(ctx2, ids, members, fracs, batches, 4)
+    assert got.tobytes() == got2.tobytes()
+    assert np.array_equal(losses, losses2, equal_nan=True)
+    for a, b in zip(weights[0], weights2[0]):
+        assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("hidden,feat", [(128, 256), (256, 128)])
+def test_ffma_chain_other_cluster_sizes(hidden, feat, monkeypatch):
+    """H = 128 (8-CTA clusters, 16 owned rows per CTA) and F = 128 against
+    the per-step FFMA kernels bit for bit."""
+    dims = dict(BENCH, hidden_dim=hidden, feat_dim=feat)
+    ids, members, fracs, batches = _jobs(2)
+    ctx, _, _ = setup(seed=43, **dims)
+    got, losses, weights = _run(ctx, ids, members, fracs, batches, 2)
+    monkeypatch.setenv("ECCO_FFMA_CHAIN", "0")
+    ctx2, _, _ = setup(seed=43, **dims)
+    got2, losses2, weights2 = _run(ctx2, ids, members, fracs, batches, 2)
+    assert got.tobytes() == got2.tobytes()
+    assert np.array_equal(losses, losses2, equal_nan=True)
+    for w, w2 in zip(weights, weights2):
+        for a, b in zip(w, w2):
+            assert a.tobytes() == b.tobytes()

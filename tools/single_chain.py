@@ -5,7 +5,7 @@ replay's extension chains run.  Prints the CUDA-event time per chain launch
 and per call.  With an instrumented build (tools/chain_trace.py on) and
 ECCO_CHAIN_TRACE=0 the per-phase clock64 trace of CTA 0 is printed too.
 
-  python tools/single_chain.py [depth] [reps] [c4|c5]
+  python tools/single_chain.py [depth] [reps] [c4|c5] [tc|ffma]
 
 c5: the detection-head shape F1024-H1024-C96 (the wide fused chain,
 wide_kernels.cu; members evaluated on the general tensor-core path)."""
@@ -26,10 +26,11 @@ def main():
     depth = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     shape = sys.argv[3] if len(sys.argv) > 3 else "c4"
+    math = ecco.FFMA_EXACT if len(sys.argv) > 4 and sys.argv[4] == "ffma" else ecco.TC_BF16
     dims = (dict(feat_dim=512, hidden_dim=256, num_classes=16) if shape == "c4" else
             dict(feat_dim=1024, hidden_dim=1024, num_classes=96))
     N, per = 400, 20
-    ctx = ecco.Context(backend=ecco.LEARNED, math=ecco.TC_BF16, max_cameras=N, max_jobs=4,
+    ctx = ecco.Context(backend=ecco.LEARNED, math=math, max_cameras=N, max_jobs=4,
                        max_depth=64, steps_per_gpu_s=16.0, minibatch=128, ring_frames=512,
                        eval_samples=64, **dims)
     scenes = np.array([[0.1 * (c // per % 10), 0.1 * (c // per // 10)] for c in range(N)])
@@ -54,7 +55,7 @@ def main():
     n2, ms2, _, _ = ctx.kernel_stat(ecco.KSTAT_EVAL_PAIRS)
     other = {k: ctx.kernel_stat(getattr(ecco, "KSTAT_" + k))[:2]
              for k in ("EVAL_MATRIX", "TRAIN_DW1", "TRAIN_HEAD")}
-    print(json.dumps({"shape": shape, "other_kernels": other, "depth": depth, "ms_per_call": e0.elapsed_time(e1) / reps,
+    print(json.dumps({"shape": shape, "math": "ffma" if math == ecco.FFMA_EXACT else "tc", "other_kernels": other, "depth": depth, "ms_per_call": e0.elapsed_time(e1) / reps,
                       "ms_per_micro_window": e0.elapsed_time(e1) / reps / depth,
                       "chain_launch_ms": ms / max(n, 1), "chain_launches": n,
                       "eval_launch_ms": ms2 / max(n2, 1), "us_per_sgd_step": ms / max(n, 1) / 16 * 1e3}))
