@@ -207,20 +207,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
     __syncthreads();
     // ------------------------------ Z = X.W1 + b1 of the own 16 units --
     FTS(1);
+    // warp w: units [4 (w % 4), +4) (warp-uniform: the W1 loads broadcast),
+    // rows 64 (w / 4) + 2 lane + {0, 1}; 8 features per iteration, X by one
+    // 16-byte load per row (the (s >> 1) & 7 chunk swizzle keeps each
+    // quarter-warp's 8 rows on distinct banks)
     float acc[2][4];
-    const int hq = (lane & 3) * 4, s0 = warp * 16 + (lane >> 2) * 2;
+    const int hq = (warp & 3) * 4, s0 = (warp >> 2) * 64 + 2 * lane;
     {
       float2 ac[2][2] = {};  // (row, unit pair): fma.rn.f32x2, each lane an fmaf chain
 #pragma unroll 2
-      for (int f = 0; f < F; f += 4) {
-        float x0[4], x1[4];
-        ld_x4(xs, F, s0, f, x0);
-        ld_x4(xs, F, s0 + 1, f, x1);
+      for (int f = 0; f < F; f += 8) {
+        const uint4 va = *reinterpret_cast<const uint4*>(xs + xoff(F, s0, f));
+        const uint4 vb = *reinterpret_cast<const uint4*>(xs + xoff(F, s0 + 1, f));
+        const uint32_t pa[4] = {va.x, va.y, va.z, va.w}, pb[4] = {vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
+          const float x0 = __uint_as_float(i & 1 ? pa[i >> 1] & 0xFFFF0000u : pa[i >> 1] << 16);
+          const float x1 = __uint_as_float(i & 1 ? pb[i >> 1] & 0xFFFF0000u : pb[i >> 1] << 16);
           const float4 w = *reinterpret_cast<const float4*>(w1s + (f + i) * kHS + hq);
           const float2 wa = make_float2(w.x, w.y), wb = make_float2(w.z, w.w);
-          const float2 xa = make_float2(x0[i], x0[i]), xb = make_float2(x1[i], x1[i]);
+          const float2 xa = make_float2(x0, x0), xb = make_float2(x1, x1);
           ac[0][0] = fma2(xa, wa, ac[0][0]);
           ac[0][1] = fma2(xa, wb, ac[0][1]);
           ac[1][0] = fma2(xb, wa, ac[1][0]);
@@ -261,37 +267,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
         const int sl = o / C, c = o % C;
         const float* rr = rrecv + sl * H;
         float acc = 0.0f;
+#pragma unroll 8
         for (int k = 0; k < H; ++k) acc = __fmaf_rn(rr[k], w2s[k * CP + c], acc);
         lown[sl * C + c] = __fadd_rn(acc, b2s[c]);
       }
       __syncthreads();
-      if (tid < RP) {  // softmax cross-entropy of owned row rb + tid (k_l_softmax_grad)
-        float* l = lown + tid * C;
+      // softmax cross-entropy of the owned rows (k_l_softmax_grad's
+      // sequence): one half-warp per row, lane c holds class c; the max and
+      // the ascending sum are formed in the same order by every lane
+      for (int o = tid; o < RP * C; o += kThreads) {
+        const int sl = o / C, c = o % C;
+        const unsigned hm = 0xFFFFu << (lane & 16);
+        const float* l = lown + sl * C;
         float m = l[0];
-        for (int c = 1; c < C; ++c) m = l[c] > m ? l[c] : m;
-        float sum = 0.0f;
-        for (int c = 0; c < C; ++c) sum = __fadd_rn(sum, ecco_expf(__fsub_rn(l[c], m)));
-        const float invB = __fdiv_rn(1.0f, (float)kB);
-        const int y = a.labs[rstep * kB + rb + tid];
-        const float loss = logf(sum) - (l[y] - m);
-        float dl[C];
-        for (int c = 0; c < C; ++c) {
-          const float p = __fdiv_rn(ecco_expf(__fsub_rn(l[c], m)), sum);
-          dl[c] = __fmul_rn(__fsub_rn(p, c == y ? 1.0f : 0.0f), invB);
-        }
-        for (int c = 0; c < C; ++c) l[c] = dl[c];
-        const uint32_t drow = dl_a + (uint32_t)((rb + tid) * C * 4);
-        for (uint32_t d = 0; d < (uint32_t)NC; ++d) {
 #pragma unroll
-          for (int c4 = 0; c4 < C; c4 += 4)
-            st_cluster_v4(mapa_shared(drow + c4 * 4, d), dl[c4], dl[c4 + 1], dl[c4 + 2], dl[c4 + 3]);
-        }
-        st_cluster_f32(mapa_shared(loss_a + (uint32_t)((rb + tid) * 4), 0u), loss);
+        for (int cc = 1; cc < C; ++cc) m = l[cc] > m ? l[cc] : m;
+        const float lc = l[c];
+        const float e = ecco_expf(__fsub_rn(lc, m));
+        float sum = 0.0f;
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) sum = __fadd_rn(sum, __shfl_sync(hm, e, cc, 16));
+        const float invB = __fdiv_rn(1.0f, (float)kB);
+        const int y = a.labs[rstep * kB + rb + sl];
+        const float p = __fdiv_rn(e, sum);
+        const float dl = __fmul_rn(__fsub_rn(p, c == y ? 1.0f : 0.0f), invB);
+        const float ly = l[y];
+        __syncwarp(hm);
+        lown[sl * C + c] = dl;
+        const uint32_t dst = dl_a + (uint32_t)(((rb + sl) * C + c) * 4);
+        for (uint32_t d = 0; d < (uint32_t)NC; ++d) st_cluster_f32(mapa_shared(dst, d), dl);
+        if (c == 0)
+          st_cluster_f32(mapa_shared(loss_a + (uint32_t)((rb + sl) * 4), 0u),
+                         logf(sum) - (ly - m));
       }
       __syncthreads();
       // dH of the owned rows for every unit (pre-update W2), to the unit's CTA
       for (int sl = warp; sl < RP; sl += kThreads / 32) {
-        const float* dlr = lown + sl * C;
+        float dlr[C];  // (registers: the DSMEM stores below clobber memory)
+#pragma unroll
+        for (int c = 0; c < C; ++c) dlr[c] = lown[sl * C + c];
         const float* rr = rrecv + sl * H;
         for (int k = lane; k < H; k += 32) {
           float acc = 0.0f;
@@ -309,56 +323,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
     FTS(5);
     // ------------------------------------------------------- updates --
     {
-      // own W2 rows (one element per thread), to every CTA's copy
-      for (int o = tid; o < kHS * C; o += kThreads) {
-        const int kl = o / C, c = o % C, k = h0 + kl;
-        float acc = 0.0f;
-        for (int s = 0; s < kB; ++s) {
-          const float z = zs[s * kHS + kl];
-          acc = __fmaf_rn(z > 0.0f ? z : 0.0f, dls[s * C + c], acc);
-        }
-        const float w = __fmaf_rn(-lr, acc, w2s[k * CP + c]);
-        const uint32_t wa = w2_a + (uint32_t)((k * CP + c) * 4);
-        for (uint32_t d = 0; d < (uint32_t)NC; ++d) st_cluster_f32(mapa_shared(wa, d), w);
-      }
-      if (tid < C) {  // b2 (every CTA, same inputs, same order)
-        float acc = 0.0f;
-        for (int s = 0; s < kB; ++s) acc = __fadd_rn(acc, dls[s * C + tid]);
-        b2s[tid] = __fmaf_rn(-lr, acc, b2s[tid]);
-      }
-      if (tid >= 32 && tid < 32 + kHS) {  // own b1
-        const int h = tid - 32;
-        float acc = 0.0f;
-        for (int s = 0; s < kB; ++s) acc = __fadd_rn(acc, dhs[s * kHS + h]);
-        b1s[h] = __fmaf_rn(-lr, acc, b1s[h]);
-      }
-      // W1 += -lr X^T dH: 4 features x 8 units per thread, rows ascending
-      for (int fb = tid >> 1; fb < F / 4; fb += kThreads / 2) {
-        const int f0 = fb * 4, hq = (tid & 1) * 8;
-        float2 acc[4][4] = {};  // (feature, unit pair)
+      // warps 0-3: W1 += -lr X^T dH, 8 features x 8 units per thread (rows
+      // ascending); warps 4-7 meanwhile: the own W2 rows (two elements per
+      // thread, to every CTA's copy), b2 and the own b1 (rows ascending)
+      if (warp < 4) {
+        const int hq = (tid & 1) * 8;
+        for (int fb = tid >> 1; fb < F / 8; fb += 64) {
+          const int f0 = fb * 8;
+          float2 acc[8][4] = {};  // (feature, unit pair)
 #pragma unroll 2
-        for (int s = 0; s < kB; ++s) {
-          float x[4];
-          ld_x4(xs, F, s, f0, x);
-          const float4 d0 = *reinterpret_cast<const float4*>(dhs + s * kHS + hq);
-          const float4 d1 = *reinterpret_cast<const float4*>(dhs + s * kHS + hq + 4);
-          const float2 d[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w),
-                               make_float2(d1.x, d1.y), make_float2(d1.z, d1.w)};
+          for (int s = 0; s < kB; ++s) {
+            const uint4 v = *reinterpret_cast<const uint4*>(xs + xoff(F, s, f0));
+            const uint32_t pv[4] = {v.x, v.y, v.z, v.w};
+            const float4 d0 = *reinterpret_cast<const float4*>(dhs + s * kHS + hq);
+            const float4 d1 = *reinterpret_cast<const float4*>(dhs + s * kHS + hq + 4);
+            const float2 d[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w),
+                                 make_float2(d1.x, d1.y), make_float2(d1.z, d1.w)};
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float2 xi = make_float2(x[i], x[i]);
+            for (int i = 0; i < 8; ++i) {
+              const float x = __uint_as_float(i & 1 ? pv[i >> 1] & 0xFFFF0000u : pv[i >> 1] << 16);
+              const float2 xi = make_float2(x, x);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[i][q] = fma2(xi, d[q], acc[i][q]);
+              for (int q = 0; q < 4; ++q) acc[i][q] = fma2(xi, d[q], acc[i][q]);
+            }
           }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float* w = w1s + (f0 + i) * kHS + hq + 2 * q;
+              w[0] = __fmaf_rn(-lr, acc[i][q].x, w[0]);
+              w[1] = __fmaf_rn(-lr, acc[i][q].y, w[1]);
+            }
+        }
+      } else {
+        const int u2 = tid - 128;  // 0..127: W2 elements u2 and u2 + 128
+        float aw[2] = {0.0f, 0.0f}, ab = 0.0f;
+        const int kl0 = u2 / C, kl1 = (u2 + 128) / C, cw = u2 % C;
+#pragma unroll 8
+        for (int s = 0; s < kB; ++s) {
+          const float z0 = zs[s * kHS + kl0], z1 = zs[s * kHS + kl1], g = dls[s * C + cw];
+          aw[0] = __fmaf_rn(z0 > 0.0f ? z0 : 0.0f, g, aw[0]);
+          aw[1] = __fmaf_rn(z1 > 0.0f ? z1 : 0.0f, g, aw[1]);
+          if (u2 < C) ab = __fadd_rn(ab, g);
+          else if (u2 >= 32 && u2 < 32 + kHS) ab = __fadd_rn(ab, dhs[s * kHS + u2 - 32]);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float* w = w1s + (f0 + i) * kHS + hq + 2 * q;
-            w[0] = __fmaf_rn(-lr, acc[i][q].x, w[0]);
-            w[1] = __fmaf_rn(-lr, acc[i][q].y, w[1]);
-          }
+        for (int e = 0; e < 2; ++e) {
+          const int k = h0 + (e ? kl1 : kl0);
+          const float w = __fmaf_rn(-lr, aw[e], w2s[k * CP + cw]);
+          const uint32_t wa = w2_a + (uint32_t)((k * CP + cw) * 4);
+          for (uint32_t d = 0; d < (uint32_t)NC; ++d) st_cluster_f32(mapa_shared(wa, d), w);
+        }
+        if (u2 < C) b2s[u2] = __fmaf_rn(-lr, ab, b2s[u2]);
+        else if (u2 >= 32 && u2 < 32 + kHS) b1s[u2 - 32] = __fmaf_rn(-lr, ab, b1s[u2 - 32]);
       }
       if (r == 0 && tid == 64 && ((t + 1) % nsteps == 0)) {  // the micro-window's last step loss
         double s = 0.0;
