@@ -223,11 +223,103 @@ __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* 
   }
 }
 
+// Wide-grid form: 64 rows x 128 hidden units per block of 128 threads, 8
+// rows x 8 units per thread (8 + 8 operands from shared memory per 64 FMAs:
+// the 1 B/FMA the FFMA pipe sustains, where the 4 x 8 tile above needs 1.5),
+// packed fma.rn.f32x2 pairs along the units (each lane an fmaf chain, f
+// ascending from 0, b1 added last: the oracle's order), the next K tile
+// loaded into registers while this one computes.
+__global__ void __launch_bounds__(128) k_l_hidden_ffma8(LDims g, const uint16_t* xbase,
+                                                        const int64_t* row_off,
+                                                        const int* blk_slot, Gate gate,
+                                                        const float* wbase, size_t n_params,
+                                                        float* Z) {
+  constexpr int HB = 128;
+  const int blk = blockIdx.x;
+  if (!gate.live_row((size_t)blk * kRB)) return;
+  const int h0 = blockIdx.y * HB;
+  const float* W1 = wbase + (size_t)blk_slot[blk] * n_params;
+  const float* b1 = W1 + (size_t)g.F * g.H;
+  __shared__ __align__(16) float As[kKT][kRB];  // [k][row]
+  __shared__ __align__(16) float Bs[kKT][HB];   // [k][unit]
+  __shared__ int64_t rows[kRB];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // units 8 tx.., rows 8 ty..
+  if (tid < kRB) rows[tid] = row_off[(size_t)blk * kRB + tid];
+  __syncthreads();
+  // per K tile: X 64 rows x 32 k (bf16 pairs: 1024 words, 8 per thread),
+  // W1 32 k x 128 units (1024 float4, 8 per thread)
+  uint32_t xr[8];
+  float4 wr[8];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // a thread keeps one row (L1 hits), lanes cover rows
+      const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;
+      xr[u] = *reinterpret_cast<const uint32_t*>(xbase + rows[r] + k0 + kk);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * 128, kk = e >> 5, c4 = (e & 31) * 4;
+      wr[u] = *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + kk) * g.H + h0 + c4);
+    }
+  };
+  float2 acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = make_float2(0.0f, 0.0f);
+  fetch(0);
+  for (int k0 = 0; k0 < g.F; k0 += kKT) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;  // (conflict-free stores)
+      As[kk][r] = __uint_as_float(xr[u] << 16);
+      As[kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
+      const int kw = e >> 5, c4 = (e & 31) * 4;
+      *reinterpret_cast<float4*>(&Bs[kw][c4]) = wr[u];
+    }
+    __syncthreads();
+    if (k0 + kKT < g.F) fetch(k0 + kKT);
+#pragma unroll 4
+    for (int kk = 0; kk < kKT; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8]);
+      const float4 b1v = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8 + 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                           make_float2(b1v.x, b1v.y), make_float2(b1v.z, b1v.w)};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 ai = make_float2(a[i], a[i]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[i][q] = __ffma2_rn(ai, b[q], acc[i][q]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const size_t r = (size_t)blk * kRB + ty * 8 + i;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int h = h0 + tx * 8 + 2 * q;
+      *reinterpret_cast<float2*>(Z + r * g.H + h) =
+          make_float2(__fadd_rn(acc[i][q].x, b1[h]), __fadd_rn(acc[i][q].y, b1[h + 1]));
+    }
+  }
+}
+
 // Launches the hidden layer with the widest tile that still fills the GPU.
 static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint16_t* xbase,
                                const int64_t* row_off, const int* blk_slot, Gate gate,
                                const float* wbase, size_t n_params, float* Z) {
-  if ((long)nb * (g.H / kHB) >= 2 * 148)
+  // ECCO_FFMA_HIDDEN8: 0 never, 1 always (tests), unset: wide grids only
+  const char* e = getenv("ECCO_FFMA_HIDDEN8");
+  const bool h8 = e ? e[0] == '1' : (long)nb * (g.H / kHB) >= 8 * 148;
+  if (h8 && g.H % 128 == 0 && g.F % kKT == 0)
+    k_l_hidden_ffma8<<<dim3(nb, g.H / 128), 128, 0, ctx->stream>>>(g, xbase, row_off, blk_slot, gate,
+                                                                    wbase, n_params, Z);
+  else if ((long)nb * (g.H / kHB) >= 2 * 148)
     k_l_hidden_ffma<kHB><<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(g, xbase, row_off, blk_slot,
                                                                        gate, wbase, n_params, Z);
   else

@@ -91,3 +91,25 @@ def test_ffma_chain_other_cluster_sizes(hidden, feat, monkeypatch):
     for w, w2 in zip(weights, weights2):
         for a, b in zip(w, w2):
             assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("wide", ["1", "0"])
+def test_ffma_eval_matrix_hidden_tiles_bit_exact(wide, monkeypatch):
+    """The FFMA evaluation matrix with the 8 x 8 per-thread hidden tile
+    (k_l_hidden_ffma8, forced on) and with the 4 x 8 one: both equal the
+    oracle's counts bit for bit."""
+    monkeypatch.setenv("ECCO_FFMA_HIDDEN8", wide)
+    ctx, orc, _ = setup(seed=44, **BENCH)
+    ids = [2, 5, 6]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members, fracs = [[0, 1], [2, 3], [4, 5]], [[0.5, 0.5]] * 3
+    batches = [(30.0, 1080.0, 1.0)] * 3
+    ctx.train_trajectories(ids, batches, members, fracs, members, 1.0, 1, window=3)
+    orc.trajectories(ids, batches, members, fracs, members, 1.0, 1)
+    ctx.commit(ids, [1, 1, 1])
+    orc.commit(ids, [1, 1, 1])
+    M = ctx.eval_matrix(ids, cams=np.arange(6))
+    W = np.array([[orc.count(orc.models[j], c) / 64 for j in ids] for c in range(6)])
+    assert M.tobytes() == W.tobytes()
