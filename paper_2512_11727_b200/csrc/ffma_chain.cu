@@ -22,16 +22,17 @@
 // Cluster of H/16 CTAs (16 for H = 256: a non-portable cluster); CTA r owns
 // hidden units [16r, 16r+16) and rows [r RP, r RP + RP) (RP = 128 / cluster):
 //   smem    X (the step's 128 sampled rows, bf16, 16-byte chunks XOR-swizzled
-//           by row pair), the fp32 W1 master slice [F][16] (resident for the
+//           by row quad), the fp32 W1 master slice [F][16] (resident for the
 //           whole micro-window), a full copy of W2 (rows padded to C + 1:
 //           conflict-free both along k and along c), b1 slice, b2, the own
 //           pre-activations Z[128][16], and the exchange buffers below
-//   step    gather X (cp.async) -> Z of own units (FFMA, 2 rows x 4 units per
-//           thread) -> relu rows to the row owners (DSMEM) -> cluster barrier
+//   step    gather X (cp.async) -> Z of own units (FFMA, 4 rows x 4 units per
+//           thread, warps 0-3) -> relu rows to the row owners (DSMEM) -> cluster barrier
 //           -> owner: logits of its rows over all H, softmax, dL (to every
 //           CTA), dH of its rows for all units (to each unit's CTA), row
 //           losses (to CTA 0) -> cluster barrier -> own W2 rows (to every
-//           CTA's copy), b2, b1, W1 (FFMA, 4 features x 8 units per thread)
+//           CTA's copy), b2, b1 (warps 4-7) beside W1 (FFMA, 8 features x 8
+//           units per thread, warps 0-3)
 // Two cluster barriers per step; everything else is CTA-local.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -78,14 +79,14 @@ struct FfmaArgs {
 };
 
 struct FLayout {
-  uint32_t x, w1, w2, b1, b2, z, rrecv, dl, dh, lown, loss, total;
+  uint32_t x, w1, w2, b1, b2, z, rrecv, dl, dh, lown, loss, rows, total;
 };
 
 __host__ __device__ inline FLayout flayout(int F, int H, int nc) {
   FLayout L{};
   const int rp = kB / nc;
   uint32_t o = 0;
-  L.x = o;  // [128][F] bf16, 16-byte chunk j of row s at j ^ ((s >> 1) & 7)
+  L.x = o;  // [128][F] bf16, 16-byte chunk j of row s at j ^ ((s >> 2) & 7)
   o += (uint32_t)kB * F * 2u;
   L.w1 = o;  // [F][16] fp32
   o += (uint32_t)F * kHS * 4u;
@@ -108,6 +109,8 @@ __host__ __device__ inline FLayout flayout(int F, int H, int nc) {
   o += (uint32_t)rp * kC * 4u;
   L.loss = o;  // [128] row losses (CTA 0)
   o += kB * 4u;
+  L.rows = o;  // [2][128] frame-table rows of this step and the next
+  o += 2u * kB * 4u;
   L.total = o;
   return L;
 }
@@ -123,7 +126,7 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, f
 
 // Byte offset of bf16 element (s, f) in the swizzled X tile (row = F * 2 bytes).
 __device__ __forceinline__ uint32_t xoff(int F, int s, int f) {
-  const uint32_t chunk = (uint32_t)(f >> 3) ^ (uint32_t)((s >> 1) & 7);
+  const uint32_t chunk = (uint32_t)(f >> 3) ^ (uint32_t)((s >> 2) & 7);
   return (uint32_t)s * (uint32_t)F * 2u + (chunk << 4) + (uint32_t)(f & 7) * 2u;
 }
 
@@ -138,10 +141,18 @@ __device__ __forceinline__ void ld_x4(const uint8_t* xs, int F, int s, int f, fl
 
 // [step][point] clock64 of CTA 0, steps 0-3 (ECCO_FFMA_TRACE)
 __device__ long long g_ffma_trace[4 * 16];
+// (compiled in only with -DECCO_FFMA_TRACE_BUILD: the clock reads stall the
+// warp that takes them, measurably, even when the stamp is not stored)
+#ifdef ECCO_FFMA_TRACE_BUILD
 #define FTS(k)                                                                              \
   do {                                                                                      \
     if (a.trace && blockIdx.x == 0 && tid == 0 && t < 4) g_ffma_trace[t * 16 + (k)] = clock64(); \
   } while (0)
+#else
+#define FTS(k) \
+  do {         \
+  } while (0)
+#endif
 
 // Packed FP32 FMA (fma.rn.f32x2, sm_100): two IEEE fmaf in one instruction.
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
@@ -165,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
   float* dhs = reinterpret_cast<float*>(smem + L.dh);
   float* lown = reinterpret_cast<float*>(smem + L.lown);
   float* lossv = reinterpret_cast<float*>(smem + L.loss);
+  int32_t* rowbuf = reinterpret_cast<int32_t*>(smem + L.rows);
 
   const uint32_t r = cluster_ctarank();
   const int j = blockIdx.x / NC;
@@ -193,7 +205,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
   for (int t = 0; t < total; ++t) {
     const int u = t / (nsteps > 0 ? nsteps : 1);
     const size_t rstep = (size_t)j * a.rows_T + a.row_step0 + t;
-    const int32_t* rows = a.rows + rstep * kB;
+    // this step's frame-table rows were staged in shared memory during the
+    // previous step (the first step's here); the next step's are staged now
+    // and used after the end-of-step barrier
+    const int32_t* rows = rowbuf + (t & 1) * kB;
+    if (t == 0) {
+      if (tid < kB) rowbuf[tid] = a.rows[rstep * kB + tid];
+      __syncthreads();
+    }
+
     // ------------------------------------------------------ gather X --
     FTS(0);
     {
@@ -207,48 +227,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
     __syncthreads();
     // ------------------------------ Z = X.W1 + b1 of the own 16 units --
     FTS(1);
-    // warp w: units [4 (w % 4), +4) (warp-uniform: the W1 loads broadcast),
-    // rows 64 (w / 4) + 2 lane + {0, 1}; 8 features per iteration, X by one
-    // 16-byte load per row (the (s >> 1) & 7 chunk swizzle keeps each
-    // quarter-warp's 8 rows on distinct banks)
-    float acc[2][4];
-    const int hq = (warp & 3) * 4, s0 = (warp >> 2) * 64 + 2 * lane;
-    {
-      float2 ac[2][2] = {};  // (row, unit pair): fma.rn.f32x2, each lane an fmaf chain
+    // warps 0-3: warp w owns units [4w, 4w+4) (warp-uniform: the W1 loads
+    // broadcast), lane l rows 4l..4l+3; 8 features per iteration, X by one
+    // 16-byte load per row (the (s >> 2) & 7 chunk swizzle keeps each
+    // quarter-warp's 8 rows on distinct banks).  4 x 4 outputs per thread:
+    // ~1.5 B of shared memory per FMA, the least a 128-thread tile needs.
+    if (warp >= 4 && t + 1 < total)  // (idle in the forward) the next step's rows
+      rowbuf[((t + 1) & 1) * kB + tid - 128] = a.rows[(rstep + 1) * kB + tid - 128];
+    if (warp < 4) {
+      const int hq = warp * 4, s0 = 4 * lane;
+      float2 ac[4][2] = {};  // (row, unit pair): fma.rn.f32x2, each lane an fmaf chain
 #pragma unroll 2
       for (int f = 0; f < F; f += 8) {
-        const uint4 va = *reinterpret_cast<const uint4*>(xs + xoff(F, s0, f));
-        const uint4 vb = *reinterpret_cast<const uint4*>(xs + xoff(F, s0 + 1, f));
-        const uint32_t pa[4] = {va.x, va.y, va.z, va.w}, pb[4] = {vb.x, vb.y, vb.z, vb.w};
+        uint32_t px[4][4];
+#pragma unroll
+        for (int r4 = 0; r4 < 4; ++r4) {
+          const uint4 v = *reinterpret_cast<const uint4*>(xs + xoff(F, s0 + r4, f));
+          px[r4][0] = v.x;
+          px[r4][1] = v.y;
+          px[r4][2] = v.z;
+          px[r4][3] = v.w;
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float x0 = __uint_as_float(i & 1 ? pa[i >> 1] & 0xFFFF0000u : pa[i >> 1] << 16);
-          const float x1 = __uint_as_float(i & 1 ? pb[i >> 1] & 0xFFFF0000u : pb[i >> 1] << 16);
           const float4 w = *reinterpret_cast<const float4*>(w1s + (f + i) * kHS + hq);
           const float2 wa = make_float2(w.x, w.y), wb = make_float2(w.z, w.w);
-          const float2 xa = make_float2(x0, x0), xb = make_float2(x1, x1);
-          ac[0][0] = fma2(xa, wa, ac[0][0]);
-          ac[0][1] = fma2(xa, wb, ac[0][1]);
-          ac[1][0] = fma2(xb, wa, ac[1][0]);
-          ac[1][1] = fma2(xb, wb, ac[1][1]);
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4) {
+            const uint32_t pw = px[r4][i >> 1];
+            const float x = __uint_as_float(i & 1 ? pw & 0xFFFF0000u : pw << 16);
+            const float2 xx = make_float2(x, x);
+            ac[r4][0] = fma2(xx, wa, ac[r4][0]);
+            ac[r4][1] = fma2(xx, wb, ac[r4][1]);
+          }
         }
       }
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        acc[i][0] = ac[i][0].x;
-        acc[i][1] = ac[i][0].y;
-        acc[i][2] = ac[i][1].x;
-        acc[i][3] = ac[i][1].y;
-      }
-    }
-    {
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < 4; ++i) {
         const int s = s0 + i;
         float z[4], rl[4];
+        const float av[4] = {ac[i][0].x, ac[i][0].y, ac[i][1].x, ac[i][1].y};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          z[q] = __fadd_rn(acc[i][q], b1s[hq + q]);
+          z[q] = __fadd_rn(av[q], b1s[hq + q]);
           rl[q] = z[q] > 0.0f ? z[q] : 0.0f;
         }
         *reinterpret_cast<float4*>(zs + s * kHS + hq) = make_float4(z[0], z[1], z[2], z[3]);

@@ -24,7 +24,13 @@ wide_eval() {  # k_eval_wide (X streamed beside the model): odd shape, pairs mod
     run $tool wide_eval 1500 $PYT tests/test_gpu_wide_eval.py -k "logits and odd or pairs_equal or regime and 2"
   done
 }
+ffma_chain() {  # the fused FP32 chain (DSMEM exchanges, cluster barriers) and the 8 x 8 FFMA GEMM
+  for tool in memcheck synccheck racecheck; do
+    run $tool ffma_chain 1500 $PYT tests/test_gpu_ffma_chain.py -k "unequal or serial or hidden_tiles and 1"
+  done
+}
 [ "${SANITIZE_ONLY:-}" = "wide_eval" ] && { : > "$SUM"; wide_eval; cat "$SUM"; exit 0; }
+[ "${SANITIZE_ONLY:-}" = "ffma_chain" ] && { : > "$SUM"; ffma_chain; cat "$SUM"; exit 0; }
 for tool in memcheck synccheck racecheck; do
   run $tool smoke 900 python __graft_entry__.py
 done
@@ -35,4 +41,5 @@ for tool in memcheck synccheck; do
   run $tool sim 900 $PYT tests/test_gpu_sim.py -k "c1_ten or drift_recovery"
 done
 wide_eval
+ffma_chain
 cat "$SUM"
