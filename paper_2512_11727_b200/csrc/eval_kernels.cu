@@ -769,7 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars->w2_full[b], 1);
       mbar_init(&bars->w2_empty[b], 1);    // the layer-2 MMA commit
       mbar_init(&bars->bias_full[b], 32);  // the producer warp's lanes
-      mbar_init(&bars->bias_empty[b], 8);  // every epilogue warp: b1 read, and b2 by the logits warps
+      mbar_init(&bars->bias_empty[b], 256);  // every epilogue thread: b1 read, and b2 by the logits warps
       mbar_init(&bars->z_full[b], 1);
       mbar_init(&bars->z_empty[b], 8);
       mbar_init(&bars->r_full[b], 8);
@@ -953,9 +953,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&bars->r_full[zb]);
           }
         }
-        if (cp != 0) {  // this warp's last b1 read of the entry is done
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars->bias_empty[bb]);
+        if (cp != 0) {  // this thread's last b1 read of the entry is done
+          mbar_arrive(&bars->bias_empty[bb]);
           continue;
         }
         const int slot = a.ent_slot[e];
@@ -981,10 +980,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&bars->l_empty[lb]);
-          mbar_arrive(&bars->bias_empty[bb]);  // b1 (all halves done) and b2 no longer read
-        }
+        if (lane == 0) mbar_arrive(&bars->l_empty[lb]);
+        mbar_arrive(&bars->bias_empty[bb]);  // b1 (all halves done) and b2 no longer read
         const bool ok = valid && best == label && (pslot < 0 || pslot == slot);
         const unsigned bal = __ballot_sync(0xffffffffu, ok);
         if (lane == 0 && bal) {

@@ -199,6 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
   }
   __syncthreads();
 
+  // every CTA of the cluster is running before any DSMEM store reaches it
+  cluster_sync();
   const uint32_t rrecv_a = smem_u32(rrecv), dl_a = smem_u32(dls), dh_a = smem_u32(dhs);
   const uint32_t loss_a = smem_u32(lossv), w2_a = smem_u32(w2s);
   const int total = nsteps * a.n_micro_launch;
