@@ -638,9 +638,8 @@ def run_e2e(args, retr, wl, torch, dist):
             with torch.cuda.stream(retr.stream):
                 best_host.copy_(retr.best, non_blocking=True)  # group assignments to the host
             retr.stream.synchronize()
-        else:
-            retr.retrain(w, mid=swap)
-            stage_next()
+        else:  # (no regroup matrix) window w+1's staging overlaps the greedy's chains
+            retr.retrain(w, mid=swap, after_initial=stage_next)
         return time.perf_counter() - t0, retr.stats["committed_samples"]
 
     # pipeline fill + one untimed warm-up window through the same ingest path
