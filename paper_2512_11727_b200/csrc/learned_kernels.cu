@@ -224,12 +224,12 @@ __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* 
 }
 
 // Wide-grid form: 64 rows x 128 hidden units per block of 128 threads, 8
-// rows x 8 units per thread (8 + 8 operands from shared memory per 64 FMAs:
+// rows x 8 units (two groups of 4) per thread (8 + 8 operands from shared memory per 64 FMAs:
 // the 1 B/FMA the FFMA pipe sustains, where the 4 x 8 tile above needs 1.5),
 // packed fma.rn.f32x2 pairs along the units (each lane an fmaf chain, f
 // ascending from 0, b1 added last: the oracle's order), the next K tile
 // loaded into registers while this one computes.
-__global__ void __launch_bounds__(128) k_l_hidden_ffma8(LDims g, const uint16_t* xbase,
+__global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16_t* xbase,
                                                         const int64_t* row_off,
                                                         const int* blk_slot, Gate gate,
                                                         const float* wbase, size_t n_params,
@@ -283,8 +283,10 @@ __global__ void __launch_bounds__(128) k_l_hidden_ffma8(LDims g, const uint16_t*
     for (int kk = 0; kk < kKT; ++kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8]);
-      const float4 b1v = *reinterpret_cast<const float4*>(&Bs[kk][tx * 8 + 4]);
+      // units 4 tx..4 tx+3 and 64 + 4 tx..: lanes at a 16-byte stride (no
+      // bank conflict; a 32-byte stride would conflict 2-way)
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float4 b1v = *reinterpret_cast<const float4*>(&Bs[kk][64 + tx * 4]);
       const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
                            make_float2(b1v.x, b1v.y), make_float2(b1v.z, b1v.w)};
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(128) k_l_hidden_ffma8(LDims g, const uint16_t*
     const size_t r = (size_t)blk * kRB + ty * 8 + i;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int h = h0 + tx * 8 + 2 * q;
+      const int h = h0 + (q < 2 ? tx * 4 + 2 * q : 64 + tx * 4 + 2 * (q - 2));
       *reinterpret_cast<float2*>(Z + r * g.H + h) =
           make_float2(__fadd_rn(acc[i][q].x, b1[h]), __fadd_rn(acc[i][q].y, b1[h + 1]));
     }
