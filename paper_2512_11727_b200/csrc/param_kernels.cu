@@ -240,7 +240,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_p_trajectories(
   __shared__ uint64_t s_tab[256];
   __shared__ double s_model[kWarpsPerBlock][kModelDoubles];
   __shared__ double s_acc[kWarpsPerBlock][32];
-  __shared__ int s_kc[kWarpsPerBlock][2];
+  __shared__ int s_kc[kWarpsPerBlock][4];
+  __shared__ int s_best[kWarpsPerBlock][32];
+  __shared__ double s_w[kWarpsPerBlock][ECCO_PMAX_K];
   load_tab(s_tab);
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
   const int j = blockIdx.x * kWarpsPerBlock + w;
@@ -263,17 +265,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) k_p_trajectories(
   const double effort = p_effort(batch[3 * j], batch[3 * j + 1], batch[3 * j + 2], gpu_s, ns,
                                  src_cam + s0, t.cam_tp);
   for (int step = 1; step <= depth; ++step) {
-    if (lane == 0) {
-      int kk = k, cc = clen;
-      const int rc = p_train_step(&kk, cl, prof, &cc, cen, K, d, effort, ns, src_cam + s0,
-                                  src_frac + s0, t.cam_scenes, t.m.p, s_tab);
-      if (rc) atomicMax(t.status, rc);
-      s_kc[w][0] = kk;
-      s_kc[w][1] = cc;
-    }
+    // the step on the whole warp (p_train_step_warp: lookups on the lanes)
+    const int rc = p_train_step_warp(&k, cl, prof, &clen, cen, K, d, effort, ns, src_cam + s0,
+                                     src_frac + s0, t.cam_scenes, t.m.p, s_tab, s_best[w],
+                                     s_acc[w], s_w[w], s_kc[w]);
+    if (rc && lane == 0) atomicMax(t.status, rc);
     __syncwarp();
-    k = s_kc[w][0];
-    clen = s_kc[w][1];
     store_state(t, slot, step, k, clen, cl, prof, cen);
     out[(size_t)j * (depth + 1) + step] = warp_mean_eval(k, cl, prof, clen, cen, d, t.m.p, nm,
                                                          mem_cam + m0, t.cam_scenes, s_acc[w], s_tab);

@@ -149,6 +149,104 @@ __device__ __forceinline__ double p_effort(double fps, double res, double qualit
   return __dmul_rn(__dmul_rn(gpu_s, suff), quality);
 }
 
+// p_train_step on a whole warp (same results bit for bit): the sources'
+// cluster lookups against the clusters that exist at the step's start run
+// on the lanes (one source each); lane 0 then walks the sources in map
+// order, continuing each lookup over the clusters appended earlier in the
+// step (the same ascending-c, strict-'>' sequence of comparisons as
+// p_find_cluster), appending, and accumulating weights and the centroid;
+// the per-cluster proficiency updates run on the lanes again.  Scratch:
+// s_best / s_bsim [32], s_w [kmax] weights, s_kc [4] (k, rc, have_cen,
+// touched mask; kmax <= 32).  Returns 0 or 2 (cluster capacity) on every
+// lane; k / clen are updated on every lane.
+__device__ __forceinline__ int p_train_step_warp(int* k, double* cl, double* prof, int* clen,
+                                                 double* cen, int kmax, int d, double effort,
+                                                 int n_src, const int* src_cam,
+                                                 const double* src_frac, const double* cam_scenes,
+                                                 const PParams& p, const uint64_t* tab, int* s_best,
+                                                 double* s_bsim, double* s_w, int* s_kc) {
+  if (!(effort > 0.0)) return 0;
+  const int lane = threadIdx.x & 31;
+  const int k0 = *k;
+  for (int c = lane; c < kmax; c += 32) s_w[c] = 0.0;
+  if (lane == 0) {
+    s_kc[0] = k0;
+    s_kc[1] = 0;  // rc
+    s_kc[2] = 0;  // have_cen
+    s_kc[3] = 0;  // touched clusters (bit c)
+  }
+  double acc_cen[ECCO_PMAX_D];
+  for (int j = 0; j < d; ++j) acc_cen[j] = 0.0;
+  __syncwarp();
+  for (int base = 0; base < n_src; base += 32) {
+    const int i = base + lane;
+    int b = -1;
+    double bs = 0.0;
+    if (i < n_src) {
+      const double* sc = cam_scenes + (size_t)src_cam[i] * d;
+      for (int c = 0; c < k0; ++c) {
+        const double sv = p_similarity(cl + c * d, sc, d, p, tab);
+        if (sv > bs) {
+          bs = sv;
+          b = c;
+        }
+      }
+    }
+    s_best[lane] = b;
+    s_bsim[lane] = bs;
+    __syncwarp();
+    if (lane == 0 && s_kc[1] == 0) {
+      int kk = s_kc[0];
+      const int cnt = n_src - base < 32 ? n_src - base : 32;
+      for (int t = 0; t < cnt; ++t) {
+        const int ii = base + t;
+        const double* sc = cam_scenes + (size_t)src_cam[ii] * d;
+        int bb = s_best[t];
+        double bsv = s_bsim[t];
+        for (int c = k0; c < kk; ++c) {  // clusters appended earlier in this step
+          const double sv = p_similarity(cl + c * d, sc, d, p, tab);
+          if (sv > bsv) {
+            bsv = sv;
+            bb = c;
+          }
+        }
+        int c = (bb >= 0 && bsv >= p.thr) ? bb : -1;
+        if (c < 0) {
+          if (kk >= kmax) {
+            s_kc[1] = 2;
+            break;
+          }
+          for (int j = 0; j < d; ++j) cl[kk * d + j] = sc[j];
+          prof[kk] = 0.0;
+          c = kk++;
+        }
+        s_w[c] = __dadd_rn(s_w[c], src_frac[ii]);
+        s_kc[3] = (int)((unsigned)s_kc[3] | (1u << c));
+        s_kc[2] = 1;
+        for (int j = 0; j < d; ++j) acc_cen[j] = __dadd_rn(acc_cen[j], __dmul_rn(src_frac[ii], sc[j]));
+      }
+      s_kc[0] = kk;
+    }
+    __syncwarp();
+  }
+  *k = s_kc[0];
+  const int rc = s_kc[1];
+  if (rc) return rc;
+  for (int c = lane; c < *k; c += 32) {  // proficiencies of the touched clusters
+    const double w = s_w[c];
+    if (!(((unsigned)s_kc[3] >> c) & 1u) || w <= 0.0) continue;
+    const double pr = prof[c];
+    const double e = ecco_exp_tab(__dmul_rn(__dmul_rn(-p.k, effort), w), tab);
+    prof[c] = __dsub_rn(1.0, __dmul_rn(__dsub_rn(1.0, pr), e));
+  }
+  if (lane == 0 && s_kc[2]) {
+    for (int j = 0; j < d; ++j) cen[j] = acc_cen[j];
+  }
+  __syncwarp();
+  if (s_kc[2]) *clen = d;
+  return 0;
+}
+
 // train_step body after validation: accuracy_model.cpp:86-110.  The model
 // (cl: kmax*d, prof: kmax) is updated in place.  Returns 0, or 2 when a new
 // cluster would exceed kmax.
