@@ -870,8 +870,9 @@ ecco_status ecco_eval_matrix_dev(ecco_ctx* ctx, int n, const double* scenes, con
 ecco_status ecco_eval_matrix_dev_async(ecco_ctx* ctx, int n, const int* cam_idx, int g,
                                        const int* job_ids, void* out_dev, int reserve_sms) {
   return guarded(ctx, [&] {
-    ECCO_REQUIRE(learned(ctx) && ctx->fused_eval,
-                 "eval_matrix_dev_async: learned backend with tensor-core math");
+    const bool exact = learned(ctx) && !ctx->fused_eval && ctx->cfg.math == ECCO_MATH_FFMA_EXACT;
+    ECCO_REQUIRE(learned(ctx) && (ctx->fused_eval || exact),
+                 "eval_matrix_dev_async: learned backend with fused tensor-core or FFMA_EXACT math");
     ECCO_REQUIRE(reserve_sms >= 0, "eval_matrix_dev_async: reserve_sms must be >= 0");
     if (n == 0 || g == 0) return;
     if (!ctx->matrix_stream) {
@@ -882,7 +883,16 @@ ecco_status ecco_eval_matrix_dev_async(ecco_ctx* ctx, int n, const int* cam_idx,
     // the committed models' evaluation shadows are rebuilt on the CONTEXT
     // stream first: the chains that run meanwhile evaluate from the same
     // shadows, and must not see one half rebuilt by the matrix stream
-    {
+    // (FFMA_EXACT evaluates the fp32 masters themselves: the matrix reads a
+    // copy taken here, so commits on the context stream meanwhile -- the
+    // greedy's extended groups, whose columns the caller re-evaluates --
+    // never race with its reads)
+    float* wread = ctx->d_w;
+    if (exact) {
+      const size_t bytes = sizeof(float) * (size_t)ctx->cfg.max_jobs * ctx->n_params;
+      wread = (float*)ctx->side_w.get(bytes);
+      ECCO_CUDA(cudaMemcpyAsync(wread, ctx->d_w, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
       auto s = slots_of(ctx, g, job_ids);
       lbackend::refresh_models(ctx, s.data(), g);
     }
@@ -898,18 +908,22 @@ ecco_status ecco_eval_matrix_dev_async(ecco_ctx* ctx, int n, const int* cam_idx,
       std::swap(ctx->tile_ctr, ctx->side_tile_ctr);
     };
     swap_side();
+    float* const w_main = ctx->d_w;
     ctx->stream = ctx->matrix_stream;
     ctx->reserve_sms = reserve_sms;
+    ctx->d_w = wread;
     try {
       eval_matrix_impl(ctx, n, nullptr, cam_idx, g, job_ids, nullptr, (double*)out_dev);
     } catch (...) {
       ctx->stream = main_stream;
       ctx->reserve_sms = 0;
+      ctx->d_w = w_main;
       swap_side();
       throw;
     }
     ctx->stream = main_stream;
     ctx->reserve_sms = 0;
+    ctx->d_w = w_main;
     swap_side();
     ECCO_CUDA(cudaEventRecord(ctx->ev_matrix_done, ctx->matrix_stream));
   });

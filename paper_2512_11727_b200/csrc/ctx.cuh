@@ -226,6 +226,7 @@ struct ecco_ctx {
   cudaStream_t matrix_stream = nullptr;
   cudaEvent_t ev_matrix_in = nullptr, ev_matrix_done = nullptr;
   DevBuf side_scratch[20], side_em_args[3], side_tile_ctr;
+  DevBuf side_w;  // FFMA_EXACT: the committed masters the async matrix reads
   int reserve_sms = 0;
   unsigned long long* d_zc_rows = nullptr;
 

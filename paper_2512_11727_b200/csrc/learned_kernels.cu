@@ -229,23 +229,27 @@ __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* 
 // packed fma.rn.f32x2 pairs along the units (each lane an fmaf chain, f
 // ascending from 0, b1 added last: the oracle's order), the next K tile
 // loaded into registers while this one computes.
-__global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16_t* xbase,
-                                                        const int64_t* row_off,
-                                                        const int* blk_slot, Gate gate,
-                                                        const float* wbase, size_t n_params,
-                                                        float* Z) {
+// One 64-row x 128-unit tile (row block blk, unit block hb) on 128 threads
+// (tid 0..127), with its own shared-memory tile and a barrier over those
+// threads only (sync).
+struct H8Smem {
+  float As[kKT][kRB];  // [k][row]
+  float Bs[kKT][128];  // [k][unit]
+  int64_t rows[kRB];
+};
+
+template <typename Sync>
+__device__ __forceinline__ void hidden8_tile(const LDims& g, const uint16_t* xbase,
+                                             const int64_t* row_off, const int* blk_slot,
+                                             const float* wbase, size_t n_params, float* Z,
+                                             int blk, int hb, int tid, H8Smem& sm, Sync sync) {
   constexpr int HB = 128;
-  const int blk = blockIdx.x;
-  if (!gate.live_row((size_t)blk * kRB)) return;
-  const int h0 = blockIdx.y * HB;
+  const int h0 = hb * HB;
   const float* W1 = wbase + (size_t)blk_slot[blk] * n_params;
   const float* b1 = W1 + (size_t)g.F * g.H;
-  __shared__ __align__(16) float As[kKT][kRB];  // [k][row]
-  __shared__ __align__(16) float Bs[kKT][HB];   // [k][unit]
-  __shared__ int64_t rows[kRB];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // units 8 tx.., rows 8 ty..
-  if (tid < kRB) rows[tid] = row_off[(size_t)blk * kRB + tid];
-  __syncthreads();
+  const int tx = tid & 15, ty = tid >> 4;  // units 4 tx.. and 64 + 4 tx.., rows 8 ty..
+  if (tid < kRB) sm.rows[tid] = row_off[(size_t)blk * kRB + tid];
+  sync();
   // per K tile: X 64 rows x 32 k (bf16 pairs: 1024 words, 8 per thread),
   // W1 32 k x 128 units (1024 float4, 8 per thread)
   uint32_t xr[8];
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16
 #pragma unroll
     for (int u = 0; u < 8; ++u) {  // a thread keeps one row (L1 hits), lanes cover rows
       const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;
-      xr[u] = *reinterpret_cast<const uint32_t*>(xbase + rows[r] + k0 + kk);
+      xr[u] = *reinterpret_cast<const uint32_t*>(xbase + sm.rows[r] + k0 + kk);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -272,32 +276,32 @@ __global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;  // (conflict-free stores)
-      As[kk][r] = __uint_as_float(xr[u] << 16);
-      As[kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
+      sm.As[kk][r] = __uint_as_float(xr[u] << 16);
+      sm.As[kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
       const int kw = e >> 5, c4 = (e & 31) * 4;
-      *reinterpret_cast<float4*>(&Bs[kw][c4]) = wr[u];
+      *reinterpret_cast<float4*>(&sm.Bs[kw][c4]) = wr[u];
     }
-    __syncthreads();
+    sync();
     if (k0 + kKT < g.F) fetch(k0 + kKT);
 #pragma unroll 4
     for (int kk = 0; kk < kKT; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+      const float4 a0 = *reinterpret_cast<const float4*>(&sm.As[kk][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&sm.As[kk][ty * 8 + 4]);
       // units 4 tx..4 tx+3 and 64 + 4 tx..: lanes at a 16-byte stride (no
       // bank conflict; a 32-byte stride would conflict 2-way)
-      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
-      const float4 b1v = *reinterpret_cast<const float4*>(&Bs[kk][64 + tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
-                           make_float2(b1v.x, b1v.y), make_float2(b1v.z, b1v.w)};
+      const float4 b0 = *reinterpret_cast<const float4*>(&sm.Bs[kk][tx * 4]);
+      const float4 b1v = *reinterpret_cast<const float4*>(&sm.Bs[kk][64 + tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                            make_float2(b1v.x, b1v.y), make_float2(b1v.z, b1v.w)};
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float2 ai = make_float2(a[i], a[i]);
+        const float2 ai = make_float2(av[i], av[i]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[i][q] = __ffma2_rn(ai, b[q], acc[i][q]);
+        for (int q = 0; q < 4; ++q) acc[i][q] = __ffma2_rn(ai, bv[q], acc[i][q]);
       }
     }
-    __syncthreads();
+    sync();
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -311,6 +315,45 @@ __global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16
   }
 }
 
+// Wide-grid form: 64 rows x 128 hidden units per block of 128 threads, 8
+// rows x 8 units (two groups of 4) per thread (8 + 8 operands from shared
+// memory per 64 FMAs: the 1 B/FMA the FFMA pipe sustains, where the 4 x 8
+// tile above needs 1.5), packed fma.rn.f32x2 pairs along the units (each
+// lane an fmaf chain, f ascending from 0, b1 added last: the oracle's
+// order), the next K tile loaded into registers while this one computes.
+__global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16_t* xbase,
+                                                        const int64_t* row_off,
+                                                        const int* blk_slot, Gate gate,
+                                                        const float* wbase, size_t n_params,
+                                                        float* Z) {
+  __shared__ __align__(16) H8Smem sm;
+  if (!gate.live_row((size_t)blockIdx.x * kRB)) return;
+  hidden8_tile(g, xbase, row_off, blk_slot, wbase, n_params, Z, blockIdx.x, blockIdx.y,
+               threadIdx.x, sm, [] { __syncthreads(); });
+}
+
+// Persistent form for a matrix that runs BESIDE other work (the
+// oracle-exact window's regroup matrix next to the serial chains): one
+// 512-thread block per SM (4 independent 128-thread tile workers, a named
+// barrier each; the padded shared memory keeps a second block off the SM),
+// at most (SMs - reserve) blocks, so the reserved SMs stay whole for the
+// chains' clusters.  Same tiles, same arithmetic.
+constexpr uint32_t kH8PersistentSmem = 120u * 1024u;
+__global__ void __launch_bounds__(512, 1) k_l_hidden_ffma8_persistent(
+    LDims g, const uint16_t* xbase, const int64_t* row_off, const int* blk_slot, Gate gate,
+    const float* wbase, size_t n_params, float* Z, int nb, int nhb) {
+  extern __shared__ __align__(16) uint8_t dsm[];
+  const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;
+  H8Smem& sm = reinterpret_cast<H8Smem*>(dsm)[grp];
+  auto sync = [grp] { asm volatile("bar.sync %0, 128;" ::"r"(grp + 1) : "memory"); };
+  for (long w = (long)blockIdx.x * 4 + grp; w < (long)nb * nhb; w += (long)gridDim.x * 4) {
+    const int blk = (int)(w / nhb), hb = (int)(w % nhb);
+    if (!gate.live_row((size_t)blk * kRB)) continue;
+    hidden8_tile(g, xbase, row_off, blk_slot, wbase, n_params, Z, blk, hb, tid, sm, sync);
+    sync();  // (the next tile's row table overwrites this one's)
+  }
+}
+
 // Launches the hidden layer with the widest tile that still fills the GPU.
 static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint16_t* xbase,
                                const int64_t* row_off, const int* blk_slot, Gate gate,
@@ -318,7 +361,22 @@ static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint
   // ECCO_FFMA_HIDDEN8: 0 never, 1 always (tests), unset: wide grids only
   const char* e = getenv("ECCO_FFMA_HIDDEN8");
   const bool h8 = e ? e[0] == '1' : (long)nb * (g.H / kHB) >= 8 * 148;
-  if (h8 && g.H % 128 == 0 && g.F % kKT == 0)
+  if (h8 && g.H % 128 == 0 && g.F % kKT == 0 && ctx->reserve_sms > 0) {
+    // beside the context stream's chains: persistent, the reserved SMs left whole
+    static DeviceFlags attr;
+    if (!attr.done(ctx->cfg.device)) {
+      ECCO_CUDA(cudaFuncSetAttribute(k_l_hidden_ffma8_persistent,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kH8PersistentSmem));
+      attr.mark(ctx->cfg.device);
+    }
+    int sms = 0;
+    ECCO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device));
+    const long items = (long)nb * (g.H / 128);
+    const int grid = (int)std::max(1L, std::min<long>((items + 3) / 4, sms - ctx->reserve_sms));
+    k_l_hidden_ffma8_persistent<<<grid, 512, kH8PersistentSmem, ctx->stream>>>(
+        g, xbase, row_off, blk_slot, gate, wbase, n_params, Z, nb, g.H / 128);
+  } else if (h8 && g.H % 128 == 0 && g.F % kKT == 0)
     k_l_hidden_ffma8<<<dim3(nb, g.H / 128), 128, 0, ctx->stream>>>(g, xbase, row_off, blk_slot, gate,
                                                                     wbase, n_params, Z);
   else if ((long)nb * (g.H / kHB) >= 2 * 148)
@@ -1023,12 +1081,14 @@ void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const 
   ECCO_LAUNCHED(ctx);
 }
 
-// Counts for a list of (slot, camera) pairs, chunked to bound scratch.
+// Counts for a list of (slot, camera) pairs, chunked to bound scratch (1 GiB
+// of hidden activations per chunk: few, large launches -- a full C4 matrix
+// in ~300 chunks, each a wide grid).
 static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, const int* d_pair_cam,
                         int* d_counts) {
   const LDims g = dims(ctx);
   ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(n_pairs, 1), ctx->stream));
-  const int chunk = std::max(1, (int)std::min<size_t>(n_pairs, (size_t)(256u << 20) / ((size_t)g.S * g.H * 4)));
+  const int chunk = std::max(1, (int)std::min<size_t>(n_pairs, (size_t)(1u << 30) / ((size_t)g.S * g.H * 4)));
   for (int p0 = 0; p0 < n_pairs; p0 += chunk) {
     const int np = std::min(chunk, n_pairs - p0);
     const int rows = np * g.S;

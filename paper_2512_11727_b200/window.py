@@ -33,10 +33,11 @@ the cameras' eval sets; the replay on the gathered trajectories.  So the
 results are bit-identical at 1, 2, ... ranks (tests/test_gpu_multirank.py).
 """
 import math
+import os
 
 import numpy as np
 
-from . import TC_BF16, LEARNED, Context, allocate_trajectories
+from . import FFMA_EXACT, TC_BF16, LEARNED, Context, allocate_trajectories
 from .shard import Placement
 
 
@@ -307,7 +308,19 @@ class GroupRetrainer:
         ingest), mark() once the retrain is committed (phase timing).
         Returns (counts, best group per camera, its accuracy)."""
         torch = self.torch
-        fused = bool(self.local) and self.ctx.cfg.math == TC_BF16
+        # the overlap needs a matrix that can run beside the chains: the
+        # fused tensor-core evaluation, or FFMA_EXACT's persistent GEMM (on a
+        # copy of the committed masters), which leaves whole SMs to the
+        # exact chain's cluster of H/16 CTAs
+        # (on one or two ranks the exact matrix share -- seconds -- dwarfs the
+        # exact chains: keeping SMs from it costs more than the overlap saves;
+        # C4 measured: 1 rank 2.54 s without / 3.01 s with, emulated 2 ranks
+        # 1.38 / 1.46 s, 4 ranks 0.80 / 0.73 s, 8 ranks 0.51 / 0.37 s)
+        math = self.ctx.cfg.math
+        exact_overlap = self.world >= 4 or os.environ.get("ECCO_EXACT_OVERLAP") == "1"
+        fused = bool(self.local) and (math == TC_BF16 or (math == FFMA_EXACT and exact_overlap))
+        if math == FFMA_EXACT:
+            reserve_sms = max(reserve_sms, self.ctx.cfg.hidden_dim // 16)
 
         def launch_matrix():
             if self.local and fused:

@@ -41,7 +41,7 @@ def _layout():
     return groups, scenes, np.full(c, 8.192e6)
 
 
-def _worker(rank, world, port, q, mode="split"):
+def _worker(rank, world, port, q, mode="split", exact=False):
     import torch
     dist = None
     if world > 1:
@@ -50,11 +50,12 @@ def _worker(rank, world, port, q, mode="split"):
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2512_11727_b200 import TC_BF16
+        from paper_2512_11727_b200 import FFMA_EXACT, TC_BF16
         from paper_2512_11727_b200.window import GroupRetrainer
         groups, scenes, tp = _layout()
         r = GroupRetrainer(scenes, tp, groups, rank=rank, world=world, dist=dist, device=0,
-                           math=TC_BF16, depth=2, micro_windows=3 * len(groups),
+                           math=FFMA_EXACT if exact else TC_BF16, depth=2,
+                           micro_windows=3 * len(groups),
                            steps_per_gpu_s=4.0, dims=DIMS)
         out = []
         for w in range(WINDOWS):
@@ -75,12 +76,13 @@ def _worker(rank, world, port, q, mode="split"):
             dist.destroy_process_group()
 
 
-def _spawn(world, mode="split"):
+def _spawn(world, mode="split", exact=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode, exact))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
@@ -117,3 +119,28 @@ def test_two_ranks_bit_identical_to_one(mode):
         for g in local:
             assert weights[g] == one[3][g], g
 
+
+
+def test_exact_window_overlap_bit_identical(monkeypatch):
+    """FFMA_EXACT (the oracle-exact math): the overlapped window -- the
+    persistent FFMA GEMM (forced on) evaluating a copy of the committed
+    masters on the matrix stream beside the exact chains, extended groups
+    re-evaluated -- equals retrain() then regroup(), on 1 and 2 ranks."""
+    monkeypatch.setenv("ECCO_FFMA_HIDDEN8", "1")
+    monkeypatch.setenv("ECCO_EXACT_OVERLAP", "1")  # (the product overlaps from 4 ranks on)
+    one = _spawn(1, "split", exact=True)[0]
+    runs = _spawn(2, "window", exact=True) + _spawn(1, "window", exact=True)
+    ext = 0
+    for w in range(WINDOWS):
+        a = one[2][w]
+        for _, _, out, _ in runs:
+            b = out[w]
+            assert a["best"].tobytes() == b["best"].tobytes(), w
+            assert a["acc"].tobytes() == b["acc"].tobytes(), w
+            assert a["traj"].tobytes() == b["traj"].tobytes(), w
+            assert (a["schedule"] == b["schedule"]).all() and (a["counts"] == b["counts"]).all()
+        ext += a["extensions"]
+    assert ext > 0
+    for _, local, _, weights in runs:
+        for g in local:
+            assert weights[g] == one[3][g], g
