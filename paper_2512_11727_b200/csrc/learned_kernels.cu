@@ -223,20 +223,21 @@ __global__ void __launch_bounds__(256) k_l_hidden_ffma(LDims g, const uint16_t* 
   }
 }
 
-// Wide-grid form: 64 rows x 128 hidden units per block of 128 threads, 8
-// rows x 8 units (two groups of 4) per thread (8 + 8 operands from shared memory per 64 FMAs:
-// the 1 B/FMA the FFMA pipe sustains, where the 4 x 8 tile above needs 1.5),
-// packed fma.rn.f32x2 pairs along the units (each lane an fmaf chain, f
-// ascending from 0, b1 added last: the oracle's order), the next K tile
-// loaded into registers while this one computes.
 // One 64-row x 128-unit tile (row block blk, unit block hb) on 128 threads
 // (tid 0..127), with its own shared-memory tile and a barrier over those
 // threads only (sync).
 struct H8Smem {
-  float As[kKT][kRB];  // [k][row]
-  float Bs[kKT][128];  // [k][unit]
+  float As[2][kKT][kRB];  // [buffer][k][row]
+  float Bs[2][kKT][128];  // [buffer][k][unit]
   int64_t rows[kRB];
 };
+
+__device__ __forceinline__ void h8_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
 
 template <typename Sync>
 __device__ __forceinline__ void hidden8_tile(const LDims& g, const uint16_t* xbase,
@@ -250,47 +251,61 @@ __device__ __forceinline__ void hidden8_tile(const LDims& g, const uint16_t* xba
   const int tx = tid & 15, ty = tid >> 4;  // units 4 tx.. and 64 + 4 tx.., rows 8 ty..
   if (tid < kRB) sm.rows[tid] = row_off[(size_t)blk * kRB + tid];
   sync();
-  // per K tile: X 64 rows x 32 k (bf16 pairs: 1024 words, 8 per thread),
-  // W1 32 k x 128 units (1024 float4, 8 per thread)
+  // per K tile: X 64 rows x 32 k (bf16 pairs, 8 words per thread) through
+  // registers (fp32 conversion and transpose), W1 32 k x 128 units by
+  // cp.async straight into the other buffer; one barrier per K tile
   uint32_t xr[8];
-  float4 wr[8];
-  auto fetch = [&](int k0) {
+  auto fetch_x = [&](int k0) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {  // a thread keeps one row (L1 hits), lanes cover rows
       const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;
       xr[u] = *reinterpret_cast<const uint32_t*>(xbase + sm.rows[r] + k0 + kk);
     }
+  };
+  auto store_x = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;  // (conflict-free stores)
+      sm.As[buf][kk][r] = __uint_as_float(xr[u] << 16);
+      sm.As[buf][kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
+    }
+  };
+  auto fetch_w = [&](int k0, int buf) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = tid + u * 128, kk = e >> 5, c4 = (e & 31) * 4;
-      wr[u] = *reinterpret_cast<const float4*>(W1 + (size_t)(k0 + kk) * g.H + h0 + c4);
+      h8_cp16(&sm.Bs[buf][kk][c4], W1 + (size_t)(k0 + kk) * g.H + h0 + c4);
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   float2 acc[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[i][q] = make_float2(0.0f, 0.0f);
-  fetch(0);
-  for (int k0 = 0; k0 < g.F; k0 += kKT) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;  // (conflict-free stores)
-      sm.As[kk][r] = __uint_as_float(xr[u] << 16);
-      sm.As[kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
-      const int kw = e >> 5, c4 = (e & 31) * 4;
-      *reinterpret_cast<float4*>(&sm.Bs[kw][c4]) = wr[u];
+  fetch_w(0, 0);
+  fetch_x(0);
+  store_x(0);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  sync();
+  const int nkt = g.F / kKT;
+  for (int t = 0; t < nkt; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    const bool more = t + 1 < nkt;
+    if (more) {
+      fetch_w((t + 1) * kKT, nxt);
+      fetch_x((t + 1) * kKT);
     }
-    sync();
-    if (k0 + kKT < g.F) fetch(k0 + kKT);
+    const float(*As)[kRB] = sm.As[cur];
+    const float(*Bs)[128] = sm.Bs[cur];
 #pragma unroll 4
     for (int kk = 0; kk < kKT; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&sm.As[kk][ty * 8]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&sm.As[kk][ty * 8 + 4]);
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
       // units 4 tx..4 tx+3 and 64 + 4 tx..: lanes at a 16-byte stride (no
       // bank conflict; a 32-byte stride would conflict 2-way)
-      const float4 b0 = *reinterpret_cast<const float4*>(&sm.Bs[kk][tx * 4]);
-      const float4 b1v = *reinterpret_cast<const float4*>(&sm.Bs[kk][64 + tx * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float4 b1v = *reinterpret_cast<const float4*>(&Bs[kk][64 + tx * 4]);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
                             make_float2(b1v.x, b1v.y), make_float2(b1v.z, b1v.w)};
@@ -300,6 +315,10 @@ __device__ __forceinline__ void hidden8_tile(const LDims& g, const uint16_t* xba
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[i][q] = __ffma2_rn(ai, bv[q], acc[i][q]);
       }
+    }
+    if (more) {
+      store_x(nxt);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     sync();
   }
@@ -326,7 +345,8 @@ __global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16
                                                         const int* blk_slot, Gate gate,
                                                         const float* wbase, size_t n_params,
                                                         float* Z) {
-  __shared__ __align__(16) H8Smem sm;
+  extern __shared__ __align__(16) uint8_t dsm8[];
+  H8Smem& sm = *reinterpret_cast<H8Smem*>(dsm8);
   if (!gate.live_row((size_t)blockIdx.x * kRB)) return;
   hidden8_tile(g, xbase, row_off, blk_slot, wbase, n_params, Z, blockIdx.x, blockIdx.y,
                threadIdx.x, sm, [] { __syncthreads(); });
@@ -338,7 +358,7 @@ __global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16
 // barrier each; the padded shared memory keeps a second block off the SM),
 // at most (SMs - reserve) blocks, so the reserved SMs stay whole for the
 // chains' clusters.  Same tiles, same arithmetic.
-constexpr uint32_t kH8PersistentSmem = 120u * 1024u;
+constexpr uint32_t kH8PersistentSmem = 4u * (uint32_t)sizeof(H8Smem);  // 4 workers: one block per SM
 __global__ void __launch_bounds__(512, 1) k_l_hidden_ffma8_persistent(
     LDims g, const uint16_t* xbase, const int64_t* row_off, const int* blk_slot, Gate gate,
     const float* wbase, size_t n_params, float* Z, int nb, int nhb) {
@@ -376,9 +396,16 @@ static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint
     const int grid = (int)std::max(1L, std::min<long>((items + 3) / 4, sms - ctx->reserve_sms));
     k_l_hidden_ffma8_persistent<<<grid, 512, kH8PersistentSmem, ctx->stream>>>(
         g, xbase, row_off, blk_slot, gate, wbase, n_params, Z, nb, g.H / 128);
-  } else if (h8 && g.H % 128 == 0 && g.F % kKT == 0)
-    k_l_hidden_ffma8<<<dim3(nb, g.H / 128), 128, 0, ctx->stream>>>(g, xbase, row_off, blk_slot, gate,
-                                                                    wbase, n_params, Z);
+  } else if (h8 && g.H % 128 == 0 && g.F % kKT == 0) {
+    static DeviceFlags attr8;
+    if (!attr8.done(ctx->cfg.device)) {
+      ECCO_CUDA(cudaFuncSetAttribute(k_l_hidden_ffma8, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(H8Smem)));
+      attr8.mark(ctx->cfg.device);
+    }
+    k_l_hidden_ffma8<<<dim3(nb, g.H / 128), 128, sizeof(H8Smem), ctx->stream>>>(
+        g, xbase, row_off, blk_slot, gate, wbase, n_params, Z);
+  }
   else if ((long)nb * (g.H / kHB) >= 2 * 148)
     k_l_hidden_ffma<kHB><<<dim3(nb, g.H / kHB), 256, 0, ctx->stream>>>(g, xbase, row_off, blk_slot,
                                                                        gate, wbase, n_params, Z);
