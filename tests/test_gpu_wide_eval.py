@@ -153,3 +153,28 @@ def test_wide_fused_counts_close_to_general_path(monkeypatch):
     b = ctx2.eval_matrix(ids, cams=np.arange(n_cams)) * 64
     diff = np.abs(a - b)
     assert diff.max() <= 3 and diff.mean() <= 0.5, (diff.max(), diff.mean())
+
+
+# edges: S = 128 (a tile is one camera's frames), C = 128 (the logits take
+# the last TMEM columns), F = 64 (one K chunk), H = 128 (one hidden half)
+EDGE = [dict(feat_dim=1024, hidden_dim=256, num_classes=128, minibatch=128, ring_frames=64,
+             eval_samples=128),
+        dict(feat_dim=64, hidden_dim=128, num_classes=80, minibatch=128, ring_frames=64,
+             eval_samples=64)]
+
+
+@pytest.mark.parametrize("dims", EDGE, ids=["s128_c128", "f64_h128"])
+def test_wide_edges_match_bf16_emulation(dims):
+    n_cams, ids = 3, [0, 2]
+    ctx, rng = _ctx(dims, n_cams, 6)
+    models = _random_models(ctx, rng, ids)
+    got = ctx.debug_eval_logits(ids, np.arange(n_cams))
+    x, el = _frames(ctx, n_cams)
+    M = ctx.eval_matrix(ids, cams=np.arange(n_cams))
+    S = dims["eval_samples"]
+    for jj, j in enumerate(ids):
+        for c in range(n_cams):
+            want = _emulate(dims, x[c], models[j])
+            assert np.abs(got[c, :, jj, :] - want).max() <= 4e-2, (j, c)
+            cnt = (np.argmax(want, 1) == el[c]).sum()
+            assert abs(M[c, jj] * S - cnt) <= 2, (j, c)
