@@ -94,6 +94,7 @@ void free_all(ecco_ctx* c) {
   c->zc_missing.release();
   for (auto& b : c->commit_args) b.release();
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->copy_stream2) cudaStreamDestroy(c->copy_stream2);
   for (auto& b : c->side_scratch) b.release();
   for (auto& b : c->side_em_args) b.release();
   c->side_tile_ctr.release();
@@ -323,6 +324,7 @@ ecco_status ecco_transfer_bytes(const ecco_ctx* ctx, uint64_t* h2d, uint64_t* d2
   if (ctx->d_zc_rows) {  // + rows read from pinned host memory by the sampled-row fetch
     unsigned long long n = 0;
     if (cudaStreamSynchronize(ctx->copy_stream) != cudaSuccess ||
+        (ctx->copy_stream2 && cudaStreamSynchronize(ctx->copy_stream2) != cudaSuccess) ||
         cudaStreamSynchronize(ctx->stream) != cudaSuccess ||  // (top-up fetches)
         cudaMemcpy(&n, ctx->d_zc_rows, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess)
       return ECCO_ERR_CUDA;
@@ -405,6 +407,7 @@ void open_back_buffers(ecco_ctx* ctx, int parts) {
   const ecco_config& g = ctx->cfg;
   if (!ctx->copy_stream) {
     ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    ECCO_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream2, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
       ECCO_CUDA(cudaEventCreateWithFlags(&ctx->copy_done[i], cudaEventDisableTiming));
       ECCO_CUDA(cudaEventCreateWithFlags(&ctx->back_free[i], cudaEventDisableTiming));
@@ -419,7 +422,7 @@ void open_back_buffers(ecco_ctx* ctx, int parts) {
     if (!((parts >> i) & 1)) continue;
     ECCO_REQUIRE(!ctx->staged[i], i == 0 ? "stage_frames: staged rings not swapped in yet"
                                          : "stage_frames: staged eval sets not swapped in yet");
-    if (ctx->back_busy[i]) ECCO_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->back_free[i], 0));
+    if (ctx->back_busy[i]) ECCO_CUDA(cudaStreamWaitEvent(ctx->part_stream(i), ctx->back_free[i], 0));
   }
 }
 
@@ -427,7 +430,7 @@ void open_back_buffers(ecco_ctx* ctx, int parts) {
 void staged_parts(ecco_ctx* ctx, int parts) {
   for (int i = 0; i < 2; ++i)
     if ((parts >> i) & 1) {
-      ECCO_CUDA(cudaEventRecord(ctx->copy_done[i], ctx->copy_stream));
+      ECCO_CUDA(cudaEventRecord(ctx->copy_done[i], ctx->part_stream(i)));
       ctx->staged[i] = true;
     }
 }
@@ -448,8 +451,8 @@ ecco_status ecco_stage_frames_range(ecco_ctx* ctx, int first, int n, const uint1
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_frames + f0 * g.feat_dim, frames, fr * g.feat_dim * 2, k,
                          ctx->copy_stream));
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels + f0, labels, fr * 4, k, ctx->copy_stream));
-    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream));
-    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream2));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream2));
     staged_parts(ctx, parts);
     if (parts & 1) ctx->back_partial = false;  // whole rings (of the caller's range)
   });
@@ -542,8 +545,8 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
     stage::fetch_rows(ctx, st, (const uint16_t*)fdev, ctx->b_frames, flags, words, ctx->d_zc_rows);
     ECCO_CUDA(ctx_memcpy(ctx, ctx->b_labels, labels, rows * 4, k, st));
     const size_t ev = (size_t)n_eval * g.eval_samples;
-    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, st));
-    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, st));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval, eval, ev * g.feat_dim * 2, k, ctx->copy_stream2));
+    ECCO_CUDA(ctx_memcpy(ctx, ctx->b_eval_labels, eval_labels, ev * 4, k, ctx->copy_stream2));
     staged_parts(ctx, parts);
     ctx->back_partial = true;  // only the drawn rows: zc_flags says which
   });

@@ -200,6 +200,8 @@ struct ecco_ctx {
   uint16_t* b_eval = nullptr;
   int32_t* b_eval_labels = nullptr;
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream2 = nullptr;  // the eval-set part: its DMA beside the rings' fetch
+  cudaStream_t part_stream(int part) const { return part == 0 ? copy_stream : copy_stream2; }
   // per part (0: rings + labels, 1: eval sets + labels): the staged copy's
   // completion, and the point after which the back buffer is no longer read
   cudaEvent_t copy_done[2] = {nullptr, nullptr}, back_free[2] = {nullptr, nullptr};
