@@ -546,10 +546,19 @@ def kernel_roofline(name, stat, pk, pk_kind, args, traffic=None, fused=True):
             how = (f"half the {pk_kind} bf16 dense peak ({peak:.1f} sustained, {burst:.1f} burst): "
                    "kind::tf32 MMAs")
     gbs = by / (ms / 1e3) / 1e9
-    return {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak, "frac_burst": achieved / burst,
-            "peak_source": how, "avg_launch_ms": ms / n, "launches": n, "traffic": traffic,
-            "algorithmic_gbs": gbs, "hbm_frac": gbs / pk["hbm_gbs"]}
+    out = {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak,
+           "unit": "TFLOP/s", "frac": achieved / peak, "frac_burst": achieved / burst,
+           "peak_source": how, "avg_launch_ms": ms / n, "launches": n, "traffic": traffic,
+           "algorithmic_gbs": gbs, "hbm_frac": gbs / pk["hbm_gbs"]}
+    if name == "TRAIN_CHAIN" and args.math != "ffma":
+        # (the fraction is of the whole GPU: the window's chains are one
+        # group's dependent SGD steps on one cluster -- DESIGN.md 4 / 8)
+        out["regime"] = ("latency: the exact schedule's serial chain runs one group's dependent "
+                         "SGD steps on ONE cluster (C4: 4 SMs, ~6.3 us per step, the step's "
+                         "tail bound by the shared-memory port; C5: 16 SMs, ~19 us per step, "
+                         "bound by the fp32 master's read-modify-write through L2) beside the "
+                         "regroup matrix; the throughput regime is the `probes` leg")
+    return out
 
 
 def roofline(kst, pk, pk_kind, args, fused=True, window_ms=None):
