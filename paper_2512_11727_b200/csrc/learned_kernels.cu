@@ -352,6 +352,106 @@ __global__ void __launch_bounds__(128, 4) k_l_hidden_ffma8(LDims g, const uint16
                threadIdx.x, sm, [] { __syncthreads(); });
 }
 
+// 64-thread form: 8 rows x 16 units per thread (64 packed accumulator pairs:
+// 0.75 B of shared memory per FMA, the FFMA pipe the bound), same tiles,
+// buffers and per-output order as hidden8_tile.
+__global__ void __launch_bounds__(64, 4) k_l_hidden_ffma16(LDims g, const uint16_t* xbase,
+                                                        const int64_t* row_off,
+                                                        const int* blk_slot, Gate gate,
+                                                        const float* wbase, size_t n_params,
+                                                        float* Z) {
+  extern __shared__ __align__(16) uint8_t dsm16[];
+  H8Smem& sm = *reinterpret_cast<H8Smem*>(dsm16);
+  const int blk = blockIdx.x;
+  if (!gate.live_row((size_t)blk * kRB)) return;
+  constexpr int HB = 128;
+  const int h0 = blockIdx.y * HB;
+  const float* W1 = wbase + (size_t)blk_slot[blk] * n_params;
+  const float* b1 = W1 + (size_t)g.F * g.H;
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;  // units 4 tx + 32 j.., rows 8 ty..
+  sm.rows[tid] = row_off[(size_t)blk * kRB + tid];
+  __syncthreads();
+  uint32_t xr[16];
+  auto fetch_x = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {  // a thread keeps one row (L1 hits), lanes cover rows
+      const int e = tid + u * 64, r = e & 63, kk = (e >> 6) * 2;
+      xr[u] = *reinterpret_cast<const uint32_t*>(xbase + sm.rows[r] + k0 + kk);
+    }
+  };
+  auto store_x = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 64, r = e & 63, kk = (e >> 6) * 2;
+      sm.As[buf][kk][r] = __uint_as_float(xr[u] << 16);
+      sm.As[buf][kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
+    }
+  };
+  auto fetch_w = [&](int k0, int buf) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 64, kk = e >> 5, c4 = (e & 31) * 4;
+      h8_cp16(&sm.Bs[buf][kk][c4], W1 + (size_t)(k0 + kk) * g.H + h0 + c4);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float2 acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[i][q] = make_float2(0.0f, 0.0f);
+  fetch_w(0, 0);
+  fetch_x(0);
+  store_x(0);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int nkt = g.F / kKT;
+  for (int t = 0; t < nkt; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    const bool more = t + 1 < nkt;
+    if (more) {
+      fetch_w((t + 1) * kKT, nxt);
+      fetch_x((t + 1) * kKT);
+    }
+    const float(*As)[kRB] = sm.As[cur];
+    const float(*Bs)[128] = sm.Bs[cur];
+#pragma unroll 2
+    for (int kk = 0; kk < kKT; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float2 bv[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // units 32 j + 4 tx..: lanes at a 16-byte stride
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][32 * j + tx * 4]);
+        bv[2 * j] = make_float2(b.x, b.y);
+        bv[2 * j + 1] = make_float2(b.z, b.w);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 ai = make_float2(av[i], av[i]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[i][q] = __ffma2_rn(ai, bv[q], acc[i][q]);
+      }
+    }
+    if (more) {
+      store_x(nxt);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const size_t r = (size_t)blk * kRB + ty * 8 + i;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int h = h0 + 32 * (q >> 1) + tx * 4 + 2 * (q & 1);
+      *reinterpret_cast<float2*>(Z + r * g.H + h) =
+          make_float2(__fadd_rn(acc[i][q].x, b1[h]), __fadd_rn(acc[i][q].y, b1[h + 1]));
+    }
+  }
+}
+
 // Persistent form for a matrix that runs BESIDE other work (the
 // oracle-exact window's regroup matrix next to the serial chains): one
 // 512-thread block per SM (4 independent 128-thread tile workers, a named
@@ -396,6 +496,17 @@ static void launch_hidden_ffma(ecco_ctx* ctx, int nb, const LDims& g, const uint
     const int grid = (int)std::max(1L, std::min<long>((items + 3) / 4, sms - ctx->reserve_sms));
     k_l_hidden_ffma8_persistent<<<grid, 512, kH8PersistentSmem, ctx->stream>>>(
         g, xbase, row_off, blk_slot, gate, wbase, n_params, Z, nb, g.H / 128);
+  } else if (h8 && g.H % 128 == 0 && g.F % kKT == 0 &&
+             !(getenv("ECCO_FFMA_HIDDEN16") && getenv("ECCO_FFMA_HIDDEN16")[0] == '0')) {
+    // (8 x 16 per thread: +2.6% over the 8 x 8 tile at C3; ECCO_FFMA_HIDDEN16=0 keeps that one)
+    static DeviceFlags attr16;
+    if (!attr16.done(ctx->cfg.device)) {
+      ECCO_CUDA(cudaFuncSetAttribute(k_l_hidden_ffma16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(H8Smem)));
+      attr16.mark(ctx->cfg.device);
+    }
+    k_l_hidden_ffma16<<<dim3(nb, g.H / 128), 64, sizeof(H8Smem), ctx->stream>>>(
+        g, xbase, row_off, blk_slot, gate, wbase, n_params, Z);
   } else if (h8 && g.H % 128 == 0 && g.F % kKT == 0) {
     static DeviceFlags attr8;
     if (!attr8.done(ctx->cfg.device)) {

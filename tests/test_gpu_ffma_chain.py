@@ -93,12 +93,13 @@ def test_ffma_chain_other_cluster_sizes(hidden, feat, monkeypatch):
             assert a.tobytes() == b.tobytes()
 
 
-@pytest.mark.parametrize("wide", ["1", "0"])
-def test_ffma_eval_matrix_hidden_tiles_bit_exact(wide, monkeypatch):
-    """The FFMA evaluation matrix with the 8 x 8 per-thread hidden tile
-    (k_l_hidden_ffma8, forced on) and with the 4 x 8 one: both equal the
-    oracle's counts bit for bit."""
+@pytest.mark.parametrize("wide,t16", [("1", "1"), ("1", "0"), ("0", "1")])
+def test_ffma_eval_matrix_hidden_tiles_bit_exact(wide, t16, monkeypatch):
+    """The FFMA evaluation matrix with the wide-grid hidden tiles forced on
+    (8 x 16 per thread, k_l_hidden_ffma16, or 8 x 8, k_l_hidden_ffma8) and
+    with the 4 x 8 one: all equal the oracle's counts bit for bit."""
     monkeypatch.setenv("ECCO_FFMA_HIDDEN8", wide)
+    monkeypatch.setenv("ECCO_FFMA_HIDDEN16", t16)
     ctx, orc, _ = setup(seed=44, **BENCH)
     ids = [2, 5, 6]
     ctx.seed_models(ids)
