@@ -539,11 +539,16 @@ constexpr int kHT = 32;  // reduction chunk of the tiled head kernels
 // oracle's: block z covers hidden units [z*kspan, (z+1)*kspan) and writes
 // its partial (no b2) to L + z*n_rows*C; k_l_logits_sum adds the partials in
 // z order and b2.  kspan = H is the exact form.)
-__global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const int* blk_slot,
-                                                    Gate gate, const float* wbase,
-                                                    size_t n_params, const float* Z, float* L,
-                                                    int kspan = 0) {
-  const int blk = blockIdx.x, c0 = blockIdx.y * 32;
+// NT threads: a block covers 64 rows x NT / 4 classes (NT = 128: 32 classes;
+// NT = 64: the 16 of the classifier, no idle class lanes), 4 rows x 4
+// classes per thread, k ascending from 0 per output.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_l_logits_t(LDims g, int n_rows, const int* blk_slot,
+                                                   Gate gate, const float* wbase,
+                                                   size_t n_params, const float* Z, float* L,
+                                                   int kspan = 0) {
+  constexpr int CW = NT / 4;  // classes per block
+  const int blk = blockIdx.x, c0 = blockIdx.y * CW;
   const int kb = kspan > 0 ? blockIdx.z * kspan : 0;
   const int ke = kspan > 0 ? kb + kspan : g.H;
   const bool part = kspan > 0;
@@ -552,22 +557,22 @@ __global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const i
   const float* W2 = wbase + (size_t)blk_slot[blk] * n_params + (size_t)g.F * g.H + g.H;
   const float* b2 = W2 + (size_t)g.H * g.C;
   __shared__ __align__(16) float Zs[kHT][kRB + 4];
-  __shared__ __align__(16) float Ws[kHT][32 + 4];
-  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  __shared__ __align__(16) float Ws[kHT][CW + 4];
+  const int tid = threadIdx.x, tx = tid % (CW / 4), ty = tid / (CW / 4);
   float acc[4][4] = {};
   const size_t r0 = (size_t)blk * kRB;
   // next chunk's Z / W2 values prefetched into registers (load-latency bound)
-  constexpr int kZ = kRB * kHT / 128, kW = kHT * 32 / 128;
+  constexpr int kZ = kRB * kHT / NT, kW = kHT * CW / NT;
   float zr[kZ], wr[kW];
   auto fetch = [&](int k0) {
 #pragma unroll
     for (int u = 0; u < kZ; ++u) {
-      const int e = tid + u * 128, r = e / kHT, k = e % kHT;
+      const int e = tid + u * NT, r = e / kHT, k = e % kHT;
       zr[u] = Z[(r0 + r) * g.H + k0 + k];
     }
 #pragma unroll
     for (int u = 0; u < kW; ++u) {
-      const int e = tid + u * 128, k = e / 32, c = e % 32;
+      const int e = tid + u * NT, k = e / CW, c = e % CW;
       wr[u] = c0 + c < g.C ? W2[(size_t)(k0 + k) * g.C + c0 + c] : 0.0f;
     }
   };
@@ -575,13 +580,13 @@ __global__ void __launch_bounds__(128) k_l_logits_t(LDims g, int n_rows, const i
   for (int k0 = kb; k0 < ke; k0 += kHT) {
 #pragma unroll
     for (int u = 0; u < kZ; ++u) {
-      const int e = tid + u * 128;
+      const int e = tid + u * NT;
       Zs[e % kHT][e / kHT] = zr[u] > 0.0f ? zr[u] : 0.0f;
     }
 #pragma unroll
     for (int u = 0; u < kW; ++u) {
-      const int e = tid + u * 128;
-      Ws[e / 32][e % 32] = wr[u];
+      const int e = tid + u * NT;
+      Ws[e / CW][e % CW] = wr[u];
     }
     __syncthreads();
     if (k0 + kHT < ke) fetch(k0 + kHT);
@@ -1185,7 +1190,7 @@ static void pair_counts_general_planned(ecco_ctx* ctx, const GeneralPlan& pl, co
   tc::fwd_hidden_bf16(ctx, ctx->d_eval, row_off, pl.d_tiles, pl.n_tiles, nullptr, 0, w1t, n_img,
                       wbase, wstride, Z, (double)rows);
   ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
-             (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
+             (k_l_logits_t<128><<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
                  g, rows, blk_slot, Gate{nullptr, 0, 1}, wbase, wstride, Z, L)));
   ECCO_LAUNCHED(ctx);
   k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, L, ctx->d_eval_labels, d_pair_cam,
@@ -1274,9 +1279,15 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
                                     Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z));
       ECCO_LAUNCHED(ctx);
     }
-    ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
-               (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
-                   g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L)));
+    // (C <= 16: 64-thread blocks of 16 classes, no idle class lanes)
+    if (g.C <= 16)
+      ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
+                 (k_l_logits_t<64><<<dim3(rows / kRB, 1), 64, 0, ctx->stream>>>(
+                     g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L)));
+    else
+      ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_PAIRS, 2.0 * rows * g.H * g.C, (double)rows * g.H * 4,
+                 (k_l_logits_t<128><<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
+                     g, rows, blk_slot, Gate{nullptr, 0, 1}, ctx->d_w, ctx->n_params, Z, L)));
     ECCO_LAUNCHED(ctx);
     k_l_count<<<nblk(rows, 256), 256, 0, ctx->stream>>>(g, np, L, ctx->d_eval_labels,
                                                          d_pair_cam + p0, d_counts + p0);
@@ -1709,12 +1720,12 @@ void trajectories(ecco_ctx* ctx, int n_jobs, const int* h_job_ids, const int* d_
       }
       ECCO_TIMED(ctx, ECCO_KSTAT_TRAIN_HEAD, 8.0 * lrows * g.H * g.C, lrows * g.H * 12,
                  ((head_ks > 1
-                       ? (k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32, head_ks), 128, 0,
+                       ? (k_l_logits_t<128><<<dim3(rows / kRB, (g.C + 31) / 32, head_ks), 128, 0,
                                          ctx->stream>>>(g, rows, blk_slot, gate, wt, spec_stride,
                                                         Z, Lp, g.H / head_ks),
                           k_l_logits_sum<<<nblk((size_t)rows * g.C, 256), 256, 0, ctx->stream>>>(
                               g, rows, head_ks, blk_slot, gate, wt, spec_stride, Lp, L))
-                       : k_l_logits_t<<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
+                       : k_l_logits_t<128><<<dim3(rows / kRB, (g.C + 31) / 32), 128, 0, ctx->stream>>>(
                              g, rows, blk_slot, gate, wt, spec_stride, Z, L)),
                   (k_l_softmax_grad<<<nblk(rows, 128), 128, 0, ctx->stream>>>(
                       g, rows, gate, L, row_lab, DL, loss_rows)),
