@@ -1224,12 +1224,191 @@ void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const 
   ECCO_LAUNCHED(ctx);
 }
 
+// The whole oracle-exact evaluation of one (slot, camera) pair in one block
+// (FFMA math, S = 64 rows, H = 256, C = 16): Z = X.W1 + b1 for all 256 units
+// (8 rows x 16 units per thread, W1 tiles by cp.async into double buffers),
+// relu rows into shared memory, logits = relu(Z).W2 + b2 (one fmaf chain per
+// output, k ascending), the first-max argmax per row, the correct count --
+// no hidden activations or logits in HBM, one launch for any number of
+// pairs.  Every output keeps the oracle's order (orc count_correct).
+constexpr int kFE_H = 256, kFE_C = 16;
+struct FESmem {
+  union {
+    struct {
+      float As[2][kKT][kRB];      // [buffer][k][row]
+      float Bs[2][kKT][kFE_H];    // [buffer][k][unit]
+    } g;
+    float Rs[kRB][kFE_H + 4];     // relu(Z + b1) rows (after the GEMM)
+  } u;
+  float W2s[kFE_H][kFE_C];
+};
+__global__ void __launch_bounds__(128, 2) k_l_eval_ffma_fused(LDims g, int n_pairs,
+                                                             const int* pair_slot,
+                                                             const int* pair_cam,
+                                                             const uint16_t* eval,
+                                                             const int32_t* eval_labels,
+                                                             const float* wbase, size_t n_params,
+                                                             int* counts) {
+  extern __shared__ __align__(16) uint8_t dsmf[];
+  FESmem& sm = *reinterpret_cast<FESmem*>(dsmf);
+  const int p = blockIdx.x;
+  const int slot = pair_slot[p], cam = pair_cam[p];
+  const float* W1 = wbase + (size_t)slot * n_params;
+  const float* b1 = W1 + (size_t)g.F * kFE_H;
+  const float* W2 = b1 + kFE_H;
+  const float* b2 = W2 + (size_t)kFE_H * kFE_C;
+  const uint16_t* X = eval + (size_t)cam * kRB * g.F;  // the camera's 64 eval rows
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // units 4 tx + 64 j.., rows 8 ty..
+  // W2 (16 KB) beside the first K tile
+  for (int e = tid; e < kFE_H * kFE_C / 4; e += 128) h8_cp16(&sm.W2s[0][0] + 4 * e, W2 + 4 * e);
+  uint32_t xr[8];
+  auto fetch_x = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // a thread keeps one row (L1 hits), lanes cover rows
+      const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;
+      xr[u] = *reinterpret_cast<const uint32_t*>(X + (size_t)r * g.F + k0 + kk);
+    }
+  };
+  auto store_x = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;
+      sm.u.g.As[buf][kk][r] = __uint_as_float(xr[u] << 16);
+      sm.u.g.As[buf][kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
+    }
+  };
+  auto fetch_w = [&](int k0, int buf) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 128, kk = e >> 6, c4 = (e & 63) * 4;
+      h8_cp16(&sm.u.g.Bs[buf][kk][c4], W1 + (size_t)(k0 + kk) * kFE_H + c4);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float2 acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[i][q] = make_float2(0.0f, 0.0f);
+  fetch_w(0, 0);
+  fetch_x(0);
+  store_x(0);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  const int nkt = g.F / kKT;
+  for (int t = 0; t < nkt; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    const bool more = t + 1 < nkt;
+    if (more) {
+      fetch_w((t + 1) * kKT, nxt);
+      fetch_x((t + 1) * kKT);
+    }
+    const float(*As)[kRB] = sm.u.g.As[cur];
+    const float(*Bs)[kFE_H] = sm.u.g.Bs[cur];
+#pragma unroll 2
+    for (int kk = 0; kk < kKT; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float2 bv[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // units 64 j + 4 tx..: lanes at a 16-byte stride
+        const float4 b = *reinterpret_cast<const float4*>(&Bs[kk][64 * j + tx * 4]);
+        bv[2 * j] = make_float2(b.x, b.y);
+        bv[2 * j + 1] = make_float2(b.z, b.w);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float2 ai = make_float2(av[i], av[i]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[i][q] = __ffma2_rn(ai, bv[q], acc[i][q]);
+      }
+    }
+    if (more) {
+      store_x(nxt);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  // relu(Z + b1) rows into shared memory (the GEMM buffers are dead)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int r = ty * 8 + i;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int h = 64 * (q >> 1) + tx * 4 + 2 * (q & 1);
+      const float z0 = __fadd_rn(acc[i][q].x, __ldg(b1 + h));
+      const float z1 = __fadd_rn(acc[i][q].y, __ldg(b1 + h + 1));
+      *reinterpret_cast<float2*>(&sm.u.Rs[r][h]) =
+          make_float2(z0 > 0.0f ? z0 : 0.0f, z1 > 0.0f ? z1 : 0.0f);
+    }
+  }
+  __syncthreads();
+  // logits: thread t -> row t / 2, classes 8 (t & 1)..+8, k ascending
+  const int r = tid >> 1, cb = (tid & 1) * 8;
+  float l[8] = {};
+  for (int k = 0; k < kFE_H; ++k) {
+    const float z = sm.u.Rs[r][k];
+    const float4 w0 = *reinterpret_cast<const float4*>(&sm.W2s[k][cb]);
+    const float4 w1 = *reinterpret_cast<const float4*>(&sm.W2s[k][cb + 4]);
+    l[0] = __fmaf_rn(z, w0.x, l[0]);
+    l[1] = __fmaf_rn(z, w0.y, l[1]);
+    l[2] = __fmaf_rn(z, w0.z, l[2]);
+    l[3] = __fmaf_rn(z, w0.w, l[3]);
+    l[4] = __fmaf_rn(z, w1.x, l[4]);
+    l[5] = __fmaf_rn(z, w1.y, l[5]);
+    l[6] = __fmaf_rn(z, w1.z, l[6]);
+    l[7] = __fmaf_rn(z, w1.w, l[7]);
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) l[c] = __fadd_rn(l[c], __ldg(b2 + cb + c));
+  // first-max argmax over the 16 classes, scanned in order by the even thread
+  float lo[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) lo[c] = __shfl_down_sync(0xffffffffu, l[c], 1);
+  bool ok = false;
+  if ((tid & 1) == 0) {
+    int best = 0;
+    float bv = l[0];
+#pragma unroll
+    for (int c = 1; c < 16; ++c) {
+      const float v = c < 8 ? l[c] : lo[c - 8];
+      if (v > bv) {
+        bv = v;
+        best = c;
+      }
+    }
+    ok = best == eval_labels[(size_t)cam * kRB + r];
+  }
+  const int n = __syncthreads_count(ok);
+  if (tid == 0) counts[p] = n;
+}
+
 // Counts for a list of (slot, camera) pairs, chunked to bound scratch (1 GiB
 // of hidden activations per chunk: few, large launches -- a full C4 matrix
 // in ~300 chunks, each a wide grid).
 static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, const int* d_pair_cam,
                         int* d_counts) {
   const LDims g = dims(ctx);
+  const char* ef = getenv("ECCO_FFMA_FUSED_EVAL");
+  if (ctx->cfg.math == ECCO_MATH_FFMA_EXACT && g.S == kRB && g.H == kFE_H && g.C == kFE_C &&
+      g.F % kKT == 0 && n_pairs > 0 && !(ef && ef[0] == '0')) {
+    // one block per pair: hidden layer, head, argmax and count on chip
+    static DeviceFlags attr;
+    if (!attr.done(ctx->cfg.device)) {
+      ECCO_CUDA(cudaFuncSetAttribute(k_l_eval_ffma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(FESmem)));
+      attr.mark(ctx->cfg.device);
+    }
+    const double rows = (double)n_pairs * g.S;
+    ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_MATRIX, 2.0 * rows * g.F * g.H + 2.0 * rows * g.H * g.C,
+               rows * g.F * 2 + (double)n_pairs * 4,
+               (k_l_eval_ffma_fused<<<n_pairs, 128, sizeof(FESmem), ctx->stream>>>(
+                   g, n_pairs, d_pair_slot, d_pair_cam, ctx->d_eval, ctx->d_eval_labels, ctx->d_w,
+                   ctx->n_params, d_counts)));
+    ECCO_LAUNCHED(ctx);
+    return;
+  }
   ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(n_pairs, 1), ctx->stream));
   const int chunk = std::max(1, (int)std::min<size_t>(n_pairs, (size_t)(1u << 30) / ((size_t)g.S * g.H * 4)));
   for (int p0 = 0; p0 < n_pairs; p0 += chunk) {

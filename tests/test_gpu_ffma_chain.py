@@ -93,14 +93,20 @@ def test_ffma_chain_other_cluster_sizes(hidden, feat, monkeypatch):
             assert a.tobytes() == b.tobytes()
 
 
-@pytest.mark.parametrize("wide,t16", [("1", "1"), ("1", "0"), ("0", "1")])
-def test_ffma_eval_matrix_hidden_tiles_bit_exact(wide, t16, monkeypatch):
-    """The FFMA evaluation matrix with the wide-grid hidden tiles forced on
-    (8 x 16 per thread, k_l_hidden_ffma16, or 8 x 8, k_l_hidden_ffma8) and
-    with the 4 x 8 one: all equal the oracle's counts bit for bit."""
+@pytest.mark.parametrize("fused,wide,t16", [("1", "1", "1"), ("0", "1", "1"), ("0", "1", "0"),
+                                            ("0", "0", "1")])
+@pytest.mark.parametrize("feat", [512, 128])
+def test_ffma_eval_matrix_hidden_tiles_bit_exact(fused, wide, t16, feat, monkeypatch):
+    """The FFMA evaluation matrix through the fused per-pair kernel
+    (k_l_eval_ffma_fused: hidden layer, head, argmax, count in one block) and,
+    with it disabled, through the chunked kernels with the wide-grid hidden
+    tiles forced on (8 x 16 per thread, k_l_hidden_ffma16, or 8 x 8,
+    k_l_hidden_ffma8) and with the 4 x 8 one: all equal the oracle's counts
+    bit for bit."""
+    monkeypatch.setenv("ECCO_FFMA_FUSED_EVAL", fused)
     monkeypatch.setenv("ECCO_FFMA_HIDDEN8", wide)
     monkeypatch.setenv("ECCO_FFMA_HIDDEN16", t16)
-    ctx, orc, _ = setup(seed=44, **BENCH)
+    ctx, orc, _ = setup(seed=44, **dict(BENCH, feat_dim=feat))
     ids = [2, 5, 6]
     ctx.seed_models(ids)
     for j in ids:
