@@ -575,7 +575,8 @@ def roofline(kst, pk, pk_kind, args, fused=True, window_ms=None):
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get(name)
+            key = args.config if args.math == "bf16" else f"{args.config}_{args.math}"
+            traffic = json.load(open(tpath)).get(key, {}).get(name)
         except (OSError, ValueError, AttributeError):
             traffic = None
     head = kernel_roofline(name, kst[name], pk, pk_kind, args, traffic, fused)

@@ -1226,23 +1226,26 @@ void seed(ecco_ctx* ctx, int n, const int* h_job_ids, const int* d_slots, const 
 
 // The whole oracle-exact evaluation of one (slot, camera) pair in one block
 // (FFMA math, S = 64 rows, H = 256, C = 16): Z = X.W1 + b1 for all 256 units
-// (8 rows x 16 units per thread, W1 tiles by cp.async into double buffers),
-// relu rows into shared memory, logits = relu(Z).W2 + b2 (one fmaf chain per
-// output, k ascending), the first-max argmax per row, the correct count --
-// no hidden activations or logits in HBM, one launch for any number of
-// pairs.  Every output keeps the oracle's order (orc count_correct).
-constexpr int kFE_H = 256, kFE_C = 16;
+// (8 rows x 16 units per thread, W1 tiles of 16 k by cp.async into double
+// buffers), relu rows into shared memory in two 32-row halves, logits =
+// relu(Z).W2 + b2 (one fmaf chain per output, k ascending), the first-max
+// argmax per row, the correct count -- no hidden activations or logits in
+// HBM, one launch for any number of pairs.  168 registers and 56 KB of
+// shared memory: three blocks (12 warps) per SM hide the FFMA2 and shared
+// load latencies that two blocks left exposed.  Every output keeps the
+// oracle's order (orc count_correct).
+constexpr int kFE_H = 256, kFE_C = 16, kFE_KT = 16, kFE_HALF = kRB / 2;
 struct FESmem {
   union {
     struct {
-      float As[2][kKT][kRB];      // [buffer][k][row]
-      float Bs[2][kKT][kFE_H];    // [buffer][k][unit]
+      float As[2][kFE_KT][kRB];      // [buffer][k][row]
+      float Bs[2][kFE_KT][kFE_H];    // [buffer][k][unit]
     } g;
-    float Rs[kRB][kFE_H + 4];     // relu(Z + b1) rows (after the GEMM)
+    float Rs[kFE_HALF][kFE_H + 4];   // relu(Z + b1), one half of the rows
   } u;
   float W2s[kFE_H][kFE_C];
 };
-__global__ void __launch_bounds__(128, 2) k_l_eval_ffma_fused(LDims g, int n_pairs,
+__global__ void __launch_bounds__(128, 3) k_l_eval_ffma_fused(LDims g, int n_pairs,
                                                              const int* pair_slot,
                                                              const int* pair_cam,
                                                              const uint16_t* eval,
@@ -1261,17 +1264,18 @@ __global__ void __launch_bounds__(128, 2) k_l_eval_ffma_fused(LDims g, int n_pai
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;  // units 4 tx + 64 j.., rows 8 ty..
   // W2 (16 KB) beside the first K tile
   for (int e = tid; e < kFE_H * kFE_C / 4; e += 128) h8_cp16(&sm.W2s[0][0] + 4 * e, W2 + 4 * e);
-  uint32_t xr[8];
+  constexpr int kXU = kRB * kFE_KT / 2 / 128;  // bf16 pairs per thread per tile
+  uint32_t xr[kXU];
   auto fetch_x = [&](int k0) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {  // a thread keeps one row (L1 hits), lanes cover rows
+    for (int u = 0; u < kXU; ++u) {  // lanes cover rows, a thread keeps one row
       const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;
       xr[u] = *reinterpret_cast<const uint32_t*>(X + (size_t)r * g.F + k0 + kk);
     }
   };
   auto store_x = [&](int buf) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kXU; ++u) {
       const int e = tid + u * 128, r = e & 63, kk = (e >> 6) * 2;
       sm.u.g.As[buf][kk][r] = __uint_as_float(xr[u] << 16);
       sm.u.g.As[buf][kk + 1][r] = __uint_as_float(xr[u] & 0xFFFF0000u);
@@ -1279,7 +1283,7 @@ __global__ void __launch_bounds__(128, 2) k_l_eval_ffma_fused(LDims g, int n_pai
   };
   auto fetch_w = [&](int k0, int buf) {
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
+    for (int u = 0; u < kFE_KT * kFE_H / 4 / 128; ++u) {
       const int e = tid + u * 128, kk = e >> 6, c4 = (e & 63) * 4;
       h8_cp16(&sm.u.g.Bs[buf][kk][c4], W1 + (size_t)(k0 + kk) * kFE_H + c4);
     }
@@ -1295,18 +1299,18 @@ __global__ void __launch_bounds__(128, 2) k_l_eval_ffma_fused(LDims g, int n_pai
   store_x(0);
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  const int nkt = g.F / kKT;
+  const int nkt = g.F / kFE_KT;
   for (int t = 0; t < nkt; ++t) {
     const int cur = t & 1, nxt = cur ^ 1;
     const bool more = t + 1 < nkt;
     if (more) {
-      fetch_w((t + 1) * kKT, nxt);
-      fetch_x((t + 1) * kKT);
+      fetch_w((t + 1) * kFE_KT, nxt);
+      fetch_x((t + 1) * kFE_KT);
     }
     const float(*As)[kRB] = sm.u.g.As[cur];
     const float(*Bs)[kFE_H] = sm.u.g.Bs[cur];
 #pragma unroll 2
-    for (int kk = 0; kk < kKT; ++kk) {
+    for (int kk = 0; kk < kFE_KT; ++kk) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[kk][ty * 8]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[kk][ty * 8 + 4]);
       const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
@@ -1318,11 +1322,9 @@ __global__ void __launch_bounds__(128, 2) k_l_eval_ffma_fused(LDims g, int n_pai
         bv[2 * j + 1] = make_float2(b.z, b.w);
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 ai = make_float2(av[i], av[i]);
+      for (int q = 0; q < 8; ++q)  // b pair in the operand reuse cache across rows
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[i][q] = __ffma2_rn(ai, bv[q], acc[i][q]);
-      }
+        for (int i = 0; i < 8; ++i) acc[i][q] = __ffma2_rn(make_float2(av[i], av[i]), bv[q], acc[i][q]);
     }
     if (more) {
       store_x(nxt);
@@ -1330,58 +1332,61 @@ __global__ void __launch_bounds__(128, 2) k_l_eval_ffma_fused(LDims g, int n_pai
     }
     __syncthreads();
   }
-  // relu(Z + b1) rows into shared memory (the GEMM buffers are dead)
+  // per half: relu(Z + b1) rows into shared memory (the GEMM buffers are
+  // dead), then logits: thread t -> row t / 4 of the half, classes
+  // 4 (t & 3)..+4, k ascending; the row's 16 logits meet in lane t & ~3,
+  // which scans them in class order (first max).
+  const int lr = tid >> 2, cb = (tid & 3) * 4;
+  int n_ok = 0;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    if ((ty >> 2) == half) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int r = ty * 8 + i;
+      for (int i = 0; i < 8; ++i) {
+        const int r = (ty & 3) * 8 + i;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int h = 64 * (q >> 1) + tx * 4 + 2 * (q & 1);
-      const float z0 = __fadd_rn(acc[i][q].x, __ldg(b1 + h));
-      const float z1 = __fadd_rn(acc[i][q].y, __ldg(b1 + h + 1));
-      *reinterpret_cast<float2*>(&sm.u.Rs[r][h]) =
-          make_float2(z0 > 0.0f ? z0 : 0.0f, z1 > 0.0f ? z1 : 0.0f);
-    }
-  }
-  __syncthreads();
-  // logits: thread t -> row t / 2, classes 8 (t & 1)..+8, k ascending
-  const int r = tid >> 1, cb = (tid & 1) * 8;
-  float l[8] = {};
-  for (int k = 0; k < kFE_H; ++k) {
-    const float z = sm.u.Rs[r][k];
-    const float4 w0 = *reinterpret_cast<const float4*>(&sm.W2s[k][cb]);
-    const float4 w1 = *reinterpret_cast<const float4*>(&sm.W2s[k][cb + 4]);
-    l[0] = __fmaf_rn(z, w0.x, l[0]);
-    l[1] = __fmaf_rn(z, w0.y, l[1]);
-    l[2] = __fmaf_rn(z, w0.z, l[2]);
-    l[3] = __fmaf_rn(z, w0.w, l[3]);
-    l[4] = __fmaf_rn(z, w1.x, l[4]);
-    l[5] = __fmaf_rn(z, w1.y, l[5]);
-    l[6] = __fmaf_rn(z, w1.z, l[6]);
-    l[7] = __fmaf_rn(z, w1.w, l[7]);
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) l[c] = __fadd_rn(l[c], __ldg(b2 + cb + c));
-  // first-max argmax over the 16 classes, scanned in order by the even thread
-  float lo[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) lo[c] = __shfl_down_sync(0xffffffffu, l[c], 1);
-  bool ok = false;
-  if ((tid & 1) == 0) {
-    int best = 0;
-    float bv = l[0];
-#pragma unroll
-    for (int c = 1; c < 16; ++c) {
-      const float v = c < 8 ? l[c] : lo[c - 8];
-      if (v > bv) {
-        bv = v;
-        best = c;
+        for (int q = 0; q < 8; ++q) {
+          const int h = 64 * (q >> 1) + tx * 4 + 2 * (q & 1);
+          const float z0 = __fadd_rn(acc[i][q].x, __ldg(b1 + h));
+          const float z1 = __fadd_rn(acc[i][q].y, __ldg(b1 + h + 1));
+          *reinterpret_cast<float2*>(&sm.u.Rs[r][h]) =
+              make_float2(z0 > 0.0f ? z0 : 0.0f, z1 > 0.0f ? z1 : 0.0f);
+        }
       }
     }
-    ok = best == eval_labels[(size_t)cam * kRB + r];
+    __syncthreads();
+    float l[4] = {};
+#pragma unroll 8
+    for (int k = 0; k < kFE_H; ++k) {
+      const float z = sm.u.Rs[lr][k];
+      const float4 w = *reinterpret_cast<const float4*>(&sm.W2s[k][cb]);
+      l[0] = __fmaf_rn(z, w.x, l[0]);
+      l[1] = __fmaf_rn(z, w.y, l[1]);
+      l[2] = __fmaf_rn(z, w.z, l[2]);
+      l[3] = __fmaf_rn(z, w.w, l[3]);
+    }
+    float v[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float lc = __fadd_rn(l[c], __ldg(b2 + cb + c));
+#pragma unroll
+      for (int s = 0; s < 4; ++s) v[4 * s + c] = __shfl_sync(0xffffffffu, lc, (tid & ~3) + s);
+    }
+    if ((tid & 3) == 0) {
+      int best = 0;
+      float bv = v[0];
+#pragma unroll
+      for (int c = 1; c < 16; ++c)
+        if (v[c] > bv) {
+          bv = v[c];
+          best = c;
+        }
+      n_ok += best == eval_labels[(size_t)cam * kRB + half * kFE_HALF + lr];
+    }
+    __syncthreads();  // Rs is rewritten by the next half
   }
-  const int n = __syncthreads_count(ok);
-  if (tid == 0) counts[p] = n;
+  const int n0 = __syncthreads_count(n_ok & 1), n1 = __syncthreads_count(n_ok >> 1);
+  if (tid == 0) counts[p] = n0 + 2 * n1;
 }
 
 // Counts for a list of (slot, camera) pairs, chunked to bound scratch (1 GiB
@@ -1392,7 +1397,7 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
   const LDims g = dims(ctx);
   const char* ef = getenv("ECCO_FFMA_FUSED_EVAL");
   if (ctx->cfg.math == ECCO_MATH_FFMA_EXACT && g.S == kRB && g.H == kFE_H && g.C == kFE_C &&
-      g.F % kKT == 0 && n_pairs > 0 && !(ef && ef[0] == '0')) {
+      g.F % kFE_KT == 0 && n_pairs > 0 && !(ef && ef[0] == '0')) {
     // one block per pair: hidden layer, head, argmax and count on chip
     static DeviceFlags attr;
     if (!attr.done(ctx->cfg.device)) {
@@ -1501,16 +1506,25 @@ void eval_matrix(ecco_ctx* ctx, int n, const int* d_cams, int gj, const int* d_s
     ECCO_CUDA(ctx_memcpy(ctx, mask.data(), d_mask, total, cudaMemcpyDeviceToHost, ctx->stream));
   }
   ECCO_CUDA(cudaStreamSynchronize(ctx->stream));
+  // Pairs in group tiles: tile_g groups (their W1 stays in L2: 64 x 512 KB
+  // at the bench shape), cameras outer and the tile's groups inner, so each
+  // camera's eval rows are read once per tile and each W1 once per window
+  // rather than once per pair (camera-major order re-read the 500 groups'
+  // 256 MB of W1 from HBM for every camera).  Counts are per pair and land
+  // through po, so the order is invisible to the result.
+  const char* et = getenv("ECCO_PAIR_TILE");
+  const int tile_g = std::max(1, et ? atoi(et) : 64);
   std::vector<int> ps, pc, po;
   ps.reserve(total);
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < gj; ++j) {
-      const size_t o = (size_t)i * gj + j;
-      if (d_mask && !mask[o]) continue;
-      ps.push_back(slots[j]);
-      pc.push_back(cams[i]);
-      po.push_back((int)o);
-    }
+  for (int j0 = 0; j0 < gj; j0 += tile_g)
+    for (int i = 0; i < n; ++i)
+      for (int j = j0; j < std::min(gj, j0 + tile_g); ++j) {
+        const size_t o = (size_t)i * gj + j;
+        if (d_mask && !mask[o]) continue;
+        ps.push_back(slots[j]);
+        pc.push_back(cams[i]);
+        po.push_back((int)o);
+      }
   if (d_mask) {
     k_l_fill_nan<<<nblk(total, 256), 256, 0, ctx->stream>>>(total, d_out);
     ECCO_LAUNCHED(ctx);
