@@ -254,14 +254,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
         for (int i = 0; i < 8; ++i) {
           const float4 w = *reinterpret_cast<const float4*>(w1s + (f + i) * kHS + hq);
           const float2 wa = make_float2(w.x, w.y), wb = make_float2(w.z, w.w);
+          float xs4[4];
 #pragma unroll
           for (int r4 = 0; r4 < 4; ++r4) {
             const uint32_t pw = px[r4][i >> 1];
-            const float x = __uint_as_float(i & 1 ? pw & 0xFFFF0000u : pw << 16);
-            const float2 xx = make_float2(x, x);
-            ac[r4][0] = fma2(xx, wa, ac[r4][0]);
-            ac[r4][1] = fma2(xx, wb, ac[r4][1]);
+            xs4[r4] = __uint_as_float(i & 1 ? pw & 0xFFFF0000u : pw << 16);
           }
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4)  // wa, then wb, in the operand reuse cache
+            ac[r4][0] = fma2(make_float2(xs4[r4], xs4[r4]), wa, ac[r4][0]);
+#pragma unroll
+          for (int r4 = 0; r4 < 4; ++r4)
+            ac[r4][1] = fma2(make_float2(xs4[r4], xs4[r4]), wb, ac[r4][1]);
         }
       }
 #pragma unroll
@@ -362,13 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
             const float4 d1 = *reinterpret_cast<const float4*>(dhs + s * kHS + hq + 4);
             const float2 d[4] = {make_float2(d0.x, d0.y), make_float2(d0.z, d0.w),
                                  make_float2(d1.x, d1.y), make_float2(d1.z, d1.w)};
+            float xv[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float x = __uint_as_float(i & 1 ? pv[i >> 1] & 0xFFFF0000u : pv[i >> 1] << 16);
-              const float2 xi = make_float2(x, x);
+            for (int i = 0; i < 8; ++i)
+              xv[i] = __uint_as_float(i & 1 ? pv[i >> 1] & 0xFFFF0000u : pv[i >> 1] << 16);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) acc[i][q] = fma2(xi, d[q], acc[i][q]);
-            }
+            for (int q = 0; q < 4; ++q)  // d pair in the operand reuse cache across features
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i][q] = fma2(make_float2(xv[i], xv[i]), d[q], acc[i][q]);
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i)

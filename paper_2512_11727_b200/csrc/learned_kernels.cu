@@ -310,11 +310,9 @@ __device__ __forceinline__ void hidden8_tile(const LDims& g, const uint16_t* xba
       const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
                             make_float2(b1v.x, b1v.y), make_float2(b1v.z, b1v.w)};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 ai = make_float2(av[i], av[i]);
+      for (int q = 0; q < 4; ++q)  // b pair in the operand reuse cache across rows
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[i][q] = __ffma2_rn(ai, bv[q], acc[i][q]);
-      }
+        for (int i = 0; i < 8; ++i) acc[i][q] = __ffma2_rn(make_float2(av[i], av[i]), bv[q], acc[i][q]);
     }
     if (more) {
       store_x(nxt);
@@ -428,11 +426,9 @@ __global__ void __launch_bounds__(64, 4) k_l_hidden_ffma16(LDims g, const uint16
         bv[2 * j + 1] = make_float2(b.z, b.w);
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 ai = make_float2(av[i], av[i]);
+      for (int q = 0; q < 8; ++q)  // b pair in the operand reuse cache across rows
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[i][q] = __ffma2_rn(ai, bv[q], acc[i][q]);
-      }
+        for (int i = 0; i < 8; ++i) acc[i][q] = __ffma2_rn(make_float2(av[i], av[i]), bv[q], acc[i][q]);
     }
     if (more) {
       store_x(nxt);
