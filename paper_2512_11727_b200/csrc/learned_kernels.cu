@@ -1393,8 +1393,10 @@ static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, cons
   const LDims g = dims(ctx);
   const char* ef = getenv("ECCO_FFMA_FUSED_EVAL");
   if (ctx->cfg.math == ECCO_MATH_FFMA_EXACT && g.S == kRB && g.H == kFE_H && g.C == kFE_C &&
-      g.F % kFE_KT == 0 && n_pairs > 0 && !(ef && ef[0] == '0')) {
+      g.F % kFE_KT == 0 && n_pairs > 0 && ctx->reserve_sms == 0 && !(ef && ef[0] == '0')) {
     // one block per pair: hidden layer, head, argmax and count on chip
+    // (not beside the chains: there the persistent GEMM below leaves whole
+    // SMs to the chain's cluster)
     static DeviceFlags attr;
     if (!attr.done(ctx->cfg.device)) {
       ECCO_CUDA(cudaFuncSetAttribute(k_l_eval_ffma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
