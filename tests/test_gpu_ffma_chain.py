@@ -120,3 +120,36 @@ def test_ffma_eval_matrix_hidden_tiles_bit_exact(fused, wide, t16, feat, monkeyp
     M = ctx.eval_matrix(ids, cams=np.arange(6))
     W = np.array([[orc.count(orc.models[j], c) / 64 for j in ids] for c in range(6)])
     assert M.tobytes() == W.tobytes()
+
+
+@pytest.mark.parametrize("tile", ["2", "3", "64"])
+def test_ffma_eval_matrix_group_tiles_and_mask(tile, monkeypatch):
+    """The evaluation matrix's pairs are ordered in group tiles (ECCO_PAIR_TILE
+    groups, cameras outer): with several tiles, a ragged last tile and a
+    mask, every unmasked entry equals the oracle's count bit for bit and
+    every masked one is NaN (through k_l_eval_ffma_fused at the bench shape,
+    and through the chunked kernels with it disabled)."""
+    monkeypatch.setenv("ECCO_PAIR_TILE", tile)
+    ctx, orc, rng = setup(seed=45, **BENCH)
+    ids = [1, 3, 4, 6, 9]
+    ctx.seed_models(ids)
+    for j in ids:
+        orc.seed(j)
+    members = [[0, 1], [2, 3], [4, 5], [1, 2], [3, 4]]
+    fracs = [[0.5, 0.5]] * 5
+    batches = [(30.0, 1080.0, 1.0), (2.0, 1080.0, 1.0), (30.0, 1080.0, 1.0), (0.1, 1080.0, 1.0),
+               (30.0, 1080.0, 1.0)]
+    ctx.train_trajectories(ids, batches, members, fracs, members, 1.0, 1, window=3)
+    orc.trajectories(ids, batches, members, fracs, members, 1.0, 1)
+    ctx.commit(ids, [1] * 5)
+    orc.commit(ids, [1] * 5)
+    want = np.array([[orc.count(orc.models[j], c) / 64 for j in ids] for c in range(6)])
+    mask = (rng.random((6, 5)) < 0.7).astype(np.uint8)
+    mask[0, :] = 0
+    for fused in ("1", "0"):
+        monkeypatch.setenv("ECCO_FFMA_FUSED_EVAL", fused)
+        M = ctx.eval_matrix(ids, cams=np.arange(6))
+        assert M.tobytes() == want.tobytes(), fused
+        Mm = ctx.eval_matrix(ids, cams=np.arange(6), mask=mask)
+        assert np.isnan(Mm[mask == 0]).all()
+        assert Mm[mask == 1].tobytes() == want[mask == 1].tobytes(), fused
