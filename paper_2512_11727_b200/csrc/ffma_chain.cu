@@ -26,8 +26,8 @@
 //           whole micro-window), a full copy of W2 (rows padded to C + 1:
 //           conflict-free both along k and along c), b1 slice, b2, the own
 //           pre-activations Z[128][16], and the exchange buffers below
-//   step    gather X (cp.async) -> Z of own units (FFMA, 4 rows x 4 units per
-//           thread, warps 0-3) -> relu rows to the row owners (DSMEM) -> cluster barrier
+//   step    gather X (cp.async) -> Z of own units (FFMA, 2 rows x 4 units per
+//           thread, all warps) -> relu rows to the row owners (DSMEM) -> cluster barrier
 //           -> owner: logits of its rows over all H, softmax, dL (to every
 //           CTA), dH of its rows for all units (to each unit's CTA), row
 //           losses (to CTA 0) -> cluster barrier -> own W2 rows (to every
@@ -218,6 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
 
     // ------------------------------------------------------ gather X --
     FTS(0);
+    // the next step's frame-table rows: loaded now, stored after the forward
+    const int32_t next_row =
+        warp >= 4 && t + 1 < total ? __ldg(a.rows + (rstep + 1) * kB + tid - 128) : 0;
     {
       const int cpr = F / 8;  // 16-byte chunks per row
       for (int e = tid; e < kB * cpr; e += kThreads) {
@@ -229,47 +232,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
     __syncthreads();
     // ------------------------------ Z = X.W1 + b1 of the own 16 units --
     FTS(1);
-    // warps 0-3: warp w owns units [4w, 4w+4) (warp-uniform: the W1 loads
-    // broadcast), lane l rows 4l..4l+3; 8 features per iteration, X by one
-    // 16-byte load per row (the (s >> 2) & 7 chunk swizzle keeps each
-    // quarter-warp's 8 rows on distinct banks).  4 x 4 outputs per thread:
-    // ~1.5 B of shared memory per FMA, the least a 128-thread tile needs.
-    if (warp >= 4 && t + 1 < total)  // (idle in the forward) the next step's rows
-      rowbuf[((t + 1) & 1) * kB + tid - 128] = a.rows[(rstep + 1) * kB + tid - 128];
-    if (warp < 4) {
-      const int hq = warp * 4, s0 = 4 * lane;
-      float2 ac[4][2] = {};  // (row, unit pair): fma.rn.f32x2, each lane an fmaf chain
+    // all 8 warps: warp w owns units [4 (w & 3), +4) (warp-uniform: the W1
+    // loads broadcast), lane l rows 4l + 2 (w >> 2) + {0, 1}; 8 features per
+    // iteration, X by one 16-byte load per row (the (s >> 2) & 7 chunk
+    // swizzle keeps each quarter-warp's 8 rows on distinct banks).  2 x 4
+    // outputs per thread, two warps per scheduler to hide the shared-load
+    // latency (one warp per scheduler left it exposed).
+    {
+      const int hq = (warp & 3) * 4, s0 = 4 * lane + 2 * (warp >> 2);
+      float2 ac[2][2] = {};  // (row, unit pair): fma.rn.f32x2, each lane an fmaf chain
 #pragma unroll 2
       for (int f = 0; f < F; f += 8) {
-        uint32_t px[4][4];
+        uint32_t px[2][4];
 #pragma unroll
-        for (int r4 = 0; r4 < 4; ++r4) {
-          const uint4 v = *reinterpret_cast<const uint4*>(xs + xoff(F, s0 + r4, f));
-          px[r4][0] = v.x;
-          px[r4][1] = v.y;
-          px[r4][2] = v.z;
-          px[r4][3] = v.w;
+        for (int r2 = 0; r2 < 2; ++r2) {
+          const uint4 v = *reinterpret_cast<const uint4*>(xs + xoff(F, s0 + r2, f));
+          px[r2][0] = v.x;
+          px[r2][1] = v.y;
+          px[r2][2] = v.z;
+          px[r2][3] = v.w;
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float4 w = *reinterpret_cast<const float4*>(w1s + (f + i) * kHS + hq);
           const float2 wa = make_float2(w.x, w.y), wb = make_float2(w.z, w.w);
-          float xs4[4];
+          float xs2[2];
 #pragma unroll
-          for (int r4 = 0; r4 < 4; ++r4) {
-            const uint32_t pw = px[r4][i >> 1];
-            xs4[r4] = __uint_as_float(i & 1 ? pw & 0xFFFF0000u : pw << 16);
+          for (int r2 = 0; r2 < 2; ++r2) {
+            const uint32_t pw = px[r2][i >> 1];
+            xs2[r2] = __uint_as_float(i & 1 ? pw & 0xFFFF0000u : pw << 16);
           }
 #pragma unroll
-          for (int r4 = 0; r4 < 4; ++r4)  // wa, then wb, in the operand reuse cache
-            ac[r4][0] = fma2(make_float2(xs4[r4], xs4[r4]), wa, ac[r4][0]);
+          for (int r2 = 0; r2 < 2; ++r2)  // wa, then wb, in the operand reuse cache
+            ac[r2][0] = fma2(make_float2(xs2[r2], xs2[r2]), wa, ac[r2][0]);
 #pragma unroll
-          for (int r4 = 0; r4 < 4; ++r4)
-            ac[r4][1] = fma2(make_float2(xs4[r4], xs4[r4]), wb, ac[r4][1]);
+          for (int r2 = 0; r2 < 2; ++r2)
+            ac[r2][1] = fma2(make_float2(xs2[r2], xs2[r2]), wb, ac[r2][1]);
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 2; ++i) {
         const int s = s0 + i;
         float z[4], rl[4];
         const float av[4] = {ac[i][0].x, ac[i][0].y, ac[i][1].x, ac[i][1].y};
@@ -284,6 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_train_ffma(FfmaArgs a) {
         st_cluster_v4(mapa_shared(dst, (uint32_t)(s / RP)), rl[0], rl[1], rl[2], rl[3]);
       }
     }
+    if (warp >= 4 && t + 1 < total)  // the next step's rows (loaded before the gather)
+      rowbuf[((t + 1) & 1) * kB + tid - 128] = next_row;
     FTS(2);
     cluster_sync();  // every owned row's relu values are in
     FTS(3);
