@@ -22,6 +22,18 @@ namespace {
 // context to hold it): ecco_last_error(nullptr) returns it.
 thread_local std::string g_create_error = "no context";
 
+// The device address of pinned (mapped) host memory, nullptr for pageable
+// memory -- asked of the pointer's attributes, so a refused pointer raises
+// no CUDA API error (cudaHostGetDevicePointer would).
+static void* mapped_device_ptr(const void* host) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 // Makes the context's device current for the call and restores the caller's
 // current device afterwards (several contexts on different GPUs in one
 // process must not move the calling thread's device, e.g. torch's).
@@ -487,10 +499,8 @@ ecco_status ecco_stage_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
                      src_fracs + src_off[j]);
     const ecco_config& g = ctx->cfg;
     void* fdev = nullptr;  // the device address of the pinned ring table
-    if (cudaHostGetDevicePointer(&fdev, (void*)frames, 0) != cudaSuccess) {
-      (void)cudaGetLastError();  // not sticky: clear it so later launch checks do not see it
-      ECCO_REQUIRE(false, "stage_sampled_frames: frames must be pinned (mapped) host memory");
-    }
+    fdev = mapped_device_ptr(frames);
+    ECCO_REQUIRE(fdev != nullptr, "stage_sampled_frames: frames must be pinned (mapped) host memory");
     const int parts = 1 | (n_eval > 0 ? 2 : 0);
     open_back_buffers(ctx, parts);
     cudaStream_t st = ctx->copy_stream;
@@ -569,10 +579,8 @@ ecco_status ecco_fetch_sampled_frames(ecco_ctx* ctx, int n_jobs, const int* job_
                      src_fracs + src_off[j]);
     if (!ctx->ring_partial || n_jobs == 0) return;  // complete rings: nothing to fetch
     void* fdev = nullptr;
-    if (cudaHostGetDevicePointer(&fdev, (void*)frames, 0) != cudaSuccess) {
-      (void)cudaGetLastError();
-      ECCO_REQUIRE(false, "fetch_sampled_frames: frames must be pinned (mapped) host memory");
-    }
+    fdev = mapped_device_ptr(frames);
+    ECCO_REQUIRE(fdev != nullptr, "fetch_sampled_frames: frames must be pinned (mapped) host memory");
     const ecco_config& g = ctx->cfg;
     cudaStream_t st = ctx->stream;
     std::vector<int> steps(n_jobs), mb(n_jobs, 0);

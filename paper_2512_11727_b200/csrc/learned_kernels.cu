@@ -1241,17 +1241,34 @@ struct FESmem {
   } u;
   float W2s[kFE_H][kFE_C];
 };
+// Dense matrix mode (cams != nullptr): block p is the p-th pair of the
+// n x gj matrix in group tiles of `tile` groups, cameras outer (eval_matrix's
+// order), its count written at i * gj + j -- no pair lists.
+struct FEMatrix {
+  const int* cams = nullptr;
+  const int* slots = nullptr;
+  int n = 0, gj = 0, tile = 1;
+};
 __global__ void __launch_bounds__(128, 3) k_l_eval_ffma_fused(LDims g, int n_pairs,
                                                              const int* pair_slot,
-                                                             const int* pair_cam,
+                                                             const int* pair_cam, FEMatrix mx,
                                                              const uint16_t* eval,
                                                              const int32_t* eval_labels,
                                                              const float* wbase, size_t n_params,
                                                              int* counts) {
   extern __shared__ __align__(16) uint8_t dsmf[];
   FESmem& sm = *reinterpret_cast<FESmem*>(dsmf);
-  const int p = blockIdx.x;
-  const int slot = pair_slot[p], cam = pair_cam[p];
+  int p = blockIdx.x, slot, cam;
+  if (mx.cams) {
+    const int per_tile = mx.n * mx.tile, t = p / per_tile, rr = p - t * per_tile;
+    const int w = min(mx.tile, mx.gj - t * mx.tile), i = rr / w, j = t * mx.tile + rr % w;
+    slot = mx.slots[j];
+    cam = mx.cams[i];
+    p = i * mx.gj + j;  // the count's place in the matrix
+  } else {
+    slot = pair_slot[p];
+    cam = pair_cam[p];
+  }
   const float* W1 = wbase + (size_t)slot * n_params;
   const float* b1 = W1 + (size_t)g.F * kFE_H;
   const float* W2 = b1 + kFE_H;
@@ -1385,31 +1402,41 @@ __global__ void __launch_bounds__(128, 3) k_l_eval_ffma_fused(LDims g, int n_pai
   if (tid == 0) counts[p] = n0 + 2 * n1;
 }
 
+// The exact pair evaluation in one block applies: FFMA math at S = 64,
+// H = 256, C = 16, F % 16 = 0, not beside the chains (there the persistent
+// GEMM leaves whole SMs to the chain's cluster); ECCO_FFMA_FUSED_EVAL=0
+// keeps the chunked kernels.
+static bool fe_ok(ecco_ctx* ctx, const LDims& g) {
+  const char* ef = getenv("ECCO_FFMA_FUSED_EVAL");
+  return ctx->cfg.math == ECCO_MATH_FFMA_EXACT && g.S == kRB && g.H == kFE_H && g.C == kFE_C &&
+         g.F % kFE_KT == 0 && ctx->reserve_sms == 0 && !(ef && ef[0] == '0');
+}
+static void fe_launch(ecco_ctx* ctx, const LDims& g, int n_pairs, const int* d_pair_slot,
+                      const int* d_pair_cam, FEMatrix mx, int* d_counts) {
+  if (n_pairs <= 0) return;
+  static DeviceFlags attr;
+  if (!attr.done(ctx->cfg.device)) {
+    ECCO_CUDA(cudaFuncSetAttribute(k_l_eval_ffma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sizeof(FESmem)));
+    attr.mark(ctx->cfg.device);
+  }
+  const double rows = (double)n_pairs * g.S;
+  ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_MATRIX, 2.0 * rows * g.F * g.H + 2.0 * rows * g.H * g.C,
+             rows * g.F * 2 + (double)n_pairs * 4,
+             (k_l_eval_ffma_fused<<<n_pairs, 128, sizeof(FESmem), ctx->stream>>>(
+                 g, n_pairs, d_pair_slot, d_pair_cam, mx, ctx->d_eval, ctx->d_eval_labels,
+                 ctx->d_w, ctx->n_params, d_counts)));
+  ECCO_LAUNCHED(ctx);
+}
+
 // Counts for a list of (slot, camera) pairs, chunked to bound scratch (1 GiB
 // of hidden activations per chunk: few, large launches -- a full C4 matrix
 // in ~300 chunks, each a wide grid).
 static void pair_counts(ecco_ctx* ctx, int n_pairs, const int* d_pair_slot, const int* d_pair_cam,
                         int* d_counts) {
   const LDims g = dims(ctx);
-  const char* ef = getenv("ECCO_FFMA_FUSED_EVAL");
-  if (ctx->cfg.math == ECCO_MATH_FFMA_EXACT && g.S == kRB && g.H == kFE_H && g.C == kFE_C &&
-      g.F % kFE_KT == 0 && n_pairs > 0 && ctx->reserve_sms == 0 && !(ef && ef[0] == '0')) {
-    // one block per pair: hidden layer, head, argmax and count on chip
-    // (not beside the chains: there the persistent GEMM below leaves whole
-    // SMs to the chain's cluster)
-    static DeviceFlags attr;
-    if (!attr.done(ctx->cfg.device)) {
-      ECCO_CUDA(cudaFuncSetAttribute(k_l_eval_ffma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(FESmem)));
-      attr.mark(ctx->cfg.device);
-    }
-    const double rows = (double)n_pairs * g.S;
-    ECCO_TIMED(ctx, ECCO_KSTAT_EVAL_MATRIX, 2.0 * rows * g.F * g.H + 2.0 * rows * g.H * g.C,
-               rows * g.F * 2 + (double)n_pairs * 4,
-               (k_l_eval_ffma_fused<<<n_pairs, 128, sizeof(FESmem), ctx->stream>>>(
-                   g, n_pairs, d_pair_slot, d_pair_cam, ctx->d_eval, ctx->d_eval_labels, ctx->d_w,
-                   ctx->n_params, d_counts)));
-    ECCO_LAUNCHED(ctx);
+  if (fe_ok(ctx, g)) {  // one block per pair: hidden layer, head, argmax and count on chip
+    fe_launch(ctx, g, n_pairs, d_pair_slot, d_pair_cam, FEMatrix{}, d_counts);
     return;
   }
   ECCO_CUDA(cudaMemsetAsync(d_counts, 0, sizeof(int) * std::max(n_pairs, 1), ctx->stream));
@@ -1493,8 +1520,23 @@ void eval_matrix(ecco_ctx* ctx, int n, const int* d_cams, int gj, const int* d_s
     fused::counts_to_acc(ctx, (size_t)n * gj, d_cnt, d_mask, d_out);
     return;
   }
-  // host-side pair list (mask applied on the host copy when given)
   const size_t total = (size_t)n * gj;
+  const char* et = getenv("ECCO_PAIR_TILE");
+  const int tile_g = std::max(1, et ? atoi(et) : 64);
+  if (!d_mask && fe_ok(ctx, dims(ctx)) && total <= (size_t)INT32_MAX) {
+    // dense exact matrix: the pairs' order from the block index, no lists
+    int* d_cnt = (int*)ctx->scratch[3].get(sizeof(int) * total);
+    FEMatrix mx;
+    mx.cams = d_cams;
+    mx.slots = d_slots;
+    mx.n = n;
+    mx.gj = gj;
+    mx.tile = tile_g;
+    fe_launch(ctx, dims(ctx), (int)total, nullptr, nullptr, mx, d_cnt);
+    fused::counts_to_acc(ctx, total, d_cnt, nullptr, d_out);
+    return;
+  }
+  // host-side pair list (mask applied on the host copy when given)
   std::vector<int> slots(gj), cams(n);
   ECCO_CUDA(ctx_memcpy(ctx, slots.data(), d_slots, sizeof(int) * gj, cudaMemcpyDeviceToHost, ctx->stream));
   ECCO_CUDA(ctx_memcpy(ctx, cams.data(), d_cams, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1510,8 +1552,6 @@ void eval_matrix(ecco_ctx* ctx, int n, const int* d_cams, int gj, const int* d_s
   // rather than once per pair (camera-major order re-read the 500 groups'
   // 256 MB of W1 from HBM for every camera).  Counts are per pair and land
   // through po, so the order is invisible to the result.
-  const char* et = getenv("ECCO_PAIR_TILE");
-  const int tile_g = std::max(1, et ? atoi(et) : 64);
   std::vector<int> ps, pc, po;
   ps.reserve(total);
   for (int j0 = 0; j0 < gj; j0 += tile_g)

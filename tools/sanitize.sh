@@ -31,17 +31,22 @@ ffma_chain() {  # the fused FP32 chain (DSMEM exchanges, cluster barriers) and t
 }
 [ "${SANITIZE_ONLY:-}" = "wide_eval" ] && { : > "$SUM"; wide_eval; cat "$SUM"; exit 0; }
 [ "${SANITIZE_ONLY:-}" = "ffma_chain" ] && { : > "$SUM"; ffma_chain; cat "$SUM"; exit 0; }
+[ "${SANITIZE_ONLY:-}" = "learned" ] && { : > "$SUM"
+  for tool in memcheck synccheck; do
+    run $tool learned 1800 $PYT tests/test_gpu_learned.py -k "not detection and not bench_shape and not wide_chain and not (serial_chain and wide)"
+    ECCO_WIDE_ST_ASYNC=1 run $tool wide_chain 1800 $PYT tests/test_gpu_learned.py -k "wide_chain_within or (serial_chain and wide)"
+  done; cat "$SUM"; exit 0; }
 for tool in memcheck synccheck racecheck; do
   run $tool smoke 900 python __graft_entry__.py
 done
 for tool in memcheck synccheck; do
   run $tool parametric 1500 $PYT tests/test_gpu_parametric.py -k "not exp_port"
-  run $tool learned 1800 $PYT tests/test_gpu_learned.py -k "not detection and not bench_shape and not wide_chain"
+  run $tool learned 1800 $PYT tests/test_gpu_learned.py -k "not detection and not bench_shape and not wide_chain and not (serial_chain and wide)"
   # the wide chain's partial-logit exchange by bulk shared::cta ->
   # shared::cluster copies is not modelled by memcheck (it reports the remote
   # destination as "not located in remote CTA"): its per-thread st.async
   # variant, bit-identical by test, runs under the tools instead
-  ECCO_WIDE_ST_ASYNC=1 run $tool wide_chain 1800 $PYT tests/test_gpu_learned.py -k "wide_chain_within"
+  ECCO_WIDE_ST_ASYNC=1 run $tool wide_chain 1800 $PYT tests/test_gpu_learned.py -k "wide_chain_within or (serial_chain and wide)"
   run $tool fused_eval 1500 $PYT tests/test_gpu_fused_eval.py -k "pair and (multi_tile_regime_matches and 2 or pairs_equal or route or staged)"
   run $tool sim 900 $PYT tests/test_gpu_sim.py -k "c1_ten or drift_recovery"
 done
